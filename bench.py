@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""Benchmark of the ADS wave step (arXiv:1911.08158 hot path) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+Workload: BASELINE.json configs[3] (c4: p=3, 512^3 elements, 515^3 = 136.6M DOFs,
+tau 5e-4, 8 seeded Gaussian bumps) -- the 512^3 case the north_star's targets
+name.  One "step" = one full time step of the hot path (drift+source+K apply,
+x/y/z partitioned banded sweeps, fused kick).  Metric: DOF-steps/s (fp64).
+
+Timing: W untimed warm-up steps, then exactly K steps bracketed by a barrier +
+torch.cuda.synchronize() on both sides, CUDA events on the library's stream,
+max over ranks.  Every field (1.09 GB) is larger than L2 (126 MB), so no L2
+flush is needed.  Per-kernel CUDA-event timing inside the library
+(ads_profile_*) gives the roofline of the dominant kernel.
+
+N > 1 (torchrun): each rank runs an independent replica of the workload (the
+z-slab-distributed handle is not built yet), reported as weak scaling.
+
+--impl reference: the CPU oracle (oracle/, single thread) on a bounded sample
+of the same workload recipe; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "P-wave DOF-steps/sec (fp64)"
+UNIT = "DOF-steps/s"
+FALLBACK_HBM_GBS = 6650.0
+# algorithmic HBM bytes per DOF for one launch of each kernel class:
+#   kop: read U, V; write P, r            -> 4 x 8 B
+#   sweep x, sweep y: read in; write out  -> 2 x 8 B
+#   sweep z + kick: read r, V; write V    -> 3 x 8 B (+8 B for a on the last step of a batch)
+KERNELS = ["kop", "sweep_x", "sweep_y", "sweep_z_kick"]
+BYTES_PER_DOF = [32.0, 16.0, 16.0, 24.0]
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured", d
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback", {}
+
+
+class ClockSampler:
+    """Samples SM clock / throttle reasons with NVML during the timed region."""
+
+    def __init__(self, device_index=0, period=0.02):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_init():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------ CPU oracle
+def oracle_sample(wl, nel_sample, steps, warmup=0):
+    """Time the oracle (as it stands, 1 thread) on `steps` steps of the workload recipe
+    scaled to nel_sample^3 elements.  Returns (DOF-steps/s, seconds, sample description)."""
+    import oracle
+    w = wl.scaled(nel_sample, steps) if nel_sample != wl.nel[0] else wl
+    o = oracle.make_solver(w)
+    if warmup:
+        o.step(warmup)
+    t0 = time.perf_counter()
+    o.step(steps)
+    dt = time.perf_counter() - t0
+    n = w.ndof
+    desc = (f"oracle (oracle/ads_oracle.c, gcc -O2, 1 thread) on {steps} step(s) of the {wl.name} recipe at "
+            f"{w.nel[0]}^3 elements ({n} DOFs), after set_state and {warmup} warm-up step(s); wall clock")
+    return n * steps / dt, dt, desc
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    wl = workloads.get(args.config)
+    nel = args.ref_nel
+    val, dt, desc = oracle_sample(wl, nel, args.steps, warmup=args.warmup)
+    n = wl.scaled(nel).ndof
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, workloads/)",
+        "config": {"workload": f"{wl.name} recipe at {nel}^3 elements (bounded CPU sample)", "p": wl.p,
+                   "n_dof": n, "tau": wl.tau},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_1911_08158_b200 as ads
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    wl = workloads.get(args.config)
+    N = wl.ndof
+    s = ads.make_solver(wl)
+    stream = torch.cuda.Stream()
+    s.set_stream(stream)
+    # warm-up, then restart from the initial state so every run times the same steps
+    s.step(args.warmup)
+    torch.cuda.synchronize()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = s.launch_count()
+    s.profile_enable(True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        s.step(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = ev0.elapsed_time(ev1)
+    kms, kcnt = s.profile_read()
+    s.profile_enable(False)
+    launches = s.launch_count() - launches0
+    ms = max_over_ranks(ms, world)
+    value = N * args.steps * world / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (algorithmic bytes / its average launch time)
+    hbm, peak_kind, _ = peaks()
+    shares = kms / kms.sum() if kms.sum() > 0 else kms
+    dom = int(np.argmax(kms))
+    per_launch_ms = kms / np.maximum(kcnt, 1)
+    kernels = {}
+    for i, name in enumerate(KERNELS):
+        bpd = BYTES_PER_DOF[i]
+        if i == 3:  # a is stored on the last step of a batch only
+            bpd = BYTES_PER_DOF[i] + 8.0 / max(kcnt[i], 1)
+        gbs = N * bpd / (per_launch_ms[i] / 1e3) / 1e9 if per_launch_ms[i] > 0 else 0.0
+        kernels[name] = {"ms_per_launch": per_launch_ms[i], "launches": int(kcnt[i]), "share": float(shares[i]),
+                         "bytes_per_dof": bpd, "achieved_gbs": gbs, "frac": gbs / hbm}
+    achieved = kernels[KERNELS[dom]]["achieved_gbs"]
+    step_bytes = N * (sum(BYTES_PER_DOF) + 8.0 / args.steps)
+    roofline = {"bound": "hbm", "kernel": KERNELS[dom], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
+                "step_achieved": step_bytes / (ms / 1e3) / 1e9, "step_frac": step_bytes / (ms / 1e3) / 1e9 / hbm,
+                "step_bytes_per_dof": step_bytes / N, "floor_bytes_per_dof": 64.0}
+
+    # ---- end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
+    nz, ny, nx = s.shape
+    u_host = torch.empty((nz, ny, nx), dtype=torch.float64, pin_memory=True)
+    ud_host = torch.empty_like(u_host, pin_memory=True)
+    a_host = torch.empty_like(u_host, pin_memory=True)
+    s.get_state(u_host, ud_host, a_host)  # the state the run starts from (also warms the copy path)
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    s.set_state(u_host, ud_host)          # H2D u, udot + half-kick init
+    s.step(args.steps)
+    e = s.energy()                        # D2H 3 doubles
+    s.get_state(u_host, ud_host, a_host)  # D2H u, udot, a
+    torch.cuda.synchronize()
+    t_e2e = max_over_ranks(time.perf_counter() - t0, world)
+    e2e = {"value": N * args.steps * world / t_e2e, "unit": UNIT,
+           "h2d_bytes_per_step": 2 * 8 * N / args.steps, "d2h_bytes_per_step": (3 * 8 * N + 24) / args.steps,
+           "what": "ads_set_state(host u, udot) + ads_step(K) + ads_energy + ads_get_state(host u, udot, a); "
+                   "pinned host buffers; wall clock incl. copies", "energy": list(map(float, e))}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads/)",
+        "config": {"workload": f"{wl.name}: {wl.description}", "p": wl.p, "nel": list(wl.nel),
+                   "n_dof": N, "tau": wl.tau, "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (1.09 GB per field vs 126 MB L2); no flush"},
+        "roofline": roofline, "kernels": kernels, "gpu_launches": int(launches),
+        "clocks": clk.summary(), "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if args.cpu_full:
+            val, dt, desc = oracle_sample(wl, wl.nel[0], 1)
+        else:
+            val, dt, desc = oracle_sample(wl, args.ref_nel, args.cpu_steps)
+        line["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                                "seconds": dt}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    s.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-nel", type=int, default=128, help="oracle sample grid (elements per direction)")
+    ap.add_argument("--cpu-steps", type=int, default=40, help="oracle steps for the cpu_baseline sample")
+    ap.add_argument("--cpu-full", action="store_true", help="time the oracle on one full-size step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        ap.error("--warmup must be >= 3")
+    rank, world, local = dist_init()
+    if args.impl == "reference":
+        rc = run_reference(args, rank, world)
+    else:
+        rc = run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

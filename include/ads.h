@@ -1,0 +1,161 @@
+/*
+ * ads.h -- C ABI of the B200-native alternating-direction-split (ADS)
+ * isogeometric implicit wave solver (hot path of arXiv:1911.08158).
+ *
+ * The library implements, on one NVIDIA B200 (sm_100a), in fp64, the time step
+ * of the paper's split scheme (Eq. 16, read as R1 -- see
+ * DESIGN.md §3) on a tensor-product B-spline grid of degree p on [0,1]^3:
+ *
+ *   P   = U_n + tau V_n                         drift (= U_{n+1})
+ *   r   = F(t_{n+1}) - K P                      K = Kx(x)My(x)Mz + Mx(x)Ky(x)Mz + Mx(x)My(x)Kz
+ *                                               (Eq. 14, 3D)
+ *   a   = (A_x (x) A_y (x) A_z)^{-1} r          A_d = M_d + tau^2/4 K_d
+ *                                               three sweeps of banded solves
+ *                                               (Appendix)
+ *   V_{n+1} = V_n + tau a ;  U_{n+1} = P        kick (R1)
+ *
+ * and the 3D elasticity variant (DESIGN.md §3 E1).
+ *
+ * Conventions
+ *  - Every function returns an int status: ADS_OK (0) or a negative ADS_E_*.
+ *    Nothing throws across the ABI.  After ADS_E_CUDA the handle is sticky-
+ *    failed: every call except ads_destroy / ads_last_error returns ADS_E_STATE.
+ *  - nx, ny, nz are numbers of ELEMENTS per direction.  The number of DOFs per
+ *    direction is n_d = n_el,d + p and arrays hold N = n_x n_y n_z doubles
+ *    (3N for elasticity, component-major), x fastest:
+ *        u[(k * n_y + j) * n_x + i].
+ *    With ADS_BC_DIRICHLET0 the boundary entries are ignored on input and are
+ *    0 on output (interior restriction of each 1D space, C3).
+ *  - Memory: `mem` = ADS_MEM_HOST (pageable or pinned host pointer) or
+ *    ADS_MEM_DEVICE (a device pointer on the handle's device).  The library owns
+ *    all its device buffers and copies caller arrays in/out; the caller owns
+ *    every pointer it passes.
+ *  - Streams: all device work is ordered on the handle's stream (default: a
+ *    stream the library creates; ads_set_stream attaches a caller stream, e.g.
+ *    torch.cuda.current_stream().cuda_stream).  ads_step is asynchronous;
+ *    ads_energy / ads_get_state synchronise the stream.
+ *  - A handle is single-writer (not thread-safe).
+ */
+#ifndef ADS_B200_H
+#define ADS_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ads_ctx *ads_handle;
+
+enum { ADS_BC_NATURAL = 0, ADS_BC_DIRICHLET0 = 1 };
+enum {
+    ADS_OK = 0,
+    ADS_E_INVAL = -1,    /* invalid argument (SPEC.md exit 2) */
+    ADS_E_SINGULAR = -2, /* banded LU pivot < 1e-14 max|band| */
+    ADS_E_CUDA = -3,     /* CUDA runtime error (sticky) */
+    ADS_E_NCCL = -4,     /* NCCL error (distributed handles) */
+    ADS_E_NOMEM = -5,    /* device or host allocation failed */
+    ADS_E_STATE = -6     /* handle is failed or call out of order */
+};
+enum { ADS_MEM_HOST = 0, ADS_MEM_DEVICE = 1 };
+enum { ADS_FUNC_SIN = 0, ADS_FUNC_GAUSS = 1 };
+enum { ADS_WAVELET_NONE = 0, ADS_WAVELET_RICKER = 1 };
+
+/* Create a scalar P-wave solver.
+ *   p in [1,5]; nx,ny,nz >= 1 (Dirichlet needs n_d >= 3); tau finite > 0;
+ *   bc in {ADS_BC_NATURAL, ADS_BC_DIRICHLET0}; n_d <= 1024.
+ * Assembles M_d, K_d by Gauss quadrature, factors
+ * A_d = M_d + tau^2/4 K_d by banded LU without pivoting, builds
+ * the partitioned-elimination tables, allocates device fields on the current
+ * CUDA device.  State is zero, t = 0.  Errors: ADS_E_INVAL, ADS_E_SINGULAR,
+ * ADS_E_NOMEM, ADS_E_CUDA.  On error *h is NULL. */
+int ads_create(ads_handle *h, int nx, int ny, int nz, int p, double tau, int bc);
+
+/* Create a 3D isotropic elasticity solver, 3 components,
+ * Lame lambda >= 0, mu > 0, density rho > 0.  Same grid rules as ads_create. */
+int ads_create_elastic(ads_handle *h, int nx, int ny, int nz, int p, double tau, int bc,
+                       double lambda, double mu, double rho);
+
+/* Attach a CUDA stream (cudaStream_t passed as void*); NULL = library stream. */
+int ads_set_stream(ads_handle h, void *cuda_stream);
+
+/* Host-side 1D helpers for separable data (L2 projection).
+ * ads_load_vector: out[a] = int_0^1 f(x) N_a(x) dx in direction d (0=x,1=y,2=z),
+ *   f = sin(pi x) (ADS_FUNC_SIN) or exp(-(x-c)^2/(2 sigma^2)) (ADS_FUNC_GAUSS),
+ *   8 Gauss points per element (C4); Dirichlet entries zeroed.
+ *   out: host array of n_d doubles.
+ * ads_mass_solve_1d: x <- M_d^{-1} x in place (host array of n_d doubles), with
+ *   the Dirichlet identity rows when bc = ADS_BC_DIRICHLET0. */
+int ads_load_vector(ads_handle h, int d, int func, double c, double sigma, double *out);
+int ads_mass_solve_1d(ads_handle h, int d, double *x);
+
+/* Separable source F(t) = amp g(t) (b_x (x) b_y (x) b_z) (C14):
+ * bx,by,bz host arrays of n_d doubles (load vectors, dual -- not projected);
+ * g = Ricker (1 - 2 pi^2 f0^2 (t-t0)^2) exp(-pi^2 f0^2 (t-t0)^2) or 1 (NONE).
+ * F is evaluated at t_{n+1} = (n+1) tau by step n -> n+1.  bx = NULL clears. */
+int ads_set_source(ads_handle h, const double *bx, const double *by, const double *bz,
+                   int wavelet, double f0, double t0, double amp);
+
+/* Set the state (u0, udot0) and reset t = 0 (C2, half-kick start):
+ *   a0 = D^{-1}(F(0) - K u0),  V0 = udot0 + tau/2 a0   (P-wave)
+ *   V0 = udot0 + tau/2 D~^{-1}(f(0) - Ups u0)          (elasticity)
+ * u: N (3N) doubles; udot may be NULL (= 0).  mem: ADS_MEM_HOST/DEVICE. */
+int ads_set_state(ads_handle h, const double *u, const double *udot, int mem);
+
+/* u0 = sum_t amp[t] sx_t (x) sy_t (x) sz_t on component comp[t] (NULL comp = 0),
+ * udot0 = 0; then as ads_set_state.  sx: nterms*n_x host doubles (term-major),
+ * likewise sy, sz.  The outer products are expanded on the device. */
+int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const int *comp,
+                            const double *sx, const double *sy, const double *sz);
+
+/* Advance nsteps >= 0 time steps (asynchronous on the handle's stream). */
+int ads_step(ads_handle h, int nsteps);
+
+/* Energies (C6), synchronising: out[0] kinetic 1/2 v'Mv with
+ * v = V - tau/2 a (rho M for elasticity), out[1] potential 1/2 U'KU (U'Ups U),
+ * out[2] the conserved invariant 1/2 V'DV + 1/2 U_n' K U_{n+1}.
+ * out: host array of 3 doubles.  Deterministic (fixed reduction order). */
+int ads_energy(ads_handle h, double out[3]);
+
+/* Copy out U_n, udot_n = V_n - tau/2 a_n and a_n (any pointer may be NULL).
+ * Synchronising.  mem: ADS_MEM_HOST/DEVICE. */
+int ads_get_state(ads_handle h, double *u, double *udot, double *a, int mem);
+
+/* Simulation time t_n = n tau, and step count n. */
+double ads_time(ads_handle h);
+long ads_step_count(ads_handle h);
+
+/* Grid query: n_d per direction, number of components. */
+int ads_dims(ads_handle h, int *nx, int *ny, int *nz, int *ncomp);
+
+/* Unit operations on device arrays of N doubles (for kernel-level parity
+ * tests; asynchronous on the handle's stream):
+ *   ads_apply_k:   out = K x                  (P-wave operator, fused kernel)
+ *   ads_solve_d:   out = (A_x(x)A_y(x)A_z)^{-1} x  (three partitioned sweeps)
+ *   ads_sweep:     out = A_d^{-1} x along direction d only
+ * x and out must not alias for ads_apply_k. */
+int ads_apply_k(ads_handle h, const double *x_dev, double *out_dev);
+int ads_solve_d(ads_handle h, const double *x_dev, double *out_dev);
+int ads_sweep(ads_handle h, int d, const double *x_dev, double *out_dev);
+
+/* Number of kernel launches issued by the library so far (instrumentation). */
+long ads_launch_count(ads_handle h);
+
+/* Per-kernel-class timing with CUDA events recorded on the handle's stream
+ * around every launch of the step kernels (instrumentation for bench.py).
+ * Classes: 0 = kop (drift+source+K), 1 = sweep x, 2 = sweep y, 3 = sweep z+kick.
+ * ads_profile_enable(h, 1) clears and starts recording; ads_profile_read
+ * synchronises and returns total milliseconds and launch counts per class
+ * (host arrays of ADS_NPROF entries). */
+#define ADS_NPROF 4
+int ads_profile_enable(ads_handle h, int on);
+int ads_profile_read(ads_handle h, double *ms, long *count);
+
+/* Last error message of the handle ("" if none); valid until the next call. */
+const char *ads_last_error(ads_handle h);
+
+/* Free device memory and the handle.  h may be NULL. */
+int ads_destroy(ads_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADS_B200_H */

@@ -1,0 +1,280 @@
+// host_setup.cpp -- see host_setup.h.  Runs once per ads_create on the host.
+#include "host_setup.h"
+
+#include <algorithm>
+#include <cmath>
+
+namespace ads {
+
+// Gauss-Legendre nodes/weights on [-1,1]: Newton iteration on P_m using the
+// Bonnet recurrence (j+1) P_{j+1} = (2j+1) x P_j - j P_{j-1};
+// w = 2 / ((1 - x^2) P_m'(x)^2).
+int gauss_legendre(int m, double *x, double *w) {
+    const double kPi = 3.141592653589793238462643383;
+    for (int i = 0; i < (m + 1) / 2; ++i) {
+        double z = std::cos(kPi * (i + 0.75) / (m + 0.5));
+        double pm = 0, dpm = 0;
+        for (int it = 0; it < 64; ++it) {
+            double pjm1 = 0.0, pj = 1.0;
+            for (int j = 0; j < m; ++j) {
+                double pjp1 = ((2.0 * j + 1.0) * z * pj - j * pjm1) / (j + 1.0);
+                pjm1 = pj;
+                pj = pjp1;
+            }
+            pm = pj;
+            dpm = m * (z * pj - pjm1) / (z * z - 1.0);
+            double dz = pm / dpm;
+            z -= dz;
+            if (std::fabs(dz) <= 1e-17) break;
+        }
+        {
+            double pjm1 = 0.0, pj = 1.0;
+            for (int j = 0; j < m; ++j) {
+                double pjp1 = ((2.0 * j + 1.0) * z * pj - j * pjm1) / (j + 1.0);
+                pjm1 = pj;
+                pj = pjp1;
+            }
+            dpm = m * (z * pj - pjm1) / (z * z - 1.0);
+        }
+        double wi = 2.0 / ((1.0 - z * z) * dpm * dpm);
+        x[i] = -z;
+        x[m - 1 - i] = z;
+        w[i] = w[m - 1 - i] = wi;
+    }
+    if (m % 2 == 1) x[m / 2] = 0.0;
+    return 0;
+}
+
+// de Boor's triangular evaluation of the p+1 nonzero B-splines and their first
+// derivatives in knot span `span` (t[span] <= x < t[span+1]).
+void basis_and_derivs(const std::vector<double> &t, int p, int span, double x, double *N, double *dN) {
+    double ndu[8][8];
+    double left[8], right[8];
+    ndu[0][0] = 1.0;
+    for (int j = 1; j <= p; ++j) {
+        left[j] = x - t[span + 1 - j];
+        right[j] = t[span + j] - x;
+        double saved = 0.0;
+        for (int r = 0; r < j; ++r) {
+            ndu[j][r] = right[r + 1] + left[j - r];      // lower triangle: knot differences
+            double tmp = ndu[r][j - 1] / ndu[j][r];
+            ndu[r][j] = saved + right[r + 1] * tmp;      // upper triangle: basis values
+            saved = left[j - r] * tmp;
+        }
+        ndu[j][j] = saved;
+    }
+    for (int r = 0; r <= p; ++r) N[r] = ndu[r][p];
+    // first derivative: N'_{r} = p (N_{r,p-1}/(t_{r+p}-t_r) - N_{r+1,p-1}/(t_{r+p+1}-t_{r+1}))
+    for (int r = 0; r <= p; ++r) {
+        double d = 0.0;
+        if (r >= 1) d += ndu[r - 1][p - 1] / ndu[p][r - 1];
+        if (r <= p - 1) d -= ndu[r][p - 1] / ndu[p][r];
+        dN[r] = p * d;
+    }
+}
+
+int build_space(int p, int nel, int bc, Space1D &s) {
+    if (p < 1 || p > 5 || nel < 1) return -1;
+    s.p = p;
+    s.nel = nel;
+    s.n = nel + p;
+    s.bc = bc;
+    s.knots.assign(nel + 2 * p + 1, 0.0);
+    for (int i = 0; i < (int)s.knots.size(); ++i) {
+        int e = std::min(std::max(i - p, 0), nel);
+        s.knots[i] = (double)e / nel;
+    }
+    s.M = Band(s.n, p);
+    s.K = Band(s.n, p);
+    s.B = Band(s.n, p);
+    double xg[8], wg[8];
+    gauss_legendre(p + 1, xg, wg);
+    double N[8], dN[8];
+    for (int e = 0; e < nel; ++e) {
+        int span = e + p;
+        double a = s.knots[span], b = s.knots[span + 1];
+        double half = 0.5 * (b - a), mid = 0.5 * (a + b);
+        for (int q = 0; q <= p; ++q) {
+            double x = mid + half * xg[q], w = half * wg[q];
+            basis_and_derivs(s.knots, p, span, x, N, dN);
+            for (int r = 0; r <= p; ++r)
+                for (int c = 0; c <= p; ++c) {
+                    int ia = e + r, ic = e + c;
+                    s.M.at(ia, ic) += w * N[r] * N[c];
+                    s.K.at(ia, ic) += w * dN[r] * dN[c];
+                    s.B.at(ia, ic) += w * dN[r] * N[c];
+                }
+        }
+    }
+    if (bc == 1) {
+        // interior restriction (C3): the two end functions are removed
+        for (int end : {0, s.n - 1})
+            for (int j = end - p; j <= end + p; ++j) {
+                if (j < 0 || j >= s.n) continue;
+                s.M.at(end, j) = s.M.at(j, end) = 0.0;
+                s.K.at(end, j) = s.K.at(j, end) = 0.0;
+                s.B.at(end, j) = s.B.at(j, end) = 0.0;
+            }
+    }
+    return 0;
+}
+
+void load_vector(const Space1D &s, int func, double c, double sigma, double *out) {
+    const double kPi = 3.141592653589793238462643383;
+    double xg[8], wg[8], N[8], dN[8];
+    gauss_legendre(8, xg, wg);
+    std::fill(out, out + s.n, 0.0);
+    for (int e = 0; e < s.nel; ++e) {
+        int span = e + s.p;
+        double a = s.knots[span], b = s.knots[span + 1];
+        double half = 0.5 * (b - a), mid = 0.5 * (a + b);
+        for (int q = 0; q < 8; ++q) {
+            double x = mid + half * xg[q], w = half * wg[q];
+            double f = (func == 0) ? std::sin(kPi * x) : std::exp(-(x - c) * (x - c) / (2.0 * sigma * sigma));
+            basis_and_derivs(s.knots, s.p, span, x, N, dN);
+            for (int r = 0; r <= s.p; ++r) out[e + r] += w * f * N[r];
+        }
+    }
+    if (s.bc == 1) out[0] = out[s.n - 1] = 0.0;
+}
+
+int banded_lu(const Band &A, LUFactors &f) {
+    const int n = A.n, p = A.p;
+    f.n = n;
+    f.p = p;
+    f.l.assign((size_t)n * p, 0.0);
+    f.us.assign((size_t)n * p, 0.0);
+    f.dinv.assign(n, 0.0);
+    Band W = A;
+    double amax = 0.0;
+    for (double v : A.v) amax = std::max(amax, std::fabs(v));
+    if (amax == 0.0) return -2;
+    for (int k = 0; k < n; ++k) {
+        double piv = W.at(k, k);
+        if (!(std::fabs(piv) >= 1e-14 * amax)) return -2;
+        for (int i = k + 1; i <= std::min(n - 1, k + p); ++i) {
+            double m = W.at(i, k) / piv;
+            W.at(i, k) = m;
+            for (int j = k + 1; j <= std::min(n - 1, k + p); ++j) W.at(i, j) -= m * W.at(k, j);
+        }
+    }
+    for (int i = 0; i < n; ++i) {
+        double d = W.at(i, i);
+        f.dinv[i] = 1.0 / d;
+        for (int k = 1; k <= p; ++k) {
+            if (i - k >= 0) f.l[(size_t)i * p + k - 1] = W.at(i, i - k);
+            if (i + k < n) f.us[(size_t)i * p + k - 1] = W.at(i, i + k) / d;
+        }
+    }
+    return 0;
+}
+
+void lu_solve_host(const LUFactors &f, double *x) {
+    const int n = f.n, p = f.p;
+    for (int i = 0; i < n; ++i)
+        for (int k = 1; k <= p && i - k >= 0; ++k) x[i] -= f.l[(size_t)i * p + k - 1] * x[i - k];
+    for (int i = n - 1; i >= 0; --i) {
+        double v = x[i] * f.dinv[i];
+        for (int k = 1; k <= p && i + k < n; ++k) v -= f.us[(size_t)i * p + k - 1] * x[i + k];
+        x[i] = v;
+    }
+}
+
+void choose_chunks(int n, int p, int cmax, bool odd_len, std::vector<int> &cs) {
+    int minlen = std::max(p, 1);
+    int C = std::max(1, std::min(cmax, n / minlen));
+    int L = (n + C - 1) / C;
+    if (odd_len && L % 2 == 0 && C > 1) L += 1;
+    C = (n + L - 1) / L;
+    // last chunk must hold >= minlen rows; otherwise fold it into its neighbour
+    while (C > 1 && n - (C - 1) * L < minlen) C -= 1;
+    cs.resize(C + 1);
+    for (int c = 0; c < C; ++c) cs[c] = c * L;
+    cs[C] = n;
+}
+
+void build_part_tables(const LUFactors &f, const std::vector<int> &cs, PartTables &t) {
+    const int n = f.n, p = f.p, C = (int)cs.size() - 1;
+    t.n = n;
+    t.p = p;
+    t.C = C;
+    t.cs = cs;
+    t.lmax = 0;
+    for (int c = 0; c < C; ++c) t.lmax = std::max(t.lmax, cs[c + 1] - cs[c]);
+    t.levels = 0;
+    while ((1 << t.levels) < C) ++t.levels;
+    t.gf.assign((size_t)n * p, 0.0);
+    t.gb.assign((size_t)n * p, 0.0);
+    std::vector<double> y(n + 2 * p);
+    for (int c = 0; c < C; ++c) {
+        int s = cs[c], e = cs[c + 1];
+        for (int m = 0; m < p; ++m) {
+            // forward homogeneous recurrence with incoming y_{s-1-m} = 1
+            std::fill(y.begin(), y.end(), 0.0);
+            double *Y = y.data() + p;  // Y[i] for i >= -p
+            if (s - 1 - m >= -p) Y[s - 1 - m] = 1.0;
+            for (int i = s; i < e; ++i) {
+                double v = 0.0;
+                for (int k = 1; k <= p; ++k)
+                    if (i - k >= s - p) v -= f.l[(size_t)i * p + k - 1] * Y[i - k];
+                Y[i] = v;
+                t.gf[(size_t)i * p + m] = v;
+            }
+            // backward homogeneous recurrence with incoming x_{e+m} = 1
+            std::fill(y.begin(), y.end(), 0.0);
+            Y = y.data();
+            if (e + m < n + p) Y[e + m] = 1.0;
+            for (int i = e - 1; i >= s; --i) {
+                double v = 0.0;
+                for (int k = 1; k <= p; ++k)
+                    if (i + k < n) v -= f.us[(size_t)i * p + k - 1] * Y[i + k];
+                Y[i] = v;
+                t.gb[(size_t)i * p + m] = v;
+            }
+        }
+    }
+    // scan matrices
+    int L = std::max(t.levels, 1);
+    t.phif.assign((size_t)L * C * p * p, 0.0);
+    t.phib.assign((size_t)L * C * p * p, 0.0);
+    auto Tf = [&](int c, int a, int b) { return t.gf[(size_t)(cs[c + 1] - 1 - a) * p + b]; };
+    auto Rb = [&](int c, int a, int b) { return t.gb[(size_t)(cs[c] + a) * p + b]; };
+    std::vector<double> acc(p * p), tmp(p * p);
+    for (int lv = 0; lv < t.levels; ++lv) {
+        int d = 1 << lv;
+        for (int c = 0; c < C; ++c) {
+            // forward: T_c T_{c-1} ... T_{c-d+1}
+            if (c - d + 1 >= 0) {
+                for (int a = 0; a < p; ++a)
+                    for (int b = 0; b < p; ++b) acc[a * p + b] = Tf(c, a, b);
+                for (int q = c - 1; q >= c - d + 1; --q) {
+                    for (int a = 0; a < p; ++a)
+                        for (int b = 0; b < p; ++b) {
+                            double v = 0.0;
+                            for (int k = 0; k < p; ++k) v += acc[a * p + k] * Tf(q, k, b);
+                            tmp[a * p + b] = v;
+                        }
+                    acc = tmp;
+                }
+                std::copy(acc.begin(), acc.end(), t.phif.begin() + ((size_t)lv * C + c) * p * p);
+            }
+            // backward: R_c R_{c+1} ... R_{c+d-1}
+            if (c + d - 1 < C) {
+                for (int a = 0; a < p; ++a)
+                    for (int b = 0; b < p; ++b) acc[a * p + b] = Rb(c, a, b);
+                for (int q = c + 1; q <= c + d - 1; ++q) {
+                    for (int a = 0; a < p; ++a)
+                        for (int b = 0; b < p; ++b) {
+                            double v = 0.0;
+                            for (int k = 0; k < p; ++k) v += acc[a * p + k] * Rb(q, k, b);
+                            tmp[a * p + b] = v;
+                        }
+                    acc = tmp;
+                }
+                std::copy(acc.begin(), acc.end(), t.phib.begin() + ((size_t)lv * C + c) * p * p);
+            }
+        }
+    }
+}
+
+}  // namespace ads

@@ -1,0 +1,73 @@
+// host_setup.h -- host-side (once per ads_create) 1D discretisation and
+// factor tables for the B200 ADS solver.  Independent of oracle/ (no shared
+// code): B-spline values by de Boor's triangular scheme, Gauss-Legendre by
+// Newton on the Bonnet recurrence, Gram matrices accumulated in band storage,
+// banded LU in band storage, partitioned-elimination (SPIKE-style) tables.
+#pragma once
+#include <vector>
+
+namespace ads {
+
+// Band storage of an n x n matrix with half-bandwidth p:
+// band[i*(2p+1) + (j - i + p)] = A(i, j) for |i-j| <= p (0 outside the matrix).
+struct Band {
+    int n = 0, p = 0;
+    std::vector<double> v;
+    Band() = default;
+    Band(int n_, int p_) : n(n_), p(p_), v((size_t)n_ * (2 * p_ + 1), 0.0) {}
+    double &at(int i, int j) { return v[(size_t)i * (2 * p + 1) + (j - i + p)]; }
+    double get(int i, int j) const {
+        if (i < 0 || j < 0 || i >= n || j >= n || j - i > p || i - j > p) return 0.0;
+        return v[(size_t)i * (2 * p + 1) + (j - i + p)];
+    }
+};
+
+// 1D open-uniform B-spline space on [0,1] with its Gram matrices
+// M = (N_a, N_c), K = (N'_a, N'_c), B = (N'_a, N_c).
+struct Space1D {
+    int p = 0, nel = 0, n = 0, bc = 0;
+    std::vector<double> knots;
+    Band M, K, B;
+};
+
+int gauss_legendre(int m, double *x, double *w);
+// Nonzero basis values/derivatives at x in knot span `span` (p <= span < n):
+// N[0..p], dN[0..p] belong to functions span-p .. span.
+void basis_and_derivs(const std::vector<double> &t, int p, int span, double x, double *N, double *dN);
+int build_space(int p, int nel, int bc, Space1D &s);
+// b_a = int f N_a over [0,1], 8-point Gauss per element; func 0 sin(pi x), 1 Gaussian.
+void load_vector(const Space1D &s, int func, double c, double sigma, double *out);
+
+// Banded LU without pivoting of A (n x n, half-bandwidth p), returned as
+//   l[i*p + (k-1)]  = L(i, i-k)            (unit lower)
+//   us[i*p + (k-1)] = U(i, i+k) / U(i, i)  (row-scaled upper)
+//   dinv[i]         = 1 / U(i, i)
+// Returns 0, or -2 if a pivot falls below 1e-14 * max|A|.
+struct LUFactors {
+    int n = 0, p = 0;
+    std::vector<double> l, us, dinv;
+};
+int banded_lu(const Band &A, LUFactors &f);
+void lu_solve_host(const LUFactors &f, double *x);  // in place, one vector
+
+// Partitioned elimination tables for one direction (chunks of a line solved
+// independently, then coupled by an exact scan over chunk boundary states).
+//   cs[c]           chunk c = [cs[c], cs[c+1])
+//   gf[i*p + m]     response of the forward (L) recurrence at i to incoming
+//                   state y_{s-1-m} = 1 (s = start of i's chunk)
+//   gb[i*p + m]     response of the backward (U) recurrence at i to incoming
+//                   state x_{e+m} = 1 (e = end of i's chunk)
+//   phif[(lv*C + c)*p*p + a*p + b]  product T_c T_{c-1} ... T_{c-2^lv+1}
+//   phib[(lv*C + c)*p*p + a*p + b]  product R_c R_{c+1} ... R_{c+2^lv-1}
+// with T_c[a][b] = gf[(e_c-1-a)*p + b] and R_c[a][b] = gb[(s_c+a)*p + b].
+struct PartTables {
+    int n = 0, p = 0, C = 0, levels = 0, lmax = 0;
+    std::vector<int> cs;
+    std::vector<double> gf, gb, phif, phib;
+};
+// Choose chunks: C <= cmax, every chunk length >= max(p,1); if odd_len, prefer
+// odd uniform chunk lengths (bank-conflict-free shared-memory transposes).
+void choose_chunks(int n, int p, int cmax, bool odd_len, std::vector<int> &cs);
+void build_part_tables(const LUFactors &f, const std::vector<int> &cs, PartTables &t);
+
+}  // namespace ads

@@ -1,0 +1,63 @@
+// kernels.cuh -- device kernel interfaces of the B200 ADS solver (sm_100a, fp64).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace ads {
+
+// Banded 1D matrix on the device: b[i*(2p+1) + c] = A(i, i - p + c).
+// Factor tables of A_d = M_d + tau^2/4 K_d (see host_setup.h LUFactors/PartTables).
+struct SolveTab {
+    const double *l = nullptr, *us = nullptr, *dinv = nullptr;
+    const double *phif = nullptr, *phib = nullptr;
+    const int *cs = nullptr;
+    int n = 0, C = 0, levels = 0, lmax = 0;
+};
+
+// Geometry of a field: x-fastest, sy = row stride, sz = plane stride (elements).
+struct Geom {
+    int n0 = 0, n1 = 0, n2 = 0;
+    long sy = 0, sz = 0;
+};
+
+// r = g * (bx (x) by (x) bz) + sign * K P,  P = U + tau V  (P written to Pout if non-null).
+// K = Kx(x)My(x)Mz + Mx(x)Ky(x)Mz + Mx(x)My(x)Kz by sum factorisation.
+struct KopArgs {
+    const double *U = nullptr, *V = nullptr;
+    double *Pout = nullptr, *r = nullptr;
+    double tau = 0.0, g = 0.0, sign = -1.0;
+    const double *bx = nullptr, *by = nullptr, *bz = nullptr;
+    const double *mx = nullptr, *kx = nullptr, *my = nullptr, *ky = nullptr, *mz = nullptr, *kz = nullptr;
+    Geom geo;
+    int zlen = 0;
+};
+
+// Batched banded solve along direction dir of every line of `in`.
+// mode 0: out = A^-1 in; mode 1: V += kick * (A^-1 in) and out = A^-1 in if out != nullptr.
+struct SweepArgs {
+    const double *in = nullptr;
+    double *out = nullptr;
+    double *V = nullptr;
+    double kick = 0.0;
+    SolveTab t;
+    Geom geo;
+    int dir = 0;
+    int mode = 0;
+};
+
+int launch_kop(int p, const KopArgs &a, cudaStream_t s);
+int launch_sweep(int p, const SweepArgs &a, cudaStream_t s);
+
+// Small helpers (diagnostics / state I/O, not on the per-step path).
+// out = A along axis d applied to in (band table [n_d][2p+1]).
+int launch_axis_apply(int p, int d, const double *band, const double *in, double *out, const Geom &g, cudaStream_t s);
+// y = alpha x + beta y over N elements
+int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s);
+// zero the boundary faces of a field (Dirichlet masking)
+int launch_mask_boundary(double *u, const Geom &g, cudaStream_t s);
+// u += amp * sx (x) sy (x) sz
+int launch_add_separable(double *u, double amp, const double *sx, const double *sy, const double *sz, const Geom &g,
+                         cudaStream_t s);
+// deterministic dot product: partial sums into `partial` (>= 1024 doubles), result into *res (device)
+int launch_dot(long N, const double *x, const double *y, double *partial, double *res, cudaStream_t s);
+
+}  // namespace ads

@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle (-m gpu).
+
+Tolerances (BASELINE.json north_star): relative L2 <= 1e-12 after one step and
+<= 1e-9 after the full run, on U, the returned udot and a.  Unit operators are
+held to 1e-13 (a single application; cond(A_d) <= ~30).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle.modal import ModalPWave
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+STEP1_TOL = 1e-12
+RUN_TOL = 1e-9
+OP_TOL = 1e-13
+
+
+def rel(a, b):
+    a = np.asarray(a).ravel()
+    b = np.asarray(b).ravel()
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def ads():
+    import torch
+    import paper_1911_08158_b200 as ads
+    from paper_1911_08158_b200 import build
+    build.build()
+    assert torch.cuda.is_available()
+    return ads
+
+
+def _dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+# grids spanning several kop tiles (32 x 8) / sweep chunk layouts with ragged tails
+OP_CASES = [
+    ((37, 21, 13), 3, 1),
+    ((40, 9, 70), 2, 0),
+    ((5, 6, 7), 1, 1),
+    ((11, 12, 13), 4, 0),
+    ((9, 8, 10), 5, 1),
+    ((1, 1, 1), 2, 0),
+    ((1, 1, 1), 1, 0),
+    ((1, 2, 1), 2, 1),
+    ((100, 3, 5), 3, 1),
+]
+
+
+@pytest.mark.parametrize("nel,p,bc", OP_CASES)
+def test_unit_operators(ads, nel, p, bc):
+    """K-apply (fused kernel), each directional sweep and the full D^-1 vs the oracle."""
+    import torch
+    tau = 0.013 * (1 + p)
+    s = ads.Solver(nel, p, tau, bc)
+    o = oracle.PWave(nel, p, tau, bc)
+    x = workloads.random_field(100 + p, s.N).reshape(s.shape)
+    xd = _dev(x)
+    out = torch.empty_like(xd)
+    s.apply_k(xd, out)
+    torch.cuda.synchronize()
+    assert rel(out.cpu().numpy(), o.kapply(x)) < OP_TOL
+    s.solve_d(xd, out)
+    torch.cuda.synchronize()
+    assert rel(out.cpu().numpy(), o.dsolve(x)) < OP_TOL
+    # single-direction sweeps vs dense 1D solves along that axis
+    for d in range(3):
+        s.sweep(d, xd, out)
+        torch.cuda.synchronize()
+        A = o.matrix(d, 2)
+        axis = 2 - d  # numpy (z, y, x)
+        ref = np.moveaxis(np.linalg.solve(A, np.moveaxis(x, axis, 0).reshape(A.shape[0], -1)).reshape(
+            np.moveaxis(x, axis, 0).shape), 0, axis)
+        assert rel(out.cpu().numpy(), ref) < OP_TOL, d
+
+
+def _compare_run(ads, wl, nsteps_list, tol_first=STEP1_TOL, tol_run=RUN_TOL):
+    g = ads.make_solver(wl)
+    o = oracle.make_solver(wl)
+    done = 0
+    for k, nsteps in enumerate(nsteps_list):
+        g.step(nsteps - done)
+        o.step(nsteps - done)
+        done = nsteps
+        gu, gud, ga = g.get_state()
+        ou, oud, oa = o.get_state()
+        tol = tol_first if nsteps == 1 else tol_run
+        errs = (rel(gu, ou), rel(gud, oud), rel(ga, oa))
+        assert max(errs) < tol, (wl.name, nsteps, errs)
+    return g, o
+
+
+def test_c1_full_run(ads):
+    """BASELINE config 1 exactly (p=2, 16^3 el, tau 1e-2, 20 steps)."""
+    wl = workloads.get("c1")
+    g, o = _compare_run(ads, wl, [1, wl.steps])
+    ge, oe = g.energy(), o.energy()
+    assert np.allclose(ge, oe, rtol=1e-12, atol=1e-15)
+
+
+def test_c2_full_run(ads):
+    """BASELINE config 2 exactly (p=3, 64^3 el, tau 5e-3, 100 steps)."""
+    wl = workloads.get("c2")
+    _compare_run(ads, wl, [1, wl.steps])
+
+
+def test_c3_recipe_scaled(ads):
+    """Config 3 recipe (Ricker x Gaussian source, zero state) on 40^3 elements, full 200 steps."""
+    wl = workloads.get("c3").scaled(40)
+    g, o = _compare_run(ads, wl, [1, 60, wl.steps])
+    ge, oe = g.energy(), o.energy()
+    assert np.allclose(ge, oe, rtol=1e-11)
+
+
+def test_c4_recipe_scaled(ads):
+    """Config 4 recipe (8 seeded bumps, p=3) on 48^3 elements, full 100 steps."""
+    wl = workloads.get("c4").scaled(48)
+    _compare_run(ads, wl, [1, wl.steps])
+
+
+def test_anisotropic_natural_bc(ads):
+    wl = workloads.get("c2").scaled(10, 30)
+    wl.nel = (23, 10, 17)
+    wl.bc = 0
+    _compare_run(ads, wl, [1, 30])
+
+
+def test_set_get_roundtrip_and_energy_invariant(ads):
+    wl = workloads.get("c2").scaled(12, 0)
+    g = ads.make_solver(wl)
+    u0 = oracle.project_separable(wl)
+    u, ud, a = g.get_state()
+    assert rel(u, u0) < 1e-14
+    assert np.abs(ud).max() < 1e-14 * np.abs(u0).max() + 1e-300
+    e0 = g.energy()
+    g.step(50)
+    e1 = g.energy()
+    assert abs(e1[2] - e0[2]) < 1e-12 * e0[2]
+
+
+def test_device_state_io_and_stream(ads):
+    """set_state/get_state with device (torch) tensors and a caller stream."""
+    import torch
+    wl = workloads.get("c1")
+    g = ads.Solver(wl.nel, wl.p, wl.tau, wl.bc)
+    st = torch.cuda.Stream()
+    g.set_stream(st)
+    u0 = oracle.project_separable(wl)
+    v0 = 0.3 * u0
+    g.set_state(_dev(u0), _dev(v0))
+    g.step(5)
+    u = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    ud = torch.empty_like(u)
+    a = torch.empty_like(u)
+    g.get_state(u, ud, a)
+    o = oracle.PWave(wl.nel, wl.p, wl.tau, wl.bc)
+    o.set_state(u0, v0)
+    o.step(5)
+    ou, oud, oa = o.get_state()
+    assert rel(u.cpu().numpy(), ou) < 1e-12 and rel(ud.cpu().numpy(), oud) < 1e-12 and rel(a.cpu().numpy(), oa) < 1e-12
+
+
+def test_errors(ads):
+    g = ads.Solver(4, 2, 0.1)
+    with pytest.raises(ads.AdsError) as e:
+        g.step(1)  # before set_state
+    assert e.value.code == -6
+    with pytest.raises(ads.AdsError):
+        g.load_vector(3, ("sin",))
+    g.set_state(np.zeros(g.shape))
+    with pytest.raises(ads.AdsError):
+        g.step(-1)
+    g.step(0)
+    assert g.step_count() == 0
+
+
+# ------------------------------------------------------------------ full-size cases (slow)
+@pytest.mark.slow
+def test_c3_full_size_vs_modal(ads):
+    """Full config 3 (258^3, 200 steps, forced) vs the modal oracle (exact mode-by-mode)."""
+    wl = workloads.get("c3")
+    g = ads.make_solver(wl)
+    g.step(wl.steps)
+    gu, gud, ga = g.get_state()
+    src = wl.source
+    mu, mud, ma = ModalPWave(wl.nel, wl.p, wl.tau).run(np.zeros(g.shape), nsteps=wl.steps,
+                                                        source=oracle.source_vectors(wl), wavelet=src.wavelet,
+                                                        f0=src.f0, t0=src.t0)
+    assert rel(gu, mu) < RUN_TOL and rel(gud, mud) < RUN_TOL and rel(ga, ma) < RUN_TOL
+
+
+@pytest.mark.slow
+def test_c4_full_size_one_step_and_run(ads):
+    """Full config 4 (515^3): one step vs the C oracle element by element, full 100-step run vs
+    the modal oracle."""
+    wl = workloads.get("c4")
+    g = ads.make_solver(wl)
+    g.step(1)
+    gu, gud, ga = g.get_state()
+    o = oracle.make_solver(wl)
+    o.step(1)
+    ou, oud, oa = o.get_state()
+    del o
+    assert rel(gu, ou) < STEP1_TOL and rel(gud, oud) < STEP1_TOL and rel(ga, oa) < STEP1_TOL
+    del ou, oud, oa
+    g.step(wl.steps - 1)
+    gu, gud, ga = g.get_state()
+    u0 = oracle.project_separable(wl)
+    mu, mud, ma = ModalPWave(wl.nel, wl.p, wl.tau).run(u0, nsteps=wl.steps)
+    assert rel(gu, mu) < RUN_TOL and rel(gud, mud) < RUN_TOL and rel(ga, ma) < RUN_TOL
