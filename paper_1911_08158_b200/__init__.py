@@ -141,13 +141,13 @@ class Solver:
         self._check(lib().ads_set_stream(self.h, ptr))
 
     def load_vector(self, d, func):
-        out = np.zeros(self.n[d])
+        out = np.zeros(max(self.n))
         if func[0] == "sin":
             self._check(lib().ads_load_vector(self.h, d, ADS_FUNC_SIN, 0.0, 1.0, out.ctypes.data))
         else:
             self._check(lib().ads_load_vector(self.h, d, ADS_FUNC_GAUSS, float(func[1]), float(func[2]),
                                               out.ctypes.data))
-        return out
+        return out[:self.n[d]]
 
     def mass_solve_1d(self, d, x):
         x = np.array(x, dtype=np.float64, copy=True)

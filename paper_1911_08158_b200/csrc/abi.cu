@@ -162,10 +162,11 @@ int build_direction(ads_ctx *h, int d) {
         Mm.at(n - 1, n - 1) = 1.0;
     }
     LUFactors f;
-    if (banded_lu(A, f)) return fail(h, ADS_E_SINGULAR, "A_%d singular", d);
+    if (banded_lu(A, f, /*freeze=*/true)) return fail(h, ADS_E_SINGULAR, "A_%d singular", d);
     if (banded_lu(Mm, h->mass_lu[d])) return fail(h, ADS_E_SINGULAR, "M_%d singular", d);
     std::vector<int> cs;
-    choose_chunks(n, p, 32, d == 0, cs);
+    const int L = choose_chunks(n, p, 32, cs);
+    if (L == 0) return fail(h, ADS_E_INVAL, "n_%d = %d: no supported chunking", d, n);
     PartTables pt;
     build_part_tables(f, cs, pt);
     DirDev &D = h->dd[d];
@@ -185,8 +186,16 @@ int build_direction(ads_ctx *h, int d) {
     D.tab.n = n;
     D.tab.C = pt.C;
     D.tab.levels = pt.levels;
-    D.tab.lmax = pt.lmax;
-    if (pt.lmax > 33) return fail(h, ADS_E_INVAL, "n_%d = %d too large (chunk %d > 33)", d, n, pt.lmax);
+    D.tab.L = L;
+    D.tab.i_lo = f.i_lo;
+    D.tab.i_hi = f.i_hi;
+    if (f.i_hi > f.i_lo) {
+        for (int k = 0; k < p; ++k) {
+            D.tab.lc[k] = f.l[(size_t)f.i_lo * p + k];
+            D.tab.usc[k] = f.us[(size_t)f.i_lo * p + k];
+        }
+        D.tab.dic = f.dinv[f.i_lo];
+    }
     return ADS_OK;
 }
 

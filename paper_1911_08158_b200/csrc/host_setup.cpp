@@ -106,6 +106,28 @@ int build_space(int p, int nel, int bc, Space1D &s) {
                 }
         }
     }
+    // Uniform mesh: every row whose basis function and all p neighbours on each
+    // side are interior cardinal B-splines (rows [2p, n-1-2p]) has the same band
+    // in exact arithmetic (h-scaled cardinal B-spline autocorrelation); quadrature
+    // rounding jitters them by a few ulp.  Use the middle row for all of them so
+    // the interior is bitwise Toeplitz ("Toeplitz interior").
+    {
+        const int lo = 2 * p, hi = s.n - 1 - 2 * p, mid = s.n / 2;
+        if (hi - lo >= 2) {
+            double rm[2 * 8 + 1], rk[2 * 8 + 1], rb[2 * 8 + 1];
+            for (int k = -p; k <= p; ++k) {
+                rm[k + p] = s.M.at(mid, mid + k);
+                rk[k + p] = s.K.at(mid, mid + k);
+                rb[k + p] = s.B.at(mid, mid + k);
+            }
+            for (int i = lo; i <= hi; ++i)
+                for (int k = -p; k <= p; ++k) {
+                    s.M.at(i, i + k) = rm[k + p];
+                    s.K.at(i, i + k) = rk[k + p];
+                    s.B.at(i, i + k) = rb[k + p];
+                }
+        }
+    }
     if (bc == 1) {
         // interior restriction (C3): the two end functions are removed
         for (int end : {0, s.n - 1})
@@ -138,32 +160,102 @@ void load_vector(const Space1D &s, int func, double c, double sigma, double *out
     if (s.bc == 1) out[0] = out[s.n - 1] = 0.0;
 }
 
-int banded_lu(const Band &A, LUFactors &f) {
-    const int n = A.n, p = A.p;
+// Row-wise Doolittle on band storage: row i of L and U from row i of A and the
+// previous p rows of U (no pivoting).
+static bool lu_row(const Band &A, std::vector<double> &Lw, std::vector<double> &Ur, int i, double amax) {
+    const int n = A.n, p = A.p, W = 2 * p + 1;
+    // L(i, j) for j in [i-p, i): stored Lw[i*p + (i-j-1)]
+    for (int j = std::max(0, i - p); j < i; ++j) {
+        double v = A.get(i, j);
+        for (int m = std::max(0, i - p); m < j; ++m) v -= Lw[(size_t)i * p + (i - m - 1)] * Ur[(size_t)m * W + (j - m)];
+        Lw[(size_t)i * p + (i - j - 1)] = v / Ur[(size_t)j * W + 0];
+    }
+    // U(i, j) for j in [i, i+p]: stored Ur[i*W + (j-i)]
+    for (int j = i; j <= std::min(n - 1, i + p); ++j) {
+        double v = A.get(i, j);
+        for (int m = std::max(0, j - p); m < i; ++m) v -= Lw[(size_t)i * p + (i - m - 1)] * Ur[(size_t)m * W + (j - m)];
+        Ur[(size_t)i * W + (j - i)] = v;
+    }
+    return std::fabs(Ur[(size_t)i * W]) >= 1e-14 * amax;
+}
+
+int banded_lu(const Band &A, LUFactors &f, bool freeze) {
+    const int n = A.n, p = A.p, W = 2 * p + 1;
     f.n = n;
     f.p = p;
-    f.l.assign((size_t)n * p, 0.0);
-    f.us.assign((size_t)n * p, 0.0);
-    f.dinv.assign(n, 0.0);
-    Band W = A;
+    f.i_lo = f.i_hi = 0;
     double amax = 0.0;
     for (double v : A.v) amax = std::max(amax, std::fabs(v));
     if (amax == 0.0) return -2;
-    for (int k = 0; k < n; ++k) {
-        double piv = W.at(k, k);
-        if (!(std::fabs(piv) >= 1e-14 * amax)) return -2;
-        for (int i = k + 1; i <= std::min(n - 1, k + p); ++i) {
-            double m = W.at(i, k) / piv;
-            W.at(i, k) = m;
-            for (int j = k + 1; j <= std::min(n - 1, k + p); ++j) W.at(i, j) -= m * W.at(k, j);
+    std::vector<double> Lw((size_t)n * p, 0.0), Ur((size_t)n * W, 0.0);
+    for (int i = 0; i < n; ++i)
+        if (!lu_row(A, Lw, Ur, i, amax)) return -2;
+
+    auto row_close = [&](int a, int b) {
+        for (int k = 0; k < p; ++k) {
+            double x = Lw[(size_t)a * p + k], y = Lw[(size_t)b * p + k];
+            if (std::fabs(x - y) > 4.5e-16 * std::max(std::fabs(x), std::fabs(y))) return false;
+        }
+        for (int k = 0; k <= p; ++k) {
+            double x = Ur[(size_t)a * W + k], y = Ur[(size_t)b * W + k];
+            if (std::fabs(x - y) > 4.5e-16 * std::max(std::fabs(x), std::fabs(y))) return false;
+        }
+        return true;
+    };
+    if (freeze && n > 4 * p + 8) {
+        // A is Toeplitz on rows [2p, n-1-2p] (uniform mesh, host_setup build_space)
+        const int a_hi = n - 1 - 2 * p;
+        int i_lo = -1;
+        for (int i = 2 * p + 1; i + p < a_hi; ++i) {
+            bool ok = true;
+            for (int q = i - p; q < i && ok; ++q) ok = row_close(q, i);
+            if (ok) { i_lo = i; break; }
+        }
+        int i_hi = a_hi - p;  // rows >= i_hi are recomputed from the frozen rows
+        if (i_lo > 0 && i_hi - i_lo > 2 * p) {
+            std::vector<double> L2 = Lw, U2 = Ur;
+            for (int i = i_lo + 1; i < i_hi; ++i) {
+                for (int k = 0; k < p; ++k) L2[(size_t)i * p + k] = Lw[(size_t)i_lo * p + k];
+                for (int k = 0; k < W; ++k) U2[(size_t)i * W + k] = Ur[(size_t)i_lo * W + k];
+            }
+            bool ok = true;
+            for (int i = i_hi; i < n && ok; ++i) ok = lu_row(A, L2, U2, i, amax);
+            // residual of the frozen factorisation over the band
+            double res = 0.0;
+            for (int i = 0; i < n && ok; ++i)
+                for (int j = std::max(0, i - p); j <= std::min(n - 1, i + p); ++j) {
+                    double s = 0.0;
+                    for (int m = std::max(0, std::max(i, j) - p); m <= std::min(i, j); ++m) {
+                        double lim = (m == i) ? 1.0 : L2[(size_t)i * p + (i - m - 1)];
+                        s += lim * U2[(size_t)m * W + (j - m)];
+                    }
+                    res = std::max(res, std::fabs(s - A.get(i, j)));
+                }
+            if (ok && res <= 1e-14 * amax) {
+                Lw.swap(L2);
+                Ur.swap(U2);
+                f.i_lo = i_lo;
+                f.i_hi = i_hi;
+                f.residual = res / amax;
+            }
         }
     }
+    f.l.assign((size_t)n * p, 0.0);
+    f.us.assign((size_t)n * p, 0.0);
+    f.dinv.assign(n, 0.0);
     for (int i = 0; i < n; ++i) {
-        double d = W.at(i, i);
+        double d = Ur[(size_t)i * W];
         f.dinv[i] = 1.0 / d;
         for (int k = 1; k <= p; ++k) {
-            if (i - k >= 0) f.l[(size_t)i * p + k - 1] = W.at(i, i - k);
-            if (i + k < n) f.us[(size_t)i * p + k - 1] = W.at(i, i + k) / d;
+            if (i - k >= 0) f.l[(size_t)i * p + k - 1] = Lw[(size_t)i * p + (k - 1)];
+            if (i + k < n) f.us[(size_t)i * p + k - 1] = Ur[(size_t)i * W + k] / d;
+        }
+    }
+    if (f.i_hi > f.i_lo) {
+        // the frozen rows of us/dinv must be bitwise uniform too
+        for (int i = f.i_lo + 1; i < f.i_hi; ++i) {
+            f.dinv[i] = f.dinv[f.i_lo];
+            for (int k = 0; k < p; ++k) f.us[(size_t)i * p + k] = f.us[(size_t)f.i_lo * p + k];
         }
     }
     return 0;
@@ -180,17 +272,19 @@ void lu_solve_host(const LUFactors &f, double *x) {
     }
 }
 
-void choose_chunks(int n, int p, int cmax, bool odd_len, std::vector<int> &cs) {
-    int minlen = std::max(p, 1);
-    int C = std::max(1, std::min(cmax, n / minlen));
-    int L = (n + C - 1) / C;
-    if (odd_len && L % 2 == 0 && C > 1) L += 1;
-    C = (n + L - 1) / L;
-    // last chunk must hold >= minlen rows; otherwise fold it into its neighbour
-    while (C > 1 && n - (C - 1) * L < minlen) C -= 1;
-    cs.resize(C + 1);
-    for (int c = 0; c < C; ++c) cs[c] = c * L;
-    cs[C] = n;
+int choose_chunks(int n, int p, int cmax, std::vector<int> &cs) {
+    const int need = std::max((n + cmax - 1) / cmax, std::max(p, 1));
+    for (int L : kChunkLens) {
+        if (L < need) continue;
+        const int C = (n + L - 1) / L;
+        // the last chunk must hold >= p rows (its boundary state is p values)
+        if (C > 1 && n - (C - 1) * L < std::max(p, 1)) continue;
+        cs.resize(C + 1);
+        for (int c = 0; c < C; ++c) cs[c] = c * L;
+        cs[C] = n;
+        return L;
+    }
+    return 0;
 }
 
 void build_part_tables(const LUFactors &f, const std::vector<int> &cs, PartTables &t) {

@@ -43,11 +43,22 @@ void load_vector(const Space1D &s, int func, double c, double sigma, double *out
 //   us[i*p + (k-1)] = U(i, i+k) / U(i, i)  (row-scaled upper)
 //   dinv[i]         = 1 / U(i, i)
 // Returns 0, or -2 if a pivot falls below 1e-14 * max|A|.
+//
+// With freeze = true the rows of the factors that have converged in the
+// Toeplitz interior of A (entries changing by < 2 ulp over p+1 consecutive
+// rows) are replaced by one constant row for i in [i_lo, i_hi); rows from
+// i_hi on (where A stops being Toeplitz) are recomputed by the row-wise
+// Doolittle recurrence from the frozen rows.  The result is an LU
+// factorisation of A to rounding; it is accepted only if
+// max |(LU - A)_ij| <= 1e-14 max|A| (else the plain factors are kept and
+// i_lo = i_hi = 0).  Kernels keep the constant row in registers.
 struct LUFactors {
     int n = 0, p = 0;
     std::vector<double> l, us, dinv;
+    int i_lo = 0, i_hi = 0;  // frozen (uniform) rows [i_lo, i_hi)
+    double residual = 0.0;   // max |(LU - A)_ij| / max |A|
 };
-int banded_lu(const Band &A, LUFactors &f);
+int banded_lu(const Band &A, LUFactors &f, bool freeze = false);
 void lu_solve_host(const LUFactors &f, double *x);  // in place, one vector
 
 // Partitioned elimination tables for one direction (chunks of a line solved
@@ -65,9 +76,11 @@ struct PartTables {
     std::vector<int> cs;
     std::vector<double> gf, gb, phif, phib;
 };
-// Choose chunks: C <= cmax, every chunk length >= max(p,1); if odd_len, prefer
-// odd uniform chunk lengths (bank-conflict-free shared-memory transposes).
-void choose_chunks(int n, int p, int cmax, bool odd_len, std::vector<int> &cs);
+// Choose chunks of uniform length L (the last one may be shorter, >= p):
+// L is the smallest value of kChunkLens >= max(ceil(n / cmax), p); returns L
+// (0 if n needs a chunk longer than the largest instantiated length).
+constexpr int kChunkLens[] = {1, 2, 3, 4, 5, 8, 9, 12, 13, 16, 17, 24, 25, 32, 33};
+int choose_chunks(int n, int p, int cmax, std::vector<int> &cs);
 void build_part_tables(const LUFactors &f, const std::vector<int> &cs, PartTables &t);
 
 }  // namespace ads

@@ -23,123 +23,145 @@ namespace ads {
 
 // ------------------------------------------------------------------------------------------
 // fused drift + source + K-apply
+//
+// Tile: 32 (x) x 8 (y) outputs per CTA, marching along z.  Per input plane kk:
+//   commit  P(kk) = U + tau V  -> shared tile (haloed by p in x and y) [+ HBM for owned points]
+//   y-pass  Y1 = My P, Y2 = Ky P          on the 8 owned rows, 32+2p columns
+//   x-pass  S  = Kx Y1 + Mx Y2, T = Mx Y1 on the 32x8 owned points -> register ring slot
+//   z-pass  K P(k) = Mz S + Kz T over the ring (k = kk - p), + source -> r
+// (K = Kx My Mz + Mx Ky Mz + Mx My Kz; 1D factors along different axes commute.)
+// The ring of 2p+1 planes is rotated by unrolling the plane loop 2p+1 times.
 // ------------------------------------------------------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(256) kop_kernel(const KopArgs a) {
-    constexpr int TX = 32, TY = 8, W = 2 * P + 1, HX = TX + 2 * P, HY = TY + 2 * P;
-    constexpr int NE = HX * HY, NQ = (NE + TX * TY - 1) / (TX * TY);
-    __shared__ double Ps[HY][HX];
-    __shared__ double X1[HY][TX], X2[HY][TX];
+struct KopSmem {
+    static constexpr int TX = 32, TY = 8, W = 2 * P + 1, HX = TX + 2 * P, HY = TY + 2 * P;
+    double Ps[HY][HX];
+    double Y1[TY][HX], Y2[TY][HX];
+    double zc[2][2][W];  // [parity][Mz|Kz][c] rows of the output plane
+};
 
-    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+template <int P>
+__global__ void __launch_bounds__(256, 2) kop_kernel(const KopArgs a) {
+    using S_ = KopSmem<P>;
+    constexpr int TX = S_::TX, TY = S_::TY, W = S_::W, HX = S_::HX, HY = S_::HY;
+    __shared__ S_ sm;
+
+    const int tx = threadIdx.x, ty = threadIdx.y;
     const int n0 = a.geo.n0, n1 = a.geo.n1, n2 = a.geo.n2;
     const long sy = a.geo.sy, sz = a.geo.sz;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const int z0 = blockIdx.z * a.zlen, z1 = min(n2, z0 + a.zlen);
     const int gx = x0 + tx, gy = y0 + ty;
-    const bool inx = gx < n0, iny = gy < n1;
+    const bool own = gx < n0 && gy < n1;
 
-    double mxr[W], kxr[W], myr[W], kyr[W];
+    // band rows of this thread's x (Mx, Kx) and y (My, Ky)
+    double mx[W], kx[W], my[W], ky[W];
 #pragma unroll
     for (int c = 0; c < W; ++c) {
-        mxr[c] = inx ? __ldg(a.mx + (long)gx * W + c) : 0.0;
-        kxr[c] = inx ? __ldg(a.kx + (long)gx * W + c) : 0.0;
-        myr[c] = iny ? __ldg(a.my + (long)gy * W + c) : 0.0;
-        kyr[c] = iny ? __ldg(a.ky + (long)gy * W + c) : 0.0;
+        mx[c] = gx < n0 ? __ldg(a.mx + (long)gx * W + c) : 0.0;
+        kx[c] = gx < n0 ? __ldg(a.kx + (long)gx * W + c) : 0.0;
+        my[c] = gy < n1 ? __ldg(a.my + (long)gy * W + c) : 0.0;
+        ky[c] = gy < n1 ? __ldg(a.ky + (long)gy * W + c) : 0.0;
     }
-    double Sr[W], Tr[W];
-#pragma unroll
-    for (int c = 0; c < W; ++c) Sr[c] = Tr[c] = 0.0;
+    const double sxy = (a.bx && own) ? __ldg(a.bx + gx) * __ldg(a.by + gy) : 0.0;
 
-    // prefetch registers for one haloed plane
-    double pu[NQ], pv[NQ];
-    long pidx[NQ];
-    bool pval[NQ];
+    // load slots: haloed (ry, rx) = (ty + 8 sr, tx + 32 sc)
+    constexpr int NSR = (HY + TY - 1) / TY, NS = 2 * NSR;
+    bool sv[NS];
+    long soff[NS];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        int e = tid + q * TX * TY;
-        int ry = e / HX, rx = e - ry * HX;
-        int X = x0 - P + rx, Y = y0 - P + ry;
-        pval[q] = (e < NE) && X >= 0 && X < n0 && Y >= 0 && Y < n1;
-        pidx[q] = (long)Y * sy + X;
+    for (int q = 0; q < NS; ++q) {
+        const int ry = ty + TY * (q >> 1), rx = tx + TX * (q & 1);
+        const int X = x0 - P + rx, Y = y0 - P + ry;
+        sv[q] = ry < HY && rx < HX && X >= 0 && X < n0 && Y >= 0 && Y < n1;
+        soff[q] = (long)Y * sy + X;
     }
+    double pu[NS], pv[NS];
     auto load = [&](int kin) {
         const bool kv = kin >= 0 && kin < n2;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            if (pval[q] && kv) {
-                long idx = (long)kin * sz + pidx[q];
-                pu[q] = __ldg(a.U + idx);
-                pv[q] = __ldg(a.V + idx);
-            } else {
-                pu[q] = 0.0;
-                pv[q] = 0.0;
+        for (int q = 0; q < NS; ++q) {
+            pu[q] = 0.0;
+            pv[q] = 0.0;
+            if (sv[q] && kv) {
+                pu[q] = __ldg(a.U + (long)kin * sz + soff[q]);
+                pv[q] = __ldg(a.V + (long)kin * sz + soff[q]);
             }
         }
     };
 
+    double Sr[W], Tr[W];
+#pragma unroll
+    for (int c = 0; c < W; ++c) Sr[c] = Tr[c] = 0.0;
+
+    const int tid = ty * TX + tx;
     load(z0 - P);
-    for (int kin = z0 - P; kin < z1 + P; ++kin) {
-        // commit plane kin: P = U + tau V into shared memory (and HBM for owned points)
+    for (int kb = z0 - P; kb < z1 + P; kb += W) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            int e = tid + q * TX * TY;
-            if (e < NE) {
-                int ry = e / HX, rx = e - ry * HX;
-                double pp = fma(a.tau, pv[q], pu[q]);
-                Ps[ry][rx] = pp;
-                if (a.Pout && kin >= z0 && kin < z1 && pval[q] && rx >= P && rx < P + TX && ry >= P && ry < P + TY)
-                    a.Pout[(long)kin * sz + pidx[q]] = pp;
-            }
-        }
-        __syncthreads();
-        if (kin + 1 < z1 + P) load(kin + 1);  // in flight during the passes below
+        for (int u = 0; u < W; ++u) {
+            const int kk = kb + u;
+            if (kk < z1 + P) {
+                const int k = kk - P;  // output plane
+                // commit plane kk
+#pragma unroll
+                for (int q = 0; q < NS; ++q) {
+                    const int ry = ty + TY * (q >> 1), rx = tx + TX * (q & 1);
+                    if (ry < HY && rx < HX) {
+                        const double pp = fma(a.tau, pv[q], pu[q]);
+                        sm.Ps[ry][rx] = pp;
+                        if (a.Pout && sv[q] && kk >= z0 && kk < z1 && ry >= P && rx >= P && rx < P + TX &&
+                            ry < P + TY)
+                            a.Pout[(long)kk * sz + soff[q]] = pp;
+                    }
+                }
+                if (tid < 2 * W && k >= z0) {
+                    const double *src = (tid < W ? a.mz : a.kz) + (long)k * W + (tid < W ? tid : tid - W);
+                    sm.zc[kk & 1][tid < W ? 0 : 1][tid < W ? tid : tid - W] = __ldg(src);
+                }
+                __syncthreads();
+                if (kk + 1 < z1 + P) load(kk + 1);  // in flight during the passes below
 
-        // x-pass: X1 = Mx P, X2 = Kx P on all haloed rows
-        for (int ry = ty; ry < HY; ry += TY) {
-            double s1 = 0.0, s2 = 0.0;
+                // y-pass on owned rows, all haloed columns
 #pragma unroll
-            for (int c = 0; c < W; ++c) {
-                double v = Ps[ry][tx + c];
-                s1 = fma(mxr[c], v, s1);
-                s2 = fma(kxr[c], v, s2);
+                for (int cs = 0; cs < 2; ++cs) {
+                    const int col = tx + TX * cs;
+                    if (col < HX) {
+                        double y1 = 0.0, y2 = 0.0;
+#pragma unroll
+                        for (int c = 0; c < W; ++c) {
+                            const double v = sm.Ps[ty + c][col];
+                            y1 = fma(my[c], v, y1);
+                            y2 = fma(ky[c], v, y2);
+                        }
+                        sm.Y1[ty][col] = y1;
+                        sm.Y2[ty][col] = y2;
+                    }
+                }
+                __syncthreads();
+                // x-pass on owned points
+                double s = 0.0, t = 0.0;
+#pragma unroll
+                for (int c = 0; c < W; ++c) {
+                    const double y1 = sm.Y1[ty][tx + c], y2 = sm.Y2[ty][tx + c];
+                    s = fma(kx[c], y1, s);
+                    s = fma(mx[c], y2, s);
+                    t = fma(mx[c], y1, t);
+                }
+                Sr[u] = s;
+                Tr[u] = t;
+                // z-pass: plane k-p+c sits in ring slot (u + 1 + c) mod W
+                if (k >= z0 && own) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int c = 0; c < W; ++c) {
+                        const int slot = (u + 1 + c) % W;
+                        acc = fma(sm.zc[kk & 1][0][c], Sr[slot], acc);
+                        acc = fma(sm.zc[kk & 1][1][c], Tr[slot], acc);
+                    }
+                    const double src = (a.bx) ? a.g * sxy * __ldg(a.bz + k) : 0.0;
+                    a.r[(long)k * sz + (long)gy * sy + gx] = fma(a.sign, acc, src);
+                }
             }
-            X1[ry][tx] = s1;
-            X2[ry][tx] = s2;
-        }
-        __syncthreads();
-
-        // y-pass: S = My Kx P + Ky Mx P,  T = My Mx P
-        double S = 0.0, T = 0.0;
-#pragma unroll
-        for (int c = 0; c < W; ++c) {
-            double x1 = X1[ty + c][tx], x2 = X2[ty + c][tx];
-            S = fma(myr[c], x2, S);
-            S = fma(kyr[c], x1, S);
-            T = fma(myr[c], x1, T);
-        }
-#pragma unroll
-        for (int c = 0; c < W - 1; ++c) {
-            Sr[c] = Sr[c + 1];
-            Tr[c] = Tr[c + 1];
-        }
-        Sr[W - 1] = S;
-        Tr[W - 1] = T;
-
-        // z-pass for output plane k = kin - P:  K P = Mz S + Kz T
-        const int k = kin - P;
-        if (k >= z0 && inx && iny) {
-            const double *mzr = a.mz + (long)k * W;
-            const double *kzr = a.kz + (long)k * W;
-            double acc = 0.0;
-#pragma unroll
-            for (int c = 0; c < W; ++c) {
-                acc = fma(__ldg(mzr + c), Sr[c], acc);
-                acc = fma(__ldg(kzr + c), Tr[c], acc);
-            }
-            double src = 0.0;
-            if (a.bx) src = a.g * __ldg(a.bx + gx) * __ldg(a.by + gy) * __ldg(a.bz + k);
-            a.r[(long)k * sz + (long)gy * sy + gx] = fma(a.sign, acc, src);
         }
     }
 }
@@ -191,16 +213,90 @@ __device__ __forceinline__ void chunk_scan(double (&o)[P], double (&inc)[P], dou
     __syncthreads();
 }
 
-template <int P, int LMAX>
-__global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
+// Forward recurrence y_i = r_i - sum_k l_{i,k} y_{i-k} over the chunk, from the
+// incoming state h (h[0] = y_{s-1}, ...).  UNI: constant coefficients lc.
+// STORE: overwrite v with y.  On return h holds the chunk's tail state.
+template <int P, int L, bool UNI, bool STORE>
+__device__ __forceinline__ void fwd_pass(double (&v)[L], double (&h)[P], int s, int len, const double *__restrict__ Lt,
+                                         const double (&lc)[P]) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+        if (UNI || j < len) {
+            double t = v[j];
+#pragma unroll
+            for (int k = P - 1; k >= 0; --k) t = fma(-(UNI ? lc[k] : __ldg(Lt + (long)(s + j) * P + k)), h[k], t);
+#pragma unroll
+            for (int m = P - 1; m > 0; --m) h[m] = h[m - 1];
+            h[0] = t;
+            if (STORE) v[j] = t;
+        }
+    }
+}
+
+// Backward recurrence x_i = y_i / u_ii - sum_k (u_{i,i+k}/u_ii) x_{i+k} over the chunk,
+// from the incoming state h (h[0] = x_e, ...).  On return h holds the head state.
+template <int P, int L, bool UNI, bool STORE>
+__device__ __forceinline__ void bwd_pass(double (&v)[L], double (&h)[P], int s, int len, const double *__restrict__ Ut,
+                                         const double *__restrict__ Dt, const double (&uc)[P], double dc) {
+#pragma unroll
+    for (int j = L - 1; j >= 0; --j) {
+        if (UNI || j < len) {
+            double t = v[j] * (UNI ? dc : __ldg(Dt + s + j));
+#pragma unroll
+            for (int k = P - 1; k >= 0; --k) t = fma(-(UNI ? uc[k] : __ldg(Ut + (long)(s + j) * P + k)), h[k], t);
+#pragma unroll
+            for (int m = P - 1; m > 0; --m) h[m] = h[m - 1];
+            h[0] = t;
+            if (STORE) v[j] = t;
+        }
+    }
+}
+
+// Uniform chunks (len == L, constant coefficients): the last P values live in a
+// register ring R indexed by position mod P (all indices compile-time).
+template <int P, int L, bool STORE>
+__device__ __forceinline__ void fwd_uni(double (&v)[L], double (&h)[P], const double (&lc)[P]) {
+    double R[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) R[((-1 - m) % P + P) % P] = h[m];  // y_{-1-m}
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+        double t = v[j];
+#pragma unroll
+        for (int k = P; k >= 1; --k) t = fma(-lc[k - 1], R[((j - k) % P + P) % P], t);
+        R[j % P] = t;
+        if (STORE) v[j] = t;
+    }
+#pragma unroll
+    for (int m = 0; m < P; ++m) h[m] = R[((L - 1 - m) % P + P) % P];  // tail y_{L-1-m}
+}
+
+template <int P, int L, bool STORE>
+__device__ __forceinline__ void bwd_uni(double (&v)[L], double (&h)[P], const double (&uc)[P], double dc) {
+    double R[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) R[(L + m) % P] = h[m];  // x_{L+m}
+#pragma unroll
+    for (int j = L - 1; j >= 0; --j) {
+        double t = v[j] * dc;
+#pragma unroll
+        for (int k = P; k >= 1; --k) t = fma(-uc[k - 1], R[(j + k) % P], t);
+        R[j % P] = t;
+        if (STORE) v[j] = t;
+    }
+#pragma unroll
+    for (int m = 0; m < P; ++m) h[m] = R[m % P];  // head x_m
+}
+
+template <int P, int L>
+__global__ void __launch_bounds__(256, 3) sweep_kernel(const SweepArgs a) {
     extern __shared__ double smem[];
     const int xl = threadIdx.x, c = threadIdx.y, C = a.t.C;
     const int nthr = XW * C, tid = c * XW + xl;
     const int n = a.t.n;
-    double *sbuf = smem;                        // 3 * C * XW * P scan buffers
-    double *tile = smem + 3 * C * XW * P;       // x-lines: XW x npad
+    double *sbuf = smem;                   // 3 * C * XW * P scan buffers
+    double *tile = smem + 3 * C * XW * P;  // x-lines: XW x npad
 
-    // line set: lines indexed (la, lb); the XW lines of this CTA are la0 .. la0+XW-1
     const Geom &g = a.geo;
     long sa, sb, sl;
     int na;
@@ -209,130 +305,102 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
     else { sa = 1; sb = g.sy; sl = g.sz; na = g.n0; }
     const int la0 = blockIdx.x * XW, lb = blockIdx.y;
     const long base = (long)lb * sb + (long)la0 * sa;
-    const int la = la0 + xl;
-    const bool valid = la < na;
+    const bool valid = la0 + xl < na;
 
-    const int s = __ldg(a.t.cs + c), len = __ldg(a.t.cs + c + 1) - s;
-    double v[LMAX];
+    const int s = c * L, len = min(L, n - s);
+    const bool uni = s >= a.t.i_lo && s + L <= a.t.i_hi;
+    double lc[P], uc[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        lc[k] = a.t.lc[k];
+        uc[k] = a.t.usc[k];
+    }
+    const double dc = a.t.dic;
 
-    int npad = n | 1;  // odd row pitch: conflict-free transposed reads
+    double v[L];
+    const int npad = n | 1;  // odd row pitch: conflict-free transposed reads
+    const int ntile = min(XW, na - la0) * n;  // x: nl consecutive lines, contiguous (sy == n0)
+    const double inv_n = 1.0 / n;
     if (a.dir == 0) {
-        const int nl = min(XW, na - la0);
-        for (int q = 0; q < nl; ++q) {
-            const double *src = a.in + base + (long)q * sa;
-            for (int i = tid; i < n; i += nthr) tile[q * npad + i] = __ldg(src + i);
+        // every thread issues its L loads before any store (loads in flight together)
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            const int e = tid + j * nthr;
+            v[j] = e < ntile ? __ldg(a.in + base + e) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            const int e = tid + j * nthr;
+            if (e < ntile) {
+                const int q = __double2int_rz((e + 0.5) * inv_n);
+                tile[q * npad + (e - q * n)] = v[j];
+            }
         }
         __syncthreads();
 #pragma unroll
-        for (int j = 0; j < LMAX; ++j) v[j] = (j < len && valid) ? tile[xl * npad + s + j] : 0.0;
+        for (int j = 0; j < L; ++j) v[j] = (j < len && valid) ? tile[xl * npad + s + j] : 0.0;
     } else {
         const double *src = a.in + base + xl + (long)s * sl;
 #pragma unroll
-        for (int j = 0; j < LMAX; ++j) v[j] = (j < len && valid) ? __ldg(src + (long)j * sl) : 0.0;
+        for (int j = 0; j < L; ++j) v[j] = (j < len && valid) ? __ldg(src + (long)j * sl) : 0.0;
     }
 
-    const double *L = a.t.l, *US = a.t.us, *DI = a.t.dinv;
-    double h[P], o[P], inc[P];
+    const double *Lt = a.t.l, *Ut = a.t.us, *Dt = a.t.dinv;
+    double h[P], inc[P];
 
-    // pass 1: forward recurrence y_i = r_i - sum_k l_{i,k} y_{i-k} from zero state -> tail
+    // pass 1: forward from zero state -> tail; scan; pass 2: forward from the exact state
 #pragma unroll
     for (int m = 0; m < P; ++m) h[m] = 0.0;
-#pragma unroll
-    for (int j = 0; j < LMAX; ++j) {
-        if (j < len) {
-            const double *lr = L + (long)(s + j) * P;
-            double t = v[j];
-#pragma unroll
-            for (int k = P - 1; k >= 0; --k) t = fma(-__ldg(lr + k), h[k], t);
-#pragma unroll
-            for (int m = P - 1; m > 0; --m) h[m] = h[m - 1];
-            h[0] = t;
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < P; ++m) o[m] = h[m];
-    if (a.t.C > 1) {
-        chunk_scan<P, true>(o, inc, sbuf, a.t.phif, C, a.t.levels, c, xl);
-    } else {
+    if (uni) fwd_uni<P, L, false>(v, h, lc);
+    else fwd_pass<P, L, false, false>(v, h, s, len, Lt, lc);
+    if (C > 1) chunk_scan<P, true>(h, inc, sbuf, a.t.phif, C, a.t.levels, c, xl);
+    else {
 #pragma unroll
         for (int m = 0; m < P; ++m) inc[m] = 0.0;
     }
-    // pass 2: forward recurrence from the exact incoming state
 #pragma unroll
     for (int m = 0; m < P; ++m) h[m] = inc[m];
-#pragma unroll
-    for (int j = 0; j < LMAX; ++j) {
-        if (j < len) {
-            const double *lr = L + (long)(s + j) * P;
-            double t = v[j];
-#pragma unroll
-            for (int k = P - 1; k >= 0; --k) t = fma(-__ldg(lr + k), h[k], t);
-#pragma unroll
-            for (int m = P - 1; m > 0; --m) h[m] = h[m - 1];
-            h[0] = t;
-            v[j] = t;
-        }
-    }
-    // pass 3: backward recurrence x_i = y_i / u_ii - sum_k (u_{i,i+k}/u_ii) x_{i+k} from zero -> head
+    if (uni) fwd_uni<P, L, true>(v, h, lc);
+    else fwd_pass<P, L, false, true>(v, h, s, len, Lt, lc);
+
+    // pass 3: backward from zero state -> head; scan; pass 4: backward from the exact state
 #pragma unroll
     for (int m = 0; m < P; ++m) h[m] = 0.0;
-#pragma unroll
-    for (int j = LMAX - 1; j >= 0; --j) {
-        if (j < len) {
-            const double *ur = US + (long)(s + j) * P;
-            double t = v[j] * __ldg(DI + s + j);
-#pragma unroll
-            for (int k = P - 1; k >= 0; --k) t = fma(-__ldg(ur + k), h[k], t);
-#pragma unroll
-            for (int m = P - 1; m > 0; --m) h[m] = h[m - 1];
-            h[0] = t;
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < P; ++m) o[m] = h[m];
-    if (a.t.C > 1) {
-        chunk_scan<P, false>(o, inc, sbuf, a.t.phib, C, a.t.levels, c, xl);
-    } else {
+    if (uni) bwd_uni<P, L, false>(v, h, uc, dc);
+    else bwd_pass<P, L, false, false>(v, h, s, len, Ut, Dt, uc, dc);
+    if (C > 1) chunk_scan<P, false>(h, inc, sbuf, a.t.phib, C, a.t.levels, c, xl);
+    else {
 #pragma unroll
         for (int m = 0; m < P; ++m) inc[m] = 0.0;
     }
-    // pass 4: backward recurrence from the exact incoming state
 #pragma unroll
     for (int m = 0; m < P; ++m) h[m] = inc[m];
-#pragma unroll
-    for (int j = LMAX - 1; j >= 0; --j) {
-        if (j < len) {
-            const double *ur = US + (long)(s + j) * P;
-            double t = v[j] * __ldg(DI + s + j);
-#pragma unroll
-            for (int k = P - 1; k >= 0; --k) t = fma(-__ldg(ur + k), h[k], t);
-#pragma unroll
-            for (int m = P - 1; m > 0; --m) h[m] = h[m - 1];
-            h[0] = t;
-            v[j] = t;
-        }
-    }
+    if (uni) bwd_uni<P, L, true>(v, h, uc, dc);
+    else bwd_pass<P, L, false, true>(v, h, s, len, Ut, Dt, uc, dc);
 
     // store
     if (a.dir == 0) {
 #pragma unroll
-        for (int j = 0; j < LMAX; ++j)
+        for (int j = 0; j < L; ++j)
             if (j < len) tile[xl * npad + s + j] = v[j];
         __syncthreads();
-        const int nl = min(XW, na - la0);
-        for (int q = 0; q < nl; ++q) {
-            double *dst = a.out + base + (long)q * sa;
-            for (int i = tid; i < n; i += nthr) dst[i] = tile[q * npad + i];
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            const int e = tid + j * nthr;
+            if (e < ntile) {
+                const int q = __double2int_rz((e + 0.5) * inv_n);
+                a.out[base + e] = tile[q * npad + (e - q * n)];
+            }
         }
     } else if (valid) {
         const long off = base + xl + (long)s * sl;
         if (a.mode == 0) {
 #pragma unroll
-            for (int j = 0; j < LMAX; ++j)
+            for (int j = 0; j < L; ++j)
                 if (j < len) a.out[off + (long)j * sl] = v[j];
         } else {
 #pragma unroll
-            for (int j = 0; j < LMAX; ++j)
+            for (int j = 0; j < L; ++j)
                 if (j < len) {
                     const long idx = off + (long)j * sl;
                     a.V[idx] = fma(a.kick, v[j], a.V[idx]);
@@ -455,7 +523,7 @@ int launch_kop(int p, const KopArgs &a, cudaStream_t s) {
     return 0;
 }
 
-template <int P, int LMAX>
+template <int P, int L>
 static void sweep_launch(const SweepArgs &a, cudaStream_t s) {
     const Geom &g = a.geo;
     int na = a.dir == 0 ? g.n1 : g.n0;
@@ -466,23 +534,22 @@ static void sweep_launch(const SweepArgs &a, cudaStream_t s) {
     if (a.dir == 0) sm += sizeof(double) * (size_t)XW * (a.t.n | 1);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(sweep_kernel<P, LMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(sweep_kernel<P, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    sweep_kernel<P, LMAX><<<grd, blk, sm, s>>>(a);
+    sweep_kernel<P, L><<<grd, blk, sm, s>>>(a);
 }
 
 template <int P>
 static int sweep_dispatch(const SweepArgs &a, cudaStream_t s) {
-    int L = a.t.lmax;
-    if (L <= 4) sweep_launch<P, 4>(a, s);
-    else if (L <= 8) sweep_launch<P, 8>(a, s);
-    else if (L <= 12) sweep_launch<P, 12>(a, s);
-    else if (L <= 17) sweep_launch<P, 17>(a, s);
-    else if (L <= 24) sweep_launch<P, 24>(a, s);
-    else if (L <= 33) sweep_launch<P, 33>(a, s);
-    else return -1;
-    return 0;
+    switch (a.t.L) {
+#define ADS_L(LV) \
+    case LV: sweep_launch<P, LV>(a, s); return 0;
+        ADS_L(1) ADS_L(2) ADS_L(3) ADS_L(4) ADS_L(5) ADS_L(8) ADS_L(9) ADS_L(12) ADS_L(13) ADS_L(16) ADS_L(17)
+        ADS_L(24) ADS_L(25) ADS_L(32) ADS_L(33)
+#undef ADS_L
+    }
+    return -1;
 }
 
 int launch_sweep(int p, const SweepArgs &a, cudaStream_t s) {

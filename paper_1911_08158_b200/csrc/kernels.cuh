@@ -6,11 +6,17 @@ namespace ads {
 
 // Banded 1D matrix on the device: b[i*(2p+1) + c] = A(i, i - p + c).
 // Factor tables of A_d = M_d + tau^2/4 K_d (see host_setup.h LUFactors/PartTables).
+// Rows [i_lo, i_hi) of the factors are one constant row (lc, usc, dic): chunks
+// entirely inside run with register-resident coefficients.  Chunks are of
+// uniform length L (the last one may be shorter).
+constexpr int kMaxP = 5;
 struct SolveTab {
     const double *l = nullptr, *us = nullptr, *dinv = nullptr;
     const double *phif = nullptr, *phib = nullptr;
     const int *cs = nullptr;
-    int n = 0, C = 0, levels = 0, lmax = 0;
+    int n = 0, C = 0, levels = 0, L = 0;
+    int i_lo = 0, i_hi = 0;
+    double lc[kMaxP] = {0, 0, 0, 0, 0}, usc[kMaxP] = {0, 0, 0, 0, 0}, dic = 0.0;
 };
 
 // Geometry of a field: x-fastest, sy = row stride, sz = plane stride (elements).
