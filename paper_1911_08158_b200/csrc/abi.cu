@@ -167,14 +167,23 @@ int build_direction(ads_ctx *h, int d) {
     std::vector<int> cs;
     const int L = choose_chunks(n, p, 32, cs);
     if (L == 0) return fail(h, ADS_E_INVAL, "n_%d = %d: no supported chunking", d, n);
+    // pad the factors to C*L rows with identity rows: every chunk has length L
+    const int C = (int)cs.size() - 1, npad = C * L;
+    LUFactors fp = f;
+    fp.n = npad;
+    fp.l.resize((size_t)npad * p, 0.0);
+    fp.us.resize((size_t)npad * p, 0.0);
+    fp.dinv.resize(npad, 1.0);
+    std::vector<int> csp(cs);
+    csp[C] = npad;
     PartTables pt;
-    build_part_tables(f, cs, pt);
+    build_part_tables(fp, csp, pt);
     DirDev &D = h->dd[d];
     int rc;
     std::vector<double> mb(s.M.v), kb(s.K.v), ab(A.v);
     (void)W;
     if ((rc = upload(h, &D.mband, mb)) || (rc = upload(h, &D.kband, kb)) || (rc = upload(h, &D.aband, ab)) ||
-        (rc = upload(h, &D.l, f.l)) || (rc = upload(h, &D.us, f.us)) || (rc = upload(h, &D.dinv, f.dinv)) ||
+        (rc = upload(h, &D.l, fp.l)) || (rc = upload(h, &D.us, fp.us)) || (rc = upload(h, &D.dinv, fp.dinv)) ||
         (rc = upload(h, &D.phif, pt.phif)) || (rc = upload(h, &D.phib, pt.phib)) || (rc = upload(h, &D.cs, pt.cs)))
         return rc;
     D.tab.l = D.l;
@@ -187,9 +196,11 @@ int build_direction(ads_ctx *h, int d) {
     D.tab.C = pt.C;
     D.tab.levels = pt.levels;
     D.tab.L = L;
-    D.tab.i_lo = f.i_lo;
-    D.tab.i_hi = f.i_hi;
-    if (f.i_hi > f.i_lo) {
+    // uniform region aligned to whole chunks: chunks [c_lo, c_hi) lie inside [i_lo, i_hi)
+    const int c_lo = (f.i_lo + L - 1) / L, c_hi = f.i_hi / L;
+    D.tab.i_lo = c_hi > c_lo ? c_lo * L : 0;
+    D.tab.i_hi = c_hi > c_lo ? c_hi * L : 0;
+    if (D.tab.i_hi > D.tab.i_lo) {
         for (int k = 0; k < p; ++k) {
             D.tab.lc[k] = f.l[(size_t)f.i_lo * p + k];
             D.tab.usc[k] = f.us[(size_t)f.i_lo * p + k];

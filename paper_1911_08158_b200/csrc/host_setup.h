@@ -79,7 +79,8 @@ struct PartTables {
 // Choose chunks of uniform length L (the last one may be shorter, >= p):
 // L is the smallest value of kChunkLens >= max(ceil(n / cmax), p); returns L
 // (0 if n needs a chunk longer than the largest instantiated length).
-constexpr int kChunkLens[] = {1, 2, 3, 4, 5, 8, 9, 12, 13, 16, 17, 24, 25, 32, 33};
+// odd lengths only: lane-per-chunk shared-memory reads (stride L) are bank-conflict-free
+constexpr int kChunkLens[] = {1, 3, 5, 9, 13, 17, 21, 25, 33};
 int choose_chunks(int n, int p, int cmax, std::vector<int> &cs);
 void build_part_tables(const LUFactors &f, const std::vector<int> &cs, PartTables &t);
 

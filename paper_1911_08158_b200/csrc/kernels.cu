@@ -15,6 +15,7 @@
 //                  and one write per element.  x-lines are staged through shared
 //                  memory (coalesced); y/z lines are loaded coalesced across 8
 //                  adjacent x-lines.  The z sweep fuses the kick V += tau a.
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -168,245 +169,296 @@ __global__ void __launch_bounds__(256, 2) kop_kernel(const KopArgs a) {
 
 // ------------------------------------------------------------------------------------------
 // partitioned banded sweeps
+//
+// A CTA owns a tile of XW = 8 adjacent lines; warp w solves line w, lane c owns
+// chunk c (rows [cL, cL+L), L odd, C <= 32 chunks; lines are padded to C*L rows
+// with identity rows).  Per lane, four p-term recurrences over its chunk held in
+// registers:
+//   1. forward  y_i = r_i - sum_k l_{i,k} y_{i-k}                 zero incoming state -> tail
+//   2. forward                                                    exact incoming state
+//   3. backward x_i = y_i/u_ii - sum_k (u_{i,i+k}/u_ii) x_{i+k}    zero incoming state -> head
+//   4. backward                                                   exact incoming state
+// The exact incoming states come from a Kogge-Stone scan of the affine chunk
+// maps across the lanes (shuffles; Phi = products of chunk transfer matrices,
+// host-precomputed).  No block barrier inside the solve.
+// The tile moves HBM <-> shared memory with coalesced cooperative loads/stores;
+// y/z tiles are stored [row][XW+1] (odd pitch) and x tiles [line][n], so the
+// lane-per-chunk reads (stride L, odd) are bank-conflict-free.
+// Rows [i_lo, i_hi) of the factors are one constant row held in registers;
+// the other ("edge") rows are read from a shared-memory table.
 // ------------------------------------------------------------------------------------------
-constexpr int XW = 8;  // lines per CTA (adjacent lines; coalescing axis for y/z)
+constexpr int XW = 8;        // lines per CTA
+constexpr int YP = XW + 1;   // y/z tile row pitch (doubles)
+constexpr int SWEEP_THREADS = 32 * XW;
 
-// Kogge-Stone scan of the chunk boundary states across the C chunks of each of
-// the XW lines of the CTA.  forward: o_c += Phi_c^(lv) o_{c-2^lv};
-// backward: o_c += Psi_c^(lv) o_{c+2^lv}.  Returns the neighbour's final state
-// (the incoming state of this chunk) in inc[].
 template <int P, bool FWD>
-__device__ __forceinline__ void chunk_scan(double (&o)[P], double (&inc)[P], double *sbuf, const double *phi,
-                                           int C, int levels, int c, int xl) {
+__device__ __forceinline__ void warp_scan(double (&o)[P], double (&inc)[P], const double *phi, int C, int levels,
+                                          int lane) {
     for (int lv = 0; lv < levels; ++lv) {
         const int d = 1 << lv;
-        double *buf = sbuf + (lv & 1) * (C * XW * P);
+        double u[P];
 #pragma unroll
-        for (int m = 0; m < P; ++m) buf[(c * XW + xl) * P + m] = o[m];
-        __syncthreads();
-        const int src = FWD ? c - d : c + d;
-        if (FWD ? (src >= 0) : (src < C)) {
-            double u[P];
-#pragma unroll
-            for (int m = 0; m < P; ++m) u[m] = buf[(src * XW + xl) * P + m];
-            const double *ph = phi + ((long)lv * C + c) * P * P;
+        for (int m = 0; m < P; ++m)
+            u[m] = FWD ? __shfl_up_sync(0xffffffffu, o[m], d) : __shfl_down_sync(0xffffffffu, o[m], d);
+        const bool has = FWD ? (lane >= d && lane < C) : (lane + d < C);
+        if (has) {
+            const double *ph = phi + (lv * C + lane) * P * P;
             double t[P];
 #pragma unroll
             for (int i = 0; i < P; ++i) {
                 double s = o[i];
 #pragma unroll
-                for (int j = 0; j < P; ++j) s = fma(__ldg(ph + i * P + j), u[j], s);
+                for (int j = 0; j < P; ++j) s = fma(ph[i * P + j], u[j], s);
                 t[i] = s;
             }
 #pragma unroll
             for (int i = 0; i < P; ++i) o[i] = t[i];
         }
     }
-    double *buf = sbuf + 2 * (C * XW * P);
 #pragma unroll
-    for (int m = 0; m < P; ++m) buf[(c * XW + xl) * P + m] = o[m];
-    __syncthreads();
-    const int nb = FWD ? c - 1 : c + 1;
-    const bool has = FWD ? (nb >= 0) : (nb < C);
-#pragma unroll
-    for (int m = 0; m < P; ++m) inc[m] = has ? buf[(nb * XW + xl) * P + m] : 0.0;
-    __syncthreads();
-}
-
-// Forward recurrence y_i = r_i - sum_k l_{i,k} y_{i-k} over the chunk, from the
-// incoming state h (h[0] = y_{s-1}, ...).  UNI: constant coefficients lc.
-// STORE: overwrite v with y.  On return h holds the chunk's tail state.
-template <int P, int L, bool UNI, bool STORE>
-__device__ __forceinline__ void fwd_pass(double (&v)[L], double (&h)[P], int s, int len, const double *__restrict__ Lt,
-                                         const double (&lc)[P]) {
-#pragma unroll
-    for (int j = 0; j < L; ++j) {
-        if (UNI || j < len) {
-            double t = v[j];
-#pragma unroll
-            for (int k = P - 1; k >= 0; --k) t = fma(-(UNI ? lc[k] : __ldg(Lt + (long)(s + j) * P + k)), h[k], t);
-#pragma unroll
-            for (int m = P - 1; m > 0; --m) h[m] = h[m - 1];
-            h[0] = t;
-            if (STORE) v[j] = t;
-        }
+    for (int m = 0; m < P; ++m) {
+        const double w = FWD ? __shfl_up_sync(0xffffffffu, o[m], 1) : __shfl_down_sync(0xffffffffu, o[m], 1);
+        inc[m] = (FWD ? lane >= 1 : lane + 1 < C) ? w : 0.0;
     }
 }
 
-// Backward recurrence x_i = y_i / u_ii - sum_k (u_{i,i+k}/u_ii) x_{i+k} over the chunk,
-// from the incoming state h (h[0] = x_e, ...).  On return h holds the head state.
-template <int P, int L, bool UNI, bool STORE>
-__device__ __forceinline__ void bwd_pass(double (&v)[L], double (&h)[P], int s, int len, const double *__restrict__ Ut,
-                                         const double *__restrict__ Dt, const double (&uc)[P], double dc) {
-#pragma unroll
-    for (int j = L - 1; j >= 0; --j) {
-        if (UNI || j < len) {
-            double t = v[j] * (UNI ? dc : __ldg(Dt + s + j));
-#pragma unroll
-            for (int k = P - 1; k >= 0; --k) t = fma(-(UNI ? uc[k] : __ldg(Ut + (long)(s + j) * P + k)), h[k], t);
-#pragma unroll
-            for (int m = P - 1; m > 0; --m) h[m] = h[m - 1];
-            h[0] = t;
-            if (STORE) v[j] = t;
-        }
-    }
-}
+// Coefficient rows in shared memory, 16-byte aligned records of CW doubles:
+//   forward  record: l_1 .. l_P            (padded to an even count)
+//   backward record: dinv, us_1 .. us_P    (padded to an even count)
+template <int P> struct CoefLayout {
+    static constexpr int FW = (P + 1) & ~1;        // forward record doubles
+    static constexpr int BW = (P + 2) & ~1;        // backward record doubles
+};
 
-// Uniform chunks (len == L, constant coefficients): the last P values live in a
-// register ring R indexed by position mod P (all indices compile-time).
-template <int P, int L, bool STORE>
-__device__ __forceinline__ void fwd_uni(double (&v)[L], double (&h)[P], const double (&lc)[P]) {
+// One recurrence pass over a chunk (all lanes run the same instructions).
+// FWD: y_j = v_j - sum_k l_k y_{j-k};   BWD: x_j = v_j d_j - sum_k us_k x_{j+k}.
+// h: incoming state on entry (h[0] = y_{s-1} / x_{e}), outgoing state on exit
+// (tail y_{e-1-m} / head x_{s+m}).  Register ring R[pos mod P] (no moves).
+// Row j of the chunk's coefficients is at rec + j*rstride (rstride = 0 for
+// chunks inside the uniform interior: every read is the same broadcast row).
+template <int P, int L, bool FWD, bool STORE>
+__device__ __forceinline__ void rec_pass(double (&v)[L], double (&h)[P], const double *rec, int rstride) {
+    constexpr int NC = FWD ? CoefLayout<P>::FW : CoefLayout<P>::BW;
     double R[P];
+    if (FWD) {
 #pragma unroll
-    for (int m = 0; m < P; ++m) R[((-1 - m) % P + P) % P] = h[m];  // y_{-1-m}
+        for (int m = 0; m < P; ++m) R[((-1 - m) % P + P) % P] = h[m];
+    } else {
 #pragma unroll
-    for (int j = 0; j < L; ++j) {
-        double t = v[j];
+        for (int m = 0; m < P; ++m) R[(L + m) % P] = h[m];
+    }
 #pragma unroll
-        for (int k = P; k >= 1; --k) t = fma(-lc[k - 1], R[((j - k) % P + P) % P], t);
+    for (int q = 0; q < L; ++q) {
+        const int j = FWD ? q : L - 1 - q;
+        const double2 *rp = reinterpret_cast<const double2 *>(rec + j * rstride);
+        double cf[NC];
+#pragma unroll
+        for (int k = 0; k < NC / 2; ++k) {
+            const double2 d2 = rp[k];
+            cf[2 * k] = d2.x;
+            cf[2 * k + 1] = d2.y;
+        }
+        double t;
+        if (FWD) {
+            t = v[j];
+#pragma unroll
+            for (int k = P; k >= 1; --k) t = fma(-cf[k - 1], R[((j - k) % P + P) % P], t);
+        } else {
+            t = v[j] * cf[0];
+#pragma unroll
+            for (int k = P; k >= 1; --k) t = fma(-cf[k], R[(j + k) % P], t);
+        }
         R[j % P] = t;
         if (STORE) v[j] = t;
     }
+    if (FWD) {
 #pragma unroll
-    for (int m = 0; m < P; ++m) h[m] = R[((L - 1 - m) % P + P) % P];  // tail y_{L-1-m}
-}
-
-template <int P, int L, bool STORE>
-__device__ __forceinline__ void bwd_uni(double (&v)[L], double (&h)[P], const double (&uc)[P], double dc) {
-    double R[P];
+        for (int m = 0; m < P; ++m) h[m] = R[((L - 1 - m) % P + P) % P];
+    } else {
 #pragma unroll
-    for (int m = 0; m < P; ++m) R[(L + m) % P] = h[m];  // x_{L+m}
-#pragma unroll
-    for (int j = L - 1; j >= 0; --j) {
-        double t = v[j] * dc;
-#pragma unroll
-        for (int k = P; k >= 1; --k) t = fma(-uc[k - 1], R[(j + k) % P], t);
-        R[j % P] = t;
-        if (STORE) v[j] = t;
+        for (int m = 0; m < P; ++m) h[m] = R[m];
     }
-#pragma unroll
-    for (int m = 0; m < P; ++m) h[m] = R[m % P];  // head x_m
 }
 
+// Lanes >= C (no chunk) skip the passes; the warp scans are reached by all lanes.
+#ifdef ADS_PHASE_TIMING
+__device__ long long g_sub[4][8];
+#define SUB(k)                                                                                  \
+    do {                                                                                        \
+        if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 64 + 10))                    \
+            g_sub[threadIdx.x == 0 ? 0 : 1][k] = clock64();                                     \
+    } while (0)
+#else
+#define SUB(k) \
+    do {       \
+    } while (0)
+#endif
 template <int P, int L>
-__global__ void __launch_bounds__(256, 3) sweep_kernel(const SweepArgs a) {
-    extern __shared__ double smem[];
-    const int xl = threadIdx.x, c = threadIdx.y, C = a.t.C;
-    const int nthr = XW * C, tid = c * XW + xl;
-    const int n = a.t.n;
-    double *sbuf = smem;                   // 3 * C * XW * P scan buffers
-    double *tile = smem + 3 * C * XW * P;  // x-lines: XW x npad
+__device__ __forceinline__ void solve_chunk(double (&v)[L], bool active, const double *fr, const double *br,
+                                            int rstride_f, int rstride_b, const double *phif, const double *phib,
+                                            int C, int levels, int lane) {
+    double h[P], inc[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) h[m] = 0.0;
+    SUB(0);
+    if (active) rec_pass<P, L, true, false>(v, h, fr, rstride_f);
+    __syncwarp();
+    SUB(1);
+    warp_scan<P, true>(h, inc, phif, C, levels, lane);
+    SUB(2);
+    if (active) rec_pass<P, L, true, true>(v, inc, fr, rstride_f);
+    SUB(3);
+#pragma unroll
+    for (int m = 0; m < P; ++m) h[m] = 0.0;
+    if (active) rec_pass<P, L, false, false>(v, h, br, rstride_b);
+    __syncwarp();
+    SUB(4);
+    warp_scan<P, false>(h, inc, phib, C, levels, lane);
+    SUB(5);
+    if (active) rec_pass<P, L, false, true>(v, inc, br, rstride_b);
+    SUB(6);
+}
+
+#ifdef ADS_PHASE_TIMING
+__device__ long long g_phase[64][16];
+#define PHASE(k)                                                                  \
+    do {                                                                          \
+        if (blockIdx.x < 8 && t == (int)blockIdx.x && (tid == 0 || tid == 80))     \
+            g_phase[blockIdx.x * 3 + (tid == 0 ? 0 : 1)][k] = clock64();          \
+    } while (0)
+#else
+#define PHASE(k) \
+    do {         \
+    } while (0)
+#endif
+
+// Persistent CTAs; tiles (XW lines) round-robin.
+template <int P, int L>
+__global__ void __launch_bounds__(SWEEP_THREADS, 4) sweep_kernel(const SweepArgs a) {
+    constexpr int FW = CoefLayout<P>::FW, BW = CoefLayout<P>::BW;
+    extern __shared__ __align__(16) double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int C = a.t.C, n = a.t.n, levels = a.t.levels;
+    const int i_lo = a.t.i_lo, i_hi = a.t.i_hi, nedge = C * L - (i_hi - i_lo);
+    const int nphi = max(levels, 1) * C * P * P;
+    // edge rows (outside [i_lo, i_hi)) + one extra record: the constant interior row
+    double *fwd = smem;                            // (nedge + 1) * FW
+    double *bwd = fwd + (nedge + 1) * FW;          // (nedge + 1) * BW
+    double *sphif = bwd + (nedge + 1) * BW;        // scan matrices (forward, backward)
+    double *sphib = sphif + nphi;
+    double *tile = sphib + nphi;                   // x: [XW][n]; y/z: [C*L][YP]
+    for (int e = tid; e < nphi; e += SWEEP_THREADS) {
+        sphif[e] = __ldg(a.t.phif + e);
+        sphib[e] = __ldg(a.t.phib + e);
+    }
+    for (int e = tid; e <= nedge; e += SWEEP_THREADS) {
+        const bool cst = e == nedge;
+        const int i = e < i_lo ? e : e + (i_hi - i_lo);
+#pragma unroll
+        for (int k = 0; k < FW; ++k) fwd[e * FW + k] = k < P ? (cst ? a.t.lc[k] : __ldg(a.t.l + (long)i * P + k)) : 0.0;
+        bwd[e * BW] = cst ? a.t.dic : __ldg(a.t.dinv + i);
+#pragma unroll
+        for (int k = 1; k < BW; ++k)
+            bwd[e * BW + k] = k <= P ? (cst ? a.t.usc[k - 1] : __ldg(a.t.us + (long)i * P + k - 1)) : 0.0;
+    }
 
     const Geom &g = a.geo;
     long sa, sb, sl;
-    int na;
-    if (a.dir == 0) { sa = g.sy; sb = g.sz; sl = 1; na = g.n1; }
-    else if (a.dir == 1) { sa = 1; sb = g.sz; sl = g.sy; na = g.n0; }
-    else { sa = 1; sb = g.sy; sl = g.sz; na = g.n0; }
-    const int la0 = blockIdx.x * XW, lb = blockIdx.y;
-    const long base = (long)lb * sb + (long)la0 * sa;
-    const bool valid = la0 + xl < na;
+    int na, nb;
+    if (a.dir == 0) { sa = g.sy; sb = g.sz; sl = 1; na = g.n1; nb = g.n2; }
+    else if (a.dir == 1) { sa = 1; sb = g.sz; sl = g.sy; na = g.n0; nb = g.n2; }
+    else { sa = 1; sb = g.sy; sl = g.sz; na = g.n0; nb = g.n1; }
+    const int nab = (na + XW - 1) / XW, ntiles = nab * nb;
 
-    const int s = c * L, len = min(L, n - s);
-    const bool uni = s >= a.t.i_lo && s + L <= a.t.i_hi;
-    double lc[P], uc[P];
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        lc[k] = a.t.lc[k];
-        uc[k] = a.t.usc[k];
-    }
-    const double dc = a.t.dic;
+    const int s = lane * L;  // chunk start (lanes >= C idle in the passes)
+    const bool active = lane < C;
+    const bool uni = s >= i_lo && s + L <= i_hi;
+    const int erow = uni ? nedge : (s < i_lo ? s : s - (i_hi - i_lo));
+    const double *fr = fwd + (active ? erow : nedge) * FW;
+    const double *br = bwd + (active ? erow : nedge) * BW;
+    const int rsf = (uni || !active) ? 0 : FW, rsb = (uni || !active) ? 0 : BW;
+    constexpr int NLD = 20;  // cooperative transfer slots per thread (XW*n <= NLD*256 for n <= 640)
 
-    double v[L];
-    const int npad = n | 1;  // odd row pitch: conflict-free transposed reads
-    const int ntile = min(XW, na - la0) * n;  // x: nl consecutive lines, contiguous (sy == n0)
-    const double inv_n = 1.0 / n;
-    if (a.dir == 0) {
-        // every thread issues its L loads before any store (loads in flight together)
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int la0 = (t % nab) * XW, lb = t / nab, nl = min(XW, na - la0);
+        const long base = (long)lb * sb + (long)la0 * sa;
+        const int ntot = nl * n;
+        __syncthreads();  // previous tile fully stored / tables staged
+        PHASE(0);
+        // ---- cooperative coalesced load: all requests in flight, then to shared memory
+        if (a.dir == 0) {
+            // nl consecutive x-lines are one contiguous block of nl*n doubles (sy == n0)
+            for (int e0 = 0; e0 < ntot; e0 += NLD * SWEEP_THREADS) {
+                double r[NLD];
 #pragma unroll
-        for (int j = 0; j < L; ++j) {
-            const int e = tid + j * nthr;
-            v[j] = e < ntile ? __ldg(a.in + base + e) : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < L; ++j) {
-            const int e = tid + j * nthr;
-            if (e < ntile) {
-                const int q = __double2int_rz((e + 0.5) * inv_n);
-                tile[q * npad + (e - q * n)] = v[j];
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < L; ++j) v[j] = (j < len && valid) ? tile[xl * npad + s + j] : 0.0;
-    } else {
-        const double *src = a.in + base + xl + (long)s * sl;
-#pragma unroll
-        for (int j = 0; j < L; ++j) v[j] = (j < len && valid) ? __ldg(src + (long)j * sl) : 0.0;
-    }
-
-    const double *Lt = a.t.l, *Ut = a.t.us, *Dt = a.t.dinv;
-    double h[P], inc[P];
-
-    // pass 1: forward from zero state -> tail; scan; pass 2: forward from the exact state
-#pragma unroll
-    for (int m = 0; m < P; ++m) h[m] = 0.0;
-    if (uni) fwd_uni<P, L, false>(v, h, lc);
-    else fwd_pass<P, L, false, false>(v, h, s, len, Lt, lc);
-    if (C > 1) chunk_scan<P, true>(h, inc, sbuf, a.t.phif, C, a.t.levels, c, xl);
-    else {
-#pragma unroll
-        for (int m = 0; m < P; ++m) inc[m] = 0.0;
-    }
-#pragma unroll
-    for (int m = 0; m < P; ++m) h[m] = inc[m];
-    if (uni) fwd_uni<P, L, true>(v, h, lc);
-    else fwd_pass<P, L, false, true>(v, h, s, len, Lt, lc);
-
-    // pass 3: backward from zero state -> head; scan; pass 4: backward from the exact state
-#pragma unroll
-    for (int m = 0; m < P; ++m) h[m] = 0.0;
-    if (uni) bwd_uni<P, L, false>(v, h, uc, dc);
-    else bwd_pass<P, L, false, false>(v, h, s, len, Ut, Dt, uc, dc);
-    if (C > 1) chunk_scan<P, false>(h, inc, sbuf, a.t.phib, C, a.t.levels, c, xl);
-    else {
-#pragma unroll
-        for (int m = 0; m < P; ++m) inc[m] = 0.0;
-    }
-#pragma unroll
-    for (int m = 0; m < P; ++m) h[m] = inc[m];
-    if (uni) bwd_uni<P, L, true>(v, h, uc, dc);
-    else bwd_pass<P, L, false, true>(v, h, s, len, Ut, Dt, uc, dc);
-
-    // store
-    if (a.dir == 0) {
-#pragma unroll
-        for (int j = 0; j < L; ++j)
-            if (j < len) tile[xl * npad + s + j] = v[j];
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < L; ++j) {
-            const int e = tid + j * nthr;
-            if (e < ntile) {
-                const int q = __double2int_rz((e + 0.5) * inv_n);
-                a.out[base + e] = tile[q * npad + (e - q * n)];
-            }
-        }
-    } else if (valid) {
-        const long off = base + xl + (long)s * sl;
-        if (a.mode == 0) {
-#pragma unroll
-            for (int j = 0; j < L; ++j)
-                if (j < len) a.out[off + (long)j * sl] = v[j];
-        } else {
-#pragma unroll
-            for (int j = 0; j < L; ++j)
-                if (j < len) {
-                    const long idx = off + (long)j * sl;
-                    a.V[idx] = fma(a.kick, v[j], a.V[idx]);
-                    if (a.out) a.out[idx] = v[j];
+                for (int k = 0; k < NLD; ++k) {
+                    const int e = e0 + tid + k * SWEEP_THREADS;
+                    r[k] = e < ntot ? __ldg(a.in + base + e) : 0.0;
                 }
+#pragma unroll
+                for (int k = 0; k < NLD; ++k) {
+                    const int e = e0 + tid + k * SWEEP_THREADS;
+                    if (e < ntot) tile[e] = r[k];
+                }
+            }
+        } else {
+            const int tot = n * XW;
+            for (int e0 = 0; e0 < tot; e0 += NLD * SWEEP_THREADS) {
+                double r[NLD];
+#pragma unroll
+                for (int k = 0; k < NLD; ++k) {
+                    const int e = e0 + tid + k * SWEEP_THREADS, i = e >> 3, q = e & (XW - 1);
+                    r[k] = (e < tot && q < nl) ? __ldg(a.in + base + (long)i * sl + q) : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < NLD; ++k) {
+                    const int e = e0 + tid + k * SWEEP_THREADS;
+                    if (e < tot) tile[(e >> 3) * YP + (e & (XW - 1))] = r[k];
+                }
+            }
         }
+        __syncthreads();
+        PHASE(1);
+        // ---- warp w solves line w (lane = chunk)
+        if (w < nl) {
+            double v[L];
+#pragma unroll
+            for (int j = 0; j < L; ++j) {
+                const int i = s + j;
+                v[j] = i < n ? (a.dir == 0 ? tile[w * n + i] : tile[i * YP + w]) : 0.0;
+            }
+            solve_chunk<P, L>(v, active, fr, br, rsf, rsb, sphif, sphib, C, levels, lane);
+#pragma unroll
+            for (int j = 0; j < L; ++j) {
+                const int i = s + j;
+                if (i < n) {
+                    if (a.dir == 0) tile[w * n + i] = v[j];
+                    else tile[i * YP + w] = v[j];
+                }
+            }
+        }
+        __syncthreads();
+        PHASE(2);
+        // ---- cooperative coalesced store (z: fused kick V += kick * a)
+        if (a.dir == 0) {
+            for (int e = tid; e < ntot; e += SWEEP_THREADS) a.out[base + e] = tile[e];
+        } else {
+            const int tot = n * XW;
+            for (int e = tid; e < tot; e += SWEEP_THREADS) {
+                const int i = e >> 3, q = e & (XW - 1);
+                if (q < nl) {
+                    const long idx = base + (long)i * sl + q;
+                    const double x = tile[i * YP + q];
+                    if (a.mode == 0) {
+                        a.out[idx] = x;
+                    } else {
+                        a.V[idx] = fma(a.kick, x, a.V[idx]);
+                        if (a.out) a.out[idx] = x;
+                    }
+                }
+            }
+        }
+        PHASE(3);
     }
 }
 
@@ -526,18 +578,23 @@ int launch_kop(int p, const KopArgs &a, cudaStream_t s) {
 template <int P, int L>
 static void sweep_launch(const SweepArgs &a, cudaStream_t s) {
     const Geom &g = a.geo;
-    int na = a.dir == 0 ? g.n1 : g.n0;
-    int nb = a.dir == 2 ? g.n1 : g.n2;
-    dim3 blk(XW, a.t.C);
-    dim3 grd((na + XW - 1) / XW, nb);
-    size_t sm = sizeof(double) * (3 * (size_t)a.t.C * XW * P);
-    if (a.dir == 0) sm += sizeof(double) * (size_t)XW * (a.t.n | 1);
-    static bool attr_set = false;
-    if (!attr_set) {
+    const int na = a.dir == 0 ? g.n1 : g.n0, nb = a.dir == 2 ? g.n1 : g.n2;
+    const int ntiles = ((na + XW - 1) / XW) * nb;
+    const int nedge = a.t.C * L - (a.t.i_hi - a.t.i_lo);
+    const size_t nphi = (size_t)std::max(a.t.levels, 1) * a.t.C * P * P;
+    size_t tile = a.dir == 0 ? (size_t)XW * a.t.n : (size_t)a.t.n * YP;
+    size_t sm = sizeof(double) * (2 * nphi + (size_t)(nedge + 1) * (CoefLayout<P>::FW + CoefLayout<P>::BW) + tile);
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(sweep_kernel<P, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
     }
-    sweep_kernel<P, L><<<grd, blk, sm, s>>>(a);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<P, L>, SWEEP_THREADS, sm);
+    dim3 grd(std::min(ntiles, std::max(per_sm, 1) * nsm));
+    sweep_kernel<P, L><<<grd, SWEEP_THREADS, sm, s>>>(a);
 }
 
 template <int P>
@@ -545,8 +602,7 @@ static int sweep_dispatch(const SweepArgs &a, cudaStream_t s) {
     switch (a.t.L) {
 #define ADS_L(LV) \
     case LV: sweep_launch<P, LV>(a, s); return 0;
-        ADS_L(1) ADS_L(2) ADS_L(3) ADS_L(4) ADS_L(5) ADS_L(8) ADS_L(9) ADS_L(12) ADS_L(13) ADS_L(16) ADS_L(17)
-        ADS_L(24) ADS_L(25) ADS_L(32) ADS_L(33)
+        ADS_L(1) ADS_L(3) ADS_L(5) ADS_L(9) ADS_L(13) ADS_L(17) ADS_L(21) ADS_L(25) ADS_L(33)
 #undef ADS_L
     }
     return -1;
