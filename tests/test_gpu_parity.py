@@ -201,10 +201,16 @@ def test_c4_full_size_one_step_and_run(ads):
     """Full config 4 (515^3): one step vs the C oracle element by element, full 100-step run vs
     the modal oracle."""
     wl = workloads.get("c4")
-    g = ads.make_solver(wl)
+    # both sides start from the SAME coefficients (the oracle's L2 projection): at 515^3 the
+    # operator K amplifies the last-ulp differences of two independent projections by
+    # |K||u|/|Ku| ~ (sigma/h)^2 ~ 1e3, which alone exceeds 1e-12 in a0 (DESIGN.md §7)
+    u0 = oracle.project_separable(wl)
+    g = ads.Solver(wl.nel, wl.p, wl.tau, wl.bc)
+    g.set_state(u0)
     g.step(1)
     gu, gud, ga = g.get_state()
-    o = oracle.make_solver(wl)
+    o = oracle.PWave(wl.nel, wl.p, wl.tau, wl.bc)
+    o.set_state(u0)
     o.step(1)
     ou, oud, oa = o.get_state()
     del o
@@ -212,6 +218,5 @@ def test_c4_full_size_one_step_and_run(ads):
     del ou, oud, oa
     g.step(wl.steps - 1)
     gu, gud, ga = g.get_state()
-    u0 = oracle.project_separable(wl)
     mu, mud, ma = ModalPWave(wl.nel, wl.p, wl.tau).run(u0, nsteps=wl.steps)
     assert rel(gu, mu) < RUN_TOL and rel(gud, mud) < RUN_TOL and rel(ga, ma) < RUN_TOL
