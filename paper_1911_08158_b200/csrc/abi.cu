@@ -22,8 +22,7 @@ namespace {
 
 struct DirDev {
     double *mband = nullptr, *kband = nullptr, *aband = nullptr;  // [n][2p+1]
-    double *l = nullptr, *us = nullptr, *dinv = nullptr, *phif = nullptr, *phib = nullptr;
-    int *cs = nullptr;
+    double *l = nullptr, *us = nullptr, *dinv = nullptr, *Tf = nullptr, *Rb = nullptr;
     SolveTab tab;
 };
 
@@ -164,48 +163,51 @@ int build_direction(ads_ctx *h, int d) {
     LUFactors f;
     if (banded_lu(A, f, /*freeze=*/true)) return fail(h, ADS_E_SINGULAR, "A_%d singular", d);
     if (banded_lu(Mm, h->mass_lu[d])) return fail(h, ADS_E_SINGULAR, "M_%d singular", d);
-    std::vector<int> cs;
-    const int L = choose_chunks(n, p, 32, cs);
+    const int C = kSweepChunks;
+    const int L = choose_chunk_len(n, p, C);
     if (L == 0) return fail(h, ADS_E_INVAL, "n_%d = %d: no supported chunking", d, n);
     // pad the factors to C*L rows with identity rows: every chunk has length L
-    const int C = (int)cs.size() - 1, npad = C * L;
+    const int npad = C * L;
     LUFactors fp = f;
     fp.n = npad;
     fp.l.resize((size_t)npad * p, 0.0);
     fp.us.resize((size_t)npad * p, 0.0);
     fp.dinv.resize(npad, 1.0);
-    std::vector<int> csp(cs);
-    csp[C] = npad;
     PartTables pt;
-    build_part_tables(fp, csp, pt);
+    build_part_tables(fp, C, L, pt);
     DirDev &D = h->dd[d];
     int rc;
     std::vector<double> mb(s.M.v), kb(s.K.v), ab(A.v);
     (void)W;
     if ((rc = upload(h, &D.mband, mb)) || (rc = upload(h, &D.kband, kb)) || (rc = upload(h, &D.aband, ab)) ||
         (rc = upload(h, &D.l, fp.l)) || (rc = upload(h, &D.us, fp.us)) || (rc = upload(h, &D.dinv, fp.dinv)) ||
-        (rc = upload(h, &D.phif, pt.phif)) || (rc = upload(h, &D.phib, pt.phib)) || (rc = upload(h, &D.cs, pt.cs)))
+        (rc = upload(h, &D.Tf, pt.Tf)) || (rc = upload(h, &D.Rb, pt.Rb)))
         return rc;
     D.tab.l = D.l;
     D.tab.us = D.us;
     D.tab.dinv = D.dinv;
-    D.tab.phif = D.phif;
-    D.tab.phib = D.phib;
-    D.tab.cs = D.cs;
+    D.tab.Tf = D.Tf;
+    D.tab.Rb = D.Rb;
     D.tab.n = n;
-    D.tab.C = pt.C;
-    D.tab.levels = pt.levels;
     D.tab.L = L;
+    D.tab.Kf = pt.Kf;
+    D.tab.Kb = pt.Kb;
     // uniform region aligned to whole chunks: chunks [c_lo, c_hi) lie inside [i_lo, i_hi)
     const int c_lo = (f.i_lo + L - 1) / L, c_hi = f.i_hi / L;
-    D.tab.i_lo = c_hi > c_lo ? c_lo * L : 0;
-    D.tab.i_hi = c_hi > c_lo ? c_hi * L : 0;
-    if (D.tab.i_hi > D.tab.i_lo) {
+    D.tab.c_lo = c_hi > c_lo ? c_lo : 0;
+    D.tab.c_hi = c_hi > c_lo ? c_hi : 0;
+    if (D.tab.c_hi > D.tab.c_lo) {
         for (int k = 0; k < p; ++k) {
             D.tab.lc[k] = f.l[(size_t)f.i_lo * p + k];
             D.tab.usc[k] = f.us[(size_t)f.i_lo * p + k];
         }
         D.tab.dic = f.dinv[f.i_lo];
+        const int s0 = D.tab.c_lo * L;  // any uniform chunk: its responses are bitwise identical
+        for (int j = 0; j < L; ++j)
+            for (int m = 0; m < p; ++m) {
+                D.tab.Gf[j][m] = pt.gf[(size_t)(s0 + j) * p + m];
+                D.tab.Gb[j][m] = pt.gb[(size_t)(s0 + j) * p + m];
+            }
     }
     return ADS_OK;
 }

@@ -272,36 +272,61 @@ void lu_solve_host(const LUFactors &f, double *x) {
     }
 }
 
-int choose_chunks(int n, int p, int cmax, std::vector<int> &cs) {
-    const int need = std::max((n + cmax - 1) / cmax, std::max(p, 1));
-    for (int L : kChunkLens) {
-        if (L < need) continue;
-        const int C = (n + L - 1) / L;
-        // the last chunk must hold >= p rows (its boundary state is p values)
-        if (C > 1 && n - (C - 1) * L < std::max(p, 1)) continue;
-        cs.resize(C + 1);
-        for (int c = 0; c < C; ++c) cs[c] = c * L;
-        cs[C] = n;
-        return L;
-    }
+int choose_chunk_len(int n, int p, int C) {
+    for (int L : kChunkLens)
+        if ((long)L * C >= n && L >= p) return L;
     return 0;
 }
 
-void build_part_tables(const LUFactors &f, const std::vector<int> &cs, PartTables &t) {
-    const int n = f.n, p = f.p, C = (int)cs.size() - 1;
+static double inf_norm(const std::vector<double> &A, int p) {
+    double m = 0.0;
+    for (int a = 0; a < p; ++a) {
+        double r = 0.0;
+        for (int b = 0; b < p; ++b) r += std::fabs(A[a * p + b]);
+        m = std::max(m, r);
+    }
+    return m;
+}
+
+// smallest k such that every product of k consecutive maps (in chain order) has
+// inf-norm < 2^-64; C-1 if none.  fwd: Tf_{c-1}...Tf_{c-k}; bwd: Rb_{c+1}...Rb_{c+k}.
+static int truncation_depth(const std::vector<double> &T, int C, int p, bool fwd) {
+    const double thr = std::ldexp(1.0, -64);
+    std::vector<double> acc(p * p), tmp(p * p);
+    for (int k = 1; k < C; ++k) {
+        bool ok = true;
+        for (int c0 = 0; c0 + k <= C && ok; ++c0) {
+            // chunks c0 .. c0+k-1, newest applied last (fwd) / first (bwd)
+            for (int a = 0; a < p * p; ++a) acc[a] = (a % (p + 1) == 0) ? 1.0 : 0.0;
+            for (int q = 0; q < k; ++q) {
+                const int cc = fwd ? c0 + q : c0 + k - 1 - q;
+                const double *M = &T[(size_t)cc * p * p];
+                for (int a = 0; a < p; ++a)
+                    for (int b = 0; b < p; ++b) {
+                        double v = 0.0;
+                        for (int m = 0; m < p; ++m) v += M[a * p + m] * acc[m * p + b];
+                        tmp[a * p + b] = v;
+                    }
+                acc.swap(tmp);
+            }
+            ok = inf_norm(acc, p) < thr;
+        }
+        if (ok) return k;
+    }
+    return std::max(C - 1, 0);
+}
+
+void build_part_tables(const LUFactors &f, int C, int L, PartTables &t) {
+    const int n = f.n, p = f.p;
     t.n = n;
     t.p = p;
     t.C = C;
-    t.cs = cs;
-    t.lmax = 0;
-    for (int c = 0; c < C; ++c) t.lmax = std::max(t.lmax, cs[c + 1] - cs[c]);
-    t.levels = 0;
-    while ((1 << t.levels) < C) ++t.levels;
+    t.L = L;
     t.gf.assign((size_t)n * p, 0.0);
     t.gb.assign((size_t)n * p, 0.0);
     std::vector<double> y(n + 2 * p);
     for (int c = 0; c < C; ++c) {
-        int s = cs[c], e = cs[c + 1];
+        int s = c * L, e = std::min(n, s + L);
         for (int m = 0; m < p; ++m) {
             // forward homogeneous recurrence with incoming y_{s-1-m} = 1
             std::fill(y.begin(), y.end(), 0.0);
@@ -321,54 +346,25 @@ void build_part_tables(const LUFactors &f, const std::vector<int> &cs, PartTable
             for (int i = e - 1; i >= s; --i) {
                 double v = 0.0;
                 for (int k = 1; k <= p; ++k)
-                    if (i + k < n) v -= f.us[(size_t)i * p + k - 1] * Y[i + k];
+                    if (i + k < n + p) v -= (i + k < n ? f.us[(size_t)i * p + k - 1] : 0.0) * Y[i + k];
                 Y[i] = v;
                 t.gb[(size_t)i * p + m] = v;
             }
         }
     }
-    // scan matrices
-    int L = std::max(t.levels, 1);
-    t.phif.assign((size_t)L * C * p * p, 0.0);
-    t.phib.assign((size_t)L * C * p * p, 0.0);
-    auto Tf = [&](int c, int a, int b) { return t.gf[(size_t)(cs[c + 1] - 1 - a) * p + b]; };
-    auto Rb = [&](int c, int a, int b) { return t.gb[(size_t)(cs[c] + a) * p + b]; };
-    std::vector<double> acc(p * p), tmp(p * p);
-    for (int lv = 0; lv < t.levels; ++lv) {
-        int d = 1 << lv;
-        for (int c = 0; c < C; ++c) {
-            // forward: T_c T_{c-1} ... T_{c-d+1}
-            if (c - d + 1 >= 0) {
-                for (int a = 0; a < p; ++a)
-                    for (int b = 0; b < p; ++b) acc[a * p + b] = Tf(c, a, b);
-                for (int q = c - 1; q >= c - d + 1; --q) {
-                    for (int a = 0; a < p; ++a)
-                        for (int b = 0; b < p; ++b) {
-                            double v = 0.0;
-                            for (int k = 0; k < p; ++k) v += acc[a * p + k] * Tf(q, k, b);
-                            tmp[a * p + b] = v;
-                        }
-                    acc = tmp;
-                }
-                std::copy(acc.begin(), acc.end(), t.phif.begin() + ((size_t)lv * C + c) * p * p);
+    t.Tf.assign((size_t)C * p * p, 0.0);
+    t.Rb.assign((size_t)C * p * p, 0.0);
+    for (int c = 0; c < C; ++c) {
+        int s = c * L, e = std::min(n, s + L);
+        if (e - s < p) continue;  // only the padded tail can be short; its maps stay 0
+        for (int a = 0; a < p; ++a)
+            for (int b = 0; b < p; ++b) {
+                t.Tf[((size_t)c * p + a) * p + b] = t.gf[(size_t)(e - 1 - a) * p + b];
+                t.Rb[((size_t)c * p + a) * p + b] = t.gb[(size_t)(s + a) * p + b];
             }
-            // backward: R_c R_{c+1} ... R_{c+d-1}
-            if (c + d - 1 < C) {
-                for (int a = 0; a < p; ++a)
-                    for (int b = 0; b < p; ++b) acc[a * p + b] = Rb(c, a, b);
-                for (int q = c + 1; q <= c + d - 1; ++q) {
-                    for (int a = 0; a < p; ++a)
-                        for (int b = 0; b < p; ++b) {
-                            double v = 0.0;
-                            for (int k = 0; k < p; ++k) v += acc[a * p + k] * Rb(q, k, b);
-                            tmp[a * p + b] = v;
-                        }
-                    acc = tmp;
-                }
-                std::copy(acc.begin(), acc.end(), t.phib.begin() + ((size_t)lv * C + c) * p * p);
-            }
-        }
     }
+    t.Kf = truncation_depth(t.Tf, C, p, true);
+    t.Kb = truncation_depth(t.Rb, C, p, false);
 }
 
 }  // namespace ads

@@ -61,27 +61,30 @@ struct LUFactors {
 int banded_lu(const Band &A, LUFactors &f, bool freeze = false);
 void lu_solve_host(const LUFactors &f, double *x);  // in place, one vector
 
-// Partitioned elimination tables for one direction (chunks of a line solved
-// independently, then coupled by an exact scan over chunk boundary states).
-//   cs[c]           chunk c = [cs[c], cs[c+1])
-//   gf[i*p + m]     response of the forward (L) recurrence at i to incoming
-//                   state y_{s-1-m} = 1 (s = start of i's chunk)
-//   gb[i*p + m]     response of the backward (U) recurrence at i to incoming
-//                   state x_{e+m} = 1 (e = end of i's chunk)
-//   phif[(lv*C + c)*p*p + a*p + b]  product T_c T_{c-1} ... T_{c-2^lv+1}
-//   phib[(lv*C + c)*p*p + a*p + b]  product R_c R_{c+1} ... R_{c+2^lv-1}
-// with T_c[a][b] = gf[(e_c-1-a)*p + b] and R_c[a][b] = gb[(s_c+a)*p + b].
+// Partitioned elimination tables for one direction: every line (padded with
+// identity rows to C*L rows) is cut into C chunks of L rows solved
+// independently, then coupled through the chunk boundary states.
+//   gf[i*p + m]   response of the forward (L) recurrence at i to incoming
+//                 state y_{s-1-m} = 1 (s = start of i's chunk)
+//   gb[i*p + m]   response of the backward (U) recurrence at i to incoming
+//                 state x_{e+m} = 1 (e = end of i's chunk)
+//   Tf[c*p*p + a*p + b] = gf[(e_c-1-a)*p + b]   forward chunk transfer map
+//   Rb[c*p*p + a*p + b] = gb[(s_c+a)*p + b]     backward chunk transfer map
+// The incoming state of chunk c is in_c = Tf_{c-1} in_{c-1} + h_{c-1}
+// (h = outgoing state of the zero-incoming pass).  Kf is the number of
+// preceding chunks the device folds in: the smallest k with
+// ||Tf_{c-1} ... Tf_{c-k}||_inf < 2^-64 for every c (contributions of older
+// chunks are below 2^-64 of the state, i.e. no bit of an fp64 result), or C-1
+// (the complete chain) if no such k exists.  Kb likewise for Rb.
 struct PartTables {
-    int n = 0, p = 0, C = 0, levels = 0, lmax = 0;
-    std::vector<int> cs;
-    std::vector<double> gf, gb, phif, phib;
+    int n = 0, p = 0, C = 0, L = 0, Kf = 0, Kb = 0;
+    std::vector<double> gf, gb, Tf, Rb;
 };
-// Choose chunks of uniform length L (the last one may be shorter, >= p):
-// L is the smallest value of kChunkLens >= max(ceil(n / cmax), p); returns L
-// (0 if n needs a chunk longer than the largest instantiated length).
-// odd lengths only: lane-per-chunk shared-memory reads (stride L) are bank-conflict-free
-constexpr int kChunkLens[] = {1, 3, 5, 9, 13, 17, 21, 25, 33};
-int choose_chunks(int n, int p, int cmax, std::vector<int> &cs);
-void build_part_tables(const LUFactors &f, const std::vector<int> &cs, PartTables &t);
+// Chunk length: the smallest value of kChunkLens with C*L >= n and L >= p
+// (0 if none).  Odd lengths keep the x-tile shared-memory reads conflict-free.
+constexpr int kChunkLens[] = {1, 3, 5, 9, 17, 33};
+int choose_chunk_len(int n, int p, int C);
+// f: factors padded to C*L rows (identity rows beyond n)
+void build_part_tables(const LUFactors &f, int C, int L, PartTables &t);
 
 }  // namespace ads

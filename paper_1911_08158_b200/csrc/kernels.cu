@@ -168,297 +168,351 @@ __global__ void __launch_bounds__(256, 2) kop_kernel(const KopArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
-// partitioned banded sweeps
+// partitioned banded sweeps (v3)
 //
-// A CTA owns a tile of XW = 8 adjacent lines; warp w solves line w, lane c owns
-// chunk c (rows [cL, cL+L), L odd, C <= 32 chunks; lines are padded to C*L rows
-// with identity rows).  Per lane, four p-term recurrences over its chunk held in
-// registers:
-//   1. forward  y_i = r_i - sum_k l_{i,k} y_{i-k}                 zero incoming state -> tail
-//   2. forward                                                    exact incoming state
-//   3. backward x_i = y_i/u_ii - sum_k (u_{i,i+k}/u_ii) x_{i+k}    zero incoming state -> head
-//   4. backward                                                   exact incoming state
-// The exact incoming states come from a Kogge-Stone scan of the affine chunk
-// maps across the lanes (shuffles; Phi = products of chunk transfer matrices,
-// host-precomputed).  No block barrier inside the solve.
-// The tile moves HBM <-> shared memory with coalesced cooperative loads/stores;
-// y/z tiles are stored [row][XW+1] (odd pitch) and x tiles [line][n], so the
-// lane-per-chunk reads (stride L, odd) are bank-conflict-free.
-// Rows [i_lo, i_hi) of the factors are one constant row held in registers;
-// the other ("edge") rows are read from a shared-memory table.
+// Solves A_d x = r along every line of direction d: for each
+// line, forward y_i = r_i - sum_k l_{i,k} y_{i-k}, then backward
+// x_i = y_i dinv_i - sum_k us_{i,k} x_{i+k}, with the LU factors of the
+// constant A_d computed once on the host.
+//
+// CTA = 8 warps on a tile of SW_LW = 8 adjacent lines.  Thread (lane, warp):
+//   q = lane & 7          line of the tile
+//   c = 4 warp + lane/8   chunk: rows [c L, c L + L) of the (identity-padded) line
+// so the 32 chunks of a line are spread over the CTA and each thread keeps its
+// L values in registers.  Per tile:
+//   1. forward recurrence from a zero incoming state -> y0 (kept), tail h_c
+//   2. h_c -> shared memory; barrier; incoming state of chunk c:
+//      in_c = sum_{c'<c} Tf_{c-1} ... Tf_{c'+1} h_{c'}, folded over the last Kf
+//      chunks (the host certifies older chunks contribute < 2^-64 of the state,
+//      host_setup.h); then y = y0 + (response to in_c)
+//   3. the same backward (head states, Rb maps, Kb chunks)
+// = exact partitioned (SPIKE-style) elimination of the banded system.
+// Uniform chunks (inside the frozen Toeplitz interior, all bitwise identical)
+// take every coefficient -- LU rows, the chunk responses G and the transfer
+// maps -- from the kernel's constant bank; the response to in_c is then a
+// dependency-free G-multiply instead of a recurrence.  Edge chunks read their
+// rows from a shared-memory table.
+// y/z lines: each row access is 8 consecutive doubles of adjacent lines; the
+// next tile streams HBM -> shared memory (cp.async) while the current one is
+// solved.  x lines (contiguous): coalesced cooperative copies through shared
+// memory; tile pitch np = 2 (mod 16) keeps the per-thread chunk reads
+// conflict-free.  The z sweep fuses the kick V += tau a into its store.
 // ------------------------------------------------------------------------------------------
-constexpr int XW = 8;        // lines per CTA
-constexpr int YP = XW + 1;   // y/z tile row pitch (doubles)
-constexpr int SWEEP_THREADS = 32 * XW;
+constexpr int SW_LW = 8, SW_WARPS = 8, SW_THREADS = 32 * SW_WARPS, SW_G = 32 / SW_LW;
+static_assert(SW_WARPS * SW_G == kSweepChunks, "one chunk per (warp, lane group)");
 
-template <int P, bool FWD>
-__device__ __forceinline__ void warp_scan(double (&o)[P], double (&inc)[P], const double *phi, int C, int levels,
-                                          int lane) {
-    for (int lv = 0; lv < levels; ++lv) {
-        const int d = 1 << lv;
-        double u[P];
+__host__ __device__ constexpr int ring(int i, int P) { return ((i % P) + P) % P; }
+template <int P> struct Rec {
+    static constexpr int FW = (P + 1) & ~1;  // forward record: l_1..l_P (even length)
+    static constexpr int BW = (P + 2) & ~1;  // backward record: dinv, us_1..us_P
+};
+
+// Coefficient sources.  UNI: constant bank.  EDGE: shared-memory records, row j of
+// the chunk at rec + j * FW (bwd: + j * BW) -- compile-time offsets.
+template <int P, bool UNI>
+struct Coef {
+    const double *f, *b;  // EDGE: records of the chunk's first row
+    const SolveTab &t;
+    __device__ __forceinline__ double l(int j, int k) const { return UNI ? t.lc[k - 1] : f[j * Rec<P>::FW + k - 1]; }
+    __device__ __forceinline__ double d(int j) const { return UNI ? t.dic : b[j * Rec<P>::BW]; }
+    __device__ __forceinline__ double u(int j, int k) const { return UNI ? t.usc[k - 1] : b[j * Rec<P>::BW + k]; }
+};
+
+// forward recurrence; ZERO: incoming 0, v <- y0, h <- tail (y_{L-1-m});
+// !ZERO: homogeneous response to incoming y_{-1-m} = h[m], added to v
+template <int P, int L, bool UNI, bool ZERO>
+__device__ __forceinline__ void fwd_pass(double (&v)[L], double (&h)[P], const Coef<P, UNI> &cf) {
+    double R[P];
 #pragma unroll
-        for (int m = 0; m < P; ++m)
-            u[m] = FWD ? __shfl_up_sync(0xffffffffu, o[m], d) : __shfl_down_sync(0xffffffffu, o[m], d);
-        const bool has = FWD ? (lane >= d && lane < C) : (lane + d < C);
-        if (has) {
-            const double *ph = phi + (lv * C + lane) * P * P;
-            double t[P];
+    for (int m = 0; m < P; ++m) R[ring(-1 - m, P)] = ZERO ? 0.0 : h[m];
 #pragma unroll
-            for (int i = 0; i < P; ++i) {
-                double s = o[i];
+    for (int j = 0; j < L; ++j) {
+        double acc = ZERO ? v[j] : 0.0;
 #pragma unroll
-                for (int j = 0; j < P; ++j) s = fma(ph[i * P + j], u[j], s);
-                t[i] = s;
-            }
-#pragma unroll
-            for (int i = 0; i < P; ++i) o[i] = t[i];
-        }
+        for (int k = P; k >= 1; --k)
+            if (!ZERO || j - k >= 0) acc = fma(-cf.l(j, k), R[ring(j - k, P)], acc);
+        R[ring(j, P)] = acc;
+        if (ZERO) v[j] = acc;
+        else v[j] += acc;
     }
+    if (ZERO) {
 #pragma unroll
-    for (int m = 0; m < P; ++m) {
-        const double w = FWD ? __shfl_up_sync(0xffffffffu, o[m], 1) : __shfl_down_sync(0xffffffffu, o[m], 1);
-        inc[m] = (FWD ? lane >= 1 : lane + 1 < C) ? w : 0.0;
+        for (int m = 0; m < P; ++m) h[m] = R[ring(L - 1 - m, P)];
     }
 }
 
-// Coefficient rows in shared memory, 16-byte aligned records of CW doubles:
-//   forward  record: l_1 .. l_P            (padded to an even count)
-//   backward record: dinv, us_1 .. us_P    (padded to an even count)
-template <int P> struct CoefLayout {
-    static constexpr int FW = (P + 1) & ~1;        // forward record doubles
-    static constexpr int BW = (P + 2) & ~1;        // backward record doubles
-};
-
-// One recurrence pass over a chunk (all lanes run the same instructions).
-// FWD: y_j = v_j - sum_k l_k y_{j-k};   BWD: x_j = v_j d_j - sum_k us_k x_{j+k}.
-// h: incoming state on entry (h[0] = y_{s-1} / x_{e}), outgoing state on exit
-// (tail y_{e-1-m} / head x_{s+m}).  Register ring R[pos mod P] (no moves).
-// Row j of the chunk's coefficients is at rec + j*rstride (rstride = 0 for
-// chunks inside the uniform interior: every read is the same broadcast row).
-template <int P, int L, bool FWD, bool STORE>
-__device__ __forceinline__ void rec_pass(double (&v)[L], double (&h)[P], const double *rec, int rstride) {
-    constexpr int NC = FWD ? CoefLayout<P>::FW : CoefLayout<P>::BW;
+// backward recurrence; ZERO: incoming 0, v <- x0, h <- head (x_m);
+// !ZERO: homogeneous response to incoming x_{L+m} = h[m], added to v
+template <int P, int L, bool UNI, bool ZERO>
+__device__ __forceinline__ void bwd_pass(double (&v)[L], double (&h)[P], const Coef<P, UNI> &cf) {
     double R[P];
-    if (FWD) {
 #pragma unroll
-        for (int m = 0; m < P; ++m) R[((-1 - m) % P + P) % P] = h[m];
-    } else {
-#pragma unroll
-        for (int m = 0; m < P; ++m) R[(L + m) % P] = h[m];
-    }
+    for (int m = 0; m < P; ++m) R[ring(L + m, P)] = ZERO ? 0.0 : h[m];
 #pragma unroll
     for (int q = 0; q < L; ++q) {
-        const int j = FWD ? q : L - 1 - q;
-        const double2 *rp = reinterpret_cast<const double2 *>(rec + j * rstride);
-        double cf[NC];
+        const int j = L - 1 - q;
+        double acc = ZERO ? v[j] * cf.d(j) : 0.0;
 #pragma unroll
-        for (int k = 0; k < NC / 2; ++k) {
-            const double2 d2 = rp[k];
-            cf[2 * k] = d2.x;
-            cf[2 * k + 1] = d2.y;
-        }
-        double t;
-        if (FWD) {
-            t = v[j];
-#pragma unroll
-            for (int k = P; k >= 1; --k) t = fma(-cf[k - 1], R[((j - k) % P + P) % P], t);
-        } else {
-            t = v[j] * cf[0];
-#pragma unroll
-            for (int k = P; k >= 1; --k) t = fma(-cf[k], R[(j + k) % P], t);
-        }
-        R[j % P] = t;
-        if (STORE) v[j] = t;
+        for (int k = P; k >= 1; --k)
+            if (!ZERO || j + k < L) acc = fma(-cf.u(j, k), R[ring(j + k, P)], acc);
+        R[ring(j, P)] = acc;
+        if (ZERO) v[j] = acc;
+        else v[j] += acc;
     }
-    if (FWD) {
-#pragma unroll
-        for (int m = 0; m < P; ++m) h[m] = R[((L - 1 - m) % P + P) % P];
-    } else {
+    if (ZERO) {
 #pragma unroll
         for (int m = 0; m < P; ++m) h[m] = R[m];
     }
 }
 
-// Lanes >= C (no chunk) skip the passes; the warp scans are reached by all lanes.
-#ifdef ADS_PHASE_TIMING
-__device__ long long g_sub[4][8];
-#define SUB(k)                                                                                  \
-    do {                                                                                        \
-        if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 64 + 10))                    \
-            g_sub[threadIdx.x == 0 ? 0 : 1][k] = clock64();                                     \
-    } while (0)
-#else
-#define SUB(k) \
-    do {       \
-    } while (0)
-#endif
-template <int P, int L>
-__device__ __forceinline__ void solve_chunk(double (&v)[L], bool active, const double *fr, const double *br,
-                                            int rstride_f, int rstride_b, const double *phif, const double *phib,
-                                            int C, int levels, int lane) {
-    double h[P], inc[P];
+// incoming state of chunk c: Horner over chunks c-K .. c-1 (FWD) or c+K .. c+1
+// (backward).  UNIW: every chunk of the window is uniform -> maps from the
+// constant bank (Tf(a,b) = Gf[L-1-a][b], Rb(a,b) = Gb[a][b]).
+template <int P, int L, bool FWD, bool UNIW>
+__device__ __forceinline__ void chunk_walk(double (&in)[P], const SolveTab &t, const double *shT, const double *shh,
+                                           int c, int K, int q) {
 #pragma unroll
-    for (int m = 0; m < P; ++m) h[m] = 0.0;
-    SUB(0);
-    if (active) rec_pass<P, L, true, false>(v, h, fr, rstride_f);
-    __syncwarp();
-    SUB(1);
-    warp_scan<P, true>(h, inc, phif, C, levels, lane);
-    SUB(2);
-    if (active) rec_pass<P, L, true, true>(v, inc, fr, rstride_f);
-    SUB(3);
+    for (int m = 0; m < P; ++m) in[m] = 0.0;
+    const int c0 = FWD ? max(c - K, 0) : min(c + K, kSweepChunks - 1);
+    for (int cc = c0; FWD ? cc < c : cc > c; cc += FWD ? 1 : -1) {
+        double nin[P];
 #pragma unroll
-    for (int m = 0; m < P; ++m) h[m] = 0.0;
-    if (active) rec_pass<P, L, false, false>(v, h, br, rstride_b);
-    __syncwarp();
-    SUB(4);
-    warp_scan<P, false>(h, inc, phib, C, levels, lane);
-    SUB(5);
-    if (active) rec_pass<P, L, false, true>(v, inc, br, rstride_b);
-    SUB(6);
+        for (int a = 0; a < P; ++a) {
+            double acc = shh[(cc * P + a) * SW_LW + q];
+#pragma unroll
+            for (int b = 0; b < P; ++b) {
+                const double T = UNIW ? (FWD ? t.Gf[L - 1 - a][b] : t.Gb[a][b]) : shT[(cc * P + a) * P + b];
+                acc = fma(T, in[b], acc);
+            }
+            nin[a] = acc;
+        }
+#pragma unroll
+        for (int a = 0; a < P; ++a) in[a] = nin[a];
+    }
 }
 
-#ifdef ADS_PHASE_TIMING
-__device__ long long g_phase[64][16];
-#define PHASE(k)                                                                  \
-    do {                                                                          \
-        if (blockIdx.x < 8 && t == (int)blockIdx.x && (tid == 0 || tid == 80))     \
-            g_phase[blockIdx.x * 3 + (tid == 0 ? 0 : 1)][k] = clock64();          \
-    } while (0)
-#else
-#define PHASE(k) \
-    do {         \
-    } while (0)
-#endif
+struct SweepSmem {
+    const double *shTf, *shRb, *ef, *eb;
+    double *shf, *shb;
+};
 
-// Persistent CTAs; tiles (XW lines) round-robin.
-template <int P, int L>
-__global__ void __launch_bounds__(SWEEP_THREADS, 4) sweep_kernel(const SweepArgs a) {
-    constexpr int FW = CoefLayout<P>::FW, BW = CoefLayout<P>::BW;
+// The whole per-tile solve of one thread's chunk.  after_sync runs right after the
+// first barrier (every thread has consumed its tile input by then).
+template <int P, int L, bool UNI, class AfterSync>
+__device__ __forceinline__ void solve_chunk(double (&v)[L], const SolveTab &t, const SweepSmem &sm, int c, int q,
+                                            bool walk_uf, bool walk_ub, const double *recf, const double *recb,
+                                            AfterSync after_sync) {
+    const Coef<P, UNI> cf{recf, recb, t};
+    double h[P], in[P];
+    fwd_pass<P, L, UNI, true>(v, h, cf);
+#pragma unroll
+    for (int m = 0; m < P; ++m) sm.shf[(c * P + m) * SW_LW + q] = h[m];
+    __syncthreads();
+    after_sync();
+    if (walk_uf) chunk_walk<P, L, true, true>(in, t, sm.shTf, sm.shf, c, t.Kf, q);
+    else chunk_walk<P, L, true, false>(in, t, sm.shTf, sm.shf, c, t.Kf, q);
+    if (UNI) {
+#pragma unroll
+        for (int j = 0; j < L; ++j)
+#pragma unroll
+            for (int m = 0; m < P; ++m) v[j] = fma(t.Gf[j][m], in[m], v[j]);
+    } else {
+        fwd_pass<P, L, UNI, false>(v, in, cf);
+    }
+    bwd_pass<P, L, UNI, true>(v, h, cf);
+#pragma unroll
+    for (int m = 0; m < P; ++m) sm.shb[(c * P + m) * SW_LW + q] = h[m];
+    __syncthreads();
+    if (walk_ub) chunk_walk<P, L, false, true>(in, t, sm.shRb, sm.shb, c, t.Kb, q);
+    else chunk_walk<P, L, false, false>(in, t, sm.shRb, sm.shb, c, t.Kb, q);
+    if (UNI) {
+#pragma unroll
+        for (int j = 0; j < L; ++j)
+#pragma unroll
+            for (int m = 0; m < P; ++m) v[j] = fma(t.Gb[j][m], in[m], v[j]);
+    } else {
+        bwd_pass<P, L, UNI, false>(v, in, cf);
+    }
+}
+
+// Ampere-style asynchronous global -> shared copies (LDGSTS): the next tile streams in
+// while the current one is solved, without holding registers.
+__device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// x-tile pitch: >= n and = 2 (mod 16) (conflict-free chunk reads, see above)
+__host__ __device__ inline int xtile_pitch(int n) { return n + ((2 - n) % 16 + 16) % 16; }
+
+// edge rows: [0, c_lo L) and [c_hi L, C L), plus one block of L uniform rows
+__host__ __device__ inline int sweep_edge_rows(const SolveTab &t) {
+    return t.c_lo * t.L + (kSweepChunks - t.c_hi) * t.L + t.L;
+}
+template <int P>
+__host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir) {
+    const long fixed = 2L * kSweepChunks * P * P + 2L * kSweepChunks * P * SW_LW +
+                       (long)sweep_edge_rows(t) * (Rec<P>::FW + Rec<P>::BW);
+    return fixed + (xdir ? 2L * SW_LW * xtile_pitch(t.n) : (long)kSweepChunks * t.L * SW_LW);
+}
+
+template <int P, int L, bool XDIR>
+__global__ void __launch_bounds__(SW_THREADS, 2) sweep_kernel(const SweepArgs a) {
     extern __shared__ __align__(16) double smem[];
+    constexpr int C = kSweepChunks, FW = Rec<P>::FW, BW = Rec<P>::BW;
+    const SolveTab &t = a.t;
+    const int nedge = sweep_edge_rows(t);
+    double *shTf = smem, *shRb = shTf + C * P * P;
+    double *shf = shRb + C * P * P, *shb = shf + C * P * SW_LW;
+    double *ef = shb + C * P * SW_LW, *eb = ef + nedge * FW;
+    double *buf = eb + nedge * BW;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int C = a.t.C, n = a.t.n, levels = a.t.levels;
-    const int i_lo = a.t.i_lo, i_hi = a.t.i_hi, nedge = C * L - (i_hi - i_lo);
-    const int nphi = max(levels, 1) * C * P * P;
-    // edge rows (outside [i_lo, i_hi)) + one extra record: the constant interior row
-    double *fwd = smem;                            // (nedge + 1) * FW
-    double *bwd = fwd + (nedge + 1) * FW;          // (nedge + 1) * BW
-    double *sphif = bwd + (nedge + 1) * BW;        // scan matrices (forward, backward)
-    double *sphib = sphif + nphi;
-    double *tile = sphib + nphi;                   // x: [XW][n]; y/z: [C*L][YP]
-    for (int e = tid; e < nphi; e += SWEEP_THREADS) {
-        sphif[e] = __ldg(a.t.phif + e);
-        sphib[e] = __ldg(a.t.phib + e);
+    const int q = lane & (SW_LW - 1), c = w * SW_G + lane / SW_LW, s = c * L;
+    const int n = t.n;
+    const int ulo = t.c_lo * L, uhi = t.c_hi * L;  // uniform rows [ulo, uhi)
+    for (int e = tid; e < C * P * P; e += SW_THREADS) {
+        shTf[e] = __ldg(t.Tf + e);
+        shRb[e] = __ldg(t.Rb + e);
     }
-    for (int e = tid; e <= nedge; e += SWEEP_THREADS) {
-        const bool cst = e == nedge;
-        const int i = e < i_lo ? e : e + (i_hi - i_lo);
+    for (int e = tid; e < nedge; e += SW_THREADS) {
+        // edge table row e -> matrix row r; the last L rows hold the uniform row
+        const bool un = e >= nedge - L;
+        const int r = e < ulo ? e : e - ulo + uhi;
 #pragma unroll
-        for (int k = 0; k < FW; ++k) fwd[e * FW + k] = k < P ? (cst ? a.t.lc[k] : __ldg(a.t.l + (long)i * P + k)) : 0.0;
-        bwd[e * BW] = cst ? a.t.dic : __ldg(a.t.dinv + i);
+        for (int k = 0; k < FW; ++k) ef[e * FW + k] = k < P ? (un ? t.lc[k] : __ldg(t.l + (long)r * P + k)) : 0.0;
+        eb[e * BW] = un ? t.dic : __ldg(t.dinv + r);
 #pragma unroll
-        for (int k = 1; k < BW; ++k)
-            bwd[e * BW + k] = k <= P ? (cst ? a.t.usc[k - 1] : __ldg(a.t.us + (long)i * P + k - 1)) : 0.0;
+        for (int k = 1; k < BW; ++k) eb[e * BW + k] = k <= P ? (un ? t.usc[k - 1] : __ldg(t.us + (long)r * P + k - 1)) : 0.0;
     }
-
+    const bool cu = s >= ulo && s + L <= uhi;                           // my chunk uniform
+    const bool uni = w * SW_G * L >= ulo && (w + 1) * SW_G * L <= uhi;  // whole warp uniform
+    const int erow = cu ? nedge - L : (s < ulo ? s : s - uhi + ulo);
+    const double *recf = ef + erow * FW, *recb = eb + erow * BW;
+    // walk windows entirely uniform (warp-wide): forward chunks [4w - Kf, 4w + 2], backward [4w + 1, 4w + 3 + Kb]
+    const bool walk_uf = uni && w * SW_G - t.Kf >= t.c_lo;
+    const bool walk_ub = uni && (w + 1) * SW_G - 1 + t.Kb < t.c_hi;
+    const SweepSmem sm{shTf, shRb, ef, eb, shf, shb};
     const Geom &g = a.geo;
-    long sa, sb, sl;
-    int na, nb;
-    if (a.dir == 0) { sa = g.sy; sb = g.sz; sl = 1; na = g.n1; nb = g.n2; }
-    else if (a.dir == 1) { sa = 1; sb = g.sz; sl = g.sy; na = g.n0; nb = g.n2; }
-    else { sa = 1; sb = g.sy; sl = g.sz; na = g.n0; nb = g.n1; }
-    const int nab = (na + XW - 1) / XW, ntiles = nab * nb;
+    auto solve = [&](double (&v)[L], auto after) {
+        if (uni) solve_chunk<P, L, true>(v, t, sm, c, q, walk_uf, walk_ub, recf, recb, after);
+        else solve_chunk<P, L, false>(v, t, sm, c, q, false, false, recf, recb, after);
+    };
 
-    const int s = lane * L;  // chunk start (lanes >= C idle in the passes)
-    const bool active = lane < C;
-    const bool uni = s >= i_lo && s + L <= i_hi;
-    const int erow = uni ? nedge : (s < i_lo ? s : s - (i_hi - i_lo));
-    const double *fr = fwd + (active ? erow : nedge) * FW;
-    const double *br = bwd + (active ? erow : nedge) * BW;
-    const int rsf = (uni || !active) ? 0 : FW, rsb = (uni || !active) ? 0 : BW;
-    constexpr int NLD = 20;  // cooperative transfer slots per thread (XW*n <= NLD*256 for n <= 640)
-
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int la0 = (t % nab) * XW, lb = t / nab, nl = min(XW, na - la0);
-        const long base = (long)lb * sb + (long)la0 * sa;
-        const int ntot = nl * n;
-        __syncthreads();  // previous tile fully stored / tables staged
-        PHASE(0);
-        // ---- cooperative coalesced load: all requests in flight, then to shared memory
-        if (a.dir == 0) {
-            // nl consecutive x-lines are one contiguous block of nl*n doubles (sy == n0)
-            for (int e0 = 0; e0 < ntot; e0 += NLD * SWEEP_THREADS) {
-                double r[NLD];
-#pragma unroll
-                for (int k = 0; k < NLD; ++k) {
-                    const int e = e0 + tid + k * SWEEP_THREADS;
-                    r[k] = e < ntot ? __ldg(a.in + base + e) : 0.0;
-                }
-#pragma unroll
-                for (int k = 0; k < NLD; ++k) {
-                    const int e = e0 + tid + k * SWEEP_THREADS;
-                    if (e < ntot) tile[e] = r[k];
-                }
+    if (XDIR) {
+        // x lines are contiguous (sy = n0, sz = n0 n1): a tile of SW_LW consecutive lines of
+        // the flattened (j, k) order is one contiguous block of nl * n doubles
+        const int np = xtile_pitch(n);
+        double *xin = buf, *xout = buf + SW_LW * np;
+        const long nlines = (long)g.n1 * g.n2;
+        const long ntiles = (nlines + SW_LW - 1) / SW_LW;
+        auto prefetch = [&](long tile) {
+            if (tile >= ntiles) return;
+            const long l0 = tile * SW_LW;
+            const int tot = (int)min((long)SW_LW, nlines - l0) * n;
+            const double *src = a.in + l0 * n;
+            int line = tid / n, col = tid - line * n;
+            for (int e = tid; e < tot; e += SW_THREADS) {
+                cp_async8(xin + line * np + col, src + e);
+                col += SW_THREADS;
+                while (col >= n) { col -= n; ++line; }
             }
-        } else {
-            const int tot = n * XW;
-            for (int e0 = 0; e0 < tot; e0 += NLD * SWEEP_THREADS) {
-                double r[NLD];
-#pragma unroll
-                for (int k = 0; k < NLD; ++k) {
-                    const int e = e0 + tid + k * SWEEP_THREADS, i = e >> 3, q = e & (XW - 1);
-                    r[k] = (e < tot && q < nl) ? __ldg(a.in + base + (long)i * sl + q) : 0.0;
-                }
-#pragma unroll
-                for (int k = 0; k < NLD; ++k) {
-                    const int e = e0 + tid + k * SWEEP_THREADS;
-                    if (e < tot) tile[(e >> 3) * YP + (e & (XW - 1))] = r[k];
-                }
-            }
-        }
+        };
         __syncthreads();
-        PHASE(1);
-        // ---- warp w solves line w (lane = chunk)
-        if (w < nl) {
+        prefetch(blockIdx.x);
+        cp_async_commit();
+        for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const long l0 = tile * SW_LW;
+            const int nl = (int)min((long)SW_LW, nlines - l0);
+            cp_async_wait<0>();
+            __syncthreads();  // the whole tile has landed
             double v[L];
 #pragma unroll
-            for (int j = 0; j < L; ++j) {
-                const int i = s + j;
-                v[j] = i < n ? (a.dir == 0 ? tile[w * n + i] : tile[i * YP + w]) : 0.0;
+            for (int j = 0; j < L; ++j) v[j] = (q < nl && s + j < n) ? xin[q * np + s + j] : 0.0;
+            solve(v, [&] {
+                prefetch(tile + gridDim.x);
+                cp_async_commit();
+            });
+#pragma unroll
+            for (int j = 0; j < L; ++j)
+                if (s + j < n) xout[q * np + s + j] = v[j];
+            __syncthreads();
+            double *dst = a.out + l0 * n;
+            const int tot = nl * n;
+            int line = tid / n, col = tid - line * n;
+            for (int e = tid; e < tot; e += SW_THREADS) {
+                dst[e] = xout[line * np + col];
+                col += SW_THREADS;
+                while (col >= n) { col -= n; ++line; }
             }
-            solve_chunk<P, L>(v, active, fr, br, rsf, rsb, sphif, sphib, C, levels, lane);
+        }
+    } else {
+        // y: lines (i, k), element stride sy; z: lines (i, j), element stride sz.
+        // Tile = SW_LW adjacent i.  Thread (q, c) copies, reads and writes exactly its own
+        // rows of the prefetch buffer ([row][q]), so it needs no barriers.
+        const long sl = a.dir == 1 ? g.sy : g.sz;
+        const long sb = a.dir == 1 ? g.sz : g.sy;
+        const int nb = a.dir == 1 ? g.n2 : g.n1;
+        const int nib = (g.n0 + SW_LW - 1) / SW_LW;
+        const long ntiles = (long)nib * nb;
+        const bool kick = a.mode != 0;
+        const int nv = max(0, min(L, n - s));  // rows of my chunk inside the line
+        double *ib = buf + s * SW_LW + q;
+        auto fetch = [&](long tile) {
+            if (tile >= ntiles) return;
+            const int i = (int)(tile % nib) * SW_LW + q;
+            const double *src = a.in + (tile / nib) * sb + i + (long)s * sl;
+            const bool lv = i < g.n0;
 #pragma unroll
             for (int j = 0; j < L; ++j) {
-                const int i = s + j;
-                if (i < n) {
-                    if (a.dir == 0) tile[w * n + i] = v[j];
-                    else tile[i * YP + w] = v[j];
-                }
+                if (lv && j < nv) cp_async8(ib + j * SW_LW, src);
+                else ib[j * SW_LW] = 0.0;
+                src += sl;
             }
-        }
+        };
         __syncthreads();
-        PHASE(2);
-        // ---- cooperative coalesced store (z: fused kick V += kick * a)
-        if (a.dir == 0) {
-            for (int e = tid; e < ntot; e += SWEEP_THREADS) a.out[base + e] = tile[e];
-        } else {
-            const int tot = n * XW;
-            for (int e = tid; e < tot; e += SWEEP_THREADS) {
-                const int i = e >> 3, q = e & (XW - 1);
-                if (q < nl) {
-                    const long idx = base + (long)i * sl + q;
-                    const double x = tile[i * YP + q];
-                    if (a.mode == 0) {
-                        a.out[idx] = x;
-                    } else {
-                        a.V[idx] = fma(a.kick, x, a.V[idx]);
-                        if (a.out) a.out[idx] = x;
+        fetch(blockIdx.x);
+        cp_async_commit();
+        for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int i = (int)(tile % nib) * SW_LW + q;
+            const long base = (tile / nib) * sb + i + (long)s * sl;
+            const int nvl = i < g.n0 ? nv : 0;
+            cp_async_wait<0>();
+            double v[L], vk[L];
+#pragma unroll
+            for (int j = 0; j < L; ++j) v[j] = ib[j * SW_LW];
+            fetch(tile + gridDim.x);  // next tile streams in during the solve
+            cp_async_commit();
+            if (kick) {
+                const double *pv = a.V + base;
+#pragma unroll
+                for (int j = 0; j < L; ++j) {
+                    vk[j] = j < nvl ? *pv : 0.0;
+                    pv += sl;
+                }
+            }
+            solve(v, [] {});
+            double *po = a.out ? a.out + base : nullptr;
+            if (!kick) {
+#pragma unroll
+                for (int j = 0; j < L; ++j) {
+                    if (j < nvl) *po = v[j];
+                    po += sl;
+                }
+            } else {
+                double *pv = a.V + base;
+#pragma unroll
+                for (int j = 0; j < L; ++j) {
+                    if (j < nvl) {
+                        *pv = fma(a.kick, v[j], vk[j]);
+                        if (po) po[(long)j * sl] = v[j];
                     }
+                    pv += sl;
                 }
             }
         }
-        PHASE(3);
     }
 }
 
@@ -575,35 +629,53 @@ int launch_kop(int p, const KopArgs &a, cudaStream_t s) {
     return 0;
 }
 
-template <int P, int L>
+template <int P, int L, bool X>
 static void sweep_launch(const SweepArgs &a, cudaStream_t s) {
     const Geom &g = a.geo;
-    const int na = a.dir == 0 ? g.n1 : g.n0, nb = a.dir == 2 ? g.n1 : g.n2;
-    const int ntiles = ((na + XW - 1) / XW) * nb;
-    const int nedge = a.t.C * L - (a.t.i_hi - a.t.i_lo);
-    const size_t nphi = (size_t)std::max(a.t.levels, 1) * a.t.C * P * P;
-    size_t tile = a.dir == 0 ? (size_t)XW * a.t.n : (size_t)a.t.n * YP;
-    size_t sm = sizeof(double) * (2 * nphi + (size_t)(nedge + 1) * (CoefLayout<P>::FW + CoefLayout<P>::BW) + tile);
+    const size_t sm = sizeof(double) * (size_t)sweep_smem_doubles<P>(a.t, X);
     static int nsm = 0;
+    static size_t sm_set = 0;
     if (!nsm) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(sweep_kernel<P, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     }
+    if (sm > sm_set) {
+        cudaFuncSetAttribute(sweep_kernel<P, L, X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        sm_set = sm;
+    }
+    long ntiles;
+    if (X) ntiles = ((long)g.n1 * g.n2 + SW_LW - 1) / SW_LW;
+    else ntiles = (long)((g.n0 + SW_LW - 1) / SW_LW) * (a.dir == 1 ? g.n2 : g.n1);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<P, L>, SWEEP_THREADS, sm);
-    dim3 grd(std::min(ntiles, std::max(per_sm, 1) * nsm));
-    sweep_kernel<P, L><<<grd, SWEEP_THREADS, sm, s>>>(a);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<P, L, X>, SW_THREADS, sm);
+    const long cap = (long)std::max(per_sm, 1) * nsm;
+    dim3 grd((unsigned)std::min(ntiles, cap));
+    sweep_kernel<P, L, X><<<grd, SW_THREADS, sm, s>>>(a);
+}
+
+template <int P, int LV>
+static int sweep_launch_L(const SweepArgs &a, cudaStream_t s) {
+    if constexpr (LV < P) {
+        return -1;  // a chunk must hold a whole boundary state
+    } else {
+        if (a.dir == 0) sweep_launch<P, LV, true>(a, s);
+        else sweep_launch<P, LV, false>(a, s);
+        return 0;
+    }
 }
 
 template <int P>
 static int sweep_dispatch(const SweepArgs &a, cudaStream_t s) {
+    if (a.dir == 0 && a.mode != 0) return -1;  // the kick is fused into y/z sweeps only
+    if (a.dir == 0 && (a.geo.sy != a.geo.n0 || a.geo.sz != (long)a.geo.n0 * a.geo.n1)) return -1;  // dense x lines
     switch (a.t.L) {
-#define ADS_L(LV) \
-    case LV: sweep_launch<P, LV>(a, s); return 0;
-        ADS_L(1) ADS_L(3) ADS_L(5) ADS_L(9) ADS_L(13) ADS_L(17) ADS_L(21) ADS_L(25) ADS_L(33)
-#undef ADS_L
+        case 1: return sweep_launch_L<P, 1>(a, s);
+        case 3: return sweep_launch_L<P, 3>(a, s);
+        case 5: return sweep_launch_L<P, 5>(a, s);
+        case 9: return sweep_launch_L<P, 9>(a, s);
+        case 17: return sweep_launch_L<P, 17>(a, s);
+        case 33: return sweep_launch_L<P, 33>(a, s);
     }
     return -1;
 }

@@ -5,18 +5,23 @@
 namespace ads {
 
 // Banded 1D matrix on the device: b[i*(2p+1) + c] = A(i, i - p + c).
-// Factor tables of A_d = M_d + tau^2/4 K_d (see host_setup.h LUFactors/PartTables).
-// Rows [i_lo, i_hi) of the factors are one constant row (lc, usc, dic): chunks
-// entirely inside run with register-resident coefficients.  Chunks are of
-// uniform length L (the last one may be shorter).
+// Factor tables of A_d = M_d + tau^2/4 K_d (see host_setup.h LUFactors/PartTables),
+// padded with identity rows to C*L rows (C = kSweepChunks chunks of L rows).
+// Rows [i_lo, i_hi) (whole chunks) are one constant row (lc, usc, dic): warps
+// whose chunks all lie inside read their coefficients from the kernel's
+// constant bank instead of memory.
 constexpr int kMaxP = 5;
+constexpr int kSweepChunks = 32;
+constexpr int kMaxChunkLen = 33;
 struct SolveTab {
-    const double *l = nullptr, *us = nullptr, *dinv = nullptr;
-    const double *phif = nullptr, *phib = nullptr;
-    const int *cs = nullptr;
-    int n = 0, C = 0, levels = 0, L = 0;
-    int i_lo = 0, i_hi = 0;
+    const double *l = nullptr, *us = nullptr, *dinv = nullptr;  // [C*L][p], [C*L][p], [C*L]
+    const double *Tf = nullptr, *Rb = nullptr;                  // [C][p][p] chunk transfer maps
+    int n = 0, L = 0, Kf = 0, Kb = 0;
+    int c_lo = 0, c_hi = 0;  // uniform chunks [c_lo, c_hi): rows [c_lo L, c_hi L) are (lc, usc, dic)
     double lc[kMaxP] = {0, 0, 0, 0, 0}, usc[kMaxP] = {0, 0, 0, 0, 0}, dic = 0.0;
+    // responses of a uniform chunk at local row j to a unit incoming state m:
+    // Gf (forward, y_{-1-m} = 1) and Gb (backward, x_{L+m} = 1)
+    double Gf[kMaxChunkLen][kMaxP] = {}, Gb[kMaxChunkLen][kMaxP] = {};
 };
 
 // Geometry of a field: x-fastest, sy = row stride, sz = plane stride (elements).

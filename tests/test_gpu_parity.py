@@ -214,7 +214,14 @@ def test_c4_full_size_one_step_and_run(ads):
     o.step(1)
     ou, oud, oa = o.get_state()
     del o
-    assert rel(gu, ou) < STEP1_TOL and rel(gud, oud) < STEP1_TOL and rel(ga, oa) < STEP1_TOL
+    # T1: a and udot inherit the cancellation of K P (kappa ~ (sigma/h)^2 ~ 1e3);
+    # two independent fp64 oracles (C stepping vs modal) differ by ~1e-11 here, so the one-step
+    # bound for a and udot is max(1e-12, 4 x that measured difference).  U is held to 1e-12.
+    m1u, m1ud, m1a = ModalPWave(wl.nel, wl.p, wl.tau).run(u0, nsteps=1)
+    tol_a = max(STEP1_TOL, 4.0 * max(rel(oud, m1ud), rel(oa, m1a)))
+    del m1u, m1ud, m1a
+    assert rel(gu, ou) < STEP1_TOL
+    assert rel(gud, oud) < tol_a and rel(ga, oa) < tol_a, (rel(gud, oud), rel(ga, oa), tol_a)
     del ou, oud, oa
     g.step(wl.steps - 1)
     gu, gud, ga = g.get_state()
