@@ -23,6 +23,8 @@ namespace {
 struct DirDev {
     double *mband = nullptr, *kband = nullptr, *aband = nullptr;  // [n][2p+1]
     double *l = nullptr, *us = nullptr, *dinv = nullptr, *Tf = nullptr, *Rb = nullptr;
+    int t_lo = 1, t_hi = 0;  // rows [t_lo, t_hi] of M, K are the Toeplitz row (mrow, krow)
+    double mrow[2 * kMaxP + 1] = {}, krow[2 * kMaxP + 1] = {};
     SolveTab tab;
 };
 
@@ -176,6 +178,21 @@ int build_direction(ads_ctx *h, int d) {
     PartTables pt;
     build_part_tables(fp, C, L, pt);
     DirDev &D = h->dd[d];
+    // Toeplitz interior of M, K (build_space made rows [2p, n-1-2p] bitwise equal)
+    if (n - 1 - 2 * p - 2 * p >= 2) {
+        D.t_lo = 2 * p;
+        D.t_hi = n - 1 - 2 * p;
+        for (int c = 0; c < W; ++c) {
+            D.mrow[c] = s.M.v[(size_t)D.t_lo * W + c];
+            D.krow[c] = s.K.v[(size_t)D.t_lo * W + c];
+        }
+        for (int i = D.t_lo; i <= D.t_hi; ++i)
+            for (int c = 0; c < W; ++c)
+                if (s.M.v[(size_t)i * W + c] != D.mrow[c] || s.K.v[(size_t)i * W + c] != D.krow[c]) {
+                    D.t_lo = 1;
+                    D.t_hi = 0;
+                }
+    }
     int rc;
     std::vector<double> mb(s.M.v), kb(s.K.v), ab(A.v);
     (void)W;
@@ -242,6 +259,14 @@ int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g
     a.kz = h->dd[2].kband;
     a.geo = h->geo;
     a.zlen = 0;
+    for (int d = 0; d < 3; ++d) {
+        a.ilo[d] = h->dd[d].t_lo;
+        a.ihi[d] = h->dd[d].t_hi;
+        for (int c = 0; c < 2 * h->p + 1; ++c) {
+            a.mc[d][c] = h->dd[d].mrow[c];
+            a.kc[d][c] = h->dd[d].krow[c];
+        }
+    }
     ProfScope ps(h, 0);
     if (launch_kop(h->p, a, h->stream)) return fail(h, ADS_E_INVAL, "kop: unsupported p");
     return check_launch(h, "kop");

@@ -16,156 +16,12 @@
 //                  memory (coalesced); y/z lines are loaded coalesced across 8
 //                  adjacent x-lines.  The z sweep fuses the kick V += tau a.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 
 #include "kernels.cuh"
 
 namespace ads {
-
-// ------------------------------------------------------------------------------------------
-// fused drift + source + K-apply
-//
-// Tile: 32 (x) x 8 (y) outputs per CTA, marching along z.  Per input plane kk:
-//   commit  P(kk) = U + tau V  -> shared tile (haloed by p in x and y) [+ HBM for owned points]
-//   y-pass  Y1 = My P, Y2 = Ky P          on the 8 owned rows, 32+2p columns
-//   x-pass  S  = Kx Y1 + Mx Y2, T = Mx Y1 on the 32x8 owned points -> register ring slot
-//   z-pass  K P(k) = Mz S + Kz T over the ring (k = kk - p), + source -> r
-// (K = Kx My Mz + Mx Ky Mz + Mx My Kz; 1D factors along different axes commute.)
-// The ring of 2p+1 planes is rotated by unrolling the plane loop 2p+1 times.
-// ------------------------------------------------------------------------------------------
-template <int P>
-struct KopSmem {
-    static constexpr int TX = 32, TY = 8, W = 2 * P + 1, HX = TX + 2 * P, HY = TY + 2 * P;
-    double Ps[HY][HX];
-    double Y1[TY][HX], Y2[TY][HX];
-    double zc[2][2][W];  // [parity][Mz|Kz][c] rows of the output plane
-};
-
-template <int P>
-__global__ void __launch_bounds__(256, 2) kop_kernel(const KopArgs a) {
-    using S_ = KopSmem<P>;
-    constexpr int TX = S_::TX, TY = S_::TY, W = S_::W, HX = S_::HX, HY = S_::HY;
-    __shared__ S_ sm;
-
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int n0 = a.geo.n0, n1 = a.geo.n1, n2 = a.geo.n2;
-    const long sy = a.geo.sy, sz = a.geo.sz;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int z0 = blockIdx.z * a.zlen, z1 = min(n2, z0 + a.zlen);
-    const int gx = x0 + tx, gy = y0 + ty;
-    const bool own = gx < n0 && gy < n1;
-
-    // band rows of this thread's x (Mx, Kx) and y (My, Ky)
-    double mx[W], kx[W], my[W], ky[W];
-#pragma unroll
-    for (int c = 0; c < W; ++c) {
-        mx[c] = gx < n0 ? __ldg(a.mx + (long)gx * W + c) : 0.0;
-        kx[c] = gx < n0 ? __ldg(a.kx + (long)gx * W + c) : 0.0;
-        my[c] = gy < n1 ? __ldg(a.my + (long)gy * W + c) : 0.0;
-        ky[c] = gy < n1 ? __ldg(a.ky + (long)gy * W + c) : 0.0;
-    }
-    const double sxy = (a.bx && own) ? __ldg(a.bx + gx) * __ldg(a.by + gy) : 0.0;
-
-    // load slots: haloed (ry, rx) = (ty + 8 sr, tx + 32 sc)
-    constexpr int NSR = (HY + TY - 1) / TY, NS = 2 * NSR;
-    bool sv[NS];
-    long soff[NS];
-#pragma unroll
-    for (int q = 0; q < NS; ++q) {
-        const int ry = ty + TY * (q >> 1), rx = tx + TX * (q & 1);
-        const int X = x0 - P + rx, Y = y0 - P + ry;
-        sv[q] = ry < HY && rx < HX && X >= 0 && X < n0 && Y >= 0 && Y < n1;
-        soff[q] = (long)Y * sy + X;
-    }
-    double pu[NS], pv[NS];
-    auto load = [&](int kin) {
-        const bool kv = kin >= 0 && kin < n2;
-#pragma unroll
-        for (int q = 0; q < NS; ++q) {
-            pu[q] = 0.0;
-            pv[q] = 0.0;
-            if (sv[q] && kv) {
-                pu[q] = __ldg(a.U + (long)kin * sz + soff[q]);
-                pv[q] = __ldg(a.V + (long)kin * sz + soff[q]);
-            }
-        }
-    };
-
-    double Sr[W], Tr[W];
-#pragma unroll
-    for (int c = 0; c < W; ++c) Sr[c] = Tr[c] = 0.0;
-
-    const int tid = ty * TX + tx;
-    load(z0 - P);
-    for (int kb = z0 - P; kb < z1 + P; kb += W) {
-#pragma unroll
-        for (int u = 0; u < W; ++u) {
-            const int kk = kb + u;
-            if (kk < z1 + P) {
-                const int k = kk - P;  // output plane
-                // commit plane kk
-#pragma unroll
-                for (int q = 0; q < NS; ++q) {
-                    const int ry = ty + TY * (q >> 1), rx = tx + TX * (q & 1);
-                    if (ry < HY && rx < HX) {
-                        const double pp = fma(a.tau, pv[q], pu[q]);
-                        sm.Ps[ry][rx] = pp;
-                        if (a.Pout && sv[q] && kk >= z0 && kk < z1 && ry >= P && rx >= P && rx < P + TX &&
-                            ry < P + TY)
-                            a.Pout[(long)kk * sz + soff[q]] = pp;
-                    }
-                }
-                if (tid < 2 * W && k >= z0) {
-                    const double *src = (tid < W ? a.mz : a.kz) + (long)k * W + (tid < W ? tid : tid - W);
-                    sm.zc[kk & 1][tid < W ? 0 : 1][tid < W ? tid : tid - W] = __ldg(src);
-                }
-                __syncthreads();
-                if (kk + 1 < z1 + P) load(kk + 1);  // in flight during the passes below
-
-                // y-pass on owned rows, all haloed columns
-#pragma unroll
-                for (int cs = 0; cs < 2; ++cs) {
-                    const int col = tx + TX * cs;
-                    if (col < HX) {
-                        double y1 = 0.0, y2 = 0.0;
-#pragma unroll
-                        for (int c = 0; c < W; ++c) {
-                            const double v = sm.Ps[ty + c][col];
-                            y1 = fma(my[c], v, y1);
-                            y2 = fma(ky[c], v, y2);
-                        }
-                        sm.Y1[ty][col] = y1;
-                        sm.Y2[ty][col] = y2;
-                    }
-                }
-                __syncthreads();
-                // x-pass on owned points
-                double s = 0.0, t = 0.0;
-#pragma unroll
-                for (int c = 0; c < W; ++c) {
-                    const double y1 = sm.Y1[ty][tx + c], y2 = sm.Y2[ty][tx + c];
-                    s = fma(kx[c], y1, s);
-                    s = fma(mx[c], y2, s);
-                    t = fma(mx[c], y1, t);
-                }
-                Sr[u] = s;
-                Tr[u] = t;
-                // z-pass: plane k-p+c sits in ring slot (u + 1 + c) mod W
-                if (k >= z0 && own) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int c = 0; c < W; ++c) {
-                        const int slot = (u + 1 + c) % W;
-                        acc = fma(sm.zc[kk & 1][0][c], Sr[slot], acc);
-                        acc = fma(sm.zc[kk & 1][1][c], Tr[slot], acc);
-                    }
-                    const double src = (a.bx) ? a.g * sxy * __ldg(a.bz + k) : 0.0;
-                    a.r[(long)k * sz + (long)gy * sy + gx] = fma(a.sign, acc, src);
-                }
-            }
-        }
-    }
-}
 
 // ------------------------------------------------------------------------------------------
 // partitioned banded sweeps (v3)
@@ -517,6 +373,248 @@ __global__ void __launch_bounds__(SW_THREADS, 2) sweep_kernel(const SweepArgs a)
 }
 
 // ------------------------------------------------------------------------------------------
+// fused drift + source + K-apply (v2)
+//
+//   P = U + tau V (written to Pout),  r = g (bx (x) by (x) bz) + sign K P,
+//   K = Kx My Mz + Mx Ky Mz + Mx My Kz   (Eq. 14, 3D)
+// by sum factorisation: y-pass Y1 = My P, Y2 = Ky P; x-pass S = Kx Y1 + Mx Y2,
+// T = Mx Y1; z-pass K P = Mz S + Kz T  (7 banded passes).
+//
+// CTA = 256 threads on a KT_X x KT_Y = 32 x 16 output tile, marching along z over
+// [z0, z1).  Per input plane kk:
+//   - the raw U, V plane of the haloed tile ((32+2p) x (16+2p)) streams HBM -> shared
+//     memory with cp.async, KT_NPF-1 planes ahead (ring of KT_NPF buffers);
+//   - y-pass: thread (column, group of 4 rows) forms P on 4+2p rows from the raw
+//     values, writes the owned P to HBM, and Y1/Y2 of its 4 rows to shared memory;
+//   - x-pass: lane = x, warp = 2 rows: S, T from 2p+1 neighbouring (Y1, Y2);
+//   - z-pass: S, T of the last 2p+1 planes stay in registers (the plane loop is
+//     unrolled 2p+1 times so the ring never moves); output plane kk - p gets
+//     r = src + sign (Mz S + Kz T).
+// Band rows inside the Toeplitz interior come from the kernel's constant bank
+// (tile-/plane-uniform branches); boundary tiles read staged rows from shared memory.
+// HBM traffic: U, V read once (the halo is re-read from L2), P and r written once.
+// ------------------------------------------------------------------------------------------
+constexpr int KT_X = 32, KT_Y = 16, KT_THREADS = 256, KT_NPF = 4, KT_RY = 4;
+template <int P>
+struct KopGeo {
+    static constexpr int W = 2 * P + 1, HX = KT_X + 2 * P, HY = KT_Y + 2 * P, HN = HX * HY;
+    static constexpr int HNP = (HN + 1) & ~1;
+    static constexpr int NSLOT = (HN + KT_THREADS - 1) / KT_THREADS;
+    static constexpr int NITEM = HX * (KT_Y / KT_RY);
+    // shared memory (doubles): raw ring | Y tile (double2) | x rows | y rows
+    static constexpr int RING = KT_NPF * 2 * HNP, YT = KT_Y * HX * 2, XB = KT_X * 2 * W, YB = KT_Y * 2 * W;
+    static constexpr int SMEM = RING + YT + XB + YB;
+};
+static_assert(KopGeo<5>::NITEM <= KT_THREADS, "one y-pass item per thread");
+
+// z-pass scatter of one input plane kk (ring slot U = (kk - kk0) mod W, see kop_tile)
+template <int P, int U>
+__device__ __forceinline__ void kop_zscatter(const KopArgs &a, double (&A0)[2 * P + 1], double (&A1)[2 * P + 1],
+                                             double s0, double t0, double s1, double t1, int kk, bool zint,
+                                             int z0, bool own0, bool own1, double sxy0, double sxy1, long oxy) {
+    constexpr int W = 2 * P + 1;
+    if (zint) {
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+            const int sl = ((U - P + c) % W + W) % W;
+            A0[sl] = fma(a.mc[2][2 * P - c], s0, A0[sl]);
+            A0[sl] = fma(a.kc[2][2 * P - c], t0, A0[sl]);
+            A1[sl] = fma(a.mc[2][2 * P - c], s1, A1[sl]);
+            A1[sl] = fma(a.kc[2][2 * P - c], t1, A1[sl]);
+        }
+    } else {
+        const int n2 = a.geo.n2;
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+            const int sl = ((U - P + c) % W + W) % W;
+            const int k = kk - P + c;
+            double mz_ = 0.0, kz_ = 0.0;
+            if (k >= 0 && k < n2) {
+                mz_ = __ldg(a.mz + (long)k * W + 2 * P - c);
+                kz_ = __ldg(a.kz + (long)k * W + 2 * P - c);
+            }
+            A0[sl] = fma(mz_, s0, A0[sl]);
+            A0[sl] = fma(kz_, t0, A0[sl]);
+            A1[sl] = fma(mz_, s1, A1[sl]);
+            A1[sl] = fma(kz_, t1, A1[sl]);
+        }
+    }
+    constexpr int so = ((U - P) % W + W) % W;  // slot of the completed output k = kk - P
+    const int k = kk - P;
+    if (k >= z0) {
+        const double gz = a.bx ? a.g * __ldg(a.bz + k) : 0.0;
+        const long o = (long)k * a.geo.sz + oxy;
+        if (own0) a.r[o] = fma(a.sign, A0[so], gz * sxy0);
+        if (own1) a.r[o + a.geo.sy] = fma(a.sign, A1[so], gz * sxy1);
+    }
+    A0[so] = 0.0;
+    A1[so] = 0.0;
+}
+
+template <int P, bool XI, bool YI>
+__device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0, int y0, int z0, int z1) {
+    using G = KopGeo<P>;
+    constexpr int W = G::W, HX = G::HX, HNP = G::HNP;
+    double *ring = smem;
+    double2 *Ys = reinterpret_cast<double2 *>(smem + G::RING);
+    double *xb = smem + G::RING + G::YT;  // [KT_X][2][W]: (Mx, Kx) rows of x0 + lane
+    double *yb = xb + G::XB;              // [KT_Y][2][W]: (My, Ky) rows of y0 + row
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int n0 = a.geo.n0, n1 = a.geo.n1, n2 = a.geo.n2;
+    const long sy = a.geo.sy, sz = a.geo.sz;
+
+    // stage boundary band rows (zero outside the domain)
+    if (!XI)
+        for (int e = tid; e < KT_X * 2 * W; e += KT_THREADS) {
+            const int xr = e / (2 * W), m = (e / W) & 1, c = e % W, X = x0 + xr;
+            xb[e] = X < n0 ? __ldg((m ? a.kx : a.mx) + (long)X * W + c) : 0.0;
+        }
+    if (!YI)
+        for (int e = tid; e < KT_Y * 2 * W; e += KT_THREADS) {
+            const int yr = e / (2 * W), m = (e / W) & 1, c = e % W, Y = y0 + yr;
+            yb[e] = Y < n1 ? __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
+        }
+
+    // load slots of the haloed plane (fixed per thread): element e = tid + 256 m of the
+    // [HY][HX] tile; global offset relative to the tile origin (x0 - P, y0 - P)
+    int goff[G::NSLOT];
+    unsigned inr = 0;
+#pragma unroll
+    for (int m = 0; m < G::NSLOT; ++m) {
+        const int e = tid + m * KT_THREADS, hy = e / HX, hx = e - hy * HX;
+        const int X = x0 - P + hx, Y = y0 - P + hy;
+        goff[m] = hy * (int)sy + hx;
+        if (e < G::HN && X >= 0 && X < n0 && Y >= 0 && Y < n1) inr |= 1u << m;
+    }
+    const long org = (long)(y0 - P) * sy + (x0 - P);
+    const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;
+    auto issue = [&](int ii) {
+        if (ii < npl) {
+            const int kk = kk0 + ii;
+            double *bu = ring + (ii & (KT_NPF - 1)) * 2 * HNP, *bv = bu + HNP;
+            const bool kv = kk >= 0 && kk < n2;
+            const long zo = (long)kk * sz + org;
+#pragma unroll
+            for (int m = 0; m < G::NSLOT; ++m) {
+                const int e = tid + m * KT_THREADS;
+                if (e >= G::HN) continue;
+                if (kv && (inr >> m & 1)) {
+                    cp_async8(bu + e, a.U + zo + goff[m]);
+                    cp_async8(bv + e, a.V + zo + goff[m]);
+                } else {
+                    bu[e] = 0.0;
+                    bv[e] = 0.0;
+                }
+            }
+        }
+        cp_async_commit();
+    };
+
+    // y-pass item: column col of the haloed tile, output rows 4 grp .. 4 grp + 3
+    const bool yitem = tid < G::NITEM;
+    const int col = tid % HX, grp = tid / HX;
+    const int Xc = x0 - P + col;
+    const bool pown = yitem && col >= P && col < P + KT_X && Xc < n0;
+    // x-pass outputs: X = x0 + lane, rows 2w, 2w+1
+    const int X = x0 + lane;
+    const int Yo0 = y0 + 2 * w;
+    const bool own0 = X < n0 && Yo0 < n1, own1 = X < n0 && Yo0 + 1 < n1;
+    const double sxy0 = (a.bx && own0) ? __ldg(a.bx + X) * __ldg(a.by + Yo0) : 0.0;
+    const double sxy1 = (a.bx && own1) ? __ldg(a.bx + X) * __ldg(a.by + Yo0 + 1) : 0.0;
+
+    // pending outputs: A0/A1[(k - kk0) mod W] accumulates plane k = kk - P + c of rows 2w, 2w+1
+    double A0[W], A1[W];
+#pragma unroll
+    for (int c = 0; c < W; ++c) A0[c] = A1[c] = 0.0;
+
+#pragma unroll
+    for (int i = 0; i < KT_NPF - 1; ++i) issue(i);
+    __syncthreads();  // staged band rows visible
+
+    for (int ii = 0; ii < npl; ++ii) {
+        {
+            {
+                const int kk = kk0 + ii;
+                cp_async_wait<KT_NPF - 2>();
+                __syncthreads();  // plane kk landed in every thread's slots; Ys free
+                issue(ii + KT_NPF - 1);
+                // ---- y-pass
+                if (yitem) {
+                    const double *bu = ring + (ii & (KT_NPF - 1)) * 2 * HNP, *bv = bu + HNP;
+                    double pr[KT_RY + 2 * P];
+#pragma unroll
+                    for (int r = 0; r < KT_RY + 2 * P; ++r) {
+                        const int e = (KT_RY * grp + r) * HX + col;
+                        pr[r] = fma(a.tau, bv[e], bu[e]);
+                    }
+                    if (a.Pout && pown && kk >= z0 && kk < z1) {
+#pragma unroll
+                        for (int r = 0; r < KT_RY; ++r) {
+                            const int Y = y0 + KT_RY * grp + r;
+                            if (Y < n1) a.Pout[(long)kk * sz + (long)Y * sy + Xc] = pr[r + P];
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < KT_RY; ++r) {
+                        const int yr = KT_RY * grp + r;
+                        double y1 = 0.0, y2 = 0.0;
+#pragma unroll
+                        for (int c = 0; c < W; ++c) {
+                            const double m_ = YI ? a.mc[1][c] : yb[(yr * 2 + 0) * W + c];
+                            const double k_ = YI ? a.kc[1][c] : yb[(yr * 2 + 1) * W + c];
+                            y1 = fma(m_, pr[r + c], y1);
+                            y2 = fma(k_, pr[r + c], y2);
+                        }
+                        Ys[yr * HX + col] = make_double2(y1, y2);
+                    }
+                }
+                __syncthreads();  // Ys complete
+                // ---- x-pass
+                double s0 = 0.0, t0 = 0.0, s1 = 0.0, t1 = 0.0;
+#pragma unroll
+                for (int c = 0; c < W; ++c) {
+                    const double mx_ = XI ? a.mc[0][c] : xb[(lane * 2 + 0) * W + c];
+                    const double kx_ = XI ? a.kc[0][c] : xb[(lane * 2 + 1) * W + c];
+                    const double2 q0 = Ys[(2 * w) * HX + lane + c];
+                    const double2 q1 = Ys[(2 * w + 1) * HX + lane + c];
+                    s0 = fma(kx_, q0.x, s0);
+                    s0 = fma(mx_, q0.y, s0);
+                    t0 = fma(mx_, q0.x, t0);
+                    s1 = fma(kx_, q1.x, s1);
+                    s1 = fma(mx_, q1.y, s1);
+                    t1 = fma(mx_, q1.x, t1);
+                }
+                // ---- z-pass, scatter form: input plane kk feeds outputs k = kk - P + c (c = 0..2P)
+                // with Mz(k, kk) = mz[k][2P - c]; output kk - P is then complete.  The ring slot
+                // of output k is (k - kk0) mod W; a switch makes every slot index compile-time.
+                const bool zint = kk - P >= a.ilo[2] && kk + P <= a.ihi[2];
+                switch (ii % W) {
+#define ADS_ZCASE(U)                                                                                  \
+    case U:                                                                                           \
+        if constexpr (U < W) kop_zscatter<P, U>(a, A0, A1, s0, t0, s1, t1, kk, zint, z0, own0, own1, \
+                                                 sxy0, sxy1, (long)Yo0 * sy + X);                     \
+        break;
+                    ADS_ZCASE(0) ADS_ZCASE(1) ADS_ZCASE(2) ADS_ZCASE(3) ADS_ZCASE(4) ADS_ZCASE(5)
+                    ADS_ZCASE(6) ADS_ZCASE(7) ADS_ZCASE(8) ADS_ZCASE(9) ADS_ZCASE(10)
+#undef ADS_ZCASE
+                }
+            }
+        }
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(KT_THREADS, 2) kop_kernel(const KopArgs a) {
+    extern __shared__ __align__(16) double smem[];
+    const int x0 = blockIdx.x * KT_X, y0 = blockIdx.y * KT_Y;
+    const int z0 = blockIdx.z * a.zlen, z1 = min(a.geo.n2, z0 + a.zlen);
+    const bool xi = x0 >= a.ilo[0] && x0 + KT_X - 1 <= a.ihi[0];
+    const bool yi = y0 >= a.ilo[1] && y0 + KT_Y - 1 <= a.ihi[1];
+    if (xi && yi) kop_tile<P, true, true>(a, smem, x0, y0, z0, z1);
+    else kop_tile<P, false, false>(a, smem, x0, y0, z0, z1);
+}
+
+// ------------------------------------------------------------------------------------------
 // helpers
 // ------------------------------------------------------------------------------------------
 template <int P>
@@ -609,12 +707,34 @@ static int grid_for(long N) {
 
 template <int P>
 static void kop_launch(const KopArgs &a, cudaStream_t s) {
-    dim3 blk(32, 8);
-    int zl = a.zlen > 0 ? a.zlen : a.geo.n2;
-    dim3 grd((a.geo.n0 + 31) / 32, (a.geo.n1 + 7) / 8, (a.geo.n2 + zl - 1) / zl);
+    using G = KopGeo<P>;
+    const size_t sm = sizeof(double) * G::SMEM;
+    static int nsm = 0, per_sm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(kop_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kop_kernel<P>, KT_THREADS, sm);
+        per_sm = std::max(per_sm, 1);
+    }
+    const int gx = (a.geo.n0 + KT_X - 1) / KT_X, gy = (a.geo.n1 + KT_Y - 1) / KT_Y;
+    // z split: enough CTAs to fill whole waves, each z piece re-reads 2p halo planes
+    const long resident = (long)per_sm * nsm, tiles = (long)gx * gy;
+    int best = 1;
+    double best_cost = 1e300;
+    for (int nz = 1; nz <= 16; ++nz) {
+        const int zl = (a.geo.n2 + nz - 1) / nz;
+        if (zl < 2 * P + 1 && nz > 1) break;
+        const long ctas = tiles * ((a.geo.n2 + zl - 1) / zl);
+        const double waves = std::ceil((double)ctas / resident);
+        const double cost = waves * (zl + 2.0 * P) * ((double)resident / std::min<long>(ctas, resident));
+        if (cost < best_cost * 0.999) { best_cost = cost; best = nz; }
+    }
     KopArgs b = a;
-    b.zlen = zl;
-    kop_kernel<P><<<grd, blk, 0, s>>>(b);
+    b.zlen = a.zlen > 0 ? a.zlen : (a.geo.n2 + best - 1) / best;
+    dim3 grd(gx, gy, (a.geo.n2 + b.zlen - 1) / b.zlen);
+    kop_kernel<P><<<grd, KT_THREADS, sm, s>>>(b);
 }
 
 int launch_kop(int p, const KopArgs &a, cudaStream_t s) {

@@ -32,6 +32,8 @@ struct Geom {
 
 // r = g * (bx (x) by (x) bz) + sign * K P,  P = U + tau V  (P written to Pout if non-null).
 // K = Kx(x)My(x)Mz + Mx(x)Ky(x)Mz + Mx(x)My(x)Kz by sum factorisation.
+// Rows [ilo[d], ihi[d]] of M_d, K_d are the Toeplitz row (mc[d], kc[d]) bitwise (uniform mesh,
+// host_setup build_space); tiles/planes inside read these from the constant bank.
 struct KopArgs {
     const double *U = nullptr, *V = nullptr;
     double *Pout = nullptr, *r = nullptr;
@@ -40,6 +42,8 @@ struct KopArgs {
     const double *mx = nullptr, *kx = nullptr, *my = nullptr, *ky = nullptr, *mz = nullptr, *kz = nullptr;
     Geom geo;
     int zlen = 0;
+    int ilo[3] = {1, 1, 1}, ihi[3] = {0, 0, 0};
+    double mc[3][2 * kMaxP + 1] = {}, kc[3][2 * kMaxP + 1] = {};
 };
 
 // Batched banded solve along direction dir of every line of `in`.
