@@ -197,6 +197,10 @@ __device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
 }
+// shared address + zero fill: copies nbytes (0 or 8) and fills the rest of the 8 bytes with 0
+__device__ __forceinline__ void cp_async8_zfill(unsigned sdst, const double *gsrc, unsigned nbytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(nbytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -476,35 +480,32 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
         }
 
     // load slots of the haloed plane (fixed per thread): element e = tid + 256 m of the
-    // [HY][HX] tile; global offset relative to the tile origin (x0 - P, y0 - P)
+    // [HY][HX] tile.  Out-of-domain elements are zero-filled by the copy itself
+    // (cp.async src-size 0), so every slot issues exactly one copy per field and plane.
     int goff[G::NSLOT];
     unsigned inr = 0;
 #pragma unroll
     for (int m = 0; m < G::NSLOT; ++m) {
         const int e = tid + m * KT_THREADS, hy = e / HX, hx = e - hy * HX;
         const int X = x0 - P + hx, Y = y0 - P + hy;
-        goff[m] = hy * (int)sy + hx;
-        if (e < G::HN && X >= 0 && X < n0 && Y >= 0 && Y < n1) inr |= 1u << m;
+        const bool in = e < G::HN && X >= 0 && X < n0 && Y >= 0 && Y < n1;
+        goff[m] = in ? (Y * (int)sy + X) : 0;  // plane-relative offset (a safe one when zero-filled)
+        if (in) inr |= 1u << m;
     }
-    const long org = (long)(y0 - P) * sy + (x0 - P);
     const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 8u * tid;
     auto issue = [&](int ii) {
         if (ii < npl) {
             const int kk = kk0 + ii;
-            double *bu = ring + (ii & (KT_NPF - 1)) * 2 * HNP, *bv = bu + HNP;
+            const unsigned su = ring_s + 8u * (unsigned)((ii & (KT_NPF - 1)) * 2 * HNP);
             const bool kv = kk >= 0 && kk < n2;
-            const long zo = (long)kk * sz + org;
+            const double *pu = a.U + (kv ? (long)kk * sz : 0), *pv = a.V + (kv ? (long)kk * sz : 0);
 #pragma unroll
             for (int m = 0; m < G::NSLOT; ++m) {
-                const int e = tid + m * KT_THREADS;
-                if (e >= G::HN) continue;
-                if (kv && (inr >> m & 1)) {
-                    cp_async8(bu + e, a.U + zo + goff[m]);
-                    cp_async8(bv + e, a.V + zo + goff[m]);
-                } else {
-                    bu[e] = 0.0;
-                    bv[e] = 0.0;
-                }
+                if (m == G::NSLOT - 1 && tid + m * KT_THREADS >= G::HN) break;
+                const unsigned nb = (kv && (inr >> m & 1)) ? 8u : 0u;
+                cp_async8_zfill(su + 8u * m * KT_THREADS, pu + goff[m], nb);
+                cp_async8_zfill(su + 8u * (m * KT_THREADS + HNP), pv + goff[m], nb);
             }
         }
         cp_async_commit();
