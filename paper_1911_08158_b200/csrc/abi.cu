@@ -42,7 +42,8 @@ struct ads_ctx {
     int device = 0;
     long launches = 0;
     Geom geo;
-    long N = 0;
+    long N = 0;       // logical DOFs n0 n1 n2 (dense caller arrays)
+    long Nalloc = 0;  // device field length sz * n2 (rows padded to a multiple of 8 doubles)
     Space1D sp[3];
     LUFactors mass_lu[3];
     DirDev dd[3];
@@ -309,13 +310,16 @@ int init_state(ads_ctx *h) {
 
 int copy_in(ads_ctx *h, double *dst, const double *src, int mem) {
     cudaMemcpyKind k = mem == ADS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    CUDA_TRY(h, cudaMemcpyAsync(dst, src, sizeof(double) * h->N, k, h->stream));
+    // dense caller array -> pitched device field
+    CUDA_TRY(h, cudaMemcpy2DAsync(dst, sizeof(double) * h->geo.sy, src, sizeof(double) * h->n[0],
+                                  sizeof(double) * h->n[0], (size_t)h->n[1] * h->n[2], k, h->stream));
     return ADS_OK;
 }
 
 int copy_out(ads_ctx *h, double *dst, const double *src, int mem) {
     cudaMemcpyKind k = mem == ADS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    CUDA_TRY(h, cudaMemcpyAsync(dst, src, sizeof(double) * h->N, k, h->stream));
+    CUDA_TRY(h, cudaMemcpy2DAsync(dst, sizeof(double) * h->n[0], src, sizeof(double) * h->geo.sy,
+                                  sizeof(double) * h->n[0], (size_t)h->n[1] * h->n[2], k, h->stream));
     return ADS_OK;
 }
 
@@ -348,10 +352,13 @@ int ads_create(ads_handle *out, int nx, int ny, int nz, int p, double tau, int b
         h->geo.n0 = h->n[0];
         h->geo.n1 = h->n[1];
         h->geo.n2 = h->n[2];
-        h->geo.sy = h->n[0];
-        h->geo.sz = (long)h->n[0] * h->n[1];
+        // rows padded to a multiple of 8 doubles: every 8-line tile row segment of the
+        // y/z sweeps is one aligned 64-byte block, x-sweep tiles start 64-byte aligned
+        h->geo.sy = (h->n[0] + 7) / 8 * 8;
+        h->geo.sz = h->geo.sy * h->n[1];
         h->N = (long)h->n[0] * h->n[1] * h->n[2];
-        size_t fb = sizeof(double) * h->N;
+        h->Nalloc = h->geo.sz * h->n[2];
+        size_t fb = sizeof(double) * h->Nalloc;
         if ((rc = dalloc(h, (void **)&h->U, fb)) == ADS_OK && (rc = dalloc(h, (void **)&h->U2, fb)) == ADS_OK &&
             (rc = dalloc(h, (void **)&h->V, fb)) == ADS_OK && (rc = dalloc(h, (void **)&h->A, fb)) == ADS_OK &&
             (rc = dalloc(h, (void **)&h->R, fb)) == ADS_OK && (rc = dalloc(h, (void **)&h->Wk, fb)) == ADS_OK &&
@@ -362,9 +369,7 @@ int ads_create(ads_handle *out, int nx, int ny, int nz, int p, double tau, int b
             h->own_stream = true;
         }
         if (rc == ADS_OK) {
-            cudaMemsetAsync(h->U, 0, fb, h->stream);
-            cudaMemsetAsync(h->V, 0, fb, h->stream);
-            cudaMemsetAsync(h->A, 0, fb, h->stream);
+            for (double *f : {h->U, h->U2, h->V, h->A, h->R, h->Wk}) cudaMemsetAsync(f, 0, fb, h->stream);
             if (cudaStreamSynchronize(h->stream) != cudaSuccess) rc = fail(h, ADS_E_CUDA, "memset failed");
         }
     }
@@ -449,7 +454,7 @@ int ads_set_state(ads_handle h, const double *u, const double *udot, int mem) {
     if (udot) {
         if ((rc = copy_in(h, h->V, udot, mem))) return rc;
     } else {
-        CUDA_TRY(h, cudaMemsetAsync(h->V, 0, sizeof(double) * h->N, h->stream));
+        CUDA_TRY(h, cudaMemsetAsync(h->V, 0, sizeof(double) * h->Nalloc, h->stream));
     }
     if (h->bc == ADS_BC_DIRICHLET0) {
         launch_mask_boundary(h->U, h->geo, h->stream);
@@ -466,8 +471,8 @@ int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const i
     if (rc) return rc;
     if (nterms < 0 || (nterms > 0 && (!amp || !sx || !sy || !sz)))
         return fail(h, ADS_E_INVAL, "ads_set_state_separable: bad argument");
-    CUDA_TRY(h, cudaMemsetAsync(h->U, 0, sizeof(double) * h->N, h->stream));
-    CUDA_TRY(h, cudaMemsetAsync(h->V, 0, sizeof(double) * h->N, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(h->U, 0, sizeof(double) * h->Nalloc, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(h->V, 0, sizeof(double) * h->Nalloc, h->stream));
     if (nterms > 0) {
         const int n0 = h->n[0], n1 = h->n[1], n2 = h->n[2];
         std::vector<double> packed((size_t)nterms * (n0 + n1 + n2));
@@ -518,7 +523,7 @@ int ads_energy(ads_handle h, double out[3]) {
     if (rc) return rc;
     if (!out) return fail(h, ADS_E_INVAL, "ads_energy: out is NULL");
     const Geom &g = h->geo;
-    const long N = h->N;
+    const long N = h->Nalloc;  // padding entries are 0 in every field
     double res[3];
     // v = V - tau/2 a ; kinetic = 1/2 v' M v
     CUDA_TRY(h, cudaMemcpyAsync(h->R, h->V, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->stream));
@@ -559,8 +564,8 @@ int ads_get_state(ads_handle h, double *u, double *udot, double *a, int mem) {
     if (mem != ADS_MEM_HOST && mem != ADS_MEM_DEVICE) return fail(h, ADS_E_INVAL, "bad mem");
     if (u && (rc = copy_out(h, u, h->U, mem))) return rc;
     if (udot) {
-        CUDA_TRY(h, cudaMemcpyAsync(h->Wk, h->V, sizeof(double) * h->N, cudaMemcpyDeviceToDevice, h->stream));
-        launch_axpby(h->N, -0.5 * h->tau, h->A, 1.0, h->Wk, h->stream);
+        CUDA_TRY(h, cudaMemcpyAsync(h->Wk, h->V, sizeof(double) * h->Nalloc, cudaMemcpyDeviceToDevice, h->stream));
+        launch_axpby(h->Nalloc, -0.5 * h->tau, h->A, 1.0, h->Wk, h->stream);
         if ((rc = check_launch(h, "axpby"))) return rc;
         if ((rc = copy_out(h, udot, h->Wk, mem))) return rc;
     }
@@ -581,27 +586,35 @@ int ads_dims(ads_handle h, int *nx, int *ny, int *nz, int *ncomp) {
     return ADS_OK;
 }
 
+// Unit operators act on dense caller device arrays: copy into a pitched work field,
+// run the kernels, copy back out.
 int ads_apply_k(ads_handle h, const double *x, double *out) {
     int rc = guard(h);
     if (rc) return rc;
     if (!x || !out || x == out) return fail(h, ADS_E_INVAL, "ads_apply_k: bad pointers");
-    return run_kop(h, x, x, 0.0, 0.0, 1.0, nullptr, out);
+    if ((rc = copy_in(h, h->U2, x, ADS_MEM_DEVICE))) return rc;
+    if ((rc = run_kop(h, h->U2, h->U2, 0.0, 0.0, 1.0, nullptr, h->R))) return rc;
+    return copy_out(h, out, h->R, ADS_MEM_DEVICE);
 }
 
 int ads_solve_d(ads_handle h, const double *x, double *out) {
     int rc = guard(h);
     if (rc) return rc;
     if (!x || !out) return fail(h, ADS_E_INVAL, "ads_solve_d: bad pointers");
-    if ((rc = run_sweep(h, 0, x, h->Wk, nullptr, 0.0))) return rc;
+    if ((rc = copy_in(h, h->R, x, ADS_MEM_DEVICE))) return rc;
+    if ((rc = run_sweep(h, 0, h->R, h->Wk, nullptr, 0.0))) return rc;
     if ((rc = run_sweep(h, 1, h->Wk, h->R, nullptr, 0.0))) return rc;
-    return run_sweep(h, 2, h->R, out, nullptr, 0.0);
+    if ((rc = run_sweep(h, 2, h->R, h->Wk, nullptr, 0.0))) return rc;
+    return copy_out(h, out, h->Wk, ADS_MEM_DEVICE);
 }
 
 int ads_sweep(ads_handle h, int d, const double *x, double *out) {
     int rc = guard(h);
     if (rc) return rc;
     if (!x || !out || d < 0 || d > 2) return fail(h, ADS_E_INVAL, "ads_sweep: bad argument");
-    return run_sweep(h, d, x, out, nullptr, 0.0);
+    if ((rc = copy_in(h, h->R, x, ADS_MEM_DEVICE))) return rc;
+    if ((rc = run_sweep(h, d, h->R, h->Wk, nullptr, 0.0))) return rc;
+    return copy_out(h, out, h->Wk, ADS_MEM_DEVICE);
 }
 
 long ads_launch_count(ads_handle h) { return h ? h->launches : -1; }

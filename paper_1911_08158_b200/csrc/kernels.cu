@@ -54,8 +54,12 @@ namespace ads {
 // memory; tile pitch np = 2 (mod 16) keeps the per-thread chunk reads
 // conflict-free.  The z sweep fuses the kick V += tau a into its store.
 // ------------------------------------------------------------------------------------------
-constexpr int SW_LW = 8, SW_WARPS = 8, SW_THREADS = 32 * SW_WARPS, SW_G = 32 / SW_LW;
-static_assert(SW_WARPS * SW_G == kSweepChunks, "one chunk per (warp, lane group)");
+// LW lines per tile (x: 8, y/z: 16); 32/LW chunks per warp; kSweepChunks LW threads
+template <int LW>
+struct SW {
+    static constexpr int G = 32 / LW, WARPS = kSweepChunks / G, THREADS = 32 * WARPS;
+    static_assert(WARPS * G == kSweepChunks, "one chunk per (warp, lane group)");
+};
 
 __host__ __device__ constexpr int ring(int i, int P) { return ((i % P) + P) % P; }
 template <int P> struct Rec {
@@ -124,7 +128,7 @@ __device__ __forceinline__ void bwd_pass(double (&v)[L], double (&h)[P], const C
 // incoming state of chunk c: Horner over chunks c-K .. c-1 (FWD) or c+K .. c+1
 // (backward).  UNIW: every chunk of the window is uniform -> maps from the
 // constant bank (Tf(a,b) = Gf[L-1-a][b], Rb(a,b) = Gb[a][b]).
-template <int P, int L, bool FWD, bool UNIW>
+template <int P, int L, int LW, bool FWD, bool UNIW>
 __device__ __forceinline__ void chunk_walk(double (&in)[P], const SolveTab &t, const double *shT, const double *shh,
                                            int c, int K, int q) {
 #pragma unroll
@@ -134,7 +138,7 @@ __device__ __forceinline__ void chunk_walk(double (&in)[P], const SolveTab &t, c
         double nin[P];
 #pragma unroll
         for (int a = 0; a < P; ++a) {
-            double acc = shh[(cc * P + a) * SW_LW + q];
+            double acc = shh[(cc * P + a) * LW + q];
 #pragma unroll
             for (int b = 0; b < P; ++b) {
                 const double T = UNIW ? (FWD ? t.Gf[L - 1 - a][b] : t.Gb[a][b]) : shT[(cc * P + a) * P + b];
@@ -154,7 +158,7 @@ struct SweepSmem {
 
 // The whole per-tile solve of one thread's chunk.  after_sync runs right after the
 // first barrier (every thread has consumed its tile input by then).
-template <int P, int L, bool UNI, class AfterSync>
+template <int P, int L, int LW, bool UNI, class AfterSync>
 __device__ __forceinline__ void solve_chunk(double (&v)[L], const SolveTab &t, const SweepSmem &sm, int c, int q,
                                             bool walk_uf, bool walk_ub, const double *recf, const double *recb,
                                             AfterSync after_sync) {
@@ -162,11 +166,11 @@ __device__ __forceinline__ void solve_chunk(double (&v)[L], const SolveTab &t, c
     double h[P], in[P];
     fwd_pass<P, L, UNI, true>(v, h, cf);
 #pragma unroll
-    for (int m = 0; m < P; ++m) sm.shf[(c * P + m) * SW_LW + q] = h[m];
+    for (int m = 0; m < P; ++m) sm.shf[(c * P + m) * LW + q] = h[m];
     __syncthreads();
     after_sync();
-    if (walk_uf) chunk_walk<P, L, true, true>(in, t, sm.shTf, sm.shf, c, t.Kf, q);
-    else chunk_walk<P, L, true, false>(in, t, sm.shTf, sm.shf, c, t.Kf, q);
+    if (walk_uf) chunk_walk<P, L, LW, true, true>(in, t, sm.shTf, sm.shf, c, t.Kf, q);
+    else chunk_walk<P, L, LW, true, false>(in, t, sm.shTf, sm.shf, c, t.Kf, q);
     if (UNI) {
 #pragma unroll
         for (int j = 0; j < L; ++j)
@@ -177,10 +181,10 @@ __device__ __forceinline__ void solve_chunk(double (&v)[L], const SolveTab &t, c
     }
     bwd_pass<P, L, UNI, true>(v, h, cf);
 #pragma unroll
-    for (int m = 0; m < P; ++m) sm.shb[(c * P + m) * SW_LW + q] = h[m];
+    for (int m = 0; m < P; ++m) sm.shb[(c * P + m) * LW + q] = h[m];
     __syncthreads();
-    if (walk_ub) chunk_walk<P, L, false, true>(in, t, sm.shRb, sm.shb, c, t.Kb, q);
-    else chunk_walk<P, L, false, false>(in, t, sm.shRb, sm.shb, c, t.Kb, q);
+    if (walk_ub) chunk_walk<P, L, LW, false, true>(in, t, sm.shRb, sm.shb, c, t.Kb, q);
+    else chunk_walk<P, L, LW, false, false>(in, t, sm.shRb, sm.shb, c, t.Kb, q);
     if (UNI) {
 #pragma unroll
         for (int j = 0; j < L; ++j)
@@ -197,6 +201,10 @@ __device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async16(double *sdst, const double *gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
 // shared address + zero fill: copies nbytes (0 or 8) and fills the rest of the 8 bytes with 0
 __device__ __forceinline__ void cp_async8_zfill(unsigned sdst, const double *gsrc, unsigned nbytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(nbytes) : "memory");
@@ -205,22 +213,23 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// x-tile pitch: >= n and = 2 (mod 16) (conflict-free chunk reads, see above)
-__host__ __device__ inline int xtile_pitch(int n) { return n + ((2 - n) % 16 + 16) % 16; }
+// x-tile pitch: >= the row pitch sy and = 2 (mod 16) (conflict-free chunk reads, see above)
+__host__ __device__ inline int xtile_pitch(int sy) { return sy + ((2 - sy) % 16 + 16) % 16; }
 
 // edge rows: [0, c_lo L) and [c_hi L, C L), plus one block of L uniform rows
 __host__ __device__ inline int sweep_edge_rows(const SolveTab &t) {
     return t.c_lo * t.L + (kSweepChunks - t.c_hi) * t.L + t.L;
 }
-template <int P>
-__host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir) {
-    const long fixed = 2L * kSweepChunks * P * P + 2L * kSweepChunks * P * SW_LW +
+template <int P, int LW>
+__host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir, long sy) {
+    const long fixed = 2L * kSweepChunks * P * P + 2L * kSweepChunks * P * LW +
                        (long)sweep_edge_rows(t) * (Rec<P>::FW + Rec<P>::BW);
-    return fixed + (xdir ? 2L * SW_LW * xtile_pitch(t.n) : (long)kSweepChunks * t.L * SW_LW);
+    return fixed + (xdir ? 2L * LW * xtile_pitch((int)sy) : 2L * kSweepChunks * t.L * LW);
 }
 
-template <int P, int L, bool XDIR>
-__global__ void __launch_bounds__(SW_THREADS, 2) sweep_kernel(const SweepArgs a) {
+template <int P, int L, bool XDIR, int LW>
+__global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_kernel(const SweepArgs a) {
+    constexpr int SW_LW = LW, SW_G = SW<LW>::G, SW_THREADS = SW<LW>::THREADS;
     extern __shared__ __align__(16) double smem[];
     constexpr int C = kSweepChunks, FW = Rec<P>::FW, BW = Rec<P>::BW;
     const SolveTab &t = a.t;
@@ -257,29 +266,34 @@ __global__ void __launch_bounds__(SW_THREADS, 2) sweep_kernel(const SweepArgs a)
     const SweepSmem sm{shTf, shRb, ef, eb, shf, shb};
     const Geom &g = a.geo;
     auto solve = [&](double (&v)[L], auto after) {
-        if (uni) solve_chunk<P, L, true>(v, t, sm, c, q, walk_uf, walk_ub, recf, recb, after);
-        else solve_chunk<P, L, false>(v, t, sm, c, q, false, false, recf, recb, after);
+        if (uni) solve_chunk<P, L, LW, true>(v, t, sm, c, q, walk_uf, walk_ub, recf, recb, after);
+        else solve_chunk<P, L, LW, false>(v, t, sm, c, q, false, false, recf, recb, after);
     };
 
     if (XDIR) {
-        // x lines are contiguous (sy = n0, sz = n0 n1): a tile of SW_LW consecutive lines of
-        // the flattened (j, k) order is one contiguous block of nl * n doubles
-        const int np = xtile_pitch(n);
+        // x lines: the flattened (j, k) line index l has base l * sy (sz = n1 sy), so a tile of
+        // SW_LW consecutive lines is one contiguous block of nl * sy doubles; sy is a multiple of
+        // 8, so the block is 64-byte aligned and moves in 16-byte copies
+        const int sy = (int)g.sy, nc2 = sy / 2;  // 16-byte columns per line
+        const int np = xtile_pitch(sy);
         double *xin = buf, *xout = buf + SW_LW * np;
         const long nlines = (long)g.n1 * g.n2;
         const long ntiles = (nlines + SW_LW - 1) / SW_LW;
+        // thread tid moves 16-byte columns e = tid + 256 m of the flattened [nl][sy/2] block
+        const int li0 = tid / nc2, c20 = tid - li0 * nc2;
         auto prefetch = [&](long tile) {
             if (tile >= ntiles) return;
             const long l0 = tile * SW_LW;
-            const int tot = (int)min((long)SW_LW, nlines - l0) * n;
-            const double *src = a.in + l0 * n;
-            int line = tid / n, col = tid - line * n;
+            const int tot = (int)min((long)SW_LW, nlines - l0) * nc2;
+            const double *src = a.in + l0 * sy;
+            int li = li0, c2 = c20;
             for (int e = tid; e < tot; e += SW_THREADS) {
-                cp_async8(xin + line * np + col, src + e);
-                col += SW_THREADS;
-                while (col >= n) { col -= n; ++line; }
+                cp_async16(xin + li * np + 2 * c2, src + 2 * e);
+                c2 += SW_THREADS;
+                while (c2 >= nc2) { c2 -= nc2; ++li; }
             }
         };
+        for (int e = tid; e < SW_LW * np; e += SW_THREADS) xout[e] = 0.0;  // row padding stays 0
         __syncthreads();
         prefetch(blockIdx.x);
         cp_async_commit();
@@ -299,13 +313,13 @@ __global__ void __launch_bounds__(SW_THREADS, 2) sweep_kernel(const SweepArgs a)
             for (int j = 0; j < L; ++j)
                 if (s + j < n) xout[q * np + s + j] = v[j];
             __syncthreads();
-            double *dst = a.out + l0 * n;
-            const int tot = nl * n;
-            int line = tid / n, col = tid - line * n;
+            double2 *dst = reinterpret_cast<double2 *>(a.out + l0 * sy);
+            const int tot = nl * nc2;
+            int li = li0, c2 = c20;
             for (int e = tid; e < tot; e += SW_THREADS) {
-                dst[e] = xout[line * np + col];
-                col += SW_THREADS;
-                while (col >= n) { col -= n; ++line; }
+                dst[e] = *reinterpret_cast<const double2 *>(xout + li * np + 2 * c2);
+                c2 += SW_THREADS;
+                while (c2 >= nc2) { c2 -= nc2; ++li; }
             }
         }
     } else {
@@ -319,11 +333,11 @@ __global__ void __launch_bounds__(SW_THREADS, 2) sweep_kernel(const SweepArgs a)
         const long ntiles = (long)nib * nb;
         const bool kick = a.mode != 0;
         const int nv = max(0, min(L, n - s));  // rows of my chunk inside the line
-        double *ib = buf + s * SW_LW + q;
-        auto fetch = [&](long tile) {
+        double *ib = buf + s * SW_LW + q, *vb = ib + C * L * SW_LW;
+        auto fetch = [&](double *ib, const double *field, long tile) {
             if (tile >= ntiles) return;
             const int i = (int)(tile % nib) * SW_LW + q;
-            const double *src = a.in + (tile / nib) * sb + i + (long)s * sl;
+            const double *src = field + (tile / nib) * sb + i + (long)s * sl;
             const bool lv = i < g.n0;
 #pragma unroll
             for (int j = 0; j < L; ++j) {
@@ -333,26 +347,20 @@ __global__ void __launch_bounds__(SW_THREADS, 2) sweep_kernel(const SweepArgs a)
             }
         };
         __syncthreads();
-        fetch(blockIdx.x);
+        fetch(ib, a.in, blockIdx.x);
         cp_async_commit();
         for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int i = (int)(tile % nib) * SW_LW + q;
             const long base = (tile / nib) * sb + i + (long)s * sl;
             const int nvl = i < g.n0 ? nv : 0;
             cp_async_wait<0>();
-            double v[L], vk[L];
+            double v[L];
 #pragma unroll
             for (int j = 0; j < L; ++j) v[j] = ib[j * SW_LW];
-            fetch(tile + gridDim.x);  // next tile streams in during the solve
+            if (kick) fetch(vb, a.V, tile);  // this tile's V (consumed after the solve)
             cp_async_commit();
-            if (kick) {
-                const double *pv = a.V + base;
-#pragma unroll
-                for (int j = 0; j < L; ++j) {
-                    vk[j] = j < nvl ? *pv : 0.0;
-                    pv += sl;
-                }
-            }
+            fetch(ib, a.in, tile + gridDim.x);  // next tile streams in during the solve
+            cp_async_commit();
             solve(v, [] {});
             double *po = a.out ? a.out + base : nullptr;
             if (!kick) {
@@ -362,11 +370,12 @@ __global__ void __launch_bounds__(SW_THREADS, 2) sweep_kernel(const SweepArgs a)
                     po += sl;
                 }
             } else {
+                cp_async_wait<1>();  // V of this tile has landed (the next input may still fly)
                 double *pv = a.V + base;
 #pragma unroll
                 for (int j = 0; j < L; ++j) {
                     if (j < nvl) {
-                        *pv = fma(a.kick, v[j], vk[j]);
+                        *pv = fma(a.kick, v[j], vb[j * SW_LW]);
                         if (po) po[(long)j * sl] = v[j];
                     }
                     pv += sl;
@@ -752,8 +761,10 @@ int launch_kop(int p, const KopArgs &a, cudaStream_t s) {
 
 template <int P, int L, bool X>
 static void sweep_launch(const SweepArgs &a, cudaStream_t s) {
+    constexpr int LW = X ? 8 : 16;
+    constexpr int NT = SW<LW>::THREADS;
     const Geom &g = a.geo;
-    const size_t sm = sizeof(double) * (size_t)sweep_smem_doubles<P>(a.t, X);
+    const size_t sm = sizeof(double) * (size_t)sweep_smem_doubles<P, LW>(a.t, X, a.geo.sy);
     static int nsm = 0;
     static size_t sm_set = 0;
     if (!nsm) {
@@ -762,17 +773,17 @@ static void sweep_launch(const SweepArgs &a, cudaStream_t s) {
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     if (sm > sm_set) {
-        cudaFuncSetAttribute(sweep_kernel<P, L, X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(sweep_kernel<P, L, X, LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         sm_set = sm;
     }
     long ntiles;
-    if (X) ntiles = ((long)g.n1 * g.n2 + SW_LW - 1) / SW_LW;
-    else ntiles = (long)((g.n0 + SW_LW - 1) / SW_LW) * (a.dir == 1 ? g.n2 : g.n1);
+    if (X) ntiles = ((long)g.n1 * g.n2 + LW - 1) / LW;
+    else ntiles = (long)((g.n0 + LW - 1) / LW) * (a.dir == 1 ? g.n2 : g.n1);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<P, L, X>, SW_THREADS, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<P, L, X, LW>, NT, sm);
     const long cap = (long)std::max(per_sm, 1) * nsm;
     dim3 grd((unsigned)std::min(ntiles, cap));
-    sweep_kernel<P, L, X><<<grd, SW_THREADS, sm, s>>>(a);
+    sweep_kernel<P, L, X, LW><<<grd, NT, sm, s>>>(a);
 }
 
 template <int P, int LV>
@@ -789,7 +800,7 @@ static int sweep_launch_L(const SweepArgs &a, cudaStream_t s) {
 template <int P>
 static int sweep_dispatch(const SweepArgs &a, cudaStream_t s) {
     if (a.dir == 0 && a.mode != 0) return -1;  // the kick is fused into y/z sweeps only
-    if (a.dir == 0 && (a.geo.sy != a.geo.n0 || a.geo.sz != (long)a.geo.n0 * a.geo.n1)) return -1;  // dense x lines
+    if (a.dir == 0 && (a.geo.sy % 2 != 0 || a.geo.sz != a.geo.sy * a.geo.n1)) return -1;  // even pitch, packed planes
     switch (a.t.L) {
         case 1: return sweep_launch_L<P, 1>(a, s);
         case 3: return sweep_launch_L<P, 3>(a, s);
