@@ -120,6 +120,13 @@ int build_space(int p, int nel, int bc, Space1D &s) {
                 rk[k + p] = s.K.at(mid, mid + k);
                 rb[k + p] = s.B.at(mid, mid + k);
             }
+            // M and K are symmetric; make the Toeplitz row bitwise symmetric too (the
+            // quadrature sums of row entries +k and -k differ by rounding only), so
+            // kernels may use pair sums with p+1 distinct coefficients.
+            for (int k = 1; k <= p; ++k) {
+                rm[p + k] = rm[p - k] = 0.5 * (rm[p + k] + rm[p - k]);
+                rk[p + k] = rk[p - k] = 0.5 * (rk[p + k] + rk[p - k]);
+            }
             for (int i = lo; i <= hi; ++i)
                 for (int k = -p; k <= p; ++k) {
                     s.M.at(i, i + k) = rm[k + p];

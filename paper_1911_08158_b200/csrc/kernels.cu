@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
 }
 
 // ------------------------------------------------------------------------------------------
-// fused drift + source + K-apply (v2)
+// fused drift + source + K-apply (v3)
 //
 //   P = U + tau V (written to Pout),  r = g (bx (x) by (x) bz) + sign K P,
 //   K = Kx My Mz + Mx Ky Mz + Mx My Kz   (Eq. 14, 3D)
@@ -394,31 +394,37 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
 // T = Mx Y1; z-pass K P = Mz S + Kz T  (7 banded passes).
 //
 // CTA = 256 threads on a KT_X x KT_Y = 32 x 16 output tile, marching along z over
-// [z0, z1).  Per input plane kk:
-//   - the raw U, V plane of the haloed tile ((32+2p) x (16+2p)) streams HBM -> shared
-//     memory with cp.async, KT_NPF-1 planes ahead (ring of KT_NPF buffers);
-//   - y-pass: thread (column, group of 4 rows) forms P on 4+2p rows from the raw
-//     values, writes the owned P to HBM, and Y1/Y2 of its 4 rows to shared memory;
-//   - x-pass: lane = x, warp = 2 rows: S, T from 2p+1 neighbouring (Y1, Y2);
-//   - z-pass: S, T of the last 2p+1 planes stay in registers (the plane loop is
-//     unrolled 2p+1 times so the ring never moves); output plane kk - p gets
-//     r = src + sign (Mz S + Kz T).
-// Band rows inside the Toeplitz interior come from the kernel's constant bank
-// (tile-/plane-uniform branches); boundary tiles read staged rows from shared memory.
-// HBM traffic: U, V read once (the halo is re-read from L2), P and r written once.
+// [z0, z1).  Per input plane kk (two barriers):
+//   - copy warps stream the raw U, V plane of the haloed tile HBM -> shared memory in
+//     16-byte cp.async pieces (the x halo is rounded up to an even width so every piece
+//     is aligned; out-of-domain pieces are zero-filled by the copy), KT_NPF-1 planes ahead;
+//   - y-pass warps: item (column, 4 rows) forms P = U + tau V on 4+2p rows, writes the
+//     owned P to HBM and Y1/Y2 of its 4 rows to shared memory;
+//   - x-pass, all warps: lane = x, warp = 2 rows: S, T from 2p+1 neighbouring (Y1, Y2);
+//   - z-pass: input plane kk adds Mz(k,kk) S + Kz(k,kk) T to the 2p+1 pending output
+//     planes k = kk-p..kk+p held in registers; output kk-p is complete and stored.
+// Interior tiles/planes (Toeplitz rows, symmetric after host_setup build_space) use the
+// constant-bank rows in pair-sum form (p+1 distinct coefficients per band); boundary
+// tiles read staged rows from shared memory, boundary planes from global memory.
+// HBM traffic: U, V read once (halos re-read from L2), P and r written once.
 // ------------------------------------------------------------------------------------------
 constexpr int KT_X = 32, KT_Y = 16, KT_THREADS = 256, KT_NPF = 4, KT_RY = 4;
 template <int P>
 struct KopGeo {
-    static constexpr int W = 2 * P + 1, HX = KT_X + 2 * P, HY = KT_Y + 2 * P, HN = HX * HY;
-    static constexpr int HNP = (HN + 1) & ~1;
-    static constexpr int NSLOT = (HN + KT_THREADS - 1) / KT_THREADS;
-    static constexpr int NITEM = HX * (KT_Y / KT_RY);
-    // shared memory (doubles): raw ring | Y tile (double2) | x rows | y rows
-    static constexpr int RING = KT_NPF * 2 * HNP, YT = KT_Y * HX * 2, XB = KT_X * 2 * W, YB = KT_Y * 2 * W;
+    static constexpr int W = 2 * P + 1;
+    static constexpr int PA = (P + 1) & ~1;               // even x halo of the copied tile
+    static constexpr int HX = KT_X + 2 * PA, HY = KT_Y + 2 * P, HN = HX * HY;
+    static constexpr int NC = KT_X + 2 * P;               // columns the x-pass needs
+    static constexpr int NITEM = NC * (KT_Y / KT_RY);     // y-pass items
+    static constexpr int YW = (NITEM + 31) / 32;          // y-pass warps
+    static constexpr int NCT = KT_THREADS - 32 * YW;      // copy threads
+    static constexpr int NPAIR = HN / 2;                  // 16-byte pieces per field and plane
+    static constexpr int NSLOT = (NPAIR + NCT - 1) / NCT;
+    // shared memory (doubles): raw ring [NPF][U|V][HY][HX] | Y tile [KT_Y][NC] double2 | rows
+    static constexpr int RING = KT_NPF * 2 * HN, YT = KT_Y * NC * 2, XB = KT_X * 2 * W, YB = KT_Y * 2 * W;
     static constexpr int SMEM = RING + YT + XB + YB;
+    static_assert(NCT >= 32, "at least one copy warp");
 };
-static_assert(KopGeo<5>::NITEM <= KT_THREADS, "one y-pass item per thread");
 
 // z-pass scatter of one input plane kk (ring slot U = (kk - kk0) mod W, see kop_tile)
 template <int P, int U>
@@ -429,11 +435,11 @@ __device__ __forceinline__ void kop_zscatter(const KopArgs &a, double (&A0)[2 * 
     if (zint) {
 #pragma unroll
         for (int c = 0; c < W; ++c) {
-            const int sl = ((U - P + c) % W + W) % W;
-            A0[sl] = fma(a.mc[2][2 * P - c], s0, A0[sl]);
-            A0[sl] = fma(a.kc[2][2 * P - c], t0, A0[sl]);
-            A1[sl] = fma(a.mc[2][2 * P - c], s1, A1[sl]);
-            A1[sl] = fma(a.kc[2][2 * P - c], t1, A1[sl]);
+            const int sl = ((U - P + c) % W + W) % W, d = c < P ? P - c : c - P;
+            A0[sl] = fma(a.mc[2][P + d], s0, A0[sl]);
+            A0[sl] = fma(a.kc[2][P + d], t0, A0[sl]);
+            A1[sl] = fma(a.mc[2][P + d], s1, A1[sl]);
+            A1[sl] = fma(a.kc[2][P + d], t1, A1[sl]);
         }
     } else {
         const int n2 = a.geo.n2;
@@ -464,10 +470,14 @@ __device__ __forceinline__ void kop_zscatter(const KopArgs &a, double (&A0)[2 * 
     A1[so] = 0.0;
 }
 
-template <int P, bool XI, bool YI>
+__device__ __forceinline__ void cp_async16_zfill(unsigned sdst, const double *gsrc, unsigned nbytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(nbytes) : "memory");
+}
+
+template <int P, bool INT>
 __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0, int y0, int z0, int z1) {
     using G = KopGeo<P>;
-    constexpr int W = G::W, HX = G::HX, HNP = G::HNP;
+    constexpr int W = G::W, HX = G::HX, HN = G::HN, NC = G::NC, PA = G::PA;
     double *ring = smem;
     double2 *Ys = reinterpret_cast<double2 *>(smem + G::RING);
     double *xb = smem + G::RING + G::YT;  // [KT_X][2][W]: (Mx, Kx) rows of x0 + lane
@@ -476,63 +486,63 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
     const int n0 = a.geo.n0, n1 = a.geo.n1, n2 = a.geo.n2;
     const long sy = a.geo.sy, sz = a.geo.sz;
 
-    // stage boundary band rows (zero outside the domain)
-    if (!XI)
+    if (!INT) {  // stage boundary band rows (zero outside the domain)
         for (int e = tid; e < KT_X * 2 * W; e += KT_THREADS) {
             const int xr = e / (2 * W), m = (e / W) & 1, c = e % W, X = x0 + xr;
             xb[e] = X < n0 ? __ldg((m ? a.kx : a.mx) + (long)X * W + c) : 0.0;
         }
-    if (!YI)
         for (int e = tid; e < KT_Y * 2 * W; e += KT_THREADS) {
             const int yr = e / (2 * W), m = (e / W) & 1, c = e % W, Y = y0 + yr;
             yb[e] = Y < n1 ? __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
         }
+    }
 
-    // load slots of the haloed plane (fixed per thread): element e = tid + 256 m of the
-    // [HY][HX] tile.  Out-of-domain elements are zero-filled by the copy itself
-    // (cp.async src-size 0), so every slot issues exactly one copy per field and plane.
+    // ---- copy threads: 16-byte pieces e = ct + NCT m of the [HY][HX/2] plane (fixed per thread)
+    const bool copier = tid >= 32 * G::YW;
+    const int ct = tid - 32 * G::YW;
     int goff[G::NSLOT];
     unsigned inr = 0;
 #pragma unroll
     for (int m = 0; m < G::NSLOT; ++m) {
-        const int e = tid + m * KT_THREADS, hy = e / HX, hx = e - hy * HX;
-        const int X = x0 - P + hx, Y = y0 - P + hy;
-        const bool in = e < G::HN && X >= 0 && X < n0 && Y >= 0 && Y < n1;
-        goff[m] = in ? (Y * (int)sy + X) : 0;  // plane-relative offset (a safe one when zero-filled)
+        const int e = ct + m * G::NCT, hy = e / (HX / 2), hx = 2 * (e - hy * (HX / 2));
+        const int X = x0 - PA + hx, Y = y0 - P + hy;
+        const bool in = copier && e < G::NPAIR && X >= 0 && X < n0 && Y >= 0 && Y < n1;
+        goff[m] = in ? (Y * (int)sy + X) : 0;
         if (in) inr |= 1u << m;
     }
     const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;
-    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 8u * tid;
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * (ct > 0 ? ct : 0);
     auto issue = [&](int ii) {
-        if (ii < npl) {
+        if (copier && ii < npl) {
             const int kk = kk0 + ii;
-            const unsigned su = ring_s + 8u * (unsigned)((ii & (KT_NPF - 1)) * 2 * HNP);
+            const unsigned su = ring_s + 8u * (unsigned)((ii & (KT_NPF - 1)) * 2 * HN);
             const bool kv = kk >= 0 && kk < n2;
             const double *pu = a.U + (kv ? (long)kk * sz : 0), *pv = a.V + (kv ? (long)kk * sz : 0);
 #pragma unroll
             for (int m = 0; m < G::NSLOT; ++m) {
-                if (m == G::NSLOT - 1 && tid + m * KT_THREADS >= G::HN) break;
-                const unsigned nb = (kv && (inr >> m & 1)) ? 8u : 0u;
-                cp_async8_zfill(su + 8u * m * KT_THREADS, pu + goff[m], nb);
-                cp_async8_zfill(su + 8u * (m * KT_THREADS + HNP), pv + goff[m], nb);
+                if (ct + m * G::NCT >= G::NPAIR) break;
+                const unsigned nb = (kv && (inr >> m & 1)) ? 16u : 0u;
+                cp_async16_zfill(su + 16u * m * G::NCT, pu + goff[m], nb);
+                cp_async16_zfill(su + 16u * m * G::NCT + 8u * HN, pv + goff[m], nb);
             }
         }
         cp_async_commit();
     };
 
-    // y-pass item: column col of the haloed tile, output rows 4 grp .. 4 grp + 3
+    // ---- y-pass item: needed column nc (haloed column PA - P + nc), output rows 4 grp .. 4 grp + 3
     const bool yitem = tid < G::NITEM;
-    const int col = tid % HX, grp = tid / HX;
-    const int Xc = x0 - P + col;
-    const bool pown = yitem && col >= P && col < P + KT_X && Xc < n0;
-    // x-pass outputs: X = x0 + lane, rows 2w, 2w+1
+    const int nc = tid % NC, grp = tid / NC, hcol = PA - P + nc;
+    const int Xc = x0 - P + nc;
+    const bool pown = yitem && nc >= P && nc < P + KT_X && Xc < n0;
+    // ---- x-pass outputs: X = x0 + lane, rows 2w, 2w+1
     const int X = x0 + lane;
     const int Yo0 = y0 + 2 * w;
     const bool own0 = X < n0 && Yo0 < n1, own1 = X < n0 && Yo0 + 1 < n1;
     const double sxy0 = (a.bx && own0) ? __ldg(a.bx + X) * __ldg(a.by + Yo0) : 0.0;
     const double sxy1 = (a.bx && own1) ? __ldg(a.bx + X) * __ldg(a.by + Yo0 + 1) : 0.0;
+    const long oxy = (long)Yo0 * sy + X;
 
-    // pending outputs: A0/A1[(k - kk0) mod W] accumulates plane k = kk - P + c of rows 2w, 2w+1
+    // pending outputs: A0/A1[(k - kk0) mod W] accumulates plane k of rows 2w, 2w+1
     double A0[W], A1[W];
 #pragma unroll
     for (int c = 0; c < W; ++c) A0[c] = A1[c] = 0.0;
@@ -542,73 +552,98 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
     __syncthreads();  // staged band rows visible
 
     for (int ii = 0; ii < npl; ++ii) {
-        {
-            {
-                const int kk = kk0 + ii;
-                cp_async_wait<KT_NPF - 2>();
-                __syncthreads();  // plane kk landed in every thread's slots; Ys free
-                issue(ii + KT_NPF - 1);
-                // ---- y-pass
-                if (yitem) {
-                    const double *bu = ring + (ii & (KT_NPF - 1)) * 2 * HNP, *bv = bu + HNP;
-                    double pr[KT_RY + 2 * P];
+        const int kk = kk0 + ii;
+        cp_async_wait<KT_NPF - 2>();
+        __syncthreads();  // plane kk landed in every copier's pieces; Ys free
+        issue(ii + KT_NPF - 1);
+        // ---- y-pass
+        if (yitem) {
+            const double *bu = ring + (ii & (KT_NPF - 1)) * 2 * HN, *bv = bu + HN;
+            double pr[KT_RY + 2 * P];
 #pragma unroll
-                    for (int r = 0; r < KT_RY + 2 * P; ++r) {
-                        const int e = (KT_RY * grp + r) * HX + col;
-                        pr[r] = fma(a.tau, bv[e], bu[e]);
-                    }
-                    if (a.Pout && pown && kk >= z0 && kk < z1) {
+            for (int r = 0; r < KT_RY + 2 * P; ++r) {
+                const int e = (KT_RY * grp + r) * HX + hcol;
+                pr[r] = fma(a.tau, bv[e], bu[e]);
+            }
+            if (a.Pout && pown && kk >= z0 && kk < z1) {
 #pragma unroll
-                        for (int r = 0; r < KT_RY; ++r) {
-                            const int Y = y0 + KT_RY * grp + r;
-                            if (Y < n1) a.Pout[(long)kk * sz + (long)Y * sy + Xc] = pr[r + P];
-                        }
-                    }
-#pragma unroll
-                    for (int r = 0; r < KT_RY; ++r) {
-                        const int yr = KT_RY * grp + r;
-                        double y1 = 0.0, y2 = 0.0;
-#pragma unroll
-                        for (int c = 0; c < W; ++c) {
-                            const double m_ = YI ? a.mc[1][c] : yb[(yr * 2 + 0) * W + c];
-                            const double k_ = YI ? a.kc[1][c] : yb[(yr * 2 + 1) * W + c];
-                            y1 = fma(m_, pr[r + c], y1);
-                            y2 = fma(k_, pr[r + c], y2);
-                        }
-                        Ys[yr * HX + col] = make_double2(y1, y2);
-                    }
-                }
-                __syncthreads();  // Ys complete
-                // ---- x-pass
-                double s0 = 0.0, t0 = 0.0, s1 = 0.0, t1 = 0.0;
-#pragma unroll
-                for (int c = 0; c < W; ++c) {
-                    const double mx_ = XI ? a.mc[0][c] : xb[(lane * 2 + 0) * W + c];
-                    const double kx_ = XI ? a.kc[0][c] : xb[(lane * 2 + 1) * W + c];
-                    const double2 q0 = Ys[(2 * w) * HX + lane + c];
-                    const double2 q1 = Ys[(2 * w + 1) * HX + lane + c];
-                    s0 = fma(kx_, q0.x, s0);
-                    s0 = fma(mx_, q0.y, s0);
-                    t0 = fma(mx_, q0.x, t0);
-                    s1 = fma(kx_, q1.x, s1);
-                    s1 = fma(mx_, q1.y, s1);
-                    t1 = fma(mx_, q1.x, t1);
-                }
-                // ---- z-pass, scatter form: input plane kk feeds outputs k = kk - P + c (c = 0..2P)
-                // with Mz(k, kk) = mz[k][2P - c]; output kk - P is then complete.  The ring slot
-                // of output k is (k - kk0) mod W; a switch makes every slot index compile-time.
-                const bool zint = kk - P >= a.ilo[2] && kk + P <= a.ihi[2];
-                switch (ii % W) {
-#define ADS_ZCASE(U)                                                                                  \
-    case U:                                                                                           \
-        if constexpr (U < W) kop_zscatter<P, U>(a, A0, A1, s0, t0, s1, t1, kk, zint, z0, own0, own1, \
-                                                 sxy0, sxy1, (long)Yo0 * sy + X);                     \
-        break;
-                    ADS_ZCASE(0) ADS_ZCASE(1) ADS_ZCASE(2) ADS_ZCASE(3) ADS_ZCASE(4) ADS_ZCASE(5)
-                    ADS_ZCASE(6) ADS_ZCASE(7) ADS_ZCASE(8) ADS_ZCASE(9) ADS_ZCASE(10)
-#undef ADS_ZCASE
+                for (int r = 0; r < KT_RY; ++r) {
+                    const int Y = y0 + KT_RY * grp + r;
+                    if (Y < n1) a.Pout[(long)kk * sz + (long)Y * sy + Xc] = pr[r + P];
                 }
             }
+#pragma unroll
+            for (int r = 0; r < KT_RY; ++r) {
+                const int yr = KT_RY * grp + r;
+                double y1, y2;
+                if (INT) {
+                    const double ce = pr[r + P];
+                    y1 = a.mc[1][P] * ce;
+                    y2 = a.kc[1][P] * ce;
+#pragma unroll
+                    for (int d = 1; d <= P; ++d) {
+                        const double sp = pr[r + P - d] + pr[r + P + d];
+                        y1 = fma(a.mc[1][P + d], sp, y1);
+                        y2 = fma(a.kc[1][P + d], sp, y2);
+                    }
+                } else {
+                    y1 = 0.0;
+                    y2 = 0.0;
+#pragma unroll
+                    for (int c = 0; c < W; ++c) {
+                        y1 = fma(yb[(yr * 2 + 0) * W + c], pr[r + c], y1);
+                        y2 = fma(yb[(yr * 2 + 1) * W + c], pr[r + c], y2);
+                    }
+                }
+                Ys[yr * NC + nc] = make_double2(y1, y2);
+            }
+        }
+        __syncthreads();  // Ys complete
+        // ---- x-pass
+        double s0, t0, s1, t1;
+        if (INT) {
+            const double2 c0 = Ys[(2 * w) * NC + lane + P], c1 = Ys[(2 * w + 1) * NC + lane + P];
+            s0 = fma(a.kc[0][P], c0.x, a.mc[0][P] * c0.y);
+            t0 = a.mc[0][P] * c0.x;
+            s1 = fma(a.kc[0][P], c1.x, a.mc[0][P] * c1.y);
+            t1 = a.mc[0][P] * c1.x;
+#pragma unroll
+            for (int d = 1; d <= P; ++d) {
+                const double2 l0 = Ys[(2 * w) * NC + lane + P - d], r0 = Ys[(2 * w) * NC + lane + P + d];
+                const double2 l1 = Ys[(2 * w + 1) * NC + lane + P - d], r1 = Ys[(2 * w + 1) * NC + lane + P + d];
+                const double a0 = l0.x + r0.x, b0 = l0.y + r0.y, a1 = l1.x + r1.x, b1 = l1.y + r1.y;
+                s0 = fma(a.kc[0][P + d], a0, s0);
+                s0 = fma(a.mc[0][P + d], b0, s0);
+                t0 = fma(a.mc[0][P + d], a0, t0);
+                s1 = fma(a.kc[0][P + d], a1, s1);
+                s1 = fma(a.mc[0][P + d], b1, s1);
+                t1 = fma(a.mc[0][P + d], a1, t1);
+            }
+        } else {
+            s0 = t0 = s1 = t1 = 0.0;
+#pragma unroll
+            for (int c = 0; c < W; ++c) {
+                const double mx_ = xb[(lane * 2 + 0) * W + c], kx_ = xb[(lane * 2 + 1) * W + c];
+                const double2 q0 = Ys[(2 * w) * NC + lane + c], q1 = Ys[(2 * w + 1) * NC + lane + c];
+                s0 = fma(kx_, q0.x, s0);
+                s0 = fma(mx_, q0.y, s0);
+                t0 = fma(mx_, q0.x, t0);
+                s1 = fma(kx_, q1.x, s1);
+                s1 = fma(mx_, q1.y, s1);
+                t1 = fma(mx_, q1.x, t1);
+            }
+        }
+        // ---- z-pass (a switch makes every ring slot index compile-time)
+        const bool zint = kk - P >= a.ilo[2] && kk + P <= a.ihi[2];
+        switch (ii % W) {
+#define ADS_ZCASE(U)                                                                                          \
+    case U:                                                                                                   \
+        if constexpr (U < W)                                                                                  \
+            kop_zscatter<P, U>(a, A0, A1, s0, t0, s1, t1, kk, zint, z0, own0, own1, sxy0, sxy1, oxy);         \
+        break;
+            ADS_ZCASE(0) ADS_ZCASE(1) ADS_ZCASE(2) ADS_ZCASE(3) ADS_ZCASE(4) ADS_ZCASE(5)
+            ADS_ZCASE(6) ADS_ZCASE(7) ADS_ZCASE(8) ADS_ZCASE(9) ADS_ZCASE(10)
+#undef ADS_ZCASE
         }
     }
 }
@@ -620,8 +655,8 @@ __global__ void __launch_bounds__(KT_THREADS, 2) kop_kernel(const KopArgs a) {
     const int z0 = blockIdx.z * a.zlen, z1 = min(a.geo.n2, z0 + a.zlen);
     const bool xi = x0 >= a.ilo[0] && x0 + KT_X - 1 <= a.ihi[0];
     const bool yi = y0 >= a.ilo[1] && y0 + KT_Y - 1 <= a.ihi[1];
-    if (xi && yi) kop_tile<P, true, true>(a, smem, x0, y0, z0, z1);
-    else kop_tile<P, false, false>(a, smem, x0, y0, z0, z1);
+    if (xi && yi) kop_tile<P, true>(a, smem, x0, y0, z0, z1);
+    else kop_tile<P, false>(a, smem, x0, y0, z0, z1);
 }
 
 // ------------------------------------------------------------------------------------------
