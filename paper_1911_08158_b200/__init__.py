@@ -129,9 +129,9 @@ class Solver:
             raise AdsError(rc, lib().ads_last_error(self.h).decode())
 
     def close(self):
-        if getattr(self, "h", None):
-            lib().ads_destroy(self.h)
-            self.h = None
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ads_destroy(self.h)
+        self.h = None
 
     __del__ = close
 

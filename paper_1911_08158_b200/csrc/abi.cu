@@ -22,10 +22,12 @@ namespace {
 
 struct DirDev {
     double *mband = nullptr, *kband = nullptr, *aband = nullptr;  // [n][2p+1]
-    double *l = nullptr, *us = nullptr, *dinv = nullptr, *Tf = nullptr, *Rb = nullptr;
+    double *bband = nullptr, *btband = nullptr;                    // elasticity: B, B^T
+    double *slband = nullptr, *ssband = nullptr;                   // elasticity: M + c K (apply)
     int t_lo = 1, t_hi = 0;  // rows [t_lo, t_hi] of M, K are the Toeplitz row (mrow, krow)
     double mrow[2 * kMaxP + 1] = {}, krow[2 * kMaxP + 1] = {};
-    SolveTab tab;
+    SolveTab tab;               // P-wave: A_d = M_d + tau^2/4 K_d
+    SolveTab tabL, tabS, tabM;  // elasticity: M + c_L K, M + c_S K, M
 };
 
 }  // namespace
@@ -34,6 +36,7 @@ struct ads_ctx {
     int nel[3] = {0, 0, 0}, n[3] = {0, 0, 0};
     int p = 0, bc = 0, ncomp = 1;
     double tau = 0.0;
+    double lam = 0.0, mu = 0.0, rho = 1.0;  // elasticity (ncomp = 3)
     long step = 0;
     bool failed = false, have_state = false;
     std::string err;
@@ -48,7 +51,9 @@ struct ads_ctx {
     LUFactors mass_lu[3];
     DirDev dd[3];
     // fields
+    // fields (ncomp components each, component-major, Nalloc doubles per component)
     double *U = nullptr, *U2 = nullptr, *V = nullptr, *A = nullptr, *R = nullptr, *Wk = nullptr;
+    double *W = nullptr, *T1 = nullptr, *T2 = nullptr, *T3 = nullptr;  // elasticity scratch
     double *dpartial = nullptr, *dres = nullptr;
     // source
     double *src[3] = {nullptr, nullptr, nullptr};
@@ -149,26 +154,15 @@ double source_g(const ads_ctx *h, double t) {
     return h->wavelet == ADS_WAVELET_RICKER ? h->amp * ricker(t, h->f0, h->t0) : h->amp;
 }
 
-int build_direction(ads_ctx *h, int d) {
-    Space1D &s = h->sp[d];
-    const int p = h->p;
-    if (build_space(p, h->nel[d], h->bc, s)) return fail(h, ADS_E_INVAL, "bad 1D space");
-    const int n = s.n, W = 2 * p + 1;
-    const double eta = h->tau * h->tau / 4.0;
-    Band A(n, p), Mm = s.M;
-    for (size_t q = 0; q < A.v.size(); ++q) A.v[q] = s.M.v[q] + eta * s.K.v[q];
-    if (h->bc == ADS_BC_DIRICHLET0) {
-        A.at(0, 0) = 1.0;
-        A.at(n - 1, n - 1) = 1.0;
-        Mm.at(0, 0) = 1.0;
-        Mm.at(n - 1, n - 1) = 1.0;
-    }
+// Factor A (band, Dirichlet identity rows already set) and build the device tables of
+// the partitioned sweeps (host_setup.h PartTables; kernels.cuh SolveTab).
+int make_solve_tab(ads_ctx *h, const Band &A, const char *what, SolveTab &tab) {
+    const int n = A.n, p = A.p;
     LUFactors f;
-    if (banded_lu(A, f, /*freeze=*/true)) return fail(h, ADS_E_SINGULAR, "A_%d singular", d);
-    if (banded_lu(Mm, h->mass_lu[d])) return fail(h, ADS_E_SINGULAR, "M_%d singular", d);
+    if (banded_lu(A, f, /*freeze=*/true)) return fail(h, ADS_E_SINGULAR, "%s singular", what);
     const int C = kSweepChunks;
     const int L = choose_chunk_len(n, p, C);
-    if (L == 0) return fail(h, ADS_E_INVAL, "n_%d = %d: no supported chunking", d, n);
+    if (L == 0) return fail(h, ADS_E_INVAL, "%s: n = %d has no supported chunking", what, n);
     // pad the factors to C*L rows with identity rows: every chunk has length L
     const int npad = C * L;
     LUFactors fp = f;
@@ -178,6 +172,59 @@ int build_direction(ads_ctx *h, int d) {
     fp.dinv.resize(npad, 1.0);
     PartTables pt;
     build_part_tables(fp, C, L, pt);
+    int rc;
+    double *l, *us, *dinv, *Tf, *Rb;
+    if ((rc = upload(h, &l, fp.l)) || (rc = upload(h, &us, fp.us)) || (rc = upload(h, &dinv, fp.dinv)) ||
+        (rc = upload(h, &Tf, pt.Tf)) || (rc = upload(h, &Rb, pt.Rb)))
+        return rc;
+    tab = SolveTab();
+    tab.l = l;
+    tab.us = us;
+    tab.dinv = dinv;
+    tab.Tf = Tf;
+    tab.Rb = Rb;
+    tab.n = n;
+    tab.L = L;
+    tab.Kf = pt.Kf;
+    tab.Kb = pt.Kb;
+    // uniform region aligned to whole chunks: chunks [c_lo, c_hi) lie inside [i_lo, i_hi)
+    const int c_lo = (f.i_lo + L - 1) / L, c_hi = f.i_hi / L;
+    tab.c_lo = c_hi > c_lo ? c_lo : 0;
+    tab.c_hi = c_hi > c_lo ? c_hi : 0;
+    if (tab.c_hi > tab.c_lo) {
+        for (int k = 0; k < p; ++k) {
+            tab.lc[k] = f.l[(size_t)f.i_lo * p + k];
+            tab.usc[k] = f.us[(size_t)f.i_lo * p + k];
+        }
+        tab.dic = f.dinv[f.i_lo];
+        const int s0 = tab.c_lo * L;  // any uniform chunk: its responses are bitwise identical
+        for (int j = 0; j < L; ++j)
+            for (int m = 0; m < p; ++m) {
+                tab.Gf[j][m] = pt.gf[(size_t)(s0 + j) * p + m];
+                tab.Gb[j][m] = pt.gb[(size_t)(s0 + j) * p + m];
+            }
+    }
+    return ADS_OK;
+}
+
+// M + c K with the Dirichlet identity rows (the matrices the sweeps invert)
+Band shifted(const Space1D &s, double c, int bc) {
+    Band A(s.n, s.p);
+    for (size_t q = 0; q < A.v.size(); ++q) A.v[q] = s.M.v[q] + c * s.K.v[q];
+    if (bc == ADS_BC_DIRICHLET0) {
+        A.at(0, 0) = 1.0;
+        A.at(s.n - 1, s.n - 1) = 1.0;
+    }
+    return A;
+}
+
+int build_direction(ads_ctx *h, int d) {
+    Space1D &s = h->sp[d];
+    const int p = h->p;
+    if (build_space(p, h->nel[d], h->bc, s)) return fail(h, ADS_E_INVAL, "bad 1D space");
+    const int n = s.n, W = 2 * p + 1;
+    Band Mm = shifted(s, 0.0, h->bc);
+    if (banded_lu(Mm, h->mass_lu[d])) return fail(h, ADS_E_SINGULAR, "M_%d singular", d);
     DirDev &D = h->dd[d];
     // Toeplitz interior of M, K (build_space made rows [2p, n-1-2p] bitwise equal)
     if (n - 1 - 2 * p - 2 * p >= 2) {
@@ -195,38 +242,42 @@ int build_direction(ads_ctx *h, int d) {
                 }
     }
     int rc;
-    std::vector<double> mb(s.M.v), kb(s.K.v), ab(A.v);
-    (void)W;
-    if ((rc = upload(h, &D.mband, mb)) || (rc = upload(h, &D.kband, kb)) || (rc = upload(h, &D.aband, ab)) ||
-        (rc = upload(h, &D.l, fp.l)) || (rc = upload(h, &D.us, fp.us)) || (rc = upload(h, &D.dinv, fp.dinv)) ||
-        (rc = upload(h, &D.Tf, pt.Tf)) || (rc = upload(h, &D.Rb, pt.Rb)))
-        return rc;
-    D.tab.l = D.l;
-    D.tab.us = D.us;
-    D.tab.dinv = D.dinv;
-    D.tab.Tf = D.Tf;
-    D.tab.Rb = D.Rb;
-    D.tab.n = n;
-    D.tab.L = L;
-    D.tab.Kf = pt.Kf;
-    D.tab.Kb = pt.Kb;
-    // uniform region aligned to whole chunks: chunks [c_lo, c_hi) lie inside [i_lo, i_hi)
-    const int c_lo = (f.i_lo + L - 1) / L, c_hi = f.i_hi / L;
-    D.tab.c_lo = c_hi > c_lo ? c_lo : 0;
-    D.tab.c_hi = c_hi > c_lo ? c_hi : 0;
-    if (D.tab.c_hi > D.tab.c_lo) {
-        for (int k = 0; k < p; ++k) {
-            D.tab.lc[k] = f.l[(size_t)f.i_lo * p + k];
-            D.tab.usc[k] = f.us[(size_t)f.i_lo * p + k];
+    char what[32];
+    if (h->ncomp == 1) {
+        // P-wave: A_d = M_d + tau^2/4 K_d (eta = tau^2/4 PAPER.md:173)
+        const double eta = h->tau * h->tau / 4.0;
+        Band A = shifted(s, eta, h->bc);
+        snprintf(what, sizeof what, "A_%d", d);
+        if ((rc = make_solve_tab(h, A, what, D.tab))) return rc;
+        if ((rc = upload(h, &D.aband, A.v))) return rc;
+    } else {
+        // elasticity: S_i = rho (x)_d (M_d + c_{i,d} K_d), c = tau^2/(4 rho) (2mu+lam | mu)
+        // (Eq. 37, 3D reading DESIGN.md E1); B_d for the coupling blocks
+        const double cl = h->tau * h->tau / (4.0 * h->rho) * (2.0 * h->mu + h->lam);
+        const double cs = h->tau * h->tau / (4.0 * h->rho) * h->mu;
+        Band AL = shifted(s, cl, h->bc), AS = shifted(s, cs, h->bc);
+        snprintf(what, sizeof what, "SL_%d", d);
+        if ((rc = make_solve_tab(h, AL, what, D.tabL))) return rc;
+        snprintf(what, sizeof what, "SS_%d", d);
+        if ((rc = make_solve_tab(h, AS, what, D.tabS))) return rc;
+        snprintf(what, sizeof what, "M_%d", d);
+        if ((rc = make_solve_tab(h, Mm, what, D.tabM))) return rc;
+        Band BT(n, p);
+        for (int i = 0; i < n; ++i)
+            for (int j = i - p; j <= i + p; ++j)
+                if (j >= 0 && j < n) BT.at(i, j) = s.B.get(j, i);
+        // the apply bands: boundary rows/columns stay zero (inputs and outputs vanish there)
+        Band SLa(n, p), SSa(n, p);
+        for (size_t q = 0; q < SLa.v.size(); ++q) {
+            SLa.v[q] = s.M.v[q] + cl * s.K.v[q];
+            SSa.v[q] = s.M.v[q] + cs * s.K.v[q];
         }
-        D.tab.dic = f.dinv[f.i_lo];
-        const int s0 = D.tab.c_lo * L;  // any uniform chunk: its responses are bitwise identical
-        for (int j = 0; j < L; ++j)
-            for (int m = 0; m < p; ++m) {
-                D.tab.Gf[j][m] = pt.gf[(size_t)(s0 + j) * p + m];
-                D.tab.Gb[j][m] = pt.gb[(size_t)(s0 + j) * p + m];
-            }
+        if ((rc = upload(h, &D.bband, s.B.v)) || (rc = upload(h, &D.btband, BT.v)) ||
+            (rc = upload(h, &D.slband, SLa.v)) || (rc = upload(h, &D.ssband, SSa.v)))
+            return rc;
     }
+    std::vector<double> mb(s.M.v), kb(s.K.v);
+    if ((rc = upload(h, &D.mband, mb)) || (rc = upload(h, &D.kband, kb))) return rc;
     return ADS_OK;
 }
 
@@ -273,13 +324,13 @@ int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g
     return check_launch(h, "kop");
 }
 
-int run_sweep(ads_ctx *h, int d, const double *in, double *out, double *V, double kick) {
+int run_sweep_tab(ads_ctx *h, int d, const SolveTab &tab, const double *in, double *out, double *V, double kick) {
     SweepArgs a;
     a.in = in;
     a.out = out;
     a.V = V;
     a.kick = kick;
-    a.t = h->dd[d].tab;
+    a.t = tab;
     a.geo = h->geo;
     a.dir = d;
     a.mode = V ? 1 : 0;
@@ -288,7 +339,10 @@ int run_sweep(ads_ctx *h, int d, const double *in, double *out, double *V, doubl
     return check_launch(h, "sweep");
 }
 
-// a = D^-1 r along x, y, z; z-sweep kicks V += kick * a and stores a into aout (nullable)
+int run_sweep(ads_ctx *h, int d, const double *in, double *out, double *V, double kick) {
+    return run_sweep_tab(h, d, h->dd[d].tab, in, out, V, kick);
+}
+
 int run_solve(ads_ctx *h, const double *r_in, double *scratch, double *r2, double *aout, double *V, double kick) {
     int rc;
     if ((rc = run_sweep(h, 0, r_in, scratch, nullptr, 0.0))) return rc;
@@ -305,6 +359,163 @@ int init_state(ads_ctx *h) {
     if ((rc = run_sweep(h, 2, h->R, h->A, h->V, 0.5 * h->tau))) return rc;
     h->step = 0;
     h->have_state = true;
+    return ADS_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// 3D isotropic elasticity (readings C10-C13, E1).  Fields are
+// component-major: component c of a field F is F + c * Nalloc.
+//   Ups_ii = (2mu+lam) K_(i) + mu sum_{d != i} K_(d) = mu K + (mu+lam) K_(i)
+//   Ups_ik = mu [B]_k [B^T]_i + lam [B]_i [B^T]_k      (i != k, M in the third direction)
+// where [F]_d is F acting along direction d.  Kronecker triples run as three banded axis
+// passes (T1, T2 scratch); K = Kx My Mz + ... runs in the fused operator kernel.
+// ---------------------------------------------------------------------------------------
+double *comp(double *f, const ads_ctx *h, int c) { return f + (long)c * h->Nalloc; }
+
+// out = alpha (Fx (x) Fy (x) Fz) in + beta out   (Fd: band [n_d][2p+1], acting along d)
+int tri(ads_ctx *h, double *out, const double *in, const double *fx, const double *fy, const double *fz,
+        double alpha, double beta) {
+    if (launch_axis_apply(h->p, 0, fx, in, h->T1, h->geo, 1.0, 0.0, h->stream) ||
+        launch_axis_apply(h->p, 1, fy, h->T1, h->T2, h->geo, 1.0, 0.0, h->stream) ||
+        launch_axis_apply(h->p, 2, fz, h->T2, out, h->geo, alpha, beta, h->stream))
+        return fail(h, ADS_E_INVAL, "axis apply: unsupported p");
+    return check_launch(h, "axis_apply");
+}
+
+// out += coef Ups_ik in   (i != k)
+int ups_offdiag(ads_ctx *h, int i, int k, const double *in, double *out, double coef) {
+    const double *F[3];
+    int rc;
+    for (int e = 0; e < 3; ++e) F[e] = e == k ? h->dd[e].bband : e == i ? h->dd[e].btband : h->dd[e].mband;
+    if ((rc = tri(h, out, in, F[0], F[1], F[2], coef * h->mu, 1.0))) return rc;
+    for (int e = 0; e < 3; ++e) F[e] = e == i ? h->dd[e].bband : e == k ? h->dd[e].btband : h->dd[e].mband;
+    return tri(h, out, in, F[0], F[1], F[2], coef * h->lam, 1.0);
+}
+
+// out_i (+)= coef (Ups in)_i for all i.  The diagonal blocks go through the fused operator
+// kernel: out_i = coef mu K (in_i + tau_d v_i) with the drift written to pout_i if non-null.
+int ups_apply(ads_ctx *h, const double *in, const double *v, double tau_d, double *pout, double *out, double coef) {
+    int rc;
+    for (int i = 0; i < 3; ++i)
+        if ((rc = run_kop(h, comp((double *)in, h, i), comp((double *)v, h, i), tau_d, 0.0, coef * h->mu,
+                          pout ? comp(pout, h, i) : nullptr, comp(out, h, i))))
+            return rc;
+    const double *P = pout ? pout : in;  // the drifted field the blocks act on
+    for (int i = 0; i < 3; ++i) {
+        const double *F[3];
+        for (int e = 0; e < 3; ++e) F[e] = e == i ? h->dd[e].kband : h->dd[e].mband;
+        if ((rc = tri(h, comp(out, h, i), comp((double *)P, h, i), F[0], F[1], F[2], coef * (h->mu + h->lam),
+                      1.0)))
+            return rc;
+        for (int k = 0; k < 3; ++k)
+            if (k != i && (rc = ups_offdiag(h, i, k, comp((double *)P, h, k), comp(out, h, i), coef))) return rc;
+    }
+    return ADS_OK;
+}
+
+// x <- S_i^-1 x,  S_i = rho (x)_d (M_d + c_{i,d} K_d)  (Eq. 37)
+int s_solve(ads_ctx *h, int i, double *x) {
+    int rc;
+    for (int d = 0; d < 3; ++d)
+        if ((rc = run_sweep_tab(h, d, d == i ? h->dd[d].tabL : h->dd[d].tabS, x, x, nullptr, 0.0))) return rc;
+    launch_axpby(h->Nalloc, 1.0 / h->rho, x, 0.0, x, h->stream);
+    return check_launch(h, "axpby");
+}
+
+// X <- D~^-1 X, D~ = L~ (rho M)^-1 L~^T: predictor x -> y -> z, corrector z -> y -> x
+// (Eqs. 35-36 in delta form, E1).  W: 3-component scratch.
+int el_dsolve(ads_ctx *h, double *X) {
+    const double hh = -0.5 * h->tau * h->tau;
+    const long fb = sizeof(double) * h->Nalloc;
+    int rc;
+    for (int i = 0; i < 3; ++i) {
+        double *wi = comp(h->W, h, i);
+        CUDA_TRY(h, cudaMemcpyAsync(wi, comp(X, h, i), fb, cudaMemcpyDeviceToDevice, h->stream));
+        for (int j = 0; j < i; ++j)
+            if ((rc = ups_offdiag(h, i, j, comp(h->W, h, j), wi, hh))) return rc;
+        if ((rc = s_solve(h, i, wi))) return rc;
+    }
+    for (int i = 2; i >= 0; --i) {
+        double *zi = comp(X, h, i);
+        if ((rc = tri(h, zi, comp(h->W, h, i), h->dd[0].mband, h->dd[1].mband, h->dd[2].mband, h->rho, 0.0)))
+            return rc;
+        for (int j = i + 1; j < 3; ++j)
+            if ((rc = ups_offdiag(h, i, j, comp(X, h, j), zi, hh))) return rc;
+        if ((rc = s_solve(h, i, zi))) return rc;
+    }
+    return ADS_OK;
+}
+
+// one elastic step: P = U + tau V (-> U2), A = -Ups P, A <- D~^-1 A, V += tau A, U <- P
+int el_step(ads_ctx *h) {
+    int rc;
+    if ((rc = ups_apply(h, h->U, h->V, h->tau, h->U2, h->A, -1.0))) return rc;
+    if ((rc = el_dsolve(h, h->A))) return rc;
+    launch_axpby(3 * h->Nalloc, h->tau, h->A, 1.0, h->V, h->stream);
+    if ((rc = check_launch(h, "axpby"))) return rc;
+    std::swap(h->U, h->U2);
+    return ADS_OK;
+}
+
+// half-kick start: V0 = udot0 + tau/2 D~^-1 (-Ups U0)   (C13)
+int el_init(ads_ctx *h) {
+    int rc;
+    if ((rc = ups_apply(h, h->U, h->U, 0.0, nullptr, h->A, -1.0))) return rc;
+    if ((rc = el_dsolve(h, h->A))) return rc;
+    launch_axpby(3 * h->Nalloc, 0.5 * h->tau, h->A, 1.0, h->V, h->stream);
+    if ((rc = check_launch(h, "axpby"))) return rc;
+    h->step = 0;
+    h->have_state = true;
+    return ADS_OK;
+}
+
+// energies (C6 for elasticity): kinetic 1/2 rho v'Mv (v = V - tau/2 a),
+// potential 1/2 U'Ups U, invariant 1/2 V'D~V + 1/2 U'Ups(U + tau V) with
+// V'D~V = sum_i g_i' (rho M)^-1 g_i, g_i = S_i V_i + tau^2/2 sum_{j>i} Ups_ij V_j.
+int el_energy(ads_ctx *h, double res[3]) {
+    const long N3 = 3 * h->Nalloc;
+    const long fb = sizeof(double) * h->Nalloc;
+    int rc;
+    double acc[3] = {0, 0, 0};
+    auto dot = [&](long n, const double *x, const double *y, double &dst) -> int {
+        double v = 0.0;
+        launch_dot(n, x, y, h->dpartial, h->dres, h->stream);
+        CUDA_TRY(h, cudaMemcpyAsync(&v, h->dres, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+        dst += v;
+        return ADS_OK;
+    };
+    // kinetic
+    CUDA_TRY(h, cudaMemcpyAsync(h->W, h->V, sizeof(double) * N3, cudaMemcpyDeviceToDevice, h->stream));
+    launch_axpby(N3, -0.5 * h->tau, h->A, 1.0, h->W, h->stream);
+    for (int c = 0; c < 3; ++c) {
+        if ((rc = tri(h, h->T3, comp(h->W, h, c), h->dd[0].mband, h->dd[1].mband, h->dd[2].mband, h->rho, 0.0)))
+            return rc;
+        if ((rc = dot(h->Nalloc, comp(h->W, h, c), h->T3, acc[0]))) return rc;
+    }
+    // potential
+    if ((rc = ups_apply(h, h->U, h->U, 0.0, nullptr, h->W, 1.0))) return rc;
+    if ((rc = dot(N3, h->U, h->W, acc[1]))) return rc;
+    // invariant: U' Ups (U + tau V)
+    if ((rc = ups_apply(h, h->U, h->V, h->tau, h->U2, h->W, 1.0))) return rc;
+    if ((rc = dot(N3, h->U, h->W, acc[2]))) return rc;
+    double inv = 0.0;
+    for (int i = 0; i < 3; ++i) {
+        double *g = comp(h->W, h, i);
+        const double *F[3];
+        for (int d = 0; d < 3; ++d) F[d] = d == i ? h->dd[d].slband : h->dd[d].ssband;
+        if ((rc = tri(h, g, comp(h->V, h, i), F[0], F[1], F[2], h->rho, 0.0))) return rc;
+        for (int j = i + 1; j < 3; ++j)
+            if ((rc = ups_offdiag(h, i, j, comp(h->V, h, j), g, 0.5 * h->tau * h->tau))) return rc;
+        CUDA_TRY(h, cudaMemcpyAsync(h->T3, g, fb, cudaMemcpyDeviceToDevice, h->stream));
+        for (int d = 0; d < 3; ++d)
+            if ((rc = run_sweep_tab(h, d, h->dd[d].tabM, h->T3, h->T3, nullptr, 0.0))) return rc;
+        launch_axpby(h->Nalloc, 1.0 / h->rho, h->T3, 0.0, h->T3, h->stream);
+        if ((rc = dot(h->Nalloc, g, h->T3, inv))) return rc;
+    }
+    res[0] = 0.5 * acc[0];
+    res[1] = 0.5 * acc[1];
+    res[2] = 0.5 * inv + 0.5 * acc[2];
     return ADS_OK;
 }
 
@@ -327,18 +538,24 @@ int copy_out(ads_ctx *h, double *dst, const double *src, int mem) {
 
 extern "C" {
 
-int ads_create(ads_handle *out, int nx, int ny, int nz, int p, double tau, int bc) {
+static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double tau, int bc, int ncomp,
+                         double lam, double mu, double rho) {
     if (!out) return ADS_E_INVAL;
     *out = nullptr;
     if (p < 1 || p > 5 || nx < 1 || ny < 1 || nz < 1 || !(tau > 0.0) || !std::isfinite(tau) ||
         (bc != ADS_BC_NATURAL && bc != ADS_BC_DIRICHLET0))
         return ADS_E_INVAL;
     if (bc == ADS_BC_DIRICHLET0 && (nx + p < 3 || ny + p < 3 || nz + p < 3)) return ADS_E_INVAL;
+    if (nx + p > 1056 || ny + p > 1056 || nz + p > 1056) return ADS_E_INVAL;  // n_d <= 32 x 33
     ads_ctx *h = new (std::nothrow) ads_ctx;
     if (!h) return ADS_E_NOMEM;
     h->p = p;
     h->bc = bc;
     h->tau = tau;
+    h->ncomp = ncomp;
+    h->lam = lam;
+    h->mu = mu;
+    h->rho = rho;
     h->nel[0] = nx;
     h->nel[1] = ny;
     h->nel[2] = nz;
@@ -358,18 +575,23 @@ int ads_create(ads_handle *out, int nx, int ny, int nz, int p, double tau, int b
         h->geo.sz = h->geo.sy * h->n[1];
         h->N = (long)h->n[0] * h->n[1] * h->n[2];
         h->Nalloc = h->geo.sz * h->n[2];
-        size_t fb = sizeof(double) * h->Nalloc;
-        if ((rc = dalloc(h, (void **)&h->U, fb)) == ADS_OK && (rc = dalloc(h, (void **)&h->U2, fb)) == ADS_OK &&
-            (rc = dalloc(h, (void **)&h->V, fb)) == ADS_OK && (rc = dalloc(h, (void **)&h->A, fb)) == ADS_OK &&
-            (rc = dalloc(h, (void **)&h->R, fb)) == ADS_OK && (rc = dalloc(h, (void **)&h->Wk, fb)) == ADS_OK &&
-            (rc = dalloc(h, (void **)&h->dpartial, sizeof(double) * 1024)) == ADS_OK &&
+        const size_t fb = sizeof(double) * h->Nalloc * ncomp, sb = sizeof(double) * h->Nalloc;
+        std::vector<std::pair<double **, size_t>> fields = {{&h->U, fb}, {&h->U2, fb}, {&h->V, fb},
+                                                            {&h->A, fb}, {&h->R, sb},  {&h->Wk, sb}};
+        if (ncomp == 3)
+            for (auto f : std::initializer_list<std::pair<double **, size_t>>{
+                     {&h->W, fb}, {&h->T1, sb}, {&h->T2, sb}, {&h->T3, sb}})
+                fields.push_back(f);
+        for (auto &f : fields)
+            if (rc == ADS_OK) rc = dalloc(h, (void **)f.first, f.second);
+        if (rc == ADS_OK && (rc = dalloc(h, (void **)&h->dpartial, sizeof(double) * 1024)) == ADS_OK &&
             (rc = dalloc(h, (void **)&h->dres, sizeof(double) * 8)) == ADS_OK) {
             cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
             if (e != cudaSuccess) rc = fail(h, ADS_E_CUDA, "stream: %s", cudaGetErrorString(e));
             h->own_stream = true;
         }
-        if (rc == ADS_OK) {
-            for (double *f : {h->U, h->U2, h->V, h->A, h->R, h->Wk}) cudaMemsetAsync(f, 0, fb, h->stream);
+        if (rc == ADS_OK) {  // zero everything: the row padding of every field stays 0 forever
+            for (auto &f : fields) cudaMemsetAsync(*f.first, 0, f.second, h->stream);
             if (cudaStreamSynchronize(h->stream) != cudaSuccess) rc = fail(h, ADS_E_CUDA, "memset failed");
         }
     }
@@ -381,9 +603,17 @@ int ads_create(ads_handle *out, int nx, int ny, int nz, int p, double tau, int b
     return ADS_OK;
 }
 
-int ads_create_elastic(ads_handle *out, int, int, int, int, double, int, double, double, double) {
+int ads_create(ads_handle *out, int nx, int ny, int nz, int p, double tau, int bc) {
+    return create_common(out, nx, ny, nz, p, tau, bc, 1, 0.0, 0.0, 1.0);
+}
+
+int ads_create_elastic(ads_handle *out, int nx, int ny, int nz, int p, double tau, int bc, double lambda, double mu,
+                       double rho) {
     if (out) *out = nullptr;
-    return ADS_E_INVAL;  // implemented in a later milestone
+    if (!(lambda >= 0.0) || !(mu > 0.0) || !(rho > 0.0) || !std::isfinite(lambda) || !std::isfinite(mu) ||
+        !std::isfinite(rho))
+        return ADS_E_INVAL;
+    return create_common(out, nx, ny, nz, p, tau, bc, 3, lambda, mu, rho);
 }
 
 int ads_set_stream(ads_handle h, void *stream) {
@@ -427,6 +657,7 @@ int ads_set_source(ads_handle h, const double *bx, const double *by, const doubl
         h->has_src = false;
         return ADS_OK;
     }
+    if (h->ncomp != 1) return fail(h, ADS_E_INVAL, "ads_set_source: P-wave handles only (elastic f = 0)");
     if (!by || !bz || (wavelet != ADS_WAVELET_NONE && wavelet != ADS_WAVELET_RICKER))
         return fail(h, ADS_E_INVAL, "ads_set_source: bad argument");
     const double *b[3] = {bx, by, bz};
@@ -450,29 +681,34 @@ int ads_set_state(ads_handle h, const double *u, const double *udot, int mem) {
     int rc = guard(h);
     if (rc) return rc;
     if (!u || (mem != ADS_MEM_HOST && mem != ADS_MEM_DEVICE)) return fail(h, ADS_E_INVAL, "ads_set_state: bad argument");
-    if ((rc = copy_in(h, h->U, u, mem))) return rc;
-    if (udot) {
-        if ((rc = copy_in(h, h->V, udot, mem))) return rc;
-    } else {
-        CUDA_TRY(h, cudaMemsetAsync(h->V, 0, sizeof(double) * h->Nalloc, h->stream));
+    for (int c = 0; c < h->ncomp; ++c) {
+        if ((rc = copy_in(h, comp(h->U, h, c), u + c * h->N, mem))) return rc;
+        if (udot) {
+            if ((rc = copy_in(h, comp(h->V, h, c), udot + c * h->N, mem))) return rc;
+        } else {
+            CUDA_TRY(h, cudaMemsetAsync(comp(h->V, h, c), 0, sizeof(double) * h->Nalloc, h->stream));
+        }
+        if (h->bc == ADS_BC_DIRICHLET0) {
+            launch_mask_boundary(comp(h->U, h, c), h->geo, h->stream);
+            if ((rc = check_launch(h, "mask"))) return rc;
+            launch_mask_boundary(comp(h->V, h, c), h->geo, h->stream);
+            if ((rc = check_launch(h, "mask"))) return rc;
+        }
     }
-    if (h->bc == ADS_BC_DIRICHLET0) {
-        launch_mask_boundary(h->U, h->geo, h->stream);
-        if ((rc = check_launch(h, "mask"))) return rc;
-        launch_mask_boundary(h->V, h->geo, h->stream);
-        if ((rc = check_launch(h, "mask"))) return rc;
-    }
-    return init_state(h);
+    return h->ncomp == 3 ? el_init(h) : init_state(h);
 }
 
-int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const int *comp, const double *sx,
+int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const int *cmp, const double *sx,
                             const double *sy, const double *sz) {
     int rc = guard(h);
     if (rc) return rc;
     if (nterms < 0 || (nterms > 0 && (!amp || !sx || !sy || !sz)))
         return fail(h, ADS_E_INVAL, "ads_set_state_separable: bad argument");
-    CUDA_TRY(h, cudaMemsetAsync(h->U, 0, sizeof(double) * h->Nalloc, h->stream));
-    CUDA_TRY(h, cudaMemsetAsync(h->V, 0, sizeof(double) * h->Nalloc, h->stream));
+    for (int t = 0; t < nterms; ++t)
+        if (cmp && (cmp[t] < 0 || cmp[t] >= h->ncomp))
+            return fail(h, ADS_E_INVAL, "component %d on a handle with %d components", cmp[t], h->ncomp);
+    CUDA_TRY(h, cudaMemsetAsync(h->U, 0, sizeof(double) * h->Nalloc * h->ncomp, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(h->V, 0, sizeof(double) * h->Nalloc * h->ncomp, h->stream));
     if (nterms > 0) {
         const int n0 = h->n[0], n1 = h->n[1], n2 = h->n[2];
         std::vector<double> packed((size_t)nterms * (n0 + n1 + n2));
@@ -485,20 +721,20 @@ int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const i
         }
         CUDA_TRY(h, cudaMemcpy(d, packed.data(), sizeof(double) * packed.size(), cudaMemcpyHostToDevice));
         for (int t = 0; t < nterms; ++t) {
-            if (comp && comp[t] != 0) return fail(h, ADS_E_INVAL, "component %d on a scalar handle", comp[t]);
             const double *b = d + (size_t)t * (n0 + n1 + n2);
-            launch_add_separable(h->U, amp[t], b, b + n0, b + n0 + n1, h->geo, h->stream);
+            launch_add_separable(comp(h->U, h, cmp ? cmp[t] : 0), amp[t], b, b + n0, b + n0 + n1, h->geo, h->stream);
             if ((rc = check_launch(h, "separable"))) return rc;
         }
         CUDA_TRY(h, cudaStreamSynchronize(h->stream));
         cudaFree(d);
         h->allocs.pop_back();
     }
-    if (h->bc == ADS_BC_DIRICHLET0) {
-        launch_mask_boundary(h->U, h->geo, h->stream);
-        if ((rc = check_launch(h, "mask"))) return rc;
-    }
-    return init_state(h);
+    if (h->bc == ADS_BC_DIRICHLET0)
+        for (int c = 0; c < h->ncomp; ++c) {
+            launch_mask_boundary(comp(h->U, h, c), h->geo, h->stream);
+            if ((rc = check_launch(h, "mask"))) return rc;
+        }
+    return h->ncomp == 3 ? el_init(h) : init_state(h);
 }
 
 int ads_step(ads_handle h, int nsteps) {
@@ -507,6 +743,11 @@ int ads_step(ads_handle h, int nsteps) {
     if (nsteps < 0) return fail(h, ADS_E_INVAL, "nsteps < 0");
     if (!h->have_state) return fail(h, ADS_E_STATE, "ads_step before ads_set_state");
     for (int s = 0; s < nsteps; ++s) {
+        if (h->ncomp == 3) {
+            if ((rc = el_step(h))) return rc;
+            h->step += 1;
+            continue;
+        }
         const double t1 = (double)(h->step + 1) * h->tau;  // F at t_{n+1} (C14)
         // drift + RHS: U2 = U + tau V, R = F(t_{n+1}) - K U2
         if ((rc = run_kop(h, h->U, h->V, h->tau, source_g(h, t1), -1.0, h->U2, h->R))) return rc;
@@ -522,35 +763,40 @@ int ads_energy(ads_handle h, double out[3]) {
     int rc = guard(h);
     if (rc) return rc;
     if (!out) return fail(h, ADS_E_INVAL, "ads_energy: out is NULL");
-    const Geom &g = h->geo;
-    const long N = h->Nalloc;  // padding entries are 0 in every field
+    if (!h->have_state) return fail(h, ADS_E_STATE, "ads_energy before ads_set_state");
     double res[3];
-    // v = V - tau/2 a ; kinetic = 1/2 v' M v
-    CUDA_TRY(h, cudaMemcpyAsync(h->R, h->V, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->stream));
-    launch_axpby(N, -0.5 * h->tau, h->A, 1.0, h->R, h->stream);
-    if ((rc = check_launch(h, "axpby"))) return rc;
-    launch_axis_apply(h->p, 0, h->dd[0].mband, h->R, h->Wk, g, h->stream);
-    launch_axis_apply(h->p, 1, h->dd[1].mband, h->Wk, h->U2, g, h->stream);
-    launch_axis_apply(h->p, 2, h->dd[2].mband, h->U2, h->Wk, g, h->stream);
-    if ((rc = check_launch(h, "axis_apply"))) return rc;
-    launch_dot(N, h->R, h->Wk, h->dpartial, h->dres + 0, h->stream);
-    // potential = 1/2 U' K U
-    if ((rc = run_kop(h, h->U, h->V, 0.0, 0.0, 1.0, nullptr, h->R))) return rc;
-    launch_dot(N, h->U, h->R, h->dpartial, h->dres + 1, h->stream);
-    // invariant = 1/2 V' D V + 1/2 U_n' K U_{n+1}
-    launch_axis_apply(h->p, 0, h->dd[0].aband, h->V, h->Wk, g, h->stream);
-    launch_axis_apply(h->p, 1, h->dd[1].aband, h->Wk, h->U2, g, h->stream);
-    launch_axis_apply(h->p, 2, h->dd[2].aband, h->U2, h->Wk, g, h->stream);
-    launch_dot(N, h->V, h->Wk, h->dpartial, h->dres + 2, h->stream);
-    if ((rc = run_kop(h, h->U, h->V, h->tau, 0.0, 1.0, nullptr, h->R))) return rc;
-    launch_dot(N, h->U, h->R, h->dpartial, h->dres + 3, h->stream);
-    if ((rc = check_launch(h, "dot"))) return rc;
-    double d4[4];
-    CUDA_TRY(h, cudaMemcpyAsync(d4, h->dres, sizeof(double) * 4, cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-    res[0] = 0.5 * d4[0];
-    res[1] = 0.5 * d4[1];
-    res[2] = 0.5 * d4[2] + 0.5 * d4[3];
+    if (h->ncomp == 3) {
+        if ((rc = el_energy(h, res))) return rc;
+    } else {
+        const Geom &g = h->geo;
+        const long N = h->Nalloc;  // padding entries are 0 in every field
+        // v = V - tau/2 a ; kinetic = 1/2 v' M v
+        CUDA_TRY(h, cudaMemcpyAsync(h->R, h->V, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->stream));
+        launch_axpby(N, -0.5 * h->tau, h->A, 1.0, h->R, h->stream);
+        if ((rc = check_launch(h, "axpby"))) return rc;
+        launch_axis_apply(h->p, 0, h->dd[0].mband, h->R, h->Wk, g, 1.0, 0.0, h->stream);
+        launch_axis_apply(h->p, 1, h->dd[1].mband, h->Wk, h->U2, g, 1.0, 0.0, h->stream);
+        launch_axis_apply(h->p, 2, h->dd[2].mband, h->U2, h->Wk, g, 1.0, 0.0, h->stream);
+        if ((rc = check_launch(h, "axis_apply"))) return rc;
+        launch_dot(N, h->R, h->Wk, h->dpartial, h->dres + 0, h->stream);
+        // potential = 1/2 U' K U
+        if ((rc = run_kop(h, h->U, h->V, 0.0, 0.0, 1.0, nullptr, h->R))) return rc;
+        launch_dot(N, h->U, h->R, h->dpartial, h->dres + 1, h->stream);
+        // invariant = 1/2 V' D V + 1/2 U_n' K U_{n+1}
+        launch_axis_apply(h->p, 0, h->dd[0].aband, h->V, h->Wk, g, 1.0, 0.0, h->stream);
+        launch_axis_apply(h->p, 1, h->dd[1].aband, h->Wk, h->U2, g, 1.0, 0.0, h->stream);
+        launch_axis_apply(h->p, 2, h->dd[2].aband, h->U2, h->Wk, g, 1.0, 0.0, h->stream);
+        launch_dot(N, h->V, h->Wk, h->dpartial, h->dres + 2, h->stream);
+        if ((rc = run_kop(h, h->U, h->V, h->tau, 0.0, 1.0, nullptr, h->R))) return rc;
+        launch_dot(N, h->U, h->R, h->dpartial, h->dres + 3, h->stream);
+        if ((rc = check_launch(h, "dot"))) return rc;
+        double d4[4];
+        CUDA_TRY(h, cudaMemcpyAsync(d4, h->dres, sizeof(double) * 4, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+        res[0] = 0.5 * d4[0];
+        res[1] = 0.5 * d4[1];
+        res[2] = 0.5 * d4[2] + 0.5 * d4[3];
+    }
     for (int i = 0; i < 3; ++i) {
         if (!std::isfinite(res[i])) return fail(h, ADS_E_STATE, "non-finite energy (NaN/Inf in state)");
         out[i] = res[i];
@@ -562,14 +808,17 @@ int ads_get_state(ads_handle h, double *u, double *udot, double *a, int mem) {
     int rc = guard(h);
     if (rc) return rc;
     if (mem != ADS_MEM_HOST && mem != ADS_MEM_DEVICE) return fail(h, ADS_E_INVAL, "bad mem");
-    if (u && (rc = copy_out(h, u, h->U, mem))) return rc;
-    if (udot) {
-        CUDA_TRY(h, cudaMemcpyAsync(h->Wk, h->V, sizeof(double) * h->Nalloc, cudaMemcpyDeviceToDevice, h->stream));
-        launch_axpby(h->Nalloc, -0.5 * h->tau, h->A, 1.0, h->Wk, h->stream);
-        if ((rc = check_launch(h, "axpby"))) return rc;
-        if ((rc = copy_out(h, udot, h->Wk, mem))) return rc;
+    for (int c = 0; c < h->ncomp; ++c) {
+        if (u && (rc = copy_out(h, u + c * h->N, comp(h->U, h, c), mem))) return rc;
+        if (udot) {
+            CUDA_TRY(h, cudaMemcpyAsync(h->Wk, comp(h->V, h, c), sizeof(double) * h->Nalloc, cudaMemcpyDeviceToDevice,
+                                        h->stream));
+            launch_axpby(h->Nalloc, -0.5 * h->tau, comp(h->A, h, c), 1.0, h->Wk, h->stream);
+            if ((rc = check_launch(h, "axpby"))) return rc;
+            if ((rc = copy_out(h, udot + c * h->N, h->Wk, mem))) return rc;
+        }
+        if (a && (rc = copy_out(h, a + c * h->N, comp(h->A, h, c), mem))) return rc;
     }
-    if (a && (rc = copy_out(h, a, h->A, mem))) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     return ADS_OK;
 }
@@ -592,7 +841,14 @@ int ads_apply_k(ads_handle h, const double *x, double *out) {
     int rc = guard(h);
     if (rc) return rc;
     if (!x || !out || x == out) return fail(h, ADS_E_INVAL, "ads_apply_k: bad pointers");
-    if ((rc = copy_in(h, h->U2, x, ADS_MEM_DEVICE))) return rc;
+    for (int c = 0; c < h->ncomp; ++c)
+        if ((rc = copy_in(h, comp(h->U2, h, c), x + c * h->N, ADS_MEM_DEVICE))) return rc;
+    if (h->ncomp == 3) {
+        if ((rc = ups_apply(h, h->U2, h->U2, 0.0, nullptr, h->A, 1.0))) return rc;
+        for (int c = 0; c < 3; ++c)
+            if ((rc = copy_out(h, out + c * h->N, comp(h->A, h, c), ADS_MEM_DEVICE))) return rc;
+        return ADS_OK;
+    }
     if ((rc = run_kop(h, h->U2, h->U2, 0.0, 0.0, 1.0, nullptr, h->R))) return rc;
     return copy_out(h, out, h->R, ADS_MEM_DEVICE);
 }
@@ -601,6 +857,14 @@ int ads_solve_d(ads_handle h, const double *x, double *out) {
     int rc = guard(h);
     if (rc) return rc;
     if (!x || !out) return fail(h, ADS_E_INVAL, "ads_solve_d: bad pointers");
+    if (h->ncomp == 3) {
+        for (int c = 0; c < 3; ++c)
+            if ((rc = copy_in(h, comp(h->A, h, c), x + c * h->N, ADS_MEM_DEVICE))) return rc;
+        if ((rc = el_dsolve(h, h->A))) return rc;
+        for (int c = 0; c < 3; ++c)
+            if ((rc = copy_out(h, out + c * h->N, comp(h->A, h, c), ADS_MEM_DEVICE))) return rc;
+        return ADS_OK;
+    }
     if ((rc = copy_in(h, h->R, x, ADS_MEM_DEVICE))) return rc;
     if ((rc = run_sweep(h, 0, h->R, h->Wk, nullptr, 0.0))) return rc;
     if ((rc = run_sweep(h, 1, h->Wk, h->R, nullptr, 0.0))) return rc;
@@ -612,6 +876,7 @@ int ads_sweep(ads_handle h, int d, const double *x, double *out) {
     int rc = guard(h);
     if (rc) return rc;
     if (!x || !out || d < 0 || d > 2) return fail(h, ADS_E_INVAL, "ads_sweep: bad argument");
+    if (h->ncomp != 1) return fail(h, ADS_E_INVAL, "ads_sweep: P-wave handles only");
     if ((rc = copy_in(h, h->R, x, ADS_MEM_DEVICE))) return rc;
     if ((rc = run_sweep(h, d, h->R, h->Wk, nullptr, 0.0))) return rc;
     return copy_out(h, out, h->Wk, ADS_MEM_DEVICE);

@@ -662,27 +662,27 @@ __global__ void __launch_bounds__(KT_THREADS, 2) kop_kernel(const KopArgs a) {
 // ------------------------------------------------------------------------------------------
 // helpers
 // ------------------------------------------------------------------------------------------
+// out = alpha (A along axis d) in + beta out  (beta == 0: out is not read).  One thread per
+// x position of a row; rows (j, k) strided over the grid's y dimension.
 template <int P>
 __global__ void axis_apply_kernel(int d, const double *__restrict__ band, const double *__restrict__ in,
-                                  double *__restrict__ out, Geom g) {
+                                  double *__restrict__ out, Geom g, double alpha, double beta) {
     constexpr int W = 2 * P + 1;
-    long N = (long)g.n0 * g.n1 * g.n2;
-    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x) {
-        int i = q % g.n0;
-        long t = q / g.n0;
-        int j = t % g.n1;
-        int k = t / g.n1;
-        int r = d == 0 ? i : d == 1 ? j : k;
-        int nd = d == 0 ? g.n0 : d == 1 ? g.n1 : g.n2;
-        long st = d == 0 ? 1 : d == 1 ? g.sy : g.sz;
-        long idx = (long)k * g.sz + (long)j * g.sy + i;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n0) return;
+    const int nd = d == 0 ? g.n0 : d == 1 ? g.n1 : g.n2;
+    const long st = d == 0 ? 1 : d == 1 ? g.sy : g.sz;
+    for (long row = blockIdx.y; row < (long)g.n1 * g.n2; row += gridDim.y) {
+        const int j = (int)(row % g.n1), k = (int)(row / g.n1);
+        const int r = d == 0 ? i : d == 1 ? j : k;
+        const long idx = (long)k * g.sz + (long)j * g.sy + i;
         double acc = 0.0;
 #pragma unroll
         for (int c = 0; c < W; ++c) {
-            int col = r - P + c;
-            if (col >= 0 && col < nd) acc = fma(band[(long)r * W + c], in[idx + (long)(col - r) * st], acc);
+            const int col = r - P + c;
+            if (col >= 0 && col < nd) acc = fma(__ldg(band + (long)r * W + c), in[idx + (long)(col - r) * st], acc);
         }
-        out[idx] = acc;
+        out[idx] = beta == 0.0 ? alpha * acc : fma(alpha, acc, beta * out[idx]);
     }
 }
 
@@ -858,16 +858,15 @@ int launch_sweep(int p, const SweepArgs &a, cudaStream_t s) {
     return -1;
 }
 
-int launch_axis_apply(int p, int d, const double *band, const double *in, double *out, const Geom &g,
-                      cudaStream_t s) {
-    long N = (long)g.n0 * g.n1 * g.n2;
-    int grd = grid_for(N);
+int launch_axis_apply(int p, int d, const double *band, const double *in, double *out, const Geom &g, double alpha,
+                      double beta, cudaStream_t s) {
+    dim3 blk(128), grd((g.n0 + 127) / 128, (unsigned)std::min<long>((long)g.n1 * g.n2, 65535));
     switch (p) {
-        case 1: axis_apply_kernel<1><<<grd, 256, 0, s>>>(d, band, in, out, g); break;
-        case 2: axis_apply_kernel<2><<<grd, 256, 0, s>>>(d, band, in, out, g); break;
-        case 3: axis_apply_kernel<3><<<grd, 256, 0, s>>>(d, band, in, out, g); break;
-        case 4: axis_apply_kernel<4><<<grd, 256, 0, s>>>(d, band, in, out, g); break;
-        case 5: axis_apply_kernel<5><<<grd, 256, 0, s>>>(d, band, in, out, g); break;
+        case 1: axis_apply_kernel<1><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta); break;
+        case 2: axis_apply_kernel<2><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta); break;
+        case 3: axis_apply_kernel<3><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta); break;
+        case 4: axis_apply_kernel<4><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta); break;
+        case 5: axis_apply_kernel<5><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta); break;
         default: return -1;
     }
     return 0;

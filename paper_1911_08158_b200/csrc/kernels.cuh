@@ -63,8 +63,9 @@ int launch_kop(int p, const KopArgs &a, cudaStream_t s);
 int launch_sweep(int p, const SweepArgs &a, cudaStream_t s);
 
 // Small helpers (diagnostics / state I/O, not on the per-step path).
-// out = A along axis d applied to in (band table [n_d][2p+1]).
-int launch_axis_apply(int p, int d, const double *band, const double *in, double *out, const Geom &g, cudaStream_t s);
+// out = alpha (A along axis d) in + beta out (band table [n_d][2p+1]; beta == 0: out not read).
+int launch_axis_apply(int p, int d, const double *band, const double *in, double *out, const Geom &g, double alpha,
+                      double beta, cudaStream_t s);
 // y = alpha x + beta y over N elements
 int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s);
 // zero the boundary faces of a field (Dirichlet masking)
