@@ -74,6 +74,32 @@ int ads_create(ads_handle *h, int nx, int ny, int nz, int p, double tau, int bc)
 int ads_create_elastic(ads_handle *h, int nx, int ny, int nz, int p, double tau, int bc,
                        double lambda, double mu, double rho);
 
+/* ---- z-slab decomposition over GPUs ----
+ * The grid is cut along z into `world` slabs of balanced plane counts (slab r owns global
+ * planes [z_begin, z_begin + z_count), ads_slab_plan).  Per step each slab exchanges p halo
+ * planes of U and V with its neighbours (operator z-pass), runs the x and y
+ * sweeps locally, solves its diagonal block of A_z, exchanges p "tip" planes and applies the
+ * exact SPIKE correction (interface systems 2p x 2p per line; the couplings dropped between
+ * non-adjacent interfaces are certified < 2^-64 at create, else ADS_E_INVAL) fused with the
+ * kick.  P-wave handles only.
+ *
+ * ads_get_unique_id: NCCL unique id (128 bytes, caller-owned) for ads_create_dist; rank 0
+ *   creates it and broadcasts it (e.g. with torch.distributed).  Host-only call.
+ * ads_slab_plan: host-only slab extent of `rank` for nz ELEMENTS (nz + p planes).
+ * ads_create_dist: one slab per process/GPU; collective over the `world` ranks (NCCL
+ *   communicator on `device`).  State I/O (set_state/get_state) uses the LOCAL planes
+ *   (z_count x n_y x n_x doubles); ads_energy returns the global energies (NCCL allreduce).
+ * ads_create_virtual: all `nslabs` slabs on the current device in one handle, exchanging by
+ *   device copies -- runs the distributed algorithm on one GPU (parity tests); state I/O
+ *   uses the global arrays.
+ * ads_local_extent: the handle's owned global planes. */
+int ads_get_unique_id(unsigned char uid[128]);
+int ads_slab_plan(int nz, int p, int world, int rank, int *z_begin, int *z_count);
+int ads_create_dist(ads_handle *h, int nx, int ny, int nz, int p, double tau, int bc, int rank, int world,
+                    const unsigned char uid[128], int device);
+int ads_create_virtual(ads_handle *h, int nx, int ny, int nz, int p, double tau, int bc, int nslabs);
+int ads_local_extent(ads_handle h, int *z_begin, int *z_count);
+
 /* Attach a CUDA stream (cudaStream_t passed as void*); NULL = library stream. */
 int ads_set_stream(ads_handle h, void *cuda_stream);
 

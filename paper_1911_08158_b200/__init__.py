@@ -30,6 +30,7 @@ EXPORTS = [
     "ads_set_source", "ads_set_state", "ads_set_state_separable", "ads_step", "ads_energy", "ads_get_state",
     "ads_time", "ads_step_count", "ads_dims", "ads_apply_k", "ads_solve_d", "ads_sweep", "ads_launch_count",
     "ads_last_error", "ads_destroy", "ads_profile_enable", "ads_profile_read",
+    "ads_get_unique_id", "ads_slab_plan", "ads_create_dist", "ads_create_virtual", "ads_local_extent",
 ]
 
 
@@ -74,6 +75,11 @@ def lib():
             "ads_destroy": (_I, [_H]),
             "ads_profile_enable": (_I, [_H, _I]),
             "ads_profile_read": (_I, [_H, _VP, _VP]),
+            "ads_get_unique_id": (_I, [_VP]),
+            "ads_slab_plan": (_I, [_I, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+            "ads_create_dist": (_I, [ctypes.POINTER(_H), _I, _I, _I, _I, _D, _I, _I, _I, _VP, _I]),
+            "ads_create_virtual": (_I, [ctypes.POINTER(_H), _I, _I, _I, _I, _D, _I, _I]),
+            "ads_local_extent": (_I, [_H, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -102,15 +108,58 @@ def _ptr_mem(x):
     return a, p, ADS_MEM_HOST
 
 
-class Solver:
-    """One ADS solver handle (P-wave or elasticity) on the current CUDA device."""
+def get_unique_id() -> bytes:
+    """NCCL unique id (128 bytes) for Solver(dist=...); host-only."""
+    buf = (ctypes.c_ubyte * 128)()
+    rc = lib().ads_get_unique_id(buf)
+    if rc != 0:
+        raise AdsError(rc, "ads_get_unique_id failed")
+    return bytes(buf)
 
-    def __init__(self, nel, p, tau, bc=ADS_BC_DIRICHLET0, elastic=False, lam=1.0, mu=1.0, rho=1.0):
+
+def slab_plan(nz, p, world, rank):
+    """(z_begin, z_count): global planes owned by slab `rank` for nz elements (host-only)."""
+    b, c = ctypes.c_int(), ctypes.c_int()
+    rc = lib().ads_slab_plan(nz, p, world, rank, ctypes.byref(b), ctypes.byref(c))
+    if rc != 0:
+        raise AdsError(rc, "ads_slab_plan failed")
+    return b.value, c.value
+
+
+def broadcast_unique_id(rank, group=None) -> bytes:
+    """Rank 0 creates the NCCL id, torch.distributed broadcasts it (any backend, CPU tensor)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        t = torch.tensor(list(get_unique_id()), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.broadcast(t, src=0, group=group)
+    return bytes(t.cpu().tolist())
+
+
+class Solver:
+    """One ADS solver handle on the current CUDA device: P-wave or elasticity on one GPU,
+    a z-slab of a multi-GPU grid (dist=(rank, world, uid)), or all slabs of a grid on this
+    device exchanging by device copies (virtual_slabs=G)."""
+
+    def __init__(self, nel, p, tau, bc=ADS_BC_DIRICHLET0, elastic=False, lam=1.0, mu=1.0, rho=1.0, dist=None,
+                 virtual_slabs=0, device=None):
         if isinstance(nel, int):
             nel = (nel, nel, nel)
         h = _H()
         if elastic:
             rc = lib().ads_create_elastic(ctypes.byref(h), nel[0], nel[1], nel[2], p, tau, bc, lam, mu, rho)
+        elif dist is not None:
+            rank, world, uid = dist
+            buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+            if device is None:
+                import torch
+                device = torch.cuda.current_device()
+            rc = lib().ads_create_dist(ctypes.byref(h), nel[0], nel[1], nel[2], p, tau, bc, rank, world, buf, device)
+        elif virtual_slabs:
+            rc = lib().ads_create_virtual(ctypes.byref(h), nel[0], nel[1], nel[2], p, tau, bc, virtual_slabs)
         else:
             rc = lib().ads_create(ctypes.byref(h), nel[0], nel[1], nel[2], p, tau, bc)
         if rc != 0:
@@ -119,7 +168,10 @@ class Solver:
         self.nel, self.p, self.tau, self.bc, self.elastic = tuple(nel), p, tau, bc, elastic
         n = (ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int())
         lib().ads_dims(h, *(ctypes.byref(x) for x in n))
-        self.n = (n[0].value, n[1].value, n[2].value)
+        zb, zc = ctypes.c_int(), ctypes.c_int()
+        lib().ads_local_extent(h, ctypes.byref(zb), ctypes.byref(zc))
+        self.z_begin, self.z_count = zb.value, zc.value
+        self.n = (n[0].value, n[1].value, n[2].value)  # z: owned planes for a dist slab
         self.ncomp = n[3].value
         self.N = self.n[0] * self.n[1] * self.n[2]
         self.shape = ((3,) if elastic else ()) + (self.n[2], self.n[1], self.n[0])
@@ -141,13 +193,15 @@ class Solver:
         self._check(lib().ads_set_stream(self.h, ptr))
 
     def load_vector(self, d, func):
-        out = np.zeros(max(self.n))
+        """1D load vector (global length n_d = nel_d + p, also for slabs)."""
+        nd = self.nel[d] + self.p if 0 <= d < 3 else 1  # bad d: the library reports ADS_E_INVAL
+        out = np.zeros(nd)
         if func[0] == "sin":
             self._check(lib().ads_load_vector(self.h, d, ADS_FUNC_SIN, 0.0, 1.0, out.ctypes.data))
         else:
             self._check(lib().ads_load_vector(self.h, d, ADS_FUNC_GAUSS, float(func[1]), float(func[2]),
                                               out.ctypes.data))
-        return out[:self.n[d]]
+        return out
 
     def mass_solve_1d(self, d, x):
         x = np.array(x, dtype=np.float64, copy=True)
@@ -233,9 +287,11 @@ def project_1d(solver, func, d):
     return solver.mass_solve_1d(d, solver.load_vector(d, func))
 
 
-def make_solver(wl):
-    """Solver for a workloads.Workload with its initial state and source set (library-side projection)."""
-    s = Solver(wl.nel, wl.p, wl.tau, wl.bc, elastic=wl.elastic, lam=wl.lam, mu=wl.mu, rho=wl.rho)
+def make_solver(wl, dist=None, virtual_slabs=0):
+    """Solver for a workloads.Workload with its initial state and source set (library-side projection).
+    dist=(rank, world, uid): this process's z-slab; virtual_slabs=G: all G slabs on this device."""
+    s = Solver(wl.nel, wl.p, wl.tau, wl.bc, elastic=wl.elastic, lam=wl.lam, mu=wl.mu, rho=wl.rho, dist=dist,
+               virtual_slabs=virtual_slabs)
     if wl.source is not None:
         src = wl.source
         b = [s.load_vector(d, src.f[d]) for d in range(3)]

@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         objs.append(obj)
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs, "-lcudart"]
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs, "-lcudart", "-lnccl"]
     subprocess.check_call(cmd)
     for o in objs:
         os.remove(o)

@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/ads.h"
 #include "host_setup.h"
 #include "kernels.cuh"
@@ -54,6 +56,20 @@ struct ads_ctx {
     // fields (ncomp components each, component-major, Nalloc doubles per component)
     double *U = nullptr, *U2 = nullptr, *V = nullptr, *A = nullptr, *R = nullptr, *Wk = nullptr;
     double *W = nullptr, *T1 = nullptr, *T2 = nullptr, *T3 = nullptr;  // elasticity scratch
+    // z-slab decomposition: dist = 1 NCCL slab (one per process/GPU),
+    // 2 virtual group (all slabs of the grid on this device, exchanges by device copies),
+    // 3 member slab of a virtual group.  This slab owns global planes [zbeg, zbeg + n[2]);
+    // fields carry p halo planes below and above the owned planes (pointers are to the
+    // first owned plane).
+    int dist = 0, rank = 0, world = 1, zbeg = 0, ngz = 0, halo = 0;
+    bool has_prev = false, has_next = false;
+    SolveTab tabZ;                                   // A_z restricted to the slab (diagonal block)
+    double *Vsp = nullptr, *Wsp = nullptr;           // SPIKE columns [nl][p]
+    double *tip_prev = nullptr, *tip_next = nullptr; // p planes received from the neighbours
+    double qt[2 * kMaxP][2 * kMaxP] = {}, qb[2 * kMaxP][2 * kMaxP] = {};
+    ncclComm_t comm = nullptr;
+    std::vector<ads_ctx *> members;                  // dist = 2
+    ads_ctx *prev = nullptr, *next = nullptr;        // dist = 3
     double *dpartial = nullptr, *dres = nullptr;
     // source
     double *src[3] = {nullptr, nullptr, nullptr};
@@ -218,6 +234,42 @@ Band shifted(const Space1D &s, double c, int bc) {
     return A;
 }
 
+// z-slab tables of this slab (distributed exact SPIKE, host_setup.h build_slab_spikes): the
+// diagonal block's sweep tables, its spike columns, and the interface inverses towards the
+// neighbours.  Every rank recomputes its neighbours' spikes (1D, cheap): no setup traffic.
+int build_slab_tables(ads_ctx *h, const Band &A) {
+    std::vector<int> z0s, nls;
+    slab_plan(h->ngz, h->world, z0s, nls);
+    const int r = h->rank, p = h->p;
+    for (int j = 0; j < h->world; ++j)
+        if (nls[j] < 2 * p + 1) return fail(h, ADS_E_INVAL, "slab %d has %d < 2p+1 planes", j, nls[j]);
+    SlabSpikes me, nb;
+    if (build_slab_spikes(A, z0s[r], nls[r], me)) return fail(h, ADS_E_SINGULAR, "slab block singular");
+    int rc;
+    if ((rc = make_solve_tab(h, me.block, "A_z slab", h->tabZ))) return rc;
+    if ((rc = upload(h, &h->Vsp, me.V)) || (rc = upload(h, &h->Wsp, me.W))) return rc;
+    const double thr = std::ldexp(1.0, -64);
+    std::vector<double> Q;
+    const int m = 2 * p;
+    if (h->has_prev) {
+        if (build_slab_spikes(A, z0s[r - 1], nls[r - 1], nb)) return fail(h, ADS_E_SINGULAR, "slab block singular");
+        const double dropped = interface_inverse(nb, me, p, Q);
+        if (!(dropped < thr))
+            return fail(h, ADS_E_INVAL, "slabs too thin for the spike decay (dropped coupling %.3g >= 2^-64)", dropped);
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) h->qt[a][b] = Q[a * m + b];
+    }
+    if (h->has_next) {
+        if (build_slab_spikes(A, z0s[r + 1], nls[r + 1], nb)) return fail(h, ADS_E_SINGULAR, "slab block singular");
+        const double dropped = interface_inverse(me, nb, p, Q);
+        if (!(dropped < thr))
+            return fail(h, ADS_E_INVAL, "slabs too thin for the spike decay (dropped coupling %.3g >= 2^-64)", dropped);
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) h->qb[a][b] = Q[a * m + b];
+    }
+    return ADS_OK;
+}
+
 int build_direction(ads_ctx *h, int d) {
     Space1D &s = h->sp[d];
     const int p = h->p;
@@ -248,7 +300,11 @@ int build_direction(ads_ctx *h, int d) {
         const double eta = h->tau * h->tau / 4.0;
         Band A = shifted(s, eta, h->bc);
         snprintf(what, sizeof what, "A_%d", d);
-        if ((rc = make_solve_tab(h, A, what, D.tab))) return rc;
+        if (d == 2 && h->dist) {
+            if ((rc = build_slab_tables(h, A))) return rc;
+        } else if ((rc = make_solve_tab(h, A, what, D.tab))) {
+            return rc;
+        }
         if ((rc = upload(h, &D.aband, A.v))) return rc;
     } else {
         // elasticity: S_i = rho (x)_d (M_d + c_{i,d} K_d), c = tau^2/(4 rho) (2mu+lam | mu)
@@ -311,6 +367,11 @@ int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g
     a.kz = h->dd[2].kband;
     a.geo = h->geo;
     a.zlen = 0;
+    if (h->halo) {  // slab: band rows / source entries are global rows, halo planes exist
+        a.zoff = h->zbeg;
+        a.zv0 = -h->halo;
+        a.zv1 = h->n[2] + h->halo;
+    }
     for (int d = 0; d < 3; ++d) {
         a.ilo[d] = h->dd[d].t_lo;
         a.ihi[d] = h->dd[d].t_hi;
@@ -350,15 +411,25 @@ int run_solve(ads_ctx *h, const double *r_in, double *scratch, double *r2, doubl
     return run_sweep(h, 2, r2, aout, V, kick);
 }
 
+int dist_solve(ads_ctx *G, double tau_d, double g, double kick, bool keepA);
+
 int init_state(ads_ctx *h) {
     // half-kick start (C2): a0 = D^-1 (F(0) - K u0); V0 = udot0 + tau/2 a0
     int rc;
-    if ((rc = run_kop(h, h->U, h->V, 0.0, source_g(h, 0.0), -1.0, nullptr, h->R))) return rc;
-    if ((rc = run_sweep(h, 0, h->R, h->Wk, nullptr, 0.0))) return rc;
-    if ((rc = run_sweep(h, 1, h->Wk, h->R, nullptr, 0.0))) return rc;
-    if ((rc = run_sweep(h, 2, h->R, h->A, h->V, 0.5 * h->tau))) return rc;
+    if (h->dist) {
+        if ((rc = dist_solve(h, 0.0, source_g(h, 0.0), 0.5 * h->tau, true))) return rc;
+    } else {
+        if ((rc = run_kop(h, h->U, h->V, 0.0, source_g(h, 0.0), -1.0, nullptr, h->R))) return rc;
+        if ((rc = run_sweep(h, 0, h->R, h->Wk, nullptr, 0.0))) return rc;
+        if ((rc = run_sweep(h, 1, h->Wk, h->R, nullptr, 0.0))) return rc;
+        if ((rc = run_sweep(h, 2, h->R, h->A, h->V, 0.5 * h->tau))) return rc;
+    }
     h->step = 0;
     h->have_state = true;
+    for (ads_ctx *m : h->members) {
+        m->step = 0;
+        m->have_state = true;
+    }
     return ADS_OK;
 }
 
@@ -519,6 +590,177 @@ int el_energy(ads_ctx *h, double res[3]) {
     return ADS_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// z-slab decomposition.  Per step, on every slab:
+//   1. halo exchange of U, V (p planes per side)       -- NCCL send/recv, or device copies
+//   2. fused operator (drift + source + K P) on the owned planes, reading the halos
+//   3. x, y sweeps (local), z sweep of the slab's diagonal block (local solve, zero tips)
+//   4. tip exchange (first/last p planes of the local z solution)
+//   5. exact SPIKE fix-up of the slab (interface inverses, spike columns) fused with the kick
+// The dropped couplings of the interface systems are certified < 2^-64 at create.
+// ---------------------------------------------------------------------------------------
+std::vector<ads_ctx *> slabs_of(ads_ctx *h) {
+    if (h->dist == 2) return h->members;
+    return {h};
+}
+
+#define NCCL_TRY(h, call)                                                                       \
+    do {                                                                                        \
+        ncclResult_t r_ = (call);                                                               \
+        if (r_ != ncclSuccess) return fail(h, ADS_E_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+    } while (0)
+
+// send first p owned planes of F down / last p up; receive the neighbours' into the halos
+int exch_halo(ads_ctx *G, double *ads_ctx::*F) {
+    for (ads_ctx *m : slabs_of(G)) {
+        const long sz = m->geo.sz, hp = (long)m->halo * sz, nl = m->n[2];
+        double *f = m->*F;
+        if (m->dist == 3) {
+            if (m->prev)
+                CUDA_TRY(m, cudaMemcpyAsync(f - hp, m->prev->*F + (m->prev->n[2] - m->halo) * sz, sizeof(double) * hp,
+                                            cudaMemcpyDeviceToDevice, m->stream));
+            if (m->next)
+                CUDA_TRY(m, cudaMemcpyAsync(f + nl * sz, m->next->*F, sizeof(double) * hp, cudaMemcpyDeviceToDevice,
+                                            m->stream));
+        } else if (m->dist == 1) {
+            NCCL_TRY(m, ncclGroupStart());
+            if (m->has_prev) {
+                NCCL_TRY(m, ncclSend(f, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
+                NCCL_TRY(m, ncclRecv(f - hp, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
+            }
+            if (m->has_next) {
+                NCCL_TRY(m, ncclSend(f + (nl - m->halo) * sz, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
+                NCCL_TRY(m, ncclRecv(f + nl * sz, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
+            }
+            NCCL_TRY(m, ncclGroupEnd());
+        }
+    }
+    return ADS_OK;
+}
+
+// tips of the local z solution X = Wk: tip_prev <- previous slab's last p planes,
+// tip_next <- next slab's first p planes
+int exch_tips(ads_ctx *G) {
+    for (ads_ctx *m : slabs_of(G)) {
+        const long sz = m->geo.sz, hp = (long)m->p * sz, nl = m->n[2];
+        if (m->dist == 3) {
+            if (m->prev)
+                CUDA_TRY(m, cudaMemcpyAsync(m->tip_prev, m->prev->Wk + (m->prev->n[2] - m->p) * sz, sizeof(double) * hp,
+                                            cudaMemcpyDeviceToDevice, m->stream));
+            if (m->next)
+                CUDA_TRY(m, cudaMemcpyAsync(m->tip_next, m->next->Wk, sizeof(double) * hp, cudaMemcpyDeviceToDevice,
+                                            m->stream));
+        } else if (m->dist == 1) {
+            NCCL_TRY(m, ncclGroupStart());
+            if (m->has_prev) {
+                NCCL_TRY(m, ncclSend(m->Wk, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
+                NCCL_TRY(m, ncclRecv(m->tip_prev, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
+            }
+            if (m->has_next) {
+                NCCL_TRY(m, ncclSend(m->Wk + (nl - m->p) * sz, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
+                NCCL_TRY(m, ncclRecv(m->tip_next, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
+            }
+            NCCL_TRY(m, ncclGroupEnd());
+        }
+    }
+    return ADS_OK;
+}
+
+int run_zfix(ads_ctx *m, double *Aout, double kick) {
+    ZfixArgs a;
+    a.X = m->Wk;
+    a.tip_prev = m->has_prev ? m->tip_prev : nullptr;
+    a.tip_next = m->has_next ? m->tip_next : nullptr;
+    a.Vsp = m->Vsp;
+    a.Wsp = m->Wsp;
+    a.Vf = m->V;
+    a.A = Aout;
+    a.kick = kick;
+    for (int i = 0; i < 2 * kMaxP; ++i)
+        for (int j = 0; j < 2 * kMaxP; ++j) {
+            a.qt[i][j] = m->qt[i][j];
+            a.qb[i][j] = m->qb[i][j];
+        }
+    a.geo = m->geo;
+    ProfScope ps(m, 3);
+    if (launch_zfix(m->p, a, m->stream)) return fail(m, ADS_E_INVAL, "zfix: unsupported p");
+    return check_launch(m, "zfix");
+}
+
+// One drift + solve + kick over all slabs: A = D^-1 (F(t) - K (U + tau_d V)), V += kick A,
+// U <- U + tau_d V when tau_d != 0 (the step) -- with tau_d = 0 this is the half-kick init.
+int dist_solve(ads_ctx *G, double tau_d, double g, double kick, bool keepA) {
+    int rc;
+    if ((rc = exch_halo(G, &ads_ctx::U)) || (rc = exch_halo(G, &ads_ctx::V))) return rc;
+    for (ads_ctx *m : slabs_of(G)) {
+        if ((rc = run_kop(m, m->U, m->V, tau_d, g, -1.0, tau_d != 0.0 ? m->U2 : nullptr, m->R))) return rc;
+        if ((rc = run_sweep(m, 0, m->R, m->Wk, nullptr, 0.0)) || (rc = run_sweep(m, 1, m->Wk, m->R, nullptr, 0.0)) ||
+            (rc = run_sweep_tab(m, 2, m->tabZ, m->R, m->Wk, nullptr, 0.0)))
+            return rc;
+    }
+    if ((rc = exch_tips(G))) return rc;
+    for (ads_ctx *m : slabs_of(G)) {
+        if ((rc = run_zfix(m, keepA ? m->A : nullptr, kick))) return rc;
+        if (tau_d != 0.0) std::swap(m->U, m->U2);
+    }
+    return ADS_OK;
+}
+
+// partial energy dots of one slab (or the single-GPU field) into m->dres[0..3]:
+//   v'Mv (v = V - tau/2 a), U'KU, V'DV, U'K(U + tau V); x/y passes run over the halo planes
+//   so that the z pass sees its neighbours (needs the U, V, R halos exchanged)
+int energy_partials(ads_ctx *m) {
+    const Geom &g = m->geo;
+    const long hl = (long)m->halo * g.sz, N = m->Nalloc;
+    Geom ge = g;
+    ge.n2 = g.n2 + 2 * m->halo;
+    const int zv0 = -m->halo, zv1 = g.n2 + m->halo;
+    int rc;
+    // kinetic (R = v already formed on owned planes, halos exchanged)
+    if (launch_axis_apply(m->p, 0, m->dd[0].mband, m->R - hl, m->Wk - hl, ge, 1.0, 0.0, m->stream) ||
+        launch_axis_apply(m->p, 1, m->dd[1].mband, m->Wk - hl, m->U2 - hl, ge, 1.0, 0.0, m->stream) ||
+        launch_axis_apply(m->p, 2, m->dd[2].mband, m->U2, m->Wk, g, 1.0, 0.0, m->stream, m->zbeg, zv0, zv1))
+        return fail(m, ADS_E_INVAL, "axis apply: unsupported p");
+    if ((rc = check_launch(m, "axis_apply"))) return rc;
+    launch_dot(N, m->R, m->Wk, m->dpartial, m->dres + 0, m->stream);
+    // potential
+    if ((rc = run_kop(m, m->U, m->V, 0.0, 0.0, 1.0, nullptr, m->R))) return rc;
+    launch_dot(N, m->U, m->R, m->dpartial, m->dres + 1, m->stream);
+    // invariant
+    if (launch_axis_apply(m->p, 0, m->dd[0].aband, m->V - hl, m->Wk - hl, ge, 1.0, 0.0, m->stream) ||
+        launch_axis_apply(m->p, 1, m->dd[1].aband, m->Wk - hl, m->U2 - hl, ge, 1.0, 0.0, m->stream) ||
+        launch_axis_apply(m->p, 2, m->dd[2].aband, m->U2, m->Wk, g, 1.0, 0.0, m->stream, m->zbeg, zv0, zv1))
+        return fail(m, ADS_E_INVAL, "axis apply: unsupported p");
+    launch_dot(N, m->V, m->Wk, m->dpartial, m->dres + 2, m->stream);
+    if ((rc = run_kop(m, m->U, m->V, m->tau, 0.0, 1.0, nullptr, m->R))) return rc;
+    launch_dot(N, m->U, m->R, m->dpartial, m->dres + 3, m->stream);
+    return check_launch(m, "dot");
+}
+
+int pwave_energy(ads_ctx *G, double res[3]) {
+    int rc;
+    if ((rc = exch_halo(G, &ads_ctx::U)) || (rc = exch_halo(G, &ads_ctx::V))) return rc;
+    for (ads_ctx *m : slabs_of(G)) {
+        CUDA_TRY(m, cudaMemcpyAsync(m->R, m->V, sizeof(double) * m->Nalloc, cudaMemcpyDeviceToDevice, m->stream));
+        launch_axpby(m->Nalloc, -0.5 * m->tau, m->A, 1.0, m->R, m->stream);
+        if ((rc = check_launch(m, "axpby"))) return rc;
+    }
+    if ((rc = exch_halo(G, &ads_ctx::R))) return rc;
+    double d4[4] = {0, 0, 0, 0};
+    for (ads_ctx *m : slabs_of(G)) {
+        if ((rc = energy_partials(m))) return rc;
+        if (m->dist == 1) NCCL_TRY(m, ncclAllReduce(m->dres, m->dres, 4, ncclDouble, ncclSum, m->comm, m->stream));
+        double e[4];
+        CUDA_TRY(m, cudaMemcpyAsync(e, m->dres, sizeof(double) * 4, cudaMemcpyDeviceToHost, m->stream));
+        CUDA_TRY(m, cudaStreamSynchronize(m->stream));
+        for (int i = 0; i < 4; ++i) d4[i] += e[i];
+    }
+    res[0] = 0.5 * d4[0];
+    res[1] = 0.5 * d4[1];
+    res[2] = 0.5 * d4[2] + 0.5 * d4[3];
+    return ADS_OK;
+}
+
 int copy_in(ads_ctx *h, double *dst, const double *src, int mem) {
     cudaMemcpyKind k = mem == ADS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     // dense caller array -> pitched device field
@@ -538,15 +780,18 @@ int copy_out(ads_ctx *h, double *dst, const double *src, int mem) {
 
 extern "C" {
 
+// dist: 0 single GPU; 1 NCCL slab `rank` of `world`; 3 member slab of a virtual group
 static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double tau, int bc, int ncomp,
-                         double lam, double mu, double rho) {
+                         double lam, double mu, double rho, int dist = 0, int rank = 0, int world = 1,
+                         ncclComm_t comm = nullptr) {
     if (!out) return ADS_E_INVAL;
     *out = nullptr;
     if (p < 1 || p > 5 || nx < 1 || ny < 1 || nz < 1 || !(tau > 0.0) || !std::isfinite(tau) ||
         (bc != ADS_BC_NATURAL && bc != ADS_BC_DIRICHLET0))
         return ADS_E_INVAL;
     if (bc == ADS_BC_DIRICHLET0 && (nx + p < 3 || ny + p < 3 || nz + p < 3)) return ADS_E_INVAL;
-    if (nx + p > 1056 || ny + p > 1056 || nz + p > 1056) return ADS_E_INVAL;  // n_d <= 32 x 33
+    if (nx + p > 1056 || ny + p > 1056) return ADS_E_INVAL;  // n_d <= 32 x 33 (sweep chunking)
+    if (world < 1 || rank < 0 || rank >= world) return ADS_E_INVAL;
     ads_ctx *h = new (std::nothrow) ads_ctx;
     if (!h) return ADS_E_NOMEM;
     h->p = p;
@@ -559,11 +804,32 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
     h->nel[0] = nx;
     h->nel[1] = ny;
     h->nel[2] = nz;
+    h->dist = dist;
+    h->rank = rank;
+    h->world = world;
+    h->comm = comm;
+    h->ngz = nz + p;
     int rc = ADS_OK;
+    if (dist) {
+        std::vector<int> z0s, nls;
+        slab_plan(h->ngz, world, z0s, nls);
+        h->zbeg = z0s[rank];
+        h->halo = p;
+        h->has_prev = rank > 0;
+        h->has_next = rank < world - 1;
+        if (ncomp != 1) rc = fail(h, ADS_E_INVAL, "z-slabs: P-wave handles only");
+    } else if (nz + p > 1056) {
+        rc = ADS_E_INVAL;
+    }
     cudaGetDevice(&h->device);
     for (int d = 0; d < 3 && rc == ADS_OK; ++d) {
         h->n[d] = h->nel[d] + p;
         rc = build_direction(h, d);
+    }
+    if (rc == ADS_OK && dist) {
+        std::vector<int> z0s, nls;
+        slab_plan(h->ngz, world, z0s, nls);
+        h->n[2] = nls[rank];  // owned planes
     }
     if (rc == ADS_OK) {
         h->geo.n0 = h->n[0];
@@ -575,13 +841,19 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
         h->geo.sz = h->geo.sy * h->n[1];
         h->N = (long)h->n[0] * h->n[1] * h->n[2];
         h->Nalloc = h->geo.sz * h->n[2];
-        const size_t fb = sizeof(double) * h->Nalloc * ncomp, sb = sizeof(double) * h->Nalloc;
+        // every field carries `halo` planes below and above its owned planes
+        const long hl = (long)h->halo * h->geo.sz;
+        const size_t fb = sizeof(double) * (h->Nalloc + 2 * hl) * ncomp, sb = sizeof(double) * (h->Nalloc + 2 * hl);
         std::vector<std::pair<double **, size_t>> fields = {{&h->U, fb}, {&h->U2, fb}, {&h->V, fb},
                                                             {&h->A, fb}, {&h->R, sb},  {&h->Wk, sb}};
         if (ncomp == 3)
             for (auto f : std::initializer_list<std::pair<double **, size_t>>{
                      {&h->W, fb}, {&h->T1, sb}, {&h->T2, sb}, {&h->T3, sb}})
                 fields.push_back(f);
+        if (dist) {
+            fields.push_back({&h->tip_prev, sizeof(double) * p * h->geo.sz});
+            fields.push_back({&h->tip_next, sizeof(double) * p * h->geo.sz});
+        }
         for (auto &f : fields)
             if (rc == ADS_OK) rc = dalloc(h, (void **)f.first, f.second);
         if (rc == ADS_OK && (rc = dalloc(h, (void **)&h->dpartial, sizeof(double) * 1024)) == ADS_OK &&
@@ -590,12 +862,14 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
             if (e != cudaSuccess) rc = fail(h, ADS_E_CUDA, "stream: %s", cudaGetErrorString(e));
             h->own_stream = true;
         }
-        if (rc == ADS_OK) {  // zero everything: the row padding of every field stays 0 forever
+        if (rc == ADS_OK) {  // zero everything: row padding and domain-boundary halos stay 0 forever
             for (auto &f : fields) cudaMemsetAsync(*f.first, 0, f.second, h->stream);
             if (cudaStreamSynchronize(h->stream) != cudaSuccess) rc = fail(h, ADS_E_CUDA, "memset failed");
+            for (int f = 0; f < 6 + (ncomp == 3 ? 4 : 0); ++f) *fields[f].first += hl;  // owned planes
         }
     }
     if (rc != ADS_OK) {
+        h->comm = nullptr;  // owned by the caller of create_common
         ads_destroy(h);
         return rc;
     }
@@ -616,6 +890,87 @@ int ads_create_elastic(ads_handle *out, int nx, int ny, int nz, int p, double ta
     return create_common(out, nx, ny, nz, p, tau, bc, 3, lambda, mu, rho);
 }
 
+int ads_get_unique_id(unsigned char uid[128]) {
+    if (!uid) return ADS_E_INVAL;
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return ADS_E_NCCL;
+    std::memcpy(uid, &id, sizeof id);
+    return ADS_OK;
+}
+
+int ads_slab_plan(int nz, int p, int world, int rank, int *z_begin, int *z_count) {
+    if (nz < 1 || p < 1 || world < 1 || rank < 0 || rank >= world || !z_begin || !z_count) return ADS_E_INVAL;
+    std::vector<int> z0s, nls;
+    slab_plan(nz + p, world, z0s, nls);
+    *z_begin = z0s[rank];
+    *z_count = nls[rank];
+    return ADS_OK;
+}
+
+int ads_create_dist(ads_handle *out, int nx, int ny, int nz, int p, double tau, int bc, int rank, int world,
+                    const unsigned char uid[128], int device) {
+    if (!out || !uid || world < 1 || rank < 0 || rank >= world) return ADS_E_INVAL;
+    *out = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess) return ADS_E_CUDA;
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof id);
+    ncclComm_t comm = nullptr;
+    if (ncclCommInitRank(&comm, world, id, rank) != ncclSuccess) return ADS_E_NCCL;
+    int rc = create_common(out, nx, ny, nz, p, tau, bc, 1, 0.0, 0.0, 1.0, 1, rank, world, comm);
+    if (rc != ADS_OK) ncclCommDestroy(comm);
+    return rc;
+}
+
+int ads_create_virtual(ads_handle *out, int nx, int ny, int nz, int p, double tau, int bc, int nslabs) {
+    if (!out || nslabs < 1) return ADS_E_INVAL;
+    *out = nullptr;
+    ads_ctx *G = new (std::nothrow) ads_ctx;
+    if (!G) return ADS_E_NOMEM;
+    G->dist = 2;
+    G->world = nslabs;
+    G->p = p;
+    G->bc = bc;
+    G->tau = tau;
+    G->nel[0] = nx;
+    G->nel[1] = ny;
+    G->nel[2] = nz;
+    for (int d = 0; d < 3; ++d) G->n[d] = G->nel[d] + p;
+    G->ngz = G->n[2];
+    G->N = (long)G->n[0] * G->n[1] * G->n[2];
+    cudaGetDevice(&G->device);
+    int rc = ADS_OK;
+    if (cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking) != cudaSuccess) rc = ADS_E_CUDA;
+    G->own_stream = true;
+    for (int r = 0; r < nslabs && rc == ADS_OK; ++r) {
+        ads_handle m = nullptr;
+        rc = create_common(&m, nx, ny, nz, p, tau, bc, 1, 0.0, 0.0, 1.0, 3, r, nslabs, nullptr);
+        if (rc == ADS_OK) {
+            G->members.push_back(m);
+            rc = ads_set_stream(m, G->stream);  // one stream orders every slab's work
+        } else if (m) {
+            G->err = m->err;
+        }
+    }
+    for (int r = 0; r < (int)G->members.size(); ++r) {
+        G->members[r]->prev = r > 0 ? G->members[r - 1] : nullptr;
+        G->members[r]->next = r + 1 < (int)G->members.size() ? G->members[r + 1] : nullptr;
+    }
+    if (rc != ADS_OK) {
+        ads_destroy(G);
+        return rc;
+    }
+    *out = G;
+    return ADS_OK;
+}
+
+int ads_local_extent(ads_handle h, int *z_begin, int *z_count) {
+    if (!h || !z_begin || !z_count) return ADS_E_INVAL;
+    *z_begin = h->dist == 2 ? 0 : h->zbeg;
+    *z_count = h->dist == 2 ? h->ngz : h->n[2];
+    return ADS_OK;
+}
+
 int ads_set_stream(ads_handle h, void *stream) {
     int rc = guard(h);
     if (rc) return rc;
@@ -628,6 +983,8 @@ int ads_set_stream(ads_handle h, void *stream) {
         CUDA_TRY(h, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         h->own_stream = true;
     }
+    for (ads_ctx *m : h->members)
+        if ((rc = ads_set_stream(m, h->stream))) return rc;
     return ADS_OK;
 }
 
@@ -637,7 +994,7 @@ int ads_load_vector(ads_handle h, int d, int func, double c, double sigma, doubl
     if (d < 0 || d > 2 || !out || (func != ADS_FUNC_SIN && func != ADS_FUNC_GAUSS) ||
         (func == ADS_FUNC_GAUSS && !(sigma > 0.0)))
         return fail(h, ADS_E_INVAL, "ads_load_vector: bad argument");
-    load_vector(h->sp[d], func, c, sigma, out);
+    load_vector((h->dist == 2 ? h->members[0] : h)->sp[d], func, c, sigma, out);
     return ADS_OK;
 }
 
@@ -645,7 +1002,7 @@ int ads_mass_solve_1d(ads_handle h, int d, double *x) {
     int rc = guard(h);
     if (rc) return rc;
     if (d < 0 || d > 2 || !x) return fail(h, ADS_E_INVAL, "ads_mass_solve_1d: bad argument");
-    lu_solve_host(h->mass_lu[d], x);
+    lu_solve_host((h->dist == 2 ? h->members[0] : h)->mass_lu[d], x);
     return ADS_OK;
 }
 
@@ -655,19 +1012,23 @@ int ads_set_source(ads_handle h, const double *bx, const double *by, const doubl
     if (rc) return rc;
     if (!bx) {
         h->has_src = false;
+        for (ads_ctx *m : h->members) m->has_src = false;
         return ADS_OK;
     }
     if (h->ncomp != 1) return fail(h, ADS_E_INVAL, "ads_set_source: P-wave handles only (elastic f = 0)");
     if (!by || !bz || (wavelet != ADS_WAVELET_NONE && wavelet != ADS_WAVELET_RICKER))
         return fail(h, ADS_E_INVAL, "ads_set_source: bad argument");
+    for (ads_ctx *m : h->members)
+        if ((rc = ads_set_source(m, bx, by, bz, wavelet, f0, t0, amp))) return fail(h, rc, "member: %s", m->err.c_str());
     const double *b[3] = {bx, by, bz};
-    for (int d = 0; d < 3; ++d) {
-        std::vector<double> v(b[d], b[d] + h->n[d]);
-        if (h->bc == ADS_BC_DIRICHLET0) v[0] = v[h->n[d] - 1] = 0.0;
+    for (int d = 0; d < 3 && h->dist != 2; ++d) {
+        const int nd = d == 2 ? h->ngz : h->n[d];  // z: global rows (slabs index with zbeg)
+        std::vector<double> v(b[d], b[d] + nd);
+        if (h->bc == ADS_BC_DIRICHLET0) v[0] = v[nd - 1] = 0.0;
         if (!h->src[d]) {
-            if ((rc = dalloc(h, (void **)&h->src[d], sizeof(double) * h->n[d]))) return rc;
+            if ((rc = dalloc(h, (void **)&h->src[d], sizeof(double) * nd))) return rc;
         }
-        CUDA_TRY(h, cudaMemcpy(h->src[d], v.data(), sizeof(double) * h->n[d], cudaMemcpyHostToDevice));
+        CUDA_TRY(h, cudaMemcpy(h->src[d], v.data(), sizeof(double) * nd, cudaMemcpyHostToDevice));
     }
     h->has_src = true;
     h->wavelet = wavelet;
@@ -681,18 +1042,22 @@ int ads_set_state(ads_handle h, const double *u, const double *udot, int mem) {
     int rc = guard(h);
     if (rc) return rc;
     if (!u || (mem != ADS_MEM_HOST && mem != ADS_MEM_DEVICE)) return fail(h, ADS_E_INVAL, "ads_set_state: bad argument");
-    for (int c = 0; c < h->ncomp; ++c) {
-        if ((rc = copy_in(h, comp(h->U, h, c), u + c * h->N, mem))) return rc;
-        if (udot) {
-            if ((rc = copy_in(h, comp(h->V, h, c), udot + c * h->N, mem))) return rc;
-        } else {
-            CUDA_TRY(h, cudaMemsetAsync(comp(h->V, h, c), 0, sizeof(double) * h->Nalloc, h->stream));
-        }
-        if (h->bc == ADS_BC_DIRICHLET0) {
-            launch_mask_boundary(comp(h->U, h, c), h->geo, h->stream);
-            if ((rc = check_launch(h, "mask"))) return rc;
-            launch_mask_boundary(comp(h->V, h, c), h->geo, h->stream);
-            if ((rc = check_launch(h, "mask"))) return rc;
+    for (ads_ctx *m : slabs_of(h)) {
+        // group members read their planes out of the caller's global arrays
+        const long off = h->dist == 2 ? (long)m->zbeg * m->n[0] * m->n[1] : 0;
+        for (int c = 0; c < m->ncomp; ++c) {
+            if ((rc = copy_in(m, comp(m->U, m, c), u + off + c * m->N, mem))) return rc;
+            if (udot) {
+                if ((rc = copy_in(m, comp(m->V, m, c), udot + off + c * m->N, mem))) return rc;
+            } else {
+                CUDA_TRY(m, cudaMemsetAsync(comp(m->V, m, c), 0, sizeof(double) * m->Nalloc, m->stream));
+            }
+            if (m->bc == ADS_BC_DIRICHLET0) {
+                launch_mask_boundary(comp(m->U, m, c), m->geo, m->stream, m->zbeg, m->ngz);
+                if ((rc = check_launch(m, "mask"))) return rc;
+                launch_mask_boundary(comp(m->V, m, c), m->geo, m->stream, m->zbeg, m->ngz);
+                if ((rc = check_launch(m, "mask"))) return rc;
+            }
         }
     }
     return h->ncomp == 3 ? el_init(h) : init_state(h);
@@ -707,33 +1072,37 @@ int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const i
     for (int t = 0; t < nterms; ++t)
         if (cmp && (cmp[t] < 0 || cmp[t] >= h->ncomp))
             return fail(h, ADS_E_INVAL, "component %d on a handle with %d components", cmp[t], h->ncomp);
-    CUDA_TRY(h, cudaMemsetAsync(h->U, 0, sizeof(double) * h->Nalloc * h->ncomp, h->stream));
-    CUDA_TRY(h, cudaMemsetAsync(h->V, 0, sizeof(double) * h->Nalloc * h->ncomp, h->stream));
-    if (nterms > 0) {
-        const int n0 = h->n[0], n1 = h->n[1], n2 = h->n[2];
-        std::vector<double> packed((size_t)nterms * (n0 + n1 + n2));
-        double *d = nullptr;
-        if ((rc = dalloc(h, (void **)&d, sizeof(double) * packed.size()))) return rc;
-        for (int t = 0; t < nterms; ++t) {
-            std::memcpy(&packed[(size_t)t * (n0 + n1 + n2)], sx + (size_t)t * n0, sizeof(double) * n0);
-            std::memcpy(&packed[(size_t)t * (n0 + n1 + n2) + n0], sy + (size_t)t * n1, sizeof(double) * n1);
-            std::memcpy(&packed[(size_t)t * (n0 + n1 + n2) + n0 + n1], sz + (size_t)t * n2, sizeof(double) * n2);
+    for (ads_ctx *m : slabs_of(h)) {
+        CUDA_TRY(m, cudaMemsetAsync(m->U, 0, sizeof(double) * m->Nalloc * m->ncomp, m->stream));
+        CUDA_TRY(m, cudaMemsetAsync(m->V, 0, sizeof(double) * m->Nalloc * m->ncomp, m->stream));
+        if (nterms > 0) {
+            // factors: sx n0, sy n1, sz ngz (global z); a slab uses rows [zbeg, zbeg + nl)
+            const int n0 = m->n[0], n1 = m->n[1], n2 = m->ngz;
+            std::vector<double> packed((size_t)nterms * (n0 + n1 + n2));
+            double *d = nullptr;
+            if ((rc = dalloc(m, (void **)&d, sizeof(double) * packed.size()))) return rc;
+            for (int t = 0; t < nterms; ++t) {
+                std::memcpy(&packed[(size_t)t * (n0 + n1 + n2)], sx + (size_t)t * n0, sizeof(double) * n0);
+                std::memcpy(&packed[(size_t)t * (n0 + n1 + n2) + n0], sy + (size_t)t * n1, sizeof(double) * n1);
+                std::memcpy(&packed[(size_t)t * (n0 + n1 + n2) + n0 + n1], sz + (size_t)t * n2, sizeof(double) * n2);
+            }
+            CUDA_TRY(m, cudaMemcpy(d, packed.data(), sizeof(double) * packed.size(), cudaMemcpyHostToDevice));
+            for (int t = 0; t < nterms; ++t) {
+                const double *b = d + (size_t)t * (n0 + n1 + n2);
+                launch_add_separable(comp(m->U, m, cmp ? cmp[t] : 0), amp[t], b, b + n0, b + n0 + n1 + m->zbeg, m->geo,
+                                     m->stream);
+                if ((rc = check_launch(m, "separable"))) return rc;
+            }
+            CUDA_TRY(m, cudaStreamSynchronize(m->stream));
+            cudaFree(d);
+            m->allocs.pop_back();
         }
-        CUDA_TRY(h, cudaMemcpy(d, packed.data(), sizeof(double) * packed.size(), cudaMemcpyHostToDevice));
-        for (int t = 0; t < nterms; ++t) {
-            const double *b = d + (size_t)t * (n0 + n1 + n2);
-            launch_add_separable(comp(h->U, h, cmp ? cmp[t] : 0), amp[t], b, b + n0, b + n0 + n1, h->geo, h->stream);
-            if ((rc = check_launch(h, "separable"))) return rc;
-        }
-        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-        cudaFree(d);
-        h->allocs.pop_back();
+        if (m->bc == ADS_BC_DIRICHLET0)
+            for (int c = 0; c < m->ncomp; ++c) {
+                launch_mask_boundary(comp(m->U, m, c), m->geo, m->stream, m->zbeg, m->ngz);
+                if ((rc = check_launch(m, "mask"))) return rc;
+            }
     }
-    if (h->bc == ADS_BC_DIRICHLET0)
-        for (int c = 0; c < h->ncomp; ++c) {
-            launch_mask_boundary(comp(h->U, h, c), h->geo, h->stream);
-            if ((rc = check_launch(h, "mask"))) return rc;
-        }
     return h->ncomp == 3 ? el_init(h) : init_state(h);
 }
 
@@ -749,6 +1118,12 @@ int ads_step(ads_handle h, int nsteps) {
             continue;
         }
         const double t1 = (double)(h->step + 1) * h->tau;  // F at t_{n+1} (C14)
+        if (h->dist) {
+            if ((rc = dist_solve(h, h->tau, source_g(h, t1), h->tau, s == nsteps - 1))) return rc;
+            h->step += 1;
+            for (ads_ctx *m : h->members) m->step = h->step;
+            continue;
+        }
         // drift + RHS: U2 = U + tau V, R = F(t_{n+1}) - K U2
         if ((rc = run_kop(h, h->U, h->V, h->tau, source_g(h, t1), -1.0, h->U2, h->R))) return rc;
         // a = D^-1 R; V += tau a; keep a only on the last step of the batch
@@ -767,35 +1142,8 @@ int ads_energy(ads_handle h, double out[3]) {
     double res[3];
     if (h->ncomp == 3) {
         if ((rc = el_energy(h, res))) return rc;
-    } else {
-        const Geom &g = h->geo;
-        const long N = h->Nalloc;  // padding entries are 0 in every field
-        // v = V - tau/2 a ; kinetic = 1/2 v' M v
-        CUDA_TRY(h, cudaMemcpyAsync(h->R, h->V, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->stream));
-        launch_axpby(N, -0.5 * h->tau, h->A, 1.0, h->R, h->stream);
-        if ((rc = check_launch(h, "axpby"))) return rc;
-        launch_axis_apply(h->p, 0, h->dd[0].mband, h->R, h->Wk, g, 1.0, 0.0, h->stream);
-        launch_axis_apply(h->p, 1, h->dd[1].mband, h->Wk, h->U2, g, 1.0, 0.0, h->stream);
-        launch_axis_apply(h->p, 2, h->dd[2].mband, h->U2, h->Wk, g, 1.0, 0.0, h->stream);
-        if ((rc = check_launch(h, "axis_apply"))) return rc;
-        launch_dot(N, h->R, h->Wk, h->dpartial, h->dres + 0, h->stream);
-        // potential = 1/2 U' K U
-        if ((rc = run_kop(h, h->U, h->V, 0.0, 0.0, 1.0, nullptr, h->R))) return rc;
-        launch_dot(N, h->U, h->R, h->dpartial, h->dres + 1, h->stream);
-        // invariant = 1/2 V' D V + 1/2 U_n' K U_{n+1}
-        launch_axis_apply(h->p, 0, h->dd[0].aband, h->V, h->Wk, g, 1.0, 0.0, h->stream);
-        launch_axis_apply(h->p, 1, h->dd[1].aband, h->Wk, h->U2, g, 1.0, 0.0, h->stream);
-        launch_axis_apply(h->p, 2, h->dd[2].aband, h->U2, h->Wk, g, 1.0, 0.0, h->stream);
-        launch_dot(N, h->V, h->Wk, h->dpartial, h->dres + 2, h->stream);
-        if ((rc = run_kop(h, h->U, h->V, h->tau, 0.0, 1.0, nullptr, h->R))) return rc;
-        launch_dot(N, h->U, h->R, h->dpartial, h->dres + 3, h->stream);
-        if ((rc = check_launch(h, "dot"))) return rc;
-        double d4[4];
-        CUDA_TRY(h, cudaMemcpyAsync(d4, h->dres, sizeof(double) * 4, cudaMemcpyDeviceToHost, h->stream));
-        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-        res[0] = 0.5 * d4[0];
-        res[1] = 0.5 * d4[1];
-        res[2] = 0.5 * d4[2] + 0.5 * d4[3];
+    } else if ((rc = pwave_energy(h, res))) {
+        return rc;
     }
     for (int i = 0; i < 3; ++i) {
         if (!std::isfinite(res[i])) return fail(h, ADS_E_STATE, "non-finite energy (NaN/Inf in state)");
@@ -808,18 +1156,21 @@ int ads_get_state(ads_handle h, double *u, double *udot, double *a, int mem) {
     int rc = guard(h);
     if (rc) return rc;
     if (mem != ADS_MEM_HOST && mem != ADS_MEM_DEVICE) return fail(h, ADS_E_INVAL, "bad mem");
-    for (int c = 0; c < h->ncomp; ++c) {
-        if (u && (rc = copy_out(h, u + c * h->N, comp(h->U, h, c), mem))) return rc;
-        if (udot) {
-            CUDA_TRY(h, cudaMemcpyAsync(h->Wk, comp(h->V, h, c), sizeof(double) * h->Nalloc, cudaMemcpyDeviceToDevice,
-                                        h->stream));
-            launch_axpby(h->Nalloc, -0.5 * h->tau, comp(h->A, h, c), 1.0, h->Wk, h->stream);
-            if ((rc = check_launch(h, "axpby"))) return rc;
-            if ((rc = copy_out(h, udot + c * h->N, h->Wk, mem))) return rc;
+    for (ads_ctx *m : slabs_of(h)) {
+        const long off = h->dist == 2 ? (long)m->zbeg * m->n[0] * m->n[1] : 0;
+        for (int c = 0; c < m->ncomp; ++c) {
+            if (u && (rc = copy_out(m, u + off + c * m->N, comp(m->U, m, c), mem))) return rc;
+            if (udot) {
+                CUDA_TRY(m, cudaMemcpyAsync(m->Wk, comp(m->V, m, c), sizeof(double) * m->Nalloc,
+                                            cudaMemcpyDeviceToDevice, m->stream));
+                launch_axpby(m->Nalloc, -0.5 * m->tau, comp(m->A, m, c), 1.0, m->Wk, m->stream);
+                if ((rc = check_launch(m, "axpby"))) return rc;
+                if ((rc = copy_out(m, udot + off + c * m->N, m->Wk, mem))) return rc;
+            }
+            if (a && (rc = copy_out(m, a + off + c * m->N, comp(m->A, m, c), mem))) return rc;
         }
-        if (a && (rc = copy_out(h, a + c * h->N, comp(h->A, h, c), mem))) return rc;
+        CUDA_TRY(m, cudaStreamSynchronize(m->stream));
     }
-    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     return ADS_OK;
 }
 
@@ -840,6 +1191,7 @@ int ads_dims(ads_handle h, int *nx, int *ny, int *nz, int *ncomp) {
 int ads_apply_k(ads_handle h, const double *x, double *out) {
     int rc = guard(h);
     if (rc) return rc;
+    if (h->dist) return fail(h, ADS_E_INVAL, "unit operators: single-GPU handles only");
     if (!x || !out || x == out) return fail(h, ADS_E_INVAL, "ads_apply_k: bad pointers");
     for (int c = 0; c < h->ncomp; ++c)
         if ((rc = copy_in(h, comp(h->U2, h, c), x + c * h->N, ADS_MEM_DEVICE))) return rc;
@@ -856,6 +1208,7 @@ int ads_apply_k(ads_handle h, const double *x, double *out) {
 int ads_solve_d(ads_handle h, const double *x, double *out) {
     int rc = guard(h);
     if (rc) return rc;
+    if (h->dist) return fail(h, ADS_E_INVAL, "unit operators: single-GPU handles only");
     if (!x || !out) return fail(h, ADS_E_INVAL, "ads_solve_d: bad pointers");
     if (h->ncomp == 3) {
         for (int c = 0; c < 3; ++c)
@@ -876,17 +1229,24 @@ int ads_sweep(ads_handle h, int d, const double *x, double *out) {
     int rc = guard(h);
     if (rc) return rc;
     if (!x || !out || d < 0 || d > 2) return fail(h, ADS_E_INVAL, "ads_sweep: bad argument");
-    if (h->ncomp != 1) return fail(h, ADS_E_INVAL, "ads_sweep: P-wave handles only");
+    if (h->ncomp != 1 || h->dist) return fail(h, ADS_E_INVAL, "ads_sweep: single-GPU P-wave handles only");
     if ((rc = copy_in(h, h->R, x, ADS_MEM_DEVICE))) return rc;
     if ((rc = run_sweep(h, d, h->R, h->Wk, nullptr, 0.0))) return rc;
     return copy_out(h, out, h->Wk, ADS_MEM_DEVICE);
 }
 
-long ads_launch_count(ads_handle h) { return h ? h->launches : -1; }
+long ads_launch_count(ads_handle h) {
+    if (!h) return -1;
+    long n = h->launches;
+    for (ads_ctx *m : h->members) n += m->launches;
+    return n;
+}
 
 int ads_profile_enable(ads_handle h, int on) {
     int rc = guard(h);
     if (rc) return rc;
+    for (ads_ctx *m : h->members)
+        if ((rc = ads_profile_enable(m, on))) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     h->prof = on != 0;
     h->prof_rec.clear();
@@ -903,11 +1263,14 @@ int ads_profile_read(ads_handle h, double *ms, long *count) {
         ms[c] = 0.0;
         count[c] = 0;
     }
-    for (auto &r : h->prof_rec) {
-        float t = 0.f;
-        CUDA_TRY(h, cudaEventElapsedTime(&t, r.second.first, r.second.second));
-        ms[r.first] += t;
-        count[r.first] += 1;
+    for (ads_ctx *m : slabs_of(h)) {
+        CUDA_TRY(m, cudaStreamSynchronize(m->stream));
+        for (auto &r : m->prof_rec) {
+            float t = 0.f;
+            CUDA_TRY(m, cudaEventElapsedTime(&t, r.second.first, r.second.second));
+            ms[r.first] += t;
+            count[r.first] += 1;
+        }
     }
     return ADS_OK;
 }
@@ -917,6 +1280,9 @@ const char *ads_last_error(ads_handle h) { return h ? h->err.c_str() : "null han
 int ads_destroy(ads_handle h) {
     if (!h) return ADS_OK;
     if (h->stream) cudaStreamSynchronize(h->stream);
+    for (ads_ctx *m : h->members) ads_destroy(m);
+    h->members.clear();
+    if (h->comm && h->dist == 1) ncclCommDestroy(h->comm);
     for (void *p : h->allocs) cudaFree(p);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);

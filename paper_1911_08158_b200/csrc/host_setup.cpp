@@ -375,3 +375,92 @@ void build_part_tables(const LUFactors &f, int C, int L, PartTables &t) {
 }
 
 }  // namespace ads
+
+namespace ads {
+
+void slab_plan(int n, int G, std::vector<int> &z0, std::vector<int> &nl) {
+    z0.assign(G, 0);
+    nl.assign(G, 0);
+    int at = 0;
+    for (int j = 0; j < G; ++j) {
+        nl[j] = n / G + (j < n % G ? 1 : 0);
+        z0[j] = at;
+        at += nl[j];
+    }
+}
+
+int build_slab_spikes(const Band &A, int z0, int nl, SlabSpikes &s) {
+    const int p = A.p, n = A.n, z1 = z0 + nl;
+    s.block = Band(nl, p);
+    for (int i = 0; i < nl; ++i)
+        for (int j = i - p; j <= i + p; ++j)
+            if (j >= 0 && j < nl) s.block.at(i, j) = A.get(z0 + i, z0 + j);
+    if (banded_lu(s.block, s.lu)) return -2;
+    s.V.assign((size_t)nl * p, 0.0);
+    s.W.assign((size_t)nl * p, 0.0);
+    std::vector<double> col(nl);
+    for (int b = 0; b < p; ++b) {
+        // V column b: rhs rows nl-p+a hold B(a, b) = A(z1 - p + a, z1 + b)
+        std::fill(col.begin(), col.end(), 0.0);
+        for (int a = 0; a < p; ++a)
+            if (nl - p + a >= 0 && z1 + b < n) col[nl - p + a] = A.get(z1 - p + a, z1 + b);
+        lu_solve_host(s.lu, col.data());
+        for (int i = 0; i < nl; ++i) s.V[(size_t)i * p + b] = col[i];
+        // W column b: rhs rows a hold C(a, b) = A(z0 + a, z0 - p + b)
+        std::fill(col.begin(), col.end(), 0.0);
+        for (int a = 0; a < p; ++a)
+            if (a < nl && z0 - p + b >= 0) col[a] = A.get(z0 + a, z0 - p + b);
+        lu_solve_host(s.lu, col.data());
+        for (int i = 0; i < nl; ++i) s.W[(size_t)i * p + b] = col[i];
+    }
+    return 0;
+}
+
+double interface_inverse(const SlabSpikes &sj, const SlabSpikes &sj1, int p, std::vector<double> &Q) {
+    const int nl = sj.block.n, m = 2 * p;
+    std::vector<double> S((size_t)m * m, 0.0);
+    for (int a = 0; a < p; ++a) {
+        S[a * m + a] = 1.0;
+        S[(p + a) * m + p + a] = 1.0;
+        for (int b = 0; b < p; ++b) {
+            S[a * m + p + b] = sj.V[(size_t)(nl - p + a) * p + b];  // Vbot_j
+            S[(p + a) * m + b] = sj1.W[(size_t)a * p + b];          // Wtop_{j+1}
+        }
+    }
+    // Gauss-Jordan with partial pivoting (2p <= 10)
+    Q.assign((size_t)m * m, 0.0);
+    for (int a = 0; a < m; ++a) Q[a * m + a] = 1.0;
+    for (int c = 0; c < m; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < m; ++r)
+            if (std::fabs(S[r * m + c]) > std::fabs(S[piv * m + c])) piv = r;
+        for (int k = 0; k < m; ++k) {
+            std::swap(S[c * m + k], S[piv * m + k]);
+            std::swap(Q[c * m + k], Q[piv * m + k]);
+        }
+        const double d = S[c * m + c];
+        for (int k = 0; k < m; ++k) {
+            S[c * m + k] /= d;
+            Q[c * m + k] /= d;
+        }
+        for (int r = 0; r < m; ++r)
+            if (r != c) {
+                const double f = S[r * m + c];
+                for (int k = 0; k < m; ++k) {
+                    S[r * m + k] -= f * S[c * m + k];
+                    Q[r * m + k] -= f * Q[c * m + k];
+                }
+            }
+    }
+    // dropped couplings: W_j bottom p rows (slab j's own W) and V_{j+1} top p rows
+    double dropped = 0.0;
+    const int nl1 = sj1.block.n;
+    for (int a = 0; a < p; ++a)
+        for (int b = 0; b < p; ++b) {
+            dropped = std::max(dropped, std::fabs(sj.W[(size_t)(nl - p + a) * p + b]));
+            if (a < nl1) dropped = std::max(dropped, std::fabs(sj1.V[(size_t)a * p + b]));
+        }
+    return dropped;
+}
+
+}  // namespace ads

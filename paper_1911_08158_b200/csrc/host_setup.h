@@ -88,3 +88,27 @@ int choose_chunk_len(int n, int p, int C);
 void build_part_tables(const LUFactors &f, int C, int L, PartTables &t);
 
 }  // namespace ads
+
+namespace ads {
+
+// ---- z-slab decomposition (multi-GPU) ----
+// Balanced split of n planes over G slabs: slab j = [z0[j], z0[j] + nl[j]).
+void slab_plan(int n, int G, std::vector<int> &z0, std::vector<int> &nl);
+
+// Distributed exact SPIKE for A (global band, Dirichlet rows set) cut into slabs:
+//   x_j = xloc_j - V_j u_{j+1} - W_j b_{j-1},  xloc_j = A_jj^-1 r_j,
+//   V_j = A_jj^-1 [0; B_j], W_j = A_jj^-1 [C_j; 0]   (p spike columns, [nl][p] row-major),
+// u_{j+1} = first p values of x_{j+1}, b_{j-1} = last p values of x_{j-1}.  Interface j|j+1:
+//   [b_j; u_{j+1}] = Q_j [bl_j; ul_{j+1}],  Q_j = inverse of [[I, Vbot_j], [Wtop_{j+1}, I]]
+// which is exact when the dropped couplings W_j(bottom p rows) and V_{j+1}(top p rows) are
+// below 2^-64 (certified: `certified`), i.e. the spikes decay across a slab.
+struct SlabSpikes {
+    LUFactors lu;             // (unused by the device: tables are rebuilt from `block`)
+    Band block;               // A_jj
+    std::vector<double> V, W; // [nl][p]
+};
+int build_slab_spikes(const Band &A, int z0, int nl, SlabSpikes &s);
+// Q_j (2p x 2p row-major) from slab j and j+1; returns the max dropped coupling entry.
+double interface_inverse(const SlabSpikes &sj, const SlabSpikes &sj1, int p, std::vector<double> &Q);
+
+}  // namespace ads

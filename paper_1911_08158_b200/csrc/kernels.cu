@@ -448,9 +448,9 @@ __device__ __forceinline__ void kop_zscatter(const KopArgs &a, double (&A0)[2 * 
             const int sl = ((U - P + c) % W + W) % W;
             const int k = kk - P + c;
             double mz_ = 0.0, kz_ = 0.0;
-            if (k >= 0 && k < n2) {
-                mz_ = __ldg(a.mz + (long)k * W + 2 * P - c);
-                kz_ = __ldg(a.kz + (long)k * W + 2 * P - c);
+            if (k >= 0 && k < n2) {  // output planes; band rows are global rows k + zoff
+                mz_ = __ldg(a.mz + (long)(k + a.zoff) * W + 2 * P - c);
+                kz_ = __ldg(a.kz + (long)(k + a.zoff) * W + 2 * P - c);
             }
             A0[sl] = fma(mz_, s0, A0[sl]);
             A0[sl] = fma(kz_, t0, A0[sl]);
@@ -461,7 +461,7 @@ __device__ __forceinline__ void kop_zscatter(const KopArgs &a, double (&A0)[2 * 
     constexpr int so = ((U - P) % W + W) % W;  // slot of the completed output k = kk - P
     const int k = kk - P;
     if (k >= z0) {
-        const double gz = a.bx ? a.g * __ldg(a.bz + k) : 0.0;
+        const double gz = a.bx ? a.g * __ldg(a.bz + k + a.zoff) : 0.0;
         const long o = (long)k * a.geo.sz + oxy;
         if (own0) a.r[o] = fma(a.sign, A0[so], gz * sxy0);
         if (own1) a.r[o + a.geo.sy] = fma(a.sign, A1[so], gz * sxy1);
@@ -516,7 +516,7 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
         if (copier && ii < npl) {
             const int kk = kk0 + ii;
             const unsigned su = ring_s + 8u * (unsigned)((ii & (KT_NPF - 1)) * 2 * HN);
-            const bool kv = kk >= 0 && kk < n2;
+            const bool kv = kk >= a.zv0 && kk < a.zv1;
             const double *pu = a.U + (kv ? (long)kk * sz : 0), *pv = a.V + (kv ? (long)kk * sz : 0);
 #pragma unroll
             for (int m = 0; m < G::NSLOT; ++m) {
@@ -634,7 +634,7 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
             }
         }
         // ---- z-pass (a switch makes every ring slot index compile-time)
-        const bool zint = kk - P >= a.ilo[2] && kk + P <= a.ihi[2];
+        const bool zint = kk + a.zoff - P >= a.ilo[2] && kk + a.zoff + P <= a.ihi[2];
         switch (ii % W) {
 #define ADS_ZCASE(U)                                                                                          \
     case U:                                                                                                   \
@@ -660,17 +660,86 @@ __global__ void __launch_bounds__(KT_THREADS, 2) kop_kernel(const KopArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
+// distributed z-solve fix-up + kick (see kernels.cuh ZfixArgs).  Thread per z-line of the
+// slab (coalesced across x), streaming the nl owned planes once: 24 B/DOF (+8 when a is kept).
+// ------------------------------------------------------------------------------------------
+template <int P>
+__global__ void __launch_bounds__(256) zfix_kernel(const ZfixArgs a) {
+    const Geom &g = a.geo;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+    if (i >= g.n0 || j >= g.n1) return;
+    const int nl = g.n2;
+    const long base = (long)j * g.sy + i;
+    double bp[P], un[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) bp[m] = un[m] = 0.0;
+    if (a.tip_prev) {
+        double t[2 * P];
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            t[m] = a.tip_prev[base + (long)m * g.sz];
+            t[P + m] = a.X[base + (long)m * g.sz];
+        }
+#pragma unroll
+        for (int r = 0; r < P; ++r)
+#pragma unroll
+            for (int c = 0; c < 2 * P; ++c) bp[r] = fma(a.qt[r][c], t[c], bp[r]);
+    }
+    if (a.tip_next) {
+        double t[2 * P];
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            t[m] = a.X[base + (long)(nl - P + m) * g.sz];
+            t[P + m] = a.tip_next[base + (long)m * g.sz];
+        }
+#pragma unroll
+        for (int r = 0; r < P; ++r)
+#pragma unroll
+            for (int c = 0; c < 2 * P; ++c) un[r] = fma(a.qb[P + r][c], t[c], un[r]);
+    }
+    for (int k = 0; k < nl; ++k) {
+        const long idx = base + (long)k * g.sz;
+        double x = a.X[idx];
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            x = fma(-__ldg(a.Wsp + (long)k * P + m), bp[m], x);
+            x = fma(-__ldg(a.Vsp + (long)k * P + m), un[m], x);
+        }
+        a.Vf[idx] = fma(a.kick, x, a.Vf[idx]);
+        if (a.A) a.A[idx] = x;
+    }
+}
+
+int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {
+    dim3 blk(128), grd((a.geo.n0 + 127) / 128, a.geo.n1);
+    switch (p) {
+        case 1: zfix_kernel<1><<<grd, blk, 0, s>>>(a); break;
+        case 2: zfix_kernel<2><<<grd, blk, 0, s>>>(a); break;
+        case 3: zfix_kernel<3><<<grd, blk, 0, s>>>(a); break;
+        case 4: zfix_kernel<4><<<grd, blk, 0, s>>>(a); break;
+        case 5: zfix_kernel<5><<<grd, blk, 0, s>>>(a); break;
+        default: return -1;
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------------------------------------
 // helpers
 // ------------------------------------------------------------------------------------------
 // out = alpha (A along axis d) in + beta out  (beta == 0: out is not read).  One thread per
 // x position of a row; rows (j, k) strided over the grid's y dimension.
+// out = alpha (A along axis d) in + beta out  (beta == 0: out is not read).  One thread per
+// x position of a row; rows (j, k) strided over the grid's y dimension.  Along z the band row
+// of local plane k is global row k + zoff and input planes [zv0, zv1) exist (slab halos).
 template <int P>
 __global__ void axis_apply_kernel(int d, const double *__restrict__ band, const double *__restrict__ in,
-                                  double *__restrict__ out, Geom g, double alpha, double beta) {
+                                  double *__restrict__ out, Geom g, double alpha, double beta, int zoff, int zv0,
+                                  int zv1) {
     constexpr int W = 2 * P + 1;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= g.n0) return;
-    const int nd = d == 0 ? g.n0 : d == 1 ? g.n1 : g.n2;
+    const int lo = d == 2 ? zv0 : 0, hi = d == 0 ? g.n0 : d == 1 ? g.n1 : zv1;
+    const int ro = d == 2 ? zoff : 0;
     const long st = d == 0 ? 1 : d == 1 ? g.sy : g.sz;
     for (long row = blockIdx.y; row < (long)g.n1 * g.n2; row += gridDim.y) {
         const int j = (int)(row % g.n1), k = (int)(row / g.n1);
@@ -680,7 +749,8 @@ __global__ void axis_apply_kernel(int d, const double *__restrict__ band, const 
 #pragma unroll
         for (int c = 0; c < W; ++c) {
             const int col = r - P + c;
-            if (col >= 0 && col < nd) acc = fma(__ldg(band + (long)r * W + c), in[idx + (long)(col - r) * st], acc);
+            if (col >= lo && col < hi)
+                acc = fma(__ldg(band + (long)(r + ro) * W + c), in[idx + (long)(col - r) * st], acc);
         }
         out[idx] = beta == 0.0 ? alpha * acc : fma(alpha, acc, beta * out[idx]);
     }
@@ -691,14 +761,15 @@ __global__ void axpby_kernel(long N, double alpha, const double *__restrict__ x,
         y[q] = alpha * x[q] + beta * y[q];
 }
 
-__global__ void mask_boundary_kernel(double *u, Geom g) {
+__global__ void mask_boundary_kernel(double *u, Geom g, int zoff, int ngz) {
     long N = (long)g.n0 * g.n1 * g.n2;
     for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x) {
         int i = q % g.n0;
         long t = q / g.n0;
         int j = t % g.n1;
         int k = t / g.n1;
-        if (i == 0 || j == 0 || k == 0 || i == g.n0 - 1 || j == g.n1 - 1 || k == g.n2 - 1)
+        const int kg = k + zoff;  // global plane
+        if (i == 0 || j == 0 || kg == 0 || i == g.n0 - 1 || j == g.n1 - 1 || kg == ngz - 1)
             u[(long)k * g.sz + (long)j * g.sy + i] = 0.0;
     }
 }
@@ -778,6 +849,10 @@ static void kop_launch(const KopArgs &a, cudaStream_t s) {
     }
     KopArgs b = a;
     b.zlen = a.zlen > 0 ? a.zlen : (a.geo.n2 + best - 1) / best;
+    if (b.zv1 < b.zv0) {  // no halo planes: exactly the output planes exist
+        b.zv0 = 0;
+        b.zv1 = a.geo.n2;
+    }
     dim3 grd(gx, gy, (a.geo.n2 + b.zlen - 1) / b.zlen);
     kop_kernel<P><<<grd, KT_THREADS, sm, s>>>(b);
 }
@@ -859,16 +934,22 @@ int launch_sweep(int p, const SweepArgs &a, cudaStream_t s) {
 }
 
 int launch_axis_apply(int p, int d, const double *band, const double *in, double *out, const Geom &g, double alpha,
-                      double beta, cudaStream_t s) {
+                      double beta, cudaStream_t s, int zoff, int zv0, int zv1) {
+    if (zv1 < zv0) {
+        zv0 = 0;
+        zv1 = g.n2;
+    }
     dim3 blk(128), grd((g.n0 + 127) / 128, (unsigned)std::min<long>((long)g.n1 * g.n2, 65535));
+#define ADS_AX(PP) axis_apply_kernel<PP><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta, zoff, zv0, zv1)
     switch (p) {
-        case 1: axis_apply_kernel<1><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta); break;
-        case 2: axis_apply_kernel<2><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta); break;
-        case 3: axis_apply_kernel<3><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta); break;
-        case 4: axis_apply_kernel<4><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta); break;
-        case 5: axis_apply_kernel<5><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta); break;
+        case 1: ADS_AX(1); break;
+        case 2: ADS_AX(2); break;
+        case 3: ADS_AX(3); break;
+        case 4: ADS_AX(4); break;
+        case 5: ADS_AX(5); break;
         default: return -1;
     }
+#undef ADS_AX
     return 0;
 }
 
@@ -877,8 +958,8 @@ int launch_axpby(long N, double alpha, const double *x, double beta, double *y, 
     return 0;
 }
 
-int launch_mask_boundary(double *u, const Geom &g, cudaStream_t s) {
-    mask_boundary_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(u, g);
+int launch_mask_boundary(double *u, const Geom &g, cudaStream_t s, int zoff, int ngz) {
+    mask_boundary_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(u, g, zoff, ngz < 0 ? g.n2 : ngz);
     return 0;
 }
 

@@ -44,7 +44,25 @@ struct KopArgs {
     int zlen = 0;
     int ilo[3] = {1, 1, 1}, ihi[3] = {0, 0, 0};
     double mc[3][2 * kMaxP + 1] = {}, kc[3][2 * kMaxP + 1] = {};
+    // z-slabs: local plane k is global row k + zoff of Mz, Kz (and of bz); input planes
+    // [zv0, zv1) exist in memory (halo planes of a slab); outputs are planes [0, n2)
+    int zoff = 0, zv0 = 0, zv1 = -1;
 };
+
+// Distributed z-solve fix-up (exact SPIKE, host_setup.h build_slab_spikes) fused with the kick,
+// on the owned planes of a slab (geometry g, n2 = nl):
+//   b_prev = Qt[0:p, :] [tip_prev; X(first p)],  u_next = Qb[p:2p, :] [X(last p); tip_next]
+//   x = X - W b_prev - V u_next;  Vf += kick x;  A = x (if non-null)
+// tip_prev / tip_next: p planes (plane stride sz) received from the neighbours (null: none).
+struct ZfixArgs {
+    const double *X = nullptr, *tip_prev = nullptr, *tip_next = nullptr;
+    const double *Vsp = nullptr, *Wsp = nullptr;  // [nl][p]
+    double *Vf = nullptr, *A = nullptr;
+    double kick = 0.0;
+    double qt[2 * kMaxP][2 * kMaxP] = {}, qb[2 * kMaxP][2 * kMaxP] = {};
+    Geom geo;
+};
+int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s);
 
 // Batched banded solve along direction dir of every line of `in`.
 // mode 0: out = A^-1 in; mode 1: V += kick * (A^-1 in) and out = A^-1 in if out != nullptr.
@@ -64,12 +82,15 @@ int launch_sweep(int p, const SweepArgs &a, cudaStream_t s);
 
 // Small helpers (diagnostics / state I/O, not on the per-step path).
 // out = alpha (A along axis d) in + beta out (band table [n_d][2p+1]; beta == 0: out not read).
+// Along z: band row of local plane k is global row k + zoff; input planes [zv0, zv1) exist
+// (default: [0, n2)).
 int launch_axis_apply(int p, int d, const double *band, const double *in, double *out, const Geom &g, double alpha,
-                      double beta, cudaStream_t s);
+                      double beta, cudaStream_t s, int zoff = 0, int zv0 = 0, int zv1 = -1);
 // y = alpha x + beta y over N elements
 int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s);
 // zero the boundary faces of a field (Dirichlet masking)
-int launch_mask_boundary(double *u, const Geom &g, cudaStream_t s);
+// (slabs: local plane k is global plane k + zoff of ngz; default the field is the whole grid)
+int launch_mask_boundary(double *u, const Geom &g, cudaStream_t s, int zoff = 0, int ngz = -1);
 // u += amp * sx (x) sy (x) sz
 int launch_add_separable(double *u, double amp, const double *sx, const double *sy, const double *sz, const Geom &g,
                          cudaStream_t s);
