@@ -14,8 +14,9 @@ max over ranks.  Every field (1.09 GB) is larger than L2 (126 MB), so no L2
 flush is needed.  Per-kernel CUDA-event timing inside the library
 (ads_profile_*) gives the roofline of the dominant kernel.
 
-N > 1 (torchrun): each rank runs an independent replica of the workload (the
-z-slab-distributed handle is not built yet), reported as weak scaling.
+N > 1 (torchrun): the c4 grid is cut into N z-slabs, one per GPU (ads_create_dist: NCCL
+halo and SPIKE-tip exchanges over NVLink), reported as strong scaling: `value` is the
+whole-grid DOF-steps/s over the max-over-ranks time.
 
 --impl reference: the CPU oracle (oracle/, single thread) on a bounded sample
 of the same workload recipe; rank 0 only.
@@ -176,7 +177,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, workloads/)",
         "config": {"workload": f"{wl.name} recipe at {nel}^3 elements (bounded CPU sample)", "p": wl.p,
                    "n_dof": n, "tau": wl.tau},
@@ -194,8 +195,13 @@ def run_ours(args, rank, world, local):
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
     wl = workloads.get(args.config)
-    N = wl.ndof
-    s = ads.make_solver(wl)
+    N = wl.ndof  # global DOFs
+    if world > 1:
+        # strong scaling: the grid is cut into `world` z-slabs, one per GPU (NCCL over NVLink)
+        uid = ads.broadcast_unique_id(rank)
+        s = ads.make_solver(wl, dist=(rank, world, uid))
+    else:
+        s = ads.make_solver(wl)
     stream = torch.cuda.Stream()
     s.set_stream(stream)
     # warm-up, then restart from the initial state so every run times the same steps
@@ -218,23 +224,24 @@ def run_ours(args, rank, world, local):
     s.profile_enable(False)
     launches = s.launch_count() - launches0
     ms = max_over_ranks(ms, world)
-    value = N * args.steps * world / (ms / 1e3)
+    value = N * args.steps / (ms / 1e3)  # whole-job DOF-steps/s (every rank's slab together)
 
     # ---- roofline of the dominant kernel (algorithmic bytes / its average launch time)
     hbm, peak_kind, _ = peaks()
     shares = kms / kms.sum() if kms.sum() > 0 else kms
     dom = int(np.argmax(kms))
     per_launch_ms = kms / np.maximum(kcnt, 1)
+    Nloc = s.N  # this rank's DOFs (the per-kernel rooflines are per GPU)
     kernels = {}
     for i, name in enumerate(KERNELS):
         bpd = BYTES_PER_DOF[i]
         if i == 3:  # a is stored on the last step of a batch only
             bpd = BYTES_PER_DOF[i] + 8.0 / max(kcnt[i], 1)
-        gbs = N * bpd / (per_launch_ms[i] / 1e3) / 1e9 if per_launch_ms[i] > 0 else 0.0
+        gbs = Nloc * bpd / (per_launch_ms[i] / 1e3) / 1e9 if per_launch_ms[i] > 0 else 0.0
         kernels[name] = {"ms_per_launch": per_launch_ms[i], "launches": int(kcnt[i]), "share": float(shares[i]),
                          "bytes_per_dof": bpd, "achieved_gbs": gbs, "frac": gbs / hbm}
     achieved = kernels[KERNELS[dom]]["achieved_gbs"]
-    step_bytes = N * (sum(BYTES_PER_DOF) + 8.0 / args.steps)
+    step_bytes = Nloc * (sum(BYTES_PER_DOF) + 8.0 / args.steps)
     roofline = {"bound": "hbm", "kernel": KERNELS[dom], "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
                 "step_achieved": step_bytes / (ms / args.steps / 1e3) / 1e9,
@@ -256,7 +263,7 @@ def run_ours(args, rank, world, local):
     s.get_state(u_host, ud_host, a_host)  # D2H u, udot, a
     torch.cuda.synchronize()
     t_e2e = max_over_ranks(time.perf_counter() - t0, world)
-    e2e = {"value": N * args.steps * world / t_e2e, "unit": UNIT,
+    e2e = {"value": N * args.steps / t_e2e, "unit": UNIT,
            "h2d_bytes_per_step": 2 * 8 * N / args.steps, "d2h_bytes_per_step": (3 * 8 * N + 24) / args.steps,
            "what": "ads_set_state(host u, udot) + ads_step(K) + ads_energy + ads_get_state(host u, udot, a); "
                    "pinned host buffers; wall clock incl. copies", "energy": list(map(float, e))}
@@ -264,9 +271,9 @@ def run_ours(args, rank, world, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads/)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads/)",
         "config": {"workload": f"{wl.name}: {wl.description}", "p": wl.p, "nel": list(wl.nel),
-                   "n_dof": N, "tau": wl.tau, "parallelism": "replicas" if world > 1 else "single",
+                   "n_dof": N, "tau": wl.tau, "parallelism": f"z-slabs x{world} (NCCL)" if world > 1 else "single",
                    "l2": "inputs larger than L2 (1.09 GB per field vs 126 MB L2); no flush"},
         "roofline": roofline, "kernels": kernels, "gpu_launches": int(launches),
         "clocks": clk.summary(), "e2e": e2e,

@@ -66,7 +66,10 @@ struct ads_ctx {
     SolveTab tabZ;                                   // A_z restricted to the slab (diagonal block)
     double *Vsp = nullptr, *Wsp = nullptr;           // SPIKE columns [nl][p]
     double *tip_prev = nullptr, *tip_next = nullptr; // p planes received from the neighbours
+    double *b0buf = nullptr, *u0buf = nullptr;       // stage-1 interface values (p planes)
+    double *b0_prev2 = nullptr, *u0_next2 = nullptr; // the neighbours' stage-1 values
     double qt[2 * kMaxP][2 * kMaxP] = {}, qb[2 * kMaxP][2 * kMaxP] = {};
+    double wbp[kMaxP][kMaxP] = {}, vtm[kMaxP][kMaxP] = {}, wbm[kMaxP][kMaxP] = {}, vtn[kMaxP][kMaxP] = {};
     ncclComm_t comm = nullptr;
     std::vector<ads_ctx *> members;                  // dist = 2
     ads_ctx *prev = nullptr, *next = nullptr;        // dist = 3
@@ -240,32 +243,49 @@ Band shifted(const Space1D &s, double c, int bc) {
 int build_slab_tables(ads_ctx *h, const Band &A) {
     std::vector<int> z0s, nls;
     slab_plan(h->ngz, h->world, z0s, nls);
-    const int r = h->rank, p = h->p;
-    for (int j = 0; j < h->world; ++j)
+    const int r = h->rank, p = h->p, G = h->world, m = 2 * p;
+    for (int j = 0; j < G; ++j)
         if (nls[j] < 2 * p + 1) return fail(h, ADS_E_INVAL, "slab %d has %d < 2p+1 planes", j, nls[j]);
-    SlabSpikes me, nb;
-    if (build_slab_spikes(A, z0s[r], nls[r], me)) return fail(h, ADS_E_SINGULAR, "slab block singular");
+    // every rank builds every slab's spikes (1D, cheap) so all ranks take the same decision
+    std::vector<SlabSpikes> S(G);
+    for (int j = 0; j < G; ++j)
+        if (build_slab_spikes(A, z0s[j], nls[j], S[j])) return fail(h, ADS_E_SINGULAR, "slab block %d singular", j);
+    std::vector<std::vector<double>> Q(G > 1 ? G - 1 : 0);
+    for (int j = 0; j + 1 < G; ++j) {
+        const double d = interface_inverse(S[j], S[j + 1], p, Q[j]);
+        double qn = 0.0;
+        for (int a = 0; a < m; ++a) {
+            double rs = 0.0;
+            for (int b = 0; b < m; ++b) rs += std::fabs(Q[j][a * m + b]);
+            qn = std::max(qn, rs);
+        }
+        // stage 1 drops couplings of size <= p d; one Jacobi refinement leaves (|Q| p d)^2
+        const double e = qn * p * d;
+        if (!(e * e < std::ldexp(1.0, -64)))
+            return fail(h, ADS_E_INVAL, "slabs too thin for the spike decay (interface %d: %.3g)", j, e * e);
+    }
     int rc;
-    if ((rc = make_solve_tab(h, me.block, "A_z slab", h->tabZ))) return rc;
-    if ((rc = upload(h, &h->Vsp, me.V)) || (rc = upload(h, &h->Wsp, me.W))) return rc;
-    const double thr = std::ldexp(1.0, -64);
-    std::vector<double> Q;
-    const int m = 2 * p;
+    if ((rc = make_solve_tab(h, S[r].block, "A_z slab", h->tabZ))) return rc;
+    if ((rc = upload(h, &h->Vsp, S[r].V)) || (rc = upload(h, &h->Wsp, S[r].W))) return rc;
+    auto wbot = [&](int j, double (&o)[kMaxP][kMaxP]) {  // last p rows of W_j
+        for (int a = 0; a < p; ++a)
+            for (int b = 0; b < p; ++b) o[a][b] = S[j].W[(size_t)(nls[j] - p + a) * p + b];
+    };
+    auto vtop = [&](int j, double (&o)[kMaxP][kMaxP]) {  // first p rows of V_j
+        for (int a = 0; a < p; ++a)
+            for (int b = 0; b < p; ++b) o[a][b] = S[j].V[(size_t)a * p + b];
+    };
     if (h->has_prev) {
-        if (build_slab_spikes(A, z0s[r - 1], nls[r - 1], nb)) return fail(h, ADS_E_SINGULAR, "slab block singular");
-        const double dropped = interface_inverse(nb, me, p, Q);
-        if (!(dropped < thr))
-            return fail(h, ADS_E_INVAL, "slabs too thin for the spike decay (dropped coupling %.3g >= 2^-64)", dropped);
         for (int a = 0; a < m; ++a)
-            for (int b = 0; b < m; ++b) h->qt[a][b] = Q[a * m + b];
+            for (int b = 0; b < m; ++b) h->qt[a][b] = Q[r - 1][a * m + b];
+        wbot(r - 1, h->wbp);
+        vtop(r, h->vtm);
     }
     if (h->has_next) {
-        if (build_slab_spikes(A, z0s[r + 1], nls[r + 1], nb)) return fail(h, ADS_E_SINGULAR, "slab block singular");
-        const double dropped = interface_inverse(me, nb, p, Q);
-        if (!(dropped < thr))
-            return fail(h, ADS_E_INVAL, "slabs too thin for the spike decay (dropped coupling %.3g >= 2^-64)", dropped);
         for (int a = 0; a < m; ++a)
-            for (int b = 0; b < m; ++b) h->qb[a][b] = Q[a * m + b];
+            for (int b = 0; b < m; ++b) h->qb[a][b] = Q[r][a * m + b];
+        wbot(r, h->wbm);
+        vtop(r + 1, h->vtn);
     }
     return ADS_OK;
 }
@@ -666,25 +686,74 @@ int exch_tips(ads_ctx *G) {
     return ADS_OK;
 }
 
-int run_zfix(ads_ctx *m, double *Aout, double kick) {
-    ZfixArgs a;
+void zargs(ads_ctx *m, ZfixArgs &a) {
     a.X = m->Wk;
     a.tip_prev = m->has_prev ? m->tip_prev : nullptr;
     a.tip_next = m->has_next ? m->tip_next : nullptr;
+    a.b0_prev2 = m->rank >= 2 ? m->b0_prev2 : nullptr;
+    a.u0_next2 = m->rank + 2 < m->world ? m->u0_next2 : nullptr;
+    a.b0buf = m->b0buf;
+    a.u0buf = m->u0buf;
     a.Vsp = m->Vsp;
     a.Wsp = m->Wsp;
     a.Vf = m->V;
-    a.A = Aout;
-    a.kick = kick;
     for (int i = 0; i < 2 * kMaxP; ++i)
         for (int j = 0; j < 2 * kMaxP; ++j) {
             a.qt[i][j] = m->qt[i][j];
             a.qb[i][j] = m->qb[i][j];
         }
+    for (int i = 0; i < kMaxP; ++i)
+        for (int j = 0; j < kMaxP; ++j) {
+            a.wbp[i][j] = m->wbp[i][j];
+            a.vtm[i][j] = m->vtm[i][j];
+            a.wbm[i][j] = m->wbm[i][j];
+            a.vtn[i][j] = m->vtn[i][j];
+        }
     a.geo = m->geo;
+}
+
+int run_zint(ads_ctx *m) {
+    ZfixArgs a;
+    zargs(m, a);
+    ProfScope ps(m, 3);
+    if (launch_zint(m->p, a, m->stream)) return fail(m, ADS_E_INVAL, "zint: unsupported p");
+    return check_launch(m, "zint");
+}
+
+int run_zfix(ads_ctx *m, double *Aout, double kick) {
+    ZfixArgs a;
+    zargs(m, a);
+    a.A = Aout;
+    a.kick = kick;
     ProfScope ps(m, 3);
     if (launch_zfix(m->p, a, m->stream)) return fail(m, ADS_E_INVAL, "zfix: unsupported p");
     return check_launch(m, "zfix");
+}
+
+// stage-1 values: b0buf -> next slab's b0_prev2, u0buf -> previous slab's u0_next2
+int exch_stage1(ads_ctx *G) {
+    for (ads_ctx *m : slabs_of(G)) {
+        const long hp = (long)m->p * m->geo.sz;
+        if (m->dist == 3) {
+            if (m->prev && m->prev->has_prev)
+                CUDA_TRY(m, cudaMemcpyAsync(m->b0_prev2, m->prev->b0buf, sizeof(double) * hp, cudaMemcpyDeviceToDevice,
+                                            m->stream));
+            if (m->next && m->next->has_next)
+                CUDA_TRY(m, cudaMemcpyAsync(m->u0_next2, m->next->u0buf, sizeof(double) * hp, cudaMemcpyDeviceToDevice,
+                                            m->stream));
+        } else if (m->dist == 1) {
+            NCCL_TRY(m, ncclGroupStart());
+            if (m->has_next && m->has_prev)  // slab j+1 needs b_{j-1}^0 (exists if j >= 1)
+                NCCL_TRY(m, ncclSend(m->b0buf, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
+            if (m->rank >= 2) NCCL_TRY(m, ncclRecv(m->b0_prev2, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
+            if (m->has_prev && m->has_next)  // slab j-1 needs u_{j+1}^0 (exists if j <= G-2)
+                NCCL_TRY(m, ncclSend(m->u0buf, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
+            if (m->rank + 2 < m->world)
+                NCCL_TRY(m, ncclRecv(m->u0_next2, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
+            NCCL_TRY(m, ncclGroupEnd());
+        }
+    }
+    return ADS_OK;
 }
 
 // One drift + solve + kick over all slabs: A = D^-1 (F(t) - K (U + tau_d V)), V += kick A,
@@ -699,6 +768,11 @@ int dist_solve(ads_ctx *G, double tau_d, double g, double kick, bool keepA) {
             return rc;
     }
     if ((rc = exch_tips(G))) return rc;
+    if (G->world > 2) {  // interface refinement needs the neighbours' stage-1 values
+        for (ads_ctx *m : slabs_of(G))
+            if ((rc = run_zint(m))) return rc;
+        if ((rc = exch_stage1(G))) return rc;
+    }
     for (ads_ctx *m : slabs_of(G)) {
         if ((rc = run_zfix(m, keepA ? m->A : nullptr, kick))) return rc;
         if (tau_d != 0.0) std::swap(m->U, m->U2);
@@ -850,10 +924,9 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
             for (auto f : std::initializer_list<std::pair<double **, size_t>>{
                      {&h->W, fb}, {&h->T1, sb}, {&h->T2, sb}, {&h->T3, sb}})
                 fields.push_back(f);
-        if (dist) {
-            fields.push_back({&h->tip_prev, sizeof(double) * p * h->geo.sz});
-            fields.push_back({&h->tip_next, sizeof(double) * p * h->geo.sz});
-        }
+        if (dist)
+            for (double **b : {&h->tip_prev, &h->tip_next, &h->b0buf, &h->u0buf, &h->b0_prev2, &h->u0_next2})
+                fields.push_back({b, sizeof(double) * p * h->geo.sz});
         for (auto &f : fields)
             if (rc == ADS_OK) rc = dalloc(h, (void **)f.first, f.second);
         if (rc == ADS_OK && (rc = dalloc(h, (void **)&h->dpartial, sizeof(double) * 1024)) == ADS_OK &&

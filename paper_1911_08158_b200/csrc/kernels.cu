@@ -664,7 +664,41 @@ __global__ void __launch_bounds__(KT_THREADS, 2) kop_kernel(const KopArgs a) {
 // slab (coalesced across x), streaming the nl owned planes once: 24 B/DOF (+8 when a is kept).
 // ------------------------------------------------------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(256) zfix_kernel(const ZfixArgs a) {
+__device__ __forceinline__ void zload(const double *f, long base, long sz, int k0, double (&t)[P]) {
+#pragma unroll
+    for (int m = 0; m < P; ++m) t[m] = f ? f[base + (long)(k0 + m) * sz] : 0.0;
+}
+
+// stage 1: the two interface systems of this slab without their outer couplings
+template <int P>
+__global__ void __launch_bounds__(128) zint_kernel(const ZfixArgs a) {
+    const Geom &g = a.geo;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+    if (i >= g.n0 || j >= g.n1) return;
+    const int nl = g.n2;
+    const long base = (long)j * g.sy + i;
+    double tp[P], xf[P], xl[P], tn[P];
+    zload<P>(a.tip_prev, base, g.sz, 0, tp);
+    zload<P>(a.X, base, g.sz, 0, xf);
+    zload<P>(a.X, base, g.sz, nl - P, xl);
+    zload<P>(a.tip_next, base, g.sz, 0, tn);
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+        double b = 0.0, u = 0.0;
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+            b = fma(a.qt[r][c], tp[c], fma(a.qt[r][P + c], xf[c], b));
+            u = fma(a.qb[P + r][c], xl[c], fma(a.qb[P + r][P + c], tn[c], u));
+        }
+        if (a.tip_prev) a.b0buf[base + (long)r * g.sz] = b;
+        if (a.tip_next) a.u0buf[base + (long)r * g.sz] = u;
+    }
+}
+
+// stage 2 + correction + kick: thread per z-line of the slab (coalesced across x), streaming
+// the nl owned planes once: 24 B/DOF (+8 when a is kept)
+template <int P>
+__global__ void __launch_bounds__(128) zfix_kernel(const ZfixArgs a) {
     const Geom &g = a.geo;
     const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
     if (i >= g.n0 || j >= g.n1) return;
@@ -673,29 +707,41 @@ __global__ void __launch_bounds__(256) zfix_kernel(const ZfixArgs a) {
     double bp[P], un[P];
 #pragma unroll
     for (int m = 0; m < P; ++m) bp[m] = un[m] = 0.0;
-    if (a.tip_prev) {
-        double t[2 * P];
-#pragma unroll
-        for (int m = 0; m < P; ++m) {
-            t[m] = a.tip_prev[base + (long)m * g.sz];
-            t[P + m] = a.X[base + (long)m * g.sz];
-        }
+    if (a.tip_prev) {  // top interface (j-1|j): rhs corrected by b_{j-2}^0 and u_{j+1}^0
+        double tp[P], xf[P], b2[P], u1[P];
+        zload<P>(a.tip_prev, base, g.sz, 0, tp);
+        zload<P>(a.X, base, g.sz, 0, xf);
+        zload<P>(a.b0_prev2, base, g.sz, 0, b2);
+        zload<P>(a.tip_next ? a.u0buf : nullptr, base, g.sz, 0, u1);
 #pragma unroll
         for (int r = 0; r < P; ++r)
 #pragma unroll
-            for (int c = 0; c < 2 * P; ++c) bp[r] = fma(a.qt[r][c], t[c], bp[r]);
+            for (int c = 0; c < P; ++c) {
+                tp[r] = fma(-a.wbp[r][c], b2[c], tp[r]);
+                xf[r] = fma(-a.vtm[r][c], u1[c], xf[r]);
+            }
+#pragma unroll
+        for (int r = 0; r < P; ++r)
+#pragma unroll
+            for (int c = 0; c < P; ++c) bp[r] = fma(a.qt[r][c], tp[c], fma(a.qt[r][P + c], xf[c], bp[r]));
     }
-    if (a.tip_next) {
-        double t[2 * P];
-#pragma unroll
-        for (int m = 0; m < P; ++m) {
-            t[m] = a.X[base + (long)(nl - P + m) * g.sz];
-            t[P + m] = a.tip_next[base + (long)m * g.sz];
-        }
+    if (a.tip_next) {  // bottom interface (j|j+1): rhs corrected by b_{j-1}^0 and u_{j+2}^0
+        double xl[P], tn[P], b1[P], u2[P];
+        zload<P>(a.X, base, g.sz, nl - P, xl);
+        zload<P>(a.tip_next, base, g.sz, 0, tn);
+        zload<P>(a.tip_prev ? a.b0buf : nullptr, base, g.sz, 0, b1);
+        zload<P>(a.u0_next2, base, g.sz, 0, u2);
 #pragma unroll
         for (int r = 0; r < P; ++r)
 #pragma unroll
-            for (int c = 0; c < 2 * P; ++c) un[r] = fma(a.qb[P + r][c], t[c], un[r]);
+            for (int c = 0; c < P; ++c) {
+                xl[r] = fma(-a.wbm[r][c], b1[c], xl[r]);
+                tn[r] = fma(-a.vtn[r][c], u2[c], tn[r]);
+            }
+#pragma unroll
+        for (int r = 0; r < P; ++r)
+#pragma unroll
+            for (int c = 0; c < P; ++c) un[r] = fma(a.qb[P + r][c], xl[c], fma(a.qb[P + r][P + c], tn[c], un[r]));
     }
     for (int k = 0; k < nl; ++k) {
         const long idx = base + (long)k * g.sz;
@@ -708,6 +754,19 @@ __global__ void __launch_bounds__(256) zfix_kernel(const ZfixArgs a) {
         a.Vf[idx] = fma(a.kick, x, a.Vf[idx]);
         if (a.A) a.A[idx] = x;
     }
+}
+
+int launch_zint(int p, const ZfixArgs &a, cudaStream_t s) {
+    dim3 blk(128), grd((a.geo.n0 + 127) / 128, a.geo.n1);
+    switch (p) {
+        case 1: zint_kernel<1><<<grd, blk, 0, s>>>(a); break;
+        case 2: zint_kernel<2><<<grd, blk, 0, s>>>(a); break;
+        case 3: zint_kernel<3><<<grd, blk, 0, s>>>(a); break;
+        case 4: zint_kernel<4><<<grd, blk, 0, s>>>(a); break;
+        case 5: zint_kernel<5><<<grd, blk, 0, s>>>(a); break;
+        default: return -1;
+    }
+    return 0;
 }
 
 int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {

@@ -49,19 +49,29 @@ struct KopArgs {
     int zoff = 0, zv0 = 0, zv1 = -1;
 };
 
-// Distributed z-solve fix-up (exact SPIKE, host_setup.h build_slab_spikes) fused with the kick,
-// on the owned planes of a slab (geometry g, n2 = nl):
-//   b_prev = Qt[0:p, :] [tip_prev; X(first p)],  u_next = Qb[p:2p, :] [X(last p); tip_next]
-//   x = X - W b_prev - V u_next;  Vf += kick x;  A = x (if non-null)
+// Distributed z-solve (exact SPIKE, host_setup.h build_slab_spikes) on the owned planes of a
+// slab j (geometry g, n2 = nl), X = local solution of the slab's diagonal block:
+//   stage 1 (launch_zint):  b0 = Qt[0:p, :] [tip_prev; X(first p)]     -> b0buf  (= b_{j-1}^0)
+//                           u0 = Qb[p:2p, :] [X(last p); tip_next]      -> u0buf  (= u_{j+1}^0)
+//   exchange: b0buf -> slab j+1 (its b0_prev2), u0buf -> slab j-1 (its u0_next2)
+//   stage 2 (launch_zfix): one Jacobi refinement of both interface systems with the couplings
+//   to the next interfaces (Wbot, Vtop p x p), then x = X - W b_{j-1} - V u_{j+1} and the kick
+//   Vf += kick x (A = x if non-null).
 // tip_prev / tip_next: p planes (plane stride sz) received from the neighbours (null: none).
 struct ZfixArgs {
     const double *X = nullptr, *tip_prev = nullptr, *tip_next = nullptr;
-    const double *Vsp = nullptr, *Wsp = nullptr;  // [nl][p]
+    const double *b0_prev2 = nullptr, *u0_next2 = nullptr;  // stage-1 values of slabs j-1 / j+1
+    double *b0buf = nullptr, *u0buf = nullptr;              // this slab's stage-1 values
+    const double *Vsp = nullptr, *Wsp = nullptr;            // [nl][p]
     double *Vf = nullptr, *A = nullptr;
     double kick = 0.0;
     double qt[2 * kMaxP][2 * kMaxP] = {}, qb[2 * kMaxP][2 * kMaxP] = {};
+    // couplings dropped by stage 1: top interface (j-1|j): Wbot_{j-1}, Vtop_j;
+    // bottom interface (j|j+1): Wbot_j, Vtop_{j+1}
+    double wbp[kMaxP][kMaxP] = {}, vtm[kMaxP][kMaxP] = {}, wbm[kMaxP][kMaxP] = {}, vtn[kMaxP][kMaxP] = {};
     Geom geo;
 };
+int launch_zint(int p, const ZfixArgs &a, cudaStream_t s);
 int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s);
 
 // Batched banded solve along direction dir of every line of `in`.

@@ -75,11 +75,23 @@ def test_virtual_slabs_c4_recipe(ads, nslabs):
     assert np.allclose(ge, oe, rtol=1e-11), (ge, oe)
 
 
+@pytest.mark.parametrize("nslabs,nz", [(4, 256), (8, 513)])
+def test_virtual_slabs_thin_refined(ads, nslabs, nz):
+    """Slabs of ~64 planes (c4 at 8 GPUs): the interface systems need their one-step
+    refinement with the neighbours' stage-1 values (certified (|Q| p d)^2 < 2^-64)."""
+    wl = workloads.get("c4").scaled(8, 12)
+    wl.nel = (9, 8, nz)
+    _run(ads, wl, nslabs, [1, 12])
+
+
 def test_virtual_slabs_forced_p2(ads):
-    """c3 recipe (p = 2, Ricker x Gaussian source, zero state) with 4 slabs of >= 55 planes."""
+    """c3 recipe (p = 2, Ricker x Gaussian source, zero state): 4 slabs of 58 planes and
+    8 slabs of 32 planes (c3 at 8 GPUs)."""
     wl = workloads.get("c3").scaled(12, 60)
     wl.nel = (12, 14, 230)
     _run(ads, wl, 4, [1, 60])
+    wl.nel = (10, 9, 254)
+    _run(ads, wl, 8, [1, 60])
 
 
 def test_virtual_slabs_natural_bc(ads):
@@ -112,3 +124,21 @@ def test_thin_slabs_rejected(ads):
     with pytest.raises(ads.AdsError) as e:
         ads.Solver((8, 8, 40), 3, 5e-4, virtual_slabs=4)
     assert e.value.code == -1
+
+
+def test_nccl_slab_world1(ads):
+    """The NCCL slab handle (ads_create_dist, communicator of one rank) runs the slab path with
+    an NCCL all-reduce for the energies and matches the single-GPU handle (one GPU in this
+    harness: multi-rank NCCL runs need one GPU per rank)."""
+    wl = workloads.get("c2").scaled(12, 8)
+    u0 = oracle.project_separable(wl)
+    ref = ads.Solver(wl.nel, wl.p, wl.tau, wl.bc)
+    ref.set_state(u0)
+    ref.step(8)
+    g = ads.Solver(wl.nel, wl.p, wl.tau, wl.bc, dist=(0, 1, ads.get_unique_id()))
+    assert (g.z_begin, g.z_count) == (0, wl.nel[2] + wl.p)
+    g.set_state(u0)
+    g.step(8)
+    for x, y in zip(g.get_state(), ref.get_state()):
+        assert rel(x, y) < 1e-13
+    assert np.allclose(g.energy(), ref.energy(), rtol=1e-13)
