@@ -420,8 +420,8 @@ struct KopGeo {
     static constexpr int NCT = KT_THREADS - 32 * YW;      // copy threads
     static constexpr int NPAIR = HN / 2;                  // 16-byte pieces per field and plane
     static constexpr int NSLOT = (NPAIR + NCT - 1) / NCT;
-    // shared memory (doubles): raw ring [NPF][U|V][HY][HX] | Y tile [KT_Y][NC] double2 | rows
-    static constexpr int RING = KT_NPF * 2 * HN, YT = KT_Y * NC * 2, XB = KT_X * 2 * W, YB = KT_Y * 2 * W;
+    // shared memory (doubles): raw ring [NPF][U|V][HY][HX] | Y tiles [2][KT_Y][NC] double2 | rows
+    static constexpr int RING = KT_NPF * 2 * HN, YT = 2 * KT_Y * NC * 2, XB = KT_X * 2 * W, YB = KT_Y * 2 * W;
     static constexpr int SMEM = RING + YT + XB + YB;
     static_assert(NCT >= 32, "at least one copy warp");
 };
@@ -551,13 +551,16 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
     for (int i = 0; i < KT_NPF - 1; ++i) issue(i);
     __syncthreads();  // staged band rows visible
 
-    for (int ii = 0; ii < npl; ++ii) {
-        const int kk = kk0 + ii;
-        cp_async_wait<KT_NPF - 2>();
-        __syncthreads();  // plane kk landed in every copier's pieces; Ys free
-        issue(ii + KT_NPF - 1);
-        // ---- y-pass
-        if (yitem) {
+    // one barrier per plane: iteration ii runs the y-pass of plane ii (Ys buffer ii & 1) and the
+    // x/z passes of plane ii - 1 (buffer (ii - 1) & 1), so the two overlap across warps
+    for (int ii = 0; ii <= npl; ++ii) {
+        const int kk = kk0 + ii, kx = kk - 1;
+        if (ii < npl) cp_async_wait<KT_NPF - 2>();
+        __syncthreads();  // plane kk landed; Ys[(ii-1)&1] complete; ring slot (ii-1)%NPF free
+        if (ii < npl) issue(ii + KT_NPF - 1);
+        // ---- y-pass of plane kk into Ys buffer ii & 1
+        if (yitem && ii < npl) {
+            double2 *Ysb = Ys + (ii & 1) * KT_Y * NC;
             const double *bu = ring + (ii & (KT_NPF - 1)) * 2 * HN, *bv = bu + HN;
             double pr[KT_RY + 2 * P];
 #pragma unroll
@@ -595,22 +598,23 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
                         y2 = fma(yb[(yr * 2 + 1) * W + c], pr[r + c], y2);
                     }
                 }
-                Ys[yr * NC + nc] = make_double2(y1, y2);
+                Ysb[yr * NC + nc] = make_double2(y1, y2);
             }
         }
-        __syncthreads();  // Ys complete
-        // ---- x-pass
+        // ---- x-pass of plane kx = kk - 1 from Ys buffer (ii - 1) & 1
+        if (ii == 0) continue;
+        const double2 *Yr = Ys + ((ii - 1) & 1) * KT_Y * NC;
         double s0, t0, s1, t1;
         if (INT) {
-            const double2 c0 = Ys[(2 * w) * NC + lane + P], c1 = Ys[(2 * w + 1) * NC + lane + P];
+            const double2 c0 = Yr[(2 * w) * NC + lane + P], c1 = Yr[(2 * w + 1) * NC + lane + P];
             s0 = fma(a.kc[0][P], c0.x, a.mc[0][P] * c0.y);
             t0 = a.mc[0][P] * c0.x;
             s1 = fma(a.kc[0][P], c1.x, a.mc[0][P] * c1.y);
             t1 = a.mc[0][P] * c1.x;
 #pragma unroll
             for (int d = 1; d <= P; ++d) {
-                const double2 l0 = Ys[(2 * w) * NC + lane + P - d], r0 = Ys[(2 * w) * NC + lane + P + d];
-                const double2 l1 = Ys[(2 * w + 1) * NC + lane + P - d], r1 = Ys[(2 * w + 1) * NC + lane + P + d];
+                const double2 l0 = Yr[(2 * w) * NC + lane + P - d], r0 = Yr[(2 * w) * NC + lane + P + d];
+                const double2 l1 = Yr[(2 * w + 1) * NC + lane + P - d], r1 = Yr[(2 * w + 1) * NC + lane + P + d];
                 const double a0 = l0.x + r0.x, b0 = l0.y + r0.y, a1 = l1.x + r1.x, b1 = l1.y + r1.y;
                 s0 = fma(a.kc[0][P + d], a0, s0);
                 s0 = fma(a.mc[0][P + d], b0, s0);
@@ -624,7 +628,7 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
 #pragma unroll
             for (int c = 0; c < W; ++c) {
                 const double mx_ = xb[(lane * 2 + 0) * W + c], kx_ = xb[(lane * 2 + 1) * W + c];
-                const double2 q0 = Ys[(2 * w) * NC + lane + c], q1 = Ys[(2 * w + 1) * NC + lane + c];
+                const double2 q0 = Yr[(2 * w) * NC + lane + c], q1 = Yr[(2 * w + 1) * NC + lane + c];
                 s0 = fma(kx_, q0.x, s0);
                 s0 = fma(mx_, q0.y, s0);
                 t0 = fma(mx_, q0.x, t0);
@@ -634,12 +638,12 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
             }
         }
         // ---- z-pass (a switch makes every ring slot index compile-time)
-        const bool zint = kk + a.zoff - P >= a.ilo[2] && kk + a.zoff + P <= a.ihi[2];
-        switch (ii % W) {
+        const bool zint = kx + a.zoff - P >= a.ilo[2] && kx + a.zoff + P <= a.ihi[2];
+        switch ((ii - 1) % W) {
 #define ADS_ZCASE(U)                                                                                          \
     case U:                                                                                                   \
         if constexpr (U < W)                                                                                  \
-            kop_zscatter<P, U>(a, A0, A1, s0, t0, s1, t1, kk, zint, z0, own0, own1, sxy0, sxy1, oxy);         \
+            kop_zscatter<P, U>(a, A0, A1, s0, t0, s1, t1, kx, zint, z0, own0, own1, sxy0, sxy1, oxy);         \
         break;
             ADS_ZCASE(0) ADS_ZCASE(1) ADS_ZCASE(2) ADS_ZCASE(3) ADS_ZCASE(4) ADS_ZCASE(5)
             ADS_ZCASE(6) ADS_ZCASE(7) ADS_ZCASE(8) ADS_ZCASE(9) ADS_ZCASE(10)
