@@ -474,6 +474,9 @@ __device__ __forceinline__ void cp_async16_zfill(unsigned sdst, const double *gs
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(nbytes) : "memory");
 }
 
+// first tile origin: ilo - T when the Toeplitz interior exists (ilo <= ihi), else 0
+__host__ __device__ inline int kop_origin(int ilo, int ihi, int T) { return ilo <= ihi ? ilo - T : 0; }
+
 template <int P, bool INT>
 __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0, int y0, int z0, int z1) {
     using G = KopGeo<P>;
@@ -489,11 +492,11 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
     if (!INT) {  // stage boundary band rows (zero outside the domain)
         for (int e = tid; e < KT_X * 2 * W; e += KT_THREADS) {
             const int xr = e / (2 * W), m = (e / W) & 1, c = e % W, X = x0 + xr;
-            xb[e] = X < n0 ? __ldg((m ? a.kx : a.mx) + (long)X * W + c) : 0.0;
+            xb[e] = (X >= 0 && X < n0) ? __ldg((m ? a.kx : a.mx) + (long)X * W + c) : 0.0;
         }
         for (int e = tid; e < KT_Y * 2 * W; e += KT_THREADS) {
             const int yr = e / (2 * W), m = (e / W) & 1, c = e % W, Y = y0 + yr;
-            yb[e] = Y < n1 ? __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
+            yb[e] = (Y >= 0 && Y < n1) ? __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
         }
     }
 
@@ -533,11 +536,16 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
     const bool yitem = tid < G::NITEM;
     const int nc = tid % NC, grp = tid / NC, hcol = PA - P + nc;
     const int Xc = x0 - P + nc;
-    const bool pown = yitem && nc >= P && nc < P + KT_X && Xc < n0;
+    const bool pown = yitem && nc >= P && nc < P + KT_X && Xc >= 0 && Xc < n0;
+    // owned P of this item: rows y0 + 4 grp + r (r < prows) at column Xc, plane offset added per plane
+    // rows r in [prow0, prows) of the item are inside the grid
+    const int prow0 = max(0, -(y0 + KT_RY * grp)), prows = min(KT_RY, n1 - (y0 + KT_RY * grp));
+    double *const pbase = (a.Pout && pown && prows > prow0) ? a.Pout + (long)(y0 + KT_RY * grp) * sy + Xc : nullptr;
     // ---- x-pass outputs: X = x0 + lane, rows 2w, 2w+1
     const int X = x0 + lane;
     const int Yo0 = y0 + 2 * w;
-    const bool own0 = X < n0 && Yo0 < n1, own1 = X < n0 && Yo0 + 1 < n1;
+    const bool xin = X >= 0 && X < n0;
+    const bool own0 = xin && Yo0 >= 0 && Yo0 < n1, own1 = xin && Yo0 + 1 >= 0 && Yo0 + 1 < n1;
     const double sxy0 = (a.bx && own0) ? __ldg(a.bx + X) * __ldg(a.by + Yo0) : 0.0;
     const double sxy1 = (a.bx && own1) ? __ldg(a.bx + X) * __ldg(a.by + Yo0 + 1) : 0.0;
     const long oxy = (long)Yo0 * sy + X;
@@ -553,6 +561,7 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
 
     // one barrier per plane: iteration ii runs the y-pass of plane ii (Ys buffer ii & 1) and the
     // x/z passes of plane ii - 1 (buffer (ii - 1) & 1), so the two overlap across warps
+    int zslot = W - 1;  // ring slot of plane ii - 1 = (ii - 1) mod W
     for (int ii = 0; ii <= npl; ++ii) {
         const int kk = kk0 + ii, kx = kk - 1;
         if (ii < npl) cp_async_wait<KT_NPF - 2>();
@@ -568,12 +577,11 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
                 const int e = (KT_RY * grp + r) * HX + hcol;
                 pr[r] = fma(a.tau, bv[e], bu[e]);
             }
-            if (a.Pout && pown && kk >= z0 && kk < z1) {
+            if (pbase && kk >= z0 && kk < z1) {
+                double *pp = pbase + (long)kk * sz;
 #pragma unroll
-                for (int r = 0; r < KT_RY; ++r) {
-                    const int Y = y0 + KT_RY * grp + r;
-                    if (Y < n1) a.Pout[(long)kk * sz + (long)Y * sy + Xc] = pr[r + P];
-                }
+                for (int r = 0; r < KT_RY; ++r)
+                    if (r >= prow0 && r < prows) pp[r * sy] = pr[r + P];
             }
 #pragma unroll
             for (int r = 0; r < KT_RY; ++r) {
@@ -603,6 +611,7 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
         }
         // ---- x-pass of plane kx = kk - 1 from Ys buffer (ii - 1) & 1
         if (ii == 0) continue;
+        zslot = zslot == W - 1 ? 0 : zslot + 1;
         const double2 *Yr = Ys + ((ii - 1) & 1) * KT_Y * NC;
         double s0, t0, s1, t1;
         if (INT) {
@@ -639,7 +648,7 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
         }
         // ---- z-pass (a switch makes every ring slot index compile-time)
         const bool zint = kx + a.zoff - P >= a.ilo[2] && kx + a.zoff + P <= a.ihi[2];
-        switch ((ii - 1) % W) {
+        switch (zslot) {
 #define ADS_ZCASE(U)                                                                                          \
     case U:                                                                                                   \
         if constexpr (U < W)                                                                                  \
@@ -655,7 +664,10 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
 template <int P>
 __global__ void __launch_bounds__(KT_THREADS, 2) kop_kernel(const KopArgs a) {
     extern __shared__ __align__(16) double smem[];
-    const int x0 = blockIdx.x * KT_X, y0 = blockIdx.y * KT_Y;
+    // tiles are aligned to the Toeplitz interior: tile 1 starts at ilo (interior tiles use the
+    // constant-bank pair-sum form; only the first and last tile per direction are generic)
+    const int x0 = kop_origin(a.ilo[0], a.ihi[0], KT_X) + (int)blockIdx.x * KT_X;
+    const int y0 = kop_origin(a.ilo[1], a.ihi[1], KT_Y) + (int)blockIdx.y * KT_Y;
     const int z0 = blockIdx.z * a.zlen, z1 = min(a.geo.n2, z0 + a.zlen);
     const bool xi = x0 >= a.ilo[0] && x0 + KT_X - 1 <= a.ihi[0];
     const bool yi = y0 >= a.ilo[1] && y0 + KT_Y - 1 <= a.ihi[1];
@@ -897,7 +909,8 @@ static void kop_launch(const KopArgs &a, cudaStream_t s) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kop_kernel<P>, KT_THREADS, sm);
         per_sm = std::max(per_sm, 1);
     }
-    const int gx = (a.geo.n0 + KT_X - 1) / KT_X, gy = (a.geo.n1 + KT_Y - 1) / KT_Y;
+    const int ox = kop_origin(a.ilo[0], a.ihi[0], KT_X), oy = kop_origin(a.ilo[1], a.ihi[1], KT_Y);
+    const int gx = (a.geo.n0 - ox + KT_X - 1) / KT_X, gy = (a.geo.n1 - oy + KT_Y - 1) / KT_Y;
     // z split: enough CTAs to fill whole waves, each z piece re-reads 2p halo planes
     const long resident = (long)per_sm * nsm, tiles = (long)gx * gy;
     int best = 1;
