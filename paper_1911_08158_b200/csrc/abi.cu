@@ -416,7 +416,9 @@ int run_sweep_tab(ads_ctx *h, int d, const SolveTab &tab, const double *in, doub
     a.dir = d;
     a.mode = V ? 1 : 0;
     ProfScope ps(h, 1 + d);
-    if (launch_sweep(h->p, a, h->stream)) return fail(h, ADS_E_INVAL, "sweep: unsupported p/chunk");
+    const int lr = launch_sweep(h->p, a, h->stream);
+    if (lr == -2) return fail(h, ADS_E_CUDA, "sweep: TMA descriptor encoding failed");
+    if (lr) return fail(h, ADS_E_INVAL, "sweep: unsupported p/chunk");
     return check_launch(h, "sweep");
 }
 

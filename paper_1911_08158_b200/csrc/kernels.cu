@@ -15,6 +15,8 @@
 //                  and one write per element.  x-lines are staged through shared
 //                  memory (coalesced); y/z lines are loaded coalesced across 8
 //                  adjacent x-lines.  The z sweep fuses the kick V += tau a.
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -224,11 +226,11 @@ template <int P, int LW>
 __host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir, long sy) {
     const long fixed = 2L * kSweepChunks * P * P + 2L * kSweepChunks * P * LW +
                        (long)sweep_edge_rows(t) * (Rec<P>::FW + Rec<P>::BW);
-    return fixed + (xdir ? 2L * LW * xtile_pitch((int)sy) : 2L * kSweepChunks * t.L * LW);
+    return fixed + (xdir ? 2L * LW * xtile_pitch((int)sy) : 2L * kSweepChunks * t.L * LW + 16 + 4);
 }
 
 template <int P, int L, bool XDIR, int LW>
-__global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_kernel(const __grid_constant__ SweepArgs a) {
     constexpr int SW_LW = LW, SW_G = SW<LW>::G, SW_THREADS = SW<LW>::THREADS;
     extern __shared__ __align__(16) double smem[];
     constexpr int C = kSweepChunks, FW = Rec<P>::FW, BW = Rec<P>::BW;
@@ -324,8 +326,11 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
         }
     } else {
         // y: lines (i, k), element stride sy; z: lines (i, j), element stride sz.
-        // Tile = SW_LW adjacent i.  Thread (q, c) copies, reads and writes exactly its own
-        // rows of the prefetch buffer ([row][q]), so it needs no barriers.
+        // Tile = SW_LW adjacent i.  One thread moves the whole tile with TMA: `nbox` 3D boxes
+        // (16 lines x rb rows) into the [row][q] buffer, rows beyond the line and lines beyond
+        // n0 zero-filled by the TMA unit (out-of-bounds fill); mbarrier completion.  The next
+        // tile's load is issued after the first in-solve barrier (everyone has read the buffer);
+        // the kick's V tile is loaded at the tile start and consumed after the solve.
         const long sl = a.dir == 1 ? g.sy : g.sz;
         const long sb = a.dir == 1 ? g.sz : g.sy;
         const int nb = a.dir == 1 ? g.n2 : g.n1;
@@ -333,35 +338,57 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
         const long ntiles = (long)nib * nb;
         const bool kick = a.mode != 0;
         const int nv = max(0, min(L, n - s));  // rows of my chunk inside the line
-        double *ib = buf + s * SW_LW + q, *vb = ib + C * L * SW_LW;
-        auto fetch = [&](double *ib, const double *field, long tile) {
-            if (tile >= ntiles) return;
-            const int i = (int)(tile % nib) * SW_LW + q;
-            const double *src = field + (tile / nib) * sb + i + (long)s * sl;
-            const bool lv = i < g.n0;
-#pragma unroll
-            for (int j = 0; j < L; ++j) {
-                if (lv && j < nv) cp_async8(ib + j * SW_LW, src);
-                else ib[j * SW_LW] = 0.0;
-                src += sl;
+        // buffers (128-byte aligned) and two mbarriers after them
+        double *ibase = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(buf) + 127) & ~uintptr_t(127));
+        double *vbase = ibase + C * L * SW_LW;
+        unsigned long long *mbar = reinterpret_cast<unsigned long long *>(vbase + (kick ? C * L * SW_LW : 0));
+        const unsigned mb_in = (unsigned)__cvta_generic_to_shared(mbar), mb_v = mb_in + 8;
+        const unsigned bytes = (unsigned)(C * L * SW_LW * sizeof(double));
+        double *ib = ibase + s * SW_LW + q, *vb = vbase + s * SW_LW + q;
+        auto tma = [&](const CUtensorMap *tm, double *dst, unsigned mb, long tile) {
+            // thread 0 only
+            const int i0 = (int)(tile % nib) * SW_LW, lb = (int)(tile / nib);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
+            for (int b = 0; b < a.nbox; ++b) {
+                const unsigned d = (unsigned)__cvta_generic_to_shared(dst + (long)b * a.rb * SW_LW);
+                const int r0 = b * a.rb;
+                const int c1 = a.dir == 1 ? r0 : lb, c2 = a.dir == 1 ? lb : r0;
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(d),
+                    "l"(reinterpret_cast<unsigned long long>(tm)), "r"(i0), "r"(c1), "r"(c2), "r"(mb)
+                    : "memory");
             }
         };
+        auto wait = [&](unsigned mb, unsigned parity) {
+            asm volatile(
+                "{\n .reg .pred P1;\n WAIT_%=:\n"
+                " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                " @!P1 bra WAIT_%=;\n}\n" ::"r"(mb), "r"(parity) : "memory");
+        };
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb_in) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb_v) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
         __syncthreads();
-        fetch(ib, a.in, blockIdx.x);
-        cp_async_commit();
-        for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (tid == 0 && (long)blockIdx.x < ntiles) tma(&a.tm_in, ibase, mb_in, blockIdx.x);
+        unsigned ph = 0;
+        for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ph ^= 1u) {
             const int i = (int)(tile % nib) * SW_LW + q;
             const long base = (tile / nib) * sb + i + (long)s * sl;
             const int nvl = i < g.n0 ? nv : 0;
-            cp_async_wait<0>();
+            if (kick && tid == 0) tma(&a.tm_v, vbase, mb_v, tile);  // V consumed by the previous tile's store
+            wait(mb_in, ph);
             double v[L];
 #pragma unroll
             for (int j = 0; j < L; ++j) v[j] = ib[j * SW_LW];
-            if (kick) fetch(vb, a.V, tile);  // this tile's V (consumed after the solve)
-            cp_async_commit();
-            fetch(ib, a.in, tile + gridDim.x);  // next tile streams in during the solve
-            cp_async_commit();
-            solve(v, [] {});
+            solve(v, [&] {
+                if (tid == 0 && tile + gridDim.x < ntiles) {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    tma(&a.tm_in, ibase, mb_in, tile + gridDim.x);
+                }
+            });
             double *po = a.out ? a.out + base : nullptr;
             if (!kick) {
 #pragma unroll
@@ -370,7 +397,7 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
                     po += sl;
                 }
             } else {
-                cp_async_wait<1>();  // V of this tile has landed (the next input may still fly)
+                wait(mb_v, ph);
                 double *pv = a.V + base;
 #pragma unroll
                 for (int j = 0; j < L; ++j) {
@@ -380,6 +407,8 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
                     }
                     pv += sl;
                 }
+                __syncthreads();  // every thread has read vbuf before the next tile's V load
+                if (tid == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             }
         }
     }
@@ -945,8 +974,35 @@ int launch_kop(int p, const KopArgs &a, cudaStream_t s) {
     return 0;
 }
 
+// ---- TMA descriptors (driver entry point through the runtime: no -lcuda) ----
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3D fp64 field (n0, n1, n2) with strides (sy, sz) elements, box (b0, b1, b2); OOB -> 0
+static int encode_field_map(CUtensorMap *m, const double *base, const Geom &g, unsigned b0, unsigned b1,
+                            unsigned b2) {
+    auto enc = tmap_encoder();
+    if (!enc) return -1;
+    const cuuint64_t dims[3] = {(cuuint64_t)g.n0, (cuuint64_t)g.n1, (cuuint64_t)g.n2};
+    const cuuint64_t strides[2] = {(cuuint64_t)g.sy * 8, (cuuint64_t)g.sz * 8};
+    const cuuint32_t box[3] = {b0, b1, b2}, es[3] = {1, 1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -1;
+}
+
 template <int P, int L, bool X>
-static void sweep_launch(const SweepArgs &a, cudaStream_t s) {
+static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
     constexpr int LW = X ? 8 : 16;
     constexpr int NT = SW<LW>::THREADS;
     const Geom &g = a.geo;
@@ -969,7 +1025,19 @@ static void sweep_launch(const SweepArgs &a, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<P, L, X, LW>, NT, sm);
     const long cap = (long)std::max(per_sm, 1) * nsm;
     dim3 grd((unsigned)std::min(ntiles, cap));
-    sweep_kernel<P, L, X, LW><<<grd, NT, sm, s>>>(a);
+    SweepArgs b = a;
+    if (!X) {
+        // boxes of 16 lines x rb rows: C L = 32 L rows in nbox = 4 (8 when L > 32) boxes
+        b.nbox = L <= 32 ? 4 : 8;
+        b.rb = kSweepChunks * L / b.nbox;
+        const unsigned rb = (unsigned)b.rb;
+        const bool y = a.dir == 1;
+        if (encode_field_map(&b.tm_in, a.in, g, LW, y ? rb : 1, y ? 1 : rb) ||
+            (a.mode && encode_field_map(&b.tm_v, a.V, g, LW, y ? rb : 1, y ? 1 : rb)))
+            return -2;  // TMA descriptor could not be encoded
+    }
+    sweep_kernel<P, L, X, LW><<<grd, NT, sm, s>>>(b);
+    return 0;
 }
 
 template <int P, int LV>
@@ -977,9 +1045,7 @@ static int sweep_launch_L(const SweepArgs &a, cudaStream_t s) {
     if constexpr (LV < P) {
         return -1;  // a chunk must hold a whole boundary state
     } else {
-        if (a.dir == 0) sweep_launch<P, LV, true>(a, s);
-        else sweep_launch<P, LV, false>(a, s);
-        return 0;
+        return a.dir == 0 ? sweep_launch<P, LV, true>(a, s) : sweep_launch<P, LV, false>(a, s);
     }
 }
 

@@ -1,5 +1,6 @@
 // kernels.cuh -- device kernel interfaces of the B200 ADS solver (sm_100a, fp64).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace ads {
@@ -85,6 +86,11 @@ struct SweepArgs {
     Geom geo;
     int dir = 0;
     int mode = 0;
+    // y/z sweeps: TMA descriptors of `in` and `V` (3D, boxes of 16 lines x rb rows), filled by
+    // the launcher; nbox boxes of rb rows cover the C L (identity-padded) rows of a line
+    alignas(64) CUtensorMap tm_in;
+    alignas(64) CUtensorMap tm_v;
+    int rb = 0, nbox = 0;
 };
 
 int launch_kop(int p, const KopArgs &a, cudaStream_t s);
