@@ -459,7 +459,7 @@ struct KopGeo {
 template <int P, int U>
 __device__ __forceinline__ void kop_zscatter(const KopArgs &a, double (&A0)[2 * P + 1], double (&A1)[2 * P + 1],
                                              double s0, double t0, double s1, double t1, int kk, bool zint,
-                                             int z0, bool own0, bool own1, double sxy0, double sxy1, long oxy) {
+                                             double &o0, double &o1) {
     constexpr int W = 2 * P + 1;
     if (zint) {
 #pragma unroll
@@ -487,14 +487,9 @@ __device__ __forceinline__ void kop_zscatter(const KopArgs &a, double (&A0)[2 * 
             A1[sl] = fma(kz_, t1, A1[sl]);
         }
     }
-    constexpr int so = ((U - P) % W + W) % W;  // slot of the completed output k = kk - P
-    const int k = kk - P;
-    if (k >= z0) {
-        const double gz = a.bx ? a.g * __ldg(a.bz + k + a.zoff) : 0.0;
-        const long o = (long)k * a.geo.sz + oxy;
-        if (own0) a.r[o] = fma(a.sign, A0[so], gz * sxy0);
-        if (own1) a.r[o + a.geo.sy] = fma(a.sign, A1[so], gz * sxy1);
-    }
+    constexpr int so = ((U - P) % W + W) % W;  // slot of the completed output kk - P
+    o0 = A0[so];
+    o1 = A1[so];
     A0[so] = 0.0;
     A1[so] = 0.0;
 }
@@ -578,6 +573,8 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
     const double sxy0 = (a.bx && own0) ? __ldg(a.bx + X) * __ldg(a.by + Yo0) : 0.0;
     const double sxy1 = (a.bx && own1) ? __ldg(a.bx + X) * __ldg(a.by + Yo0 + 1) : 0.0;
     const long oxy = (long)Yo0 * sy + X;
+    const bool has_src = a.bx != nullptr;
+    double *rq = a.r + oxy + (long)z0 * sz;  // output plane z0 first; advanced per completed plane
 
     // pending outputs: A0/A1[(k - kk0) mod W] accumulates plane k of rows 2w, 2w+1
     double A0[W], A1[W];
@@ -677,15 +674,22 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
         }
         // ---- z-pass (a switch makes every ring slot index compile-time)
         const bool zint = kx + a.zoff - P >= a.ilo[2] && kx + a.zoff + P <= a.ihi[2];
+        double o0 = 0.0, o1 = 0.0;
         switch (zslot) {
-#define ADS_ZCASE(U)                                                                                          \
-    case U:                                                                                                   \
-        if constexpr (U < W)                                                                                  \
-            kop_zscatter<P, U>(a, A0, A1, s0, t0, s1, t1, kx, zint, z0, own0, own1, sxy0, sxy1, oxy);         \
+#define ADS_ZCASE(U)                                                                   \
+    case U:                                                                            \
+        if constexpr (U < W) kop_zscatter<P, U>(a, A0, A1, s0, t0, s1, t1, kx, zint, o0, o1); \
         break;
             ADS_ZCASE(0) ADS_ZCASE(1) ADS_ZCASE(2) ADS_ZCASE(3) ADS_ZCASE(4) ADS_ZCASE(5)
             ADS_ZCASE(6) ADS_ZCASE(7) ADS_ZCASE(8) ADS_ZCASE(9) ADS_ZCASE(10)
 #undef ADS_ZCASE
+        }
+        // output plane kx - P is complete: r = g bx by bz + sign K P
+        if (kx - P >= z0) {
+            const double gz = has_src ? a.g * __ldg(a.bz + kx - P + a.zoff) : 0.0;
+            if (own0) rq[0] = fma(a.sign, o0, gz * sxy0);
+            if (own1) rq[sy] = fma(a.sign, o1, gz * sxy1);
+            rq += sz;
         }
     }
 }
