@@ -223,10 +223,10 @@ __host__ __device__ inline int sweep_edge_rows(const SolveTab &t) {
     return t.c_lo * t.L + (kSweepChunks - t.c_hi) * t.L + t.L;
 }
 template <int P, int LW>
-__host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir, long sy) {
+__host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir, long sy, bool kick) {
     const long fixed = 2L * kSweepChunks * P * P + 2L * kSweepChunks * P * LW +
                        (long)sweep_edge_rows(t) * (Rec<P>::FW + Rec<P>::BW);
-    return fixed + (xdir ? 2L * LW * xtile_pitch((int)sy) : 2L * kSweepChunks * t.L * LW + 16 + 4);
+    return fixed + (xdir ? 2L * LW * xtile_pitch((int)sy) : (kick ? 2L : 1L) * kSweepChunks * t.L * LW + 16 + 4);
 }
 
 template <int P, int L, bool XDIR, int LW>
@@ -1007,10 +1007,10 @@ static int encode_field_map(CUtensorMap *m, const double *base, const Geom &g, u
 
 template <int P, int L, bool X>
 static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
-    constexpr int LW = X ? 8 : 16;
+    constexpr int LW = (X || L > 17) ? 8 : 16;  // y/z: 16-line tiles while the buffers fit
     constexpr int NT = SW<LW>::THREADS;
     const Geom &g = a.geo;
-    const size_t sm = sizeof(double) * (size_t)sweep_smem_doubles<P, LW>(a.t, X, a.geo.sy);
+    const size_t sm = sizeof(double) * (size_t)sweep_smem_doubles<P, LW>(a.t, X, a.geo.sy, a.mode != 0);
     static int nsm = 0;
     static size_t sm_set = 0;
     if (!nsm) {

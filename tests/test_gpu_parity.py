@@ -227,3 +227,32 @@ def test_c4_full_size_one_step_and_run(ads):
     gu, gud, ga = g.get_state()
     mu, mud, ma = ModalPWave(wl.nel, wl.p, wl.tau).run(u0, nsteps=wl.steps)
     assert rel(gu, mu) < RUN_TOL and rel(gud, mud) < RUN_TOL and rel(ga, ma) < RUN_TOL
+
+
+@pytest.mark.parametrize("p,nel", [(1, (30, 9, 17)), (4, (13, 11, 9)), (5, (12, 7, 10))])
+def test_full_run_other_degrees(ads, p, nel):
+    """Degrees 1, 4, 5 (specialised kernels for every p in [1, 5]) through a 25-step forced run."""
+    wl = workloads.get("c3").scaled(8, 25)
+    wl.p, wl.nel, wl.tau = p, nel, 2e-3
+    wl.source = workloads.Source(f=(("gauss", 0.4, 0.1), ("gauss", 0.5, 0.1), ("gauss", 0.6, 0.1)), f0=10.0, t0=0.02)
+    # a = D^-1 F: the solve's rounding error is bounded by eps cond(D), cond(D) = prod_d cond(A_d)
+    # (Kronecker product); B-spline mass matrices grow ill-conditioned with p (DESIGN.md T1)
+    o = oracle.PWave(nel, p, wl.tau, 1)
+    kappa = float(np.prod([np.linalg.cond(o.matrix(d, 2)[1:-1, 1:-1]) for d in range(3)]))
+    _compare_run(ads, wl, [1, 25], tol_first=max(STEP1_TOL, 2.2e-16 * kappa))
+
+
+def test_largest_line_length(ads):
+    """n_d = 1056 (the largest supported line: 32 chunks of 33 rows) in x, y and z separately."""
+    import torch
+    for nel in [(1053, 4, 5), (4, 1053, 5), (5, 4, 1053)]:
+        s = ads.Solver(nel, 3, 1e-3, 1)
+        o = oracle.PWave(nel, 3, 1e-3, 1)
+        x = workloads.random_field(5, s.N).reshape(s.shape)
+        xd = _dev(x)
+        out = torch.empty_like(xd)
+        s.solve_d(xd, out)
+        torch.cuda.synchronize()
+        assert rel(out.cpu().numpy(), o.dsolve(x)) < OP_TOL, nel
+    with pytest.raises(ads.AdsError):
+        ads.Solver((1054, 4, 4), 3, 1e-3, 1)
