@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libads_b200.so")
+LIB_PATH = os.environ.get("ADS_B200_LIB") or os.path.join(_HERE, "libads_b200.so")  # env: experiment builds
 
 ADS_BC_NATURAL, ADS_BC_DIRICHLET0 = 0, 1
 ADS_MEM_HOST, ADS_MEM_DEVICE = 0, 1

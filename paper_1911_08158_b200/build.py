@@ -34,8 +34,10 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, extra=(), out=None) -> str:
+    """Compile the library; `out` (with `extra` nvcc flags) builds an experiment variant."""
+    lib = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
     objs = []
     nvcc = _nvcc()
@@ -46,11 +48,11 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         objs.append(obj)
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs, "-lcudart", "-lnccl"]
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-lcudart", "-lnccl"]
     subprocess.check_call(cmd)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
