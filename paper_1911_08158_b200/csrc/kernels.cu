@@ -215,8 +215,12 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// x-tile pitch: >= the row pitch sy and = 2 (mod 16) (conflict-free chunk reads, see above)
-__host__ __device__ inline int xtile_pitch(int sy) { return sy + ((2 - sy) % 16 + 16) % 16; }
+// x tiles: nbox TMA boxes of rb columns, rb = 2 (mod 16) and <= 256, nbox rb >= n
+__host__ __device__ inline int xbox_count(int n) { return (n + 241) / 242; }
+__host__ __device__ inline int xbox_cols(int n) {
+    const int c = (n + xbox_count(n) - 1) / xbox_count(n);
+    return c + ((2 - c) % 16 + 16) % 16;
+}
 
 // edge rows: [0, c_lo L) and [c_hi L, C L), plus one block of L uniform rows
 __host__ __device__ inline int sweep_edge_rows(const SolveTab &t) {
@@ -226,7 +230,11 @@ template <int P, int LW>
 __host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir, long sy, bool kick) {
     const long fixed = 2L * kSweepChunks * P * P + 2L * kSweepChunks * P * LW +
                        (long)sweep_edge_rows(t) * (Rec<P>::FW + Rec<P>::BW);
-    return fixed + (xdir ? 2L * LW * xtile_pitch((int)sy) : (kick ? 2L : 1L) * kSweepChunks * t.L * LW + 16 + 4);
+    if (xdir) {
+        const int nb = xbox_count(t.n), rb = xbox_cols(t.n);
+        return fixed + 2L * ((nb * LW * rb + 15) & ~15) + 16 + 4;
+    }
+    return fixed + (kick ? 2L : 1L) * kSweepChunks * t.L * LW + 16 + 4;
 }
 
 template <int P, int L, bool XDIR, int LW>
@@ -273,57 +281,75 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
     };
 
     if (XDIR) {
-        // x lines: the flattened (j, k) line index l has base l * sy (sz = n1 sy), so a tile of
-        // SW_LW consecutive lines is one contiguous block of nl * sy doubles; sy is a multiple of
-        // 8, so the block is 64-byte aligned and moves in 16-byte copies
-        const int sy = (int)g.sy, nc2 = sy / 2;  // 16-byte columns per line
-        const int np = xtile_pitch(sy);
-        double *xin = buf, *xout = buf + SW_LW * np;
+        // x lines: the field viewed as a 2D tensor (n0 columns x n1 n2 lines, pitch sy).  A tile
+        // of SW_LW consecutive lines moves HBM -> shared memory as a.nbox TMA boxes of a.rb
+        // columns (region b holds columns [b rb, (b+1) rb) as [line][rb]; rb = 2 mod 16 keeps the
+        // per-thread chunk reads conflict-free), results go back with TMA stores from a second
+        // buffer (out-of-bounds columns and lines are neither read nor written).
+        const int XB = a.rb, NB = a.nbox, RS = SW_LW * XB;  // region size (doubles)
+        double *xin = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(buf) + 127) & ~uintptr_t(127));
+        double *xout = xin + ((NB * RS + 15) & ~15);
+        unsigned long long *mbar = reinterpret_cast<unsigned long long *>(xout + ((NB * RS + 15) & ~15));
+        const unsigned mb = (unsigned)__cvta_generic_to_shared(mbar);
         const long nlines = (long)g.n1 * g.n2;
         const long ntiles = (nlines + SW_LW - 1) / SW_LW;
-        // thread tid moves 16-byte columns e = tid + 256 m of the flattened [nl][sy/2] block
-        const int li0 = tid / nc2, c20 = tid - li0 * nc2;
-        auto prefetch = [&](long tile) {
-            if (tile >= ntiles) return;
-            const long l0 = tile * SW_LW;
-            const int tot = (int)min((long)SW_LW, nlines - l0) * nc2;
-            const double *src = a.in + l0 * sy;
-            int li = li0, c2 = c20;
-            for (int e = tid; e < tot; e += SW_THREADS) {
-                cp_async16(xin + li * np + 2 * c2, src + 2 * e);
-                c2 += SW_THREADS;
-                while (c2 >= nc2) { c2 -= nc2; ++li; }
+        // my chunk [s, s + L): region b0 up to column (b0 + 1) XB, then region b0 + 1
+        const int b0 = s / XB, jb = min(L, (b0 + 1) * XB - s);
+        const int o0 = b0 * RS + q * XB + (s - b0 * XB), o1 = (b0 + 1) * RS + q * XB - jb;
+        auto tload = [&](long tile) {  // thread 0
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                         "r"((unsigned)(NB * RS * sizeof(double)))
+                         : "memory");
+            for (int bb = 0; bb < NB; ++bb) {
+                const unsigned d = (unsigned)__cvta_generic_to_shared(xin + bb * RS);
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, 0}], [%4];\n" ::"r"(d),
+                    "l"(reinterpret_cast<unsigned long long>(&a.tm_in)), "r"(bb * XB), "r"((int)(tile * SW_LW)),
+                    "r"(mb)
+                    : "memory");
             }
         };
-        for (int e = tid; e < SW_LW * np; e += SW_THREADS) xout[e] = 0.0;  // row padding stays 0
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
         __syncthreads();
-        prefetch(blockIdx.x);
-        cp_async_commit();
-        for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const long l0 = tile * SW_LW;
-            const int nl = (int)min((long)SW_LW, nlines - l0);
-            cp_async_wait<0>();
-            __syncthreads();  // the whole tile has landed
+        if (tid == 0 && (long)blockIdx.x < ntiles) tload(blockIdx.x);
+        unsigned ph = 0;
+        for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ph ^= 1u) {
+            asm volatile(
+                "{\n .reg .pred P1;\n WAITX_%=:\n"
+                " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                " @!P1 bra WAITX_%=;\n}\n" ::"r"(mb), "r"(ph) : "memory");
             double v[L];
 #pragma unroll
-            for (int j = 0; j < L; ++j) v[j] = (q < nl && s + j < n) ? xin[q * np + s + j] : 0.0;
+            for (int j = 0; j < L; ++j) v[j] = (s + j < n) ? xin[j < jb ? o0 + j : o1 + j] : 0.0;
             solve(v, [&] {
-                prefetch(tile + gridDim.x);
-                cp_async_commit();
+                if (tid == 0 && tile + gridDim.x < ntiles) {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    tload(tile + gridDim.x);
+                }
             });
+            if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // xout free
+            __syncthreads();
 #pragma unroll
             for (int j = 0; j < L; ++j)
-                if (s + j < n) xout[q * np + s + j] = v[j];
+                if (s + j < n) xout[j < jb ? o0 + j : o1 + j] = v[j];
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncthreads();
-            double2 *dst = reinterpret_cast<double2 *>(a.out + l0 * sy);
-            const int tot = nl * nc2;
-            int li = li0, c2 = c20;
-            for (int e = tid; e < tot; e += SW_THREADS) {
-                dst[e] = *reinterpret_cast<const double2 *>(xout + li * np + 2 * c2);
-                c2 += SW_THREADS;
-                while (c2 >= nc2) { c2 -= nc2; ++li; }
+            if (tid == 0) {
+                for (int bb = 0; bb < NB; ++bb) {
+                    const unsigned d = (unsigned)__cvta_generic_to_shared(xout + bb * RS);
+                    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, 0}], [%3];\n" ::"l"(
+                                     reinterpret_cast<unsigned long long>(&a.tm_out)),
+                                 "r"(bb * XB), "r"((int)(tile * SW_LW)), "r"(d)
+                                 : "memory");
+                }
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
             }
         }
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     } else {
         // y: lines (i, k), element stride sy; z: lines (i, j), element stride sz.
         // Tile = SW_LW adjacent i.  One thread moves the whole tile with TMA: `nbox` 3D boxes
@@ -1030,7 +1056,17 @@ static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
     const long cap = (long)std::max(per_sm, 1) * nsm;
     dim3 grd((unsigned)std::min(ntiles, cap));
     SweepArgs b = a;
-    if (!X) {
+    if (X) {
+        // 2D view: n0 columns x (n1 n2) lines of pitch sy
+        b.nbox = xbox_count(a.t.n);
+        b.rb = xbox_cols(a.t.n);
+        Geom g2 = g;
+        g2.n1 = g.n1 * g.n2;
+        g2.n2 = 1;
+        if (encode_field_map(&b.tm_in, a.in, g2, (unsigned)b.rb, LW, 1) ||
+            encode_field_map(&b.tm_out, a.out, g2, (unsigned)b.rb, LW, 1))
+            return -2;
+    } else {
         // boxes of 16 lines x rb rows: C L = 32 L rows in nbox = 4 (8 when L > 32) boxes
         b.nbox = L <= 32 ? 4 : 8;
         b.rb = kSweepChunks * L / b.nbox;

@@ -90,6 +90,7 @@ struct SweepArgs {
     // the launcher; nbox boxes of rb rows cover the C L (identity-padded) rows of a line
     alignas(64) CUtensorMap tm_in;
     alignas(64) CUtensorMap tm_v;
+    alignas(64) CUtensorMap tm_out;  // x sweep: TMA stores of the solved tile
     int rb = 0, nbox = 0;
 };
 
