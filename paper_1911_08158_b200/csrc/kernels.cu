@@ -234,7 +234,8 @@ __host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir,
         const int nb = xbox_count(t.n), rb = xbox_cols(t.n);
         return fixed + 2L * ((nb * LW * rb + 15) & ~15) + 16 + 4;
     }
-    return fixed + (kick ? 2L : 1L) * kSweepChunks * t.L * LW + 16 + 4;
+    (void)kick;
+    return fixed + 2L * kSweepChunks * t.L * LW + 16 + 4;
 }
 
 template <int P, int L, bool XDIR, int LW>
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
         // buffers (128-byte aligned) and two mbarriers after them
         double *ibase = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(buf) + 127) & ~uintptr_t(127));
         double *vbase = ibase + C * L * SW_LW;
-        unsigned long long *mbar = reinterpret_cast<unsigned long long *>(vbase + (kick ? C * L * SW_LW : 0));
+        unsigned long long *mbar = reinterpret_cast<unsigned long long *>(vbase + C * L * SW_LW);
         const unsigned mb_in = (unsigned)__cvta_generic_to_shared(mbar), mb_v = mb_in + 8;
         const unsigned bytes = (unsigned)(C * L * SW_LW * sizeof(double));
         double *ib = ibase + s * SW_LW + q, *vb = vbase + s * SW_LW + q;
@@ -404,7 +405,11 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
             const int i = (int)(tile % nib) * SW_LW + q;
             const long base = (tile / nib) * sb + i + (long)s * sl;
             const int nvl = i < g.n0 ? nv : 0;
-            if (kick && tid == 0) tma(&a.tm_v, vbase, mb_v, tile);  // V consumed by the previous tile's store
+            if (kick && tid == 0) {
+                // vbuf: the previous tile's TMA store of V must have read it before it is reloaded
+                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                tma(&a.tm_v, vbase, mb_v, tile);
+            }
             wait(mb_in, ph);
             double v[L];
 #pragma unroll
@@ -415,28 +420,40 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
                     tma(&a.tm_in, ibase, mb_in, tile + gridDim.x);
                 }
             });
-            double *po = a.out ? a.out + base : nullptr;
+            // results leave through vbuf with TMA stores (rows >= n and lines >= n0 clipped):
+            // no kick: out = x;  kick: V += kick x in place (a is written directly when requested)
             if (!kick) {
+                if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                __syncthreads();  // the previous tile's store has read vbuf
 #pragma unroll
-                for (int j = 0; j < L; ++j) {
-                    if (j < nvl) *po = v[j];
-                    po += sl;
-                }
+                for (int j = 0; j < L; ++j) vb[j * SW_LW] = v[j];
             } else {
                 wait(mb_v, ph);
-                double *pv = a.V + base;
+                double *po = a.out ? a.out + base : nullptr;
 #pragma unroll
                 for (int j = 0; j < L; ++j) {
-                    if (j < nvl) {
-                        *pv = fma(a.kick, v[j], vb[j * SW_LW]);
-                        if (po) po[(long)j * sl] = v[j];
-                    }
-                    pv += sl;
+                    vb[j * SW_LW] = fma(a.kick, v[j], vb[j * SW_LW]);
+                    if (po && j < nvl) po[(long)j * sl] = v[j];
                 }
-                __syncthreads();  // every thread has read vbuf before the next tile's V load
-                if (tid == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                const CUtensorMap *tm = kick ? &a.tm_v : &a.tm_out;
+                const int i0 = (int)(tile % nib) * SW_LW, lb = (int)(tile / nib);
+                for (int bb = 0; bb < a.nbox; ++bb) {
+                    const unsigned d = (unsigned)__cvta_generic_to_shared(vbase + (long)bb * a.rb * SW_LW);
+                    const int r0 = bb * a.rb;
+                    const int c1 = a.dir == 1 ? r0 : lb, c2 = a.dir == 1 ? lb : r0;
+                    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                                     reinterpret_cast<unsigned long long>(tm)),
+                                 "r"(i0), "r"(c1), "r"(c2), "r"(d)
+                                 : "memory");
+                }
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
             }
         }
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     }
 }
 
@@ -1073,7 +1090,8 @@ static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
         const unsigned rb = (unsigned)b.rb;
         const bool y = a.dir == 1;
         if (encode_field_map(&b.tm_in, a.in, g, LW, y ? rb : 1, y ? 1 : rb) ||
-            (a.mode && encode_field_map(&b.tm_v, a.V, g, LW, y ? rb : 1, y ? 1 : rb)))
+            (a.mode && encode_field_map(&b.tm_v, a.V, g, LW, y ? rb : 1, y ? 1 : rb)) ||
+            (!a.mode && encode_field_map(&b.tm_out, a.out, g, LW, y ? rb : 1, y ? 1 : rb)))
             return -2;  // TMA descriptor could not be encoded
     }
     sweep_kernel<P, L, X, LW><<<grd, NT, sm, s>>>(b);
