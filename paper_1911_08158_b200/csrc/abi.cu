@@ -74,6 +74,12 @@ struct ads_ctx {
     std::vector<ads_ctx *> members;                  // dist = 2
     ads_ctx *prev = nullptr, *next = nullptr;        // dist = 3
     double *dpartial = nullptr, *dres = nullptr;
+    // CUDA graphs of two P-wave steps (one per U/U2 parity) replayed by ads_step; the source
+    // time comes from a device step counter the z sweep increments
+    long *dstep = nullptr;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    double *gU[2] = {nullptr, nullptr};
+    bool graphs_off = false;
     // source
     double *src[3] = {nullptr, nullptr, nullptr};
     bool has_src = false;
@@ -365,7 +371,7 @@ int guard(ads_ctx *h) {
 
 // ---- step pieces ----
 int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g, double sign, double *Pout,
-            double *r) {
+            double *r, bool devsrc = false) {
     KopArgs a;
     a.U = U;
     a.V = V;
@@ -374,10 +380,18 @@ int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g
     a.tau = tau_d;
     a.g = g;
     a.sign = sign;
-    if (h->has_src && g != 0.0) {
+    if (h->has_src && (g != 0.0 || devsrc)) {
         a.bx = h->src[0];
         a.by = h->src[1];
         a.bz = h->src[2];
+        if (devsrc) {  // g from the device step counter at replay time
+            a.dstep = h->dstep;
+            a.wav = h->wavelet == ADS_WAVELET_RICKER;
+            a.f0 = h->f0;
+            a.t0 = h->t0;
+            a.amp = h->amp;
+            a.tau_g = h->tau;
+        }
     }
     a.mx = h->dd[0].mband;
     a.kx = h->dd[0].kband;
@@ -405,8 +419,10 @@ int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g
     return check_launch(h, "kop");
 }
 
-int run_sweep_tab(ads_ctx *h, int d, const SolveTab &tab, const double *in, double *out, double *V, double kick) {
+int run_sweep_tab(ads_ctx *h, int d, const SolveTab &tab, const double *in, double *out, double *V, double kick,
+                  long *inc = nullptr) {
     SweepArgs a;
+    a.dstep_inc = inc;
     a.in = in;
     a.out = out;
     a.V = V;
@@ -430,7 +446,64 @@ int run_solve(ads_ctx *h, const double *r_in, double *scratch, double *r2, doubl
     int rc;
     if ((rc = run_sweep(h, 0, r_in, scratch, nullptr, 0.0))) return rc;
     if ((rc = run_sweep(h, 1, scratch, r2, nullptr, 0.0))) return rc;
-    return run_sweep(h, 2, r2, aout, V, kick);
+    return run_sweep_tab(h, 2, h->dd[2].tab, r2, aout, V, kick, h->dstep);
+}
+
+// one single-GPU P-wave step n -> n+1 (drift + RHS, three sweeps, kick); devsrc: source time
+// from the device step counter (graph capture), else from the host counter
+int enqueue_step(ads_ctx *h, bool keepA, bool devsrc) {
+    const double t1 = (double)(h->step + 1) * h->tau;  // F at t_{n+1} (C14)
+    int rc;
+    if ((rc = run_kop(h, h->U, h->V, h->tau, devsrc ? 0.0 : source_g(h, t1), -1.0, h->U2, h->R, devsrc))) return rc;
+    if ((rc = run_solve(h, h->R, h->Wk, h->R, keepA ? h->A : nullptr, h->V, h->tau))) return rc;
+    std::swap(h->U, h->U2);
+    return ADS_OK;
+}
+
+// graph of two steps for the current U/U2 parity (captured once, replayed)
+int step_graph(ads_ctx *h, cudaGraphExec_t *out) {
+    const int par = h->U == h->gU[1] ? 1 : (h->U == h->gU[0] ? 0 : -1);
+    if (par >= 0 && h->gexec[par]) {
+        *out = h->gexec[par];
+        return ADS_OK;
+    }
+    const int slot = h->gexec[0] ? 1 : 0;
+    double *u0 = h->U;
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return ADS_E_CUDA;
+    const long launches = h->launches;
+    int rc = enqueue_step(h, false, true);
+    if (rc == ADS_OK) rc = enqueue_step(h, false, true);
+    h->launches = launches;
+    const cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    if (rc != ADS_OK || e != cudaSuccess || !g) {
+        cudaGetLastError();
+        if (g) cudaGraphDestroy(g);
+        h->err.clear();
+        h->failed = false;
+        h->graphs_off = true;  // fall back to direct launches for good
+        return ADS_E_CUDA;
+    }
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) {
+        cudaGetLastError();
+        h->graphs_off = true;
+        return ADS_E_CUDA;
+    }
+    h->gexec[slot] = ex;
+    h->gU[slot] = u0;
+    *out = ex;
+    return ADS_OK;
+}
+
+void drop_graphs(ads_ctx *h) {
+    for (int i = 0; i < 2; ++i) {
+        if (h->gexec[i]) cudaGraphExecDestroy(h->gexec[i]);
+        h->gexec[i] = nullptr;
+        h->gU[i] = nullptr;
+    }
 }
 
 int dist_solve(ads_ctx *G, double tau_d, double g, double kick, bool keepA);
@@ -445,6 +518,7 @@ int init_state(ads_ctx *h) {
         if ((rc = run_sweep(h, 0, h->R, h->Wk, nullptr, 0.0))) return rc;
         if ((rc = run_sweep(h, 1, h->Wk, h->R, nullptr, 0.0))) return rc;
         if ((rc = run_sweep(h, 2, h->R, h->A, h->V, 0.5 * h->tau))) return rc;
+        CUDA_TRY(h, cudaMemsetAsync(h->dstep, 0, sizeof(long), h->stream));  // device step counter n = 0
     }
     h->step = 0;
     h->have_state = true;
@@ -932,13 +1006,15 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
         for (auto &f : fields)
             if (rc == ADS_OK) rc = dalloc(h, (void **)f.first, f.second);
         if (rc == ADS_OK && (rc = dalloc(h, (void **)&h->dpartial, sizeof(double) * 1024)) == ADS_OK &&
-            (rc = dalloc(h, (void **)&h->dres, sizeof(double) * 8)) == ADS_OK) {
+            (rc = dalloc(h, (void **)&h->dres, sizeof(double) * 8)) == ADS_OK &&
+            (rc = dalloc(h, (void **)&h->dstep, sizeof(long))) == ADS_OK) {
             cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
             if (e != cudaSuccess) rc = fail(h, ADS_E_CUDA, "stream: %s", cudaGetErrorString(e));
             h->own_stream = true;
         }
         if (rc == ADS_OK) {  // zero everything: row padding and domain-boundary halos stay 0 forever
             for (auto &f : fields) cudaMemsetAsync(*f.first, 0, f.second, h->stream);
+            cudaMemsetAsync(h->dstep, 0, sizeof(long), h->stream);
             if (cudaStreamSynchronize(h->stream) != cudaSuccess) rc = fail(h, ADS_E_CUDA, "memset failed");
             for (int f = 0; f < 6 + (ncomp == 3 ? 4 : 0); ++f) *fields[f].first += hl;  // owned planes
         }
@@ -1086,6 +1162,7 @@ int ads_set_source(ads_handle h, const double *bx, const double *by, const doubl
     int rc = guard(h);
     if (rc) return rc;
     if (!bx) {
+        drop_graphs(h);
         h->has_src = false;
         for (ads_ctx *m : h->members) m->has_src = false;
         return ADS_OK;
@@ -1093,6 +1170,7 @@ int ads_set_source(ads_handle h, const double *bx, const double *by, const doubl
     if (h->ncomp != 1) return fail(h, ADS_E_INVAL, "ads_set_source: P-wave handles only (elastic f = 0)");
     if (!by || !bz || (wavelet != ADS_WAVELET_NONE && wavelet != ADS_WAVELET_RICKER))
         return fail(h, ADS_E_INVAL, "ads_set_source: bad argument");
+    drop_graphs(h);  // the graphs bake the source vectors and wavelet parameters
     for (ads_ctx *m : h->members)
         if ((rc = ads_set_source(m, bx, by, bz, wavelet, f0, t0, amp))) return fail(h, rc, "member: %s", m->err.c_str());
     const double *b[3] = {bx, by, bz};
@@ -1199,11 +1277,18 @@ int ads_step(ads_handle h, int nsteps) {
             for (ads_ctx *m : h->members) m->step = h->step;
             continue;
         }
-        // drift + RHS: U2 = U + tau V, R = F(t_{n+1}) - K U2
-        if ((rc = run_kop(h, h->U, h->V, h->tau, source_g(h, t1), -1.0, h->U2, h->R))) return rc;
-        // a = D^-1 R; V += tau a; keep a only on the last step of the batch
-        if ((rc = run_solve(h, h->R, h->Wk, h->R, s == nsteps - 1 ? h->A : nullptr, h->V, h->tau))) return rc;
-        std::swap(h->U, h->U2);
+        // pairs of steps replay a captured CUDA graph (not while profiling kernels one by one);
+        // the last step of the batch runs directly and keeps a
+        cudaGraphExec_t ex = nullptr;
+        if (!h->prof && !h->graphs_off && nsteps - s >= 3 && step_graph(h, &ex) == ADS_OK) {
+            CUDA_TRY(h, cudaGraphLaunch(ex, h->stream));
+            h->launches += 8;
+            h->step += 2;
+            ++s;
+            continue;
+        }
+        // drift + RHS: U2 = U + tau V, R = F(t_{n+1}) - K U2; a = D^-1 R; V += tau a
+        if ((rc = enqueue_step(h, s == nsteps - 1, false))) return rc;
         h->step += 1;
     }
     return ADS_OK;
@@ -1357,6 +1442,7 @@ int ads_destroy(ads_handle h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (ads_ctx *m : h->members) ads_destroy(m);
     h->members.clear();
+    drop_graphs(h);
     if (h->comm && h->dist == 1) ncclCommDestroy(h->comm);
     for (void *p : h->allocs) cudaFree(p);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);

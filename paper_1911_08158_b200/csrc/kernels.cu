@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
         }
         __syncthreads();
         if (tid == 0 && (long)blockIdx.x < ntiles) tma(&a.tm_in, ibase, mb_in, blockIdx.x);
+        if (a.dstep_inc && tid == 0 && blockIdx.x == 0) *a.dstep_inc += 1;  // read by the next step's kop
         unsigned ph = 0;
         for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ph ^= 1u) {
             const int i = (int)(tile % nib) * SW_LW + q;
@@ -617,6 +618,11 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
     const double sxy1 = (a.bx && own1) ? __ldg(a.bx + X) * __ldg(a.by + Yo0 + 1) : 0.0;
     const long oxy = (long)Yo0 * sy + X;
     const bool has_src = a.bx != nullptr;
+    double gsrc = a.g;
+    if (has_src && a.dstep) {  // source time from the device step counter (CUDA graph replays)
+        const double x = 3.141592653589793238462643383 * a.f0 * ((double)(*a.dstep + 1) * a.tau_g - a.t0);
+        gsrc = a.amp * (a.wav ? (1.0 - 2.0 * x * x) * exp(-x * x) : 1.0);
+    }
     double *rq = a.r + oxy + (long)z0 * sz;  // output plane z0 first; advanced per completed plane
 
     // pending outputs: A0/A1[(k - kk0) mod W] accumulates plane k of rows 2w, 2w+1
@@ -729,7 +735,7 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
         }
         // output plane kx - P is complete: r = g bx by bz + sign K P
         if (kx - P >= z0) {
-            const double gz = has_src ? a.g * __ldg(a.bz + kx - P + a.zoff) : 0.0;
+            const double gz = has_src ? gsrc * __ldg(a.bz + kx - P + a.zoff) : 0.0;
             if (own0) rq[0] = fma(a.sign, o0, gz * sxy0);
             if (own1) rq[sy] = fma(a.sign, o1, gz * sxy1);
             rq += sz;

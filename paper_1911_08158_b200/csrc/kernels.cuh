@@ -48,6 +48,11 @@ struct KopArgs {
     // z-slabs: local plane k is global row k + zoff of Mz, Kz (and of bz); input planes
     // [zv0, zv1) exist in memory (halo planes of a slab); outputs are planes [0, n2)
     int zoff = 0, zv0 = 0, zv1 = -1;
+    // device-side source time (CUDA graphs): when dstep is set, g = amp R((*dstep + 1) tau_g)
+    // (R = Ricker if wav, else 1) replaces the host value g
+    const long *dstep = nullptr;
+    int wav = 0;
+    double f0 = 0.0, t0 = 0.0, amp = 0.0, tau_g = 0.0;
 };
 
 // Distributed z-solve (exact SPIKE, host_setup.h build_slab_spikes) on the owned planes of a
@@ -92,6 +97,7 @@ struct SweepArgs {
     alignas(64) CUtensorMap tm_v;
     alignas(64) CUtensorMap tm_out;  // x sweep: TMA stores of the solved tile
     int rb = 0, nbox = 0;
+    long *dstep_inc = nullptr;  // y/z: block 0 increments the device step counter (graph steps)
 };
 
 int launch_kop(int p, const KopArgs &a, cudaStream_t s);
