@@ -884,33 +884,34 @@ int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {
 // helpers
 // ------------------------------------------------------------------------------------------
 // out = alpha (A along axis d) in + beta out  (beta == 0: out is not read).  One thread per
-// x position of a row; rows (j, k) strided over the grid's y dimension.
-// out = alpha (A along axis d) in + beta out  (beta == 0: out is not read).  One thread per
-// x position of a row; rows (j, k) strided over the grid's y dimension.  Along z the band row
-// of local plane k is global row k + zoff and input planes [zv0, zv1) exist (slab halos).
-template <int P>
-__global__ void axis_apply_kernel(int d, const double *__restrict__ band, const double *__restrict__ in,
-                                  double *__restrict__ out, Geom g, double alpha, double beta, int zoff, int zv0,
-                                  int zv1) {
+// output: x from the block's x range, j = blockIdx.y, k = blockIdx.z (no index division).  Along
+// z the band row of local plane k is global row k + zoff and input planes [zv0, zv1) exist (slab
+// halos).  Interior outputs (all 2P+1 taps inside) skip the per-tap bounds checks.
+template <int P, int D>
+__global__ void __launch_bounds__(128) axis_apply_kernel(const double *__restrict__ band, const double *__restrict__ in,
+                                                         double *__restrict__ out, Geom g, double alpha, double beta,
+                                                         int zoff, int zv0, int zv1) {
     constexpr int W = 2 * P + 1;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
     if (i >= g.n0) return;
-    const int lo = d == 2 ? zv0 : 0, hi = d == 0 ? g.n0 : d == 1 ? g.n1 : zv1;
-    const int ro = d == 2 ? zoff : 0;
-    const long st = d == 0 ? 1 : d == 1 ? g.sy : g.sz;
-    for (long row = blockIdx.y; row < (long)g.n1 * g.n2; row += gridDim.y) {
-        const int j = (int)(row % g.n1), k = (int)(row / g.n1);
-        const int r = d == 0 ? i : d == 1 ? j : k;
-        const long idx = (long)k * g.sz + (long)j * g.sy + i;
-        double acc = 0.0;
+    const int r = D == 0 ? i : D == 1 ? j : k;
+    const int lo = D == 2 ? zv0 : 0, hi = D == 0 ? g.n0 : D == 1 ? g.n1 : zv1;
+    const long st = D == 0 ? 1 : D == 1 ? g.sy : g.sz;
+    const long idx = (long)k * g.sz + (long)j * g.sy + i;
+    const double *brow = band + (long)(r + (D == 2 ? zoff : 0)) * W;
+    const double *src = in + idx - (long)P * st;
+    double acc = 0.0;
+    if (r - P >= lo && r + P < hi) {
+#pragma unroll
+        for (int c = 0; c < W; ++c) acc = fma(__ldg(brow + c), src[(long)c * st], acc);
+    } else {
 #pragma unroll
         for (int c = 0; c < W; ++c) {
             const int col = r - P + c;
-            if (col >= lo && col < hi)
-                acc = fma(__ldg(band + (long)(r + ro) * W + c), in[idx + (long)(col - r) * st], acc);
+            if (col >= lo && col < hi) acc = fma(__ldg(brow + c), src[(long)c * st], acc);
         }
-        out[idx] = beta == 0.0 ? alpha * acc : fma(alpha, acc, beta * out[idx]);
     }
+    out[idx] = beta == 0.0 ? alpha * acc : fma(alpha, acc, beta * out[idx]);
 }
 
 __global__ void axpby_kernel(long N, double alpha, const double *__restrict__ x, double beta, double *__restrict__ y) {
@@ -1145,16 +1146,19 @@ int launch_axis_apply(int p, int d, const double *band, const double *in, double
         zv0 = 0;
         zv1 = g.n2;
     }
-    dim3 blk(128), grd((g.n0 + 127) / 128, (unsigned)std::min<long>((long)g.n1 * g.n2, 65535));
-#define ADS_AX(PP) axis_apply_kernel<PP><<<grd, blk, 0, s>>>(d, band, in, out, g, alpha, beta, zoff, zv0, zv1)
+    dim3 blk(128), grd((g.n0 + 127) / 128, g.n1, g.n2);
+#define ADS_AX(PP, DD) axis_apply_kernel<PP, DD><<<grd, blk, 0, s>>>(band, in, out, g, alpha, beta, zoff, zv0, zv1)
+#define ADS_AXP(PP)                          \
+    case PP:                                 \
+        if (d == 0) ADS_AX(PP, 0);           \
+        else if (d == 1) ADS_AX(PP, 1);      \
+        else ADS_AX(PP, 2);                  \
+        break;
     switch (p) {
-        case 1: ADS_AX(1); break;
-        case 2: ADS_AX(2); break;
-        case 3: ADS_AX(3); break;
-        case 4: ADS_AX(4); break;
-        case 5: ADS_AX(5); break;
+        ADS_AXP(1) ADS_AXP(2) ADS_AXP(3) ADS_AXP(4) ADS_AXP(5)
         default: return -1;
     }
+#undef ADS_AXP
 #undef ADS_AX
     return 0;
 }
