@@ -542,11 +542,9 @@ double *comp(double *f, const ads_ctx *h, int c) { return f + (long)c * h->Nallo
 // out = alpha (Fx (x) Fy (x) Fz) in + beta out   (Fd: band [n_d][2p+1], acting along d)
 int tri(ads_ctx *h, double *out, const double *in, const double *fx, const double *fy, const double *fz,
         double alpha, double beta) {
-    if (launch_axis_apply(h->p, 0, fx, in, h->T1, h->geo, 1.0, 0.0, h->stream) ||
-        launch_axis_apply(h->p, 1, fy, h->T1, h->T2, h->geo, 1.0, 0.0, h->stream) ||
-        launch_axis_apply(h->p, 2, fz, h->T2, out, h->geo, alpha, beta, h->stream))
-        return fail(h, ADS_E_INVAL, "axis apply: unsupported p");
-    return check_launch(h, "axis_apply");
+    if (launch_kron3(h->p, in, out, fx, fy, fz, alpha, beta, h->geo, h->stream))
+        return fail(h, ADS_E_INVAL, "kron3: unsupported p");
+    return check_launch(h, "kron3");
 }
 
 // out += coef Ups_ik in   (i != k)

@@ -881,6 +881,107 @@ int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------------------
+// fused Kronecker triple (elasticity couplings, PAPER.md:375-387 generalised to 3D):
+//   out = alpha (Fz (x) Fy (x) Fx) in + beta out   (Fd: band [n_d][2p+1] acting along d)
+// 32 x 8 output tile marching z: per input plane the haloed plane is staged in shared memory
+// (next plane prefetched in registers), y-pass over the 32+2p columns, x-pass into a register
+// ring of 2p+1 planes, z combination of the ring.  One HBM read of `in` (+ `out` when beta != 0)
+// and one write, instead of three banded axis passes.
+// ------------------------------------------------------------------------------------------
+constexpr int K3_X = 32, K3_Y = 8;
+template <int P>
+__global__ void __launch_bounds__(K3_X * K3_Y) kron3_kernel(const double *__restrict__ in, double *__restrict__ out,
+                                                            const double *__restrict__ fx, const double *__restrict__ fy,
+                                                            const double *__restrict__ fz, double alpha, double beta,
+                                                            Geom g, int zlen) {
+    constexpr int W = 2 * P + 1, HX = K3_X + 2 * P, HY = K3_Y + 2 * P, NSLOT = (HX * HY + 255) / 256;
+    __shared__ double sp[HY][HX];
+    __shared__ double sy_[K3_Y][HX];
+    __shared__ double cx[K3_X][W], cy[K3_Y][W];
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * K3_X + tx;
+    const int x0 = blockIdx.x * K3_X, y0 = blockIdx.y * K3_Y;
+    const int n0 = g.n0, n1 = g.n1, n2 = g.n2;
+    for (int e = tid; e < K3_X * W; e += 256) {
+        const int xr = e / W, c = e % W, X = x0 + xr;
+        cx[xr][c] = X < n0 ? __ldg(fx + (long)X * W + c) : 0.0;
+    }
+    for (int e = tid; e < K3_Y * W; e += 256) {
+        const int yr = e / W, c = e % W, Y = y0 + yr;
+        cy[yr][c] = Y < n1 ? __ldg(fy + (long)Y * W + c) : 0.0;
+    }
+    long off[NSLOT];
+    bool val[NSLOT];
+#pragma unroll
+    for (int m = 0; m < NSLOT; ++m) {
+        const int e = tid + 256 * m, hy = e / HX, hx = e % HX, X = x0 - P + hx, Y = y0 - P + hy;
+        val[m] = e < HX * HY && X >= 0 && X < n0 && Y >= 0 && Y < n1;
+        off[m] = (long)Y * g.sy + X;
+    }
+    double pre[NSLOT];
+    auto load = [&](int kk) {
+#pragma unroll
+        for (int m = 0; m < NSLOT; ++m) pre[m] = (kk >= 0 && kk < n2 && val[m]) ? __ldg(in + (long)kk * g.sz + off[m]) : 0.0;
+    };
+    const int X = x0 + tx, Y = y0 + ty;
+    const bool own = X < n0 && Y < n1;
+    double ring[W];
+#pragma unroll
+    for (int c = 0; c < W; ++c) ring[c] = 0.0;
+    const int z0 = blockIdx.z * zlen, z1 = min(n2, z0 + zlen);  // output planes of this CTA
+    load(z0 - 2 * P);
+    for (int kk = z0 - 2 * P; kk < z1 + P; ++kk) {
+        __syncthreads();  // previous plane's sy_ reads done
+#pragma unroll
+        for (int m = 0; m < NSLOT; ++m) {
+            const int e = tid + 256 * m;
+            if (e < HX * HY) sp[e / HX][e % HX] = pre[m];
+        }
+        __syncthreads();
+        if (kk + 1 < z1 + P) load(kk + 1);
+        for (int e = tid; e < K3_Y * HX; e += 256) {
+            const int yr = e / HX, col = e % HX;
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < W; ++c) acc = fma(cy[yr][c], sp[yr + c][col], acc);
+            sy_[yr][col] = acc;
+        }
+        __syncthreads();
+        double xv = 0.0;
+#pragma unroll
+        for (int c = 0; c < W; ++c) xv = fma(cx[tx][c], sy_[ty][tx + c], xv);
+#pragma unroll
+        for (int c = 0; c < W - 1; ++c) ring[c] = ring[c + 1];
+        ring[W - 1] = xv;  // plane kk; ring[c] holds plane kk - 2P + c
+        const int k = kk - P;
+        if (k >= z0 && own) {
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < W; ++c) acc = fma(__ldg(fz + (long)k * W + c), ring[c], acc);
+            const long idx = (long)k * g.sz + (long)Y * g.sy + X;
+            out[idx] = beta == 0.0 ? alpha * acc : fma(alpha, acc, beta * out[idx]);
+        }
+    }
+}
+
+int launch_kron3(int p, const double *in, double *out, const double *fx, const double *fy, const double *fz,
+                 double alpha, double beta, const Geom &g, cudaStream_t s) {
+    // z pieces: about 8 CTAs per SM in total, each piece re-reads 2p halo planes
+    const int gx = (g.n0 + K3_X - 1) / K3_X, gy = (g.n1 + K3_Y - 1) / K3_Y;
+    const int want = std::max(1, (148 * 8 + gx * gy - 1) / (gx * gy));
+    const int zlen = std::max(4 * p, (g.n2 + want - 1) / want);
+    dim3 blk(K3_X, K3_Y), grd(gx, gy, (g.n2 + zlen - 1) / zlen);
+    switch (p) {
+        case 1: kron3_kernel<1><<<grd, blk, 0, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen); break;
+        case 2: kron3_kernel<2><<<grd, blk, 0, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen); break;
+        case 3: kron3_kernel<3><<<grd, blk, 0, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen); break;
+        case 4: kron3_kernel<4><<<grd, blk, 0, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen); break;
+        case 5: kron3_kernel<5><<<grd, blk, 0, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen); break;
+        default: return -1;
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------------------------------------
 // helpers
 // ------------------------------------------------------------------------------------------
 // out = alpha (A along axis d) in + beta out  (beta == 0: out is not read).  One thread per
