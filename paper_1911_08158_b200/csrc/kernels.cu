@@ -546,23 +546,24 @@ __device__ __forceinline__ void cp_async16_zfill(unsigned sdst, const double *gs
 // first tile origin: ilo - T when the Toeplitz interior exists (ilo <= ihi), else 0
 __host__ __device__ inline int kop_origin(int ilo, int ihi, int T) { return ilo <= ihi ? ilo - T : 0; }
 
-template <int P, bool INT>
+template <int P, bool XI, bool YI>
 __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0, int y0, int z0, int z1) {
     using G = KopGeo<P>;
     constexpr int W = G::W, HX = G::HX, HN = G::HN, NC = G::NC, PA = G::PA;
     double *ring = smem;
     double2 *Ys = reinterpret_cast<double2 *>(smem + G::RING);
-    double *xb = smem + G::RING + G::YT;  // [KT_X][2][W]: (Mx, Kx) rows of x0 + lane
+    double *xb = smem + G::RING + G::YT;  // [W][2][KT_X]: (Mx, Kx) rows of x0 + lane (lane fastest)
     double *yb = xb + G::XB;              // [KT_Y][2][W]: (My, Ky) rows of y0 + row
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int n0 = a.geo.n0, n1 = a.geo.n1, n2 = a.geo.n2;
     const long sy = a.geo.sy, sz = a.geo.sz;
 
-    if (!INT) {  // stage boundary band rows (zero outside the domain)
+    if (!XI)  // stage boundary band rows (zero outside the domain)
         for (int e = tid; e < KT_X * 2 * W; e += KT_THREADS) {
-            const int xr = e / (2 * W), m = (e / W) & 1, c = e % W, X = x0 + xr;
+            const int xr = e % KT_X, m = (e / KT_X) & 1, c = e / (2 * KT_X), X = x0 + xr;
             xb[e] = (X >= 0 && X < n0) ? __ldg((m ? a.kx : a.mx) + (long)X * W + c) : 0.0;
         }
+    if (!YI) {
         for (int e = tid; e < KT_Y * 2 * W; e += KT_THREADS) {
             const int yr = e / (2 * W), m = (e / W) & 1, c = e % W, Y = y0 + yr;
             yb[e] = (Y >= 0 && Y < n1) ? __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
@@ -663,7 +664,7 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
             for (int r = 0; r < KT_RY; ++r) {
                 const int yr = KT_RY * grp + r;
                 double y1, y2;
-                if (INT) {
+                if (YI) {
                     const double ce = pr[r + P];
                     y1 = a.mc[1][P] * ce;
                     y2 = a.kc[1][P] * ce;
@@ -690,7 +691,7 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
         zslot = zslot == W - 1 ? 0 : zslot + 1;
         const double2 *Yr = Ys + ((ii - 1) & 1) * KT_Y * NC;
         double s0, t0, s1, t1;
-        if (INT) {
+        if (XI) {
             const double2 c0 = Yr[(2 * w) * NC + lane + P], c1 = Yr[(2 * w + 1) * NC + lane + P];
             s0 = fma(a.kc[0][P], c0.x, a.mc[0][P] * c0.y);
             t0 = a.mc[0][P] * c0.x;
@@ -712,7 +713,7 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
             s0 = t0 = s1 = t1 = 0.0;
 #pragma unroll
             for (int c = 0; c < W; ++c) {
-                const double mx_ = xb[(lane * 2 + 0) * W + c], kx_ = xb[(lane * 2 + 1) * W + c];
+                const double mx_ = xb[(c * 2 + 0) * KT_X + lane], kx_ = xb[(c * 2 + 1) * KT_X + lane];
                 const double2 q0 = Yr[(2 * w) * NC + lane + c], q1 = Yr[(2 * w + 1) * NC + lane + c];
                 s0 = fma(kx_, q0.x, s0);
                 s0 = fma(mx_, q0.y, s0);
@@ -754,8 +755,10 @@ __global__ void __launch_bounds__(KT_THREADS, 2) kop_kernel(const KopArgs a) {
     const int z0 = blockIdx.z * a.zlen, z1 = min(a.geo.n2, z0 + a.zlen);
     const bool xi = x0 >= a.ilo[0] && x0 + KT_X - 1 <= a.ihi[0];
     const bool yi = y0 >= a.ilo[1] && y0 + KT_Y - 1 <= a.ihi[1];
-    if (xi && yi) kop_tile<P, true>(a, smem, x0, y0, z0, z1);
-    else kop_tile<P, false>(a, smem, x0, y0, z0, z1);
+    if (xi && yi) kop_tile<P, true, true>(a, smem, x0, y0, z0, z1);
+    else if (xi) kop_tile<P, true, false>(a, smem, x0, y0, z0, z1);
+    else if (yi) kop_tile<P, false, true>(a, smem, x0, y0, z0, z1);
+    else kop_tile<P, false, false>(a, smem, x0, y0, z0, z1);
 }
 
 // ------------------------------------------------------------------------------------------
