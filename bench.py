@@ -46,6 +46,7 @@ FALLBACK_HBM_GBS = 6650.0
 #   sweep x, sweep y: read in; write out  -> 2 x 8 B
 #   sweep z + kick: read r, V; write V    -> 3 x 8 B (+8 B for a on the last step of a batch)
 KERNELS = ["kop", "sweep_x", "sweep_y", "sweep_z_kick"]
+C4_DOFS = 515 ** 3  # the committed traffic captures are of config c4 on one GPU
 BYTES_PER_DOF = [32.0, 16.0, 16.0, 24.0]
 
 
@@ -57,6 +58,19 @@ def peaks():
         return float(d["hbm_gbs"]), "measured", d
     except Exception:
         return FALLBACK_HBM_GBS, "fallback", {}
+
+
+def ncu_traffic(kernel, n_dof):
+    """DRAM bytes per launch of `kernel` from the latest committed `--set full` capture
+    (profiles/r*_traffic.json, written by scripts/ncu_traffic.py for config c4), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files or n_dof != C4_DOFS:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    k = d.get("kernels", {}).get(kernel)
+    return (k["dram_bytes"] / 1e9, os.path.basename(files[-1])) if k else (None, None)
 
 
 class ClockSampler:
@@ -242,8 +256,12 @@ def run_ours(args, rank, world, local):
                          "bytes_per_dof": bpd, "achieved_gbs": gbs, "frac": gbs / hbm}
     achieved = kernels[KERNELS[dom]]["achieved_gbs"]
     step_bytes = Nloc * (sum(BYTES_PER_DOF) + 8.0 / args.steps)
+    traffic, traffic_src = ncu_traffic(KERNELS[dom], Nloc)
     roofline = {"bound": "hbm", "kernel": KERNELS[dom], "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
+                "frac": achieved / hbm, "peak_kind": peak_kind,
+                "traffic": traffic, "traffic_unit": "GB per launch (ncu dram read + write)",
+                "traffic_source": traffic_src,
+                "algorithmic_bytes": Nloc * kernels[KERNELS[dom]]["bytes_per_dof"] / 1e9,
                 "step_achieved": step_bytes / (ms / args.steps / 1e3) / 1e9,
                 "step_frac": step_bytes / (ms / args.steps / 1e3) / 1e9 / hbm,
                 "step_bytes_per_dof": step_bytes / N, "floor_bytes_per_dof": 64.0}
