@@ -228,7 +228,7 @@ __host__ __device__ inline int sweep_edge_rows(const SolveTab &t) {
     return t.c_lo * t.L + (kSweepChunks - t.c_hi) * t.L + t.L;
 }
 template <int P, int LW>
-__host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir, long sy, bool kick) {
+__host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir, long sy, bool kick, int vbufs = 1) {
     const long fixed = 2L * kSweepChunks * P * P + 2L * kSweepChunks * P * LW +
                        (long)sweep_edge_rows(t) * (Rec<P>::FW + Rec<P>::BW);
     if (xdir) {
@@ -236,7 +236,7 @@ __host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir,
         return fixed + 2L * ((nb * LW * rb + 15) & ~15) + 16 + 4;
     }
     (void)kick;
-    return fixed + 2L * kSweepChunks * t.L * LW + 16 + 4;
+    return fixed + (1L + vbufs) * kSweepChunks * t.L * LW + 16 + 4;
 }
 
 template <int P, int L, bool XDIR, int LW>
@@ -368,11 +368,11 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
         const int nv = max(0, min(L, n - s));  // rows of my chunk inside the line
         // buffers (128-byte aligned) and two mbarriers after them
         double *ibase = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(buf) + 127) & ~uintptr_t(127));
-        double *vbase = ibase + C * L * SW_LW;
-        unsigned long long *mbar = reinterpret_cast<unsigned long long *>(vbase + C * L * SW_LW);
+        double *vbase0 = ibase + C * L * SW_LW;  // a.vbufs tile buffers of C L SW_LW doubles
+        unsigned long long *mbar = reinterpret_cast<unsigned long long *>(vbase0 + a.vbufs * C * L * SW_LW);
         const unsigned mb_in = (unsigned)__cvta_generic_to_shared(mbar), mb_v = mb_in + 8;
         const unsigned bytes = (unsigned)(C * L * SW_LW * sizeof(double));
-        double *ib = ibase + s * SW_LW + q, *vb = vbase + s * SW_LW + q;
+        double *ib = ibase + s * SW_LW + q;
         auto tma = [&](const CUtensorMap *tm, double *dst, unsigned mb, long tile) {
             // thread 0 only
             const int i0 = (int)(tile % nib) * SW_LW, lb = (int)(tile / nib);
@@ -402,14 +402,21 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
         __syncthreads();
         if (tid == 0 && (long)blockIdx.x < ntiles) tma(&a.tm_in, ibase, mb_in, blockIdx.x);
         if (a.dstep_inc && tid == 0 && blockIdx.x == 0) *a.dstep_inc += 1;  // read by the next step's kop
+        // wait until at most vbufs - 1 TMA stores are still reading their buffer (thread 0)
+        auto wait_store_read = [&] {
+            if (a.vbufs > 1) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        };
         unsigned ph = 0;
-        for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ph ^= 1u) {
+        for (long tile = blockIdx.x, it = 0; tile < ntiles; tile += gridDim.x, ph ^= 1u, ++it) {
+            double *vbase = vbase0 + (a.vbufs > 1 ? (it & 1) : 0) * (C * L * SW_LW);
+            double *vb = vbase + s * SW_LW + q;
             const int i = (int)(tile % nib) * SW_LW + q;
             const long base = (tile / nib) * sb + i + (long)s * sl;
             const int nvl = i < g.n0 ? nv : 0;
             if (kick && tid == 0) {
-                // vbuf: the previous tile's TMA store of V must have read it before it is reloaded
-                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                // vbuf: the TMA store of V that last used it must have read it before it is reloaded
+                wait_store_read();
                 tma(&a.tm_v, vbase, mb_v, tile);
             }
             wait(mb_in, ph);
@@ -425,8 +432,8 @@ __global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_
             // results leave through vbuf with TMA stores (rows >= n and lines >= n0 clipped):
             // no kick: out = x;  kick: V += kick x in place (a is written directly when requested)
             if (!kick) {
-                if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-                __syncthreads();  // the previous tile's store has read vbuf
+                if (tid == 0) wait_store_read();
+                __syncthreads();  // the store that last used this vbuf has read it
 #pragma unroll
                 for (int j = 0; j < L; ++j) vb[j * SW_LW] = v[j];
             } else {
@@ -1171,7 +1178,10 @@ static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
     constexpr int LW = (X || L > 17) ? 8 : 16;  // y/z: 16-line tiles while the buffers fit
     constexpr int NT = SW<LW>::THREADS;
     const Geom &g = a.geo;
-    const size_t sm = sizeof(double) * (size_t)sweep_smem_doubles<P, LW>(a.t, X, a.geo.sy, a.mode != 0);
+    // y/z: a second output / V buffer when it fits the 227 KB of shared memory per CTA
+    const int vbufs = (!X && sizeof(double) * sweep_smem_doubles<P, LW>(a.t, X, a.geo.sy, a.mode != 0, 2) <= 227 * 1024)
+                          ? 2 : 1;
+    const size_t sm = sizeof(double) * (size_t)sweep_smem_doubles<P, LW>(a.t, X, a.geo.sy, a.mode != 0, vbufs);
     static int nsm = 0;
     static size_t sm_set = 0;
     if (!nsm) {
@@ -1191,6 +1201,7 @@ static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
     const long cap = (long)std::max(per_sm, 1) * nsm;
     dim3 grd((unsigned)std::min(ntiles, cap));
     SweepArgs b = a;
+    b.vbufs = vbufs;
     if (X) {
         // 2D view: n0 columns x (n1 n2) lines of pitch sy
         b.nbox = xbox_count(a.t.n);

@@ -97,6 +97,9 @@ struct SweepArgs {
     alignas(64) CUtensorMap tm_v;
     alignas(64) CUtensorMap tm_out;  // x sweep: TMA stores of the solved tile
     int rb = 0, nbox = 0;
+    // y/z sweeps: number of output (or V) tile buffers, 1 or 2 (set by the launcher when the
+    // shared memory holds a second one: a TMA store is then waited for two tiles later)
+    int vbufs = 1;
     long *dstep_inc = nullptr;  // y/z: block 0 increments the device step counter (graph steps)
 };
 
