@@ -79,6 +79,7 @@ struct ads_ctx {
     long *dstep = nullptr;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     double *gU[2] = {nullptr, nullptr};
+    long glaunch[2] = {0, 0};  // kernel launches in each graph (two steps)
     bool graphs_off = false;
     // source
     double *src[3] = {nullptr, nullptr, nullptr};
@@ -460,11 +461,14 @@ int enqueue_step(ads_ctx *h, bool keepA, bool devsrc) {
     return ADS_OK;
 }
 
-// graph of two steps for the current U/U2 parity (captured once, replayed)
-int step_graph(ads_ctx *h, cudaGraphExec_t *out) {
+int el_step(ads_ctx *h);
+
+// graph of two steps for the current U/U2 parity (captured once, replayed); *nl = its launches
+int step_graph(ads_ctx *h, cudaGraphExec_t *out, long *nl) {
     const int par = h->U == h->gU[1] ? 1 : (h->U == h->gU[0] ? 0 : -1);
     if (par >= 0 && h->gexec[par]) {
         *out = h->gexec[par];
+        *nl = h->glaunch[par];
         return ADS_OK;
     }
     const int slot = h->gexec[0] ? 1 : 0;
@@ -472,8 +476,11 @@ int step_graph(ads_ctx *h, cudaGraphExec_t *out) {
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return ADS_E_CUDA;
     const long launches = h->launches;
-    int rc = enqueue_step(h, false, true);
-    if (rc == ADS_OK) rc = enqueue_step(h, false, true);
+    // P-wave: source time from the device step counter; elasticity has no source term
+    auto one = [&] { return h->ncomp == 3 ? el_step(h) : enqueue_step(h, false, true); };
+    int rc = one();
+    if (rc == ADS_OK) rc = one();
+    const long captured = h->launches - launches;
     h->launches = launches;
     const cudaError_t e = cudaStreamEndCapture(h->stream, &g);
     if (rc != ADS_OK || e != cudaSuccess || !g) {
@@ -494,7 +501,9 @@ int step_graph(ads_ctx *h, cudaGraphExec_t *out) {
     }
     h->gexec[slot] = ex;
     h->gU[slot] = u0;
+    h->glaunch[slot] = captured;
     *out = ex;
+    *nl = captured;
     return ADS_OK;
 }
 
@@ -1263,7 +1272,16 @@ int ads_step(ads_handle h, int nsteps) {
     if (nsteps < 0) return fail(h, ADS_E_INVAL, "nsteps < 0");
     if (!h->have_state) return fail(h, ADS_E_STATE, "ads_step before ads_set_state");
     for (int s = 0; s < nsteps; ++s) {
-        if (h->ncomp == 3) {
+        cudaGraphExec_t ex = nullptr;
+        long nl = 0;
+        if (h->ncomp == 3) {  // pairs of elastic steps replay a graph (a is written every step)
+            if (!h->prof && !h->graphs_off && nsteps - s >= 2 && step_graph(h, &ex, &nl) == ADS_OK) {
+                CUDA_TRY(h, cudaGraphLaunch(ex, h->stream));
+                h->launches += nl;
+                h->step += 2;
+                ++s;
+                continue;
+            }
             if ((rc = el_step(h))) return rc;
             h->step += 1;
             continue;
@@ -1277,10 +1295,9 @@ int ads_step(ads_handle h, int nsteps) {
         }
         // pairs of steps replay a captured CUDA graph (not while profiling kernels one by one);
         // the last step of the batch runs directly and keeps a
-        cudaGraphExec_t ex = nullptr;
-        if (!h->prof && !h->graphs_off && nsteps - s >= 3 && step_graph(h, &ex) == ADS_OK) {
+        if (!h->prof && !h->graphs_off && nsteps - s >= 3 && step_graph(h, &ex, &nl) == ADS_OK) {
             CUDA_TRY(h, cudaGraphLaunch(ex, h->stream));
-            h->launches += 8;
+            h->launches += nl;
             h->step += 2;
             ++s;
             continue;
