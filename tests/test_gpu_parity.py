@@ -256,3 +256,40 @@ def test_largest_line_length(ads):
         assert rel(out.cpu().numpy(), o.dsolve(x)) < OP_TOL, nel
     with pytest.raises(ads.AdsError):
         ads.Solver((1054, 4, 4), 3, 1e-3, 1)
+
+
+_SPLIT_CHILD = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[3])
+import paper_1911_08158_b200 as ads, workloads
+s = ads.Solver((40, 37, 45), 3, 2e-3)
+u0 = workloads.random_field(7, s.N).reshape(s.shape)
+v0 = workloads.random_field(8, s.N).reshape(s.shape)
+for f in (u0, v0):  # zero Dirichlet DOFs
+    f[0], f[-1], f[:, 0], f[:, -1], f[:, :, 0], f[:, :, -1] = 0, 0, 0, 0, 0, 0
+s.set_state(u0, v0)
+s.step(5)
+np.save(sys.argv[2], np.stack(s.get_state()))
+'''
+
+
+@pytest.mark.parametrize("nz", [1, 3, 7])
+def test_kop_z_split_is_bitwise_invariant(ads, tmp_path, nz):
+    """The fused operator kernel's z split (launch configuration, kernels.cu kop_launch) must not
+    change a single bit: every output plane receives its 2p+1 contributions in the same order."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for tag, env_nz in (("auto", None), ("forced", str(nz))):
+        env = dict(os.environ)
+        env.pop("ADS_KOP_NZ", None)
+        if env_nz:
+            env["ADS_KOP_NZ"] = env_nz
+        f = str(tmp_path / f"{tag}.npy")
+        r = subprocess.run([sys.executable, "-c", _SPLIT_CHILD, tag, f, root], env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[tag] = np.load(f)
+    assert np.array_equal(out["auto"], out["forced"])
