@@ -93,6 +93,31 @@ int ads_create_elastic(ads_handle *h, int nx, int ny, int nz, int p, double tau,
  *   device copies -- runs the distributed algorithm on one GPU (parity tests); state I/O
  *   uses the global arrays.
  * ads_local_extent: the handle's owned global planes. */
+/* ---- exact-in-time modal propagator (§3) ----
+ * The split scheme is diagonal in the tensor eigenbasis of the 1D pencils: with
+ * K_d Phi_d = M_d Phi_d Lambda_d and Phi_d^T M_d Phi_d = I (Eqs. 17-18), a state
+ * maps to modal coordinates c = (Phi_x (x) Phi_y (x) Phi_z)^T M U (load vectors: Phi^T b, no M)
+ * and every mode advances on its own by the R1 step:
+ *   cP = cU + tau cV;  ca = (g(t_{n+1}) cF - L cP) / delta;  cV += tau ca;  cU = cP,
+ *   L = l_i + l_j + l_k,  delta = (1 + eta l_i)(1 + eta l_j)(1 + eta l_k),  eta = tau^2/4
+ * (delta is the diagonal of D = A_x (x) A_y (x) A_z).
+ *
+ * ads_modal_basis: host-only.  The basis of one direction on its active DOFs, na = nel + p
+ *   (bc = ADS_BC_NATURAL) or nel + p - 2 (ADS_BC_DIRICHLET0, interior restriction C3):
+ *   lambda[na] ascending, phi[na * na] row-major, phi[i * na + k] = entry i of eigenvector k
+ *   (caller-owned host arrays).  Dense Cholesky of M, Householder tridiagonalisation, implicit QL.
+ *   Errors: ADS_E_INVAL (sizes, NULL), ADS_E_SINGULAR (M not SPD or no convergence).
+ * ads_modal_advance: advance the handle's state (U, V, a) by nsteps R1 steps in modal space --
+ *   the same result as ads_step(h, nsteps) up to rounding.  Without a source the time does not
+ *   depend on nsteps (every mode's 2x2 amplification matrix is raised to the nsteps-th power by
+ *   repeated squaring); with a source it is linear in nsteps (per-mode recurrence, no sweeps).
+ *   Each field is mapped by three dense n_d x n_d products along x, y, z (cuBLAS DGEMM on the FP64
+ *   tensor cores): U, V in; U, V, a out.  The bases are computed on the first call (host).
+ *   Single-GPU P-wave handles only.  Errors: ADS_E_INVAL (nsteps < 0, elasticity, slabs),
+ *   ADS_E_STATE (no state), ADS_E_SINGULAR, ADS_E_CUDA. */
+int ads_modal_basis(int nel, int p, int bc, double *lambda, double *phi);
+int ads_modal_advance(ads_handle h, long nsteps);
+
 int ads_get_unique_id(unsigned char uid[128]);
 int ads_slab_plan(int nz, int p, int world, int rank, int *z_begin, int *z_count);
 int ads_create_dist(ads_handle *h, int nx, int ny, int nz, int p, double tau, int bc, int rank, int world,

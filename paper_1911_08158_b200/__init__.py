@@ -80,6 +80,8 @@ def lib():
             "ads_create_dist": (_I, [ctypes.POINTER(_H), _I, _I, _I, _I, _D, _I, _I, _I, _VP, _I]),
             "ads_create_virtual": (_I, [ctypes.POINTER(_H), _I, _I, _I, _I, _D, _I, _I]),
             "ads_local_extent": (_I, [_H, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+            "ads_modal_basis": (_I, [_I, _I, _I, _VP, _VP]),
+            "ads_modal_advance": (_I, [_H, _L]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -115,6 +117,18 @@ def get_unique_id() -> bytes:
     if rc != 0:
         raise AdsError(rc, "ads_get_unique_id failed")
     return bytes(buf)
+
+
+def modal_basis(nel, p, bc=1):
+    """(lambda, phi): the 1D generalised eigenpairs K phi = lambda M phi, phi^T M phi = I, of one
+    direction on its active DOFs (ads_modal_basis; host-only)."""
+    na = nel + p - (2 if bc == ADS_BC_DIRICHLET0 else 0)
+    lam = np.zeros(max(na, 0))
+    phi = np.zeros((max(na, 0), max(na, 0)))
+    rc = lib().ads_modal_basis(nel, p, bc, lam.ctypes.data, phi.ctypes.data)
+    if rc != 0:
+        raise AdsError(rc, "ads_modal_basis failed")
+    return lam, phi
 
 
 def slab_plan(nz, p, world, rank):
@@ -233,6 +247,10 @@ class Solver:
 
     def step(self, nsteps=1):
         self._check(lib().ads_step(self.h, nsteps))
+
+    def modal_advance(self, nsteps):
+        """Advance by nsteps R1 steps exactly in modal space (ads_modal_advance)."""
+        self._check(lib().ads_modal_advance(self.h, nsteps))
 
     def energy(self):
         out = np.zeros(3)

@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False, extra=(), out=None) -> str
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         objs.append(obj)
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-lcudart", "-lnccl"]
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-lcudart", "-lnccl", "-lcublas"]
     subprocess.check_call(cmd)
     for o in objs:
         os.remove(o)

@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include <cublas_v2.h>
 #include <nccl.h>
 
 #include "../../include/ads.h"
@@ -81,8 +82,19 @@ struct ads_ctx {
     double *gU[2] = {nullptr, nullptr};
     long glaunch[2] = {0, 0};  // kernel launches in each graph (two steps)
     bool graphs_off = false;
+    // exact-in-time modal propagator (ads_modal_advance): per direction the
+    // extended n x n forward map Q = Phi^T M and inverse map Phi (column-major, zero rows and
+    // columns at Dirichlet DOFs), eigenvalues (0 at Dirichlet DOFs), modal load vector Phi^T b
+    bool modal_ready = false;
+    cublasHandle_t cub = nullptr;
+    double *mQ[3] = {nullptr, nullptr, nullptr}, *mP[3] = {nullptr, nullptr, nullptr};
+    double *mlam[3] = {nullptr, nullptr, nullptr}, *mf[3] = {nullptr, nullptr, nullptr};
+    std::vector<double> mphi_h[3];  // active-block eigenvectors (host, for the load vectors)
+    double *mg = nullptr;           // g(t_{n+s}) of the forced recurrence
+    long mg_cap = 0;
     // source
     double *src[3] = {nullptr, nullptr, nullptr};
+    std::vector<double> src_h[3];  // host copies of the load vectors
     bool has_src = false;
     int wavelet = 0;
     double f0 = 0, t0 = 0, amp = 0;
@@ -933,6 +945,85 @@ int copy_out(ads_ctx *h, double *dst, const double *src, int mem) {
     return ADS_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// exact-in-time modal propagator (§3 decomposition):
+// c = (Q_x (x) Q_y (x) Q_z) U with Q_d = Phi_d^T M_d, per-mode R1 recurrence, U = P3 c.
+// The three directional transforms are plain dense products (cuBLAS DGEMM, FP64 tensor cores).
+// ---------------------------------------------------------------------------------------
+#define CUBLAS_TRY(h, call)                                                            \
+    do {                                                                               \
+        const cublasStatus_t st_ = (call);                                             \
+        if (st_ != CUBLAS_STATUS_SUCCESS) return fail(h, ADS_E_CUDA, "cuBLAS %s: status %d", #call, (int)st_); \
+    } while (0)
+
+int modal_prepare(ads_ctx *h) {
+    if (h->modal_ready) return ADS_OK;
+    int rc;
+    if (!h->cub) {
+        CUBLAS_TRY(h, cublasCreate(&h->cub));
+        CUBLAS_TRY(h, cublasSetStream(h->cub, h->stream));
+    }
+    const int o = h->bc == ADS_BC_DIRICHLET0 ? 1 : 0;
+    for (int d = 0; d < 3; ++d) {
+        const int n = h->n[d], na = n - 2 * o;
+        std::vector<double> lam, phi;
+        int e = -1;  // an earlier direction with the same 1D space
+        for (int c = 0; c < d; ++c)
+            if (h->nel[c] == h->nel[d]) e = c;
+        if (e >= 0) {
+            phi = h->mphi_h[e];
+        } else if (modal_basis(h->sp[d], lam, phi)) {
+            return fail(h, ADS_E_SINGULAR, "modal basis of direction %d: eigensolver failed", d);
+        }
+        if (e < 0) {
+            std::vector<double> Pm((size_t)n * n, 0.0), Qm((size_t)n * n, 0.0), le(n, 0.0);
+            for (int k = 0; k < na; ++k) {
+                le[k + o] = lam[k];
+                for (int i = 0; i < na; ++i) Pm[(size_t)(i + o) + (size_t)(k + o) * n] = phi[(size_t)i * na + k];
+                for (int j = 0; j < na; ++j) {  // Q(k, j) = sum_i phi(i, k) M(i, j) over the band of M
+                    double q = 0.0;
+                    for (int i = std::max(0, j - h->p); i <= std::min(na - 1, j + h->p); ++i)
+                        q += phi[(size_t)i * na + k] * h->sp[d].M.get(i + o, j + o);
+                    Qm[(size_t)(k + o) + (size_t)(j + o) * n] = q;
+                }
+            }
+            for (double **f : {&h->mQ[d], &h->mP[d]})
+                if ((rc = dalloc(h, (void **)f, sizeof(double) * n * n))) return rc;
+            if ((rc = dalloc(h, (void **)&h->mlam[d], sizeof(double) * n))) return rc;
+            CUDA_TRY(h, cudaMemcpy(h->mQ[d], Qm.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
+            CUDA_TRY(h, cudaMemcpy(h->mP[d], Pm.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
+            CUDA_TRY(h, cudaMemcpy(h->mlam[d], le.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+            h->mphi_h[d] = phi;
+        } else {
+            h->mQ[d] = h->mQ[e];
+            h->mP[d] = h->mP[e];
+            h->mlam[d] = h->mlam[e];
+            h->mphi_h[d] = h->mphi_h[e];
+        }
+    }
+    h->modal_ready = true;
+    return ADS_OK;
+}
+
+// out = (F_x (x) F_y (x) F_z) in along x, y, z (F = mQ forward or mP inverse); in -> a -> b -> a,
+// the result is in a (in is only read; a, b distinct scratch fields)
+int modal_transform(ads_ctx *h, double *const F[3], const double *in, double *a, double *b) {
+    const Geom &g = h->geo;
+    const double one = 1.0, zero = 0.0;
+    // x: a(:, line) = F_x in(:, line) for the n1 n2 lines (pitch sy)
+    CUBLAS_TRY(h, cublasDgemm(h->cub, CUBLAS_OP_N, CUBLAS_OP_N, g.n0, g.n1 * g.n2, g.n0, &one, F[0], g.n0, in, (int)g.sy,
+                              &zero, a, (int)g.sy));
+    // y: per plane b_z = a_z F_y^T (a_z: n0 x n1, leading dimension sy)
+    CUBLAS_TRY(h, cublasDgemmStridedBatched(h->cub, CUBLAS_OP_N, CUBLAS_OP_T, g.n0, g.n1, g.n1, &one, a, (int)g.sy,
+                                            g.sz, F[1], g.n1, 0, &zero, b, (int)g.sy, g.sz, g.n2));
+    // z: a = b F_z^T with b viewed as (sy n1) x n2 (padding columns are zero and stay zero)
+    CUBLAS_TRY(h, cublasDgemm(h->cub, CUBLAS_OP_N, CUBLAS_OP_T, (int)g.sz, g.n2, g.n2, &one, b, (int)g.sz, F[2], g.n2,
+                              &zero, a, (int)g.sz));
+    h->launches += 3;
+    return ADS_OK;
+}
+
+
 }  // namespace
 
 extern "C" {
@@ -1122,6 +1213,69 @@ int ads_create_virtual(ads_handle *out, int nx, int ny, int nz, int p, double ta
     return ADS_OK;
 }
 
+int ads_modal_basis(int nel, int p, int bc, double *lambda, double *phi) {
+    if (nel < 1 || p < 1 || p > kMaxP || (bc != ADS_BC_NATURAL && bc != ADS_BC_DIRICHLET0) || !lambda || !phi)
+        return ADS_E_INVAL;
+    Space1D sp;
+    if (build_space(p, nel, bc, sp)) return ADS_E_INVAL;
+    std::vector<double> lam, ph;
+    if (modal_basis(sp, lam, ph)) return ADS_E_SINGULAR;
+    std::memcpy(lambda, lam.data(), sizeof(double) * lam.size());
+    std::memcpy(phi, ph.data(), sizeof(double) * ph.size());
+    return ADS_OK;
+}
+
+int ads_modal_advance(ads_handle h, long nsteps) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if (nsteps < 0) return fail(h, ADS_E_INVAL, "ads_modal_advance: nsteps < 0");
+    if (h->ncomp != 1 || h->dist) return fail(h, ADS_E_INVAL, "ads_modal_advance: single-GPU P-wave handles only");
+    if (!h->have_state) return fail(h, ADS_E_STATE, "ads_modal_advance before ads_set_state");
+    if (nsteps == 0) return ADS_OK;
+    if ((rc = modal_prepare(h))) return rc;
+    const double *fvec[3] = {nullptr, nullptr, nullptr};
+    const double *gdev = nullptr;
+    if (h->has_src) {  // modal load vectors Phi_d^T b_d (dual: no M) and g(t_{n+s}), s = 1..nsteps
+        const int o = h->bc == ADS_BC_DIRICHLET0 ? 1 : 0;
+        for (int d = 0; d < 3; ++d) {
+            const int n = h->n[d], na = n - 2 * o;
+            std::vector<double> f(n, 0.0);
+            for (int k = 0; k < na; ++k) {
+                double v = 0.0;
+                for (int i = 0; i < na; ++i) v += h->mphi_h[d][(size_t)i * na + k] * h->src_h[d][i + o];
+                f[k + o] = v;
+            }
+            if (!h->mf[d] && (rc = dalloc(h, (void **)&h->mf[d], sizeof(double) * n))) return rc;
+            CUDA_TRY(h, cudaMemcpyAsync(h->mf[d], f.data(), sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
+            CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+            fvec[d] = h->mf[d];
+        }
+        if (nsteps > h->mg_cap) {
+            if ((rc = dalloc(h, (void **)&h->mg, sizeof(double) * nsteps))) return rc;
+            h->mg_cap = nsteps;
+        }
+        std::vector<double> gv(nsteps);
+        for (long s = 0; s < nsteps; ++s) gv[s] = source_g(h, (double)(h->step + s + 1) * h->tau);
+        CUDA_TRY(h, cudaMemcpy(h->mg, gv.data(), sizeof(double) * nsteps, cudaMemcpyHostToDevice));
+        gdev = h->mg;
+    }
+    // U -> cU (in R), V -> cV (in U2); modes advance in place (ca in Wk); back: cV -> V,
+    // cU -> U, ca -> A
+    double *const Fq[3] = {h->mQ[0], h->mQ[1], h->mQ[2]}, *const Fp[3] = {h->mP[0], h->mP[1], h->mP[2]};
+    if ((rc = modal_transform(h, Fq, h->U, h->R, h->Wk))) return rc;
+    if ((rc = modal_transform(h, Fq, h->V, h->U2, h->Wk))) return rc;
+    if (launch_modal(h->R, h->U2, h->Wk, h->mlam[0], h->mlam[1], h->mlam[2], fvec[0], fvec[1], fvec[2], gdev, nsteps,
+                     h->tau, h->geo, h->stream))
+        return fail(h, ADS_E_INVAL, "ads_modal_advance: grid too large for the mode kernel");
+    if ((rc = check_launch(h, "modal"))) return rc;
+    if ((rc = modal_transform(h, Fp, h->U2, h->V, h->A))) return rc;
+    if ((rc = modal_transform(h, Fp, h->R, h->U, h->A))) return rc;
+    if ((rc = modal_transform(h, Fp, h->Wk, h->A, h->R))) return rc;
+    h->step += nsteps;
+    launch_set_long(h->dstep, h->step, h->stream);  // source time of later graph replays
+    return check_launch(h, "set_step");
+}
+
 int ads_local_extent(ads_handle h, int *z_begin, int *z_count) {
     if (!h || !z_begin || !z_count) return ADS_E_INVAL;
     *z_begin = h->dist == 2 ? 0 : h->zbeg;
@@ -1143,6 +1297,7 @@ int ads_set_stream(ads_handle h, void *stream) {
     }
     for (ads_ctx *m : h->members)
         if ((rc = ads_set_stream(m, h->stream))) return rc;
+    if (h->cub) cublasSetStream(h->cub, h->stream);
     return ADS_OK;
 }
 
@@ -1189,6 +1344,7 @@ int ads_set_source(ads_handle h, const double *bx, const double *by, const doubl
             if ((rc = dalloc(h, (void **)&h->src[d], sizeof(double) * nd))) return rc;
         }
         CUDA_TRY(h, cudaMemcpy(h->src[d], v.data(), sizeof(double) * nd, cudaMemcpyHostToDevice));
+        h->src_h[d] = v;
     }
     h->has_src = true;
     h->wavelet = wavelet;
@@ -1458,6 +1614,7 @@ int ads_destroy(ads_handle h) {
     for (ads_ctx *m : h->members) ads_destroy(m);
     h->members.clear();
     drop_graphs(h);
+    if (h->cub) cublasDestroy(h->cub);
     if (h->comm && h->dist == 1) ncclCommDestroy(h->comm);
     for (void *p : h->allocs) cudaFree(p);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);

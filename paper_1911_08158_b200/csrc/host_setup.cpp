@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 
 namespace ads {
 
@@ -461,6 +462,178 @@ double interface_inverse(const SlabSpikes &sj, const SlabSpikes &sj1, int p, std
             if (a < nl1) dropped = std::max(dropped, std::fabs(sj1.V[(size_t)a * p + b]));
         }
     return dropped;
+}
+
+}  // namespace ads
+
+namespace ads {
+
+// ---- modal (fast-diagonalisation) basis of one direction ----
+// Symmetric tridiagonal reduction by Householder reflections, accumulated into Zt (row r of Zt is
+// column r of the orthogonal factor): C = Z T Z^T with T = tridiag(e, d, e).
+static void householder_tridiag(std::vector<double> &C, int n, std::vector<double> &Zt, std::vector<double> &d,
+                                std::vector<double> &e) {
+    Zt.assign((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i) Zt[(size_t)i * n + i] = 1.0;
+    std::vector<double> v(n), pv(n);
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m = n - k - 1;  // reflector acts on indices k+1 .. n-1
+        double nx = 0.0;
+        for (int i = 0; i < m; ++i) nx = std::hypot(nx, C[(size_t)(k + 1 + i) * n + k]);
+        if (nx == 0.0) continue;
+        const double x0 = C[(size_t)(k + 1) * n + k];
+        const double alpha = x0 > 0 ? -nx : nx;  // reflected column becomes alpha e_1
+        for (int i = 0; i < m; ++i) v[i] = C[(size_t)(k + 1 + i) * n + k];
+        v[0] -= alpha;
+        double nv = 0.0;
+        for (int i = 0; i < m; ++i) nv = std::hypot(nv, v[i]);
+        for (int i = 0; i < m; ++i) v[i] /= nv;
+        // H = I - 2 v v^T on the trailing block: C <- H C H = C - 2 v w^T - 2 w v^T,
+        // w = p - (v^T p) v, p = C v
+        double vp = 0.0;
+        for (int i = 0; i < m; ++i) {
+            double s = 0.0;
+            const double *row = &C[(size_t)(k + 1 + i) * n + k + 1];
+            for (int j = 0; j < m; ++j) s += row[j] * v[j];
+            pv[i] = s;
+            vp += v[i] * s;
+        }
+        for (int i = 0; i < m; ++i) pv[i] -= vp * v[i];
+        for (int i = 0; i < m; ++i) {
+            double *row = &C[(size_t)(k + 1 + i) * n + k + 1];
+            for (int j = 0; j < m; ++j) row[j] -= 2.0 * (v[i] * pv[j] + pv[i] * v[j]);
+        }
+        for (int i = 0; i < m; ++i) C[(size_t)(k + 1 + i) * n + k] = C[(size_t)k * n + k + 1 + i] = 0.0;
+        C[(size_t)(k + 1) * n + k] = C[(size_t)k * n + k + 1] = alpha;
+        // Z <- Z H: column j of Z (row j of Zt) for j in k+1..n-1 mixes by v
+        for (int r = 0; r < n; ++r) {  // row r of Z: z_r <- z_r - 2 (z_r . v) v^T on those columns
+            double s = 0.0;
+            for (int i = 0; i < m; ++i) s += Zt[(size_t)(k + 1 + i) * n + r] * v[i];
+            for (int i = 0; i < m; ++i) Zt[(size_t)(k + 1 + i) * n + r] -= 2.0 * s * v[i];
+        }
+    }
+    d.resize(n);
+    e.assign(n, 0.0);
+    for (int i = 0; i < n; ++i) d[i] = C[(size_t)i * n + i];
+    for (int i = 0; i + 1 < n; ++i) e[i] = C[(size_t)(i + 1) * n + i];
+}
+
+// Eigenvalues of tridiag(e, d, e) by implicit QL sweeps with Wilkinson-type shifts; the plane
+// rotations are accumulated into the rows of Zt (the eigenvector basis).  Returns 0 or -1.
+static int tridiag_ql(std::vector<double> &d, std::vector<double> &e, std::vector<double> &Zt, int n) {
+    const double eps = std::numeric_limits<double>::epsilon();
+    for (int l = 0; l < n; ++l) {
+        for (int iter = 0;; ++iter) {
+            int m = l;
+            for (; m + 1 < n; ++m)  // first negligible coupling at or after l
+                if (std::fabs(e[m]) <= eps * (std::fabs(d[m]) + std::fabs(d[m + 1]))) break;
+            if (m == l) break;
+            if (iter == 60) return -1;
+            // shift from the leading 2x2 block at l
+            double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+            double r = std::hypot(g, 1.0);
+            g = d[m] - d[l] + e[l] / (g + (g >= 0 ? r : -r));
+            double s = 1.0, c = 1.0, pshift = 0.0;
+            bool deflated = false;
+            for (int i = m - 1; i >= l; --i) {
+                const double f = s * e[i], b = c * e[i];
+                r = std::hypot(f, g);
+                e[i + 1] = r;
+                if (r == 0.0) {  // underflow: the block splits here
+                    d[i + 1] -= pshift;
+                    e[m] = 0.0;
+                    deflated = true;
+                    break;
+                }
+                s = f / r;
+                c = g / r;
+                g = d[i + 1] - pshift;
+                r = (d[i] - g) * s + 2.0 * c * b;
+                pshift = s * r;
+                d[i + 1] = g + pshift;
+                g = c * r - b;
+                double *zi = &Zt[(size_t)i * n], *zj = &Zt[(size_t)(i + 1) * n];
+                for (int k = 0; k < n; ++k) {
+                    const double t = zj[k];
+                    zj[k] = s * zi[k] + c * t;
+                    zi[k] = c * zi[k] - s * t;
+                }
+            }
+            if (deflated) continue;
+            d[l] -= pshift;
+            e[l] = g;
+            e[m] = 0.0;
+        }
+    }
+    return 0;
+}
+
+int modal_basis(const Space1D &s, std::vector<double> &lam, std::vector<double> &phi) {
+    const int o = s.bc == 1 ? 1 : 0, na = s.n - 2 * o;
+    if (na <= 0) return -1;
+    // dense M (lower Cholesky factor in place) and K on the active DOFs
+    std::vector<double> L((size_t)na * na, 0.0), X((size_t)na * na, 0.0);
+    for (int i = 0; i < na; ++i)
+        for (int j = 0; j < na; ++j) {
+            L[(size_t)i * na + j] = s.M.get(i + o, j + o);
+            X[(size_t)i * na + j] = s.K.get(i + o, j + o);
+        }
+    for (int j = 0; j < na; ++j) {
+        double dj = L[(size_t)j * na + j];
+        for (int k = std::max(0, j - s.p); k < j; ++k) dj -= L[(size_t)j * na + k] * L[(size_t)j * na + k];
+        if (!(dj > 0.0)) return -1;
+        dj = std::sqrt(dj);
+        L[(size_t)j * na + j] = dj;
+        for (int i = j + 1; i < std::min(na, j + s.p + 1); ++i) {  // the factor keeps M's band
+            double v = L[(size_t)i * na + j];
+            for (int k = std::max(0, i - s.p); k < j; ++k) v -= L[(size_t)i * na + k] * L[(size_t)j * na + k];
+            L[(size_t)i * na + j] = v / dj;
+        }
+        for (int i = j + s.p + 1; i < na; ++i) L[(size_t)i * na + j] = 0.0;
+    }
+    for (int i = 0; i < na; ++i)
+        for (int j = i + 1; j < na; ++j) L[(size_t)i * na + j] = 0.0;
+    // C = L^-1 K L^-T: X <- L^-1 K (columns), then C = L^-1 X^T
+    auto lower_solve_cols = [&](std::vector<double> &B) {  // B <- L^-1 B, column by column
+        for (int c = 0; c < na; ++c)
+            for (int i = 0; i < na; ++i) {
+                double v = B[(size_t)i * na + c];
+                for (int k = std::max(0, i - s.p); k < i; ++k) v -= L[(size_t)i * na + k] * B[(size_t)k * na + c];
+                B[(size_t)i * na + c] = v / L[(size_t)i * na + i];
+            }
+    };
+    lower_solve_cols(X);
+    std::vector<double> C((size_t)na * na);
+    for (int i = 0; i < na; ++i)
+        for (int j = 0; j < na; ++j) C[(size_t)i * na + j] = X[(size_t)j * na + i];
+    lower_solve_cols(C);
+    for (int i = 0; i < na; ++i)
+        for (int j = i + 1; j < na; ++j) {
+            const double a = 0.5 * (C[(size_t)i * na + j] + C[(size_t)j * na + i]);
+            C[(size_t)i * na + j] = C[(size_t)j * na + i] = a;
+        }
+    std::vector<double> Zt, d, e;
+    householder_tridiag(C, na, Zt, d, e);
+    if (tridiag_ql(d, e, Zt, na)) return -1;
+    // Phi = L^-T Z (back substitution per eigenvector), eigenpairs in ascending order
+    std::vector<int> ord(na);
+    for (int i = 0; i < na; ++i) ord[i] = i;
+    std::sort(ord.begin(), ord.end(), [&](int a, int b) { return d[a] < d[b]; });
+    lam.resize(na);
+    phi.assign((size_t)na * na, 0.0);
+    std::vector<double> z(na);
+    for (int kk = 0; kk < na; ++kk) {
+        const int k = ord[kk];
+        lam[kk] = d[k];
+        for (int i = 0; i < na; ++i) z[i] = Zt[(size_t)k * na + i];
+        for (int i = na - 1; i >= 0; --i) {
+            double v = z[i];
+            for (int r = i + 1; r < std::min(na, i + s.p + 1); ++r) v -= L[(size_t)r * na + i] * z[r];
+            z[i] = v / L[(size_t)i * na + i];
+        }
+        for (int i = 0; i < na; ++i) phi[(size_t)i * na + kk] = z[i];
+    }
+    return 0;
 }
 
 }  // namespace ads

@@ -112,3 +112,15 @@ int build_slab_spikes(const Band &A, int z0, int nl, SlabSpikes &s);
 double interface_inverse(const SlabSpikes &sj, const SlabSpikes &sj1, int p, std::vector<double> &Q);
 
 }  // namespace ads
+
+namespace ads {
+
+// ---- modal basis of one direction (Eqs. 17-18) ----
+// Generalised symmetric-definite eigenproblem of the 1D pencil on the active DOFs (all n for
+// bc = 0, the n - 2 interior ones for bc = 1): K phi = lambda M phi with Phi^T M Phi = I.
+// Dense Cholesky M = L L^T, C = L^-1 K L^-T, Householder tridiagonalisation, implicit QL,
+// Phi = L^-T Z.  lam ascending; phi row-major, phi[i * na + k] = component i of eigenvector k.
+// Returns 0, or -1 (M not positive definite, QL not converged, no active DOF).
+int modal_basis(const Space1D &s, std::vector<double> &lam, std::vector<double> &phi);
+
+}  // namespace ads

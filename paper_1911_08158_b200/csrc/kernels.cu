@@ -1307,4 +1307,71 @@ int launch_dot(long N, const double *x, const double *y, double *partial, double
     return 0;
 }
 
+// ------------------------------------------------------------------------------------------
+// modal propagation (see kernels.cuh launch_modal): thread per mode, 8 + 8 B in / 24 B out
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) modal_kernel(double *__restrict__ cU, double *__restrict__ cV,
+                                                    double *__restrict__ ca, const double *__restrict__ lx,
+                                                    const double *__restrict__ ly, const double *__restrict__ lz,
+                                                    const double *__restrict__ fx, const double *__restrict__ fy,
+                                                    const double *__restrict__ fz, const double *__restrict__ g,
+                                                    long nsteps, double tau, Geom geo) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
+    if (i >= geo.n0) return;
+    const long o = (long)k * geo.sz + (long)j * geo.sy + i;
+    const double eta = 0.25 * tau * tau;
+    const double li = lx[i], lj = ly[j], lk = lz[k];
+    const double L = li + lj + lk;
+    const double delta = (1.0 + eta * li) * (1.0 + eta * lj) * (1.0 + eta * lk);
+    double u = cU[o], v = cV[o], a;
+    if (!g) {
+        const double Ld = L / delta;
+        double a11 = 1.0, a12 = tau, a21 = -tau * Ld, a22 = 1.0 - tau * tau * Ld;
+        double r11 = 1.0, r12 = 0.0, r21 = 0.0, r22 = 1.0;
+        for (long m = nsteps; m;) {
+            if (m & 1) {
+                const double t11 = r11 * a11 + r12 * a21, t12 = r11 * a12 + r12 * a22;
+                const double t21 = r21 * a11 + r22 * a21, t22 = r21 * a12 + r22 * a22;
+                r11 = t11, r12 = t12, r21 = t21, r22 = t22;
+            }
+            m >>= 1;
+            if (m) {
+                const double t11 = a11 * a11 + a12 * a21, t12 = a11 * a12 + a12 * a22;
+                const double t21 = a21 * a11 + a22 * a21, t22 = a21 * a12 + a22 * a22;
+                a11 = t11, a12 = t12, a21 = t21, a22 = t22;
+            }
+        }
+        const double un = r11 * u + r12 * v, vn = r21 * u + r22 * v;
+        u = un;
+        v = vn;
+        a = -Ld * u;
+    } else {
+        const double F = fx[i] * fy[j] * fz[k];
+        a = ca[o];
+        for (long s = 0; s < nsteps; ++s) {
+            const double P = u + tau * v;
+            a = (__ldg(g + s) * F - L * P) / delta;
+            v = v + tau * a;
+            u = P;
+        }
+    }
+    cU[o] = u;
+    cV[o] = v;
+    ca[o] = a;
+}
+
+int launch_modal(double *cU, double *cV, double *ca, const double *lx, const double *ly, const double *lz,
+                 const double *fx, const double *fy, const double *fz, const double *g, long nsteps, double tau,
+                 const Geom &geo, cudaStream_t s) {
+    if (geo.n1 > 65535 || geo.n2 > 65535) return -1;
+    dim3 grd((geo.n0 + 127) / 128, geo.n1, geo.n2);
+    modal_kernel<<<grd, 128, 0, s>>>(cU, cV, ca, lx, ly, lz, fx, fy, fz, g, nsteps, tau, geo);
+    return 0;
+}
+
+__global__ void set_long_kernel(long *dst, long value) { *dst = value; }
+
+void launch_set_long(long *dst, long value, cudaStream_t s) { set_long_kernel<<<1, 1, 0, s>>>(dst, value); }
+
 }  // namespace ads
+

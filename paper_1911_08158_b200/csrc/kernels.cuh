@@ -104,6 +104,15 @@ struct SweepArgs {
 };
 
 int launch_kop(int p, const KopArgs &a, cudaStream_t s);
+// Modal propagation (§3, reading R1): for every mode (i, j, k)
+// of the padded layout (i < n0), L = lx_i + ly_j + lz_k, delta = (1 + eta lx_i)(1 + eta ly_j)
+// (1 + eta lz_k), eta = tau^2/4.  g == nullptr: [cU; cV] <- A^n [cU; cV],
+// A = [[1, tau], [-tau L/delta, 1 - tau^2 L/delta]] by repeated squaring, ca = -(L/delta) cU;
+// else n R1 steps cP = cU + tau cV, ca = (g[s] fx_i fy_j fz_k - L cP)/delta, cV += tau ca, cU = cP.
+int launch_modal(double *cU, double *cV, double *ca, const double *lx, const double *ly, const double *lz,
+                 const double *fx, const double *fy, const double *fz, const double *g, long nsteps, double tau,
+                 const Geom &geo, cudaStream_t s);
+void launch_set_long(long *dst, long value, cudaStream_t s);
 int launch_sweep(int p, const SweepArgs &a, cudaStream_t s);
 
 // Small helpers (diagnostics / state I/O, not on the per-step path).
