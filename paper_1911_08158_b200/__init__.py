@@ -31,6 +31,7 @@ EXPORTS = [
     "ads_time", "ads_step_count", "ads_dims", "ads_apply_k", "ads_solve_d", "ads_sweep", "ads_launch_count",
     "ads_last_error", "ads_destroy", "ads_profile_enable", "ads_profile_read",
     "ads_get_unique_id", "ads_slab_plan", "ads_create_dist", "ads_create_virtual", "ads_local_extent",
+    "ads_modal_basis", "ads_modal_advance",
 ]
 
 
