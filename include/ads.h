@@ -112,7 +112,8 @@ int ads_create_elastic(ads_handle *h, int nx, int ny, int nz, int p, double tau,
  *   depend on nsteps (every mode's 2x2 amplification matrix is raised to the nsteps-th power by
  *   repeated squaring); with a source it is linear in nsteps (per-mode recurrence, no sweeps).
  *   Each field is mapped by three dense n_d x n_d products along x, y, z (cuBLAS DGEMM on the FP64
- *   tensor cores): U, V in; U, V, a out.  The bases are computed on the first call (host).
+ *   tensor cores): U, V in and out; a_n = D^-1 (F(t_n) - K U_n) by the step's own kernels.  The
+ *   bases are computed on the first call (host).
  *   Single-GPU P-wave handles only.  Errors: ADS_E_INVAL (nsteps < 0, elasticity, slabs),
  *   ADS_E_STATE (no state), ADS_E_SINGULAR, ADS_E_CUDA. */
 int ads_modal_basis(int nel, int p, int bc, double *lambda, double *phi);
