@@ -93,6 +93,16 @@ int ads_create_elastic(ads_handle *h, int nx, int ny, int nz, int p, double tau,
  *   device copies -- runs the distributed algorithm on one GPU (parity tests); state I/O
  *   uses the global arrays.
  * ads_local_extent: the handle's owned global planes. */
+/* Time scheme (readings R1 and R0).  scheme = 1 (default): reading R1.
+ * scheme = 0: the literal Eq. 16, kept to reproduce the printed scheme:
+ *   a_{n+1} = D^-1 (F(t_{n+1}) - K (U_n + tau V_n)),  V_{n+1} = V_n + tau/2 a_{n+1},
+ *   U_{n+1} = U_n + tau V_{n+1} - tau^2/2 a_{n+1}  (= U_n + tau V_n),  V_0 = udot_0, a_0 = 0,
+ * which is inconsistent (continuum limit u'' = Laplace(u)/2; R1).  Under scheme 0
+ * ads_get_state returns udot = V and ads_energy's third value is kinetic + potential.  Single-GPU
+ * P-wave handles only; the state is invalidated (call ads_set_state again).
+ * Errors: ADS_E_INVAL (scheme not 0/1, scheme 0 on elasticity or slabs). */
+int ads_set_scheme(ads_handle h, int scheme);
+
 /* ---- exact-in-time modal propagator (§3) ----
  * The split scheme is diagonal in the tensor eigenbasis of the 1D pencils: with
  * K_d Phi_d = M_d Phi_d Lambda_d and Phi_d^T M_d Phi_d = I (Eqs. 17-18), a state

@@ -38,6 +38,9 @@ struct DirDev {
 struct ads_ctx {
     int nel[3] = {0, 0, 0}, n[3] = {0, 0, 0};
     int p = 0, bc = 0, ncomp = 1;
+    // time scheme (ads_set_scheme): 1 = reading R1 (default), 0 = the literal Eq. 16 (reading R0:
+    // kick tau/2, no half-kick start, V reported as the velocity; single-GPU P-wave only)
+    int scheme = 1;
     double tau = 0.0;
     double lam = 0.0, mu = 0.0, rho = 1.0;  // elasticity (ncomp = 3)
     long step = 0;
@@ -186,6 +189,10 @@ double ricker(double t, double f0, double t0) {
     x = x * x;
     return (1.0 - 2.0 * x) * std::exp(-x);
 }
+
+// kick coefficient of V += c a and the offset of the reported velocity udot = V - c' a
+double kick_coef(const ads_ctx *h) { return h->scheme == 1 ? h->tau : 0.5 * h->tau; }
+double vel_corr(const ads_ctx *h) { return h->scheme == 1 ? 0.5 * h->tau : 0.0; }
 
 double source_g(const ads_ctx *h, double t) {
     if (!h->has_src) return 0.0;
@@ -468,7 +475,7 @@ int enqueue_step(ads_ctx *h, bool keepA, bool devsrc) {
     const double t1 = (double)(h->step + 1) * h->tau;  // F at t_{n+1} (C14)
     int rc;
     if ((rc = run_kop(h, h->U, h->V, h->tau, devsrc ? 0.0 : source_g(h, t1), -1.0, h->U2, h->R, devsrc))) return rc;
-    if ((rc = run_solve(h, h->R, h->Wk, h->R, keepA ? h->A : nullptr, h->V, h->tau))) return rc;
+    if ((rc = run_solve(h, h->R, h->Wk, h->R, keepA ? h->A : nullptr, h->V, kick_coef(h)))) return rc;
     std::swap(h->U, h->U2);
     return ADS_OK;
 }
@@ -534,6 +541,9 @@ int init_state(ads_ctx *h) {
     int rc;
     if (h->dist) {
         if ((rc = dist_solve(h, 0.0, source_g(h, 0.0), 0.5 * h->tau, true))) return rc;
+    } else if (h->scheme == 0) {  // literal Eq. 16 (R0): no start procedure, a_0 = 0, V_0 = udot_0
+        CUDA_TRY(h, cudaMemsetAsync(h->A, 0, sizeof(double) * h->Nalloc, h->stream));
+        CUDA_TRY(h, cudaMemsetAsync(h->dstep, 0, sizeof(long), h->stream));
     } else {
         if ((rc = run_kop(h, h->U, h->V, 0.0, source_g(h, 0.0), -1.0, nullptr, h->R))) return rc;
         if ((rc = run_sweep(h, 0, h->R, h->Wk, nullptr, 0.0))) return rc;
@@ -911,7 +921,7 @@ int pwave_energy(ads_ctx *G, double res[3]) {
     if ((rc = exch_halo(G, &ads_ctx::U)) || (rc = exch_halo(G, &ads_ctx::V))) return rc;
     for (ads_ctx *m : slabs_of(G)) {
         CUDA_TRY(m, cudaMemcpyAsync(m->R, m->V, sizeof(double) * m->Nalloc, cudaMemcpyDeviceToDevice, m->stream));
-        launch_axpby(m->Nalloc, -0.5 * m->tau, m->A, 1.0, m->R, m->stream);
+        launch_axpby(m->Nalloc, -vel_corr(m), m->A, 1.0, m->R, m->stream);
         if ((rc = check_launch(m, "axpby"))) return rc;
     }
     if ((rc = exch_halo(G, &ads_ctx::R))) return rc;
@@ -926,7 +936,8 @@ int pwave_energy(ads_ctx *G, double res[3]) {
     }
     res[0] = 0.5 * d4[0];
     res[1] = 0.5 * d4[1];
-    res[2] = 0.5 * d4[2] + 0.5 * d4[3];
+    // R0 conserves no such quantity: the third slot reports kinetic + potential instead
+    res[2] = G->scheme == 1 ? 0.5 * d4[2] + 0.5 * d4[3] : res[0] + res[1];
     return ADS_OK;
 }
 
@@ -1213,6 +1224,18 @@ int ads_create_virtual(ads_handle *out, int nx, int ny, int nz, int p, double ta
     return ADS_OK;
 }
 
+int ads_set_scheme(ads_handle h, int scheme) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if (scheme != 0 && scheme != 1) return fail(h, ADS_E_INVAL, "ads_set_scheme: scheme must be 0 or 1");
+    if (scheme == 0 && (h->ncomp != 1 || h->dist))
+        return fail(h, ADS_E_INVAL, "ads_set_scheme: the literal scheme is for single-GPU P-wave handles");
+    drop_graphs(h);  // the graphs bake the kick coefficient
+    h->scheme = scheme;
+    h->have_state = false;  // V means something else under the other scheme: set the state again
+    return ADS_OK;
+}
+
 int ads_modal_basis(int nel, int p, int bc, double *lambda, double *phi) {
     if (nel < 1 || p < 1 || p > kMaxP || (bc != ADS_BC_NATURAL && bc != ADS_BC_DIRICHLET0) || !lambda || !phi)
         return ADS_E_INVAL;
@@ -1230,6 +1253,7 @@ int ads_modal_advance(ads_handle h, long nsteps) {
     if (rc) return rc;
     if (nsteps < 0) return fail(h, ADS_E_INVAL, "ads_modal_advance: nsteps < 0");
     if (h->ncomp != 1 || h->dist) return fail(h, ADS_E_INVAL, "ads_modal_advance: single-GPU P-wave handles only");
+    if (h->scheme != 1) return fail(h, ADS_E_INVAL, "ads_modal_advance: scheme R1 only");
     if (!h->have_state) return fail(h, ADS_E_STATE, "ads_modal_advance before ads_set_state");
     if (nsteps == 0) return ADS_OK;
     if ((rc = modal_prepare(h))) return rc;
@@ -1498,7 +1522,7 @@ int ads_get_state(ads_handle h, double *u, double *udot, double *a, int mem) {
             if (udot) {
                 CUDA_TRY(m, cudaMemcpyAsync(m->Wk, comp(m->V, m, c), sizeof(double) * m->Nalloc,
                                             cudaMemcpyDeviceToDevice, m->stream));
-                launch_axpby(m->Nalloc, -0.5 * m->tau, comp(m->A, m, c), 1.0, m->Wk, m->stream);
+                launch_axpby(m->Nalloc, -vel_corr(m), comp(m->A, m, c), 1.0, m->Wk, m->stream);
                 if ((rc = check_launch(m, "axpby"))) return rc;
                 if ((rc = copy_out(m, udot + off + c * m->N, m->Wk, mem))) return rc;
             }

@@ -293,3 +293,38 @@ def test_kop_z_split_is_bitwise_invariant(ads, tmp_path, nz):
         assert r.returncode == 0, r.stderr[-2000:]
         out[tag] = np.load(f)
     assert np.array_equal(out["auto"], out["forced"])
+
+
+def test_literal_scheme_r0_vs_oracle(ads):
+    """ads_set_scheme(0): the literal Eq. 16 (reading R0) against the oracle's scheme=0, c1 recipe
+    and a forced case; under R0 the c1 standing mode is visibly wrong (the garble, R1)."""
+    for wl in (workloads.get("c1"), workloads.get("c3").scaled(12, 30)):
+        g = ads.Solver(wl.nel, wl.p, wl.tau, wl.bc)
+        g.set_scheme(0)
+        o = oracle.PWave(wl.nel, wl.p, wl.tau, wl.bc, scheme=0)
+        if wl.source is not None:
+            bs = oracle.source_vectors(wl)
+            g.set_source(bs, wl.source.wavelet, wl.source.f0, wl.source.t0, wl.source.amp)
+            o.set_source(bs, wl.source.wavelet, wl.source.f0, wl.source.t0, wl.source.amp)
+        u0 = oracle.project_separable(wl) if wl.u0 else np.zeros(g.shape)
+        g.set_state(u0)
+        o.set_state(u0)
+        for n in (1, wl.steps - 1):
+            g.step(n)
+            o.step(n)
+            gs, os_ = g.get_state(), o.get_state()
+            # the literal update U + tau V' - tau^2/2 a equals U + tau V only up to rounding: from a
+            # zero state the oracle's U after one step is ~1e-26, the GPU's exactly 0, so each
+            # field is compared against the state's scale (u, tau udot, tau^2 a)
+            scale = max(np.linalg.norm(os_[0]), wl.tau * np.linalg.norm(os_[1]), wl.tau ** 2 * np.linalg.norm(os_[2]))
+            for k, (a, b) in enumerate(zip(gs, os_)):
+                f = (1.0, wl.tau, wl.tau ** 2)[k]
+                tol = STEP1_TOL if n == 1 else RUN_TOL
+                assert np.linalg.norm(a - b) <= tol * max(np.linalg.norm(b), scale / f), (n, k, rel(a, b))
+        ge, oe = g.energy(), o.energy()
+        assert abs(ge[0] - oe[0]) <= 1e-10 * abs(oe[0]) and abs(ge[1] - oe[1]) <= 1e-10 * abs(oe[1])
+    with pytest.raises(ads.AdsError):
+        g.modal_advance(2)  # the modal propagator implements R1 only
+    e = ads.Solver((4, 4, 4), 2, 1e-2, elastic=True)
+    with pytest.raises(ads.AdsError):
+        e.set_scheme(0)
