@@ -93,6 +93,14 @@ int ads_create_elastic(ads_handle *h, int nx, int ny, int nz, int p, double tau,
  *   device copies -- runs the distributed algorithm on one GPU (parity tests); state I/O
  *   uses the global arrays.
  * ads_local_extent: the handle's owned global planes. */
+/* Change the step size to tau > 0 at the current step n: the factor tables
+ * of A_d = M_d + tau^2/4 K_d are rebuilt and the run continues from the
+ * same physical state (U_n, udot_n) at the same time t_n: the half-kick start is redone at t_n,
+ * a_n = D^-1 (F(t_n) - K U_n), V = udot_n + tau/2 a_n (C2).  Later steps use
+ * t_m = t_n + (m - n) tau (ads_time).  Without a state only the tables change.  Single-GPU
+ * P-wave handles only.  Errors: ADS_E_INVAL (tau <= 0, elasticity, slabs), ADS_E_SINGULAR. */
+int ads_set_tau(ads_handle h, double tau);
+
 /* Time scheme (readings R1 and R0).  scheme = 1 (default): reading R1.
  * scheme = 0: the literal Eq. 16, kept to reproduce the printed scheme:
  *   a_{n+1} = D^-1 (F(t_{n+1}) - K (U_n + tau V_n)),  V_{n+1} = V_n + tau/2 a_{n+1},

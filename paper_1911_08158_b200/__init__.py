@@ -31,7 +31,7 @@ EXPORTS = [
     "ads_time", "ads_step_count", "ads_dims", "ads_apply_k", "ads_solve_d", "ads_sweep", "ads_launch_count",
     "ads_last_error", "ads_destroy", "ads_profile_enable", "ads_profile_read",
     "ads_get_unique_id", "ads_slab_plan", "ads_create_dist", "ads_create_virtual", "ads_local_extent",
-    "ads_modal_basis", "ads_modal_advance", "ads_set_scheme",
+    "ads_modal_basis", "ads_modal_advance", "ads_set_scheme", "ads_set_tau",
 ]
 
 
@@ -84,6 +84,7 @@ def lib():
             "ads_modal_basis": (_I, [_I, _I, _I, _VP, _VP]),
             "ads_modal_advance": (_I, [_H, _L]),
             "ads_set_scheme": (_I, [_H, _I]),
+            "ads_set_tau": (_I, [_H, _D]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -249,6 +250,11 @@ class Solver:
 
     def step(self, nsteps=1):
         self._check(lib().ads_step(self.h, nsteps))
+
+    def set_tau(self, tau):
+        """Continue with step size tau from the current state and time (ads_set_tau)."""
+        self._check(lib().ads_set_tau(self.h, tau))
+        self.tau = tau
 
     def set_scheme(self, scheme):
         """1 = reading R1 (default), 0 = the literal Eq. 16 (ads_set_scheme); set the state again."""

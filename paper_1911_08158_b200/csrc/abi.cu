@@ -41,6 +41,9 @@ struct ads_ctx {
     // time scheme (ads_set_scheme): 1 = reading R1 (default), 0 = the literal Eq. 16 (reading R0:
     // kick tau/2, no half-kick start, V reported as the velocity; single-GPU P-wave only)
     int scheme = 1;
+    // time origin (ads_set_tau): t_n = t_base + (n - n_base) tau; set_state resets it to (0, 0)
+    double t_base = 0.0;
+    long n_base = 0;
     double tau = 0.0;
     double lam = 0.0, mu = 0.0, rho = 1.0;  // elasticity (ncomp = 3)
     long step = 0;
@@ -189,6 +192,9 @@ double ricker(double t, double f0, double t0) {
     x = x * x;
     return (1.0 - 2.0 * x) * std::exp(-x);
 }
+
+// time of step n (the step size may have changed at n_base, ads_set_tau)
+double time_at(const ads_ctx *h, long n) { return h->t_base + (double)(n - h->n_base) * h->tau; }
 
 // kick coefficient of V += c a and the offset of the reported velocity udot = V - c' a
 double kick_coef(const ads_ctx *h) { return h->scheme == 1 ? h->tau : 0.5 * h->tau; }
@@ -408,7 +414,8 @@ int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g
             a.dstep = h->dstep;
             a.wav = h->wavelet == ADS_WAVELET_RICKER;
             a.f0 = h->f0;
-            a.t0 = h->t0;
+            // device time (n + 1) tau_g; shifting the wavelet centre moves the time origin
+            a.t0 = h->t0 - (h->t_base - (double)h->n_base * h->tau);
             a.amp = h->amp;
             a.tau_g = h->tau;
         }
@@ -472,7 +479,7 @@ int run_solve(ads_ctx *h, const double *r_in, double *scratch, double *r2, doubl
 // one single-GPU P-wave step n -> n+1 (drift + RHS, three sweeps, kick); devsrc: source time
 // from the device step counter (graph capture), else from the host counter
 int enqueue_step(ads_ctx *h, bool keepA, bool devsrc) {
-    const double t1 = (double)(h->step + 1) * h->tau;  // F at t_{n+1} (C14)
+    const double t1 = time_at(h, h->step + 1);  // F at t_{n+1} (C14)
     int rc;
     if ((rc = run_kop(h, h->U, h->V, h->tau, devsrc ? 0.0 : source_g(h, t1), -1.0, h->U2, h->R, devsrc))) return rc;
     if ((rc = run_solve(h, h->R, h->Wk, h->R, keepA ? h->A : nullptr, h->V, kick_coef(h)))) return rc;
@@ -552,6 +559,8 @@ int init_state(ads_ctx *h) {
         CUDA_TRY(h, cudaMemsetAsync(h->dstep, 0, sizeof(long), h->stream));  // device step counter n = 0
     }
     h->step = 0;
+    h->t_base = 0.0;
+    h->n_base = 0;
     h->have_state = true;
     for (ads_ctx *m : h->members) {
         m->step = 0;
@@ -1224,6 +1233,39 @@ int ads_create_virtual(ads_handle *out, int nx, int ny, int nz, int p, double ta
     return ADS_OK;
 }
 
+int ads_set_tau(ads_handle h, double tau) {
+    int rc = guard(h);
+    if (rc) return rc;
+    if (!(tau > 0.0) || !std::isfinite(tau)) return fail(h, ADS_E_INVAL, "ads_set_tau: tau must be > 0");
+    if (h->ncomp != 1 || h->dist) return fail(h, ADS_E_INVAL, "ads_set_tau: single-GPU P-wave handles only");
+    if (h->have_state && h->scheme == 1) {  // udot_n = V - tau_old/2 a_n, kept in Wk
+        CUDA_TRY(h, cudaMemcpyAsync(h->Wk, h->V, sizeof(double) * h->Nalloc, cudaMemcpyDeviceToDevice, h->stream));
+        launch_axpby(h->Nalloc, -vel_corr(h), h->A, 1.0, h->Wk, h->stream);
+        if ((rc = check_launch(h, "axpby"))) return rc;
+    }
+    const double t_now = time_at(h, h->step);
+    drop_graphs(h);  // the graphs bake the factor tables
+    h->tau = tau;
+    h->t_base = t_now;
+    h->n_base = h->step;
+    for (int d = 0; d < 3; ++d) {  // A_d = M_d + tau^2/4 K_d
+        Band A = shifted(h->sp[d], tau * tau / 4.0, h->bc);
+        char what[32];
+        snprintf(what, sizeof what, "A_%d", d);
+        if ((rc = make_solve_tab(h, A, what, h->dd[d].tab))) return rc;
+        if ((rc = upload(h, &h->dd[d].aband, A.v))) return rc;
+    }
+    if (h->have_state && h->scheme == 1) {
+        // restart at t_n from (U_n, udot_n): a_n = D^-1 (F(t_n) - K U_n), V = udot_n + tau/2 a_n
+        CUDA_TRY(h, cudaMemcpyAsync(h->V, h->Wk, sizeof(double) * h->Nalloc, cudaMemcpyDeviceToDevice, h->stream));
+        if ((rc = run_kop(h, h->U, h->U, 0.0, source_g(h, t_now), -1.0, nullptr, h->R))) return rc;
+        if ((rc = run_sweep(h, 0, h->R, h->Wk, nullptr, 0.0))) return rc;
+        if ((rc = run_sweep(h, 1, h->Wk, h->R, nullptr, 0.0))) return rc;
+        if ((rc = run_sweep(h, 2, h->R, h->A, h->V, 0.5 * tau))) return rc;
+    }
+    return ADS_OK;
+}
+
 int ads_set_scheme(ads_handle h, int scheme) {
     int rc = guard(h);
     if (rc) return rc;
@@ -1279,7 +1321,7 @@ int ads_modal_advance(ads_handle h, long nsteps) {
             h->mg_cap = nsteps;
         }
         std::vector<double> gv(nsteps);
-        for (long s = 0; s < nsteps; ++s) gv[s] = source_g(h, (double)(h->step + s + 1) * h->tau);
+        for (long s = 0; s < nsteps; ++s) gv[s] = source_g(h, time_at(h, h->step + s + 1));
         CUDA_TRY(h, cudaMemcpy(h->mg, gv.data(), sizeof(double) * nsteps, cudaMemcpyHostToDevice));
         gdev = h->mg;
     }
@@ -1296,7 +1338,7 @@ int ads_modal_advance(ads_handle h, long nsteps) {
     h->step += nsteps;
     // a_n = D^-1 (F(t_n) - K U_n) (= P3 ca exactly; the operator kernel and three sweeps cost
     // less than a fifth transform and compute a as ads_step does)
-    if ((rc = run_kop(h, h->U, h->U, 0.0, source_g(h, (double)h->step * h->tau), -1.0, nullptr, h->R))) return rc;
+    if ((rc = run_kop(h, h->U, h->U, 0.0, source_g(h, time_at(h, h->step)), -1.0, nullptr, h->R))) return rc;
     if ((rc = run_sweep(h, 0, h->R, h->Wk, nullptr, 0.0))) return rc;
     if ((rc = run_sweep(h, 1, h->Wk, h->R, nullptr, 0.0))) return rc;
     if ((rc = run_sweep(h, 2, h->R, h->A, nullptr, 0.0))) return rc;
@@ -1470,7 +1512,7 @@ int ads_step(ads_handle h, int nsteps) {
             h->step += 1;
             continue;
         }
-        const double t1 = (double)(h->step + 1) * h->tau;  // F at t_{n+1} (C14)
+        const double t1 = time_at(h, h->step + 1);  // F at t_{n+1} (C14)
         if (h->dist) {
             if ((rc = dist_solve(h, h->tau, source_g(h, t1), h->tau, s == nsteps - 1))) return rc;
             h->step += 1;
@@ -1533,7 +1575,7 @@ int ads_get_state(ads_handle h, double *u, double *udot, double *a, int mem) {
     return ADS_OK;
 }
 
-double ads_time(ads_handle h) { return h ? (double)h->step * h->tau : NAN; }
+double ads_time(ads_handle h) { return h ? time_at(h, h->step) : NAN; }
 long ads_step_count(ads_handle h) { return h ? h->step : -1; }
 
 int ads_dims(ads_handle h, int *nx, int *ny, int *nz, int *ncomp) {

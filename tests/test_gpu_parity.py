@@ -328,3 +328,49 @@ def test_literal_scheme_r0_vs_oracle(ads):
     e = ads.Solver((4, 4, 4), 2, 1e-2, elastic=True)
     with pytest.raises(ads.AdsError):
         e.set_scheme(0)
+
+
+@pytest.mark.parametrize("forced", [False, True])
+def test_set_tau_restart_vs_oracle(ads, forced):
+    """ads_set_tau (row f4): n1 steps at tau1, then n2 steps at tau2 from the same physical state
+    and time, against the oracle restarted from (u, udot) with tau2 and, when forced, the wavelet
+    centre shifted by t_n1 (the oracle's clock restarts at 0)."""
+    wl = workloads.get("c3").scaled(12, 0) if forced else workloads.get("c1")
+    tau1, tau2, n1, n2 = wl.tau, 0.6 * wl.tau, 9, 14
+    g = ads.Solver(wl.nel, wl.p, tau1, wl.bc)
+    o1 = oracle.PWave(wl.nel, wl.p, tau1, wl.bc)
+    bs = oracle.source_vectors(wl) if forced else None
+    if forced:
+        g.set_source(bs, wl.source.wavelet, wl.source.f0, wl.source.t0, wl.source.amp)
+        o1.set_source(bs, wl.source.wavelet, wl.source.f0, wl.source.t0, wl.source.amp)
+    u0 = oracle.project_separable(wl) if wl.u0 else np.zeros(g.shape)
+    g.set_state(u0)
+    o1.set_state(u0)
+    g.step(n1)
+    o1.step(n1)
+    ou, oud, _ = o1.get_state()
+    del o1
+    g.set_tau(tau2)
+    g.step(n2)
+    assert abs(g.time() - (n1 * tau1 + n2 * tau2)) <= 1e-15
+    o2 = oracle.PWave(wl.nel, wl.p, tau2, wl.bc)
+    if forced:
+        o2.set_source(bs, wl.source.wavelet, wl.source.f0, wl.source.t0 - n1 * tau1, wl.source.amp)
+    o2.set_state(ou, oud)
+    o2.step(n2)
+    for a, b in zip(g.get_state(), o2.get_state()):
+        assert rel(a, b) < RUN_TOL, rel(a, b)
+
+
+def test_set_tau_same_step_is_transparent(ads):
+    """set_tau with the current tau (forced, graph-replayed steps after it) reproduces the
+    uninterrupted run: the restart's a_n equals the stored one and the source clock is kept."""
+    wl = workloads.get("c3").scaled(14, 40)
+    g = ads.make_solver(wl)
+    g.step(17)
+    g.set_tau(wl.tau)
+    g.step(23)
+    s = ads.make_solver(wl)
+    s.step(40)
+    for a, b in zip(g.get_state(), s.get_state()):
+        assert rel(a, b) < 1e-12
