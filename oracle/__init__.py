@@ -108,15 +108,18 @@ def knots(p, nel):
 
 
 def matrices_1d(p, nel, bc=0):
-    """Dense (M, K, B) of the 1D space."""
-    n = nel + p
+    """Dense (M, K, B) of the 1D space; nel = 0: the 2D scheme's third
+    axis (one function, M = 1, K = B = 0)."""
+    n = 1 if nel == 0 else nel + p
     M, K, B = np.zeros((n, n)), np.zeros((n, n)), np.zeros((n, n))
     _check(lib().or_matrices_1d(p, nel, bc, _ptr(M), _ptr(K), _ptr(B)))
     return M, K, B
 
 
 def load_1d(p, nel, bc, func):
-    """b_a = int f N_a for a workloads.Func1D descriptor."""
+    """b_a = int f N_a for a workloads.Func1D descriptor (nel = 0: the 2D scheme's third axis, [1])."""
+    if nel == 0:
+        return np.ones(1)
     n = nel + p
     b = np.zeros(n)
     if func[0] == "sin":
@@ -152,7 +155,7 @@ class PWave:
         if isinstance(nel, int):
             nel = (nel, nel, nel)
         self.nel, self.p, self.tau, self.bc = tuple(nel), p, tau, bc
-        self.n = tuple(e + p for e in nel)
+        self.n = tuple(1 if e == 0 else e + p for e in nel)  # nel_z = 0: the 2D scheme (one z function)
         self.shape = (self.n[2], self.n[1], self.n[0])  # numpy (z, y, x): x fastest
         self.N = int(np.prod(self.n))
         h = _P()

@@ -131,7 +131,12 @@ void or_gauss(int m, double *xi, double *w) {
 /* bc = 1: zero Dirichlet -> rows/cols of the two end functions zeroed (C3). */
 /* ------------------------------------------------------------------------ */
 int or_matrices_1d(int p, int nel, int bc, double *M, double *K, double *B) {
-    if (p < 1 || nel < 1) return OR_E_INVAL;
+    if (p < 1 || nel < 0) return OR_E_INVAL;
+    if (nel == 0) {  /* the 2D scheme's third axis: one function, M = 1, K = B = 0 (see or_pw_create) */
+        M[0] = 1.0; K[0] = 0.0;
+        if (B) B[0] = 0.0;
+        return OR_OK;
+    }
     int n = nel + p;
     double *t = (double *)malloc(sizeof(double) * (nel + 2 * p + 1));
     double xi[16], wq[16];
@@ -300,6 +305,7 @@ double or_ricker(double t, double f0, double t0) {
 /* ------------------------------------------------------------------------ */
 typedef struct {
     int n[3], nel[3], p, bc, scheme;   /* scheme 1 = R1 (default), 0 = literal Eq. 16 */
+    int bcd[3];                        /* zero Dirichlet on direction d (the 2D axis has none) */
     double tau, eta;
     long step;
     double *M[3], *K[3], *A[3], *LU[3], *MDLU[3];
@@ -323,15 +329,19 @@ long or_pw_size(const or_pwave *h) { return (long)h->n[0] * h->n[1] * h->n[2]; }
 
 int or_pw_create(or_pwave **out, int nelx, int nely, int nelz, int p, double tau, int bc, int scheme) {
     *out = NULL;
-    if (p < 1 || p > 5 || nelx < 1 || nely < 1 || nelz < 1 || !(tau > 0.0) || !isfinite(tau) || (bc != 0 && bc != 1))
+    /* nelz = 0: the 2D scheme as the paper prints it (Eqs. 14-16): a third axis
+     * with one function, M_z = 1, K_z = 0 and no boundary, so that K = Kx(x)My + Mx(x)Ky and
+     * D = Ax(x)Ay exactly (Kronecker products with the 1 x 1 identity) */
+    if (p < 1 || p > 5 || nelx < 1 || nely < 1 || nelz < 0 || !(tau > 0.0) || !isfinite(tau) || (bc != 0 && bc != 1))
         return OR_E_INVAL;
     or_pwave *h = (or_pwave *)calloc(1, sizeof(or_pwave));
     int nel[3] = {nelx, nely, nelz};
     h->p = p; h->bc = bc; h->tau = tau; h->eta = tau * tau / 4.0; h->scheme = scheme;  /* eta: PAPER.md:173 */
     for (int d = 0; d < 3; ++d) {
-        int n = nel[d] + p;
+        int n = nel[d] == 0 ? 1 : nel[d] + p;
         h->nel[d] = nel[d]; h->n[d] = n;
-        if (bc == 1 && n < 3) { pw_free(h); return OR_E_INVAL; }
+        h->bcd[d] = nel[d] == 0 ? 0 : bc;
+        if (h->bcd[d] == 1 && n < 3) { pw_free(h); return OR_E_INVAL; }
         h->M[d] = (double *)malloc(sizeof(double) * n * n);
         h->K[d] = (double *)malloc(sizeof(double) * n * n);
         h->A[d] = (double *)malloc(sizeof(double) * n * n);
@@ -341,7 +351,7 @@ int or_pw_create(or_pwave **out, int nelx, int nely, int nelz, int p, double tau
         /* A_d = M_d + tau^2/4 K_d   (Eq. 16) */
         for (int q = 0; q < n * n; ++q) h->A[d][q] = h->M[d][q] + h->eta * h->K[d][q];
         memcpy(h->MDLU[d], h->M[d], sizeof(double) * n * n);
-        if (bc == 1) {
+        if (h->bcd[d] == 1) {
             h->A[d][0] = 1.0; h->A[d][n * n - 1] = 1.0;
             h->MDLU[d][0] = 1.0; h->MDLU[d][n * n - 1] = 1.0;
         }
@@ -374,7 +384,7 @@ int or_pw_set_source(or_pwave *h, const double *bx, const double *by, const doub
     for (int d = 0; d < 3; ++d) {
         h->src[d] = (double *)malloc(sizeof(double) * h->n[d]);
         memcpy(h->src[d], b[d], sizeof(double) * h->n[d]);
-        if (h->bc == 1) { h->src[d][0] = 0.0; h->src[d][h->n[d] - 1] = 0.0; }
+        if (h->bcd[d] == 1) { h->src[d][0] = 0.0; h->src[d][h->n[d] - 1] = 0.0; }
     }
     h->has_src = 1; h->wavelet = wavelet; h->f0 = f0; h->t0 = t0; h->amp = amp;
     return OR_OK;
@@ -442,7 +452,8 @@ int or_pw_set_state(or_pwave *h, const double *u, const double *udot) {
         for (int j = 0; j < n[1]; ++j)
             for (int i = 0; i < n[0]; ++i) {
                 long q = ((long)k * n[1] + j) * n[0] + i;
-                int bnd = h->bc == 1 && (i == 0 || j == 0 || k == 0 || i == n[0] - 1 || j == n[1] - 1 || k == n[2] - 1);
+                int bnd = (h->bcd[0] && (i == 0 || i == n[0] - 1)) || (h->bcd[1] && (j == 0 || j == n[1] - 1)) ||
+                          (h->bcd[2] && (k == 0 || k == n[2] - 1));
                 h->U[q] = bnd ? 0.0 : u[q];
                 h->V[q] = bnd ? 0.0 : (udot ? udot[q] : 0.0);
             }

@@ -23,7 +23,8 @@ implementation of the step independent of oracle/ads_oracle.c's step logic; it
 shares only the oracle's 1D Gram matrices (pinned separately against
 closed-form cardinal B-spline rows and scipy-BSpline brute-force quadrature).
 Only zero Dirichlet (bc = 1) is supported: the eigenproblem is posed on the
-interior-restricted 1D matrices (reading C3).
+interior-restricted 1D matrices (reading C3).  nel_z = 0 is the 2D scheme as printed
+(PAPER.md:123-143): the third axis has one function, M = 1, K = 0, no boundary.
 """
 from __future__ import annotations
 
@@ -38,12 +39,14 @@ class ModalPWave:
         if isinstance(nel, int):
             nel = (nel, nel, nel)
         self.nel, self.p, self.tau = tuple(nel), p, tau
-        self.n = tuple(e + p for e in nel)
+        self.n = tuple(1 if e == 0 else e + p for e in nel)
         self.eta = tau * tau / 4.0
         self.P, self.lam, self.Q = [], [], []
+        # active DOFs per direction: interior (Dirichlet) or the single function of the 2D axis
+        self.sl = tuple(slice(None) if e == 0 else slice(1, -1) for e in nel)
         for d in range(3):
             M, K, _ = matrices_1d(p, nel[d], bc=1)
-            Mi, Ki = M[1:-1, 1:-1], K[1:-1, 1:-1]
+            Mi, Ki = M[self.sl[d], self.sl[d]], K[self.sl[d], self.sl[d]]
             lam, P = scipy.linalg.eigh(Ki, Mi)   # P^T Mi P = I, Ki P = Mi P diag(lam)
             self.P.append(P)
             self.lam.append(lam)
@@ -63,13 +66,13 @@ class ModalPWave:
 
     def to_modal(self, u):
         """c = P3^T M u for a full (nz, ny, nx) coefficient array (boundary ignored)."""
-        ui = np.asarray(u)[1:-1, 1:-1, 1:-1]
+        ui = np.asarray(u)[self.sl[2], self.sl[1], self.sl[0]]
         return self._modes(ui, self.Q[0], self.Q[1], self.Q[2])
 
     def from_modal(self, c):
         ui = self._modes(c, self.P[0], self.P[1], self.P[2])
         u = np.zeros((self.n[2], self.n[1], self.n[0]))
-        u[1:-1, 1:-1, 1:-1] = ui
+        u[self.sl[2], self.sl[1], self.sl[0]] = ui
         return u
 
     def run(self, u0, udot0=None, nsteps=0, source=None, wavelet=1, f0=25.0, t0=0.04, amp=1.0):
@@ -81,7 +84,7 @@ class ModalPWave:
         cU = self.to_modal(u0)
         cV = np.zeros_like(cU) if udot0 is None else self.to_modal(udot0)
         if source is not None:
-            fs = [self.P[d].T @ np.asarray(source[d])[1:-1] for d in range(3)]
+            fs = [self.P[d].T @ np.asarray(source[d])[self.sl[d]] for d in range(3)]
             cFs = fs[2][:, None, None] * fs[1][None, :, None] * fs[0][None, None, :]
 
             def g(t):

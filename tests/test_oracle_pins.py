@@ -435,3 +435,64 @@ def test_elastic_second_order():
         errs.append(np.linalg.norm(u.ravel() - ex))
     ratios = [errs[0] / errs[1], errs[1] / errs[2]]
     assert all(3.7 < r < 4.3 for r in ratios), ratios
+
+
+# ---- the 2D scheme as printed: nel_z = 0 (row f2) ----
+
+def _wl2d(nel, p, tau, steps, source=None):
+    sin = ("sin",)
+    return workloads.Workload(name="2d", p=p, nel=nel, tau=tau, steps=steps, source=source,
+                              u0=[] if source else [workloads.SeparableTerm(1.0, 0, (sin, sin, sin))])
+
+
+def test_2d_equals_z_constant_3d_natural_bc():
+    """With natural BC the constant is in the kernel of K_z and A_z 1 = M_z 1, so a 3D state that
+    is constant in z evolves exactly as the 2D scheme (x) 1: K(u2 (x) 1) = (K2D u2) (x) M_z 1 and
+    D^-1 (v (x) M_z 1) = (D2D^-1 v) (x) 1.  Pins the 2D path on the (separately pinned) 3D one."""
+    p, tau, steps = 2, 1e-2, 12
+    o2 = oracle.PWave((9, 7, 0), p, tau, bc=0)
+    o3 = oracle.PWave((9, 7, 5), p, tau, bc=0)
+    rng = np.random.default_rng(3)
+    u2, v2 = rng.standard_normal(o2.shape), rng.standard_normal(o2.shape)
+    o2.set_state(u2, v2)
+    o3.set_state(np.repeat(u2, o3.shape[0], axis=0), np.repeat(v2, o3.shape[0], axis=0))
+    o2.step(steps)
+    o3.step(steps)
+    for a2, a3 in zip(o2.get_state(), o3.get_state()):
+        for k in range(o3.shape[0]):
+            assert np.abs(a3[k] - a2[0]).max() <= 1e-12 * np.abs(a2).max()
+
+
+def test_2d_standing_mode_closed_form():
+    """u0 = L2 projection of sin(pi x) sin(pi y), zero Dirichlet, udot0 = 0: the PDE solution is
+    cos(sqrt(2) pi t) u0; the discrete solution after 20 steps (tau = 0.01, p = 2, 16^2 elements)
+    must match it to the spatial/temporal discretisation error (~1e-4, like c1's 2.19e-4 in 3D).
+    A dropped or doubled stiffness term (wrong wave speed) misses by > 1e-2."""
+    wl = _wl2d((16, 16, 0), 2, 1e-2, 20)
+    o = oracle.make_solver(wl)
+    u0 = o.get_state()[0].copy()
+    o.step(wl.steps)
+    u = o.get_state()[0]
+    exact = math.cos(math.sqrt(2.0) * math.pi * wl.steps * wl.tau) * u0
+    err = np.linalg.norm(u - exact) / np.linalg.norm(exact)
+    assert err < 5e-4, err
+    # the same for a 1.5x wave speed (K scaled) is far off: the check has teeth
+    exact_wrong = math.cos(1.5 * math.sqrt(2.0) * math.pi * wl.steps * wl.tau) * u0
+    assert np.linalg.norm(u - exact_wrong) / np.linalg.norm(exact_wrong) > 1e-2
+
+
+@pytest.mark.parametrize("forced", [False, True])
+def test_2d_stepping_vs_modal_closed_form(forced):
+    src = workloads.Source(f=(("gauss", 0.4, 0.1), ("gauss", 0.55, 0.1), ("sin",))) if forced else None
+    wl = _wl2d((13, 10, 0), 3, 5e-3, 30, src)
+    o = oracle.make_solver(wl)
+    u0 = o.get_state()[0].copy()
+    o.step(wl.steps)
+    m = ModalPWave(wl.nel, wl.p, wl.tau)
+    if forced:
+        mu, mud, ma = m.run(u0, nsteps=wl.steps, source=oracle.source_vectors(wl), wavelet=src.wavelet,
+                            f0=src.f0, t0=src.t0)
+    else:
+        mu, mud, ma = m.run(u0, nsteps=wl.steps)
+    for a, b in zip(o.get_state(), (mu, mud, ma)):
+        assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)

@@ -83,7 +83,8 @@ class Workload:
 
     @property
     def n(self) -> Tuple[int, int, int]:
-        return tuple(e + self.p for e in self.nel)
+        # nel_z = 0: a 2D workload (one function along z)
+        return tuple(1 if e == 0 else e + self.p for e in self.nel)
 
     @property
     def ndof(self) -> int:
