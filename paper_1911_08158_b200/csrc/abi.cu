@@ -193,6 +193,9 @@ double ricker(double t, double f0, double t0) {
     return (1.0 - 2.0 * x) * std::exp(-x);
 }
 
+// global plane count for the Dirichlet mask of z, 0 when z has no boundary (2D axis)
+int zmask(const ads_ctx *m) { return m->sp[2].bc == ADS_BC_DIRICHLET0 ? m->ngz : 0; }
+
 // time of step n (the step size may have changed at n_base, ads_set_tau)
 double time_at(const ads_ctx *h, long n) { return h->t_base + (double)(n - h->n_base) * h->tau; }
 
@@ -325,9 +328,10 @@ int build_slab_tables(ads_ctx *h, const Band &A) {
 int build_direction(ads_ctx *h, int d) {
     Space1D &s = h->sp[d];
     const int p = h->p;
-    if (build_space(p, h->nel[d], h->bc, s)) return fail(h, ADS_E_INVAL, "bad 1D space");
+    if (h->nel[d] == 0) trivial_space(p, s);  // 2D: the third axis (ads_create nz = 0)
+    else if (build_space(p, h->nel[d], h->bc, s)) return fail(h, ADS_E_INVAL, "bad 1D space");
     const int n = s.n, W = 2 * p + 1;
-    Band Mm = shifted(s, 0.0, h->bc);
+    Band Mm = shifted(s, 0.0, s.bc);
     if (banded_lu(Mm, h->mass_lu[d])) return fail(h, ADS_E_SINGULAR, "M_%d singular", d);
     DirDev &D = h->dd[d];
     // Toeplitz interior of M, K (build_space made rows [2p, n-1-2p] bitwise equal)
@@ -350,7 +354,7 @@ int build_direction(ads_ctx *h, int d) {
     if (h->ncomp == 1) {
         // P-wave: A_d = M_d + tau^2/4 K_d (eta = tau^2/4 PAPER.md:173)
         const double eta = h->tau * h->tau / 4.0;
-        Band A = shifted(s, eta, h->bc);
+        Band A = shifted(s, eta, s.bc);
         snprintf(what, sizeof what, "A_%d", d);
         if (d == 2 && h->dist) {
             if ((rc = build_slab_tables(h, A))) return rc;
@@ -363,7 +367,7 @@ int build_direction(ads_ctx *h, int d) {
         // (Eq. 37, 3D reading DESIGN.md E1); B_d for the coupling blocks
         const double cl = h->tau * h->tau / (4.0 * h->rho) * (2.0 * h->mu + h->lam);
         const double cs = h->tau * h->tau / (4.0 * h->rho) * h->mu;
-        Band AL = shifted(s, cl, h->bc), AS = shifted(s, cs, h->bc);
+        Band AL = shifted(s, cl, s.bc), AS = shifted(s, cs, s.bc);
         snprintf(what, sizeof what, "SL_%d", d);
         if ((rc = make_solve_tab(h, AL, what, D.tabL))) return rc;
         snprintf(what, sizeof what, "SS_%d", d);
@@ -983,13 +987,13 @@ int modal_prepare(ads_ctx *h) {
         CUBLAS_TRY(h, cublasCreate(&h->cub));
         CUBLAS_TRY(h, cublasSetStream(h->cub, h->stream));
     }
-    const int o = h->bc == ADS_BC_DIRICHLET0 ? 1 : 0;
     for (int d = 0; d < 3; ++d) {
+        const int o = h->sp[d].bc == ADS_BC_DIRICHLET0 ? 1 : 0;
         const int n = h->n[d], na = n - 2 * o;
         std::vector<double> lam, phi;
         int e = -1;  // an earlier direction with the same 1D space
         for (int c = 0; c < d; ++c)
-            if (h->nel[c] == h->nel[d]) e = c;
+            if (h->nel[c] == h->nel[d] && h->sp[c].bc == h->sp[d].bc) e = c;
         if (e >= 0) {
             phi = h->mphi_h[e];
         } else if (modal_basis(h->sp[d], lam, phi)) {
@@ -1054,10 +1058,11 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
                          ncclComm_t comm = nullptr) {
     if (!out) return ADS_E_INVAL;
     *out = nullptr;
-    if (p < 1 || p > 5 || nx < 1 || ny < 1 || nz < 1 || !(tau > 0.0) || !std::isfinite(tau) ||
-        (bc != ADS_BC_NATURAL && bc != ADS_BC_DIRICHLET0))
+    // nz = 0: the 2D scheme (single-GPU P-wave handles; trivial_space)
+    if (p < 1 || p > 5 || nx < 1 || ny < 1 || nz < 0 || (nz == 0 && (ncomp != 1 || dist)) || !(tau > 0.0) ||
+        !std::isfinite(tau) || (bc != ADS_BC_NATURAL && bc != ADS_BC_DIRICHLET0))
         return ADS_E_INVAL;
-    if (bc == ADS_BC_DIRICHLET0 && (nx + p < 3 || ny + p < 3 || nz + p < 3)) return ADS_E_INVAL;
+    if (bc == ADS_BC_DIRICHLET0 && (nx + p < 3 || ny + p < 3 || (nz > 0 && nz + p < 3))) return ADS_E_INVAL;
     if (nx + p > 1056 || ny + p > 1056) return ADS_E_INVAL;  // n_d <= 32 x 33 (sweep chunking)
     if (world < 1 || rank < 0 || rank >= world) return ADS_E_INVAL;
     ads_ctx *h = new (std::nothrow) ads_ctx;
@@ -1076,7 +1081,7 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
     h->rank = rank;
     h->world = world;
     h->comm = comm;
-    h->ngz = nz + p;
+    h->ngz = nz == 0 ? 1 : nz + p;
     int rc = ADS_OK;
     if (dist) {
         std::vector<int> z0s, nls;
@@ -1091,7 +1096,7 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
     }
     cudaGetDevice(&h->device);
     for (int d = 0; d < 3 && rc == ADS_OK; ++d) {
-        h->n[d] = h->nel[d] + p;
+        h->n[d] = h->nel[d] == 0 ? 1 : h->nel[d] + p;
         rc = build_direction(h, d);
     }
     if (rc == ADS_OK && dist) {
@@ -1249,7 +1254,7 @@ int ads_set_tau(ads_handle h, double tau) {
     h->t_base = t_now;
     h->n_base = h->step;
     for (int d = 0; d < 3; ++d) {  // A_d = M_d + tau^2/4 K_d
-        Band A = shifted(h->sp[d], tau * tau / 4.0, h->bc);
+        Band A = shifted(h->sp[d], tau * tau / 4.0, h->sp[d].bc);
         char what[32];
         snprintf(what, sizeof what, "A_%d", d);
         if ((rc = make_solve_tab(h, A, what, h->dd[d].tab))) return rc;
@@ -1302,8 +1307,8 @@ int ads_modal_advance(ads_handle h, long nsteps) {
     const double *fvec[3] = {nullptr, nullptr, nullptr};
     const double *gdev = nullptr;
     if (h->has_src) {  // modal load vectors Phi_d^T b_d (dual: no M) and g(t_{n+s}), s = 1..nsteps
-        const int o = h->bc == ADS_BC_DIRICHLET0 ? 1 : 0;
         for (int d = 0; d < 3; ++d) {
+            const int o = h->sp[d].bc == ADS_BC_DIRICHLET0 ? 1 : 0;
             const int n = h->n[d], na = n - 2 * o;
             std::vector<double> f(n, 0.0);
             for (int k = 0; k < na; ++k) {
@@ -1409,7 +1414,7 @@ int ads_set_source(ads_handle h, const double *bx, const double *by, const doubl
     for (int d = 0; d < 3 && h->dist != 2; ++d) {
         const int nd = d == 2 ? h->ngz : h->n[d];  // z: global rows (slabs index with zbeg)
         std::vector<double> v(b[d], b[d] + nd);
-        if (h->bc == ADS_BC_DIRICHLET0) v[0] = v[nd - 1] = 0.0;
+        if (h->sp[d].bc == ADS_BC_DIRICHLET0) v[0] = v[nd - 1] = 0.0;
         if (!h->src[d]) {
             if ((rc = dalloc(h, (void **)&h->src[d], sizeof(double) * nd))) return rc;
         }
@@ -1439,9 +1444,9 @@ int ads_set_state(ads_handle h, const double *u, const double *udot, int mem) {
                 CUDA_TRY(m, cudaMemsetAsync(comp(m->V, m, c), 0, sizeof(double) * m->Nalloc, m->stream));
             }
             if (m->bc == ADS_BC_DIRICHLET0) {
-                launch_mask_boundary(comp(m->U, m, c), m->geo, m->stream, m->zbeg, m->ngz);
+                launch_mask_boundary(comp(m->U, m, c), m->geo, m->stream, m->zbeg, zmask(m));
                 if ((rc = check_launch(m, "mask"))) return rc;
-                launch_mask_boundary(comp(m->V, m, c), m->geo, m->stream, m->zbeg, m->ngz);
+                launch_mask_boundary(comp(m->V, m, c), m->geo, m->stream, m->zbeg, zmask(m));
                 if ((rc = check_launch(m, "mask"))) return rc;
             }
         }
@@ -1485,7 +1490,7 @@ int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const i
         }
         if (m->bc == ADS_BC_DIRICHLET0)
             for (int c = 0; c < m->ncomp; ++c) {
-                launch_mask_boundary(comp(m->U, m, c), m->geo, m->stream, m->zbeg, m->ngz);
+                launch_mask_boundary(comp(m->U, m, c), m->geo, m->stream, m->zbeg, zmask(m));
                 if ((rc = check_launch(m, "mask"))) return rc;
             }
     }

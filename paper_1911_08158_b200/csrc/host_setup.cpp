@@ -149,7 +149,23 @@ int build_space(int p, int nel, int bc, Space1D &s) {
     return 0;
 }
 
+void trivial_space(int p, Space1D &s) {
+    s.p = p;
+    s.nel = 0;
+    s.n = 1;
+    s.bc = 0;
+    s.knots.clear();
+    s.M = Band(1, p);
+    s.K = Band(1, p);
+    s.B = Band(1, p);
+    s.M.at(0, 0) = 1.0;
+}
+
 void load_vector(const Space1D &s, int func, double c, double sigma, double *out) {
+    if (s.nel == 0) {  // the 2D axis: the load of any f(x, y) (x) 1 has the factor 1
+        out[0] = 1.0;
+        return;
+    }
     const double kPi = 3.141592653589793238462643383;
     double xg[8], wg[8], N[8], dN[8];
     gauss_legendre(8, xg, wg);

@@ -35,6 +35,9 @@ int gauss_legendre(int m, double *x, double *w);
 // N[0..p], dN[0..p] belong to functions span-p .. span.
 void basis_and_derivs(const std::vector<double> &t, int p, int span, double x, double *N, double *dN);
 int build_space(int p, int nel, int bc, Space1D &s);
+// The 2D scheme's third axis (ads_create with nz = 0; PAPER.md:123-143 as printed in 2D): one
+// function, M = 1, K = B = 0, no boundary -- K = Kx(x)My + Mx(x)Ky and D = Ax(x)Ay exactly.
+void trivial_space(int p, Space1D &s);
 // b_a = int f N_a over [0,1], 8-point Gauss per element; func 0 sin(pi x), 1 Gaussian.
 void load_vector(const Space1D &s, int func, double c, double sigma, double *out);
 

@@ -1039,7 +1039,7 @@ __global__ void mask_boundary_kernel(double *u, Geom g, int zoff, int ngz) {
         int j = t % g.n1;
         int k = t / g.n1;
         const int kg = k + zoff;  // global plane
-        if (i == 0 || j == 0 || kg == 0 || i == g.n0 - 1 || j == g.n1 - 1 || kg == ngz - 1)
+        if (i == 0 || j == 0 || i == g.n0 - 1 || j == g.n1 - 1 || (ngz > 0 && (kg == 0 || kg == ngz - 1)))
             u[(long)k * g.sz + (long)j * g.sy + i] = 0.0;
     }
 }

@@ -374,3 +374,70 @@ def test_set_tau_same_step_is_transparent(ads):
     s.step(40)
     for a, b in zip(g.get_state(), s.get_state()):
         assert rel(a, b) < 1e-12
+
+
+def _wl2d(nel, p, tau, steps, bc=1, source=None):
+    sin = ("sin",)
+    g = ("gauss", 0.45, 0.12)
+    return workloads.Workload(name=f"2d{nel}", p=p, nel=nel, tau=tau, steps=steps, bc=bc, source=source,
+                              u0=[] if source else [workloads.SeparableTerm(1.0, 0, (sin, g, sin))])
+
+
+@pytest.mark.parametrize("nel,p,bc,forced", [((37, 21, 0), 3, 1, False), ((20, 33, 0), 2, 0, False),
+                                             ((64, 40, 0), 3, 1, True), ((150, 7, 0), 1, 1, False)])
+def test_2d_scheme_vs_oracle(ads, nel, p, bc, forced):
+    """Row f2: the 2D scheme as printed (ads_create with nz = 0) against the oracle's 2D path,
+    one step and a 40-step run, Dirichlet and natural BC, free and Ricker-forced."""
+    src = workloads.Source(f=(("gauss", 0.4, 0.1), ("gauss", 0.55, 0.1), ("sin",))) if forced else None
+    wl = _wl2d(nel, p, 4e-3, 40, bc, src)
+    tol_first = STEP1_TOL
+    if bc == 1 and not forced:
+        # T1 (DESIGN.md §3): on smooth data a = D^-1 (-K P) cancels (kappa ~ (1/(pi h))^2, 2e3 at
+        # 150 elements); the one-step bound for udot and a is max(1e-12, 4 x the spread between
+        # the two independent oracles (C stepping vs modal) on the same u0)
+        u0 = oracle.project_separable(wl)
+        o1 = oracle.PWave(wl.nel, wl.p, wl.tau, wl.bc)
+        o1.set_state(u0)
+        o1.step(1)
+        _, oud, oa = o1.get_state()
+        _, mud, ma = ModalPWave(wl.nel, wl.p, wl.tau).run(u0, nsteps=1)
+        tol_first = max(STEP1_TOL, 4.0 * max(rel(oud, mud), rel(oa, ma)))
+    # both sides start from the oracle's projection (independent projections differ in the last
+    # ulp, which the same cancellation amplifies)
+    g = ads.Solver(wl.nel, wl.p, wl.tau, wl.bc)
+    o = oracle.PWave(wl.nel, wl.p, wl.tau, wl.bc)
+    if forced:
+        bs = oracle.source_vectors(wl)
+        g.set_source(bs, src.wavelet, src.f0, src.t0, src.amp)
+        o.set_source(bs, src.wavelet, src.f0, src.t0, src.amp)
+    u0 = oracle.project_separable(wl) if wl.u0 else np.zeros(o.shape)
+    g.set_state(u0)
+    o.set_state(u0)
+    done = 0
+    for n in (1, wl.steps):
+        g.step(n - done)
+        o.step(n - done)
+        done = n
+        errs = [rel(x, y) for x, y in zip(g.get_state(), o.get_state())]
+        assert max(errs) < (tol_first if n == 1 else RUN_TOL), (n, errs, tol_first)
+    assert g.shape == (1, nel[1] + p, nel[0] + p)
+    ge, oe = g.energy(), o.energy()
+    assert np.allclose(ge, oe, rtol=1e-11, atol=1e-15)
+
+
+def test_2d_modal_and_set_tau(ads):
+    """The f3 / f4 entry points on a 2D handle: modal advance vs stepping, and a step-size change."""
+    wl = _wl2d((30, 26, 0), 2, 5e-3, 50)
+    a, b = ads.make_solver(wl), ads.make_solver(wl)
+    a.modal_advance(50)
+    b.step(50)
+    for x, y in zip(a.get_state(), b.get_state()):
+        assert rel(x, y) < 1e-11
+    b.set_tau(2.5e-3)
+    b.step(10)
+    o = oracle.PWave(wl.nel, wl.p, 2.5e-3, wl.bc)
+    u, ud, _ = a.get_state()
+    o.set_state(u, ud)
+    o.step(10)
+    for x, y in zip(b.get_state(), o.get_state()):
+        assert rel(x, y) < 1e-10
