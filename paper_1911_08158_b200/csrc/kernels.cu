@@ -891,102 +891,201 @@ int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {
     return 0;
 }
 
-// ------------------------------------------------------------------------------------------
-// fused Kronecker triple (elasticity couplings, PAPER.md:375-387 generalised to 3D):
-//   out = alpha (Fz (x) Fy (x) Fx) in + beta out   (Fd: band [n_d][2p+1] acting along d)
-// 32 x 8 output tile marching z: per input plane the haloed plane is staged in shared memory
-// (next plane prefetched in registers), y-pass over the 32+2p columns, x-pass into a register
-// ring of 2p+1 planes, z combination of the ring.  One HBM read of `in` (+ `out` when beta != 0)
-// and one write, instead of three banded axis passes.
-// ------------------------------------------------------------------------------------------
-constexpr int K3_X = 32, K3_Y = 8;
+// One Kronecker triple out = alpha (Fx (x) Fy (x) Fz) in + beta out (elasticity couplings,
+// PAPER.md:355-387; general bands, no Toeplitz assumption).  Same structure as kop_kernel:
+// 32 x 16 output tile marching z over a piece [z0, z1); per input plane (one barrier):
+//   - all threads stream the haloed plane HBM -> shared memory in 16-byte zero-filling cp.async
+//     pieces, KR_NPF - 1 planes ahead;
+//   - y-pass items (column, 4 rows): Y = Fy in from a register window of 4 + 2p rows into a
+//     double-buffered Y tile;
+//   - x-pass of the previous plane (lane = x, 2 rows per thread): X = Fx Y;
+//   - z: a register ring of the last 2p + 1 X planes; output plane kk - 2p ... gathered with Fz.
+// HBM traffic: in read once (halos from L2), out written once (read once when beta != 0).
+constexpr int KR_X = 32, KR_Y = 16, KR_THREADS = 256, KR_NPF = 4, KR_RY = 4;
 template <int P>
-__global__ void __launch_bounds__(K3_X * K3_Y) kron3_kernel(const double *__restrict__ in, double *__restrict__ out,
-                                                            const double *__restrict__ fx, const double *__restrict__ fy,
-                                                            const double *__restrict__ fz, double alpha, double beta,
-                                                            Geom g, int zlen) {
-    constexpr int W = 2 * P + 1, HX = K3_X + 2 * P, HY = K3_Y + 2 * P, NSLOT = (HX * HY + 255) / 256;
-    __shared__ double sp[HY][HX];
-    __shared__ double sy_[K3_Y][HX];
-    __shared__ double cx[K3_X][W], cy[K3_Y][W];
-    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * K3_X + tx;
-    const int x0 = blockIdx.x * K3_X, y0 = blockIdx.y * K3_Y;
+struct KronGeo {
+    static constexpr int W = 2 * P + 1;
+    static constexpr int PA = (P + 1) & ~1;  // even x halo of the copied tile (16-byte pieces)
+    static constexpr int HX = KR_X + 2 * PA, HY = KR_Y + 2 * P, HN = HX * HY;
+    static constexpr int NC = KR_X + 2 * P;  // columns the x-pass needs
+    static constexpr int NITEM = NC * (KR_Y / KR_RY);
+    static constexpr int NPAIR = HN / 2, NSLOT = (NPAIR + KR_THREADS - 1) / KR_THREADS;
+    static constexpr int RING = KR_NPF * HN, YT = 2 * KR_Y * NC, XB = W * KR_X, YB = KR_Y * W;
+    static constexpr int SMEM = RING + YT + XB + YB;
+    static_assert(NITEM <= KR_THREADS, "one y-pass item per thread");
+};
+
+template <int P>
+__global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__restrict__ in, double *__restrict__ out,
+                                                               const double *__restrict__ fx,
+                                                               const double *__restrict__ fy,
+                                                               const double *__restrict__ fz, double alpha, double beta,
+                                                               Geom g, int zlen) {
+    using G = KronGeo<P>;
+    constexpr int W = G::W, HX = G::HX, HN = G::HN, NC = G::NC, PA = G::PA;
+    extern __shared__ __align__(16) double smem[];
+    double *ring = smem;
+    double *Ys = smem + G::RING;          // [2][KR_Y][NC]
+    double *cx = Ys + G::YT;              // [W][KR_X]: Fx rows of x0 + lane (lane fastest)
+    double *cy = cx + G::XB;              // [KR_Y][W]: Fy rows of y0 + row
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int n0 = g.n0, n1 = g.n1, n2 = g.n2;
-    for (int e = tid; e < K3_X * W; e += 256) {
-        const int xr = e / W, c = e % W, X = x0 + xr;
-        cx[xr][c] = X < n0 ? __ldg(fx + (long)X * W + c) : 0.0;
+    const long sy = g.sy, sz = g.sz;
+    const int x0 = blockIdx.x * KR_X, y0 = blockIdx.y * KR_Y;
+    const int z0 = blockIdx.z * zlen, z1 = min(n2, z0 + zlen);
+    for (int e = tid; e < W * KR_X; e += KR_THREADS) {
+        const int xr = e % KR_X, c = e / KR_X, X = x0 + xr;
+        cx[e] = X < n0 ? __ldg(fx + (long)X * W + c) : 0.0;
     }
-    for (int e = tid; e < K3_Y * W; e += 256) {
+    for (int e = tid; e < KR_Y * W; e += KR_THREADS) {
         const int yr = e / W, c = e % W, Y = y0 + yr;
-        cy[yr][c] = Y < n1 ? __ldg(fy + (long)Y * W + c) : 0.0;
+        cy[e] = Y < n1 ? __ldg(fy + (long)Y * W + c) : 0.0;
     }
-    long off[NSLOT];
-    bool val[NSLOT];
+    // copies: 16-byte pieces e = tid + 256 m of the [HY][HX/2] plane
+    int goff[G::NSLOT];
+    unsigned inr = 0;
 #pragma unroll
-    for (int m = 0; m < NSLOT; ++m) {
-        const int e = tid + 256 * m, hy = e / HX, hx = e % HX, X = x0 - P + hx, Y = y0 - P + hy;
-        val[m] = e < HX * HY && X >= 0 && X < n0 && Y >= 0 && Y < n1;
-        off[m] = (long)Y * g.sy + X;
+    for (int m = 0; m < G::NSLOT; ++m) {
+        const int e = tid + m * KR_THREADS, hy = e / (HX / 2), hx = 2 * (e - hy * (HX / 2));
+        const int X = x0 - PA + hx, Y = y0 - P + hy;
+        const bool ok = e < G::NPAIR && X >= 0 && X < n0 && Y >= 0 && Y < n1;
+        goff[m] = ok ? (Y * (int)sy + X) : 0;
+        if (ok) inr |= 1u << m;
     }
-    double pre[NSLOT];
-    auto load = [&](int kk) {
+    const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;  // input planes z0 - p .. z1 + p - 1
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * tid;
+    auto issue = [&](int ii) {
+        if (ii < npl) {
+            const int kk = kk0 + ii;
+            const bool kv = kk >= 0 && kk < n2;
+            const double *pin = in + (kv ? (long)kk * sz : 0);
+            const unsigned su = ring_s + 8u * (unsigned)((ii & (KR_NPF - 1)) * HN);
 #pragma unroll
-        for (int m = 0; m < NSLOT; ++m) pre[m] = (kk >= 0 && kk < n2 && val[m]) ? __ldg(in + (long)kk * g.sz + off[m]) : 0.0;
+            for (int m = 0; m < G::NSLOT; ++m) {
+                if (tid + m * KR_THREADS >= G::NPAIR) break;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(su + 16u * m * KR_THREADS),
+                             "l"(pin + goff[m]), "r"((kv && (inr >> m & 1)) ? 16u : 0u)
+                             : "memory");
+            }
+        }
+        cp_async_commit();
     };
-    const int X = x0 + tx, Y = y0 + ty;
-    const bool own = X < n0 && Y < n1;
-    double ring[W];
+    const bool yitem = tid < G::NITEM;
+    const int nc = tid % NC, grp = tid / NC, hcol = PA - P + nc;
+    const int X = x0 + lane, Yo = y0 + 2 * w;
+    const bool own0 = X < n0 && Yo < n1, own1 = X < n0 && Yo + 1 < n1;
+    double r0[W], r1[W];  // X planes kk - 2p .. kk of rows 2w, 2w + 1 (r[W-1] newest)
 #pragma unroll
-    for (int c = 0; c < W; ++c) ring[c] = 0.0;
-    const int z0 = blockIdx.z * zlen, z1 = min(n2, z0 + zlen);  // output planes of this CTA
-    load(z0 - 2 * P);
-    for (int kk = z0 - 2 * P; kk < z1 + P; ++kk) {
-        __syncthreads();  // previous plane's sy_ reads done
+    for (int c = 0; c < W; ++c) r0[c] = r1[c] = 0.0;
+    // the epilogue's operands of output plane k (Fz row, old out when beta != 0) are loaded one
+    // plane ahead: a synchronous read-modify-write would stall every plane on DRAM latency
+    double fzr[W], ob0 = 0.0, ob1 = 0.0;
+    const long oxy = (long)Yo * sy + X;
+    auto prefetch = [&](int k) {
+        if (k >= z0 && k < z1) {
 #pragma unroll
-        for (int m = 0; m < NSLOT; ++m) {
-            const int e = tid + 256 * m;
-            if (e < HX * HY) sp[e / HX][e % HX] = pre[m];
+            for (int c = 0; c < W; ++c) fzr[c] = __ldg(fz + (long)k * W + c);
+            if (beta != 0.0) {
+                ob0 = own0 ? out[(long)k * sz + oxy] : 0.0;
+                ob1 = own1 ? out[(long)k * sz + oxy + sy] : 0.0;
+            }
         }
-        __syncthreads();
-        if (kk + 1 < z1 + P) load(kk + 1);
-        for (int e = tid; e < K3_Y * HX; e += 256) {
-            const int yr = e / HX, col = e % HX;
-            double acc = 0.0;
+    };
+    prefetch(z0);
 #pragma unroll
-            for (int c = 0; c < W; ++c) acc = fma(cy[yr][c], sp[yr + c][col], acc);
-            sy_[yr][col] = acc;
+    for (int i = 0; i < KR_NPF - 1; ++i) issue(i);
+    __syncthreads();  // band rows staged
+    for (int ii = 0; ii <= npl; ++ii) {
+        if (ii < npl) cp_async_wait<KR_NPF - 2>();
+        __syncthreads();  // plane ii landed; Y tile (ii - 1) & 1 complete; ring slot (ii - 1) free
+        issue(ii + KR_NPF - 1);
+        if (yitem && ii < npl) {  // y-pass of input plane kk0 + ii
+            const double *b = ring + (ii & (KR_NPF - 1)) * HN + KR_RY * grp * HX + hcol;
+            double pr[KR_RY + 2 * P];
+#pragma unroll
+            for (int r = 0; r < KR_RY + 2 * P; ++r) pr[r] = b[r * HX];
+            double *yb = Ys + (ii & 1) * KR_Y * NC + KR_RY * grp * NC + nc;
+#pragma unroll
+            for (int r = 0; r < KR_RY; ++r) {
+                const double *c = cy + (KR_RY * grp + r) * W;
+                double acc = 0.0;
+#pragma unroll
+                for (int q = 0; q < W; ++q) acc = fma(c[q], pr[r + q], acc);
+                yb[r * NC] = acc;
+            }
         }
-        __syncthreads();
-        double xv = 0.0;
+        if (ii == 0) continue;
+        // x-pass of input plane kx = kk0 + ii - 1, then the z gather for output kx - p
+        const int kx = kk0 + ii - 1;
+        const double *yr0 = Ys + ((ii - 1) & 1) * KR_Y * NC + (2 * w) * NC + lane, *yr1 = yr0 + NC;
+        double x0v = 0.0, x1v = 0.0;
 #pragma unroll
-        for (int c = 0; c < W; ++c) xv = fma(cx[tx][c], sy_[ty][tx + c], xv);
+        for (int c = 0; c < W; ++c) {
+            const double f = cx[c * KR_X + lane];
+            x0v = fma(f, yr0[c], x0v);
+            x1v = fma(f, yr1[c], x1v);
+        }
 #pragma unroll
-        for (int c = 0; c < W - 1; ++c) ring[c] = ring[c + 1];
-        ring[W - 1] = xv;  // plane kk; ring[c] holds plane kk - 2P + c
-        const int k = kk - P;
-        if (k >= z0 && own) {
-            double acc = 0.0;
+        for (int c = 0; c < W - 1; ++c) {
+            r0[c] = r0[c + 1];
+            r1[c] = r1[c + 1];
+        }
+        r0[W - 1] = x0v;
+        r1[W - 1] = x1v;
+        const int k = kx - P;  // ring holds planes k - p .. k + p
+        if (k >= z0 && k < z1) {
+            double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-            for (int c = 0; c < W; ++c) acc = fma(__ldg(fz + (long)k * W + c), ring[c], acc);
-            const long idx = (long)k * g.sz + (long)Y * g.sy + X;
-            out[idx] = beta == 0.0 ? alpha * acc : fma(alpha, acc, beta * out[idx]);
+            for (int c = 0; c < W; ++c) {
+                a0 = fma(fzr[c], r0[c], a0);
+                a1 = fma(fzr[c], r1[c], a1);
+            }
+            double *o = out + (long)k * sz + oxy;
+            const double w0 = beta == 0.0 ? alpha * a0 : fma(alpha, a0, beta * ob0);
+            const double w1 = beta == 0.0 ? alpha * a1 : fma(alpha, a1, beta * ob1);
+            prefetch(k + 1);
+            if (own0) o[0] = w0;
+            if (own1) o[sy] = w1;
         }
     }
 }
 
+template <int P>
+static void kron3_launch(const double *in, double *out, const double *fx, const double *fy, const double *fz,
+                         double alpha, double beta, const Geom &g, cudaStream_t s) {
+    using G = KronGeo<P>;
+    const size_t sm = sizeof(double) * G::SMEM;
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaFuncSetAttribute(kron3_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kron3_kernel<P>, KR_THREADS, sm);
+        per_sm = std::max(per_sm, 1);
+    }
+    const int gx = (g.n0 + KR_X - 1) / KR_X, gy = (g.n1 + KR_Y - 1) / KR_Y;
+        // z pieces by the fluid wave model of kop_launch (each piece reads 2p halo planes)
+    const long resident = (long)per_sm * 148, tiles = (long)gx * gy;
+    int best = 1;
+    double best_cost = 1e300;
+    for (int nz = 1; nz <= 64; ++nz) {
+        const int zl = (g.n2 + nz - 1) / nz;
+        if (zl < 2 * P + 1 && nz > 1) break;
+        const long ctas = tiles * ((g.n2 + zl - 1) / zl);
+        const double cost = ((double)ctas / resident + 0.5) * (zl + 2.0 * P);
+        if (cost < best_cost * 0.999) { best_cost = cost; best = nz; }
+    }
+    const int zlen = (g.n2 + best - 1) / best;
+    dim3 grd(gx, gy, (g.n2 + zlen - 1) / zlen);
+    kron3_kernel<P><<<grd, KR_THREADS, sm, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen);
+}
+
 int launch_kron3(int p, const double *in, double *out, const double *fx, const double *fy, const double *fz,
                  double alpha, double beta, const Geom &g, cudaStream_t s) {
-    // z pieces: about 8 CTAs per SM in total, each piece re-reads 2p halo planes
-    const int gx = (g.n0 + K3_X - 1) / K3_X, gy = (g.n1 + K3_Y - 1) / K3_Y;
-    const int want = std::max(1, (148 * 8 + gx * gy - 1) / (gx * gy));
-    const int zlen = std::max(4 * p, (g.n2 + want - 1) / want);
-    dim3 blk(K3_X, K3_Y), grd(gx, gy, (g.n2 + zlen - 1) / zlen);
     switch (p) {
-        case 1: kron3_kernel<1><<<grd, blk, 0, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen); break;
-        case 2: kron3_kernel<2><<<grd, blk, 0, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen); break;
-        case 3: kron3_kernel<3><<<grd, blk, 0, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen); break;
-        case 4: kron3_kernel<4><<<grd, blk, 0, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen); break;
-        case 5: kron3_kernel<5><<<grd, blk, 0, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen); break;
+        case 1: kron3_launch<1>(in, out, fx, fy, fz, alpha, beta, g, s); break;
+        case 2: kron3_launch<2>(in, out, fx, fy, fz, alpha, beta, g, s); break;
+        case 3: kron3_launch<3>(in, out, fx, fy, fz, alpha, beta, g, s); break;
+        case 4: kron3_launch<4>(in, out, fx, fy, fz, alpha, beta, g, s); break;
+        case 5: kron3_launch<5>(in, out, fx, fy, fz, alpha, beta, g, s); break;
         default: return -1;
     }
     return 0;
