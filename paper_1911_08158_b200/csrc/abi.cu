@@ -586,19 +586,26 @@ double *comp(double *f, const ads_ctx *h, int c) { return f + (long)c * h->Nallo
 // out = alpha (Fx (x) Fy (x) Fz) in + beta out   (Fd: band [n_d][2p+1], acting along d)
 int tri(ads_ctx *h, double *out, const double *in, const double *fx, const double *fy, const double *fz,
         double alpha, double beta) {
-    if (launch_kron3(h->p, in, out, fx, fy, fz, alpha, beta, h->geo, h->stream))
-        return fail(h, ADS_E_INVAL, "kron3: unsupported p");
+    KronTerms k3;
+    k3.fx[0] = fx, k3.fy[0] = fy, k3.fz[0] = fz, k3.alpha[0] = alpha;
+    if (launch_kron3(h->p, in, out, k3, beta, h->geo, h->stream)) return fail(h, ADS_E_INVAL, "kron3: unsupported p");
     return check_launch(h, "kron3");
 }
 
-// out += coef Ups_ik in   (i != k)
+// out += coef Ups_ik in   (i != k): mu [B]_k [B^T]_i + lam [B]_i [B^T]_k, M in the third
+// direction -- both triples act on the same input and output: one fused pass
 int ups_offdiag(ads_ctx *h, int i, int k, const double *in, double *out, double coef) {
-    const double *F[3];
-    int rc;
-    for (int e = 0; e < 3; ++e) F[e] = e == k ? h->dd[e].bband : e == i ? h->dd[e].btband : h->dd[e].mband;
-    if ((rc = tri(h, out, in, F[0], F[1], F[2], coef * h->mu, 1.0))) return rc;
-    for (int e = 0; e < 3; ++e) F[e] = e == i ? h->dd[e].bband : e == k ? h->dd[e].btband : h->dd[e].mband;
-    return tri(h, out, in, F[0], F[1], F[2], coef * h->lam, 1.0);
+    KronTerms k3;
+    k3.nterms = 2;
+    const double **F[3] = {k3.fx, k3.fy, k3.fz};
+    for (int e = 0; e < 3; ++e) {
+        F[e][0] = e == k ? h->dd[e].bband : e == i ? h->dd[e].btband : h->dd[e].mband;
+        F[e][1] = e == i ? h->dd[e].bband : e == k ? h->dd[e].btband : h->dd[e].mband;
+    }
+    k3.alpha[0] = coef * h->mu;
+    k3.alpha[1] = coef * h->lam;
+    if (launch_kron3(h->p, in, out, k3, 1.0, h->geo, h->stream)) return fail(h, ADS_E_INVAL, "kron3: unsupported p");
+    return check_launch(h, "kron3");
 }
 
 // out_i (+)= coef (Ups in)_i for all i.  The diagonal blocks go through the fused operator

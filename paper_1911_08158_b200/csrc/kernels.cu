@@ -891,8 +891,9 @@ int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {
     return 0;
 }
 
-// One Kronecker triple out = alpha (Fx (x) Fy (x) Fz) in + beta out (elasticity couplings,
-// PAPER.md:355-387; general bands, no Toeplitz assumption).  Same structure as kop_kernel:
+// Kronecker triples out = beta out + sum_t alpha_t (Fx_t (x) Fy_t (x) Fz_t) in, t < T <= 2, sharing
+// input and output (elasticity couplings: the two triples of an off-diagonal
+// block Upsilon_ik go in one pass; general bands, no Toeplitz assumption).  Same structure as kop_kernel:
 // 32 x 16 output tile marching z over a piece [z0, z1); per input plane (one barrier):
 //   - all threads stream the haloed plane HBM -> shared memory in 16-byte zero-filling cp.async
 //     pieces, KR_NPF - 1 planes ahead;
@@ -902,7 +903,7 @@ int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {
 //   - z: a register ring of the last 2p + 1 X planes; output plane kk - 2p ... gathered with Fz.
 // HBM traffic: in read once (halos from L2), out written once (read once when beta != 0).
 constexpr int KR_X = 32, KR_Y = 16, KR_THREADS = 256, KR_NPF = 4, KR_RY = 4;
-template <int P>
+template <int P, int T>
 struct KronGeo {
     static constexpr int W = 2 * P + 1;
     static constexpr int PA = (P + 1) & ~1;  // even x halo of the copied tile (16-byte pieces)
@@ -910,36 +911,38 @@ struct KronGeo {
     static constexpr int NC = KR_X + 2 * P;  // columns the x-pass needs
     static constexpr int NITEM = NC * (KR_Y / KR_RY);
     static constexpr int NPAIR = HN / 2, NSLOT = (NPAIR + KR_THREADS - 1) / KR_THREADS;
-    static constexpr int RING = KR_NPF * HN, YT = 2 * KR_Y * NC, XB = W * KR_X, YB = KR_Y * W;
+    // shared memory (doubles): ring [NPF][HY][HX] | Y tiles [2][KR_Y][NC][T] | Fx [T][W][KR_X] | Fy [T][KR_Y][W]
+    static constexpr int RING = KR_NPF * HN, YT = 2 * KR_Y * NC * T, XB = T * W * KR_X, YB = T * KR_Y * W;
     static constexpr int SMEM = RING + YT + XB + YB;
     static_assert(NITEM <= KR_THREADS, "one y-pass item per thread");
 };
 
-template <int P>
+// T terms sharing the input and the output: out = beta out + sum_t alpha_t (Fx_t (x) Fy_t (x) Fz_t) in
+template <int P, int T>
 __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__restrict__ in, double *__restrict__ out,
-                                                               const double *__restrict__ fx,
-                                                               const double *__restrict__ fy,
-                                                               const double *__restrict__ fz, double alpha, double beta,
-                                                               Geom g, int zlen) {
-    using G = KronGeo<P>;
+                                                               const KronTerms k3, double beta, Geom g, int zlen) {
+    using G = KronGeo<P, T>;
     constexpr int W = G::W, HX = G::HX, HN = G::HN, NC = G::NC, PA = G::PA;
     extern __shared__ __align__(16) double smem[];
     double *ring = smem;
-    double *Ys = smem + G::RING;          // [2][KR_Y][NC]
-    double *cx = Ys + G::YT;              // [W][KR_X]: Fx rows of x0 + lane (lane fastest)
-    double *cy = cx + G::XB;              // [KR_Y][W]: Fy rows of y0 + row
+    double *Ys = smem + G::RING;  // [2][KR_Y][NC][T]
+    double *cx = Ys + G::YT;      // [T][W][KR_X]: Fx_t rows of x0 + lane (lane fastest)
+    double *cy = cx + G::XB;      // [T][KR_Y][W]: Fy_t rows of y0 + row
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int n0 = g.n0, n1 = g.n1, n2 = g.n2;
     const long sy = g.sy, sz = g.sz;
     const int x0 = blockIdx.x * KR_X, y0 = blockIdx.y * KR_Y;
     const int z0 = blockIdx.z * zlen, z1 = min(n2, z0 + zlen);
-    for (int e = tid; e < W * KR_X; e += KR_THREADS) {
-        const int xr = e % KR_X, c = e / KR_X, X = x0 + xr;
-        cx[e] = X < n0 ? __ldg(fx + (long)X * W + c) : 0.0;
-    }
-    for (int e = tid; e < KR_Y * W; e += KR_THREADS) {
-        const int yr = e / W, c = e % W, Y = y0 + yr;
-        cy[e] = Y < n1 ? __ldg(fy + (long)Y * W + c) : 0.0;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        for (int e = tid; e < W * KR_X; e += KR_THREADS) {
+            const int xr = e % KR_X, c = e / KR_X, X = x0 + xr;
+            cx[t * W * KR_X + e] = X < n0 ? __ldg(k3.fx[t] + (long)X * W + c) : 0.0;
+        }
+        for (int e = tid; e < KR_Y * W; e += KR_THREADS) {
+            const int yr = e / W, c = e % W, Y = y0 + yr;
+            cy[t * KR_Y * W + e] = Y < n1 ? __ldg(k3.fy[t] + (long)Y * W + c) : 0.0;
+        }
     }
     // copies: 16-byte pieces e = tid + 256 m of the [HY][HX/2] plane
     int goff[G::NSLOT];
@@ -974,17 +977,21 @@ __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__re
     const int nc = tid % NC, grp = tid / NC, hcol = PA - P + nc;
     const int X = x0 + lane, Yo = y0 + 2 * w;
     const bool own0 = X < n0 && Yo < n1, own1 = X < n0 && Yo + 1 < n1;
-    double r0[W], r1[W];  // X planes kk - 2p .. kk of rows 2w, 2w + 1 (r[W-1] newest)
+    double r0[T][W], r1[T][W];  // X_t planes kk - 2p .. kk of rows 2w, 2w + 1 (r[.][W-1] newest)
 #pragma unroll
-    for (int c = 0; c < W; ++c) r0[c] = r1[c] = 0.0;
-    // the epilogue's operands of output plane k (Fz row, old out when beta != 0) are loaded one
-    // plane ahead: a synchronous read-modify-write would stall every plane on DRAM latency
-    double fzr[W], ob0 = 0.0, ob1 = 0.0;
+    for (int t = 0; t < T; ++t)
+#pragma unroll
+        for (int c = 0; c < W; ++c) r0[t][c] = r1[t][c] = 0.0;
+    // the epilogue's operands of output plane k (alpha_t Fz_t rows, old out when beta != 0) are
+    // loaded one plane ahead: a synchronous read-modify-write would stall every plane on DRAM
+    double fzr[T][W], ob0 = 0.0, ob1 = 0.0;
     const long oxy = (long)Yo * sy + X;
     auto prefetch = [&](int k) {
         if (k >= z0 && k < z1) {
 #pragma unroll
-            for (int c = 0; c < W; ++c) fzr[c] = __ldg(fz + (long)k * W + c);
+            for (int t = 0; t < T; ++t)
+#pragma unroll
+                for (int c = 0; c < W; ++c) fzr[t][c] = k3.alpha[t] * __ldg(k3.fz[t] + (long)k * W + c);
             if (beta != 0.0) {
                 ob0 = own0 ? out[(long)k * sz + oxy] : 0.0;
                 ob1 = own1 ? out[(long)k * sz + oxy + sy] : 0.0;
@@ -999,50 +1006,72 @@ __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__re
         if (ii < npl) cp_async_wait<KR_NPF - 2>();
         __syncthreads();  // plane ii landed; Y tile (ii - 1) & 1 complete; ring slot (ii - 1) free
         issue(ii + KR_NPF - 1);
-        if (yitem && ii < npl) {  // y-pass of input plane kk0 + ii
+        if (yitem && ii < npl) {  // y-pass of input plane kk0 + ii, every term from one window
             const double *b = ring + (ii & (KR_NPF - 1)) * HN + KR_RY * grp * HX + hcol;
             double pr[KR_RY + 2 * P];
 #pragma unroll
             for (int r = 0; r < KR_RY + 2 * P; ++r) pr[r] = b[r * HX];
-            double *yb = Ys + (ii & 1) * KR_Y * NC + KR_RY * grp * NC + nc;
+            double *yb = Ys + ((ii & 1) * KR_Y * NC + KR_RY * grp * NC + nc) * T;
 #pragma unroll
             for (int r = 0; r < KR_RY; ++r) {
-                const double *c = cy + (KR_RY * grp + r) * W;
-                double acc = 0.0;
+                double acc[T];
 #pragma unroll
-                for (int q = 0; q < W; ++q) acc = fma(c[q], pr[r + q], acc);
-                yb[r * NC] = acc;
+                for (int t = 0; t < T; ++t) {
+                    const double *c = cy + t * KR_Y * W + (KR_RY * grp + r) * W;
+                    acc[t] = 0.0;
+#pragma unroll
+                    for (int q = 0; q < W; ++q) acc[t] = fma(c[q], pr[r + q], acc[t]);
+                }
+                if constexpr (T == 2) reinterpret_cast<double2 *>(yb)[r * NC] = make_double2(acc[0], acc[1]);
+                else yb[r * NC] = acc[0];
             }
         }
         if (ii == 0) continue;
         // x-pass of input plane kx = kk0 + ii - 1, then the z gather for output kx - p
         const int kx = kk0 + ii - 1;
-        const double *yr0 = Ys + ((ii - 1) & 1) * KR_Y * NC + (2 * w) * NC + lane, *yr1 = yr0 + NC;
-        double x0v = 0.0, x1v = 0.0;
+        const double *yr0 = Ys + (((ii - 1) & 1) * KR_Y * NC + (2 * w) * NC + lane) * T, *yr1 = yr0 + NC * T;
+        double x0v[T], x1v[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) x0v[t] = x1v[t] = 0.0;
 #pragma unroll
         for (int c = 0; c < W; ++c) {
-            const double f = cx[c * KR_X + lane];
-            x0v = fma(f, yr0[c], x0v);
-            x1v = fma(f, yr1[c], x1v);
+            if constexpr (T == 2) {
+                const double2 q0 = reinterpret_cast<const double2 *>(yr0)[c];
+                const double2 q1 = reinterpret_cast<const double2 *>(yr1)[c];
+                const double f0 = cx[c * KR_X + lane], f1 = cx[W * KR_X + c * KR_X + lane];
+                x0v[0] = fma(f0, q0.x, x0v[0]);
+                x1v[0] = fma(f0, q1.x, x1v[0]);
+                x0v[T - 1] = fma(f1, q0.y, x0v[T - 1]);
+                x1v[T - 1] = fma(f1, q1.y, x1v[T - 1]);
+            } else {
+                const double f = cx[c * KR_X + lane];
+                x0v[0] = fma(f, yr0[c], x0v[0]);
+                x1v[0] = fma(f, yr1[c], x1v[0]);
+            }
         }
 #pragma unroll
-        for (int c = 0; c < W - 1; ++c) {
-            r0[c] = r0[c + 1];
-            r1[c] = r1[c + 1];
+        for (int t = 0; t < T; ++t) {
+#pragma unroll
+            for (int c = 0; c < W - 1; ++c) {
+                r0[t][c] = r0[t][c + 1];
+                r1[t][c] = r1[t][c + 1];
+            }
+            r0[t][W - 1] = x0v[t];
+            r1[t][W - 1] = x1v[t];
         }
-        r0[W - 1] = x0v;
-        r1[W - 1] = x1v;
-        const int k = kx - P;  // ring holds planes k - p .. k + p
+        const int k = kx - P;  // rings hold planes k - p .. k + p
         if (k >= z0 && k < z1) {
             double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-            for (int c = 0; c < W; ++c) {
-                a0 = fma(fzr[c], r0[c], a0);
-                a1 = fma(fzr[c], r1[c], a1);
-            }
+            for (int t = 0; t < T; ++t)
+#pragma unroll
+                for (int c = 0; c < W; ++c) {
+                    a0 = fma(fzr[t][c], r0[t][c], a0);
+                    a1 = fma(fzr[t][c], r1[t][c], a1);
+                }
             double *o = out + (long)k * sz + oxy;
-            const double w0 = beta == 0.0 ? alpha * a0 : fma(alpha, a0, beta * ob0);
-            const double w1 = beta == 0.0 ? alpha * a1 : fma(alpha, a1, beta * ob1);
+            const double w0 = beta == 0.0 ? a0 : fma(beta, ob0, a0);
+            const double w1 = beta == 0.0 ? a1 : fma(beta, ob1, a1);
             prefetch(k + 1);
             if (own0) o[0] = w0;
             if (own1) o[sy] = w1;
@@ -1050,19 +1079,19 @@ __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__re
     }
 }
 
-template <int P>
-static void kron3_launch(const double *in, double *out, const double *fx, const double *fy, const double *fz,
-                         double alpha, double beta, const Geom &g, cudaStream_t s) {
-    using G = KronGeo<P>;
+template <int P, int T>
+static void kron3_launch(const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
+                         cudaStream_t s) {
+    using G = KronGeo<P, T>;
     const size_t sm = sizeof(double) * G::SMEM;
     static int per_sm = 0;
     if (!per_sm) {
-        cudaFuncSetAttribute(kron3_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kron3_kernel<P>, KR_THREADS, sm);
+        cudaFuncSetAttribute(kron3_kernel<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kron3_kernel<P, T>, KR_THREADS, sm);
         per_sm = std::max(per_sm, 1);
     }
     const int gx = (g.n0 + KR_X - 1) / KR_X, gy = (g.n1 + KR_Y - 1) / KR_Y;
-        // z pieces by the fluid wave model of kop_launch (each piece reads 2p halo planes)
+    // z pieces by the fluid wave model of kop_launch (each piece reads 2p halo planes)
     const long resident = (long)per_sm * 148, tiles = (long)gx * gy;
     int best = 1;
     double best_cost = 1e300;
@@ -1075,20 +1104,39 @@ static void kron3_launch(const double *in, double *out, const double *fx, const 
     }
     const int zlen = (g.n2 + best - 1) / best;
     dim3 grd(gx, gy, (g.n2 + zlen - 1) / zlen);
-    kron3_kernel<P><<<grd, KR_THREADS, sm, s>>>(in, out, fx, fy, fz, alpha, beta, g, zlen);
+    kron3_kernel<P, T><<<grd, KR_THREADS, sm, s>>>(in, out, k3, beta, g, zlen);
 }
 
-int launch_kron3(int p, const double *in, double *out, const double *fx, const double *fy, const double *fz,
-                 double alpha, double beta, const Geom &g, cudaStream_t s) {
-    switch (p) {
-        case 1: kron3_launch<1>(in, out, fx, fy, fz, alpha, beta, g, s); break;
-        case 2: kron3_launch<2>(in, out, fx, fy, fz, alpha, beta, g, s); break;
-        case 3: kron3_launch<3>(in, out, fx, fy, fz, alpha, beta, g, s); break;
-        case 4: kron3_launch<4>(in, out, fx, fy, fz, alpha, beta, g, s); break;
-        case 5: kron3_launch<5>(in, out, fx, fy, fz, alpha, beta, g, s); break;
-        default: return -1;
+template <int P>
+static int kron3_dispatch(const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
+                          cudaStream_t s) {
+    if (k3.nterms == 1) {
+        kron3_launch<P, 1>(in, out, k3, beta, g, s);
+        return 0;
+    }
+    if constexpr (P <= 3) {  // two terms in one pass (registers: two gather rings)
+        kron3_launch<P, 2>(in, out, k3, beta, g, s);
+    } else {  // two passes, the second accumulating
+        KronTerms a = k3, b = k3;
+        a.nterms = b.nterms = 1;
+        b.fx[0] = k3.fx[1], b.fy[0] = k3.fy[1], b.fz[0] = k3.fz[1], b.alpha[0] = k3.alpha[1];
+        kron3_launch<P, 1>(in, out, a, beta, g, s);
+        kron3_launch<P, 1>(in, out, b, 1.0, g, s);
     }
     return 0;
+}
+
+int launch_kron3(int p, const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
+                 cudaStream_t s) {
+    if (k3.nterms < 1 || k3.nterms > 2) return -1;
+    switch (p) {
+        case 1: return kron3_dispatch<1>(in, out, k3, beta, g, s);
+        case 2: return kron3_dispatch<2>(in, out, k3, beta, g, s);
+        case 3: return kron3_dispatch<3>(in, out, k3, beta, g, s);
+        case 4: return kron3_dispatch<4>(in, out, k3, beta, g, s);
+        case 5: return kron3_dispatch<5>(in, out, k3, beta, g, s);
+        default: return -1;
+    }
 }
 
 // ------------------------------------------------------------------------------------------

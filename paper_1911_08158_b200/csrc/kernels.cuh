@@ -122,8 +122,15 @@ int launch_sweep(int p, const SweepArgs &a, cudaStream_t s);
 int launch_axis_apply(int p, int d, const double *band, const double *in, double *out, const Geom &g, double alpha,
                       double beta, cudaStream_t s, int zoff = 0, int zv0 = 0, int zv1 = -1);
 // out = alpha (Fx (x) Fy (x) Fz) in + beta out in one z-marching pass (beta == 0: out not read)
-int launch_kron3(int p, const double *in, double *out, const double *fx, const double *fy, const double *fz,
-                 double alpha, double beta, const Geom &g, cudaStream_t s);
+// Kronecker triples sharing input and output (elasticity):
+//   out = beta out + sum_{t < nterms} alpha_t (Fx_t (x) Fy_t (x) Fz_t) in,  bands [n_d][2p+1]
+struct KronTerms {
+    int nterms = 1;
+    const double *fx[2] = {nullptr, nullptr}, *fy[2] = {nullptr, nullptr}, *fz[2] = {nullptr, nullptr};
+    double alpha[2] = {0.0, 0.0};
+};
+int launch_kron3(int p, const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
+                 cudaStream_t s);
 // y = alpha x + beta y over N elements
 int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s);
 // zero the boundary faces of a field (Dirichlet masking)
