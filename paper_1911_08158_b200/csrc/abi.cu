@@ -401,7 +401,7 @@ int guard(ads_ctx *h) {
 
 // ---- step pieces ----
 int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g, double sign, double *Pout,
-            double *r, bool devsrc = false) {
+            double *r, bool devsrc = false, const double *kw = nullptr) {
     KopArgs a;
     a.U = U;
     a.V = V;
@@ -440,9 +440,10 @@ int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g
     for (int d = 0; d < 3; ++d) {
         a.ilo[d] = h->dd[d].t_lo;
         a.ihi[d] = h->dd[d].t_hi;
+        a.kw[d] = kw ? kw[d] : 1.0;
         for (int c = 0; c < 2 * h->p + 1; ++c) {
             a.mc[d][c] = h->dd[d].mrow[c];
-            a.kc[d][c] = h->dd[d].krow[c];
+            a.kc[d][c] = a.kw[d] * h->dd[d].krow[c];
         }
     }
     ProfScope ps(h, 0);
@@ -612,17 +613,17 @@ int ups_offdiag(ads_ctx *h, int i, int k, const double *in, double *out, double 
 // kernel: out_i = coef mu K (in_i + tau_d v_i) with the drift written to pout_i if non-null.
 int ups_apply(ads_ctx *h, const double *in, const double *v, double tau_d, double *pout, double *out, double coef) {
     int rc;
-    for (int i = 0; i < 3; ++i)
+    // diagonal blocks Ups_ii = mu K + (mu + lam) K_(i): the operator kernel with direction i's K
+    // term weighted (2 mu + lam) / mu
+    for (int i = 0; i < 3; ++i) {
+        double kw[3] = {1.0, 1.0, 1.0};
+        kw[i] = (2.0 * h->mu + h->lam) / h->mu;
         if ((rc = run_kop(h, comp((double *)in, h, i), comp((double *)v, h, i), tau_d, 0.0, coef * h->mu,
-                          pout ? comp(pout, h, i) : nullptr, comp(out, h, i))))
+                          pout ? comp(pout, h, i) : nullptr, comp(out, h, i), false, kw)))
             return rc;
+    }
     const double *P = pout ? pout : in;  // the drifted field the blocks act on
     for (int i = 0; i < 3; ++i) {
-        const double *F[3];
-        for (int e = 0; e < 3; ++e) F[e] = e == i ? h->dd[e].kband : h->dd[e].mband;
-        if ((rc = tri(h, comp(out, h, i), comp((double *)P, h, i), F[0], F[1], F[2], coef * (h->mu + h->lam),
-                      1.0)))
-            return rc;
         for (int k = 0; k < 3; ++k)
             if (k != i && (rc = ups_offdiag(h, i, k, comp((double *)P, h, k), comp(out, h, i), coef))) return rc;
     }

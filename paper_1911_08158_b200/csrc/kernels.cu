@@ -531,7 +531,7 @@ __device__ __forceinline__ void kop_zscatter(const KopArgs &a, double (&A0)[2 * 
             double mz_ = 0.0, kz_ = 0.0;
             if (k >= 0 && k < n2) {  // output planes; band rows are global rows k + zoff
                 mz_ = __ldg(a.mz + (long)(k + a.zoff) * W + 2 * P - c);
-                kz_ = __ldg(a.kz + (long)(k + a.zoff) * W + 2 * P - c);
+                kz_ = a.kw[2] * __ldg(a.kz + (long)(k + a.zoff) * W + 2 * P - c);
             }
             A0[sl] = fma(mz_, s0, A0[sl]);
             A0[sl] = fma(kz_, t0, A0[sl]);
@@ -568,12 +568,12 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
     if (!XI)  // stage boundary band rows (zero outside the domain)
         for (int e = tid; e < KT_X * 2 * W; e += KT_THREADS) {
             const int xr = e % KT_X, m = (e / KT_X) & 1, c = e / (2 * KT_X), X = x0 + xr;
-            xb[e] = (X >= 0 && X < n0) ? __ldg((m ? a.kx : a.mx) + (long)X * W + c) : 0.0;
+            xb[e] = (X >= 0 && X < n0) ? (m ? a.kw[0] : 1.0) * __ldg((m ? a.kx : a.mx) + (long)X * W + c) : 0.0;
         }
     if (!YI) {
         for (int e = tid; e < KT_Y * 2 * W; e += KT_THREADS) {
             const int yr = e / (2 * W), m = (e / W) & 1, c = e % W, Y = y0 + yr;
-            yb[e] = (Y >= 0 && Y < n1) ? __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
+            yb[e] = (Y >= 0 && Y < n1) ? (m ? a.kw[1] : 1.0) * __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
         }
     }
 

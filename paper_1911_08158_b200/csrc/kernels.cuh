@@ -45,6 +45,10 @@ struct KopArgs {
     int zlen = 0;
     int ilo[3] = {1, 1, 1}, ihi[3] = {0, 0, 0};
     double mc[3][2 * kMaxP + 1] = {}, kc[3][2 * kMaxP + 1] = {};
+    // weight of each direction's K term: K = kw0 Kx My Mz + kw1 Mx Ky Mz + kw2 Mx My Kz (1 for the
+    // P-wave; elasticity's diagonal blocks mu K + (mu + lam) K_(i)).  The interior rows kc[d]
+    // arrive pre-scaled; boundary rows are scaled where they are staged.
+    double kw[3] = {1.0, 1.0, 1.0};
     // z-slabs: local plane k is global row k + zoff of Mz, Kz (and of bz); input planes
     // [zv0, zv1) exist in memory (halo planes of a slab); outputs are planes [0, n2)
     int zoff = 0, zv0 = 0, zv1 = -1;
