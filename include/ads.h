@@ -61,7 +61,8 @@ enum { ADS_WAVELET_NONE = 0, ADS_WAVELET_RICKER = 1 };
 
 /* Create a scalar P-wave solver.
  *   p in [1,5]; nx,ny,nz >= 1 (Dirichlet needs n_d >= 3); tau finite > 0;
- *   bc in {ADS_BC_NATURAL, ADS_BC_DIRICHLET0}; n_d <= 1024.
+ *   bc in {ADS_BC_NATURAL, ADS_BC_DIRICHLET0}; n_d = n_el,d + p <= 1056 (32 chunks of at most
+ *   33 rows per line; ADS_E_INVAL beyond).
  *   nz = 0: the 2D scheme as the paper prints it (Eqs. 14-16; SURVEY.md §8
  *   row f2): the third axis carries one function with M = 1, K = 0 and no boundary, so that
  *   K = Kx(x)My + Mx(x)Ky and D = Ax(x)Ay exactly; arrays are 1 x n_y x n_x, load/source
