@@ -441,3 +441,19 @@ def test_2d_modal_and_set_tau(ads):
     o.step(10)
     for x, y in zip(b.get_state(), o.get_state()):
         assert rel(x, y) < 1e-10
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c5"])
+def test_bitwise_deterministic(ads, cfg):
+    """The path has no atomics or order-dependent reductions: two runs of the same seeded
+    workload (graph replays, z-split launches, energies) agree bit for bit."""
+    wl = workloads.get(cfg).scaled(24, 12)
+    runs = []
+    for _ in range(2):
+        s = ads.make_solver(wl)
+        s.step(wl.steps)
+        runs.append((s.get_state(), s.energy()))
+    (st0, e0), (st1, e1) = runs
+    for a, b in zip(st0, st1):
+        assert np.array_equal(a, b)
+    assert np.array_equal(e0, e1)
