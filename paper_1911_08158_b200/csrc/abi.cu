@@ -464,6 +464,11 @@ int run_sweep_tab(ads_ctx *h, int d, const SolveTab &tab, const double *in, doub
     a.dir = d;
     a.mode = V ? 1 : 0;
     ProfScope ps(h, 1 + d);
+    if (tab.n == 1) {  // the 2D axis: a 1 x 1 system per line (P-wave A_z = M_z + eta K_z = 1)
+        const double a00 = h->sp[d].M.get(0, 0) + 0.25 * h->tau * h->tau * h->sp[d].K.get(0, 0);
+        launch_line1(in, out, V, 1.0 / a00, kick, inc, h->geo, h->stream);
+        return check_launch(h, "line1");
+    }
     const int lr = launch_sweep(h->p, a, h->stream);
     if (lr == -2) return fail(h, ADS_E_CUDA, "sweep: TMA descriptor encoding failed");
     if (lr) return fail(h, ADS_E_INVAL, "sweep: unsupported p/chunk");

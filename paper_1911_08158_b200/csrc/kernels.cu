@@ -593,10 +593,11 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
     const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;
     const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * (ct > 0 ? ct : 0);
     auto issue = [&](int ii) {
-        if (copier && ii < npl) {
+        // planes outside [zv0, zv1) are zero: nothing is copied (their y/x passes are skipped)
+        if (copier && ii < npl && kk0 + ii >= a.zv0 && kk0 + ii < a.zv1) {
             const int kk = kk0 + ii;
             const unsigned su = ring_s + 8u * (unsigned)((ii & (KT_NPF - 1)) * 2 * HN);
-            const bool kv = kk >= a.zv0 && kk < a.zv1;
+            const bool kv = true;
             const double *pu = a.U + (kv ? (long)kk * sz : 0), *pv = a.V + (kv ? (long)kk * sz : 0);
 #pragma unroll
             for (int m = 0; m < G::NSLOT; ++m) {
@@ -651,8 +652,8 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
         if (ii < npl) cp_async_wait<KT_NPF - 2>();
         __syncthreads();  // plane kk landed; Ys[(ii-1)&1] complete; ring slot (ii-1)%NPF free
         if (ii < npl) issue(ii + KT_NPF - 1);
-        // ---- y-pass of plane kk into Ys buffer ii & 1
-        if (yitem && ii < npl) {
+        // ---- y-pass of plane kk into Ys buffer ii & 1 (zero planes outside [zv0, zv1) skipped)
+        if (yitem && ii < npl && kk >= a.zv0 && kk < a.zv1) {
             double2 *Ysb = Ys + (ii & 1) * KT_Y * NC;
             const double *bu = ring + (ii & (KT_NPF - 1)) * 2 * HN, *bv = bu + HN;
             double pr[KT_RY + 2 * P];
@@ -698,7 +699,9 @@ __device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0,
         zslot = zslot == W - 1 ? 0 : zslot + 1;
         const double2 *Yr = Ys + ((ii - 1) & 1) * KT_Y * NC;
         double s0, t0, s1, t1;
-        if (XI) {
+        if (kx < a.zv0 || kx >= a.zv1) {  // a zero plane: it only advances the z ring
+            s0 = t0 = s1 = t1 = 0.0;
+        } else if (XI) {
             const double2 c0 = Yr[(2 * w) * NC + lane + P], c1 = Yr[(2 * w + 1) * NC + lane + P];
             s0 = fma(a.kc[0][P], c0.x, a.mc[0][P] * c0.y);
             t0 = a.mc[0][P] * c0.x;
@@ -1520,5 +1523,23 @@ __global__ void set_long_kernel(long *dst, long value) { *dst = value; }
 
 void launch_set_long(long *dst, long value, cudaStream_t s) { set_long_kernel<<<1, 1, 0, s>>>(dst, value); }
 
-}  // namespace ads
+__global__ void line1_kernel(const double *__restrict__ in, double *__restrict__ out, double *__restrict__ V,
+                             double scale, double kick, long *inc, Geom g) {
+    const long N = (long)g.n0 * g.n1 * g.n2;
+    if (inc && blockIdx.x == 0 && threadIdx.x == 0) *inc += 1;
+    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(q % g.n0);
+        const long t = q / g.n0;
+        const long o = (t / g.n1) * g.sz + (t % g.n1) * g.sy + i;
+        const double x = scale * in[o];
+        if (V) V[o] = fma(kick, x, V[o]);
+        if (out) out[o] = x;
+    }
+}
 
+void launch_line1(const double *in, double *out, double *V, double scale, double kick, long *inc, const Geom &g,
+                  cudaStream_t s) {
+    line1_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(in, out, V, scale, kick, inc, g);
+}
+
+}  // namespace ads
