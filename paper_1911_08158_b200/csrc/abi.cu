@@ -81,6 +81,7 @@ struct ads_ctx {
     std::vector<ads_ctx *> members;                  // dist = 2
     ads_ctx *prev = nullptr, *next = nullptr;        // dist = 3
     double *dpartial = nullptr, *dres = nullptr;
+    double *stage = nullptr;  // dense staging buffer of host copies (N doubles, first use)
     // CUDA graphs of two P-wave steps (one per U/U2 parity) replayed by ads_step; the source
     // time comes from a device step counter the z sweep increments
     long *dstep = nullptr;
@@ -967,18 +968,39 @@ int pwave_energy(ads_ctx *G, double res[3]) {
     return ADS_OK;
 }
 
+// Host arrays move as one contiguous copy through a dense device staging buffer and are
+// repacked on the device (pitched host<->device 2D copies ran at ~28 GB/s against ~56 GB/s
+// contiguous on this box, scripts/copy_probe.py); device arrays use a 2D device copy.
+int stage_buffer(ads_ctx *h) {
+    return h->stage ? ADS_OK : dalloc(h, (void **)&h->stage, sizeof(double) * (size_t)h->N);
+}
+
 int copy_in(ads_ctx *h, double *dst, const double *src, int mem) {
-    cudaMemcpyKind k = mem == ADS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    // dense caller array -> pitched device field
-    CUDA_TRY(h, cudaMemcpy2DAsync(dst, sizeof(double) * h->geo.sy, src, sizeof(double) * h->n[0],
-                                  sizeof(double) * h->n[0], (size_t)h->n[1] * h->n[2], k, h->stream));
-    return ADS_OK;
+    if (mem == ADS_MEM_DEVICE) {  // dense caller array -> pitched device field
+        CUDA_TRY(h, cudaMemcpy2DAsync(dst, sizeof(double) * h->geo.sy, src, sizeof(double) * h->n[0],
+                                      sizeof(double) * h->n[0], (size_t)h->n[1] * h->n[2], cudaMemcpyDeviceToDevice,
+                                      h->stream));
+        return ADS_OK;
+    }
+    int rc;
+    if ((rc = stage_buffer(h))) return rc;
+    CUDA_TRY(h, cudaMemcpyAsync(h->stage, src, sizeof(double) * (size_t)h->N, cudaMemcpyHostToDevice, h->stream));
+    launch_repack(h->stage, dst, h->geo, 1, h->stream);
+    return check_launch(h, "repack");
 }
 
 int copy_out(ads_ctx *h, double *dst, const double *src, int mem) {
-    cudaMemcpyKind k = mem == ADS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    CUDA_TRY(h, cudaMemcpy2DAsync(dst, sizeof(double) * h->n[0], src, sizeof(double) * h->geo.sy,
-                                  sizeof(double) * h->n[0], (size_t)h->n[1] * h->n[2], k, h->stream));
+    if (mem == ADS_MEM_DEVICE) {
+        CUDA_TRY(h, cudaMemcpy2DAsync(dst, sizeof(double) * h->n[0], src, sizeof(double) * h->geo.sy,
+                                      sizeof(double) * h->n[0], (size_t)h->n[1] * h->n[2], cudaMemcpyDeviceToDevice,
+                                      h->stream));
+        return ADS_OK;
+    }
+    int rc;
+    if ((rc = stage_buffer(h))) return rc;
+    launch_repack(src, h->stage, h->geo, 0, h->stream);
+    if ((rc = check_launch(h, "repack"))) return rc;
+    CUDA_TRY(h, cudaMemcpyAsync(dst, h->stage, sizeof(double) * (size_t)h->N, cudaMemcpyDeviceToHost, h->stream));
     return ADS_OK;
 }
 

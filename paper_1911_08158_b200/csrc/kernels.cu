@@ -1542,4 +1542,20 @@ void launch_line1(const double *in, double *out, double *V, double scale, double
     line1_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(in, out, V, scale, kick, inc, g);
 }
 
+__global__ void repack_kernel(const double *__restrict__ src, double *__restrict__ dst, Geom g, int to_pitched) {
+    const long N = (long)g.n0 * g.n1 * g.n2;
+    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(q % g.n0);
+        const long t = q / g.n0;
+        const long o = (t / g.n1) * g.sz + (t % g.n1) * g.sy + i;
+        if (to_pitched) dst[o] = src[q];
+        else dst[q] = src[o];
+    }
+}
+
+void launch_repack(const double *src, double *dst, const Geom &g, int to_pitched, cudaStream_t s) {
+    repack_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(src, dst, g, to_pitched);
+}
+
 }  // namespace ads
+

@@ -117,6 +117,8 @@ int launch_modal(double *cU, double *cV, double *ca, const double *lx, const dou
                  const double *fx, const double *fy, const double *fz, const double *g, long nsteps, double tau,
                  const Geom &geo, cudaStream_t s);
 void launch_set_long(long *dst, long value, cudaStream_t s);
+// dense caller layout (n0 n1 n2, x fastest) <-> pitched field (sy, sz): to_pitched = 1 unpacks
+void launch_repack(const double *src, double *dst, const Geom &g, int to_pitched, cudaStream_t s);
 // Solve along a direction of line length 1 (the 2D scheme's third axis): x = scale in, then the
 // sweep's epilogue -- out = x (if out), V += kick x (if V), *inc += 1 (if inc).  Elementwise.
 void launch_line1(const double *in, double *out, double *V, double scale, double kick, long *inc, const Geom &g,
