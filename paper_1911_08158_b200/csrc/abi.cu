@@ -89,14 +89,19 @@ struct ads_ctx {
     double *gU[2] = {nullptr, nullptr};
     long glaunch[2] = {0, 0};  // kernel launches in each graph (two steps)
     bool graphs_off = false;
-    // exact-in-time modal propagator (ads_modal_advance): per direction the
-    // extended n x n forward map Q = Phi^T M and inverse map Phi (column-major, zero rows and
-    // columns at Dirichlet DOFs), eigenvalues (0 at Dirichlet DOFs), modal load vector Phi^T b
+    // exact-in-time modal propagator (ads_modal_advance).  The uniform basis is
+    // mirror-symmetric, so every mode is even or odd under i <-> n-1-i and each direction's maps
+    // split in halves acting on the folded line (t = [u + Ju | u - Ju], launch_mirror):
+    //   forward  Q_e (ne x H), Q_o (no x h) of Q = Phi^T M;  inverse  P_e (H x ne), P_o (h x no)
+    // (column-major; h = n/2, H = h + n%2).  Modal coordinates along d are ordered [even | odd |
+    // unused], eigenvalues mlam in that order (0 on unused), mord = the active mode at each slot.
     bool modal_ready = false;
     cublasHandle_t cub = nullptr;
-    double *mQ[3] = {nullptr, nullptr, nullptr}, *mP[3] = {nullptr, nullptr, nullptr};
+    double *mQe[3] = {}, *mQo[3] = {}, *mPe[3] = {}, *mPo[3] = {};
+    int mne[3] = {0, 0, 0}, mno[3] = {0, 0, 0};
     double *mlam[3] = {nullptr, nullptr, nullptr}, *mf[3] = {nullptr, nullptr, nullptr};
     std::vector<double> mphi_h[3];  // active-block eigenvectors (host, for the load vectors)
+    std::vector<int> mord[3];
     double *mg = nullptr;           // g(t_{n+s}) of the forced recurrence
     long mg_cap = 0;
     // source
@@ -1024,64 +1029,112 @@ int modal_prepare(ads_ctx *h) {
     }
     for (int d = 0; d < 3; ++d) {
         const int o = h->sp[d].bc == ADS_BC_DIRICHLET0 ? 1 : 0;
-        const int n = h->n[d], na = n - 2 * o;
-        std::vector<double> lam, phi;
+        const int n = h->n[d], na = n - 2 * o, hh = n / 2, H = hh + (n & 1);
         int e = -1;  // an earlier direction with the same 1D space
         for (int c = 0; c < d; ++c)
             if (h->nel[c] == h->nel[d] && h->sp[c].bc == h->sp[d].bc) e = c;
         if (e >= 0) {
-            phi = h->mphi_h[e];
-        } else if (modal_basis(h->sp[d], lam, phi)) {
+            h->mQe[d] = h->mQe[e], h->mQo[d] = h->mQo[e], h->mPe[d] = h->mPe[e], h->mPo[d] = h->mPo[e];
+            h->mne[d] = h->mne[e], h->mno[d] = h->mno[e], h->mlam[d] = h->mlam[e];
+            h->mphi_h[d] = h->mphi_h[e], h->mord[d] = h->mord[e];
+            continue;
+        }
+        std::vector<double> lam, phi;
+        std::vector<int> par;  // exact parity of each mode (even / odd blocks solved apart)
+        if (modal_basis(h->sp[d], lam, phi, &par))
             return fail(h, ADS_E_SINGULAR, "modal basis of direction %d: eigensolver failed", d);
+        std::vector<int> E, O;
+        for (int k = 0; k < na; ++k) (par[k] > 0 ? E : O).push_back(k);
+        const int ne = (int)E.size(), no = (int)O.size();
+        // Q(k, i) = sum_j phi(j, k) M(j + o, i) at extended position i; Phi(i, k) likewise
+        auto Qf = [&](int k, int i) {
+            const int ia = i - o;
+            if (ia < 0 || ia >= na) return 0.0;
+            double q = 0.0;
+            for (int j = std::max(0, ia - h->p); j <= std::min(na - 1, ia + h->p); ++j)
+                q += phi[(size_t)j * na + k] * h->sp[d].M.get(j + o, i);
+            return q;
+        };
+        auto Pf = [&](int i, int k) { return (i - o >= 0 && i - o < na) ? phi[(size_t)(i - o) * na + k] : 0.0; };
+        std::vector<double> Qe((size_t)std::max(1, ne * H)), Qo((size_t)std::max(1, no * hh)),
+            Pe((size_t)std::max(1, H * ne)), Po((size_t)std::max(1, hh * no)), le(n, 0.0);
+        for (int a = 0; a < ne; ++a) {
+            for (int i = 0; i < H; ++i) Qe[(size_t)a + (size_t)i * ne] = Qf(E[a], i);
+            for (int i = 0; i < H; ++i) Pe[(size_t)i + (size_t)a * H] = Pf(i, E[a]);
+            le[a] = lam[E[a]];
         }
-        if (e < 0) {
-            std::vector<double> Pm((size_t)n * n, 0.0), Qm((size_t)n * n, 0.0), le(n, 0.0);
-            for (int k = 0; k < na; ++k) {
-                le[k + o] = lam[k];
-                for (int i = 0; i < na; ++i) Pm[(size_t)(i + o) + (size_t)(k + o) * n] = phi[(size_t)i * na + k];
-                for (int j = 0; j < na; ++j) {  // Q(k, j) = sum_i phi(i, k) M(i, j) over the band of M
-                    double q = 0.0;
-                    for (int i = std::max(0, j - h->p); i <= std::min(na - 1, j + h->p); ++i)
-                        q += phi[(size_t)i * na + k] * h->sp[d].M.get(i + o, j + o);
-                    Qm[(size_t)(k + o) + (size_t)(j + o) * n] = q;
-                }
-            }
-            for (double **f : {&h->mQ[d], &h->mP[d]})
-                if ((rc = dalloc(h, (void **)f, sizeof(double) * n * n))) return rc;
-            if ((rc = dalloc(h, (void **)&h->mlam[d], sizeof(double) * n))) return rc;
-            CUDA_TRY(h, cudaMemcpy(h->mQ[d], Qm.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
-            CUDA_TRY(h, cudaMemcpy(h->mP[d], Pm.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
-            CUDA_TRY(h, cudaMemcpy(h->mlam[d], le.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
-            h->mphi_h[d] = phi;
-        } else {
-            h->mQ[d] = h->mQ[e];
-            h->mP[d] = h->mP[e];
-            h->mlam[d] = h->mlam[e];
-            h->mphi_h[d] = h->mphi_h[e];
+        for (int b = 0; b < no; ++b) {
+            for (int i = 0; i < hh; ++i) Qo[(size_t)b + (size_t)i * no] = Qf(O[b], i);
+            for (int i = 0; i < hh; ++i) Po[(size_t)i + (size_t)b * hh] = Pf(i, O[b]);
+            le[ne + b] = lam[O[b]];
         }
+        double **dsts[5] = {&h->mQe[d], &h->mQo[d], &h->mPe[d], &h->mPo[d], &h->mlam[d]};
+        const std::vector<double> *srcs[5] = {&Qe, &Qo, &Pe, &Po, &le};
+        for (int q = 0; q < 5; ++q) {
+            if ((rc = dalloc(h, (void **)dsts[q], sizeof(double) * srcs[q]->size()))) return rc;
+            CUDA_TRY(h, cudaMemcpy(*dsts[q], srcs[q]->data(), sizeof(double) * srcs[q]->size(), cudaMemcpyHostToDevice));
+        }
+        h->mne[d] = ne;
+        h->mno[d] = no;
+        h->mphi_h[d] = phi;
+        h->mord[d] = E;
+        h->mord[d].insert(h->mord[d].end(), O.begin(), O.end());
     }
     h->modal_ready = true;
     return ADS_OK;
 }
 
-// out = (F_x (x) F_y (x) F_z) in along x, y, z (F = mQ forward or mP inverse); in -> a -> b -> a,
-// the result is in a (in is only read; a, b distinct scratch fields)
-int modal_transform(ads_ctx *h, double *const F[3], const double *in, double *a, double *b) {
+// the two half-size products of direction d: forward C = [Q_e T_even; Q_o T_odd] (T folded),
+// inverse T = [P_e C_even; P_o C_odd]; along x over the n1 n2 lines, along y per plane (batched),
+// along z over the (sy n1)-row plane matrix.  Zero-size products are skipped.
+int modal_half_products(ads_ctx *h, int d, bool inverse, const double *src, double *dst) {
     const Geom &g = h->geo;
+    const int n = h->n[d], hh = n / 2, H = hh + (n & 1), ne = h->mne[d], no = h->mno[d];
     const double one = 1.0, zero = 0.0;
-    // x: a(:, line) = F_x in(:, line) for the n1 n2 lines (pitch sy)
-    CUBLAS_TRY(h, cublasDgemm(h->cub, CUBLAS_OP_N, CUBLAS_OP_N, g.n0, g.n1 * g.n2, g.n0, &one, F[0], g.n0, in, (int)g.sy,
-                              &zero, a, (int)g.sy));
-    // y: per plane b_z = a_z F_y^T (a_z: n0 x n1, leading dimension sy)
-    CUBLAS_TRY(h, cublasDgemmStridedBatched(h->cub, CUBLAS_OP_N, CUBLAS_OP_T, g.n0, g.n1, g.n1, &one, a, (int)g.sy,
-                                            g.sz, F[1], g.n1, 0, &zero, b, (int)g.sy, g.sz, g.n2));
-    // z: a = b F_z^T with b viewed as (sy n1) x n2 (padding columns are zero and stay zero)
-    CUBLAS_TRY(h, cublasDgemm(h->cub, CUBLAS_OP_N, CUBLAS_OP_T, (int)g.sz, g.n2, g.n2, &one, b, (int)g.sz, F[2], g.n2,
-                              &zero, a, (int)g.sz));
-    h->launches += 3;
+    // per half q (even, odd): rows of the operator, its inner size, operator, offsets of in / out
+    const int mo[2] = {inverse ? H : ne, inverse ? hh : no}, kk[2] = {inverse ? ne : H, inverse ? no : hh};
+    const double *A[2] = {inverse ? h->mPe[d] : h->mQe[d], inverse ? h->mPo[d] : h->mQo[d]};
+    const long in_off[2] = {0, inverse ? ne : H}, out_off[2] = {0, inverse ? H : ne};
+    for (int q = 0; q < 2; ++q) {
+        if (mo[q] == 0 || kk[q] == 0) continue;
+        const int lda = mo[q];
+        if (d == 0) {
+            CUBLAS_TRY(h, cublasDgemm(h->cub, CUBLAS_OP_N, CUBLAS_OP_N, mo[q], g.n1 * g.n2, kk[q], &one, A[q], lda,
+                                      src + in_off[q], (int)g.sy, &zero, dst + out_off[q], (int)g.sy));
+        } else if (d == 1) {
+            CUBLAS_TRY(h, cublasDgemmStridedBatched(h->cub, CUBLAS_OP_N, CUBLAS_OP_T, g.n0, mo[q], kk[q], &one,
+                                                    src + in_off[q] * g.sy, (int)g.sy, g.sz, A[q], lda, 0, &zero,
+                                                    dst + out_off[q] * g.sy, (int)g.sy, g.sz, g.n2));
+        } else {
+            CUBLAS_TRY(h, cublasDgemm(h->cub, CUBLAS_OP_N, CUBLAS_OP_T, (int)g.sz, mo[q], kk[q], &one,
+                                      src + in_off[q] * g.sz, (int)g.sz, A[q], lda, &zero, dst + out_off[q] * g.sz,
+                                      (int)g.sz));
+        }
+        h->launches += 1;
+    }
     return ADS_OK;
 }
 
+// forward (modal coordinates) or inverse map of a whole field along x, y, z: in -> b, scratch a
+// (in is only read).  Forward per direction: fold (a), half products (b); inverse: half products
+// (a), unfold (b).
+int modal_transform(ads_ctx *h, bool inverse, const double *in, double *a, double *b) {
+    int rc;
+    const double *src = in;
+    for (int d = 0; d < 3; ++d) {
+        if (!inverse) {
+            launch_mirror(src, a, h->geo, d, 0, h->stream);
+            if ((rc = check_launch(h, "mirror"))) return rc;
+            if ((rc = modal_half_products(h, d, false, a, b))) return rc;
+        } else {
+            if ((rc = modal_half_products(h, d, true, src, a))) return rc;
+            launch_mirror(a, b, h->geo, d, 1, h->stream);
+            if ((rc = check_launch(h, "mirror"))) return rc;
+        }
+        src = b;
+    }
+    return ADS_OK;
+}
 
 }  // namespace
 
@@ -1345,11 +1398,12 @@ int ads_modal_advance(ads_handle h, long nsteps) {
         for (int d = 0; d < 3; ++d) {
             const int o = h->sp[d].bc == ADS_BC_DIRICHLET0 ? 1 : 0;
             const int n = h->n[d], na = n - 2 * o;
-            std::vector<double> f(n, 0.0);
-            for (int k = 0; k < na; ++k) {
+            std::vector<double> f(n, 0.0);  // in modal slot order (even | odd)
+            for (int slot = 0; slot < na; ++slot) {
+                const int k = h->mord[d][slot];
                 double v = 0.0;
                 for (int i = 0; i < na; ++i) v += h->mphi_h[d][(size_t)i * na + k] * h->src_h[d][i + o];
-                f[k + o] = v;
+                f[slot] = v;
             }
             if (!h->mf[d] && (rc = dalloc(h, (void **)&h->mf[d], sizeof(double) * n))) return rc;
             CUDA_TRY(h, cudaMemcpyAsync(h->mf[d], f.data(), sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
@@ -1366,15 +1420,14 @@ int ads_modal_advance(ads_handle h, long nsteps) {
         gdev = h->mg;
     }
     // U -> cU (in R), V -> cV (in U2); modes advance in place; back: cV -> V, cU -> U; then a
-    double *const Fq[3] = {h->mQ[0], h->mQ[1], h->mQ[2]}, *const Fp[3] = {h->mP[0], h->mP[1], h->mP[2]};
-    if ((rc = modal_transform(h, Fq, h->U, h->R, h->Wk))) return rc;
-    if ((rc = modal_transform(h, Fq, h->V, h->U2, h->Wk))) return rc;
+    if ((rc = modal_transform(h, false, h->U, h->Wk, h->R))) return rc;
+    if ((rc = modal_transform(h, false, h->V, h->Wk, h->U2))) return rc;
     if (launch_modal(h->R, h->U2, h->Wk, h->mlam[0], h->mlam[1], h->mlam[2], fvec[0], fvec[1], fvec[2], gdev, nsteps,
                      h->tau, h->geo, h->stream))
         return fail(h, ADS_E_INVAL, "ads_modal_advance: grid too large for the mode kernel");
     if ((rc = check_launch(h, "modal"))) return rc;
-    if ((rc = modal_transform(h, Fp, h->U2, h->V, h->A))) return rc;
-    if ((rc = modal_transform(h, Fp, h->R, h->U, h->A))) return rc;
+    if ((rc = modal_transform(h, true, h->U2, h->A, h->V))) return rc;
+    if ((rc = modal_transform(h, true, h->R, h->A, h->U))) return rc;
     h->step += nsteps;
     // a_n = D^-1 (F(t_n) - K U_n) (= P3 ca exactly; the operator kernel and three sweeps cost
     // less than a fifth transform and compute a as ads_step does)

@@ -584,16 +584,11 @@ static int tridiag_ql(std::vector<double> &d, std::vector<double> &e, std::vecto
     return 0;
 }
 
-int modal_basis(const Space1D &s, std::vector<double> &lam, std::vector<double> &phi) {
-    const int o = s.bc == 1 ? 1 : 0, na = s.n - 2 * o;
-    if (na <= 0) return -1;
-    // dense M (lower Cholesky factor in place) and K on the active DOFs
-    std::vector<double> L((size_t)na * na, 0.0), X((size_t)na * na, 0.0);
-    for (int i = 0; i < na; ++i)
-        for (int j = 0; j < na; ++j) {
-            L[(size_t)i * na + j] = s.M.get(i + o, j + o);
-            X[(size_t)i * na + j] = s.K.get(i + o, j + o);
-        }
+// K phi = lambda M phi for dense symmetric na x na matrices (M positive definite): Cholesky
+// M = L L^T, C = L^-1 K L^-T, Householder tridiagonalisation, implicit QL, Phi = L^-T Z.
+static int gen_eig_dense(int na, std::vector<double> L, std::vector<double> X, std::vector<double> &lam,
+                         std::vector<double> &phi) {
+    struct { int p; } s{na};  // no band structure assumed
     for (int j = 0; j < na; ++j) {
         double dj = L[(size_t)j * na + j];
         for (int k = std::max(0, j - s.p); k < j; ++k) dj -= L[(size_t)j * na + k] * L[(size_t)j * na + k];
@@ -648,6 +643,77 @@ int modal_basis(const Space1D &s, std::vector<double> &lam, std::vector<double> 
             z[i] = v / L[(size_t)i * na + i];
         }
         for (int i = 0; i < na; ++i) phi[(size_t)i * na + kk] = z[i];
+    }
+    return 0;
+}
+
+
+int modal_basis(const Space1D &s, std::vector<double> &lam, std::vector<double> &phi, std::vector<int> *parity) {
+    const int o = s.bc == 1 ? 1 : 0, na = s.n - 2 * o;
+    if (na <= 0) return -1;
+    // the uniform open knot vector is mirror-symmetric, so M and K (active block) commute with the
+    // reversal J: the pencil splits into an even block on (u + Ju) and an odd block on (u - Ju),
+    // each solved on its own -- every eigenvector has an exact parity (needed by the folded
+    // modal transforms) and each eigensolve is half the size
+    const int hb = na / 2, Hb = hb + (na & 1);
+    const double r2 = std::sqrt(0.5);
+    std::vector<double> M((size_t)na * na), K((size_t)na * na);
+    for (int i = 0; i < na; ++i)
+        for (int j = 0; j < na; ++j) {
+            M[(size_t)i * na + j] = s.M.get(i + o, j + o);
+            K[(size_t)i * na + j] = s.K.get(i + o, j + o);
+        }
+    struct Part { std::vector<double> lam, phi; int m, sign; };
+    Part parts[2] = {{{}, {}, Hb, 1}, {{}, {}, hb, -1}};
+    for (Part &pt : parts) {
+        const int m = pt.m;
+        if (m == 0) continue;
+        // basis columns: b_i = (e_i + sign e_{na-1-i}) / sqrt 2 (i < hb), the middle e_hb (even, odd na)
+        auto B = [&](int r, int i) {  // entry r of basis vector i
+            if (i == hb) return r == hb ? 1.0 : 0.0;
+            return (r == i ? r2 : 0.0) + (r == na - 1 - i ? pt.sign * r2 : 0.0);
+        };
+        std::vector<double> Mp((size_t)m * m), Kp((size_t)m * m);
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < m; ++j) {
+                const int ri[2] = {i, na - 1 - i}, rj[2] = {j, na - 1 - j};
+                double vm = 0.0, vk = 0.0;
+                for (int a = 0; a < (i == hb ? 1 : 2); ++a)
+                    for (int b = 0; b < (j == hb ? 1 : 2); ++b) {
+                        const double w = B(ri[a], i) * B(rj[b], j);
+                        vm += w * M[(size_t)ri[a] * na + rj[b]];
+                        vk += w * K[(size_t)ri[a] * na + rj[b]];
+                    }
+                Mp[(size_t)i * m + j] = vm;
+                Kp[(size_t)i * m + j] = vk;
+            }
+        std::vector<double> ph;
+        if (gen_eig_dense(m, Mp, Kp, pt.lam, ph)) return -1;
+        pt.phi.assign((size_t)na * m, 0.0);  // full eigenvectors phi = B ph, [na][m]
+        for (int k = 0; k < m; ++k)
+            for (int i = 0; i < m; ++i) {
+                const double c = ph[(size_t)i * m + k];
+                if (i == hb) {
+                    pt.phi[(size_t)hb * m + k] += c;
+                } else {
+                    pt.phi[(size_t)i * m + k] += r2 * c;
+                    pt.phi[(size_t)(na - 1 - i) * m + k] += pt.sign * r2 * c;
+                }
+            }
+    }
+    // merge in ascending eigenvalue order
+    std::vector<std::pair<double, std::pair<int, int>>> all;
+    for (int q = 0; q < 2; ++q)
+        for (int k = 0; k < parts[q].m; ++k) all.push_back({parts[q].lam[k], {q, k}});
+    std::sort(all.begin(), all.end());
+    lam.resize(na);
+    phi.assign((size_t)na * na, 0.0);
+    if (parity) parity->resize(na);
+    for (int c = 0; c < na; ++c) {
+        const int q = all[c].second.first, k = all[c].second.second;
+        lam[c] = all[c].first;
+        for (int i = 0; i < na; ++i) phi[(size_t)i * na + c] = parts[q].phi[(size_t)i * parts[q].m + k];
+        if (parity) (*parity)[c] = parts[q].sign;
     }
     return 0;
 }

@@ -124,6 +124,9 @@ namespace ads {
 // Dense Cholesky M = L L^T, C = L^-1 K L^-T, Householder tridiagonalisation, implicit QL,
 // Phi = L^-T Z.  lam ascending; phi row-major, phi[i * na + k] = component i of eigenvector k.
 // Returns 0, or -1 (M not positive definite, QL not converged, no active DOF).
-int modal_basis(const Space1D &s, std::vector<double> &lam, std::vector<double> &phi);
+// The reversal symmetry of the uniform basis splits the pencil into even and odd blocks solved
+// separately; parity (if non-null) receives +1 / -1 per eigenvector (exact by construction).
+int modal_basis(const Space1D &s, std::vector<double> &lam, std::vector<double> &phi,
+                std::vector<int> *parity = nullptr);
 
 }  // namespace ads

@@ -1557,5 +1557,43 @@ void launch_repack(const double *src, double *dst, const Geom &g, int to_pitched
     repack_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(src, dst, g, to_pitched);
 }
 
+__global__ void mirror_kernel(const double *__restrict__ src, double *__restrict__ dst, Geom g, int d, int unfold) {
+    const int n[3] = {g.n0, g.n1, g.n2};
+    const long st[3] = {1, g.sy, g.sz};
+    const int m = n[d], h = m / 2, H = h + (m & 1);
+    int e[3] = {n[0], n[1], n[2]};
+    e[d] = H;  // threads cover the first H positions along d
+    const long N = (long)e[0] * e[1] * e[2];
+    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x) {
+        int c[3];
+        c[0] = (int)(q % e[0]);
+        const long t = q / e[0];
+        c[1] = (int)(t % e[1]);
+        c[2] = (int)(t / e[1]);
+        const int i = c[d];
+        c[d] = 0;
+        const long base = c[0] * st[0] + c[1] * st[1] + c[2] * st[2], sd = st[d];
+        if (i < h) {
+            if (!unfold) {
+                const double a = src[base + i * sd], b = src[base + (long)(m - 1 - i) * sd];
+                dst[base + i * sd] = a + b;
+                dst[base + (long)(H + i) * sd] = a - b;
+            } else {
+                const double a = src[base + i * sd], b = src[base + (long)(H + i) * sd];
+                dst[base + i * sd] = a + b;
+                dst[base + (long)(m - 1 - i) * sd] = a - b;
+            }
+        } else {  // the middle position of an odd axis
+            dst[base + i * sd] = src[base + i * sd];
+        }
+    }
+}
+
+void launch_mirror(const double *src, double *dst, const Geom &g, int d, int unfold, cudaStream_t s) {
+    int e[3] = {g.n0, g.n1, g.n2};
+    e[d] = e[d] / 2 + (e[d] & 1);
+    mirror_kernel<<<grid_for((long)e[0] * e[1] * e[2]), 256, 0, s>>>(src, dst, g, d, unfold);
+}
+
 }  // namespace ads
 

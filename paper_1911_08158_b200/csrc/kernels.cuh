@@ -117,6 +117,11 @@ int launch_modal(double *cU, double *cV, double *ca, const double *lx, const dou
                  const double *fx, const double *fy, const double *fz, const double *g, long nsteps, double tau,
                  const Geom &geo, cudaStream_t s);
 void launch_set_long(long *dst, long value, cudaStream_t s);
+// Mirror fold along axis d (modal transforms, f3): with m the axis length, h = m / 2, H = h + m % 2,
+// fold: t_i = u_i + u_{m-1-i} (i < h), t_h = u_h (m odd), t_{H+i} = u_i - u_{m-1-i} (i < h);
+// unfold (the inverse map of the even/odd parts): u_i = t_i + t_{H+i}, u_{m-1-i} = t_i - t_{H+i},
+// u_h = t_h.  Positions are taken along axis d of the pitched field (x < n0).
+void launch_mirror(const double *src, double *dst, const Geom &g, int d, int unfold, cudaStream_t s);
 // dense caller layout (n0 n1 n2, x fastest) <-> pitched field (sy, sz): to_pitched = 1 unpacks
 void launch_repack(const double *src, double *dst, const Geom &g, int to_pitched, cudaStream_t s);
 // Solve along a direction of line length 1 (the 2D scheme's third axis): x = scale in, then the
