@@ -457,3 +457,21 @@ def test_bitwise_deterministic(ads, cfg):
     for a, b in zip(st0, st1):
         assert np.array_equal(a, b)
     assert np.array_equal(e0, e1)
+
+
+def test_next_row_argument_errors(ads):
+    """f2/f4 entry points reject what they do not support: 2D elasticity or slabs, tau <= 0,
+    scheme outside {0, 1}, tau changes on elasticity."""
+    with pytest.raises(ads.AdsError):
+        ads.Solver((8, 8, 0), 2, 1e-2, elastic=True)
+    with pytest.raises(ads.AdsError):
+        ads.Solver((8, 8, 0), 2, 1e-2, virtual_slabs=2)
+    g = ads.Solver((8, 8, 8), 2, 1e-2)
+    for bad in (0.0, -1e-3, float("nan")):
+        with pytest.raises(ads.AdsError):
+            g.set_tau(bad)
+    with pytest.raises(ads.AdsError):
+        g.set_scheme(2)
+    e = ads.Solver((4, 4, 4), 2, 1e-2, elastic=True)
+    with pytest.raises(ads.AdsError):
+        e.set_tau(5e-3)
