@@ -1450,16 +1450,22 @@ int ads_set_stream(ads_handle h, void *stream) {
     int rc = guard(h);
     if (rc) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    cudaStream_t old = h->stream, next = old;
+    bool own = h->own_stream;
     if (stream) {
-        if (h->own_stream) cudaStreamDestroy(h->stream);
-        h->stream = (cudaStream_t)stream;
-        h->own_stream = false;
+        next = (cudaStream_t)stream;
+        own = false;
     } else if (!h->own_stream) {
-        CUDA_TRY(h, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-        h->own_stream = true;
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&next, cudaStreamNonBlocking));
+        own = true;
     }
+    // the members of a virtual slab group run on the group's stream: move them while the old
+    // stream still exists, then release it
     for (ads_ctx *m : h->members)
-        if ((rc = ads_set_stream(m, h->stream))) return rc;
+        if ((rc = ads_set_stream(m, next))) return fail(h, rc, "member: %s", m->err.c_str());
+    if (h->own_stream && old != next) cudaStreamDestroy(old);
+    h->stream = next;
+    h->own_stream = own;
     if (h->cub) cublasSetStream(h->cub, h->stream);
     return ADS_OK;
 }

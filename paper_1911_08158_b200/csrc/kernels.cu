@@ -772,8 +772,9 @@ __global__ void __launch_bounds__(KT_THREADS, 2) kop_kernel(const KopArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
-// distributed z-solve fix-up + kick (see kernels.cuh ZfixArgs).  Thread per z-line of the
-// slab (coalesced across x), streaming the nl owned planes once: 24 B/DOF (+8 when a is kept).
+// distributed z-solve fix-up + kick (see kernels.cuh ZfixArgs).  Thread per z-line and z piece
+// of 32 planes (coalesced across x; each piece recomputes the line's interface values from the
+// tips), streaming the nl owned planes once: 24 B/DOF (+8 when a is kept).
 // ------------------------------------------------------------------------------------------
 template <int P>
 __device__ __forceinline__ void zload(const double *f, long base, long sz, int k0, double (&t)[P]) {
@@ -809,10 +810,11 @@ __global__ void __launch_bounds__(128) zint_kernel(const ZfixArgs a) {
 
 // stage 2 + correction + kick: thread per z-line of the slab (coalesced across x), streaming
 // the nl owned planes once: 24 B/DOF (+8 when a is kept)
+constexpr int ZF_X = 32, ZF_Y = 4, ZF_Z = 32;  // thread block 32 x 4 lines, z pieces of 32 planes
 template <int P>
-__global__ void __launch_bounds__(128) zfix_kernel(const ZfixArgs a) {
+__global__ void __launch_bounds__(ZF_X * ZF_Y) zfix_kernel(const ZfixArgs a) {
     const Geom &g = a.geo;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+    const int i = blockIdx.x * ZF_X + threadIdx.x, j = blockIdx.y * ZF_Y + threadIdx.y;
     if (i >= g.n0 || j >= g.n1) return;
     const int nl = g.n2;
     const long base = (long)j * g.sy + i;
@@ -855,16 +857,24 @@ __global__ void __launch_bounds__(128) zfix_kernel(const ZfixArgs a) {
 #pragma unroll
             for (int c = 0; c < P; ++c) un[r] = fma(a.qb[P + r][c], xl[c], fma(a.qb[P + r][P + c], tn[c], un[r]));
     }
-    for (int k = 0; k < nl; ++k) {
+    // the planes of this z piece (the fix-up of each plane is independent given the tips);
+    // restrict-qualified copies let the loads of later planes move ahead of the stores
+    const double *__restrict__ X = a.X;
+    double *__restrict__ Vf = a.Vf;
+    double *__restrict__ A = a.A;
+    const int k0 = blockIdx.z * ZF_Z, k1 = min(nl, k0 + ZF_Z);
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
         const long idx = base + (long)k * g.sz;
-        double x = a.X[idx];
+        double x = X[idx];
+        const double v = Vf[idx];
 #pragma unroll
         for (int m = 0; m < P; ++m) {
             x = fma(-__ldg(a.Wsp + (long)k * P + m), bp[m], x);
             x = fma(-__ldg(a.Vsp + (long)k * P + m), un[m], x);
         }
-        a.Vf[idx] = fma(a.kick, x, a.Vf[idx]);
-        if (a.A) a.A[idx] = x;
+        Vf[idx] = fma(a.kick, x, v);
+        if (A) A[idx] = x;
     }
 }
 
@@ -882,7 +892,7 @@ int launch_zint(int p, const ZfixArgs &a, cudaStream_t s) {
 }
 
 int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {
-    dim3 blk(128), grd((a.geo.n0 + 127) / 128, a.geo.n1);
+    dim3 blk(ZF_X, ZF_Y), grd((a.geo.n0 + ZF_X - 1) / ZF_X, (a.geo.n1 + ZF_Y - 1) / ZF_Y, (a.geo.n2 + ZF_Z - 1) / ZF_Z);
     switch (p) {
         case 1: zfix_kernel<1><<<grd, blk, 0, s>>>(a); break;
         case 2: zfix_kernel<2><<<grd, blk, 0, s>>>(a); break;

@@ -142,3 +142,20 @@ def test_nccl_slab_world1(ads):
     for x, y in zip(g.get_state(), ref.get_state()):
         assert rel(x, y) < 1e-13
     assert np.allclose(g.energy(), ref.energy(), rtol=1e-13)
+
+
+def test_virtual_group_set_stream(ads):
+    """A virtual slab group moves all its slabs to a caller stream (and back to its own) and
+    keeps stepping: results match the same run on the default stream."""
+    import torch
+    wl = workloads.get("c3").scaled(40, 8)
+    g = ads.make_solver(wl, virtual_slabs=2)
+    st = torch.cuda.Stream()
+    g.set_stream(st)
+    g.step(4)
+    g.set_stream(None)
+    g.step(4)
+    r = ads.make_solver(wl, virtual_slabs=2)
+    r.step(8)
+    for a, b in zip(g.get_state(), r.get_state()):
+        assert np.array_equal(a, b)
