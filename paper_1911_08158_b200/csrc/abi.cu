@@ -220,8 +220,15 @@ int make_solve_tab(ads_ctx *h, const Band &A, const char *what, SolveTab &tab) {
     const int n = A.n, p = A.p;
     LUFactors f;
     if (banded_lu(A, f, /*freeze=*/true)) return fail(h, ADS_E_SINGULAR, "%s singular", what);
-    const int C = kSweepChunks;
-    const int L = choose_chunk_len(n, p, C);
+    // chunking: 32 chunks, or 16 chunks of at most 17 rows when that pads the line less (e.g.
+    // 258 rows: 16 x 17 instead of 32 x 9 -- per-tile overheads are amortised over longer chunks)
+    int C = kSweepChunks;
+    int L = choose_chunk_len(n, p, C);
+    const int L16 = choose_chunk_len(n, p, 16);
+    if (L16 != 0 && L16 <= 17 && (L == 0 || 16 * L16 < C * L)) {
+        C = 16;
+        L = L16;
+    }
     if (L == 0) return fail(h, ADS_E_INVAL, "%s: n = %d has no supported chunking", what, n);
     // pad the factors to C*L rows with identity rows: every chunk has length L
     const int npad = C * L;
@@ -245,6 +252,7 @@ int make_solve_tab(ads_ctx *h, const Band &A, const char *what, SolveTab &tab) {
     tab.Rb = Rb;
     tab.n = n;
     tab.L = L;
+    tab.C = C;
     tab.Kf = pt.Kf;
     tab.Kb = pt.Kb;
     // uniform region aligned to whole chunks: chunks [c_lo, c_hi) lie inside [i_lo, i_hi)

@@ -57,11 +57,11 @@ namespace ads {
 // memory; tile pitch np = 2 (mod 16) keeps the per-thread chunk reads
 // conflict-free.  The z sweep fuses the kick V += tau a into its store.
 // ------------------------------------------------------------------------------------------
-// LW lines per tile (x: 8, y/z: 16); 32/LW chunks per warp; kSweepChunks LW threads
-template <int LW>
+// LW lines per tile (x: 8, y/z: 16); 32/LW chunks per warp; C (chunks per line) x LW threads
+template <int LW, int C = kSweepChunks>
 struct SW {
-    static constexpr int G = 32 / LW, WARPS = kSweepChunks / G, THREADS = 32 * WARPS;
-    static_assert(WARPS * G == kSweepChunks, "one chunk per (warp, lane group)");
+    static constexpr int G = 32 / LW, WARPS = C / G, THREADS = 32 * WARPS;
+    static_assert(WARPS * G == C, "one chunk per (warp, lane group)");
 };
 
 __host__ __device__ constexpr int ring(int i, int P) { return ((i % P) + P) % P; }
@@ -136,7 +136,7 @@ __device__ __forceinline__ void chunk_walk(double (&in)[P], const SolveTab &t, c
                                            int c, int K, int q) {
 #pragma unroll
     for (int m = 0; m < P; ++m) in[m] = 0.0;
-    const int c0 = FWD ? max(c - K, 0) : min(c + K, kSweepChunks - 1);
+    const int c0 = FWD ? max(c - K, 0) : min(c + K, t.C - 1);
     for (int cc = c0; FWD ? cc < c : cc > c; cc += FWD ? 1 : -1) {
         double nin[P];
 #pragma unroll
@@ -225,25 +225,26 @@ __host__ __device__ inline int xbox_cols(int n) {
 
 // edge rows: [0, c_lo L) and [c_hi L, C L), plus one block of L uniform rows
 __host__ __device__ inline int sweep_edge_rows(const SolveTab &t) {
-    return t.c_lo * t.L + (kSweepChunks - t.c_hi) * t.L + t.L;
+    return t.c_lo * t.L + (t.C - t.c_hi) * t.L + t.L;
 }
 template <int P, int LW>
 __host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir, long sy, bool kick, int vbufs = 1) {
-    const long fixed = 2L * kSweepChunks * P * P + 2L * kSweepChunks * P * LW +
+    const long fixed = 2L * t.C * P * P + 2L * t.C * P * LW +
                        (long)sweep_edge_rows(t) * (Rec<P>::FW + Rec<P>::BW);
     if (xdir) {
         const int nb = xbox_count(t.n), rb = xbox_cols(t.n);
         return fixed + 2L * ((nb * LW * rb + 15) & ~15) + 16 + 4;
     }
     (void)kick;
-    return fixed + (1L + vbufs) * kSweepChunks * t.L * LW + 16 + 4;
+    return fixed + (1L + vbufs) * t.C * t.L * LW + 16 + 4;
 }
 
-template <int P, int L, bool XDIR, int LW>
-__global__ void __launch_bounds__(SW<LW>::THREADS, 512 / SW<LW>::THREADS) sweep_kernel(const __grid_constant__ SweepArgs a) {
-    constexpr int SW_LW = LW, SW_G = SW<LW>::G, SW_THREADS = SW<LW>::THREADS;
+template <int P, int L, bool XDIR, int LW, int C>
+__global__ void __launch_bounds__(SW<LW, C>::THREADS, 512 / SW<LW, C>::THREADS)
+    sweep_kernel(const __grid_constant__ SweepArgs a) {
+    constexpr int SW_LW = LW, SW_G = SW<LW, C>::G, SW_THREADS = SW<LW, C>::THREADS;
     extern __shared__ __align__(16) double smem[];
-    constexpr int C = kSweepChunks, FW = Rec<P>::FW, BW = Rec<P>::BW;
+    constexpr int FW = Rec<P>::FW, BW = Rec<P>::BW;
     const SolveTab &t = a.t;
     const int nedge = sweep_edge_rows(t);
     double *shTf = smem, *shRb = shTf + C * P * P;
@@ -1333,10 +1334,10 @@ static int encode_field_map(CUtensorMap *m, const double *base, const Geom &g, u
     return r == CUDA_SUCCESS ? 0 : -1;
 }
 
-template <int P, int L, bool X>
+template <int P, int L, bool X, int C>
 static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
     constexpr int LW = (X || L > 17) ? 8 : 16;  // y/z: 16-line tiles while the buffers fit
-    constexpr int NT = SW<LW>::THREADS;
+    constexpr int NT = SW<LW, C>::THREADS;
     const Geom &g = a.geo;
     // y/z: a second output / V buffer when it fits the 227 KB of shared memory per CTA
     const int vbufs = (!X && sizeof(double) * sweep_smem_doubles<P, LW>(a.t, X, a.geo.sy, a.mode != 0, 2) <= 227 * 1024)
@@ -1350,14 +1351,14 @@ static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     if (sm > sm_set) {
-        cudaFuncSetAttribute(sweep_kernel<P, L, X, LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(sweep_kernel<P, L, X, LW, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         sm_set = sm;
     }
     long ntiles;
     if (X) ntiles = ((long)g.n1 * g.n2 + LW - 1) / LW;
     else ntiles = (long)((g.n0 + LW - 1) / LW) * (a.dir == 1 ? g.n2 : g.n1);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<P, L, X, LW>, NT, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<P, L, X, LW, C>, NT, sm);
     const long cap = (long)std::max(per_sm, 1) * nsm;
     dim3 grd((unsigned)std::min(ntiles, cap));
     SweepArgs b = a;
@@ -1373,9 +1374,9 @@ static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
             encode_field_map(&b.tm_out, a.out, g2, (unsigned)b.rb, LW, 1))
             return -2;
     } else {
-        // boxes of 16 lines x rb rows: C L = 32 L rows in nbox = 4 (8 when L > 32) boxes
+        // boxes of 16 lines x rb rows: the C L rows in nbox = 4 (8 when L > 32) boxes
         b.nbox = L <= 32 ? 4 : 8;
-        b.rb = kSweepChunks * L / b.nbox;
+        b.rb = C * L / b.nbox;
         const unsigned rb = (unsigned)b.rb;
         const bool y = a.dir == 1;
         if (encode_field_map(&b.tm_in, a.in, g, LW, y ? rb : 1, y ? 1 : rb) ||
@@ -1383,7 +1384,7 @@ static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
             (!a.mode && encode_field_map(&b.tm_out, a.out, g, LW, y ? rb : 1, y ? 1 : rb)))
             return -2;  // TMA descriptor could not be encoded
     }
-    sweep_kernel<P, L, X, LW><<<grd, NT, sm, s>>>(b);
+    sweep_kernel<P, L, X, LW, C><<<grd, NT, sm, s>>>(b);
     return 0;
 }
 
@@ -1392,7 +1393,13 @@ static int sweep_launch_L(const SweepArgs &a, cudaStream_t s) {
     if constexpr (LV < P) {
         return -1;  // a chunk must hold a whole boundary state
     } else {
-        return a.dir == 0 ? sweep_launch<P, LV, true>(a, s) : sweep_launch<P, LV, false>(a, s);
+        if constexpr (LV <= 17) {  // 16 chunks of at most 17 rows (make_solve_tab)
+            if (a.t.C == 16)
+                return a.dir == 0 ? sweep_launch<P, LV, true, 16>(a, s) : sweep_launch<P, LV, false, 16>(a, s);
+        }
+        if (a.t.C != kSweepChunks) return -1;
+        return a.dir == 0 ? sweep_launch<P, LV, true, kSweepChunks>(a, s)
+                          : sweep_launch<P, LV, false, kSweepChunks>(a, s);
     }
 }
 

@@ -18,6 +18,7 @@ struct SolveTab {
     const double *l = nullptr, *us = nullptr, *dinv = nullptr;  // [C*L][p], [C*L][p], [C*L]
     const double *Tf = nullptr, *Rb = nullptr;                  // [C][p][p] chunk transfer maps
     int n = 0, L = 0, Kf = 0, Kb = 0;
+    int C = kSweepChunks;  // chunks per line: 32, or 16 (chunks of <= 17 rows) when that pads less
     int c_lo = 0, c_hi = 0;  // uniform chunks [c_lo, c_hi): rows [c_lo L, c_hi L) are (lc, usc, dic)
     double lc[kMaxP] = {0, 0, 0, 0, 0}, usc[kMaxP] = {0, 0, 0, 0, 0}, dic = 0.0;
     // responses of a uniform chunk at local row j to a unit incoming state m:
