@@ -475,3 +475,26 @@ def test_next_row_argument_errors(ads):
     e = ads.Solver((4, 4, 4), 2, 1e-2, elastic=True)
     with pytest.raises(ads.AdsError):
         e.set_tau(5e-3)
+
+
+@pytest.mark.slow
+def test_maximum_grid_properties(ads):
+    """The largest supported grid (n_d = 1051 <= 1056 per direction, 1.16e9 DOFs, ~66 GB of
+    fields): a few steps from a projected bump stay finite and keep the conserved invariant
+    (C6) -- the oracle cannot run at this size, so parity here is a property."""
+    import torch
+    wl = workloads.get("c4")
+    wl.nel = (1048, 1048, 1048)
+    wl.u0 = wl.u0[:2]
+    s = ads.make_solver(wl)
+    e0 = s.energy()
+    s.step(3)
+    e1 = s.energy()
+    assert np.all(np.isfinite(e1)) and e1[1] > 0
+    assert abs(e1[2] - e0[2]) <= 1e-12 * abs(e0[2])
+    u = torch.empty(s.shape, dtype=torch.float64, device="cuda")
+    s.get_state(u, None, None)
+    assert bool(torch.isfinite(u).all())
+    s.close()
+    del u
+    torch.cuda.empty_cache()
