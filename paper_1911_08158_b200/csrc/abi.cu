@@ -221,13 +221,18 @@ int make_solve_tab(ads_ctx *h, const Band &A, const char *what, SolveTab &tab) {
     LUFactors f;
     if (banded_lu(A, f, /*freeze=*/true)) return fail(h, ADS_E_SINGULAR, "%s singular", what);
     // chunking: 32 chunks, or 16 chunks of at most 17 rows when that pads the line less (e.g.
-    // 258 rows: 16 x 17 instead of 32 x 9 -- per-tile overheads are amortised over longer chunks)
+    // 258 rows: 16 x 17 instead of 32 x 9 -- per-tile overheads are amortised over longer chunks),
+    // or 64 chunks of at most 17 rows for lines beyond 544 rows (33-row chunks held in registers
+    // ran at a third of the bandwidth)
     int C = kSweepChunks;
     int L = choose_chunk_len(n, p, C);
-    const int L16 = choose_chunk_len(n, p, 16);
+    const int L16 = choose_chunk_len(n, p, 16), L64 = choose_chunk_len(n, p, 64);
     if (L16 != 0 && L16 <= 17 && (L == 0 || 16 * L16 < C * L)) {
         C = 16;
         L = L16;
+    } else if ((L == 0 || L > 17) && L64 != 0 && L64 <= 17) {
+        C = 64;
+        L = L64;
     }
     if (L == 0) return fail(h, ADS_E_INVAL, "%s: n = %d has no supported chunking", what, n);
     // pad the factors to C*L rows with identity rows: every chunk has length L

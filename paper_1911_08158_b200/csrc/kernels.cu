@@ -1336,7 +1336,7 @@ static int encode_field_map(CUtensorMap *m, const double *base, const Geom &g, u
 
 template <int P, int L, bool X, int C>
 static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
-    constexpr int LW = (X || L > 17) ? 8 : 16;  // y/z: 16-line tiles while the buffers fit
+    constexpr int LW = (X || L > 17 || C > 32) ? 8 : 16;  // y/z: 16-line tiles while the buffers fit
     constexpr int NT = SW<LW, C>::THREADS;
     const Geom &g = a.geo;
     // y/z: a second output / V buffer when it fits the 227 KB of shared memory per CTA
@@ -1374,8 +1374,8 @@ static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
             encode_field_map(&b.tm_out, a.out, g2, (unsigned)b.rb, LW, 1))
             return -2;
     } else {
-        // boxes of 16 lines x rb rows: the C L rows in nbox = 4 (8 when L > 32) boxes
-        b.nbox = L <= 32 ? 4 : 8;
+        // boxes of LW lines x rb rows: the C L rows in nbox = 4 boxes, 8 when C L > 1024 (rb <= 256)
+        b.nbox = (L > 32 || C * L > 1024) ? 8 : 4;
         b.rb = C * L / b.nbox;
         const unsigned rb = (unsigned)b.rb;
         const bool y = a.dir == 1;
@@ -1393,9 +1393,11 @@ static int sweep_launch_L(const SweepArgs &a, cudaStream_t s) {
     if constexpr (LV < P) {
         return -1;  // a chunk must hold a whole boundary state
     } else {
-        if constexpr (LV <= 17) {  // 16 chunks of at most 17 rows (make_solve_tab)
+        if constexpr (LV <= 17) {  // 16 or 64 chunks of at most 17 rows (make_solve_tab)
             if (a.t.C == 16)
                 return a.dir == 0 ? sweep_launch<P, LV, true, 16>(a, s) : sweep_launch<P, LV, false, 16>(a, s);
+            if (a.t.C == 64)
+                return a.dir == 0 ? sweep_launch<P, LV, true, 64>(a, s) : sweep_launch<P, LV, false, 64>(a, s);
         }
         if (a.t.C != kSweepChunks) return -1;
         return a.dir == 0 ? sweep_launch<P, LV, true, kSweepChunks>(a, s)
