@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import os
 import statistics
 import sys
@@ -64,7 +65,9 @@ def ncu_traffic(kernel, n_dof):
     """DRAM bytes per launch of `kernel` from the latest committed `--set full` capture
     (profiles/r*_traffic.json, written by scripts/ncu_traffic.py for config c4), or None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    def version(path):  # r<round>_v<version>_traffic.json, compared numerically (v10 after v9)
+        return tuple(int(x) for x in re.findall(r"\d+", os.path.basename(path)))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), key=version)
     if not files or n_dof != C4_DOFS:
         return None, None
     with open(files[-1]) as f:

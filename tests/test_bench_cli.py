@@ -30,7 +30,9 @@ def test_roofline_traffic_comes_from_the_committed_capture():
     spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
     bench = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(bench)
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")),
+                   key=lambda f: tuple(int(x) for x in re.findall(r"\d+", os.path.basename(f))))
     assert files, "no committed traffic capture"
     ref = json.load(open(files[-1]))["kernels"]["kop"]["dram_bytes"] / 1e9
     got, src = bench.ncu_traffic("kop", 515 ** 3)
