@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(SW<LW, C>::THREADS, 512 / SW<LW, C>::THREADS)
         // per-thread chunk reads conflict-free), results go back with TMA stores from a second
         // buffer (out-of-bounds columns and lines are neither read nor written).
         const int XB = a.rb, NB = a.nbox, RS = SW_LW * XB;  // region size (doubles)
-        double *xin = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(buf) + 127) & ~uintptr_t(127));
+        double *xin = buf + ((128 - (reinterpret_cast<uintptr_t>(buf) & 127)) & 127) / sizeof(double);
         double *xout = xin + ((NB * RS + 15) & ~15);
         unsigned long long *mbar = reinterpret_cast<unsigned long long *>(xout + ((NB * RS + 15) & ~15));
         const unsigned mb = (unsigned)__cvta_generic_to_shared(mbar);
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(SW<LW, C>::THREADS, 512 / SW<LW, C>::THREADS)
         const bool kick = a.mode != 0;
         const int nv = max(0, min(L, n - s));  // rows of my chunk inside the line
         // buffers (128-byte aligned) and two mbarriers after them
-        double *ibase = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(buf) + 127) & ~uintptr_t(127));
+        double *ibase = buf + ((128 - (reinterpret_cast<uintptr_t>(buf) & 127)) & 127) / sizeof(double);
         double *vbase0 = ibase + C * L * SW_LW;  // a.vbufs tile buffers of C L SW_LW doubles
         unsigned long long *mbar = reinterpret_cast<unsigned long long *>(vbase0 + a.vbufs * C * L * SW_LW);
         const unsigned mb_in = (unsigned)__cvta_generic_to_shared(mbar), mb_v = mb_in + 8;
