@@ -7,7 +7,10 @@ never imports it.
 
 The C oracle is built by ``build()`` (also called from
 ``__graft_entry__.build()``) with ``gcc -O2 -ffp-contract=off``: plain,
-single-threaded fp64.
+single-threaded fp64.  The same source is also built with -DOR_LONG_DOUBLE
+(x87 extended precision, ``libads_oracle_ld.so``): ``PWave(..., ext=True)`` and
+``Elastic(..., ext=True)`` run it as the truth reference for the one-step fp64
+bound (T1).
 """
 from __future__ import annotations
 
@@ -20,7 +23,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ads_oracle.c")
 _LIB = os.path.join(_HERE, "libads_oracle.so")
+_LIB_LD = os.path.join(_HERE, "libads_oracle_ld.so")
 _lib = None
+_lib_ld = None
 
 _D = ctypes.c_double
 _I = ctypes.c_int
@@ -29,17 +34,21 @@ _DP = ctypes.POINTER(ctypes.c_double)
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-std=c99",
-                               "-o", _LIB, _SRC, "-lm"])
+    for out, extra in ((_LIB, []), (_LIB_LD, ["-DOR_LONG_DOUBLE"])):
+        if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+            subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-std=c99", *extra,
+                                   "-o", out, _SRC, "-lm"])
     return _LIB
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(ext: bool = False):
+    """The oracle library: fp64 (default) or, ext=True, the same code in x87 extended precision."""
+    global _lib, _lib_ld
+    if (_lib_ld if ext else _lib) is None:
         build()
-        L = ctypes.CDLL(_LIB)
+        L = ctypes.CDLL(_LIB_LD if ext else _LIB)
+        _D = ctypes.c_longdouble if ext else ctypes.c_double
+        _DP = ctypes.POINTER(_D)
         sig = {
             "or_knots": (None, [_I, _I, _DP]),
             "or_bspline": (_D, [_DP, _I, _I, _D]),
@@ -80,14 +89,20 @@ def lib():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
-        _lib = L
-    return _lib
+        if ext:
+            _lib_ld = L
+        else:
+            _lib = L
+    return _lib_ld if ext else _lib
 
 
 def _ptr(a):
     if a is None:
         return None
-    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    assert a.flags["C_CONTIGUOUS"]
+    if a.dtype == np.longdouble and np.longdouble != np.float64:
+        return a.ctypes.data_as(ctypes.POINTER(ctypes.c_longdouble))
+    assert a.dtype == np.float64
     return a.ctypes.data_as(_DP)
 
 
@@ -151,94 +166,95 @@ def ricker(t, f0=25.0, t0=0.04):
 class PWave:
     """Oracle P-wave solver; scheme 1 = reading R1 (default), 0 = literal Eq. 16."""
 
-    def __init__(self, nel, p, tau, bc=1, scheme=1):
+    def __init__(self, nel, p, tau, bc=1, scheme=1, ext=False):
         if isinstance(nel, int):
             nel = (nel, nel, nel)
+        self._L, self.dtype = lib(ext), (np.longdouble if ext else np.float64)
         self.nel, self.p, self.tau, self.bc = tuple(nel), p, tau, bc
         self.n = tuple(1 if e == 0 else e + p for e in nel)  # nel_z = 0: the 2D scheme (one z function)
         self.shape = (self.n[2], self.n[1], self.n[0])  # numpy (z, y, x): x fastest
         self.N = int(np.prod(self.n))
         h = _P()
-        _check(lib().or_pw_create(ctypes.byref(h), nel[0], nel[1], nel[2], p, tau, bc, scheme))
+        _check(self._L.or_pw_create(ctypes.byref(h), nel[0], nel[1], nel[2], p, tau, bc, scheme))
         self.h = h
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().or_pw_destroy(self.h)
+            self._L.or_pw_destroy(self.h)
             self.h = None
 
     def _f(self, a):
-        return np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(self.shape))
+        return np.ascontiguousarray(np.asarray(a, dtype=self.dtype).reshape(self.shape))
 
     def set_source(self, b=None, wavelet=1, f0=25.0, t0=0.04, amp=1.0):
         if b is None:
-            _check(lib().or_pw_set_source(self.h, None, None, None, 0, 0.0, 0.0, 0.0))
+            _check(self._L.or_pw_set_source(self.h, None, None, None, 0, 0.0, 0.0, 0.0))
             return
-        bs = [np.ascontiguousarray(x, dtype=np.float64) for x in b]
+        bs = [np.ascontiguousarray(x, dtype=self.dtype) for x in b]
         self._src = bs
-        _check(lib().or_pw_set_source(self.h, _ptr(bs[0]), _ptr(bs[1]), _ptr(bs[2]), wavelet, f0, t0, amp))
+        _check(self._L.or_pw_set_source(self.h, _ptr(bs[0]), _ptr(bs[1]), _ptr(bs[2]), wavelet, f0, t0, amp))
 
     def set_state(self, u, udot=None):
         u = self._f(u)
         ud = None if udot is None else self._f(udot)
-        _check(lib().or_pw_set_state(self.h, _ptr(u), _ptr(ud)))
+        _check(self._L.or_pw_set_state(self.h, _ptr(u), _ptr(ud)))
 
     def step(self, nsteps=1):
-        _check(lib().or_pw_step(self.h, nsteps))
+        _check(self._L.or_pw_step(self.h, nsteps))
 
     def get_state(self):
-        u, ud, a = (np.zeros(self.shape) for _ in range(3))
-        _check(lib().or_pw_get_state(self.h, _ptr(u), _ptr(ud), _ptr(a)))
+        u, ud, a = (np.zeros(self.shape, self.dtype) for _ in range(3))
+        _check(self._L.or_pw_get_state(self.h, _ptr(u), _ptr(ud), _ptr(a)))
         return u, ud, a
 
     def get_raw(self):
-        U, V, a = (np.zeros(self.shape) for _ in range(3))
-        _check(lib().or_pw_get_raw(self.h, _ptr(U), _ptr(V), _ptr(a)))
+        U, V, a = (np.zeros(self.shape, self.dtype) for _ in range(3))
+        _check(self._L.or_pw_get_raw(self.h, _ptr(U), _ptr(V), _ptr(a)))
         return U, V, a
 
     def energy(self):
-        e = np.zeros(3)
-        _check(lib().or_pw_energy(self.h, _ptr(e)))
+        e = np.zeros(3, self.dtype)
+        _check(self._L.or_pw_energy(self.h, _ptr(e)))
         return e
 
     def time(self):
-        return lib().or_pw_time(self.h)
+        return self._L.or_pw_time(self.h)
 
     def _op(self, fn, x):
         x = self._f(x)
-        out = np.zeros(self.shape)
+        out = np.zeros(self.shape, self.dtype)
         _check(fn(self.h, _ptr(x), _ptr(out)))
         return out
 
     def kapply(self, x):
-        return self._op(lib().or_pw_kapply, x)
+        return self._op(self._L.or_pw_kapply, x)
 
     def dapply(self, x):
-        return self._op(lib().or_pw_dapply, x)
+        return self._op(self._L.or_pw_dapply, x)
 
     def mapply(self, x):
-        return self._op(lib().or_pw_mapply, x)
+        return self._op(self._L.or_pw_mapply, x)
 
     def dsolve(self, x):
         x = self._f(x).copy()
-        _check(lib().or_pw_dsolve(self.h, _ptr(x)))
+        _check(self._L.or_pw_dsolve(self.h, _ptr(x)))
         return x
 
     def msolve(self, x):
         x = self._f(x).copy()
-        _check(lib().or_pw_msolve(self.h, _ptr(x)))
+        _check(self._L.or_pw_msolve(self.h, _ptr(x)))
         return x
 
     def msolve_1d(self, d, x):
-        x = np.ascontiguousarray(x, dtype=np.float64).copy()
-        _check(lib().or_pw_msolve_1d(self.h, d, _ptr(x)))
+        x = np.ascontiguousarray(x, dtype=self.dtype).copy()
+        _check(self._L.or_pw_msolve_1d(self.h, d, _ptr(x)))
         return x
 
     def matrix(self, d, which):
         """which: 0 = M_d, 1 = K_d, 2 = A_d, 3 = LU(A_d) (BC applied)."""
         n = self.n[d]
-        out = np.zeros((n, n))
-        _check(lib().or_pw_matrix(self.h, d, which, _ptr(out)))
+        out = np.zeros((n, n), self.dtype)
+        _check(self._L.or_pw_matrix(self.h, d, which, _ptr(out)))
         return out
 
 
@@ -246,56 +262,57 @@ class PWave:
 class Elastic:
     """Oracle 3D elasticity solver (delta-form alternating-triangular split E1)."""
 
-    def __init__(self, nel, p, tau, bc=1, lam=1.0, mu=1.0, rho=1.0):
+    def __init__(self, nel, p, tau, bc=1, lam=1.0, mu=1.0, rho=1.0, ext=False):
         if isinstance(nel, int):
             nel = (nel, nel, nel)
+        self._L, self.dtype = lib(ext), (np.longdouble if ext else np.float64)
         self.nel, self.p, self.tau, self.bc = tuple(nel), p, tau, bc
         self.n = tuple(e + p for e in nel)
         self.shape = (3, self.n[2], self.n[1], self.n[0])
         self.N = int(np.prod(self.n))
         h = _P()
-        _check(lib().or_el_create(ctypes.byref(h), nel[0], nel[1], nel[2], p, tau, bc, lam, mu, rho))
+        _check(self._L.or_el_create(ctypes.byref(h), nel[0], nel[1], nel[2], p, tau, bc, lam, mu, rho))
         self.h = h
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().or_el_destroy(self.h)
+            self._L.or_el_destroy(self.h)
             self.h = None
 
     def _f(self, a):
-        return np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(self.shape))
+        return np.ascontiguousarray(np.asarray(a, dtype=self.dtype).reshape(self.shape))
 
     def apply(self, x):
         x = self._f(x)
-        out = np.zeros(self.shape)
-        _check(lib().or_el_apply(self.h, _ptr(x), _ptr(out)))
+        out = np.zeros(self.shape, self.dtype)
+        _check(self._L.or_el_apply(self.h, _ptr(x), _ptr(out)))
         return out
 
     def dsolve(self, x):
         x = self._f(x).copy()
-        _check(lib().or_el_dsolve(self.h, _ptr(x)))
+        _check(self._L.or_el_dsolve(self.h, _ptr(x)))
         return x
 
     def set_state(self, u, udot=None):
         u = self._f(u)
         ud = None if udot is None else self._f(udot)
-        _check(lib().or_el_set_state(self.h, _ptr(u), _ptr(ud)))
+        _check(self._L.or_el_set_state(self.h, _ptr(u), _ptr(ud)))
 
     def step(self, nsteps=1):
-        _check(lib().or_el_step(self.h, nsteps))
+        _check(self._L.or_el_step(self.h, nsteps))
 
     def get_state(self):
-        u, ud, a = (np.zeros(self.shape) for _ in range(3))
-        _check(lib().or_el_get_state(self.h, _ptr(u), _ptr(ud), _ptr(a)))
+        u, ud, a = (np.zeros(self.shape, self.dtype) for _ in range(3))
+        _check(self._L.or_el_get_state(self.h, _ptr(u), _ptr(ud), _ptr(a)))
         return u, ud, a
 
     def energy(self):
-        e = np.zeros(3)
-        _check(lib().or_el_energy(self.h, _ptr(e)))
+        e = np.zeros(3, self.dtype)
+        _check(self._L.or_el_energy(self.h, _ptr(e)))
         return e
 
     def time(self):
-        return lib().or_el_time(self.h)
+        return self._L.or_el_time(self.h)
 
 
 # ---------------------------------------------------------------- workloads

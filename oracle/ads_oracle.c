@@ -37,10 +37,23 @@
  * Kronecker solve/apply, brute-force 3D quadrature stiffness and elasticity,
  * modal closed form (oracle/modal.py), exact discrete
  * energy invariant, work identity, PDE eigenmode accuracy and order 2.
+ *
+ * Arithmetic type: `real` is double (the oracle proper, libads_oracle.so).  The same source
+ * compiled with -DOR_LONG_DOUBLE (libads_oracle_ld.so) runs every step in x87 extended precision
+ * (64-bit significand): the truth reference the GPU's one-step fp64 bound is measured against
+ * (north_star "relative L2 <= 1e-12 after one step"; T1).  <tgmath.h> makes sin, cos,
+ * exp, fabs follow the argument type; the double build is bitwise the oracle it always was.
  */
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#include <tgmath.h>
+
+#ifdef OR_LONG_DOUBLE
+typedef long double real;
+#else
+typedef double real;
+#endif
 
 #define OR_OK 0
 #define OR_E_INVAL (-1)
@@ -55,12 +68,12 @@ int or_nbasis(int p, int nel) { return nel + p; }
 
 /* Open (clamped) uniform knot vector: p+1 zeros, interior e/nel, p+1 ones.
  * Length nel + 2p + 1. */
-void or_knots(int p, int nel, double *t) {
+void or_knots(int p, int nel, real *t) {
     int m = nel + 2 * p + 1;
     for (int i = 0; i < m; ++i) {
         if (i <= p) t[i] = 0.0;
         else if (i >= nel + p) t[i] = 1.0;
-        else t[i] = (double)(i - p) / (double)nel;
+        else t[i] = (real)(i - p) / (real)nel;
     }
 }
 
@@ -69,50 +82,50 @@ void or_knots(int p, int nel, double *t) {
  *   N_{i,q}(x) = (x - t_i)/(t_{i+q} - t_i) N_{i,q-1}(x)
  *              + (t_{i+q+1} - x)/(t_{i+q+1} - t_{i+1}) N_{i+1,q-1}(x)
  * with 0/0 := 0.  Only evaluated at points strictly inside elements. */
-double or_bspline(const double *t, int i, int q, double x) {
+real or_bspline(const real *t, int i, int q, real x) {
     if (q == 0) return (t[i] <= x && x < t[i + 1]) ? 1.0 : 0.0;
-    double a = 0.0, b = 0.0;
-    double d1 = t[i + q] - t[i];
-    double d2 = t[i + q + 1] - t[i + 1];
+    real a = 0.0, b = 0.0;
+    real d1 = t[i + q] - t[i];
+    real d2 = t[i + q + 1] - t[i + 1];
     if (d1 > 0.0) a = (x - t[i]) / d1 * or_bspline(t, i, q - 1, x);
     if (d2 > 0.0) b = (t[i + q + 1] - x) / d2 * or_bspline(t, i + 1, q - 1, x);
     return a + b;
 }
 
 /* Derivative: N'_{i,q} = q/(t_{i+q}-t_i) N_{i,q-1} - q/(t_{i+q+1}-t_{i+1}) N_{i+1,q-1}. */
-double or_bspline_d(const double *t, int i, int q, double x) {
+real or_bspline_d(const real *t, int i, int q, real x) {
     if (q == 0) return 0.0;
-    double a = 0.0, b = 0.0;
-    double d1 = t[i + q] - t[i];
-    double d2 = t[i + q + 1] - t[i + 1];
-    if (d1 > 0.0) a = (double)q / d1 * or_bspline(t, i, q - 1, x);
-    if (d2 > 0.0) b = (double)q / d2 * or_bspline(t, i + 1, q - 1, x);
+    real a = 0.0, b = 0.0;
+    real d1 = t[i + q] - t[i];
+    real d2 = t[i + q + 1] - t[i + 1];
+    if (d1 > 0.0) a = (real)q / d1 * or_bspline(t, i, q - 1, x);
+    if (d2 > 0.0) b = (real)q / d2 * or_bspline(t, i + 1, q - 1, x);
     return a - b;
 }
 
 /* Gauss-Legendre rule with m points on [-1,1]: Newton iteration on P_m. */
-void or_gauss(int m, double *xi, double *w) {
-    const double pi = 3.14159265358979323846;
+void or_gauss(int m, real *xi, real *w) {
+    const real pi = (real)3.14159265358979323846264338327950288L;
     for (int k = 0; k < m; ++k) {
-        double x = cos(pi * (k + 0.75) / (m + 0.5));
-        double dp = 0.0;
+        real x = cos(pi * (k + 0.75) / (m + 0.5));
+        real dp = 0.0;
         for (int it = 0; it < 100; ++it) {
-            double p0 = 1.0, p1 = x;
+            real p0 = 1.0, p1 = x;
             for (int j = 2; j <= m; ++j) {
-                double p2 = ((2.0 * j - 1.0) * x * p1 - (j - 1.0) * p0) / j;
+                real p2 = ((2.0 * j - 1.0) * x * p1 - (j - 1.0) * p0) / j;
                 p0 = p1;
                 p1 = p2;
             }
             if (m == 1) { p1 = x; p0 = 1.0; }
             dp = m * (x * p1 - p0) / (x * x - 1.0);
-            double dx = p1 / dp;
+            real dx = p1 / dp;
             x -= dx;
             if (fabs(dx) < 1e-16) break;
         }
         {
-            double p0 = 1.0, p1 = x;
+            real p0 = 1.0, p1 = x;
             for (int j = 2; j <= m; ++j) {
-                double p2 = ((2.0 * j - 1.0) * x * p1 - (j - 1.0) * p0) / j;
+                real p2 = ((2.0 * j - 1.0) * x * p1 - (j - 1.0) * p0) / j;
                 p0 = p1;
                 p1 = p2;
             }
@@ -130,7 +143,7 @@ void or_gauss(int m, double *xi, double *w) {
 /* dense row-major n x n; p+1 Gauss points per element (exact, C4).          */
 /* bc = 1: zero Dirichlet -> rows/cols of the two end functions zeroed (C3). */
 /* ------------------------------------------------------------------------ */
-int or_matrices_1d(int p, int nel, int bc, double *M, double *K, double *B) {
+int or_matrices_1d(int p, int nel, int bc, real *M, real *K, real *B) {
     if (p < 1 || nel < 0) return OR_E_INVAL;
     if (nel == 0) {  /* the 2D scheme's third axis: one function, M = 1, K = B = 0 (see or_pw_create) */
         M[0] = 1.0; K[0] = 0.0;
@@ -138,23 +151,23 @@ int or_matrices_1d(int p, int nel, int bc, double *M, double *K, double *B) {
         return OR_OK;
     }
     int n = nel + p;
-    double *t = (double *)malloc(sizeof(double) * (nel + 2 * p + 1));
-    double xi[16], wq[16];
+    real *t = (real *)malloc(sizeof(real) * (nel + 2 * p + 1));
+    real xi[16], wq[16];
     or_knots(p, nel, t);
     or_gauss(p + 1, xi, wq);
-    memset(M, 0, sizeof(double) * n * n);
-    memset(K, 0, sizeof(double) * n * n);
-    if (B) memset(B, 0, sizeof(double) * n * n);
+    memset(M, 0, sizeof(real) * n * n);
+    memset(K, 0, sizeof(real) * n * n);
+    if (B) memset(B, 0, sizeof(real) * n * n);
     for (int e = 0; e < nel; ++e) {
-        double xa = t[p + e], xb = t[p + e + 1];
-        double J = 0.5 * (xb - xa);
+        real xa = t[p + e], xb = t[p + e + 1];
+        real J = 0.5 * (xb - xa);
         for (int q = 0; q <= p; ++q) {
-            double x = 0.5 * (xa + xb) + J * xi[q];
-            double w = J * wq[q];
+            real x = 0.5 * (xa + xb) + J * xi[q];
+            real w = J * wq[q];
             for (int a = e; a <= e + p; ++a) {
-                double Na = or_bspline(t, a, p, x), dNa = or_bspline_d(t, a, p, x);
+                real Na = or_bspline(t, a, p, x), dNa = or_bspline_d(t, a, p, x);
                 for (int c = e; c <= e + p; ++c) {
-                    double Nc = or_bspline(t, c, p, x), dNc = or_bspline_d(t, c, p, x);
+                    real Nc = or_bspline(t, c, p, x), dNc = or_bspline_d(t, c, p, x);
                     M[a * n + c] += w * Na * Nc;
                     K[a * n + c] += w * dNa * dNc;
                     if (B) B[a * n + c] += w * dNa * Nc;
@@ -179,21 +192,21 @@ int or_matrices_1d(int p, int nel, int bc, double *M, double *K, double *B) {
 
 /* 1D load vector b_a = int f(x) N_a(x) dx, 8 Gauss points per element (C4).
  * kind 0: f = sin(pi x); kind 1: f = exp(-(x-c)^2/(2 sigma^2)). */
-int or_load_1d(int p, int nel, int bc, int kind, double c, double sigma, double *b) {
-    const double pi = 3.14159265358979323846;
+int or_load_1d(int p, int nel, int bc, int kind, real c, real sigma, real *b) {
+    const real pi = (real)3.14159265358979323846264338327950288L;
     int n = nel + p;
-    double *t = (double *)malloc(sizeof(double) * (nel + 2 * p + 1));
-    double xi[8], wq[8];
+    real *t = (real *)malloc(sizeof(real) * (nel + 2 * p + 1));
+    real xi[8], wq[8];
     or_knots(p, nel, t);
     or_gauss(8, xi, wq);
-    memset(b, 0, sizeof(double) * n);
+    memset(b, 0, sizeof(real) * n);
     for (int e = 0; e < nel; ++e) {
-        double xa = t[p + e], xb = t[p + e + 1];
-        double J = 0.5 * (xb - xa);
+        real xa = t[p + e], xb = t[p + e + 1];
+        real J = 0.5 * (xb - xa);
         for (int q = 0; q < 8; ++q) {
-            double x = 0.5 * (xa + xb) + J * xi[q];
-            double w = J * wq[q];
-            double f;
+            real x = 0.5 * (xa + xb) + J * xi[q];
+            real w = J * wq[q];
+            real f;
             if (kind == 0) f = sin(pi * x);
             else f = exp(-(x - c) * (x - c) / (2.0 * sigma * sigma));
             for (int a = e; a <= e + p; ++a) b[a] += w * f * or_bspline(t, a, p, x);
@@ -210,15 +223,15 @@ int or_load_1d(int p, int nel, int bc, int kind, double c, double sigma, double 
 /* L is unit lower (stored below the diagonal), U on and above.             */
 /* Singular guard: pivot < 1e-14 * max|A| -> OR_E_SINGULAR.   */
 /* ------------------------------------------------------------------------ */
-int or_banded_lu(int n, int p, double *A) {
-    double amax = 0.0;
+int or_banded_lu(int n, int p, real *A) {
+    real amax = 0.0;
     for (int i = 0; i < n * n; ++i) if (fabs(A[i]) > amax) amax = fabs(A[i]);
     for (int k = 0; k < n; ++k) {
-        double piv = A[k * n + k];
+        real piv = A[k * n + k];
         if (!(fabs(piv) >= 1e-14 * amax) || amax == 0.0) return OR_E_SINGULAR;
         int iend = (k + p < n - 1) ? k + p : n - 1;
         for (int i = k + 1; i <= iend; ++i) {
-            double l = A[i * n + k] / piv;
+            real l = A[i * n + k] / piv;
             A[i * n + k] = l;
             for (int j = k + 1; j <= iend; ++j) A[i * n + j] -= l * A[k * n + j];
         }
@@ -227,22 +240,22 @@ int or_banded_lu(int n, int p, double *A) {
 }
 
 /* Solve (LU) x = r in place for one vector with stride s. */
-static void lu_solve_strided(int n, int p, const double *LU, double *x, long s) {
+static void lu_solve_strided(int n, int p, const real *LU, real *x, long s) {
     for (int i = 0; i < n; ++i) {           /* forward: L y = r */
-        double acc = x[i * s];
+        real acc = x[i * s];
         int j0 = (i - p > 0) ? i - p : 0;
         for (int j = j0; j < i; ++j) acc -= LU[i * n + j] * x[j * s];
         x[i * s] = acc;
     }
     for (int i = n - 1; i >= 0; --i) {      /* backward: U x = y */
-        double acc = x[i * s];
+        real acc = x[i * s];
         int j1 = (i + p < n - 1) ? i + p : n - 1;
         for (int j = i + 1; j <= j1; ++j) acc -= LU[i * n + j] * x[j * s];
         x[i * s] = acc / LU[i * n + i];
     }
 }
 
-void or_lu_solve(int n, int p, const double *LU, double *x) { lu_solve_strided(n, p, LU, x, 1); }
+void or_lu_solve(int n, int p, const real *LU, real *x) { lu_solve_strided(n, p, LU, x, 1); }
 
 /* ------------------------------------------------------------------------ */
 /* 3D tensor algebra on x-fastest arrays u[(k*ny + j)*nx + i]                */
@@ -250,7 +263,7 @@ void or_lu_solve(int n, int p, const double *LU, double *x) { lu_solve_strided(n
 
 /* out = (A acting along `axis`) in, A dense na x na with band p.
  * This is the action of I(x)..(x)A(x)..(x)I on the vectorised tensor. */
-static void mode_apply(const int n[3], int axis, const double *A, int p, const double *in, double *out) {
+static void mode_apply(const int n[3], int axis, const real *A, int p, const real *in, real *out) {
     int na = n[axis];
     long stride = (axis == 0) ? 1 : (axis == 1) ? (long)n[0] : (long)n[0] * n[1];
     for (int k = 0; k < n[2]; ++k)
@@ -260,15 +273,15 @@ static void mode_apply(const int n[3], int axis, const double *A, int p, const d
                 int r = (axis == 0) ? i : (axis == 1) ? j : k;
                 long line0 = base - (long)r * stride;
                 int c0 = (r - p > 0) ? r - p : 0, c1 = (r + p < na - 1) ? r + p : na - 1;
-                double acc = 0.0;
+                real acc = 0.0;
                 for (int c = c0; c <= c1; ++c) acc += A[r * na + c] * in[line0 + (long)c * stride];
                 out[base] = acc;
             }
 }
 
 /* out += coef * (Ax (x) Ay (x) Az) in      (three mode products) */
-static void kron3_acc(const int n[3], int p, const double *Ax, const double *Ay, const double *Az,
-                      double coef, const double *in, double *out, double *t1, double *t2) {
+static void kron3_acc(const int n[3], int p, const real *Ax, const real *Ay, const real *Az,
+                      real coef, const real *in, real *out, real *t1, real *t2) {
     long N = (long)n[0] * n[1] * n[2];
     mode_apply(n, 0, Ax, p, in, t1);
     mode_apply(n, 1, Ay, p, t1, t2);
@@ -278,7 +291,7 @@ static void kron3_acc(const int n[3], int p, const double *Ax, const double *Ay,
 
 /* x <- (A_x (x) A_y (x) A_z)^{-1} x by the Appendix's three multi-RHS sweeps
  * (PAPER.md:533-618): solve along x for all (j,k), then y, then z. */
-static void kron3_solve(const int n[3], int p, double *const LU[3], double *x) {
+static void kron3_solve(const int n[3], int p, real *const LU[3], real *x) {
     for (int k = 0; k < n[2]; ++k)
         for (int j = 0; j < n[1]; ++j) lu_solve_strided(n[0], p, LU[0], x + ((long)k * n[1] + j) * n[0], 1);
     for (int k = 0; k < n[2]; ++k)
@@ -287,16 +300,16 @@ static void kron3_solve(const int n[3], int p, double *const LU[3], double *x) {
         for (int i = 0; i < n[0]; ++i) lu_solve_strided(n[2], p, LU[2], x + (long)j * n[0] + i, (long)n[0] * n[1]);
 }
 
-static double dot(long N, const double *a, const double *b) {
-    double s = 0.0;
+static real dot(long N, const real *a, const real *b) {
+    real s = 0.0;
     for (long q = 0; q < N; ++q) s += a[q] * b[q];
     return s;
 }
 
 /* Ricker wavelet R(t) = (1 - 2 pi^2 f0^2 (t-t0)^2) exp(-pi^2 f0^2 (t-t0)^2)  (C14) */
-double or_ricker(double t, double f0, double t0) {
-    const double pi = 3.14159265358979323846;
-    double a = pi * pi * f0 * f0 * (t - t0) * (t - t0);
+real or_ricker(real t, real f0, real t0) {
+    const real pi = (real)3.14159265358979323846264338327950288L;
+    real a = pi * pi * f0 * f0 * (t - t0) * (t - t0);
     return (1.0 - 2.0 * a) * exp(-a);
 }
 
@@ -306,14 +319,14 @@ double or_ricker(double t, double f0, double t0) {
 typedef struct {
     int n[3], nel[3], p, bc, scheme;   /* scheme 1 = R1 (default), 0 = literal Eq. 16 */
     int bcd[3];                        /* zero Dirichlet on direction d (the 2D axis has none) */
-    double tau, eta;
+    real tau, eta;
     long step;
-    double *M[3], *K[3], *A[3], *LU[3], *MDLU[3];
-    double *U, *V, *a;                 /* R1: V = V_{n+1/2}; R0: V = Udot_n; a = Udd_n */
-    double *src[3];
+    real *M[3], *K[3], *A[3], *LU[3], *MDLU[3];
+    real *U, *V, *a;                 /* R1: V = V_{n+1/2}; R0: V = Udot_n; a = Udd_n */
+    real *src[3];
     int has_src, wavelet;
-    double f0, t0, amp;
-    double *w1, *w2, *w3, *w4;
+    real f0, t0, amp;
+    real *w1, *w2, *w3, *w4;
 } or_pwave;
 
 static void pw_free(or_pwave *h) {
@@ -327,7 +340,7 @@ static void pw_free(or_pwave *h) {
 
 long or_pw_size(const or_pwave *h) { return (long)h->n[0] * h->n[1] * h->n[2]; }
 
-int or_pw_create(or_pwave **out, int nelx, int nely, int nelz, int p, double tau, int bc, int scheme) {
+int or_pw_create(or_pwave **out, int nelx, int nely, int nelz, int p, real tau, int bc, int scheme) {
     *out = NULL;
     /* nelz = 0: the 2D scheme as the paper prints it (Eqs. 14-16): a third axis
      * with one function, M_z = 1, K_z = 0 and no boundary, so that K = Kx(x)My + Mx(x)Ky and
@@ -342,32 +355,32 @@ int or_pw_create(or_pwave **out, int nelx, int nely, int nelz, int p, double tau
         h->nel[d] = nel[d]; h->n[d] = n;
         h->bcd[d] = nel[d] == 0 ? 0 : bc;
         if (h->bcd[d] == 1 && n < 3) { pw_free(h); return OR_E_INVAL; }
-        h->M[d] = (double *)malloc(sizeof(double) * n * n);
-        h->K[d] = (double *)malloc(sizeof(double) * n * n);
-        h->A[d] = (double *)malloc(sizeof(double) * n * n);
-        h->LU[d] = (double *)malloc(sizeof(double) * n * n);
-        h->MDLU[d] = (double *)malloc(sizeof(double) * n * n);
+        h->M[d] = (real *)malloc(sizeof(real) * n * n);
+        h->K[d] = (real *)malloc(sizeof(real) * n * n);
+        h->A[d] = (real *)malloc(sizeof(real) * n * n);
+        h->LU[d] = (real *)malloc(sizeof(real) * n * n);
+        h->MDLU[d] = (real *)malloc(sizeof(real) * n * n);
         or_matrices_1d(p, nel[d], bc, h->M[d], h->K[d], NULL);
         /* A_d = M_d + tau^2/4 K_d   (Eq. 16) */
         for (int q = 0; q < n * n; ++q) h->A[d][q] = h->M[d][q] + h->eta * h->K[d][q];
-        memcpy(h->MDLU[d], h->M[d], sizeof(double) * n * n);
+        memcpy(h->MDLU[d], h->M[d], sizeof(real) * n * n);
         if (h->bcd[d] == 1) {
             h->A[d][0] = 1.0; h->A[d][n * n - 1] = 1.0;
             h->MDLU[d][0] = 1.0; h->MDLU[d][n * n - 1] = 1.0;
         }
-        memcpy(h->LU[d], h->A[d], sizeof(double) * n * n);
+        memcpy(h->LU[d], h->A[d], sizeof(real) * n * n);
         int rc = or_banded_lu(n, p, h->LU[d]);
         if (rc == OR_OK) rc = or_banded_lu(n, p, h->MDLU[d]);
         if (rc != OR_OK) { pw_free(h); return rc; }
     }
     long N = or_pw_size(h);
-    h->U = (double *)calloc(N, sizeof(double));
-    h->V = (double *)calloc(N, sizeof(double));
-    h->a = (double *)calloc(N, sizeof(double));
-    h->w1 = (double *)calloc(N, sizeof(double));
-    h->w2 = (double *)calloc(N, sizeof(double));
-    h->w3 = (double *)calloc(N, sizeof(double));
-    h->w4 = (double *)calloc(N, sizeof(double));
+    h->U = (real *)calloc(N, sizeof(real));
+    h->V = (real *)calloc(N, sizeof(real));
+    h->a = (real *)calloc(N, sizeof(real));
+    h->w1 = (real *)calloc(N, sizeof(real));
+    h->w2 = (real *)calloc(N, sizeof(real));
+    h->w3 = (real *)calloc(N, sizeof(real));
+    h->w4 = (real *)calloc(N, sizeof(real));
     if (!h->U || !h->V || !h->a || !h->w1 || !h->w2 || !h->w3 || !h->w4) { pw_free(h); return OR_E_NOMEM; }
     *out = h;
     return OR_OK;
@@ -375,15 +388,15 @@ int or_pw_create(or_pwave **out, int nelx, int nely, int nelz, int p, double tau
 
 void or_pw_destroy(or_pwave *h) { pw_free(h); }
 
-int or_pw_set_source(or_pwave *h, const double *bx, const double *by, const double *bz,
-                     int wavelet, double f0, double t0, double amp) {
+int or_pw_set_source(or_pwave *h, const real *bx, const real *by, const real *bz,
+                     int wavelet, real f0, real t0, real amp) {
     for (int d = 0; d < 3; ++d) { free(h->src[d]); h->src[d] = NULL; }
     h->has_src = 0;
     if (!bx) return OR_OK;
-    const double *b[3] = {bx, by, bz};
+    const real *b[3] = {bx, by, bz};
     for (int d = 0; d < 3; ++d) {
-        h->src[d] = (double *)malloc(sizeof(double) * h->n[d]);
-        memcpy(h->src[d], b[d], sizeof(double) * h->n[d]);
+        h->src[d] = (real *)malloc(sizeof(real) * h->n[d]);
+        memcpy(h->src[d], b[d], sizeof(real) * h->n[d]);
         if (h->bcd[d] == 1) { h->src[d][0] = 0.0; h->src[d][h->n[d] - 1] = 0.0; }
     }
     h->has_src = 1; h->wavelet = wavelet; h->f0 = f0; h->t0 = t0; h->amp = amp;
@@ -391,7 +404,7 @@ int or_pw_set_source(or_pwave *h, const double *bx, const double *by, const doub
 }
 
 /* g(t) of F(t) = g(t) b_x(x)b_y(x)b_z */
-static double src_g(const or_pwave *h, double t) {
+static real src_g(const or_pwave *h, real t) {
     if (!h->has_src) return 0.0;
     if (h->wavelet == 1) return h->amp * or_ricker(t, h->f0, h->t0);
     return h->amp;
@@ -399,7 +412,7 @@ static double src_g(const or_pwave *h, double t) {
 
 /* out = F(t) - K P  (RHS of Eq. 14/16 with P = U + tau*Udot, 3D terms C5).
  * Dirichlet rows vanish because the 1D factors are interior-restricted. */
-static void pw_rhs(or_pwave *h, double t, const double *P, double *out) {
+static void pw_rhs(or_pwave *h, real t, const real *P, real *out) {
     const int *n = h->n;
     long N = or_pw_size(h);
     int p = h->p;
@@ -407,7 +420,7 @@ static void pw_rhs(or_pwave *h, double t, const double *P, double *out) {
     kron3_acc(n, p, h->K[0], h->M[1], h->M[2], -1.0, P, out, h->w3, h->w4);
     kron3_acc(n, p, h->M[0], h->K[1], h->M[2], -1.0, P, out, h->w3, h->w4);
     kron3_acc(n, p, h->M[0], h->M[1], h->K[2], -1.0, P, out, h->w3, h->w4);
-    double g = src_g(h, t);
+    real g = src_g(h, t);
     if (h->has_src && g != 0.0) {
         for (int k = 0; k < n[2]; ++k)
             for (int j = 0; j < n[1]; ++j)
@@ -417,7 +430,7 @@ static void pw_rhs(or_pwave *h, double t, const double *P, double *out) {
 }
 
 /* Unit operations exposed for kernel-level parity tests. */
-int or_pw_kapply(or_pwave *h, const double *P, double *out) {   /* out = K P */
+int or_pw_kapply(or_pwave *h, const real *P, real *out) {   /* out = K P */
     long N = or_pw_size(h);
     for (long q = 0; q < N; ++q) out[q] = 0.0;
     kron3_acc(h->n, h->p, h->K[0], h->M[1], h->M[2], 1.0, P, out, h->w3, h->w4);
@@ -425,27 +438,27 @@ int or_pw_kapply(or_pwave *h, const double *P, double *out) {   /* out = K P */
     kron3_acc(h->n, h->p, h->M[0], h->M[1], h->K[2], 1.0, P, out, h->w3, h->w4);
     return OR_OK;
 }
-int or_pw_dsolve(or_pwave *h, double *x) { kron3_solve(h->n, h->p, h->LU, x); return OR_OK; }  /* x <- D^-1 x */
-int or_pw_dapply(or_pwave *h, const double *x, double *out) {                              /* out = D x */
+int or_pw_dsolve(or_pwave *h, real *x) { kron3_solve(h->n, h->p, h->LU, x); return OR_OK; }  /* x <- D^-1 x */
+int or_pw_dapply(or_pwave *h, const real *x, real *out) {                              /* out = D x */
     long N = or_pw_size(h);
     for (long q = 0; q < N; ++q) out[q] = 0.0;
     kron3_acc(h->n, h->p, h->A[0], h->A[1], h->A[2], 1.0, x, out, h->w3, h->w4);
     return OR_OK;
 }
-int or_pw_mapply(or_pwave *h, const double *x, double *out) {                              /* out = M x */
+int or_pw_mapply(or_pwave *h, const real *x, real *out) {                              /* out = M x */
     long N = or_pw_size(h);
     for (long q = 0; q < N; ++q) out[q] = 0.0;
     kron3_acc(h->n, h->p, h->M[0], h->M[1], h->M[2], 1.0, x, out, h->w3, h->w4);
     return OR_OK;
 }
 /* x <- (M_x (x) M_y (x) M_z)^-1 x  (L2 projection solve) */
-int or_pw_msolve(or_pwave *h, double *x) { kron3_solve(h->n, h->p, h->MDLU, x); return OR_OK; }
+int or_pw_msolve(or_pwave *h, real *x) { kron3_solve(h->n, h->p, h->MDLU, x); return OR_OK; }
 
 /* Mass solve of a 1D vector in direction d (for separable L2 projections). */
-int or_pw_msolve_1d(or_pwave *h, int d, double *x) { or_lu_solve(h->n[d], h->p, h->MDLU[d], x); return OR_OK; }
+int or_pw_msolve_1d(or_pwave *h, int d, real *x) { or_lu_solve(h->n[d], h->p, h->MDLU[d], x); return OR_OK; }
 
 /* set_state: R1 half-kick start (C2): a0 = D^-1 (F(0) - K u0), V0 = udot0 + tau/2 a0. */
-int or_pw_set_state(or_pwave *h, const double *u, const double *udot) {
+int or_pw_set_state(or_pwave *h, const real *u, const real *udot) {
     long N = or_pw_size(h);
     const int *n = h->n;
     for (int k = 0; k < n[2]; ++k)
@@ -475,9 +488,9 @@ int or_pw_set_state(or_pwave *h, const double *u, const double *udot) {
  *     U' = U + tau Udot' - tau^2/2 Udd. */
 static void pw_step1(or_pwave *h) {
     long N = or_pw_size(h);
-    double tau = h->tau;
-    double t1 = (double)(h->step + 1) * tau;
-    double *P = h->w1;
+    real tau = h->tau;
+    real t1 = (real)(h->step + 1) * tau;
+    real *P = h->w1;
     for (long q = 0; q < N; ++q) P[q] = h->U[q] + tau * h->V[q];
     pw_rhs(h, t1, P, h->a);
     kron3_solve(h->n, h->p, h->LU, h->a);
@@ -488,7 +501,7 @@ static void pw_step1(or_pwave *h) {
         }
     } else {
         for (long q = 0; q < N; ++q) {
-            double vd = h->V[q] + 0.5 * tau * h->a[q];
+            real vd = h->V[q] + 0.5 * tau * h->a[q];
             h->U[q] = h->U[q] + tau * vd - 0.5 * tau * tau * h->a[q];
             h->V[q] = vd;
         }
@@ -503,7 +516,7 @@ int or_pw_step(or_pwave *h, int nsteps) {
 }
 
 /* get_state: U_n and udot_n = V_{n+1/2} - tau/2 a_n (R1); a_n.  Any pointer may be NULL. */
-int or_pw_get_state(or_pwave *h, double *u, double *udot, double *a) {
+int or_pw_get_state(or_pwave *h, real *u, real *udot, real *a) {
     long N = or_pw_size(h);
     for (long q = 0; q < N; ++q) {
         if (u) u[q] = h->U[q];
@@ -514,33 +527,33 @@ int or_pw_get_state(or_pwave *h, double *u, double *udot, double *a) {
 }
 
 /* Raw state (U, V as stored, a). */
-int or_pw_get_raw(or_pwave *h, double *U, double *V, double *a) {
+int or_pw_get_raw(or_pwave *h, real *U, real *V, real *a) {
     long N = or_pw_size(h);
-    if (U) memcpy(U, h->U, sizeof(double) * N);
-    if (V) memcpy(V, h->V, sizeof(double) * N);
-    if (a) memcpy(a, h->a, sizeof(double) * N);
+    if (U) memcpy(U, h->U, sizeof(real) * N);
+    if (V) memcpy(V, h->V, sizeof(real) * N);
+    if (a) memcpy(a, h->a, sizeof(real) * N);
     return OR_OK;
 }
 
-double or_pw_time(or_pwave *h) { return (double)h->step * h->tau; }
+real or_pw_time(or_pwave *h) { return (real)h->step * h->tau; }
 
 /* Energies (C6): out[0] kinetic 1/2 v'Mv with v = V - tau/2 a,
  * out[1] potential 1/2 U'KU, out[2] invariant 1/2 V'DV + 1/2 U_n' K U_{n+1}. */
-int or_pw_energy(or_pwave *h, double out[3]) {
+int or_pw_energy(or_pwave *h, real out[3]) {
     long N = or_pw_size(h);
-    double *v = h->w1, *Mv = h->w2;
+    real *v = h->w1, *Mv = h->w2;
     for (long q = 0; q < N; ++q) v[q] = (h->scheme == 1) ? h->V[q] - 0.5 * h->tau * h->a[q] : h->V[q];
     or_pw_mapply(h, v, Mv);
     out[0] = 0.5 * dot(N, v, Mv);
-    double *KU = h->w2;
+    real *KU = h->w2;
     or_pw_kapply(h, h->U, KU);
     out[1] = 0.5 * dot(N, h->U, KU);
     if (h->scheme == 1) {
-        double *DV = h->w1;
+        real *DV = h->w1;
         or_pw_dapply(h, h->V, DV);
-        double e = 0.5 * dot(N, h->V, DV);
+        real e = 0.5 * dot(N, h->V, DV);
         /* U_{n+1} = U_n + tau V */
-        double *P = h->w1;
+        real *P = h->w1;
         for (long q = 0; q < N; ++q) P[q] = h->U[q] + h->tau * h->V[q];
         or_pw_kapply(h, P, KU);
         out[2] = e + 0.5 * dot(N, h->U, KU);
@@ -551,10 +564,10 @@ int or_pw_energy(or_pwave *h, double out[3]) {
 }
 
 /* Dense 1D matrices of the handle (for tests): which 0=M 1=K 2=A 3=LU. */
-int or_pw_matrix(or_pwave *h, int d, int which, double *out) {
+int or_pw_matrix(or_pwave *h, int d, int which, real *out) {
     int n = h->n[d];
-    const double *src = which == 0 ? h->M[d] : which == 1 ? h->K[d] : which == 2 ? h->A[d] : h->LU[d];
-    memcpy(out, src, sizeof(double) * n * n);
+    const real *src = which == 0 ? h->M[d] : which == 1 ? h->K[d] : which == 2 ? h->A[d] : h->LU[d];
+    memcpy(out, src, sizeof(real) * n * n);
     return OR_OK;
 }
 
@@ -577,13 +590,13 @@ int or_pw_matrix(or_pwave *h, int d, int which, double *out) {
 /* ------------------------------------------------------------------------ */
 typedef struct {
     int n[3], p, bc;
-    double tau, lam, mu, rho;
+    real tau, lam, mu, rho;
     long step;
-    double *M[3], *K[3], *B[3], *BT[3];
-    double *SL[3], *SS[3];   /* LU of M_d + c K_d: SL with (2mu+lam), SS with mu */
-    double *MDLU[3];
-    double *U[3], *V[3], *z[3];
-    double *w[3], *r[3], *P[3], *t1, *t2, *t3;
+    real *M[3], *K[3], *B[3], *BT[3];
+    real *SL[3], *SS[3];   /* LU of M_d + c K_d: SL with (2mu+lam), SS with mu */
+    real *MDLU[3];
+    real *U[3], *V[3], *z[3];
+    real *w[3], *r[3], *P[3], *t1, *t2, *t3;
 } or_elastic;
 
 static void el_free(or_elastic *h) {
@@ -599,8 +612,8 @@ static void el_free(or_elastic *h) {
 
 long or_el_size(const or_elastic *h) { return (long)h->n[0] * h->n[1] * h->n[2]; }
 
-int or_el_create(or_elastic **out, int nelx, int nely, int nelz, int p, double tau, int bc,
-                 double lam, double mu, double rho) {
+int or_el_create(or_elastic **out, int nelx, int nely, int nelz, int p, real tau, int bc,
+                 real lam, real mu, real rho) {
     *out = NULL;
     if (p < 1 || p > 5 || nelx < 1 || nely < 1 || nelz < 1 || !(tau > 0.0) || (bc != 0 && bc != 1) ||
         !(mu > 0.0) || !(rho > 0.0) || !(lam >= 0.0))
@@ -608,17 +621,17 @@ int or_el_create(or_elastic **out, int nelx, int nely, int nelz, int p, double t
     or_elastic *h = (or_elastic *)calloc(1, sizeof(or_elastic));
     int nel[3] = {nelx, nely, nelz};
     h->p = p; h->bc = bc; h->tau = tau; h->lam = lam; h->mu = mu; h->rho = rho;
-    double cl = tau * tau / (4.0 * rho) * (2.0 * mu + lam), cs = tau * tau / (4.0 * rho) * mu;
+    real cl = tau * tau / (4.0 * rho) * (2.0 * mu + lam), cs = tau * tau / (4.0 * rho) * mu;
     for (int d = 0; d < 3; ++d) {
         int n = nel[d] + p;
         h->n[d] = n;
-        h->M[d] = (double *)malloc(sizeof(double) * n * n);
-        h->K[d] = (double *)malloc(sizeof(double) * n * n);
-        h->B[d] = (double *)malloc(sizeof(double) * n * n);
-        h->BT[d] = (double *)malloc(sizeof(double) * n * n);
-        h->SL[d] = (double *)malloc(sizeof(double) * n * n);
-        h->SS[d] = (double *)malloc(sizeof(double) * n * n);
-        h->MDLU[d] = (double *)malloc(sizeof(double) * n * n);
+        h->M[d] = (real *)malloc(sizeof(real) * n * n);
+        h->K[d] = (real *)malloc(sizeof(real) * n * n);
+        h->B[d] = (real *)malloc(sizeof(real) * n * n);
+        h->BT[d] = (real *)malloc(sizeof(real) * n * n);
+        h->SL[d] = (real *)malloc(sizeof(real) * n * n);
+        h->SS[d] = (real *)malloc(sizeof(real) * n * n);
+        h->MDLU[d] = (real *)malloc(sizeof(real) * n * n);
         or_matrices_1d(p, nel[d], bc, h->M[d], h->K[d], h->B[d]);
         for (int a = 0; a < n; ++a)
             for (int c = 0; c < n; ++c) h->BT[d][a * n + c] = h->B[d][c * n + a];
@@ -638,16 +651,16 @@ int or_el_create(or_elastic **out, int nelx, int nely, int nelz, int p, double t
     }
     long N = or_el_size(h);
     for (int c = 0; c < 3; ++c) {
-        h->U[c] = (double *)calloc(N, sizeof(double));
-        h->V[c] = (double *)calloc(N, sizeof(double));
-        h->z[c] = (double *)calloc(N, sizeof(double));
-        h->w[c] = (double *)calloc(N, sizeof(double));
-        h->r[c] = (double *)calloc(N, sizeof(double));
-        h->P[c] = (double *)calloc(N, sizeof(double));
+        h->U[c] = (real *)calloc(N, sizeof(real));
+        h->V[c] = (real *)calloc(N, sizeof(real));
+        h->z[c] = (real *)calloc(N, sizeof(real));
+        h->w[c] = (real *)calloc(N, sizeof(real));
+        h->r[c] = (real *)calloc(N, sizeof(real));
+        h->P[c] = (real *)calloc(N, sizeof(real));
     }
-    h->t1 = (double *)calloc(N, sizeof(double));
-    h->t2 = (double *)calloc(N, sizeof(double));
-    h->t3 = (double *)calloc(N, sizeof(double));
+    h->t1 = (real *)calloc(N, sizeof(real));
+    h->t2 = (real *)calloc(N, sizeof(real));
+    h->t3 = (real *)calloc(N, sizeof(real));
     *out = h;
     return OR_OK;
 }
@@ -655,11 +668,11 @@ int or_el_create(or_elastic **out, int nelx, int nely, int nelz, int p, double t
 void or_el_destroy(or_elastic *h) { el_free(h); }
 
 /* out += coef * Ups_ik in   (block (i,k) of the elasticity operator) */
-static void el_block_acc(or_elastic *h, int i, int k, double coef, const double *in, double *out) {
-    const double *F[3];
+static void el_block_acc(or_elastic *h, int i, int k, real coef, const real *in, real *out) {
+    const real *F[3];
     if (i == k) {
         for (int d = 0; d < 3; ++d) {
-            double c = (d == i) ? (2.0 * h->mu + h->lam) : h->mu;
+            real c = (d == i) ? (2.0 * h->mu + h->lam) : h->mu;
             for (int e = 0; e < 3; ++e) F[e] = (e == d) ? h->K[e] : h->M[e];
             kron3_acc(h->n, h->p, F[0], F[1], F[2], coef * c, in, out, h->t1, h->t2);
         }
@@ -674,7 +687,7 @@ static void el_block_acc(or_elastic *h, int i, int k, double coef, const double 
 }
 
 /* out_i = sum_k Ups_ik in_k  (component-major arrays of 3N) */
-int or_el_apply(or_elastic *h, const double *in, double *out) {
+int or_el_apply(or_elastic *h, const real *in, real *out) {
     long N = or_el_size(h);
     for (int i = 0; i < 3; ++i) {
         for (long q = 0; q < N; ++q) out[i * N + q] = 0.0;
@@ -683,8 +696,8 @@ int or_el_apply(or_elastic *h, const double *in, double *out) {
     return OR_OK;
 }
 
-static void el_S_solve(or_elastic *h, int i, double *x) {
-    double *LU[3];
+static void el_S_solve(or_elastic *h, int i, real *x) {
+    real *LU[3];
     for (int d = 0; d < 3; ++d) LU[d] = (d == i) ? h->SL[d] : h->SS[d];
     kron3_solve(h->n, h->p, LU, x);
     long N = or_el_size(h);
@@ -692,19 +705,19 @@ static void el_S_solve(or_elastic *h, int i, double *x) {
 }
 
 /* x <- D~^-1 x with D~ = L~ (rho M)^-1 L~^T  (3N, component-major) */
-static void el_dsolve_comp(or_elastic *h, double *const x[3]) {
+static void el_dsolve_comp(or_elastic *h, real *const x[3]) {
     long N = or_el_size(h);
-    double hh = 0.5 * h->tau * h->tau;
+    real hh = 0.5 * h->tau * h->tau;
     /* predictor: S_i w_i = x_i - tau^2/2 sum_{j<i} Ups_ij w_j */
     for (int i = 0; i < 3; ++i) {
-        double *wi = h->w[i];
-        memcpy(wi, x[i], sizeof(double) * N);
+        real *wi = h->w[i];
+        memcpy(wi, x[i], sizeof(real) * N);
         for (int j = 0; j < i; ++j) el_block_acc(h, i, j, -hh, h->w[j], wi);
         el_S_solve(h, i, wi);
     }
     /* corrector: S_i z_i = rho M w_i - tau^2/2 sum_{j>i} Ups_ij z_j */
     for (int i = 2; i >= 0; --i) {
-        double *zi = x[i];
+        real *zi = x[i];
         for (long q = 0; q < N; ++q) zi[q] = 0.0;
         kron3_acc(h->n, h->p, h->M[0], h->M[1], h->M[2], h->rho, h->w[i], zi, h->t1, h->t2);
         for (int j = i + 1; j < 3; ++j) el_block_acc(h, i, j, -hh, x[j], zi);
@@ -712,15 +725,15 @@ static void el_dsolve_comp(or_elastic *h, double *const x[3]) {
     }
 }
 
-int or_el_dsolve(or_elastic *h, double *x) {
+int or_el_dsolve(or_elastic *h, real *x) {
     long N = or_el_size(h);
-    double *xs[3] = {x, x + N, x + 2 * N};
+    real *xs[3] = {x, x + N, x + 2 * N};
     el_dsolve_comp(h, xs);
     return OR_OK;
 }
 
 /* set_state with the half-kick start (C13): V0 = udot0 + tau/2 D~^-1 (f(0) - Ups U0), f = 0. */
-int or_el_set_state(or_elastic *h, const double *u, const double *udot) {
+int or_el_set_state(or_elastic *h, const real *u, const real *udot) {
     long N = or_el_size(h);
     const int *n = h->n;
     for (int c = 0; c < 3; ++c)
@@ -745,7 +758,7 @@ int or_el_set_state(or_elastic *h, const double *u, const double *udot) {
 
 int or_el_step(or_elastic *h, int nsteps) {
     long N = or_el_size(h);
-    double tau = h->tau;
+    real tau = h->tau;
     for (int s = 0; s < nsteps; ++s) {
         for (int c = 0; c < 3; ++c)
             for (long q = 0; q < N; ++q) h->P[c][q] = h->U[c][q] + tau * h->V[c][q];
@@ -764,7 +777,7 @@ int or_el_step(or_elastic *h, int nsteps) {
     return OR_OK;
 }
 
-int or_el_get_state(or_elastic *h, double *u, double *udot, double *a) {
+int or_el_get_state(or_elastic *h, real *u, real *udot, real *a) {
     long N = or_el_size(h);
     for (int c = 0; c < 3; ++c)
         for (long q = 0; q < N; ++q) {
@@ -777,19 +790,19 @@ int or_el_get_state(or_elastic *h, double *u, double *udot, double *a) {
 
 /* Energies: kinetic 1/2 rho v'Mv, potential 1/2 U'Ups U,
  * invariant 1/2 V'D~V + 1/2 U_n' Ups U_{n+1}  with D~ = L~ (rho M)^-1 L~^T. */
-int or_el_energy(or_elastic *h, double out[3]) {
+int or_el_energy(or_elastic *h, real out[3]) {
     long N = or_el_size(h);
-    double *v = (double *)malloc(sizeof(double) * 3 * N);
-    double *y = (double *)malloc(sizeof(double) * 3 * N);
-    double *U = (double *)malloc(sizeof(double) * 3 * N);
-    double *P = (double *)malloc(sizeof(double) * 3 * N);
+    real *v = (real *)malloc(sizeof(real) * 3 * N);
+    real *y = (real *)malloc(sizeof(real) * 3 * N);
+    real *U = (real *)malloc(sizeof(real) * 3 * N);
+    real *P = (real *)malloc(sizeof(real) * 3 * N);
     for (int c = 0; c < 3; ++c)
         for (long q = 0; q < N; ++q) {
             v[c * N + q] = h->V[c][q] - 0.5 * h->tau * h->z[c][q];
             U[c * N + q] = h->U[c][q];
             P[c * N + q] = h->U[c][q] + h->tau * h->V[c][q];
         }
-    double ek = 0.0;
+    real ek = 0.0;
     for (int c = 0; c < 3; ++c) {
         for (long q = 0; q < N; ++q) h->t3[q] = 0.0;
         kron3_acc(h->n, h->p, h->M[0], h->M[1], h->M[2], h->rho, v + c * N, h->t3, h->t1, h->t2);
@@ -799,22 +812,22 @@ int or_el_energy(or_elastic *h, double out[3]) {
     or_el_apply(h, U, y);
     out[1] = 0.5 * dot(3 * N, U, y);
     /* V' D~ V = (L~^T V)' (rho M)^-1 (L~^T V) */
-    double hh = 0.5 * h->tau * h->tau;
-    double inv = 0.0;
+    real hh = 0.5 * h->tau * h->tau;
+    real inv = 0.0;
     for (int i = 0; i < 3; ++i) {
-        double *g = y + i * N;   /* g_i = S_i V_i + tau^2/2 sum_{j>i} Ups_ij V_j */
+        real *g = y + i * N;   /* g_i = S_i V_i + tau^2/2 sum_{j>i} Ups_ij V_j */
         for (long q = 0; q < N; ++q) g[q] = 0.0;
         /* S_i V_i: rho (x)_d (M_d + c_{i,d} K_d) applied as a Kronecker product */
         {
-            double cl = h->tau * h->tau / (4.0 * h->rho) * (2.0 * h->mu + h->lam);
-            double cs = h->tau * h->tau / (4.0 * h->rho) * h->mu;
+            real cl = h->tau * h->tau / (4.0 * h->rho) * (2.0 * h->mu + h->lam);
+            real cs = h->tau * h->tau / (4.0 * h->rho) * h->mu;
             int n0 = h->n[0], n1 = h->n[1], n2 = h->n[2];
-            double *Sd[3];
+            real *Sd[3];
             int nn[3] = {n0, n1, n2};
             for (int d = 0; d < 3; ++d) {
                 int n = nn[d];
-                Sd[d] = (double *)malloc(sizeof(double) * n * n);
-                double c = (d == i) ? cl : cs;
+                Sd[d] = (real *)malloc(sizeof(real) * n * n);
+                real c = (d == i) ? cl : cs;
                 for (int q = 0; q < n * n; ++q) Sd[d][q] = h->M[d][q] + c * h->K[d][q];
                 if (h->bc == 1) { Sd[d][0] = 1.0; Sd[d][n * n - 1] = 1.0; }
             }
@@ -822,7 +835,7 @@ int or_el_energy(or_elastic *h, double out[3]) {
             for (int d = 0; d < 3; ++d) free(Sd[d]);
         }
         for (int j = i + 1; j < 3; ++j) el_block_acc(h, i, j, hh, h->V[j], g);
-        memcpy(h->t3, g, sizeof(double) * N);
+        memcpy(h->t3, g, sizeof(real) * N);
         kron3_solve(h->n, h->p, h->MDLU, h->t3);
         for (long q = 0; q < N; ++q) h->t3[q] /= h->rho;
         inv += dot(N, g, h->t3);
@@ -833,4 +846,4 @@ int or_el_energy(or_elastic *h, double out[3]) {
     return OR_OK;
 }
 
-double or_el_time(or_elastic *h) { return (double)h->step * h->tau; }
+real or_el_time(or_elastic *h) { return (real)h->step * h->tau; }

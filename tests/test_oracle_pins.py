@@ -496,3 +496,102 @@ def test_2d_stepping_vs_modal_closed_form(forced):
         mu, mud, ma = m.run(u0, nsteps=wl.steps)
     for a, b in zip(o.get_state(), (mu, mud, ma)):
         assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)
+
+
+# ----------------------------------------------------------------- source pieces (C14)
+def test_ricker_closed_form_properties():
+    """or_ricker (the source of BASELINE configs[2]; reading C14) against properties of the Ricker
+    ("Mexican hat") wavelet that do not depend on how its formula is typed: peak 1 at t0, symmetric
+    about t0, zeros at t0 +- 1/(sqrt(2) pi f0), troughs -2 exp(-3/2) at t0 +- sqrt(3/2)/(pi f0),
+    zero mean; and c3's start value R(0) with f0 t0 = 1, i.e. (1 - 2 pi^2) exp(-pi^2) = -9.69e-4
+    (SURVEY.md §8(d)).  Catches a wrong constant (pi vs 2 pi, sigma convention), sign or centre."""
+    from scipy.integrate import quad
+    for f0, t0 in [(25.0, 0.04), (10.0, 0.02), (3.0, 0.7)]:
+        assert oracle.ricker(t0, f0, t0) == 1.0
+        z = 1.0 / (math.sqrt(2.0) * math.pi * f0)
+        tr = math.sqrt(1.5) / (math.pi * f0)
+        for s in (-1.0, 1.0):
+            assert abs(oracle.ricker(t0 + s * z, f0, t0)) < 1e-15
+            assert abs(oracle.ricker(t0 + s * tr, f0, t0) + 2.0 * math.exp(-1.5)) < 1e-15
+        for dt in (0.1 * z, 0.7 * z, 2.3 * z):
+            assert oracle.ricker(t0 + dt, f0, t0) == pytest.approx(oracle.ricker(t0 - dt, f0, t0), rel=1e-14)
+        # minimum over a fine grid is the trough (no lower value anywhere)
+        ts = t0 + np.linspace(-5 * z, 5 * z, 4001)
+        assert min(oracle.ricker(t, f0, t0) for t in ts) >= -2.0 * math.exp(-1.5) - 1e-15
+        span = 12.0 / f0
+        area, _ = quad(lambda t: oracle.ricker(t, f0, t0), t0 - span, t0 + span, points=[t0], limit=200)
+        assert abs(area) < 1e-10 / f0
+    g = _gold("ricker_c3.json")
+    r0 = (1.0 - 2.0 * math.pi ** 2) * math.exp(-math.pi ** 2)
+    assert abs(r0 - g["R0"]) < 5e-8          # the survey's printed value, 4 digits
+    assert abs(oracle.ricker(0.0, 25.0, 0.04) - r0) < 1e-17
+    # the peak of the c3 source falls on step t0 / tau = 40
+    assert oracle.ricker(40 * 1e-3, 25.0, 0.04) == 1.0
+
+
+@pytest.mark.parametrize("p,nel,bc", [(1, 24, 0), (2, 64, 1), (3, 40, 1), (3, 13, 0), (5, 30, 0)])
+def test_load_vector_vs_adaptive_quadrature(p, nel, bc):
+    """or_load_1d, b_a = int f N_a (the L2-projection right-hand side; reading C4: 8
+    Gauss points per element) against scipy's adaptive quad of f times the scipy BSpline basis
+    function over its support, for the Gaussian of c2-c5 (several centres and widths, incl. c3's
+    sigma = 0.02) and sin(pi x) of c1.  Catches a wrong normalisation (2 sigma^2 vs sigma^2), a
+    shifted centre, a wrong basis index or element map, and the Dirichlet end handling."""
+    from scipy.integrate import quad
+    from scipy.interpolate import BSpline
+    from pins_util import open_knots
+    t = open_knots(p, nel)
+    n = nel + p
+    brk = np.linspace(0.0, 1.0, nel + 1)
+    funcs = [("sin",), ("gauss", 0.5, 0.05), ("gauss", 0.3, 0.02), ("gauss", 0.71, 0.13)]
+    # the 8-point rule (C4) integrates f N_a to rounding only where f is resolved, h <= sigma
+    funcs = [fn for fn in funcs if fn[0] == "sin" or fn[2] * nel >= 1.0]
+    for fn in funcs:
+        f = (lambda x: math.sin(math.pi * x)) if fn[0] == "sin" else \
+            (lambda x, c=fn[1], s=fn[2]: math.exp(-(x - c) ** 2 / (2.0 * s * s)))
+        b = oracle.load_1d(p, nel, bc, fn)
+        ref = np.zeros(n)
+        for a in range(n):
+            Na = BSpline(t, np.eye(n)[a], p, extrapolate=False)
+            lo, hi = t[a], t[a + p + 1]
+            pts = [x for x in brk if lo < x < hi]
+            ref[a] = quad(lambda x: f(x) * float(np.nan_to_num(Na(x))), lo, hi, points=pts or None,
+                          limit=400, epsabs=1e-16, epsrel=1e-14)[0]
+        if bc == 1:
+            ref[0] = ref[-1] = 0.0
+        scale = np.abs(ref).max()
+        # 8-point Gauss on a degree-p polynomial times an analytic f: error ~ (h/sigma)^16
+        assert np.abs(b - ref).max() <= 2e-12 * scale, (fn, np.abs(b - ref).max() / scale)
+
+
+def test_extended_precision_oracle_rows_and_agreement():
+    """The extended-precision build (libads_oracle_ld.so, the truth reference of DESIGN.md T1) is
+    the same algorithm: its interior Gram rows equal the exact rational cardinal values to
+    long-double accuracy (the fp64 build only to ~1e-13 relative), and one step of c2's recipe
+    agrees with the fp64 build to fp64 rounding."""
+    from fractions import Fraction
+    if np.finfo(np.longdouble).eps >= 1e-17:
+        pytest.skip("long double is not extended precision on this platform")
+    g = _gold("cardinal_rows.json")
+    for p, nel in [(2, 16), (3, 32)]:
+        s = oracle.PWave((nel, 4, 4), p, 1e-3, bc=0, ext=True)
+        M, K = s.matrix(0, 0), s.matrix(0, 1)
+        row = nel // 2
+        (_, mv), (_, kv) = list(g[f"p{p}"].items())
+        msc, ksc = (120, 6) if p == 2 else (5040, 120)
+        for k in range(-p, p + 1):
+            exm = Fraction(mv[k + p], msc * nel)                 # h [..] / scale
+            exk = Fraction(kv[k + p] * nel, ksc)                 # [..] / (scale h)
+            # np.longdouble -> exact rational through its decimal repr (21 significant digits)
+            gm = Fraction(np.format_float_scientific(M[row, row + k], unique=True))
+            gk = Fraction(np.format_float_scientific(K[row, row + k], unique=True))
+            assert abs(gm - exm) <= abs(exm) * Fraction(1, 10 ** 17)
+            assert abs(gk - exk) <= abs(exk) * Fraction(1, 10 ** 17)
+    wl = workloads.get("c2").scaled(20, 1)
+    u0 = oracle.project_separable(wl)
+    a = oracle.PWave(wl.nel, wl.p, wl.tau, wl.bc)
+    b = oracle.PWave(wl.nel, wl.p, wl.tau, wl.bc, ext=True)
+    for s in (a, b):
+        s.set_state(u0)
+        s.step(1)
+    for x, y in zip(a.get_state(), b.get_state()):
+        assert rel_l2(x, np.asarray(y, dtype=np.float64)) < 1e-13
