@@ -131,16 +131,18 @@ def matrices_1d(p, nel, bc=0):
     return M, K, B
 
 
-def load_1d(p, nel, bc, func):
-    """b_a = int f N_a for a workloads.Func1D descriptor (nel = 0: the 2D scheme's third axis, [1])."""
+def load_1d(p, nel, bc, func, ext=False):
+    """b_a = int f N_a for a workloads.Func1D descriptor (nel = 0: the 2D scheme's third axis, [1]);
+    ext: computed by the extended-precision build (returned as np.longdouble)."""
+    dt = np.longdouble if ext else np.float64
     if nel == 0:
-        return np.ones(1)
+        return np.ones(1, dt)
     n = nel + p
-    b = np.zeros(n)
+    b = np.zeros(n, dt)
     if func[0] == "sin":
-        _check(lib().or_load_1d(p, nel, bc, 0, 0.0, 1.0, _ptr(b)))
+        _check(lib(ext).or_load_1d(p, nel, bc, 0, 0.0, 1.0, _ptr(b)))
     elif func[0] == "gauss":
-        _check(lib().or_load_1d(p, nel, bc, 1, float(func[1]), float(func[2]), _ptr(b)))
+        _check(lib(ext).or_load_1d(p, nel, bc, 1, float(func[1]), float(func[2]), _ptr(b)))
     else:
         raise ValueError(func)
     return b
@@ -330,21 +332,33 @@ def project_separable(wl, terms=None):
     return u if wl.elastic else u[0]
 
 
-def source_vectors(wl):
+def source_vectors(wl, ext=False):
     if wl.source is None:
         return None
-    return [load_1d(wl.p, wl.nel[d], wl.bc, wl.source.f[d]) for d in range(3)]
+    return [load_1d(wl.p, wl.nel[d], wl.bc, wl.source.f[d], ext) for d in range(3)]
 
 
-def make_solver(wl, scheme=1):
-    """Oracle solver for a workloads.Workload with its initial state and source set."""
+def make_solver(wl, scheme=1, ext=False, u0=None):
+    """Oracle solver for a workloads.Workload with its initial state and source set (ext: the
+    extended-precision build; u0: start from these coefficients instead of the projection)."""
+    u0 = project_separable(wl) if u0 is None else u0
     if wl.elastic:
-        s = Elastic(wl.nel, wl.p, wl.tau, wl.bc, wl.lam, wl.mu, wl.rho)
-        s.set_state(project_separable(wl))
+        s = Elastic(wl.nel, wl.p, wl.tau, wl.bc, wl.lam, wl.mu, wl.rho, ext=ext)
+        s.set_state(u0)
         return s
-    s = PWave(wl.nel, wl.p, wl.tau, wl.bc, scheme)
+    s = PWave(wl.nel, wl.p, wl.tau, wl.bc, scheme, ext=ext)
     if wl.source is not None:
         src = wl.source
-        s.set_source(source_vectors(wl), src.wavelet, src.f0, src.t0, src.amp)
-    s.set_state(project_separable(wl))
+        s.set_source(source_vectors(wl, ext), src.wavelet, src.f0, src.t0, src.amp)
+    s.set_state(u0)
     return s
+
+
+def one_step_truth(wl, u0=None):
+    """(u, udot, a) after one step of the extended-precision oracle, as fp64 arrays: the truth
+    the GPU's one-step bound is measured against (north_star 1e-12; T1)."""
+    s = make_solver(wl, ext=True, u0=u0)
+    s.step(1)
+    out = tuple(np.asarray(x, dtype=np.float64) for x in s.get_state())
+    del s
+    return out

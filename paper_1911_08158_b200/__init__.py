@@ -317,9 +317,10 @@ def project_1d(solver, func, d):
     return solver.mass_solve_1d(d, solver.load_vector(d, func))
 
 
-def make_solver(wl, dist=None, virtual_slabs=0):
-    """Solver for a workloads.Workload with its initial state and source set (library-side projection).
-    dist=(rank, world, uid): this process's z-slab; virtual_slabs=G: all G slabs on this device."""
+def make_solver(wl, dist=None, virtual_slabs=0, u0=None):
+    """Solver for a workloads.Workload with its initial state and source set (library-side projection,
+    or the given coefficients u0).  dist=(rank, world, uid): this process's z-slab;
+    virtual_slabs=G: all G slabs on this device."""
     s = Solver(wl.nel, wl.p, wl.tau, wl.bc, elastic=wl.elastic, lam=wl.lam, mu=wl.mu, rho=wl.rho, dist=dist,
                virtual_slabs=virtual_slabs)
     if wl.source is not None:
@@ -327,7 +328,9 @@ def make_solver(wl, dist=None, virtual_slabs=0):
         b = [s.load_vector(d, src.f[d]) for d in range(3)]
         s.set_source(b, src.wavelet, src.f0, src.t0, src.amp)
     terms = wl.u0
-    if terms:
+    if u0 is not None:
+        s.set_state(u0)
+    elif terms:
         sx = np.concatenate([project_1d(s, t.f[0], 0) for t in terms])
         sy = np.concatenate([project_1d(s, t.f[1], 1) for t in terms])
         sz = np.concatenate([project_1d(s, t.f[2], 2) for t in terms])

@@ -26,6 +26,8 @@ namespace {
 struct DirDev {
     double *mband = nullptr, *kband = nullptr, *aband = nullptr;  // [n][2p+1]
     double *bband = nullptr, *btband = nullptr;                    // elasticity: B, B^T
+    double *wzband = nullptr;                                      // K in difference form [n][2p]
+    double wzrow[2 * kMaxP] = {};                                  // its Toeplitz interior row
     double *slband = nullptr, *ssband = nullptr;                   // elasticity: M + c K (apply)
     int t_lo = 1, t_hi = 0;  // rows [t_lo, t_hi] of M, K are the Toeplitz row (mrow, krow)
     double mrow[2 * kMaxP + 1] = {}, krow[2 * kMaxP + 1] = {};
@@ -407,8 +409,11 @@ int build_direction(ads_ctx *h, int d) {
             (rc = upload(h, &D.slband, SLa.v)) || (rc = upload(h, &D.ssband, SSa.v)))
             return rc;
     }
-    std::vector<double> mb(s.M.v), kb(s.K.v);
-    if ((rc = upload(h, &D.mband, mb)) || (rc = upload(h, &D.kband, kb))) return rc;
+    std::vector<double> mb(s.M.v), kb(s.K.v), wz;
+    diff_weights(s, wz);
+    if (D.t_hi > D.t_lo)
+        for (int m = 0; m < 2 * p; ++m) D.wzrow[m] = wz[(size_t)D.t_lo * 2 * p + m];
+    if ((rc = upload(h, &D.mband, mb)) || (rc = upload(h, &D.kband, kb)) || (rc = upload(h, &D.wzband, wz))) return rc;
     return ADS_OK;
 }
 
@@ -465,8 +470,16 @@ int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g
             a.kc[d][c] = a.kw[d] * h->dd[d].krow[c];
         }
     }
+    a.wz = h->dd[2].wzband;
+    if (h->sp[2].bc == ADS_BC_DIRICHLET0) {
+        a.zd0 = 0;
+        a.zd1 = h->ngz - 1;
+    }
+    for (int m = 0; m < 2 * h->p; ++m) a.wzc[m] = a.kw[2] * h->dd[2].wzrow[m];
     ProfScope ps(h, 0);
-    if (launch_kop(h->p, a, h->stream)) return fail(h, ADS_E_INVAL, "kop: unsupported p");
+    const int lr = launch_kop(h->p, a, h->stream);
+    if (lr == -2) return fail(h, ADS_E_CUDA, "kop: TMA descriptor encoding failed");
+    if (lr) return fail(h, ADS_E_INVAL, "kop: unsupported p");
     return check_launch(h, "kop");
 }
 

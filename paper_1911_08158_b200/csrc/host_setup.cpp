@@ -7,58 +7,76 @@
 
 namespace ads {
 
+// The 1D Gram matrices and load vectors are accumulated in extended precision (x87 long double,
+// 64-bit significand) and rounded to fp64 once: quadrature in fp64 leaves entries ~1e-13 off in
+// relative terms, and the stiffness rows' rounding error is amplified by (sigma/h)^2 in K P on
+// smooth data (T1).  Host work, once per handle.
+using xreal = long double;
+
 // Gauss-Legendre nodes/weights on [-1,1]: Newton iteration on P_m using the
 // Bonnet recurrence (j+1) P_{j+1} = (2j+1) x P_j - j P_{j-1};
 // w = 2 / ((1 - x^2) P_m'(x)^2).
-int gauss_legendre(int m, double *x, double *w) {
-    const double kPi = 3.141592653589793238462643383;
+template <class T>
+static void gauss_legendre_t(int m, T *x, T *w) {
+    const T kPi = 3.14159265358979323846264338327950288L;
     for (int i = 0; i < (m + 1) / 2; ++i) {
-        double z = std::cos(kPi * (i + 0.75) / (m + 0.5));
-        double pm = 0, dpm = 0;
+        T z = std::cos(kPi * (T)(i + 0.75) / (T)(m + 0.5));
+        T pm = 0, dpm = 0;
         for (int it = 0; it < 64; ++it) {
-            double pjm1 = 0.0, pj = 1.0;
+            T pjm1 = 0.0, pj = 1.0;
             for (int j = 0; j < m; ++j) {
-                double pjp1 = ((2.0 * j + 1.0) * z * pj - j * pjm1) / (j + 1.0);
+                T pjp1 = ((2 * j + 1) * z * pj - j * pjm1) / (T)(j + 1);
                 pjm1 = pj;
                 pj = pjp1;
             }
             pm = pj;
-            dpm = m * (z * pj - pjm1) / (z * z - 1.0);
-            double dz = pm / dpm;
+            dpm = m * (z * pj - pjm1) / (z * z - 1);
+            T dz = pm / dpm;
             z -= dz;
-            if (std::fabs(dz) <= 1e-17) break;
+            if (std::fabs(dz) <= std::numeric_limits<T>::epsilon() * 0.25) break;
         }
         {
-            double pjm1 = 0.0, pj = 1.0;
+            T pjm1 = 0.0, pj = 1.0;
             for (int j = 0; j < m; ++j) {
-                double pjp1 = ((2.0 * j + 1.0) * z * pj - j * pjm1) / (j + 1.0);
+                T pjp1 = ((2 * j + 1) * z * pj - j * pjm1) / (T)(j + 1);
                 pjm1 = pj;
                 pj = pjp1;
             }
-            dpm = m * (z * pj - pjm1) / (z * z - 1.0);
+            dpm = m * (z * pj - pjm1) / (z * z - 1);
         }
-        double wi = 2.0 / ((1.0 - z * z) * dpm * dpm);
+        T wi = 2 / ((1 - z * z) * dpm * dpm);
         x[i] = -z;
         x[m - 1 - i] = z;
         w[i] = w[m - 1 - i] = wi;
     }
-    if (m % 2 == 1) x[m / 2] = 0.0;
+    if (m % 2 == 1) x[m / 2] = 0;
+}
+
+int gauss_legendre(int m, double *x, double *w) {
+    xreal xl[64], wl[64];
+    if (m < 1 || m > 64) return -1;
+    gauss_legendre_t<xreal>(m, xl, wl);
+    for (int i = 0; i < m; ++i) {
+        x[i] = (double)xl[i];
+        w[i] = (double)wl[i];
+    }
     return 0;
 }
 
 // de Boor's triangular evaluation of the p+1 nonzero B-splines and their first
 // derivatives in knot span `span` (t[span] <= x < t[span+1]).
-void basis_and_derivs(const std::vector<double> &t, int p, int span, double x, double *N, double *dN) {
-    double ndu[8][8];
-    double left[8], right[8];
-    ndu[0][0] = 1.0;
+template <class T>
+static void basis_and_derivs_t(const T *t, int p, int span, T x, T *N, T *dN) {
+    T ndu[8][8];
+    T left[8], right[8];
+    ndu[0][0] = 1;
     for (int j = 1; j <= p; ++j) {
         left[j] = x - t[span + 1 - j];
         right[j] = t[span + j] - x;
-        double saved = 0.0;
+        T saved = 0;
         for (int r = 0; r < j; ++r) {
             ndu[j][r] = right[r + 1] + left[j - r];      // lower triangle: knot differences
-            double tmp = ndu[r][j - 1] / ndu[j][r];
+            T tmp = ndu[r][j - 1] / ndu[j][r];
             ndu[r][j] = saved + right[r + 1] * tmp;      // upper triangle: basis values
             saved = left[j - r] * tmp;
         }
@@ -67,11 +85,22 @@ void basis_and_derivs(const std::vector<double> &t, int p, int span, double x, d
     for (int r = 0; r <= p; ++r) N[r] = ndu[r][p];
     // first derivative: N'_{r} = p (N_{r,p-1}/(t_{r+p}-t_r) - N_{r+1,p-1}/(t_{r+p+1}-t_{r+1}))
     for (int r = 0; r <= p; ++r) {
-        double d = 0.0;
+        T d = 0;
         if (r >= 1) d += ndu[r - 1][p - 1] / ndu[p][r - 1];
         if (r <= p - 1) d -= ndu[r][p - 1] / ndu[p][r];
         dN[r] = p * d;
     }
+}
+
+void basis_and_derivs(const std::vector<double> &t, int p, int span, double x, double *N, double *dN) {
+    basis_and_derivs_t<double>(t.data(), p, span, x, N, dN);
+}
+
+// open uniform knots in extended precision: t_i = e / nel
+static std::vector<xreal> knots_x(int p, int nel) {
+    std::vector<xreal> t(nel + 2 * p + 1);
+    for (int i = 0; i < (int)t.size(); ++i) t[i] = (xreal)std::min(std::max(i - p, 0), nel) / (xreal)nel;
+    return t;
 }
 
 int build_space(int p, int nel, int bc, Space1D &s) {
@@ -80,37 +109,42 @@ int build_space(int p, int nel, int bc, Space1D &s) {
     s.nel = nel;
     s.n = nel + p;
     s.bc = bc;
-    s.knots.assign(nel + 2 * p + 1, 0.0);
-    for (int i = 0; i < (int)s.knots.size(); ++i) {
-        int e = std::min(std::max(i - p, 0), nel);
-        s.knots[i] = (double)e / nel;
-    }
+    const std::vector<xreal> tx = knots_x(p, nel);
+    s.knots.assign(tx.size(), 0.0);
+    for (size_t i = 0; i < tx.size(); ++i) s.knots[i] = (double)tx[i];
     s.M = Band(s.n, p);
     s.K = Band(s.n, p);
     s.B = Band(s.n, p);
-    double xg[8], wg[8];
-    gauss_legendre(p + 1, xg, wg);
-    double N[8], dN[8];
+    const int W = 2 * p + 1;
+    std::vector<xreal> Mx((size_t)s.n * W, 0), Kx((size_t)s.n * W, 0), Bx((size_t)s.n * W, 0);
+    xreal xg[8], wg[8];
+    gauss_legendre_t<xreal>(p + 1, xg, wg);
+    xreal N[8], dN[8];
     for (int e = 0; e < nel; ++e) {
         int span = e + p;
-        double a = s.knots[span], b = s.knots[span + 1];
-        double half = 0.5 * (b - a), mid = 0.5 * (a + b);
+        xreal a = tx[span], b = tx[span + 1];
+        xreal half = (b - a) / 2, mid = (a + b) / 2;
         for (int q = 0; q <= p; ++q) {
-            double x = mid + half * xg[q], w = half * wg[q];
-            basis_and_derivs(s.knots, p, span, x, N, dN);
+            xreal x = mid + half * xg[q], w = half * wg[q];
+            basis_and_derivs_t<xreal>(tx.data(), p, span, x, N, dN);
             for (int r = 0; r <= p; ++r)
                 for (int c = 0; c <= p; ++c) {
-                    int ia = e + r, ic = e + c;
-                    s.M.at(ia, ic) += w * N[r] * N[c];
-                    s.K.at(ia, ic) += w * dN[r] * dN[c];
-                    s.B.at(ia, ic) += w * dN[r] * N[c];
+                    const size_t ix = (size_t)(e + r) * W + (c - r + p);
+                    Mx[ix] += w * N[r] * N[c];
+                    Kx[ix] += w * dN[r] * dN[c];
+                    Bx[ix] += w * dN[r] * N[c];
                 }
         }
+    }
+    for (size_t q = 0; q < Mx.size(); ++q) {
+        s.M.v[q] = (double)Mx[q];
+        s.K.v[q] = (double)Kx[q];
+        s.B.v[q] = (double)Bx[q];
     }
     // Uniform mesh: every row whose basis function and all p neighbours on each
     // side are interior cardinal B-splines (rows [2p, n-1-2p]) has the same band
     // in exact arithmetic (h-scaled cardinal B-spline autocorrelation); quadrature
-    // rounding jitters them by a few ulp.  Use the middle row for all of them so
+    // rounding can still jitter them by an ulp.  Use the middle row for all of them so
     // the interior is bitwise Toeplitz ("Toeplitz interior").
     {
         const int lo = 2 * p, hi = s.n - 1 - 2 * p, mid = s.n / 2;
@@ -122,7 +156,7 @@ int build_space(int p, int nel, int bc, Space1D &s) {
                 rb[k + p] = s.B.at(mid, mid + k);
             }
             // M and K are symmetric; make the Toeplitz row bitwise symmetric too (the
-            // quadrature sums of row entries +k and -k differ by rounding only), so
+            // quadrature sums of row entries +k and -k can differ by rounding), so
             // kernels may use pair sums with p+1 distinct coefficients.
             for (int k = 1; k <= p; ++k) {
                 rm[p + k] = rm[p - k] = 0.5 * (rm[p + k] + rm[p - k]);
@@ -149,6 +183,36 @@ int build_space(int p, int nel, int bc, Space1D &s) {
     return 0;
 }
 
+void diff_weights(const Space1D &s, std::vector<double> &w) {
+    const int n = s.n, p = s.p, W2 = 2 * p;
+    w.assign((size_t)n * W2, 0.0);
+    if (s.nel == 0) return;  // the 2D axis: K = 0
+    for (int k = 0; k < n; ++k) {
+        xreal wk[16] = {};
+        xreal rs = 0;  // row sum of the band row
+        for (int c = std::max(0, k - p); c <= std::min(n - 1, k + p); ++c) rs += (xreal)s.K.get(k, c);
+        // sum_c K_kc (T_c - T_k): T_c - T_k = sum_{j=k}^{c-1} dT_j (c > k), -sum_{j=c}^{k-1} dT_j (c < k)
+        for (int m = 0; m < W2; ++m) {
+            const int j = k - p + m;
+            xreal v = 0;
+            if (j >= k)
+                for (int c = j + 1; c <= k + p; ++c) v += (xreal)s.K.get(k, c);
+            else
+                for (int c = k - p; c <= j; ++c) v -= (xreal)s.K.get(k, c);
+            wk[m] = v;
+        }
+        // + s_k T_k: zero except on Dirichlet rows that lost a column (|k - end| <= p), where T = 0
+        // on the boundary function: T_k = sum_{j<k} dT_j (bottom) or -sum_{j>=k} dT_j (top)
+        if (s.bc == 1 && k > 0 && k < n - 1 && (k <= p || k >= n - 1 - p)) {
+            if (k <= p)
+                for (int j = 0; j < k; ++j) wk[j - k + p] += rs;
+            else
+                for (int j = k; j <= n - 2; ++j) wk[j - k + p] -= rs;
+        }
+        for (int m = 0; m < W2; ++m) w[(size_t)k * W2 + m] = (double)wk[m];
+    }
+}
+
 void trivial_space(int p, Space1D &s) {
     s.p = p;
     s.nel = 0;
@@ -166,21 +230,24 @@ void load_vector(const Space1D &s, int func, double c, double sigma, double *out
         out[0] = 1.0;
         return;
     }
-    const double kPi = 3.141592653589793238462643383;
-    double xg[8], wg[8], N[8], dN[8];
-    gauss_legendre(8, xg, wg);
-    std::fill(out, out + s.n, 0.0);
+    const xreal kPi = 3.14159265358979323846264338327950288L;
+    const std::vector<xreal> tx = knots_x(s.p, s.nel);
+    xreal xg[8], wg[8], N[8], dN[8];
+    gauss_legendre_t<xreal>(8, xg, wg);
+    std::vector<xreal> acc(s.n, 0);
+    const xreal cx = c, sx = sigma;
     for (int e = 0; e < s.nel; ++e) {
         int span = e + s.p;
-        double a = s.knots[span], b = s.knots[span + 1];
-        double half = 0.5 * (b - a), mid = 0.5 * (a + b);
+        xreal a = tx[span], b = tx[span + 1];
+        xreal half = (b - a) / 2, mid = (a + b) / 2;
         for (int q = 0; q < 8; ++q) {
-            double x = mid + half * xg[q], w = half * wg[q];
-            double f = (func == 0) ? std::sin(kPi * x) : std::exp(-(x - c) * (x - c) / (2.0 * sigma * sigma));
-            basis_and_derivs(s.knots, s.p, span, x, N, dN);
-            for (int r = 0; r <= s.p; ++r) out[e + r] += w * f * N[r];
+            xreal x = mid + half * xg[q], w = half * wg[q];
+            xreal f = (func == 0) ? std::sin(kPi * x) : std::exp(-(x - cx) * (x - cx) / (2 * sx * sx));
+            basis_and_derivs_t<xreal>(tx.data(), s.p, span, x, N, dN);
+            for (int r = 0; r <= s.p; ++r) acc[e + r] += w * f * N[r];
         }
     }
+    for (int i = 0; i < s.n; ++i) out[i] = (double)acc[i];
     if (s.bc == 1) out[0] = out[s.n - 1] = 0.0;
 }
 

@@ -35,6 +35,12 @@ int gauss_legendre(int m, double *x, double *w);
 // N[0..p], dN[0..p] belong to functions span-p .. span.
 void basis_and_derivs(const std::vector<double> &t, int p, int span, double x, double *N, double *dN);
 int build_space(int p, int nel, int bc, Space1D &s);
+// Stiffness rows in plane-difference form (the operator kernel's Kz, kernels.cuh KopArgs::wz):
+// (K T)_k = sum_{m < 2p} w[k*2p + m] (T_{k-p+m+1} - T_{k-p+m}) for every T of the space, using
+// the row sums the exact matrix has -- zero for every row of the unrestricted space (K 1 = 0);
+// on zero-Dirichlet rows next to a boundary the removed column's share, with T = 0 on the
+// boundary function.  Computed in extended precision from the band of s.K.
+void diff_weights(const Space1D &s, std::vector<double> &w);
 // The 2D scheme's third axis (ads_create with nz = 0; PAPER.md:123-143 as printed in 2D): one
 // function, M = 1, K = B = 0, no boundary -- K = Kx(x)My + Mx(x)Ky and D = Ax(x)Ay exactly.
 void trivial_space(int p, Space1D &s);

@@ -773,6 +773,422 @@ __global__ void __launch_bounds__(KT_THREADS, 2) kop_kernel(const KopArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
+// fused drift + source + K-apply (v4, "K first")
+//
+//   P = U + tau V (written to Pout),  r = g (bx (x) by (x) bz) + sign K P,
+//   K P = Mz [My (Kx P) + Mx (Ky P)] + Kz (Mx My P)   (Eq. 14, 3D)
+//
+// K_d annihilates constants, so K_d applied to a ROUNDED mass product amplifies its last-ulp
+// noise by ~ (sigma/h)^2 on smooth data and D^-1 passes it on (T1: the v3 kernel, which
+// formed Kx (My P) and Kz (Mx My P), missed the extended-precision step by 1e-11 at 512^3).  Here
+//   - Kx and Ky act on P itself (K first), then My / Mx;
+//   - Kz acts on T = Mx My P through plane differences: Kz T_k = sum_m wz[k][m] dT_{k-p+m} with
+//     dT_j = T_{j+1} - T_j = Mx My (P_{j+1} - P_j); the in-plane mass products of the small
+//     differences round at the differences' scale, not T's.  The 2p weights per row are built on
+//     the host from the band row with the row sum the exact matrix has (0 in the interior; the
+//     removed boundary column on Dirichlet rows, with T = 0 on the boundary plane).
+//
+// CTA = 256 threads on a K4_X x K4_Y = 32 x 16 output tile, marching along z over [z0, z1).
+// Per input plane c (TMA box of U and V over the haloed tile, K4_NPF - 1 planes ahead):
+//   A. every position of the (32 + 2p) x (16 + 2p) haloed tile: P = U + tau V into the P tile and
+//      the plane difference D = P_c - P_{c-1} (previous P kept in a register) into the D tile;
+//   B. column items (column, 4 rows): Ky P and My D, and the owned P to HBM; row items (row,
+//      4 columns): Kx P;
+//   C. lane = x, 2 rows per thread: G_c = My (Kx P) + Mx (Ky P) and dT_{c-1} = Mx (My D) scattered
+//      (weights Mz, wz) into a register ring of 2p + 1 pending output planes; output plane c - p
+//      is complete: r = g src + sign ring.
+// The three stages run skewed (A of plane ii, B of ii - 1, C of ii - 2) on double-buffered tiles
+// with one barrier per plane.  Interior tiles/planes use the Toeplitz rows (kernel parameters)
+// in pair form; boundary tiles read staged rows, boundary planes read global rows.
+// HBM traffic: U, V read once (halos from L2), P and r written once: 32 B/DOF.
+// ------------------------------------------------------------------------------------------
+constexpr int K4_X = 32, K4_Y = 16, K4_THREADS = 256, K4_NPF = 3, K4_XP = 34;
+template <int P>
+struct K4Geo {
+    static constexpr int W = 2 * P + 1;
+    static constexpr int PA = (P + 1) & ~1;             // even x halo of the TMA box
+    static constexpr int HXE = K4_X + 2 * PA;           // staged columns
+    static constexpr int HY = K4_Y + 2 * P;             // rows of the haloed tile
+    static constexpr int NC = K4_X + 2 * P;             // columns of the haloed tile
+    // P tile pitch: even with pitch/2 odd, so the row items' 16-byte loads (a quarter-warp = 2 rows
+    // x 4 column quads) hit 8 distinct bank groups
+    static constexpr int PP = ((NC / 2) % 2 == 1) ? NC : NC + 2;
+    static constexpr int NA = NC * HY;                  // stage-A positions
+    static constexpr int SA = (NA + K4_THREADS - 1) / K4_THREADS;
+    static constexpr int NCOL = NC * (K4_Y / 4);        // column items (4 output rows each)
+    static constexpr int CW = (NCOL + 31) / 32;         // warps running column items
+    static constexpr int RW = K4_THREADS / 32 - CW;     // warps running row items
+    static constexpr int RG = (HY + 3) / 4;             // row-item groups of 4 rows x 8 column quads
+    static constexpr int RWIN = 4 + 2 * P;              // row-item window (even)
+    static_assert(RW >= 1, "row-item warps");
+    static constexpr int al16(int v) { return (v + 15) & ~15; }
+    static constexpr int STG = al16(HXE * HY);          // one staged field plane (128-byte multiple)
+    static constexpr int PT = al16(HY * PP), YQ = al16(K4_Y * NC * 2);
+    static constexpr int X1 = al16(HY * K4_XP), XB = al16(K4_X * 2 * W), YB = al16(K4_Y * 2 * W);
+    static constexpr int OFF_PT = K4_NPF * 2 * STG, OFF_DT = OFF_PT + 2 * PT, OFF_YQ = OFF_DT + 2 * PT;
+    static constexpr int OFF_X1 = OFF_YQ + 2 * YQ, OFF_XB = OFF_X1 + 2 * X1, OFF_YB = OFF_XB + XB;
+    static constexpr int OFF_MB = OFF_YB + YB;
+    static constexpr int SMEM = OFF_MB + 16 + 16;       // mbarriers + 128-byte alignment slack
+};
+
+extern __shared__ __align__(128) double k4_smem[];
+
+__device__ __forceinline__ void k4_wait(unsigned mb, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n K4W_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra K4W_%=;\n}\n" ::"r"(mb), "r"(parity) : "memory");
+}
+
+// stage A of input plane kk: P tile, D = P - P_prev tile (so_[m] / po_[m]: staging / tile offsets
+// of slot m, -1: none; pv[m]: the previous plane's P at slot m)
+template <int P>
+__device__ __forceinline__ void k4_stage_a(const KopArgs &a, double (&pv)[K4Geo<P>::SA], const int (&so_)[K4Geo<P>::SA],
+                                           const int (&po_)[K4Geo<P>::SA], int sbase, int pbase, int dbase, bool live,
+                                           bool zdir) {
+    using G = K4Geo<P>;
+#pragma unroll
+    for (int m = 0; m < G::SA; ++m) {
+        if (G::NA % K4_THREADS != 0 && m == G::SA - 1 && po_[m] < 0) break;
+        const double p = live ? fma(a.tau, k4_smem[sbase + G::STG + so_[m]], k4_smem[sbase + so_[m]]) : 0.0;
+        const double pz = zdir ? 0.0 : p;  // a zero-Dirichlet z face: outside the restricted space
+        k4_smem[pbase + po_[m]] = p;
+        k4_smem[dbase + po_[m]] = pz - pv[m];
+        pv[m] = pz;
+    }
+}
+
+// z scatter of plane kk (ring slot U): G_kk with Mz(k, kk) into outputs k = kk-P .. kk+P and
+// dT_{kk-1} with wz[k][kk-1-k+P] into outputs kk-P .. kk+P-1; returns the completed output kk - P
+template <int P, int U>
+__device__ __forceinline__ void k4_zscatter(const KopArgs &a, double (&A0)[2 * P + 1], double (&A1)[2 * P + 1],
+                                            double g0, double g1, double d0, double d1, int kk, bool zint, double &o0,
+                                            double &o1) {
+    constexpr int W = 2 * P + 1;
+    if (zint) {
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+            const int sl = ((U - P + c) % W + W) % W, d = c < P ? P - c : c - P;
+            A0[sl] = fma(a.mc[2][P + d], g0, A0[sl]);
+            A1[sl] = fma(a.mc[2][P + d], g1, A1[sl]);
+            if (c < 2 * P) {  // output k = kk - P + c: dT_{kk-1} is its tap m = 2P - 1 - c
+                A0[sl] = fma(a.wzc[2 * P - 1 - c], d0, A0[sl]);
+                A1[sl] = fma(a.wzc[2 * P - 1 - c], d1, A1[sl]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+            const int sl = ((U - P + c) % W + W) % W, k = kk - P + c;
+            double mz_ = 0.0, wz_ = 0.0;
+            if (k >= 0 && k < a.geo.n2) {
+                mz_ = __ldg(a.mz + (long)(k + a.zoff) * W + 2 * P - c);
+                if (c < 2 * P) wz_ = a.kw[2] * __ldg(a.wz + (long)(k + a.zoff) * (2 * P) + 2 * P - 1 - c);
+            }
+            A0[sl] = fma(mz_, g0, A0[sl]);
+            A1[sl] = fma(mz_, g1, A1[sl]);
+            A0[sl] = fma(wz_, d0, A0[sl]);
+            A1[sl] = fma(wz_, d1, A1[sl]);
+        }
+    }
+    constexpr int so = ((U - P) % W + W) % W;
+    o0 = A0[so];
+    o1 = A1[so];
+    A0[so] = 0.0;
+    A1[so] = 0.0;
+}
+
+template <int P, bool XI, bool YI>
+__device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *tmu, const CUtensorMap *tmv, int sh,
+                                          int x0, int y0, int z0, int z1) {
+    using G = K4Geo<P>;
+    constexpr int W = G::W, NC = G::NC, HY = G::HY, PP = G::PP;
+    // shared memory: k4_smem[sh + offset]; sh aligns the TMA staging to 128 bytes
+    double *const xb = k4_smem + sh + G::OFF_XB;  // [W][2][K4_X]: (Mx, kw0 Kx) rows of x0 + xr
+    double *const yb = k4_smem + sh + G::OFF_YB;  // [K4_Y][2][W]: (My, kw1 Ky) rows of y0 + yr
+    const unsigned mb0 = (unsigned)__cvta_generic_to_shared(k4_smem + sh + G::OFF_MB);
+    const unsigned stg_s = (unsigned)__cvta_generic_to_shared(k4_smem + sh);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int n0 = a.geo.n0, n1 = a.geo.n1;
+    const long sy = a.geo.sy, sz = a.geo.sz;
+    if (!XI)
+        for (int e = tid; e < K4_X * 2 * W; e += K4_THREADS) {
+            const int xr = e % K4_X, m = (e / K4_X) & 1, c = e / (2 * K4_X), X = x0 + xr;
+            xb[e] = (X >= 0 && X < n0) ? (m ? a.kw[0] : 1.0) * __ldg((m ? a.kx : a.mx) + (long)X * W + c) : 0.0;
+        }
+    if (!YI)
+        for (int e = tid; e < K4_Y * 2 * W; e += K4_THREADS) {
+            const int yr = e / (2 * W), m = (e / W) & 1, c = e % W, Y = y0 + yr;
+            yb[e] = (Y >= 0 && Y < n1) ? (m ? a.kw[1] : 1.0) * __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
+        }
+    const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;
+    if (tid == 0) {
+        for (int i = 0; i < K4_NPF; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb0 + 8u * i) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    // thread 0: stage input plane ii into slot ii % K4_NPF (planes outside [zv0, zv1) are zero:
+    // nothing is loaded, the barrier phase completes by a plain arrival)
+    auto issue = [&](int ii) {
+        if (ii >= npl) return;
+        const int kk = kk0 + ii, slot = ii % K4_NPF;
+        const unsigned mb = mb0 + 8u * slot;
+        if (kk >= a.zv0 && kk < a.zv1) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                         "r"((unsigned)(2 * G::HXE * HY * sizeof(double)))
+                         : "memory");
+            const unsigned d = stg_s + slot * 2 * G::STG * 8u;
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(d),
+                "l"(reinterpret_cast<unsigned long long>(tmu)), "r"(x0 - G::PA), "r"(y0 - P), "r"(kk - a.zv0), "r"(mb)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(d + G::STG * 8u),
+                "l"(reinterpret_cast<unsigned long long>(tmv)), "r"(x0 - G::PA), "r"(y0 - P), "r"(kk - a.zv0), "r"(mb)
+                : "memory");
+        } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(mb) : "memory");
+        }
+    };
+    if (tid == 0)
+        for (int i = 0; i < K4_NPF - 1; ++i) issue(i);
+
+    // stage-A slot offsets (staging, P/D tiles) and previous P; stage-C rings (pending output planes)
+    int so_[G::SA], po_[G::SA];
+#pragma unroll
+    for (int m = 0; m < G::SA; ++m) {
+        const int e = tid + K4_THREADS * m, hy = e / NC, hx = e - hy * NC;
+        so_[m] = e < G::NA ? hy * G::HXE + hx + (G::PA - P) : -1;
+        po_[m] = e < G::NA ? hy * PP + hx : -1;
+    }
+    double pv[G::SA], A0[W], A1[W];
+#pragma unroll
+    for (int m = 0; m < G::SA; ++m) pv[m] = 0.0;
+#pragma unroll
+    for (int c = 0; c < W; ++c) A0[c] = A1[c] = 0.0;
+
+    // stage-C constants: output column X = x0 + lane, rows y0 + 2w, y0 + 2w + 1
+    // (tiles start at ilo - 32 / ilo - 16 for the interior alignment: X, Y can be negative)
+    const int X = x0 + lane, yr0 = 2 * w;
+    const bool xin = X >= 0 && X < n0;
+    const bool own0 = xin && y0 + yr0 >= 0 && y0 + yr0 < n1, own1 = xin && y0 + yr0 + 1 >= 0 && y0 + yr0 + 1 < n1;
+    const bool has_src = a.bx != nullptr;
+    const double sxy0 = (has_src && own0) ? __ldg(a.bx + X) * __ldg(a.by + y0 + yr0) : 0.0;
+    const double sxy1 = (has_src && own1) ? __ldg(a.bx + X) * __ldg(a.by + y0 + yr0 + 1) : 0.0;
+    double gsrc = a.g;
+    if (has_src && a.dstep) {  // source time from the device step counter (CUDA graph replays)
+        const double x = 3.141592653589793238462643383 * a.f0 * ((double)(*a.dstep + 1) * a.tau_g - a.t0);
+        gsrc = a.amp * (a.wav ? (1.0 - 2.0 * x * x) * exp(-x * x) : 1.0);
+    }
+    double *rq = a.r + (long)(y0 + yr0) * sy + X + (long)z0 * sz;
+    // stage-B column item (threads [0, NCOL)) and row item (warps [CW, 8)) constants
+    const int nc = tid % NC, g4 = tid / NC;
+    const int Xc = x0 - P + nc;
+    const bool pown = tid < G::NCOL && a.Pout && nc >= P && nc < P + K4_X && Xc >= 0 && Xc < n0;
+    double *const pq = a.Pout ? a.Pout + (long)(y0 + 4 * g4) * sy + Xc : nullptr;
+    const int rq4 = (lane & 3) + 4 * (lane >> 4), rsub = (lane >> 2) & 3;
+
+    for (int ii = 0; ii < npl + 2; ++ii) {
+        if (ii < npl && w == 0) k4_wait(mb0 + 8u * (ii % K4_NPF), (unsigned)((ii / K4_NPF) & 1));
+        __syncthreads();  // plane ii landed; A(ii-1), B(ii-2), C(ii-3) done: buffers and slot free
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(ii + K4_NPF - 1);
+        }
+        // ---- A: input plane kk = kk0 + ii
+        if (ii < npl) {
+            const int kk = kk0 + ii;
+            const int b = ii & 1;
+            k4_stage_a<P>(a, pv, so_, po_, sh + (ii % K4_NPF) * 2 * G::STG, sh + G::OFF_PT + b * G::PT,
+                          sh + G::OFF_DT + b * G::PT, kk >= a.zv0 && kk < a.zv1,
+                          kk + a.zoff == a.zd0 || kk + a.zoff == a.zd1);
+        }
+        // ---- B: plane c = kk0 + ib (Ky P, Kx P, owned P) and D = P_c - P_{c-1} (My D)
+        const int ib = ii - 1;
+        if (ib >= 0 && ib < npl) {
+            const int b = ib & 1, kc_ = kk0 + ib;
+            const double *pt = k4_smem + sh + G::OFF_PT + b * G::PT;
+            const double *dt = k4_smem + sh + G::OFF_DT + b * G::PT;
+            if (w < G::CW) {
+                if (tid < G::NCOL) {
+                    double pw[4 + 2 * P];
+#pragma unroll
+                    for (int r = 0; r < 4 + 2 * P; ++r) pw[r] = pt[(4 * g4 + r) * PP + nc];
+                    if (pown && kc_ >= z0 && kc_ < z1) {
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int Y = y0 + 4 * g4 + r;
+                            if (Y >= 0 && Y < n1) pq[(long)kc_ * sz + r * sy] = pw[r + P];
+                        }
+                    }
+                    double ky[4], mq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        if (YI) {
+                            double s = a.kc[1][P] * pw[r + P];
+#pragma unroll
+                            for (int d = 1; d <= P; ++d) s = fma(a.kc[1][P + d], pw[r + P - d] + pw[r + P + d], s);
+                            ky[r] = s;
+                        } else {
+                            const double *row = yb + ((4 * g4 + r) * 2 + 1) * W;
+                            double s = 0.0;
+#pragma unroll
+                            for (int c = 0; c < W; ++c) s = fma(row[c], pw[r + c], s);
+                            ky[r] = s;
+                        }
+                    }
+                    {
+#pragma unroll
+                        for (int r = 0; r < 4 + 2 * P; ++r) pw[r] = dt[(4 * g4 + r) * PP + nc];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            if (YI) {
+                                double s = a.mc[1][P] * pw[r + P];
+#pragma unroll
+                                for (int d = 1; d <= P; ++d) s = fma(a.mc[1][P + d], pw[r + P - d] + pw[r + P + d], s);
+                                mq[r] = s;
+                            } else {
+                                const double *row = yb + ((4 * g4 + r) * 2) * W;
+                                double s = 0.0;
+#pragma unroll
+                                for (int c = 0; c < W; ++c) s = fma(row[c], pw[r + c], s);
+                                mq[r] = s;
+                            }
+                        }
+                    }
+                    double2 *o = reinterpret_cast<double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ) + (4 * g4) * NC + nc;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) o[r * NC] = make_double2(ky[r], mq[r]);
+                }
+            } else {
+                // row items: a warp covers 4 rows x 8 column quads (16-byte window loads)
+#pragma unroll 1
+                for (int grp = w - G::CW; grp < G::RG; grp += G::RW) {
+                    const int hy = 4 * grp + rsub;
+                    if (hy < HY) {
+                        const double2 *src = reinterpret_cast<const double2 *>(pt + hy * PP + 4 * rq4);
+                        double pw[G::RWIN];
+#pragma unroll
+                        for (int j = 0; j < G::RWIN / 2; ++j) {
+                            const double2 v = src[j];
+                            pw[2 * j] = v.x;
+                            pw[2 * j + 1] = v.y;
+                        }
+                        double kx[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if (XI) {
+                                double s = a.kc[0][P] * pw[j + P];
+#pragma unroll
+                                for (int d = 1; d <= P; ++d) s = fma(a.kc[0][P + d], pw[j + P - d] + pw[j + P + d], s);
+                                kx[j] = s;
+                            } else {
+                                double s = 0.0;
+#pragma unroll
+                                for (int c = 0; c < W; ++c) s = fma(xb[(c * 2 + 1) * K4_X + 4 * rq4 + j], pw[j + c], s);
+                                kx[j] = s;
+                            }
+                        }
+                        double2 *o = reinterpret_cast<double2 *>(k4_smem + sh + G::OFF_X1 + b * G::X1 + hy * K4_XP + 4 * rq4);
+                        o[0] = make_double2(kx[0], kx[1]);
+                        o[1] = make_double2(kx[2], kx[3]);
+                    }
+                }
+            }
+        }
+        // ---- C: plane c = kk0 + ic: G = My (Kx P) + Mx (Ky P), dT_{c-1} = Mx (My D) into the z ring
+        const int ic = ii - 2;
+        if (ic >= 0) {
+            const int b = ic & 1, kc_ = kk0 + ic, kout = kc_ - P;
+            const double2 *Y0 = reinterpret_cast<const double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ) + yr0 * NC + lane;
+            const double2 *Y1 = Y0 + NC;
+            const double *Xc2 = k4_smem + sh + G::OFF_X1 + b * G::X1 + yr0 * K4_XP + lane;
+            double g0, g1, t0, t1;
+            if (XI) {
+                const double2 c0 = Y0[P], c1 = Y1[P];
+                g0 = a.mc[0][P] * c0.x;
+                t0 = a.mc[0][P] * c0.y;
+                g1 = a.mc[0][P] * c1.x;
+                t1 = a.mc[0][P] * c1.y;
+#pragma unroll
+                for (int d = 1; d <= P; ++d) {
+                    const double2 l0 = Y0[P - d], r0 = Y0[P + d], l1 = Y1[P - d], r1 = Y1[P + d];
+                    g0 = fma(a.mc[0][P + d], l0.x + r0.x, g0);
+                    t0 = fma(a.mc[0][P + d], l0.y + r0.y, t0);
+                    g1 = fma(a.mc[0][P + d], l1.x + r1.x, g1);
+                    t1 = fma(a.mc[0][P + d], l1.y + r1.y, t1);
+                }
+            } else {
+                g0 = t0 = g1 = t1 = 0.0;
+#pragma unroll
+                for (int c = 0; c < W; ++c) {
+                    const double m = xb[(c * 2) * K4_X + lane];
+                    const double2 q0 = Y0[c], q1 = Y1[c];
+                    g0 = fma(m, q0.x, g0);
+                    t0 = fma(m, q0.y, t0);
+                    g1 = fma(m, q1.x, g1);
+                    t1 = fma(m, q1.y, t1);
+                }
+            }
+            double xw[2 * P + 2];  // Kx P rows yr0 .. yr0 + 2P + 1 at column lane
+#pragma unroll
+            for (int c = 0; c < 2 * P + 2; ++c) xw[c] = Xc2[c * K4_XP];
+            if (YI) {
+                g0 = fma(a.mc[1][P], xw[P], g0);
+                g1 = fma(a.mc[1][P], xw[P + 1], g1);
+#pragma unroll
+                for (int d = 1; d <= P; ++d) {
+                    g0 = fma(a.mc[1][P + d], xw[P - d] + xw[P + d], g0);
+                    g1 = fma(a.mc[1][P + d], xw[P + 1 - d] + xw[P + 1 + d], g1);
+                }
+            } else {
+                const double *r0 = yb + (yr0 * 2) * W, *r1 = yb + ((yr0 + 1) * 2) * W;
+#pragma unroll
+                for (int c = 0; c < W; ++c) {
+                    g0 = fma(r0[c], xw[c], g0);
+                    g1 = fma(r1[c], xw[c + 1], g1);
+                }
+            }
+            const bool zint = kc_ + a.zoff - P >= a.ilo[2] && kc_ + a.zoff + P <= a.ihi[2];
+            double o0 = 0.0, o1 = 0.0;  // t0, t1: dT_{c-1} = Mx My D of rows yr0, yr0 + 1
+            switch (ic % W) {
+#define ADS_K4C(U)                                                                      \
+    case U:                                                                             \
+        if constexpr (U < W) k4_zscatter<P, U>(a, A0, A1, g0, g1, t0, t1, kc_, zint, o0, o1); \
+        break;
+                ADS_K4C(0) ADS_K4C(1) ADS_K4C(2) ADS_K4C(3) ADS_K4C(4) ADS_K4C(5)
+                ADS_K4C(6) ADS_K4C(7) ADS_K4C(8) ADS_K4C(9) ADS_K4C(10)
+#undef ADS_K4C
+            }
+            if (kout >= z0) {  // output plane kout = c - P: r = g src + sign K P
+                const double gz = has_src ? gsrc * __ldg(a.bz + kout + a.zoff) : 0.0;
+                if (own0) rq[0] = fma(a.sign, o0, gz * sxy0);
+                if (own1) rq[sy] = fma(a.sign, o1, gz * sxy1);
+                rq += sz;
+            }
+        }
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(K4_THREADS, P <= 3 ? 2 : 1)
+    kop4_kernel(const KopArgs a, const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmv) {
+    // TMA staging needs 128-byte alignment of the dynamic shared memory window
+    const int sh = (int)(((128 - (__cvta_generic_to_shared(k4_smem) & 127)) & 127) / sizeof(double));
+    const int x0 = kop_origin(a.ilo[0], a.ihi[0], K4_X) + (int)blockIdx.x * K4_X;
+    const int y0 = kop_origin(a.ilo[1], a.ihi[1], K4_Y) + (int)blockIdx.y * K4_Y;
+    const int z0 = blockIdx.z * a.zlen, z1 = min(a.geo.n2, z0 + a.zlen);
+    const bool xi = x0 >= a.ilo[0] && x0 + K4_X - 1 <= a.ihi[0];
+    const bool yi = y0 >= a.ilo[1] && y0 + K4_Y - 1 <= a.ihi[1];
+    if (xi && yi) kop4_tile<P, true, true>(a, &tmu, &tmv, sh, x0, y0, z0, z1);
+    else if (xi) kop4_tile<P, true, false>(a, &tmu, &tmv, sh, x0, y0, z0, z1);
+    else if (yi) kop4_tile<P, false, true>(a, &tmu, &tmv, sh, x0, y0, z0, z1);
+    else kop4_tile<P, false, false>(a, &tmu, &tmv, sh, x0, y0, z0, z1);
+}
+
+// ------------------------------------------------------------------------------------------
 // distributed z-solve fix-up + kick (see kernels.cuh ZfixArgs).  Thread per z-line and z piece
 // of 32 planes (coalesced across x; each piece recomputes the line's interface values from the
 // tips), streaming the nl owned planes once: 24 B/DOF (+8 when a is kept).
@@ -1252,59 +1668,91 @@ static int grid_for(long N) {
     return (int)(b < 148 * 32 ? (b < 1 ? 1 : b) : 148 * 32);
 }
 
-template <int P>
-static void kop_launch(const KopArgs &a, cudaStream_t s) {
-    using G = KopGeo<P>;
-    const size_t sm = sizeof(double) * G::SMEM;
-    static int nsm = 0, per_sm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(kop_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kop_kernel<P>, KT_THREADS, sm);
-        per_sm = std::max(per_sm, 1);
-    }
-    const int ox = kop_origin(a.ilo[0], a.ihi[0], KT_X), oy = kop_origin(a.ilo[1], a.ihi[1], KT_Y);
-    const int gx = (a.geo.n0 - ox + KT_X - 1) / KT_X, gy = (a.geo.n1 - oy + KT_Y - 1) / KT_Y;
-    // z split: CTAs are scheduled dynamically, so the time is about (CTAs per resident slot
-    // + 1/2 for the tail) x (planes per CTA incl. 2p halo planes); this fits the measured kop
-    // times at 515^3 for 1..12 pieces within 3 % (1.69 ms unsplit, 1.49 ms at 4 pieces)
-    const long resident = (long)per_sm * nsm, tiles = (long)gx * gy;
+static int encode_field_map(CUtensorMap *m, const double *base, const Geom &g, unsigned b0, unsigned b1,
+                            unsigned b2);
+
+// z split: CTAs are scheduled dynamically, so the time is about (CTAs per resident slot + 1/2 for
+// the tail) x (planes per CTA incl. 2p halo planes); this fit the measured v3 kop times at 515^3
+// for 1..12 pieces within 3 % (1.69 ms unsplit, 1.49 ms at 4 pieces)
+static int kop_pieces(int n2, int P, long tiles, long resident) {
     int best = 1;
     double best_cost = 1e300;
     for (int nz = 1; nz <= 32; ++nz) {
-        const int zl = (a.geo.n2 + nz - 1) / nz;
+        const int zl = (n2 + nz - 1) / nz;
         if (zl < 2 * P + 1 && nz > 1) break;
-        const long ctas = tiles * ((a.geo.n2 + zl - 1) / zl);
+        const long ctas = tiles * ((n2 + zl - 1) / zl);
         const double cost = ((double)ctas / resident + 0.5) * (zl + 2.0 * P);
-        if (cost < best_cost * 0.999) { best_cost = cost; best = nz; }
+        if (cost < best_cost * 0.999) {
+            best_cost = cost;
+            best = nz;
+        }
     }
     static const int nz_env = [] {  // experiment override of the split (scripts/kop_nz.py)
         const char *e = std::getenv("ADS_KOP_NZ");
         return e ? std::atoi(e) : 0;
     }();
-    if (nz_env > 0) best = nz_env;
+    return nz_env > 0 ? nz_env : best;
+}
+
+template <int P>
+static int kop_launch(const KopArgs &a, cudaStream_t s) {
+    static const bool v3 = [] {  // A/B switch: the v3 (mass-first) kernel
+        const char *e = std::getenv("ADS_KOP_V3");
+        return e && std::atoi(e) != 0;
+    }();
     KopArgs b = a;
-    b.zlen = a.zlen > 0 ? a.zlen : (a.geo.n2 + best - 1) / best;
     if (b.zv1 < b.zv0) {  // no halo planes: exactly the output planes exist
         b.zv0 = 0;
         b.zv1 = a.geo.n2;
     }
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (v3) {
+        using G = KopGeo<P>;
+        const size_t sm = sizeof(double) * G::SMEM;
+        cudaFuncSetAttribute(kop_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kop_kernel<P>, KT_THREADS, sm);
+        const int ox = kop_origin(a.ilo[0], a.ihi[0], KT_X), oy = kop_origin(a.ilo[1], a.ihi[1], KT_Y);
+        const int gx = (a.geo.n0 - ox + KT_X - 1) / KT_X, gy = (a.geo.n1 - oy + KT_Y - 1) / KT_Y;
+        const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)std::max(per_sm, 1) * nsm);
+        b.zlen = a.zlen > 0 ? a.zlen : (a.geo.n2 + nz - 1) / nz;
+        dim3 grd(gx, gy, (a.geo.n2 + b.zlen - 1) / b.zlen);
+        kop_kernel<P><<<grd, KT_THREADS, sm, s>>>(b);
+        return 0;
+    }
+    using G = K4Geo<P>;
+    const size_t sm = sizeof(double) * G::SMEM;
+    cudaFuncSetAttribute(kop4_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kop4_kernel<P>, K4_THREADS, sm);
+    const int ox = kop_origin(a.ilo[0], a.ihi[0], K4_X), oy = kop_origin(a.ilo[1], a.ihi[1], K4_Y);
+    const int gx = (a.geo.n0 - ox + K4_X - 1) / K4_X, gy = (a.geo.n1 - oy + K4_Y - 1) / K4_Y;
+    const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)std::max(per_sm, 1) * nsm);
+    b.zlen = a.zlen > 0 ? a.zlen : (a.geo.n2 + nz - 1) / nz;
+    // U and V over the planes that exist in memory, [zv0, zv1) (slabs: halo planes included)
+    Geom gm = a.geo;
+    gm.n2 = b.zv1 - b.zv0;
+    const double *ub = a.U + (long)b.zv0 * a.geo.sz, *vb = (a.V ? a.V : a.U) + (long)b.zv0 * a.geo.sz;
+    if (!a.V) b.tau = 0.0;
+    CUtensorMap tmu, tmv;
+    if (encode_field_map(&tmu, ub, gm, G::HXE, G::HY, 1) || encode_field_map(&tmv, vb, gm, G::HXE, G::HY, 1))
+        return -2;
     dim3 grd(gx, gy, (a.geo.n2 + b.zlen - 1) / b.zlen);
-    kop_kernel<P><<<grd, KT_THREADS, sm, s>>>(b);
+    kop4_kernel<P><<<grd, K4_THREADS, sm, s>>>(b, tmu, tmv);
+    return 0;
 }
 
 int launch_kop(int p, const KopArgs &a, cudaStream_t s) {
     switch (p) {
-        case 1: kop_launch<1>(a, s); break;
-        case 2: kop_launch<2>(a, s); break;
-        case 3: kop_launch<3>(a, s); break;
-        case 4: kop_launch<4>(a, s); break;
-        case 5: kop_launch<5>(a, s); break;
+        case 1: return kop_launch<1>(a, s);
+        case 2: return kop_launch<2>(a, s);
+        case 3: return kop_launch<3>(a, s);
+        case 4: return kop_launch<4>(a, s);
+        case 5: return kop_launch<5>(a, s);
         default: return -1;
     }
-    return 0;
 }
 
 // ---- TMA descriptors (driver entry point through the runtime: no -lcuda) ----

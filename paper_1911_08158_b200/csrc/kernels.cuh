@@ -50,6 +50,12 @@ struct KopArgs {
     // P-wave; elasticity's diagonal blocks mu K + (mu + lam) K_(i)).  The interior rows kc[d]
     // arrive pre-scaled; boundary rows are scaled where they are staged.
     double kw[3] = {1.0, 1.0, 1.0};
+    // Kz in plane-difference form (kop v4): (Kz T)_k = sum_m wz[k][m] (T_{k-p+m+1} - T_{k-p+m}),
+    // m < 2p, rows global (table [n2 global][2p]); wzc: the Toeplitz interior row, pre-scaled by kw[2]
+    const double *wz = nullptr;
+    double wzc[2 * kMaxP] = {};
+    // global planes whose P counts as zero in those differences (zero-Dirichlet z faces; -1: none)
+    int zd0 = -1, zd1 = -1;
     // z-slabs: local plane k is global row k + zoff of Mz, Kz (and of bz); input planes
     // [zv0, zv1) exist in memory (halo planes of a slab); outputs are planes [0, n2)
     int zoff = 0, zv0 = 0, zv1 = -1;
