@@ -8,9 +8,10 @@ tau 5e-4, 8 seeded Gaussian bumps) -- the 512^3 case the north_star's targets
 name.  One "step" = one full time step of the hot path (drift+source+K apply,
 x/y/z partitioned banded sweeps, fused kick).  Metric: DOF-steps/s (fp64).
 
-Timing: W untimed warm-up steps, then exactly K steps bracketed by a barrier +
-torch.cuda.synchronize() on both sides, CUDA events on the library's stream,
-max over ranks.  Every field (1.09 GB) is larger than L2 (126 MB), so no L2
+Timing: W untimed warm-up steps; then 5 repeats, each restarting from the initial state and
+timing exactly K steps bracketed by a barrier + torch.cuda.synchronize() on both sides, CUDA
+events on the library's stream, max over ranks; the median repeat is reported (graph-replayed
+steps: the production launch path).  A separate profiled run gives the per-kernel times.  Every field (1.09 GB) is larger than L2 (126 MB), so no L2
 flush is needed.  Per-kernel CUDA-event timing inside the library
 (ads_profile_*) gives the roofline of the dominant kernel.
 
@@ -166,6 +167,56 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
+def host_info():
+    """CPU model and core count of the host."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "oracle_threads": 1}
+
+
+# plan bytes per DOF-step of the P-wave step (DESIGN.md §6): kop 32, x/y sweeps 16 each, z + kick 24
+STEP_PLAN_BYTES = 88.0
+
+
+def config_table(ads, torch, hbm):
+    """Step time of every BASELINE.json config through the public API (graph replays, CUDA events
+    on a caller stream): the per-config view of the same build (c1/c2 are launch-bound, c5 is the
+    elasticity step, 3 components)."""
+    out = {}
+    for name in ["c1", "c2", "c3", "c4", "c5"]:
+        wl = workloads.get(name)
+        s = ads.make_solver(wl)
+        st = torch.cuda.Stream()
+        s.set_stream(st)
+        s.step(4)
+        K = min(wl.steps, 50)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            e0.record(st)
+            s.step(K)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / K)
+        ms = statistics.median(ts)
+        d = {"us_per_step": 1e3 * ms, "dof": wl.ndof, "dof_steps_per_s": wl.ndof / (ms / 1e3), "steps_timed": K}
+        if not wl.elastic:
+            d["plan_hbm_frac"] = STEP_PLAN_BYTES * wl.ndof / (ms / 1e3) / 1e9 / hbm
+        out[name] = d
+        s.close()
+        del s
+        torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------------------ CPU oracle
 def oracle_sample(wl, nel_sample, steps, warmup=0):
     """Time the oracle (as it stands, 1 thread) on `steps` steps of the workload recipe
@@ -198,7 +249,7 @@ def run_reference(args, rank, world):
         "data": "synthetic (seeded, workloads/)",
         "config": {"workload": f"{wl.name} recipe at {nel}^3 elements (bounded CPU sample)", "p": wl.p,
                    "n_dof": n, "tau": wl.tau},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc, **host_info()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -221,27 +272,40 @@ def run_ours(args, rank, world, local):
         s = ads.make_solver(wl)
     stream = torch.cuda.Stream()
     s.set_stream(stream)
-    # warm-up, then restart from the initial state so every run times the same steps
+    # the initial state (device copies), so every timed repeat restarts from it
+    u_init = torch.empty(s.shape, dtype=torch.float64, device="cuda")
+    ud_init = torch.empty_like(u_init)
+    s.get_state(u_init, ud_init, None)
     s.step(args.warmup)
     torch.cuda.synchronize()
 
+    # timed repeats (production launch path: graph replays): restart, barrier + sync, exactly K
+    # steps between CUDA events on the library's stream, barrier + sync; median over the repeats
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = s.launch_count()
-    s.profile_enable(True)
-    barrier(world)
-    torch.cuda.synchronize()
+    reps = []
     with ClockSampler(local) as clk:
-        ev0.record(stream)
-        s.step(args.steps)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    barrier(world)
-    ms = ev0.elapsed_time(ev1)
-    kms, kcnt = s.profile_read()
-    s.profile_enable(False)
-    launches = s.launch_count() - launches0
-    ms = max_over_ranks(ms, world)
+        for _ in range(args.repeats):
+            s.set_state(u_init, ud_init)
+            barrier(world)
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            s.step(args.steps)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            barrier(world)
+            reps.append(max_over_ranks(ev0.elapsed_time(ev1), world))
+    launches = (s.launch_count() - launches0) // args.repeats
+    ms = statistics.median(reps)
     value = N * args.steps / (ms / 1e3)  # whole-job DOF-steps/s (every rank's slab together)
+    # per-kernel times: a separate profiled run (events around every launch, direct launches)
+    s.set_state(u_init, ud_init)
+    s.profile_enable(True)
+    s.step(args.steps)
+    kms, kcnt = s.profile_read()
+    kms, kcnt = kms[:4], kcnt[:4]  # the step's kernel classes
+    s.profile_enable(False)
+    torch.cuda.synchronize()
 
     # ---- roofline of the dominant kernel (algorithmic bytes / its average launch time)
     hbm, peak_kind, _ = peaks()
@@ -292,6 +356,8 @@ def run_ours(args, rank, world, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "repeats": {"n": args.repeats, "ms": reps, "statistic": "median; each repeat restarts from the initial "
+                    "state (set_state) and times exactly `steps` steps"},
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads/)",
         "config": {"workload": f"{wl.name}: {wl.description}", "p": wl.p, "nel": list(wl.nel),
                    "n_dof": N, "tau": wl.tau, "parallelism": f"z-slabs x{world} (NCCL)" if world > 1 else "single",
@@ -305,7 +371,9 @@ def run_ours(args, rank, world, local):
         else:
             val, dt, desc = oracle_sample(wl, args.ref_nel, args.cpu_steps)
         line["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-                                "seconds": dt}
+                                "seconds": dt, **host_info()}
+    if rank == 0 and world == 1 and not args.no_configs:
+        line["configs"] = config_table(ads, torch, hbm)
     if rank == 0:
         print(json.dumps(line), flush=True)
     s.close()
@@ -323,6 +391,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=40, help="oracle steps for the cpu_baseline sample")
     ap.add_argument("--cpu-full", action="store_true", help="time the oracle on one full-size step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config table (c1..c5)")
+    ap.add_argument("--repeats", type=int, default=5, help="timed repeats of `steps` steps (median)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         ap.error("--warmup must be >= 3")

@@ -31,9 +31,11 @@
  *    all its device buffers and copies caller arrays in/out; the caller owns
  *    every pointer it passes.
  *  - Streams: all device work is ordered on the handle's stream (default: a
- *    stream the library creates; ads_set_stream attaches a caller stream, e.g.
- *    torch.cuda.current_stream().cuda_stream).  ads_step is asynchronous;
- *    ads_energy / ads_get_state synchronise the stream.
+ *    blocking stream the library creates, so it is ordered against CUDA's legacy
+ *    default stream -- PyTorch's default stream; ads_set_stream attaches a caller
+ *    stream, e.g. torch.cuda.current_stream().cuda_stream).  ads_step is
+ *    asynchronous; ads_energy / ads_get_state synchronise the stream.
+ *  - Device: every call works on the device that was current at ads_create.
  *  - A handle is single-writer (not thread-safe).
  */
 #ifndef ADS_B200_H
@@ -61,8 +63,9 @@ enum { ADS_WAVELET_NONE = 0, ADS_WAVELET_RICKER = 1 };
 
 /* Create a scalar P-wave solver.
  *   p in [1,5]; nx,ny,nz >= 1 (Dirichlet needs n_d >= 3); tau finite > 0;
- *   bc in {ADS_BC_NATURAL, ADS_BC_DIRICHLET0}; n_d = n_el,d + p <= 1056 (32 chunks of at most
- *   33 rows per line; ADS_E_INVAL beyond).
+ *   bc in {ADS_BC_NATURAL, ADS_BC_DIRICHLET0}; n_d = n_el,d + p <= 1056 (lines are cut into
+ *   16, 32 or 64 chunks of at most 33 rows, whichever fits a CTA's shared memory and pads least;
+ *   ADS_E_INVAL beyond).
  *   nz = 0: the 2D scheme as the paper prints it (Eqs. 14-16; SURVEY.md §8
  *   row f2): the third axis carries one function with M = 1, K = 0 and no boundary, so that
  *   K = Kx(x)My + Mx(x)Ky and D = Ax(x)Ay exactly; arrays are 1 x n_y x n_x, load/source
@@ -149,7 +152,10 @@ int ads_create_dist(ads_handle *h, int nx, int ny, int nz, int p, double tau, in
 int ads_create_virtual(ads_handle *h, int nx, int ny, int nz, int p, double tau, int bc, int nslabs);
 int ads_local_extent(ads_handle h, int *z_begin, int *z_count);
 
-/* Attach a CUDA stream (cudaStream_t passed as void*); NULL = library stream. */
+/* Attach a CUDA stream (cudaStream_t passed as void*).  NULL (which is also what
+ * torch.cuda.current_stream().cuda_stream is for PyTorch's default stream) selects the
+ * library's own stream, a blocking stream that is ordered against the legacy default
+ * stream: work PyTorch queues there before/after a call is seen by/sees the library's. */
 int ads_set_stream(ads_handle h, void *cuda_stream);
 
 /* Host-side 1D helpers for separable data (L2 projection).
@@ -194,7 +200,8 @@ int ads_energy(ads_handle h, double out[3]);
  * Synchronising.  mem: ADS_MEM_HOST/DEVICE. */
 int ads_get_state(ads_handle h, double *u, double *udot, double *a, int mem);
 
-/* Simulation time t_n = n tau, and step count n. */
+/* Simulation time t_n (n tau, or t_m + (n - m) tau after ads_set_tau changed the step at step
+ * m), and step count n. */
 double ads_time(ads_handle h);
 long ads_step_count(ads_handle h);
 
@@ -216,11 +223,12 @@ long ads_launch_count(ads_handle h);
 
 /* Per-kernel-class timing with CUDA events recorded on the handle's stream
  * around every launch of the step kernels (instrumentation for bench.py).
- * Classes: 0 = kop (drift+source+K), 1 = sweep x, 2 = sweep y, 3 = sweep z+kick.
+ * Classes: 0 = kop (drift+source+K), 1 = sweep x, 2 = sweep y, 3 = sweep z+kick,
+ * 4 = modal transform (ads_modal_advance, one launch per direction).
  * ads_profile_enable(h, 1) clears and starts recording; ads_profile_read
  * synchronises and returns total milliseconds and launch counts per class
  * (host arrays of ADS_NPROF entries). */
-#define ADS_NPROF 4
+#define ADS_NPROF 5
 int ads_profile_enable(ads_handle h, int on);
 int ads_profile_read(ads_handle h, double *ms, long *count);
 

@@ -205,7 +205,9 @@ class Solver:
     __del__ = close
 
     def set_stream(self, stream=None):
-        """Attach a torch.cuda.Stream (or raw cudaStream_t int); None = library stream."""
+        """Attach a torch.cuda.Stream (or raw cudaStream_t int).  None, or PyTorch's default stream
+        (cuda_stream 0), selects the library's own stream, which is ordered against the default
+        stream (include/ads.h ads_set_stream)."""
         ptr = None if stream is None else getattr(stream, "cuda_stream", stream)
         self._check(lib().ads_set_stream(self.h, ptr))
 
@@ -295,9 +297,9 @@ class Solver:
         self._check(lib().ads_profile_enable(self.h, 1 if on else 0))
 
     def profile_read(self):
-        """(ms[4], count[4]) per kernel class: kop, sweep x, sweep y, sweep z+kick."""
-        ms = np.zeros(4)
-        cnt = np.zeros(4, dtype=np.int64)
+        """(ms[5], count[5]) per kernel class: kop, sweep x, sweep y, sweep z+kick, modal transform."""
+        ms = np.zeros(5)
+        cnt = np.zeros(5, dtype=np.int64)
         self._check(lib().ads_profile_read(self.h, ms.ctypes.data, cnt.ctypes.data))
         return ms, cnt
 

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libads_b200.so")
-SOURCES = ["kernels.cu", "abi.cu", "host_setup.cpp"]
+SOURCES = ["kernels.cu", "modal_tc.cu", "abi.cu", "host_setup.cpp"]
 HEADERS = ["kernels.cuh", "host_setup.h", os.path.join("..", "..", "include", "ads.h")]
 
 NVCC_FLAGS = [
@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False, extra=(), out=None) -> str
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         objs.append(obj)
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-lcudart", "-lnccl", "-lcublas"]
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-lcudart", "-lnccl"]
     subprocess.check_call(cmd)
     for o in objs:
         os.remove(o)

@@ -12,7 +12,6 @@
 #include <string>
 #include <vector>
 
-#include <cublas_v2.h>
 #include <nccl.h>
 
 #include "../../include/ads.h"
@@ -93,12 +92,11 @@ struct ads_ctx {
     bool graphs_off = false;
     // exact-in-time modal propagator (ads_modal_advance).  The uniform basis is
     // mirror-symmetric, so every mode is even or odd under i <-> n-1-i and each direction's maps
-    // split in halves acting on the folded line (t = [u + Ju | u - Ju], launch_mirror):
+    // split in halves acting on the folded line (t = [u + Ju | u - Ju], folded inside modal_tc.cu):
     //   forward  Q_e (ne x H), Q_o (no x h) of Q = Phi^T M;  inverse  P_e (H x ne), P_o (h x no)
     // (column-major; h = n/2, H = h + n%2).  Modal coordinates along d are ordered [even | odd |
     // unused], eigenvalues mlam in that order (0 on unused), mord = the active mode at each slot.
     bool modal_ready = false;
-    cublasHandle_t cub = nullptr;
     double *mQe[3] = {}, *mQo[3] = {}, *mPe[3] = {}, *mPo[3] = {};
     int mne[3] = {0, 0, 0}, mno[3] = {0, 0, 0};
     double *mlam[3] = {nullptr, nullptr, nullptr}, *mf[3] = {nullptr, nullptr, nullptr};
@@ -150,6 +148,18 @@ int dalloc(ads_ctx *h, void **p, size_t bytes) {
     }
     h->allocs.push_back(*p);
     return ADS_OK;
+}
+
+// release one dalloc'd buffer (after the stream has drained: launches may still read it)
+int dfree(ads_ctx *h, const void *p) {
+    for (size_t i = 0; i < h->allocs.size(); ++i)
+        if (h->allocs[i] == p) {
+            if (h->stream) cudaStreamSynchronize(h->stream);
+            cudaFree(h->allocs[i]);
+            h->allocs.erase(h->allocs.begin() + (long)i);
+            return ADS_OK;
+        }
+    return ADS_E_INVAL;
 }
 
 template <class T>
@@ -218,6 +228,8 @@ double source_g(const ads_ctx *h, double t) {
 
 // Factor A (band, Dirichlet identity rows already set) and build the device tables of
 // the partitioned sweeps (host_setup.h PartTables; kernels.cuh SolveTab).
+int dfree(ads_ctx *h, const void *p);
+
 int make_solve_tab(ads_ctx *h, const Band &A, const char *what, SolveTab &tab) {
     const int n = A.n, p = A.p;
     LUFactors f;
@@ -225,61 +237,72 @@ int make_solve_tab(ads_ctx *h, const Band &A, const char *what, SolveTab &tab) {
     // chunking: 32 chunks, or 16 chunks of at most 17 rows when that pads the line less (e.g.
     // 258 rows: 16 x 17 instead of 32 x 9 -- per-tile overheads are amortised over longer chunks),
     // or 64 chunks of at most 17 rows for lines beyond 544 rows (33-row chunks held in registers
-    // ran at a third of the bandwidth)
-    int C = kSweepChunks;
-    int L = choose_chunk_len(n, p, C);
+    // ran at a third of the bandwidth) when their tables fit the shared memory of a CTA (the
+    // identity-padded rows of 64 x 17 land in the edge-record table: p = 4, 5 lines of 577..865
+    // rows do not fit and keep 32 x 33)
+    const int L32 = choose_chunk_len(n, p, kSweepChunks);
     const int L16 = choose_chunk_len(n, p, 16), L64 = choose_chunk_len(n, p, 64);
-    if (L16 != 0 && L16 <= 17 && (L == 0 || 16 * L16 < C * L)) {
-        C = 16;
-        L = L16;
-    } else if ((L == 0 || L > 17) && L64 != 0 && L64 <= 17) {
-        C = 64;
-        L = L64;
-    }
-    if (L == 0) return fail(h, ADS_E_INVAL, "%s: n = %d has no supported chunking", what, n);
-    // pad the factors to C*L rows with identity rows: every chunk has length L
-    const int npad = C * L;
-    LUFactors fp = f;
-    fp.n = npad;
-    fp.l.resize((size_t)npad * p, 0.0);
-    fp.us.resize((size_t)npad * p, 0.0);
-    fp.dinv.resize(npad, 1.0);
-    PartTables pt;
-    build_part_tables(fp, C, L, pt);
-    int rc;
-    double *l, *us, *dinv, *Tf, *Rb;
-    if ((rc = upload(h, &l, fp.l)) || (rc = upload(h, &us, fp.us)) || (rc = upload(h, &dinv, fp.dinv)) ||
-        (rc = upload(h, &Tf, pt.Tf)) || (rc = upload(h, &Rb, pt.Rb)))
-        return rc;
-    tab = SolveTab();
-    tab.l = l;
-    tab.us = us;
-    tab.dinv = dinv;
-    tab.Tf = Tf;
-    tab.Rb = Rb;
-    tab.n = n;
-    tab.L = L;
-    tab.C = C;
-    tab.Kf = pt.Kf;
-    tab.Kb = pt.Kb;
-    // uniform region aligned to whole chunks: chunks [c_lo, c_hi) lie inside [i_lo, i_hi)
-    const int c_lo = (f.i_lo + L - 1) / L, c_hi = f.i_hi / L;
-    tab.c_lo = c_hi > c_lo ? c_lo : 0;
-    tab.c_hi = c_hi > c_lo ? c_hi : 0;
-    if (tab.c_hi > tab.c_lo) {
-        for (int k = 0; k < p; ++k) {
-            tab.lc[k] = f.l[(size_t)f.i_lo * p + k];
-            tab.usc[k] = f.us[(size_t)f.i_lo * p + k];
-        }
-        tab.dic = f.dinv[f.i_lo];
-        const int s0 = tab.c_lo * L;  // any uniform chunk: its responses are bitwise identical
-        for (int j = 0; j < L; ++j)
-            for (int m = 0; m < p; ++m) {
-                tab.Gf[j][m] = pt.gf[(size_t)(s0 + j) * p + m];
-                tab.Gb[j][m] = pt.gb[(size_t)(s0 + j) * p + m];
+    std::vector<std::pair<int, int>> cand;  // (C, L) in order of preference
+    if (L16 != 0 && L16 <= 17 && (L32 == 0 || 16 * L16 < kSweepChunks * L32)) cand.push_back({16, L16});
+    else if ((L32 == 0 || L32 > 17) && L64 != 0 && L64 <= 17) cand.push_back({64, L64});
+    if (L32 != 0) cand.push_back({kSweepChunks, L32});
+    if (cand.empty()) return fail(h, ADS_E_INVAL, "%s: n = %d has no supported chunking", what, n);
+    for (size_t ci = 0; ci < cand.size(); ++ci) {
+        const int C = cand[ci].first, L = cand[ci].second;
+        // pad the factors to C*L rows with identity rows: every chunk has length L
+        const int npad = C * L;
+        LUFactors fp = f;
+        fp.n = npad;
+        fp.l.resize((size_t)npad * p, 0.0);
+        fp.us.resize((size_t)npad * p, 0.0);
+        fp.dinv.resize(npad, 1.0);
+        PartTables pt;
+        build_part_tables(fp, C, L, pt);
+        SolveTab t;
+        t.n = n;
+        t.L = L;
+        t.C = C;
+        t.Kf = pt.Kf;
+        t.Kb = pt.Kb;
+        // uniform region aligned to whole chunks: chunks [c_lo, c_hi) lie inside [i_lo, i_hi)
+        const int c_lo = (f.i_lo + L - 1) / L, c_hi = f.i_hi / L;
+        t.c_lo = c_hi > c_lo ? c_lo : 0;
+        t.c_hi = c_hi > c_lo ? c_hi : 0;
+        if (t.c_hi > t.c_lo) {
+            for (int k = 0; k < p; ++k) {
+                t.lc[k] = f.l[(size_t)f.i_lo * p + k];
+                t.usc[k] = f.us[(size_t)f.i_lo * p + k];
             }
+            t.dic = f.dinv[f.i_lo];
+            const int s0 = t.c_lo * L;  // any uniform chunk: its responses are bitwise identical
+            for (int j = 0; j < L; ++j)
+                for (int m = 0; m < p; ++m) {
+                    t.Gf[j][m] = pt.gf[(size_t)(s0 + j) * p + m];
+                    t.Gb[j][m] = pt.gb[(size_t)(s0 + j) * p + m];
+                }
+        }
+        const long need = std::max(sweep_smem_bytes(p, t, 0), sweep_smem_bytes(p, t, 1));
+        if (need < 0 || need > kMaxSmemPerCta) {
+            if (ci + 1 < cand.size()) continue;
+            return fail(h, ADS_E_INVAL, "%s: n = %d needs %ld B of shared memory per sweep tile", what, n, need);
+        }
+        int rc;
+        double *l, *us, *dinv, *Tf, *Rb;
+        if ((rc = upload(h, &l, fp.l)) || (rc = upload(h, &us, fp.us)) || (rc = upload(h, &dinv, fp.dinv)) ||
+            (rc = upload(h, &Tf, pt.Tf)) || (rc = upload(h, &Rb, pt.Rb)))
+            return rc;
+        // tables this handle built before (ads_set_tau rebuilds them): released, not leaked
+        for (const double *old : {tab.l, tab.us, tab.dinv, tab.Tf, tab.Rb})
+            if (old) dfree(h, old);
+        t.l = l;
+        t.us = us;
+        t.dinv = dinv;
+        t.Tf = Tf;
+        t.Rb = Rb;
+        tab = t;
+        return ADS_OK;
     }
-    return ADS_OK;
+    return fail(h, ADS_E_INVAL, "%s: no chunking", what);
 }
 
 // M + c K with the Dirichlet identity rows (the matrices the sweeps invert)
@@ -416,6 +439,20 @@ int build_direction(ads_ctx *h, int d) {
     if ((rc = upload(h, &D.mband, mb)) || (rc = upload(h, &D.kband, kb)) || (rc = upload(h, &D.wzband, wz))) return rc;
     return ADS_OK;
 }
+
+// every ABI entry works on the handle's device (the one current at ads_create), and restores the
+// caller's current device on return
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(const ads_ctx *h) {
+        int cur = 0;
+        if (h && cudaGetDevice(&cur) == cudaSuccess && cur != h->device && cudaSetDevice(h->device) == cudaSuccess)
+            prev = cur;
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 int guard(ads_ctx *h) {
     if (!h) return ADS_E_INVAL;
@@ -1038,21 +1075,13 @@ int copy_out(ads_ctx *h, double *dst, const double *src, int mem) {
 // ---------------------------------------------------------------------------------------
 // exact-in-time modal propagator (§3 decomposition):
 // c = (Q_x (x) Q_y (x) Q_z) U with Q_d = Phi_d^T M_d, per-mode R1 recurrence, U = P3 c.
-// The three directional transforms are plain dense products (cuBLAS DGEMM, FP64 tensor cores).
+// The three directional transforms are dense products on the FP64 tensor cores, hand-written
+// (modal_tc.cu) with the mirror fold of the even / odd bases fused into them.
 // ---------------------------------------------------------------------------------------
-#define CUBLAS_TRY(h, call)                                                            \
-    do {                                                                               \
-        const cublasStatus_t st_ = (call);                                             \
-        if (st_ != CUBLAS_STATUS_SUCCESS) return fail(h, ADS_E_CUDA, "cuBLAS %s: status %d", #call, (int)st_); \
-    } while (0)
 
 int modal_prepare(ads_ctx *h) {
     if (h->modal_ready) return ADS_OK;
     int rc;
-    if (!h->cub) {
-        CUBLAS_TRY(h, cublasCreate(&h->cub));
-        CUBLAS_TRY(h, cublasSetStream(h->cub, h->stream));
-    }
     for (int d = 0; d < 3; ++d) {
         const int o = h->sp[d].bc == ADS_BC_DIRICHLET0 ? 1 : 0;
         const int n = h->n[d], na = n - 2 * o, hh = n / 2, H = hh + (n & 1);
@@ -1110,54 +1139,36 @@ int modal_prepare(ads_ctx *h) {
     return ADS_OK;
 }
 
-// the two half-size products of direction d: forward C = [Q_e T_even; Q_o T_odd] (T folded),
-// inverse T = [P_e C_even; P_o C_odd]; along x over the n1 n2 lines, along y per plane (batched),
-// along z over the (sy n1)-row plane matrix.  Zero-size products are skipped.
-int modal_half_products(ads_ctx *h, int d, bool inverse, const double *src, double *dst) {
-    const Geom &g = h->geo;
-    const int n = h->n[d], hh = n / 2, H = hh + (n & 1), ne = h->mne[d], no = h->mno[d];
-    const double one = 1.0, zero = 0.0;
-    // per half q (even, odd): rows of the operator, its inner size, operator, offsets of in / out
-    const int mo[2] = {inverse ? H : ne, inverse ? hh : no}, kk[2] = {inverse ? ne : H, inverse ? no : hh};
-    const double *A[2] = {inverse ? h->mPe[d] : h->mQe[d], inverse ? h->mPo[d] : h->mQo[d]};
-    const long in_off[2] = {0, inverse ? ne : H}, out_off[2] = {0, inverse ? H : ne};
-    for (int q = 0; q < 2; ++q) {
-        if (mo[q] == 0 || kk[q] == 0) continue;
-        const int lda = mo[q];
-        if (d == 0) {
-            CUBLAS_TRY(h, cublasDgemm(h->cub, CUBLAS_OP_N, CUBLAS_OP_N, mo[q], g.n1 * g.n2, kk[q], &one, A[q], lda,
-                                      src + in_off[q], (int)g.sy, &zero, dst + out_off[q], (int)g.sy));
-        } else if (d == 1) {
-            CUBLAS_TRY(h, cublasDgemmStridedBatched(h->cub, CUBLAS_OP_N, CUBLAS_OP_T, g.n0, mo[q], kk[q], &one,
-                                                    src + in_off[q] * g.sy, (int)g.sy, g.sz, A[q], lda, 0, &zero,
-                                                    dst + out_off[q] * g.sy, (int)g.sy, g.sz, g.n2));
-        } else {
-            CUBLAS_TRY(h, cublasDgemm(h->cub, CUBLAS_OP_N, CUBLAS_OP_T, (int)g.sz, mo[q], kk[q], &one,
-                                      src + in_off[q] * g.sz, (int)g.sz, A[q], lda, &zero, dst + out_off[q] * g.sz,
-                                      (int)g.sz));
-        }
-        h->launches += 1;
-    }
-    return ADS_OK;
-}
-
 // forward (modal coordinates) or inverse map of a whole field along x, y, z: in -> b, scratch a
-// (in is only read).  Forward per direction: fold (a), half products (b); inverse: half products
-// (a), unfold (b).
+// (in is only read).  Each direction is one launch of the folded tensor-core GEMMs (modal_tc.cu):
+// the mirror fold / unfold happens in the operand loads / the epilogue.
 int modal_transform(ads_ctx *h, bool inverse, const double *in, double *a, double *b) {
-    int rc;
+    const Geom &g = h->geo;
     const double *src = in;
+    double *dsts[3] = {b, a, b};  // in -> b -> a -> b
     for (int d = 0; d < 3; ++d) {
-        if (!inverse) {
-            launch_mirror(src, a, h->geo, d, 0, h->stream);
-            if ((rc = check_launch(h, "mirror"))) return rc;
-            if ((rc = modal_half_products(h, d, false, a, b))) return rc;
-        } else {
-            if ((rc = modal_half_products(h, d, true, src, a))) return rc;
-            launch_mirror(a, b, h->geo, d, 1, h->stream);
-            if ((rc = check_launch(h, "mirror"))) return rc;
+        ModalGemmArgs m;
+        m.in = src;
+        m.out = dsts[d];
+        m.n = h->n[d];
+        m.hh = m.n / 2;
+        m.H = m.hh + (m.n & 1);
+        m.ne = h->mne[d];
+        m.no = h->mno[d];
+        m.Qe = h->mQe[d], m.Qo = h->mQo[d], m.Pe = h->mPe[d], m.Po = h->mPo[d];
+        m.inverse = inverse ? 1 : 0;
+        if (d == 0) {         // x lines: contiguous rows of pitch sy
+            m.ks = 1, m.ls = g.sy, m.nl = g.n1 * g.n2, m.bs = 0, m.nb = 1;
+        } else if (d == 1) {  // y lines: adjacent in x, one batch per plane
+            m.ks = g.sy, m.ls = 1, m.nl = g.n0, m.bs = g.sz, m.nb = g.n2;
+        } else {              // z lines: every (x, y) position of a plane, row padding included (zero)
+            m.ks = g.sz, m.ls = 1, m.nl = (int)g.sz, m.bs = 0, m.nb = 1;
         }
-        src = b;
+        ProfScope ps(h, 4);
+        if (launch_modal_gemm(m, h->stream)) return fail(h, ADS_E_INVAL, "modal transform: grid too large");
+        int rc;
+        if ((rc = check_launch(h, "modal transform"))) return rc;
+        src = dsts[d];
     }
     return ADS_OK;
 }
@@ -1245,7 +1256,7 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
         if (rc == ADS_OK && (rc = dalloc(h, (void **)&h->dpartial, sizeof(double) * 1024)) == ADS_OK &&
             (rc = dalloc(h, (void **)&h->dres, sizeof(double) * 8)) == ADS_OK &&
             (rc = dalloc(h, (void **)&h->dstep, sizeof(long))) == ADS_OK) {
-            cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+            cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamDefault);
             if (e != cudaSuccess) rc = fail(h, ADS_E_CUDA, "stream: %s", cudaGetErrorString(e));
             h->own_stream = true;
         }
@@ -1328,7 +1339,7 @@ int ads_create_virtual(ads_handle *out, int nx, int ny, int nz, int p, double ta
     G->N = (long)G->n[0] * G->n[1] * G->n[2];
     cudaGetDevice(&G->device);
     int rc = ADS_OK;
-    if (cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking) != cudaSuccess) rc = ADS_E_CUDA;
+    if (cudaStreamCreateWithFlags(&G->stream, cudaStreamDefault) != cudaSuccess) rc = ADS_E_CUDA;
     G->own_stream = true;
     for (int r = 0; r < nslabs && rc == ADS_OK; ++r) {
         ads_handle m = nullptr;
@@ -1353,6 +1364,7 @@ int ads_create_virtual(ads_handle *out, int nx, int ny, int nz, int p, double ta
 }
 
 int ads_set_tau(ads_handle h, double tau) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (!(tau > 0.0) || !std::isfinite(tau)) return fail(h, ADS_E_INVAL, "ads_set_tau: tau must be > 0");
@@ -1372,6 +1384,7 @@ int ads_set_tau(ads_handle h, double tau) {
         char what[32];
         snprintf(what, sizeof what, "A_%d", d);
         if ((rc = make_solve_tab(h, A, what, h->dd[d].tab))) return rc;
+        if (h->dd[d].aband) dfree(h, h->dd[d].aband);
         if ((rc = upload(h, &h->dd[d].aband, A.v))) return rc;
     }
     if (h->have_state && h->scheme == 1) {
@@ -1386,6 +1399,7 @@ int ads_set_tau(ads_handle h, double tau) {
 }
 
 int ads_set_scheme(ads_handle h, int scheme) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (scheme != 0 && scheme != 1) return fail(h, ADS_E_INVAL, "ads_set_scheme: scheme must be 0 or 1");
@@ -1410,6 +1424,7 @@ int ads_modal_basis(int nel, int p, int bc, double *lambda, double *phi) {
 }
 
 int ads_modal_advance(ads_handle h, long nsteps) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (nsteps < 0) return fail(h, ADS_E_INVAL, "ads_modal_advance: nsteps < 0");
@@ -1466,6 +1481,7 @@ int ads_modal_advance(ads_handle h, long nsteps) {
 }
 
 int ads_local_extent(ads_handle h, int *z_begin, int *z_count) {
+    DeviceScope ds_(h);
     if (!h || !z_begin || !z_count) return ADS_E_INVAL;
     *z_begin = h->dist == 2 ? 0 : h->zbeg;
     *z_count = h->dist == 2 ? h->ngz : h->n[2];
@@ -1473,6 +1489,7 @@ int ads_local_extent(ads_handle h, int *z_begin, int *z_count) {
 }
 
 int ads_set_stream(ads_handle h, void *stream) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -1482,7 +1499,7 @@ int ads_set_stream(ads_handle h, void *stream) {
         next = (cudaStream_t)stream;
         own = false;
     } else if (!h->own_stream) {
-        CUDA_TRY(h, cudaStreamCreateWithFlags(&next, cudaStreamNonBlocking));
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&next, cudaStreamDefault));
         own = true;
     }
     // the members of a virtual slab group run on the group's stream: move them while the old
@@ -1492,11 +1509,11 @@ int ads_set_stream(ads_handle h, void *stream) {
     if (h->own_stream && old != next) cudaStreamDestroy(old);
     h->stream = next;
     h->own_stream = own;
-    if (h->cub) cublasSetStream(h->cub, h->stream);
     return ADS_OK;
 }
 
 int ads_load_vector(ads_handle h, int d, int func, double c, double sigma, double *out) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (d < 0 || d > 2 || !out || (func != ADS_FUNC_SIN && func != ADS_FUNC_GAUSS) ||
@@ -1507,6 +1524,7 @@ int ads_load_vector(ads_handle h, int d, int func, double c, double sigma, doubl
 }
 
 int ads_mass_solve_1d(ads_handle h, int d, double *x) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (d < 0 || d > 2 || !x) return fail(h, ADS_E_INVAL, "ads_mass_solve_1d: bad argument");
@@ -1516,6 +1534,7 @@ int ads_mass_solve_1d(ads_handle h, int d, double *x) {
 
 int ads_set_source(ads_handle h, const double *bx, const double *by, const double *bz, int wavelet, double f0,
                    double t0, double amp) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (!bx) {
@@ -1550,6 +1569,7 @@ int ads_set_source(ads_handle h, const double *bx, const double *by, const doubl
 }
 
 int ads_set_state(ads_handle h, const double *u, const double *udot, int mem) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (!u || (mem != ADS_MEM_HOST && mem != ADS_MEM_DEVICE)) return fail(h, ADS_E_INVAL, "ads_set_state: bad argument");
@@ -1576,6 +1596,7 @@ int ads_set_state(ads_handle h, const double *u, const double *udot, int mem) {
 
 int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const int *cmp, const double *sx,
                             const double *sy, const double *sz) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (nterms < 0 || (nterms > 0 && (!amp || !sx || !sy || !sz)))
@@ -1618,6 +1639,7 @@ int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const i
 }
 
 int ads_step(ads_handle h, int nsteps) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (nsteps < 0) return fail(h, ADS_E_INVAL, "nsteps < 0");
@@ -1661,6 +1683,7 @@ int ads_step(ads_handle h, int nsteps) {
 }
 
 int ads_energy(ads_handle h, double out[3]) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (!out) return fail(h, ADS_E_INVAL, "ads_energy: out is NULL");
@@ -1679,6 +1702,7 @@ int ads_energy(ads_handle h, double out[3]) {
 }
 
 int ads_get_state(ads_handle h, double *u, double *udot, double *a, int mem) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (mem != ADS_MEM_HOST && mem != ADS_MEM_DEVICE) return fail(h, ADS_E_INVAL, "bad mem");
@@ -1704,6 +1728,7 @@ double ads_time(ads_handle h) { return h ? time_at(h, h->step) : NAN; }
 long ads_step_count(ads_handle h) { return h ? h->step : -1; }
 
 int ads_dims(ads_handle h, int *nx, int *ny, int *nz, int *ncomp) {
+    DeviceScope ds_(h);
     if (!h) return ADS_E_INVAL;
     if (nx) *nx = h->n[0];
     if (ny) *ny = h->n[1];
@@ -1715,16 +1740,19 @@ int ads_dims(ads_handle h, int *nx, int *ny, int *nz, int *ncomp) {
 // Unit operators act on dense caller device arrays: copy into a pitched work field,
 // run the kernels, copy back out.
 int ads_apply_k(ads_handle h, const double *x, double *out) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (h->dist) return fail(h, ADS_E_INVAL, "unit operators: single-GPU handles only");
     if (!x || !out || x == out) return fail(h, ADS_E_INVAL, "ads_apply_k: bad pointers");
+    // U2 (the drift's ping-pong buffer) and W are scratch between steps: the state (U, V, A) is
+    // left intact, so get_state and the energies stay valid after a unit operation
     for (int c = 0; c < h->ncomp; ++c)
         if ((rc = copy_in(h, comp(h->U2, h, c), x + c * h->N, ADS_MEM_DEVICE))) return rc;
     if (h->ncomp == 3) {
-        if ((rc = ups_apply(h, h->U2, h->U2, 0.0, nullptr, h->A, 1.0))) return rc;
+        if ((rc = ups_apply(h, h->U2, h->U2, 0.0, nullptr, h->W, 1.0))) return rc;
         for (int c = 0; c < 3; ++c)
-            if ((rc = copy_out(h, out + c * h->N, comp(h->A, h, c), ADS_MEM_DEVICE))) return rc;
+            if ((rc = copy_out(h, out + c * h->N, comp(h->W, h, c), ADS_MEM_DEVICE))) return rc;
         return ADS_OK;
     }
     if ((rc = run_kop(h, h->U2, h->U2, 0.0, 0.0, 1.0, nullptr, h->R))) return rc;
@@ -1732,16 +1760,17 @@ int ads_apply_k(ads_handle h, const double *x, double *out) {
 }
 
 int ads_solve_d(ads_handle h, const double *x, double *out) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (h->dist) return fail(h, ADS_E_INVAL, "unit operators: single-GPU handles only");
     if (!x || !out) return fail(h, ADS_E_INVAL, "ads_solve_d: bad pointers");
-    if (h->ncomp == 3) {
+    if (h->ncomp == 3) {  // U2 as the work field (el_dsolve's own scratch is W): A, the state, is kept
         for (int c = 0; c < 3; ++c)
-            if ((rc = copy_in(h, comp(h->A, h, c), x + c * h->N, ADS_MEM_DEVICE))) return rc;
-        if ((rc = el_dsolve(h, h->A))) return rc;
+            if ((rc = copy_in(h, comp(h->U2, h, c), x + c * h->N, ADS_MEM_DEVICE))) return rc;
+        if ((rc = el_dsolve(h, h->U2))) return rc;
         for (int c = 0; c < 3; ++c)
-            if ((rc = copy_out(h, out + c * h->N, comp(h->A, h, c), ADS_MEM_DEVICE))) return rc;
+            if ((rc = copy_out(h, out + c * h->N, comp(h->U2, h, c), ADS_MEM_DEVICE))) return rc;
         return ADS_OK;
     }
     if ((rc = copy_in(h, h->R, x, ADS_MEM_DEVICE))) return rc;
@@ -1752,6 +1781,7 @@ int ads_solve_d(ads_handle h, const double *x, double *out) {
 }
 
 int ads_sweep(ads_handle h, int d, const double *x, double *out) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (!x || !out || d < 0 || d > 2) return fail(h, ADS_E_INVAL, "ads_sweep: bad argument");
@@ -1769,6 +1799,7 @@ long ads_launch_count(ads_handle h) {
 }
 
 int ads_profile_enable(ads_handle h, int on) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     for (ads_ctx *m : h->members)
@@ -1781,6 +1812,7 @@ int ads_profile_enable(ads_handle h, int on) {
 }
 
 int ads_profile_read(ads_handle h, double *ms, long *count) {
+    DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
     if (!ms || !count) return fail(h, ADS_E_INVAL, "ads_profile_read: NULL output");
@@ -1804,12 +1836,12 @@ int ads_profile_read(ads_handle h, double *ms, long *count) {
 const char *ads_last_error(ads_handle h) { return h ? h->err.c_str() : "null handle"; }
 
 int ads_destroy(ads_handle h) {
+    DeviceScope ds_(h);
     if (!h) return ADS_OK;
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (ads_ctx *m : h->members) ads_destroy(m);
     h->members.clear();
     drop_graphs(h);
-    if (h->cub) cublasDestroy(h->cub);
     if (h->comm && h->dist == 1) ncclCommDestroy(h->comm);
     for (void *p : h->allocs) cudaFree(p);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);

@@ -21,10 +21,43 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "kernels.cuh"
 
 namespace ads {
+
+// Per-device launch facts of a kernel at a dynamic shared-memory size, cached and thread-safe:
+// the SM count, the resident CTAs per SM, and the >48 KB opt-in (raised to the largest size the
+// kernel has been launched with on that device).
+struct LaunchFacts {
+    int nsm = 1, per_sm = 1;
+};
+static LaunchFacts launch_facts(const void *fn, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void *, size_t>, LaunchFacts> cache;
+    static std::map<std::pair<int, const void *>, size_t> optin;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(dev, fn, smem);
+    const auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    size_t &cur = optin[{dev, fn}];
+    if (smem > cur) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cur = smem;
+    }
+    LaunchFacts f;
+    cudaDeviceGetAttribute(&f.nsm, cudaDevAttrMultiProcessorCount, dev);
+    int ps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, threads, smem);
+    f.per_sm = std::max(ps, 1);
+    cache[key] = f;
+    return f;
+}
 
 // ------------------------------------------------------------------------------------------
 // partitioned banded sweeps (v3)
@@ -237,6 +270,21 @@ __host__ __device__ inline long sweep_smem_doubles(const SolveTab &t, bool xdir,
     }
     (void)kick;
     return fixed + (1L + vbufs) * t.C * t.L * LW + 16 + 4;
+}
+
+// dynamic shared memory of a sweep launch (the tile width and buffers sweep_launch picks, one
+// output buffer): lets the host reject chunkings whose tables do not fit before a launch fails
+long sweep_smem_bytes(int p, const SolveTab &t, int dir) {
+    const bool X = dir == 0;
+    const bool narrow = X || t.L > 17 || t.C > 32;
+    long d = 0;
+#define ADS_SSB(PP)                                                                                   \
+    case PP:                                                                                         \
+        d = narrow ? sweep_smem_doubles<PP, 8>(t, X, 0, false, 1) : sweep_smem_doubles<PP, 16>(t, X, 0, false, 1); \
+        break;
+    switch (p) { ADS_SSB(1) ADS_SSB(2) ADS_SSB(3) ADS_SSB(4) ADS_SSB(5) default: return -1; }
+#undef ADS_SSB
+    return d * (long)sizeof(double);
 }
 
 template <int P, int L, bool XDIR, int LW, int C>
@@ -1514,15 +1562,10 @@ static void kron3_launch(const double *in, double *out, const KronTerms &k3, dou
                          cudaStream_t s) {
     using G = KronGeo<P, T>;
     const size_t sm = sizeof(double) * G::SMEM;
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaFuncSetAttribute(kron3_kernel<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kron3_kernel<P, T>, KR_THREADS, sm);
-        per_sm = std::max(per_sm, 1);
-    }
+    const LaunchFacts lf = launch_facts((const void *)kron3_kernel<P, T>, KR_THREADS, sm);
     const int gx = (g.n0 + KR_X - 1) / KR_X, gy = (g.n1 + KR_Y - 1) / KR_Y;
     // z pieces by the fluid wave model of kop_launch (each piece reads 2p halo planes)
-    const long resident = (long)per_sm * 148, tiles = (long)gx * gy;
+    const long resident = (long)lf.per_sm * lf.nsm, tiles = (long)gx * gy;
     int best = 1;
     double best_cost = 1e300;
     for (int nz = 1; nz <= 64; ++nz) {
@@ -1663,6 +1706,7 @@ __global__ void dot_final_kernel(const double *partial, double *res) {
 // ------------------------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------------------------
+
 static int grid_for(long N) {
     long b = (N + 255) / 256;
     return (int)(b < 148 * 32 ? (b < 1 ? 1 : b) : 148 * 32);
@@ -1705,18 +1749,13 @@ static int kop_launch(const KopArgs &a, cudaStream_t s) {
         b.zv0 = 0;
         b.zv1 = a.geo.n2;
     }
-    int dev = 0, nsm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (v3) {
         using G = KopGeo<P>;
         const size_t sm = sizeof(double) * G::SMEM;
-        cudaFuncSetAttribute(kop_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kop_kernel<P>, KT_THREADS, sm);
+        const LaunchFacts lf = launch_facts((const void *)kop_kernel<P>, KT_THREADS, sm);
         const int ox = kop_origin(a.ilo[0], a.ihi[0], KT_X), oy = kop_origin(a.ilo[1], a.ihi[1], KT_Y);
         const int gx = (a.geo.n0 - ox + KT_X - 1) / KT_X, gy = (a.geo.n1 - oy + KT_Y - 1) / KT_Y;
-        const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)std::max(per_sm, 1) * nsm);
+        const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)lf.per_sm * lf.nsm);
         b.zlen = a.zlen > 0 ? a.zlen : (a.geo.n2 + nz - 1) / nz;
         dim3 grd(gx, gy, (a.geo.n2 + b.zlen - 1) / b.zlen);
         kop_kernel<P><<<grd, KT_THREADS, sm, s>>>(b);
@@ -1724,12 +1763,10 @@ static int kop_launch(const KopArgs &a, cudaStream_t s) {
     }
     using G = K4Geo<P>;
     const size_t sm = sizeof(double) * G::SMEM;
-    cudaFuncSetAttribute(kop4_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kop4_kernel<P>, K4_THREADS, sm);
+    const LaunchFacts lf = launch_facts((const void *)kop4_kernel<P>, K4_THREADS, sm);
     const int ox = kop_origin(a.ilo[0], a.ihi[0], K4_X), oy = kop_origin(a.ilo[1], a.ihi[1], K4_Y);
     const int gx = (a.geo.n0 - ox + K4_X - 1) / K4_X, gy = (a.geo.n1 - oy + K4_Y - 1) / K4_Y;
-    const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)std::max(per_sm, 1) * nsm);
+    const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)lf.per_sm * lf.nsm);
     b.zlen = a.zlen > 0 ? a.zlen : (a.geo.n2 + nz - 1) / nz;
     // U and V over the planes that exist in memory, [zv0, zv1) (slabs: halo planes included)
     Geom gm = a.geo;
@@ -1791,23 +1828,12 @@ static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
     const int vbufs = (!X && sizeof(double) * sweep_smem_doubles<P, LW>(a.t, X, a.geo.sy, a.mode != 0, 2) <= 227 * 1024)
                           ? 2 : 1;
     const size_t sm = sizeof(double) * (size_t)sweep_smem_doubles<P, LW>(a.t, X, a.geo.sy, a.mode != 0, vbufs);
-    static int nsm = 0;
-    static size_t sm_set = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    if (sm > sm_set) {
-        cudaFuncSetAttribute(sweep_kernel<P, L, X, LW, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        sm_set = sm;
-    }
+    if (sm > (size_t)kMaxSmemPerCta) return -1;
+    const LaunchFacts lf = launch_facts((const void *)sweep_kernel<P, L, X, LW, C>, NT, sm);
     long ntiles;
     if (X) ntiles = ((long)g.n1 * g.n2 + LW - 1) / LW;
     else ntiles = (long)((g.n0 + LW - 1) / LW) * (a.dir == 1 ? g.n2 : g.n1);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<P, L, X, LW, C>, NT, sm);
-    const long cap = (long)std::max(per_sm, 1) * nsm;
+    const long cap = (long)lf.per_sm * lf.nsm;
     dim3 grd((unsigned)std::min(ntiles, cap));
     SweepArgs b = a;
     b.vbufs = vbufs;
@@ -2022,44 +2048,6 @@ __global__ void repack_kernel(const double *__restrict__ src, double *__restrict
 
 void launch_repack(const double *src, double *dst, const Geom &g, int to_pitched, cudaStream_t s) {
     repack_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(src, dst, g, to_pitched);
-}
-
-__global__ void mirror_kernel(const double *__restrict__ src, double *__restrict__ dst, Geom g, int d, int unfold) {
-    const int n[3] = {g.n0, g.n1, g.n2};
-    const long st[3] = {1, g.sy, g.sz};
-    const int m = n[d], h = m / 2, H = h + (m & 1);
-    int e[3] = {n[0], n[1], n[2]};
-    e[d] = H;  // threads cover the first H positions along d
-    const long N = (long)e[0] * e[1] * e[2];
-    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x) {
-        int c[3];
-        c[0] = (int)(q % e[0]);
-        const long t = q / e[0];
-        c[1] = (int)(t % e[1]);
-        c[2] = (int)(t / e[1]);
-        const int i = c[d];
-        c[d] = 0;
-        const long base = c[0] * st[0] + c[1] * st[1] + c[2] * st[2], sd = st[d];
-        if (i < h) {
-            if (!unfold) {
-                const double a = src[base + i * sd], b = src[base + (long)(m - 1 - i) * sd];
-                dst[base + i * sd] = a + b;
-                dst[base + (long)(H + i) * sd] = a - b;
-            } else {
-                const double a = src[base + i * sd], b = src[base + (long)(H + i) * sd];
-                dst[base + i * sd] = a + b;
-                dst[base + (long)(m - 1 - i) * sd] = a - b;
-            }
-        } else {  // the middle position of an odd axis
-            dst[base + i * sd] = src[base + i * sd];
-        }
-    }
-}
-
-void launch_mirror(const double *src, double *dst, const Geom &g, int d, int unfold, cudaStream_t s) {
-    int e[3] = {g.n0, g.n1, g.n2};
-    e[d] = e[d] / 2 + (e[d] & 1);
-    mirror_kernel<<<grid_for((long)e[0] * e[1] * e[2]), 256, 0, s>>>(src, dst, g, d, unfold);
 }
 
 }  // namespace ads

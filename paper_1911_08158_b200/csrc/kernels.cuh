@@ -124,11 +124,19 @@ int launch_modal(double *cU, double *cV, double *ca, const double *lx, const dou
                  const double *fx, const double *fy, const double *fz, const double *g, long nsteps, double tau,
                  const Geom &geo, cudaStream_t s);
 void launch_set_long(long *dst, long value, cudaStream_t s);
-// Mirror fold along axis d (modal transforms, f3): with m the axis length, h = m / 2, H = h + m % 2,
-// fold: t_i = u_i + u_{m-1-i} (i < h), t_h = u_h (m odd), t_{H+i} = u_i - u_{m-1-i} (i < h);
-// unfold (the inverse map of the even/odd parts): u_i = t_i + t_{H+i}, u_{m-1-i} = t_i - t_{H+i},
-// u_h = t_h.  Positions are taken along axis d of the pitched field (x < n0).
-void launch_mirror(const double *src, double *dst, const Geom &g, int d, int unfold, cudaStream_t s);
+// The folded modal transforms along one axis as FP64 tensor-core GEMMs (modal_tc.cu, f3):
+// forward out[slots] = [Q_e fold_e(in); Q_o fold_o(in); 0], inverse out = unfold(P_e in_e, P_o in_o).
+// Element k of line l in batch b at k ks + l ls + b bs (nl lines, nb batches); maps column-major.
+struct ModalGemmArgs {
+    const double *in = nullptr;
+    double *out = nullptr;
+    long ks = 1, ls = 1, bs = 0;
+    int nl = 0, nb = 1;
+    int n = 0, ne = 0, no = 0, H = 0, hh = 0;
+    const double *Qe = nullptr, *Qo = nullptr, *Pe = nullptr, *Po = nullptr;
+    int inverse = 0;
+};
+int launch_modal_gemm(const ModalGemmArgs &g, cudaStream_t s);
 // dense caller layout (n0 n1 n2, x fastest) <-> pitched field (sy, sz): to_pitched = 1 unpacks
 void launch_repack(const double *src, double *dst, const Geom &g, int to_pitched, cudaStream_t s);
 // Solve along a direction of line length 1 (the 2D scheme's third axis): x = scale in, then the
@@ -136,6 +144,9 @@ void launch_repack(const double *src, double *dst, const Geom &g, int to_pitched
 void launch_line1(const double *in, double *out, double *V, double scale, double kick, long *inc, const Geom &g,
                   cudaStream_t s);
 int launch_sweep(int p, const SweepArgs &a, cudaStream_t s);
+// dynamic shared memory (bytes) a sweep along dir needs for these tables (one output buffer)
+long sweep_smem_bytes(int p, const SolveTab &t, int dir);
+constexpr long kMaxSmemPerCta = 227L * 1024;
 
 // Small helpers (diagnostics / state I/O, not on the per-step path).
 // out = alpha (A along axis d) in + beta out (band table [n_d][2p+1]; beta == 0: out not read).

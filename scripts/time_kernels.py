@@ -10,7 +10,7 @@ import torch  # noqa: E402
 import paper_1911_08158_b200 as ads  # noqa: E402
 import workloads  # noqa: E402
 
-NAMES = ["kop", "sweep x", "sweep y", "sweep z+kick"]
+NAMES = ["kop", "sweep x", "sweep y", "sweep z+kick", "modal transform"]
 for cfg in (sys.argv[1:] or ["c4"]):
     wl = workloads.get(cfg)
     s = ads.make_solver(wl)

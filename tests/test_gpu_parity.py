@@ -481,3 +481,79 @@ def test_maximum_grid_properties(ads):
     s.close()
     del u
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("p,n", [(4, 600), (5, 600), (5, 865), (4, 590)])
+def test_long_lines_high_degree_fit_shared_memory(ads, p, n):
+    """p = 4, 5 lines of 577..865 rows (the 64 x 17 chunking's tables overflowed a CTA's
+    shared memory there): the handle picks a chunking that fits and the sweeps along that axis
+    match a dense solve, in x, y and z."""
+    import torch
+    for axis in range(3):
+        nel = [3, 4, 5]
+        nel[axis] = n - p
+        s = ads.Solver(tuple(nel), p, 1e-3, 1)
+        o = oracle.PWave(tuple(nel), p, 1e-3, 1)
+        x = workloads.random_field(11 + axis, s.N).reshape(s.shape)
+        xd = _dev(x)
+        out = torch.empty_like(xd)
+        s.solve_d(xd, out)
+        torch.cuda.synchronize()
+        assert rel(out.cpu().numpy(), o.dsolve(x)) < OP_TOL, (p, n, axis)
+
+
+def test_default_stream_ordering(ads):
+    """With PyTorch's default stream (set_stream() / current_stream().cuda_stream == 0) the library
+    works on its own blocking stream, ordered against the legacy default stream: device tensors
+    written by PyTorch right before a call are seen, and outputs are complete for PyTorch right
+    after it, with no explicit synchronisation."""
+    import torch
+    wl = workloads.get("c1")
+    g = ads.Solver(wl.nel, wl.p, wl.tau, wl.bc)
+    g.set_stream(torch.cuda.current_stream())
+    u0 = oracle.project_separable(wl)
+    big = torch.empty(1 << 26, dtype=torch.float64, device="cuda")
+    for rep in range(3):
+        ud = torch.zeros(g.shape, dtype=torch.float64, device="cuda")
+        big.normal_()  # queue a long kernel on the default stream first
+        ud.copy_(torch.from_numpy(u0).cuda(non_blocking=False) * (rep + 1))
+        out = torch.empty_like(ud)
+        g.apply_k(ud, out)
+        out2 = out * 1.0  # consumed on the default stream immediately
+        ref = oracle.PWave(wl.nel, wl.p, wl.tau, wl.bc).kapply(u0 * (rep + 1))
+        assert rel(out2.cpu().numpy(), ref) < OP_TOL
+
+
+def test_elastic_unit_ops_keep_state(ads):
+    """Unit operators on a stepped elasticity handle leave its state alone (they used A,
+    which holds a_n, as scratch): get_state and the energies are unchanged by them."""
+    import torch
+    wl = workloads.get("c5").scaled(8, 3)
+    g = ads.make_solver(wl)
+    g.step(3)
+    st0, e0 = g.get_state(), g.energy()
+    x = _dev(workloads.random_field(3, 3 * g.N).reshape(g.shape))
+    out = torch.empty_like(x)
+    g.apply_k(x, out)
+    g.solve_d(x, out)
+    torch.cuda.synchronize()
+    st1, e1 = g.get_state(), g.energy()
+    for a, b in zip(st0, st1):
+        assert np.array_equal(a, b)
+    assert np.array_equal(e0, e1)
+
+
+def test_set_tau_releases_tables(ads):
+    """Repeated ads_set_tau calls reuse device memory (each call leaked the old factor
+    tables until destroy)."""
+    import torch
+    wl = workloads.get("c2").scaled(40, 0)
+    g = ads.make_solver(wl)
+    g.set_tau(wl.tau * 0.9)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for k in range(30):
+        g.set_tau(wl.tau * (0.5 + 0.01 * k))
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 4 << 20, (free0 - free1)
