@@ -44,12 +44,10 @@ METRIC = "P-wave DOF-steps/sec (fp64)"
 UNIT = "DOF-steps/s"
 FALLBACK_HBM_GBS = 6650.0
 # algorithmic HBM bytes per DOF for one launch of each kernel class:
-#   kop: read U, V; write P, r            -> 4 x 8 B
-#   sweep x, sweep y: read in; write out  -> 2 x 8 B
-#   sweep z + kick: read r, V; write V    -> 3 x 8 B (+8 B for a on the last step of a batch)
+#   reported by the library (ads_step_bytes): kop 32 (U, V -> P, r), sweeps x, y 16 each,
+#   sweep z + kick 24 (+8 B for a on the last step of a batch)
 KERNELS = ["kop", "sweep_x", "sweep_y", "sweep_z_kick"]
 C4_DOFS = 515 ** 3  # the committed traffic captures are of config c4 on one GPU
-BYTES_PER_DOF = [32.0, 16.0, 16.0, 24.0]
 
 
 def peaks():
@@ -181,8 +179,6 @@ def host_info():
     return {"cpu_model": model, "nproc": os.cpu_count(), "oracle_threads": 1}
 
 
-# plan bytes per DOF-step of the P-wave step: kop 32, x/y sweeps 16 each, z + kick 24
-STEP_PLAN_BYTES = 88.0
 
 
 def config_table(ads, torch, hbm):
@@ -208,8 +204,11 @@ def config_table(ads, torch, hbm):
             ts.append(e0.elapsed_time(e1) / K)
         ms = statistics.median(ts)
         d = {"us_per_step": 1e3 * ms, "dof": wl.ndof, "dof_steps_per_s": wl.ndof / (ms / 1e3), "steps_timed": K}
-        if not wl.elastic:
-            d["plan_hbm_frac"] = STEP_PLAN_BYTES * wl.ndof / (ms / 1e3) / 1e9 / hbm
+        if not wl.elastic:  # the handle's own step plan (ads_step_bytes), and the 64 B/DOF floor
+            plan = float(sum(s.step_bytes()))
+            d["plan_bytes_per_dof"] = plan
+            d["plan_hbm_frac"] = plan * wl.ndof / (ms / 1e3) / 1e9 / hbm
+            d["floor_hbm_frac"] = 64.0 * wl.ndof / (ms / 1e3) / 1e9 / hbm
         out[name] = d
         s.close()
         del s
@@ -313,16 +312,18 @@ def run_ours(args, rank, world, local):
     dom = int(np.argmax(kms))
     per_launch_ms = kms / np.maximum(kcnt, 1)
     Nloc = s.N  # this rank's DOFs (the per-kernel rooflines are per GPU)
+    plan = s.step_bytes()  # algorithmic bytes per DOF of each kernel class of this handle's step
+    kick = 3  # the z sweep carries the kick
     kernels = {}
     for i, name in enumerate(KERNELS):
-        bpd = BYTES_PER_DOF[i]
-        if i == 3:  # a is stored on the last step of a batch only
-            bpd = BYTES_PER_DOF[i] + 8.0 / max(kcnt[i], 1)
+        bpd = plan[i]
+        if i == kick:  # a is stored on the last step of a batch only
+            bpd = plan[i] + 8.0 / max(kcnt[i], 1)
         gbs = Nloc * bpd / (per_launch_ms[i] / 1e3) / 1e9 if per_launch_ms[i] > 0 else 0.0
         kernels[name] = {"ms_per_launch": per_launch_ms[i], "launches": int(kcnt[i]), "share": float(shares[i]),
                          "bytes_per_dof": bpd, "achieved_gbs": gbs, "frac": gbs / hbm}
     achieved = kernels[KERNELS[dom]]["achieved_gbs"]
-    step_bytes = Nloc * (sum(BYTES_PER_DOF) + 8.0 / args.steps)
+    step_bytes = Nloc * (sum(plan) + 8.0 / args.steps)
     traffic, traffic_src = ncu_traffic(KERNELS[dom], Nloc)
     roofline = {"bound": "hbm", "kernel": KERNELS[dom], "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "peak_kind": peak_kind,

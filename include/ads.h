@@ -232,6 +232,12 @@ long ads_launch_count(ads_handle h);
 int ads_profile_enable(ads_handle h, int on);
 int ads_profile_read(ads_handle h, double *ms, long *count);
 
+/* Algorithmic HBM bytes per DOF of one launch of each step kernel class of this handle's
+ * P-wave step (host array of ADS_NPROF entries; the roofline numerators of bench.py):
+ * kop 32 (reads U, V; writes P, r), sweep x 16, sweep y 16, sweep z + kick 24 (+8 on the last
+ * step of a batch, which keeps a).  Zeros for elasticity handles. */
+int ads_step_bytes(ads_handle h, double *bytes_per_dof);
+
 /* Last error message of the handle ("" if none); valid until the next call. */
 const char *ads_last_error(ads_handle h);
 

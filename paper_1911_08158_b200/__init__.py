@@ -29,7 +29,7 @@ EXPORTS = [
     "ads_create", "ads_create_elastic", "ads_set_stream", "ads_load_vector", "ads_mass_solve_1d",
     "ads_set_source", "ads_set_state", "ads_set_state_separable", "ads_step", "ads_energy", "ads_get_state",
     "ads_time", "ads_step_count", "ads_dims", "ads_apply_k", "ads_solve_d", "ads_sweep", "ads_launch_count",
-    "ads_last_error", "ads_destroy", "ads_profile_enable", "ads_profile_read",
+    "ads_last_error", "ads_destroy", "ads_profile_enable", "ads_profile_read", "ads_step_bytes",
     "ads_get_unique_id", "ads_slab_plan", "ads_create_dist", "ads_create_virtual", "ads_local_extent",
     "ads_modal_basis", "ads_modal_advance", "ads_set_scheme", "ads_set_tau",
 ]
@@ -76,6 +76,7 @@ def lib():
             "ads_destroy": (_I, [_H]),
             "ads_profile_enable": (_I, [_H, _I]),
             "ads_profile_read": (_I, [_H, _VP, _VP]),
+            "ads_step_bytes": (_I, [_H, _VP]),
             "ads_get_unique_id": (_I, [_VP]),
             "ads_slab_plan": (_I, [_I, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
             "ads_create_dist": (_I, [ctypes.POINTER(_H), _I, _I, _I, _I, _D, _I, _I, _I, _VP, _I]),
@@ -302,6 +303,12 @@ class Solver:
         cnt = np.zeros(5, dtype=np.int64)
         self._check(lib().ads_profile_read(self.h, ms.ctypes.data, cnt.ctypes.data))
         return ms, cnt
+
+    def step_bytes(self):
+        """Algorithmic HBM bytes per DOF of each step kernel class (kop, sweep x, y, z; ads_step_bytes)."""
+        b = np.zeros(5)
+        self._check(lib().ads_step_bytes(self.h, b.ctypes.data))
+        return b[:4]
 
     # unit operations on torch device tensors
     def apply_k(self, x, out):

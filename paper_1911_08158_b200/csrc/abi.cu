@@ -1798,6 +1798,18 @@ long ads_launch_count(ads_handle h) {
     return n;
 }
 
+int ads_step_bytes(ads_handle h, double bytes_per_dof[ADS_NPROF]) {
+    DeviceScope ds_(h);
+    int rc = guard(h);
+    if (rc) return rc;
+    if (!bytes_per_dof) return fail(h, ADS_E_INVAL, "ads_step_bytes: NULL output");
+    for (int c = 0; c < ADS_NPROF; ++c) bytes_per_dof[c] = 0.0;
+    if (h->ncomp != 1) return ADS_OK;
+    // kop: U, V -> P, r; sweeps x, y: in -> out; sweep z + kick: r, V -> V (+8 B when a is kept)
+    bytes_per_dof[0] = 32.0, bytes_per_dof[1] = 16.0, bytes_per_dof[2] = 16.0, bytes_per_dof[3] = 24.0;
+    return ADS_OK;
+}
+
 int ads_profile_enable(ads_handle h, int on) {
     DeviceScope ds_(h);
     int rc = guard(h);

@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(SW<LW, C>::THREADS, 512 / SW<LW, C>::THREADS)
         const int nb = a.dir == 1 ? g.n2 : g.n1;
         const int nib = (g.n0 + SW_LW - 1) / SW_LW;
         const long ntiles = (long)nib * nb;
-        const bool kick = a.mode != 0;
+        const bool kick = a.mode == 1;
         const int nv = max(0, min(L, n - s));  // rows of my chunk inside the line
         // buffers (128-byte aligned) and two mbarriers after them
         double *ibase = buf + ((128 - (reinterpret_cast<uintptr_t>(buf) & 127)) & 127) / sizeof(double);
@@ -888,21 +888,24 @@ __device__ __forceinline__ void k4_wait(unsigned mb, unsigned parity) {
         " @!P1 bra K4W_%=;\n}\n" ::"r"(mb), "r"(parity) : "memory");
 }
 
-// stage A of input plane kk: P tile, D = P - P_prev tile (so_[m] / po_[m]: staging / tile offsets
-// of slot m, -1: none; pv[m]: the previous plane's P at slot m)
-template <int P>
+// stage A of input plane kk: P tile, D = P - P_prev tile, owned P to HBM (so_[m] / po_[m] / go_[m]:
+// staging / tile / global offsets of slot m, -1: none or not owned; pv[m]: the previous plane's P).
+// LIVE: the plane exists in memory; ZDIR: a zero-Dirichlet z face (outside the restricted space:
+// it counts as zero in the plane differences)
+template <int P, bool LIVE, bool ZDIR>
 __device__ __forceinline__ void k4_stage_a(const KopArgs &a, double (&pv)[K4Geo<P>::SA], const int (&so_)[K4Geo<P>::SA],
-                                           const int (&po_)[K4Geo<P>::SA], int sbase, int pbase, int dbase, bool live,
-                                           bool zdir) {
+                                           const int (&po_)[K4Geo<P>::SA], const long (&go_)[K4Geo<P>::SA], int sbase,
+                                           int pbase, int dbase, double *pout) {
     using G = K4Geo<P>;
 #pragma unroll
     for (int m = 0; m < G::SA; ++m) {
         if (G::NA % K4_THREADS != 0 && m == G::SA - 1 && po_[m] < 0) break;
-        const double p = live ? fma(a.tau, k4_smem[sbase + G::STG + so_[m]], k4_smem[sbase + so_[m]]) : 0.0;
-        const double pz = zdir ? 0.0 : p;  // a zero-Dirichlet z face: outside the restricted space
+        const double p = LIVE ? fma(a.tau, k4_smem[sbase + G::STG + so_[m]], k4_smem[sbase + so_[m]]) : 0.0;
+        const double pz = ZDIR ? 0.0 : p;
         k4_smem[pbase + po_[m]] = p;
         k4_smem[dbase + po_[m]] = pz - pv[m];
         pv[m] = pz;
+        if (pout && go_[m] >= 0) pout[go_[m]] = p;
     }
 }
 
@@ -969,7 +972,7 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
             const int yr = e / (2 * W), m = (e / W) & 1, c = e % W, Y = y0 + yr;
             yb[e] = (Y >= 0 && Y < n1) ? (m ? a.kw[1] : 1.0) * __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
         }
-    const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;
+    const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;  // input planes z0 - P .. z1 + P - 1
     if (tid == 0) {
         for (int i = 0; i < K4_NPF; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb0 + 8u * i) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -1005,11 +1008,16 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
 
     // stage-A slot offsets (staging, P/D tiles) and previous P; stage-C rings (pending output planes)
     int so_[G::SA], po_[G::SA];
+    long go_[G::SA];
 #pragma unroll
     for (int m = 0; m < G::SA; ++m) {
         const int e = tid + K4_THREADS * m, hy = e / NC, hx = e - hy * NC;
         so_[m] = e < G::NA ? hy * G::HXE + hx + (G::PA - P) : -1;
         po_[m] = e < G::NA ? hy * PP + hx : -1;
+        const int X = x0 - P + hx, Y = y0 - P + hy;  // owned: inside the output tile and the grid
+        const bool own = e < G::NA && hx >= P && hx < P + K4_X && hy >= P && hy < P + K4_Y && X >= 0 && X < n0 &&
+                         Y >= 0 && Y < n1;
+        go_[m] = own ? (long)Y * sy + X : -1;
     }
     double pv[G::SA], A0[W], A1[W];
 #pragma unroll
@@ -1033,9 +1041,6 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
     double *rq = a.r + (long)(y0 + yr0) * sy + X + (long)z0 * sz;
     // stage-B column item (threads [0, NCOL)) and row item (warps [CW, 8)) constants
     const int nc = tid % NC, g4 = tid / NC;
-    const int Xc = x0 - P + nc;
-    const bool pown = tid < G::NCOL && a.Pout && nc >= P && nc < P + K4_X && Xc >= 0 && Xc < n0;
-    double *const pq = a.Pout ? a.Pout + (long)(y0 + 4 * g4) * sy + Xc : nullptr;
     const int rq4 = (lane & 3) + 4 * (lane >> 4), rsub = (lane >> 2) & 3;
 
     for (int ii = 0; ii < npl + 2; ++ii) {
@@ -1049,9 +1054,13 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
         if (ii < npl) {
             const int kk = kk0 + ii;
             const int b = ii & 1;
-            k4_stage_a<P>(a, pv, so_, po_, sh + (ii % K4_NPF) * 2 * G::STG, sh + G::OFF_PT + b * G::PT,
-                          sh + G::OFF_DT + b * G::PT, kk >= a.zv0 && kk < a.zv1,
-                          kk + a.zoff == a.zd0 || kk + a.zoff == a.zd1);
+            const int sb = sh + (ii % K4_NPF) * 2 * G::STG, pb = sh + G::OFF_PT + b * G::PT;
+            const int db = sh + G::OFF_DT + b * G::PT;
+            double *const po = (a.Pout && kk >= z0 && kk < z1) ? a.Pout + (long)kk * sz : nullptr;
+            if (!(kk >= a.zv0 && kk < a.zv1)) k4_stage_a<P, false, false>(a, pv, so_, po_, go_, sb, pb, db, po);
+            else if (kk + a.zoff == a.zd0 || kk + a.zoff == a.zd1)
+                k4_stage_a<P, true, true>(a, pv, so_, po_, go_, sb, pb, db, po);
+            else k4_stage_a<P, true, false>(a, pv, so_, po_, go_, sb, pb, db, po);
         }
         // ---- B: plane c = kk0 + ib (Ky P, Kx P, owned P) and D = P_c - P_{c-1} (My D)
         const int ib = ii - 1;
@@ -1064,13 +1073,6 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
                     double pw[4 + 2 * P];
 #pragma unroll
                     for (int r = 0; r < 4 + 2 * P; ++r) pw[r] = pt[(4 * g4 + r) * PP + nc];
-                    if (pown && kc_ >= z0 && kc_ < z1) {
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            const int Y = y0 + 4 * g4 + r;
-                            if (Y >= 0 && Y < n1) pq[(long)kc_ * sz + r * sy] = pw[r + P];
-                        }
-                    }
                     double ky[4], mq[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
@@ -1453,6 +1455,7 @@ __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__re
     };
     const bool yitem = tid < G::NITEM;
     const int nc = tid % NC, grp = tid / NC, hcol = PA - P + nc;
+    const int Xc = x0 - P + nc;
     const int X = x0 + lane, Yo = y0 + 2 * w;
     const bool own0 = X < n0 && Yo < n1, own1 = X < n0 && Yo + 1 < n1;
     double r0[T][W], r1[T][W];  // X_t planes kk - 2p .. kk of rows 2w, 2w + 1 (r[.][W-1] newest)
@@ -1718,14 +1721,14 @@ static int encode_field_map(CUtensorMap *m, const double *base, const Geom &g, u
 // z split: CTAs are scheduled dynamically, so the time is about (CTAs per resident slot + 1/2 for
 // the tail) x (planes per CTA incl. 2p halo planes); this fit the measured v3 kop times at 515^3
 // for 1..12 pieces within 3 % (1.69 ms unsplit, 1.49 ms at 4 pieces)
-static int kop_pieces(int n2, int P, long tiles, long resident) {
+static int kop_pieces(int n2, int P, long tiles, long resident, double halo) {
     int best = 1;
     double best_cost = 1e300;
     for (int nz = 1; nz <= 32; ++nz) {
         const int zl = (n2 + nz - 1) / nz;
         if (zl < 2 * P + 1 && nz > 1) break;
         const long ctas = tiles * ((n2 + zl - 1) / zl);
-        const double cost = ((double)ctas / resident + 0.5) * (zl + 2.0 * P);
+        const double cost = ((double)ctas / resident + 0.5) * (zl + halo);
         if (cost < best_cost * 0.999) {
             best_cost = cost;
             best = nz;
@@ -1755,7 +1758,7 @@ static int kop_launch(const KopArgs &a, cudaStream_t s) {
         const LaunchFacts lf = launch_facts((const void *)kop_kernel<P>, KT_THREADS, sm);
         const int ox = kop_origin(a.ilo[0], a.ihi[0], KT_X), oy = kop_origin(a.ilo[1], a.ihi[1], KT_Y);
         const int gx = (a.geo.n0 - ox + KT_X - 1) / KT_X, gy = (a.geo.n1 - oy + KT_Y - 1) / KT_Y;
-        const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)lf.per_sm * lf.nsm);
+        const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)lf.per_sm * lf.nsm, 2.0 * P);
         b.zlen = a.zlen > 0 ? a.zlen : (a.geo.n2 + nz - 1) / nz;
         dim3 grd(gx, gy, (a.geo.n2 + b.zlen - 1) / b.zlen);
         kop_kernel<P><<<grd, KT_THREADS, sm, s>>>(b);
@@ -1766,7 +1769,7 @@ static int kop_launch(const KopArgs &a, cudaStream_t s) {
     const LaunchFacts lf = launch_facts((const void *)kop4_kernel<P>, K4_THREADS, sm);
     const int ox = kop_origin(a.ilo[0], a.ihi[0], K4_X), oy = kop_origin(a.ilo[1], a.ihi[1], K4_Y);
     const int gx = (a.geo.n0 - ox + K4_X - 1) / K4_X, gy = (a.geo.n1 - oy + K4_Y - 1) / K4_Y;
-    const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)lf.per_sm * lf.nsm);
+    const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)lf.per_sm * lf.nsm, 2.0 * P);
     b.zlen = a.zlen > 0 ? a.zlen : (a.geo.n2 + nz - 1) / nz;
     // U and V over the planes that exist in memory, [zv0, zv1) (slabs: halo planes included)
     Geom gm = a.geo;
