@@ -269,7 +269,7 @@ class Elastic:
             nel = (nel, nel, nel)
         self._L, self.dtype = lib(ext), (np.longdouble if ext else np.float64)
         self.nel, self.p, self.tau, self.bc = tuple(nel), p, tau, bc
-        self.n = tuple(e + p for e in nel)
+        self.n = tuple(1 if e == 0 else e + p for e in nel)  # nel_z = 0: the 2D (plane-strain) problem
         self.shape = (3, self.n[2], self.n[1], self.n[0])
         self.N = int(np.prod(self.n))
         h = _P()

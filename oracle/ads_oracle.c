@@ -590,6 +590,7 @@ int or_pw_matrix(or_pwave *h, int d, int which, real *out) {
 /* ------------------------------------------------------------------------ */
 typedef struct {
     int n[3], p, bc;
+    int bcd[3];                        /* zero Dirichlet on direction d (the 2D axis has none) */
     real tau, lam, mu, rho;
     long step;
     real *M[3], *K[3], *B[3], *BT[3];
@@ -615,7 +616,12 @@ long or_el_size(const or_elastic *h) { return (long)h->n[0] * h->n[1] * h->n[2];
 int or_el_create(or_elastic **out, int nelx, int nely, int nelz, int p, real tau, int bc,
                  real lam, real mu, real rho) {
     *out = NULL;
-    if (p < 1 || p > 5 || nelx < 1 || nely < 1 || nelz < 1 || !(tau > 0.0) || (bc != 0 && bc != 1) ||
+    /* nelz = 0: the 2D (plane-strain) problem PAPER.md:362-387 on the same code -- a third axis with
+     * one function, M_z = 1, K_z = B_z = 0 and no boundary.  The blocks Ups_xz, Ups_yz vanish
+     * (B_z = 0), so (u_x, u_y) evolve by the 2D blocks Ups_xx = (2mu+lam) Kx(x)My + mu Mx(x)Ky,
+     * Ups_xy = mu [B]_y [B^T]_x + lam [B]_x [B^T]_y, and u_z (antiplane, Ups_zz = mu (Kx My + Mx Ky))
+     * stays what it starts as (0 for the paper's 2D problem). */
+    if (p < 1 || p > 5 || nelx < 1 || nely < 1 || nelz < 0 || !(tau > 0.0) || (bc != 0 && bc != 1) ||
         !(mu > 0.0) || !(rho > 0.0) || !(lam >= 0.0))
         return OR_E_INVAL;
     or_elastic *h = (or_elastic *)calloc(1, sizeof(or_elastic));
@@ -623,8 +629,9 @@ int or_el_create(or_elastic **out, int nelx, int nely, int nelz, int p, real tau
     h->p = p; h->bc = bc; h->tau = tau; h->lam = lam; h->mu = mu; h->rho = rho;
     real cl = tau * tau / (4.0 * rho) * (2.0 * mu + lam), cs = tau * tau / (4.0 * rho) * mu;
     for (int d = 0; d < 3; ++d) {
-        int n = nel[d] + p;
+        int n = nel[d] == 0 ? 1 : nel[d] + p;
         h->n[d] = n;
+        h->bcd[d] = nel[d] == 0 ? 0 : bc;
         h->M[d] = (real *)malloc(sizeof(real) * n * n);
         h->K[d] = (real *)malloc(sizeof(real) * n * n);
         h->B[d] = (real *)malloc(sizeof(real) * n * n);
@@ -640,7 +647,7 @@ int or_el_create(or_elastic **out, int nelx, int nely, int nelz, int p, real tau
             h->SS[d][q] = h->M[d][q] + cs * h->K[d][q];
             h->MDLU[d][q] = h->M[d][q];
         }
-        if (bc == 1) {
+        if (h->bcd[d] == 1) {
             h->SL[d][0] = h->SS[d][0] = h->MDLU[d][0] = 1.0;
             h->SL[d][n * n - 1] = h->SS[d][n * n - 1] = h->MDLU[d][n * n - 1] = 1.0;
         }
@@ -741,7 +748,8 @@ int or_el_set_state(or_elastic *h, const real *u, const real *udot) {
             for (int j = 0; j < n[1]; ++j)
                 for (int i = 0; i < n[0]; ++i) {
                     long q = ((long)k * n[1] + j) * n[0] + i;
-                    int bnd = h->bc == 1 && (i == 0 || j == 0 || k == 0 || i == n[0] - 1 || j == n[1] - 1 || k == n[2] - 1);
+                    int bnd = (h->bcd[0] && (i == 0 || i == n[0] - 1)) || (h->bcd[1] && (j == 0 || j == n[1] - 1)) ||
+                              (h->bcd[2] && (k == 0 || k == n[2] - 1));
                     h->U[c][q] = bnd ? 0.0 : u[c * N + q];
                     h->V[c][q] = bnd ? 0.0 : (udot ? udot[c * N + q] : 0.0);
                 }
@@ -829,7 +837,7 @@ int or_el_energy(or_elastic *h, real out[3]) {
                 Sd[d] = (real *)malloc(sizeof(real) * n * n);
                 real c = (d == i) ? cl : cs;
                 for (int q = 0; q < n * n; ++q) Sd[d][q] = h->M[d][q] + c * h->K[d][q];
-                if (h->bc == 1) { Sd[d][0] = 1.0; Sd[d][n * n - 1] = 1.0; }
+                if (h->bcd[d] == 1) { Sd[d][0] = 1.0; Sd[d][n * n - 1] = 1.0; }
             }
             kron3_acc(h->n, h->p, Sd[0], Sd[1], Sd[2], h->rho, h->V[i], g, h->t1, h->t2);
             for (int d = 0; d < 3; ++d) free(Sd[d]);

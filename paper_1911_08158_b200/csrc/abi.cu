@@ -1183,8 +1183,9 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
                          ncclComm_t comm = nullptr) {
     if (!out) return ADS_E_INVAL;
     *out = nullptr;
-    // nz = 0: the 2D scheme (single-GPU P-wave handles; trivial_space)
-    if (p < 1 || p > 5 || nx < 1 || ny < 1 || nz < 0 || (nz == 0 && (ncomp != 1 || dist)) || !(tau > 0.0) ||
+    // nz = 0: the 2D scheme (single-GPU handles; trivial_space): P-wave, or plane-strain elasticity
+    // (u_z decouples: B_z = 0)
+    if (p < 1 || p > 5 || nx < 1 || ny < 1 || nz < 0 || (nz == 0 && dist) || !(tau > 0.0) ||
         !std::isfinite(tau) || (bc != ADS_BC_NATURAL && bc != ADS_BC_DIRICHLET0))
         return ADS_E_INVAL;
     if (bc == ADS_BC_DIRICHLET0 && (nx + p < 3 || ny + p < 3 || (nz > 0 && nz + p < 3))) return ADS_E_INVAL;

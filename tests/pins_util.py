@@ -120,3 +120,32 @@ def rel_l2(a, b):
     b = np.asarray(b).ravel()
     nb = np.linalg.norm(b)
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def brute_force_elastic_2d(p, nel, lam, mu):
+    """Dense plane-strain elasticity stiffness (PAPER.md:307-361 in 2D; the blocks PAPER.md:362-387)
+    from strains at quadrature points: a(w,u) = int 2 mu eps(w):eps(u) + lam div w div u over the
+    unit square, vector basis phi_a e_i (i in {x, y}); plus the 2D mass and the scalar stiffness.
+    Component-major, x fastest."""
+    x, w, N, dN = basis_tables(p, nel, p + 2)
+    n = nel + p
+    W = np.einsum("j,i->ji", w, w).ravel()
+    nq = len(x)
+    Phi = np.einsum("jb,ia->jiba", N, N).reshape(nq ** 2, n ** 2)
+    Gx = np.einsum("jb,ia->jiba", N, dN).reshape(nq ** 2, n ** 2)
+    Gy = np.einsum("jb,ia->jiba", dN, N).reshape(nq ** 2, n ** 2)
+    G = (Gx, Gy)
+    nd = n * n
+    A = np.zeros((2 * nd, 2 * nd))
+    for i in range(2):
+        for k in range(2):
+            blk = np.zeros((nd, nd))
+            if i == k:
+                for b in range(2):
+                    blk += mu * (G[b] * W[:, None]).T @ G[b]
+            blk += mu * (G[k] * W[:, None]).T @ G[i]
+            blk += lam * (G[i] * W[:, None]).T @ G[k]
+            A[i * nd:(i + 1) * nd, k * nd:(k + 1) * nd] = blk
+    M = (Phi * W[:, None]).T @ Phi
+    K = sum((g * W[:, None]).T @ g for g in G)
+    return M, K, A

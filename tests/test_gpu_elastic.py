@@ -135,3 +135,42 @@ def test_c5_full_size(ads):
     g0 = ads.make_solver(wl, u0=oracle.project_separable(wl))
     e0 = g0.energy()
     assert abs(e1[2] - e0[2]) < 1e-12 * wl.steps * e0[2], (e0, e1)
+
+
+def _wl2d_elastic(nel, p, bc, tau=2e-3, steps=30, lam=1.0, mu=1.0):
+    """The c5 recipe's (u_x, u_y) bumps on a 2D grid (nel_z = 0), u_z = 0: the plane-strain problem
+    PAPER.md:362-387 (row f2)."""
+    wl = workloads.get("c5").scaled(8, steps)
+    wl.nel, wl.p, wl.bc, wl.tau, wl.lam, wl.mu = nel, p, bc, tau, lam, mu
+    wl.u0 = [t for t in wl.u0 if t.comp < 2]
+    return wl
+
+
+@pytest.mark.parametrize("nel,p,bc", [((37, 21, 0), 2, 1), ((20, 33, 0), 3, 0), ((64, 48, 0), 2, 1)])
+def test_elastic_2d_vs_oracle(ads, nel, p, bc):
+    """Row f2: 2D (plane-strain) elasticity, ads_create_elastic with nz = 0, against the oracle's 2D
+    path: one step vs the extended-precision oracle at 1e-12, a 30-step run at 1e-9, energies; u_z
+    stays zero."""
+    wl = _wl2d_elastic(nel, p, bc, lam=1.3, mu=0.8)
+    g, o = _compare_run(ads, wl, [1, wl.steps])
+    assert g.shape == (3, 1, nel[1] + p, nel[0] + p)
+    assert np.allclose(g.energy(), o.energy(), rtol=1e-11, atol=1e-15)
+    u, ud, a = g.get_state()
+    assert np.abs(u[2]).max() == 0.0 and np.abs(ud[2]).max() == 0.0
+
+
+def test_elastic_2d_unit_operators(ads):
+    """2D Upsilon and D~^-1 on the GPU vs the oracle (random fields, natural BC)."""
+    import torch
+    nel, p = (23, 17, 0), 3
+    s = ads.Solver(nel, p, 0.05, 0, elastic=True, lam=1.1, mu=0.9)
+    o = oracle.Elastic(nel, p, 0.05, 0, 1.1, 0.9, 1.0)
+    x = workloads.random_field(17, 3 * s.N).reshape(s.shape)
+    xd = _dev(x)
+    out = torch.empty_like(xd)
+    s.apply_k(xd, out)
+    torch.cuda.synchronize()
+    assert rel(out.cpu().numpy(), o.apply(x)) < OP_TOL
+    s.solve_d(xd, out)
+    torch.cuda.synchronize()
+    assert rel(out.cpu().numpy(), o.dsolve(x)) < OP_TOL

@@ -443,10 +443,8 @@ def test_bitwise_deterministic(ads, cfg):
 
 
 def test_next_row_argument_errors(ads):
-    """f2/f4 entry points reject what they do not support: 2D elasticity or slabs, tau <= 0,
-    scheme outside {0, 1}, tau changes on elasticity."""
-    with pytest.raises(ads.AdsError):
-        ads.Solver((8, 8, 0), 2, 1e-2, elastic=True)
+    """f2/f4 entry points reject what they do not support: 2D slabs, tau <= 0, scheme outside
+    {0, 1}, tau changes on elasticity."""
     with pytest.raises(ads.AdsError):
         ads.Solver((8, 8, 0), 2, 1e-2, virtual_slabs=2)
     g = ads.Solver((8, 8, 8), 2, 1e-2)

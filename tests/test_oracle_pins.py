@@ -595,3 +595,96 @@ def test_extended_precision_oracle_rows_and_agreement():
         s.step(1)
     for x, y in zip(a.get_state(), b.get_state()):
         assert rel_l2(x, np.asarray(y, dtype=np.float64)) < 1e-13
+
+
+# ---- 2D elasticity (row f2): nel_z = 0, PAPER.md:362-387 ----
+def test_elastic_2d_operator_vs_bruteforce():
+    """2D Upsilon (nel_z = 0: one z function, M_z = 1, K_z = B_z = 0) == the dense plane-strain
+    stiffness assembled from strains (PAPER.md:362-387 blocks, readings C10/C11): the in-plane
+    blocks match it, the antiplane component u_z only sees mu (Kx My + Mx Ky) and nothing couples
+    it to (u_x, u_y)."""
+    from pins_util import brute_force_elastic_2d
+    p, nel, lam, mu = 2, 3, 1.7, 0.6
+    _, K2, A2 = brute_force_elastic_2d(p, nel, lam, mu)
+    el = oracle.Elastic((nel, nel, 0), p, 0.1, bc=0, lam=lam, mu=mu)
+    nd = (nel + p) ** 2
+    x = workloads.random_field(41, 3 * nd)
+    y = el.apply(x).ravel()
+    np.testing.assert_allclose(y[:2 * nd], A2 @ x[:2 * nd], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(y[2 * nd:], mu * (K2 @ x[2 * nd:]), rtol=1e-12, atol=1e-12)
+    xz = x.copy()
+    xz[:2 * nd] = 0.0
+    assert np.abs(el.apply(xz).ravel()[:2 * nd]).max() == 0.0
+
+
+def test_elastic_2d_rigid_body_kernel():
+    """Natural (traction-free) 2D BC: the three in-plane rigid motions -- two
+    translations and the rotation (-y, x) -- and the antiplane translation are in the kernel."""
+    p, nel = 3, 4
+    el = oracle.Elastic((nel, nel, 0), p, 0.1, bc=0, lam=1.3, mu=0.7)
+    n = nel + p
+    t = oracle.knots(p, nel)
+    g = np.array([t[a + 1:a + p + 1].mean() for a in range(n)])  # Greville: linear reproduction
+    Y, X = np.meshgrid(g, g, indexing="ij")
+    one, zero = np.ones_like(X), np.zeros_like(X)
+    for m in [(one, zero, zero), (zero, one, zero), (-Y, X, zero), (zero, zero, one)]:
+        u = np.stack(m)[:, None]
+        assert np.abs(el.apply(u)).max() < 1e-12 * n * n
+    # a non-rigid in-plane motion (shear) is not
+    assert np.abs(el.apply(np.stack((Y, zero, zero))[:, None])).max() > 1e-3
+
+
+@pytest.mark.parametrize("tau", [0.01, 0.5, 10.0])
+def test_elastic_2d_invariant_and_decoupling(tau):
+    """The 2D E1 scheme conserves its invariant at any tau and a state with
+    u_z = 0 keeps u_z = 0 (the 2D problem of the paper is the (u_x, u_y) part)."""
+    wl = workloads.get("c5").scaled(6)
+    wl.nel = (6, 5, 0)
+    el = oracle.Elastic(wl.nel, 2, tau, bc=1)
+    u0 = workloads_2d_elastic(wl)
+    el.set_state(u0)
+    e0 = el.energy()
+    assert e0[2] > 0
+    el.step(25)
+    e = el.energy()
+    assert abs(e[2] - e0[2]) <= 1e-12 * e0[2]
+    u, ud, a = el.get_state()
+    assert np.abs(u[2]).max() == 0.0 and np.abs(ud[2]).max() == 0.0
+
+
+def test_elastic_2d_second_order():
+    """Second order in time for the 2D problem: tau-halving against the
+    semi-discrete exact solution from a dense generalised eigensolve of the brute-force plane-strain
+    operator (Dirichlet, interior DOFs)."""
+    import scipy.linalg
+    from pins_util import brute_force_elastic_2d
+    p, nel, lam, mu, rho = 2, 4, 1.0, 1.0, 1.0
+    wl = workloads.get("c5").scaled(nel)
+    wl.nel = (nel, nel, 0)
+    u0 = workloads_2d_elastic(wl)
+    M2, _, A2 = brute_force_elastic_2d(p, nel, lam, mu)
+    n = nel + p
+    m2 = np.ones((n, n), dtype=bool)
+    m2[0, :] = m2[-1, :] = m2[:, 0] = m2[:, -1] = False
+    m = np.tile(m2.ravel(), 2)
+    RM = np.kron(np.eye(2), rho * M2)[np.ix_(m, m)]
+    lamv, Q = scipy.linalg.eigh(A2[np.ix_(m, m)], RM)
+    T = 0.5
+    uin = u0[:2].reshape(-1)[m]
+    ex = Q @ (np.cos(np.sqrt(lamv) * T) * (Q.T @ RM @ uin))
+    errs = []
+    for tau in [0.02, 0.01, 0.005]:
+        el = oracle.Elastic(wl.nel, p, tau, bc=1, lam=lam, mu=mu, rho=rho)
+        el.set_state(u0)
+        el.step(int(round(T / tau)))
+        u, _, _ = el.get_state()
+        errs.append(np.linalg.norm(u[:2].reshape(-1)[m] - ex))
+    ratios = [errs[0] / errs[1], errs[1] / errs[2]]
+    assert all(3.7 < r < 4.3 for r in ratios), ratios
+
+
+def workloads_2d_elastic(wl):
+    """A smooth 2D elastic start: the c5 recipe's bumps in (x, y), u_z = 0 (projected by the oracle)."""
+    w = workloads.Workload(name="2d-el", p=wl.p, nel=wl.nel, tau=wl.tau, steps=wl.steps, bc=wl.bc, elastic=True,
+                           u0=[t for t in wl.u0 if t.comp < 2])  # along the 2D axis every load is [1]
+    return oracle.project_separable(w)
