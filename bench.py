@@ -48,6 +48,7 @@ FALLBACK_HBM_GBS = 6650.0
 #   sweep z + kick 24 (+8 B for a on the last step of a batch)
 KERNELS = ["kop", "sweep_x", "sweep_y", "sweep_z_kick"]
 C4_DOFS = 515 ** 3  # the committed traffic captures are of config c4 on one GPU
+ELASTIC_STEP_BYTES = 176.0  # elasticity bytes per vector DOF and step (estimate)
 
 
 def peaks():
@@ -308,35 +309,46 @@ def run_ours(args, rank, world, local):
 
     # ---- roofline of the dominant kernel (algorithmic bytes / its average launch time)
     hbm, peak_kind, _ = peaks()
-    shares = kms / kms.sum() if kms.sum() > 0 else kms
-    dom = int(np.argmax(kms))
-    per_launch_ms = kms / np.maximum(kcnt, 1)
-    Nloc = s.N  # this rank's DOFs (the per-kernel rooflines are per GPU)
-    plan = s.step_bytes()  # algorithmic bytes per DOF of each kernel class of this handle's step
-    kick = 3  # the z sweep carries the kick
-    kernels = {}
-    for i, name in enumerate(KERNELS):
-        bpd = plan[i]
-        if i == kick:  # a is stored on the last step of a batch only
-            bpd = plan[i] + 8.0 / max(kcnt[i], 1)
-        gbs = Nloc * bpd / (per_launch_ms[i] / 1e3) / 1e9 if per_launch_ms[i] > 0 else 0.0
-        kernels[name] = {"ms_per_launch": per_launch_ms[i], "launches": int(kcnt[i]), "share": float(shares[i]),
-                         "bytes_per_dof": bpd, "achieved_gbs": gbs, "frac": gbs / hbm}
-    achieved = kernels[KERNELS[dom]]["achieved_gbs"]
-    step_bytes = Nloc * (sum(plan) + 8.0 / args.steps)
-    traffic, traffic_src = ncu_traffic(KERNELS[dom], Nloc)
-    roofline = {"bound": "hbm", "kernel": KERNELS[dom], "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "peak_kind": peak_kind,
-                "traffic": traffic, "traffic_unit": "GB per launch (ncu dram read + write)",
-                "traffic_source": traffic_src,
-                "algorithmic_bytes": Nloc * kernels[KERNELS[dom]]["bytes_per_dof"] / 1e9,
-                "step_achieved": step_bytes / (ms / args.steps / 1e3) / 1e9,
-                "step_frac": step_bytes / (ms / args.steps / 1e3) / 1e9 / hbm,
-                "step_bytes_per_dof": step_bytes / N, "floor_bytes_per_dof": 64.0}
+    Nloc = s.N  # this rank's DOFs per component (the per-kernel rooflines are per GPU)
+    if wl.elastic:
+        # elasticity (c5): ~40 launches per step; the roofline is that of the
+        # whole step against its estimated 176 B per vector DOF (3 components) and step
+        step_bytes = ELASTIC_STEP_BYTES * N
+        achieved = step_bytes / (ms / args.steps / 1e3) / 1e9
+        kernels = {}
+        roofline = {"bound": "hbm", "kernel": "elastic step (all launches)", "achieved": achieved, "peak": hbm,
+                    "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
+                    "algorithmic_bytes": step_bytes / 1e9, "step_bytes_per_dof": ELASTIC_STEP_BYTES,
+                    "note": "SURVEY.md §8(d) estimate: 170-180 B per vector DOF and step (6 ADS solves, "
+                            "Kronecker triples); c5 fields (17.6 MB per component) are L2-resident"}
+    else:
+        shares = kms / kms.sum() if kms.sum() > 0 else kms
+        dom = int(np.argmax(kms))
+        per_launch_ms = kms / np.maximum(kcnt, 1)
+        plan = s.step_bytes()  # algorithmic bytes per DOF of each kernel class of this handle's step
+        kick = 3  # the z sweep carries the kick
+        kernels = {}
+        for i, name in enumerate(KERNELS):
+            bpd = plan[i]
+            if i == kick:  # a is stored on the last step of a batch only
+                bpd = plan[i] + 8.0 / max(kcnt[i], 1)
+            gbs = Nloc * bpd / (per_launch_ms[i] / 1e3) / 1e9 if per_launch_ms[i] > 0 else 0.0
+            kernels[name] = {"ms_per_launch": per_launch_ms[i], "launches": int(kcnt[i]), "share": float(shares[i]),
+                             "bytes_per_dof": bpd, "achieved_gbs": gbs, "frac": gbs / hbm}
+        achieved = kernels[KERNELS[dom]]["achieved_gbs"]
+        step_bytes = Nloc * (sum(plan) + 8.0 / args.steps)
+        traffic, traffic_src = ncu_traffic(KERNELS[dom], Nloc)
+        roofline = {"bound": "hbm", "kernel": KERNELS[dom], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "peak_kind": peak_kind,
+                    "traffic": traffic, "traffic_unit": "GB per launch (ncu dram read + write)",
+                    "traffic_source": traffic_src,
+                    "algorithmic_bytes": Nloc * kernels[KERNELS[dom]]["bytes_per_dof"] / 1e9,
+                    "step_achieved": step_bytes / (ms / args.steps / 1e3) / 1e9,
+                    "step_frac": step_bytes / (ms / args.steps / 1e3) / 1e9 / hbm,
+                    "step_bytes_per_dof": step_bytes / N, "floor_bytes_per_dof": 64.0}
 
     # ---- end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
-    nz, ny, nx = s.shape
-    u_host = torch.empty((nz, ny, nx), dtype=torch.float64, pin_memory=True)
+    u_host = torch.empty(s.shape, dtype=torch.float64, pin_memory=True)
     ud_host = torch.empty_like(u_host, pin_memory=True)
     a_host = torch.empty_like(u_host, pin_memory=True)
     s.get_state(u_host, ud_host, a_host)  # the state the run starts from (also warms the copy path)
@@ -355,7 +367,7 @@ def run_ours(args, rank, world, local):
                    "pinned host buffers; wall clock incl. copies", "energy": list(map(float, e))}
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": "Elasticity DOF-steps/sec (fp64)" if wl.elastic else METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "repeats": {"n": args.repeats, "ms": reps, "statistic": "median; each repeat restarts from the initial "
                     "state (set_state) and times exactly `steps` steps"},

@@ -412,6 +412,9 @@ int build_direction(ads_ctx *h, int d) {
         const double cl = h->tau * h->tau / (4.0 * h->rho) * (2.0 * h->mu + h->lam);
         const double cs = h->tau * h->tau / (4.0 * h->rho) * h->mu;
         Band AL = shifted(s, cl, s.bc), AS = shifted(s, cs, s.bc);
+        if (d == 0)  // S_i = rho (x)_d (...): the density goes into the x factor, (rho A)^-1 = A^-1 / rho
+            for (auto *B : {&AL, &AS})
+                for (double &v : B->v) v *= h->rho;
         snprintf(what, sizeof what, "SL_%d", d);
         if ((rc = make_solve_tab(h, AL, what, D.tabL))) return rc;
         snprintf(what, sizeof what, "SS_%d", d);
@@ -667,11 +670,13 @@ int tri(ads_ctx *h, double *out, const double *in, const double *fx, const doubl
     return check_launch(h, "kron3");
 }
 
-// out += coef Ups_ik in   (i != k): mu [B]_k [B^T]_i + lam [B]_i [B^T]_k, M in the third
-// direction -- both triples act on the same input and output: one fused pass
-int ups_offdiag(ads_ctx *h, int i, int k, const double *in, double *out, double coef) {
+// out = (addend or out) + coef Ups_ik in   (i != k): mu [B]_k [B^T]_i + lam [B]_i [B^T]_k, M in
+// the third direction -- both triples act on the same input and output: one fused pass
+int ups_offdiag(ads_ctx *h, int i, int k, const double *in, double *out, double coef,
+                const double *addend = nullptr) {
     KronTerms k3;
     k3.nterms = 2;
+    k3.addend = addend;
     const double **F[3] = {k3.fx, k3.fy, k3.fz};
     for (int e = 0; e < 3; ++e) {
         F[e][0] = e == k ? h->dd[e].bband : e == i ? h->dd[e].btband : h->dd[e].mband;
@@ -704,27 +709,26 @@ int ups_apply(ads_ctx *h, const double *in, const double *v, double tau_d, doubl
     return ADS_OK;
 }
 
-// x <- S_i^-1 x,  S_i = rho (x)_d (M_d + c_{i,d} K_d)  (Eq. 37)
-int s_solve(ads_ctx *h, int i, double *x) {
+// x <- S_i^-1 in (in == nullptr: in place),  S_i = rho (x)_d (M_d + c_{i,d} K_d)  (PAPER.md:415-422
+// Eq. 37); the x tables carry the factor rho (build_direction)
+int s_solve(ads_ctx *h, int i, double *x, const double *in = nullptr) {
     int rc;
     for (int d = 0; d < 3; ++d)
-        if ((rc = run_sweep_tab(h, d, d == i ? h->dd[d].tabL : h->dd[d].tabS, x, x, nullptr, 0.0))) return rc;
-    launch_axpby(h->Nalloc, 1.0 / h->rho, x, 0.0, x, h->stream);
-    return check_launch(h, "axpby");
+        if ((rc = run_sweep_tab(h, d, d == i ? h->dd[d].tabL : h->dd[d].tabS, d == 0 && in ? in : x, x, nullptr, 0.0)))
+            return rc;
+    return ADS_OK;
 }
 
 // X <- D~^-1 X, D~ = L~ (rho M)^-1 L~^T: predictor x -> y -> z, corrector z -> y -> x
 // (Eqs. 35-36 in delta form, E1).  W: 3-component scratch.
 int el_dsolve(ads_ctx *h, double *X) {
     const double hh = -0.5 * h->tau * h->tau;
-    const long fb = sizeof(double) * h->Nalloc;
     int rc;
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 3; ++i) {  // w_i = X_i - tau^2/2 sum_{j<i} Ups_ij w_j (the first term reads X_i)
         double *wi = comp(h->W, h, i);
-        CUDA_TRY(h, cudaMemcpyAsync(wi, comp(X, h, i), fb, cudaMemcpyDeviceToDevice, h->stream));
         for (int j = 0; j < i; ++j)
-            if ((rc = ups_offdiag(h, i, j, comp(h->W, h, j), wi, hh))) return rc;
-        if ((rc = s_solve(h, i, wi))) return rc;
+            if ((rc = ups_offdiag(h, i, j, comp(h->W, h, j), wi, hh, j == 0 ? comp(X, h, i) : nullptr))) return rc;
+        if ((rc = s_solve(h, i, wi, i == 0 ? comp(X, h, 0) : nullptr))) return rc;
     }
     for (int i = 2; i >= 0; --i) {
         double *zi = comp(X, h, i);

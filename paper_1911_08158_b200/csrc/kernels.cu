@@ -1474,8 +1474,9 @@ __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__re
 #pragma unroll
                 for (int c = 0; c < W; ++c) fzr[t][c] = k3.alpha[t] * __ldg(k3.fz[t] + (long)k * W + c);
             if (beta != 0.0) {
-                ob0 = own0 ? out[(long)k * sz + oxy] : 0.0;
-                ob1 = own1 ? out[(long)k * sz + oxy + sy] : 0.0;
+                const double *ad = k3.addend ? k3.addend : out;
+                ob0 = own0 ? ad[(long)k * sz + oxy] : 0.0;
+                ob1 = own1 ? ad[(long)k * sz + oxy + sy] : 0.0;
             }
         }
     };
@@ -1595,6 +1596,7 @@ static int kron3_dispatch(const double *in, double *out, const KronTerms &k3, do
     } else {  // two passes, the second accumulating
         KronTerms a = k3, b = k3;
         a.nterms = b.nterms = 1;
+        b.addend = nullptr;  // the second pass accumulates onto the first
         b.fx[0] = k3.fx[1], b.fy[0] = k3.fy[1], b.fz[0] = k3.fz[1], b.alpha[0] = k3.alpha[1];
         kron3_launch<P, 1>(in, out, a, beta, g, s);
         kron3_launch<P, 1>(in, out, b, 1.0, g, s);

@@ -161,6 +161,7 @@ struct KronTerms {
     int nterms = 1;
     const double *fx[2] = {nullptr, nullptr}, *fy[2] = {nullptr, nullptr}, *fz[2] = {nullptr, nullptr};
     double alpha[2] = {0.0, 0.0};
+    const double *addend = nullptr;  // beta multiplies this field instead of out (nullptr: out)
 };
 int launch_kron3(int p, const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
                  cudaStream_t s);
