@@ -98,6 +98,10 @@ struct ads_ctx {
     // unused], eigenvalues mlam in that order (0 on unused), mord = the active mode at each slot.
     bool modal_ready = false;
     double *mQe[3] = {}, *mQo[3] = {}, *mPe[3] = {}, *mPo[3] = {};
+    // the same maps for the TMA-fed kernels: leading dimensions padded to multiples of 4 (16-byte
+    // TMA strides), Q_e's middle column (odd n) halved (the fold loads u(h) twice)
+    double *mQe2[3] = {}, *mQo2[3] = {}, *mPe2[3] = {}, *mPo2[3] = {};
+    int mlqe[3] = {}, mlqo[3] = {}, mlpe[3] = {}, mlpo[3] = {};
     int mne[3] = {0, 0, 0}, mno[3] = {0, 0, 0};
     double *mlam[3] = {nullptr, nullptr, nullptr}, *mf[3] = {nullptr, nullptr, nullptr};
     std::vector<double> mphi_h[3];  // active-block eigenvectors (host, for the load vectors)
@@ -1094,6 +1098,8 @@ int modal_prepare(ads_ctx *h) {
             if (h->nel[c] == h->nel[d] && h->sp[c].bc == h->sp[d].bc) e = c;
         if (e >= 0) {
             h->mQe[d] = h->mQe[e], h->mQo[d] = h->mQo[e], h->mPe[d] = h->mPe[e], h->mPo[d] = h->mPo[e];
+            h->mQe2[d] = h->mQe2[e], h->mQo2[d] = h->mQo2[e], h->mPe2[d] = h->mPe2[e], h->mPo2[d] = h->mPo2[e];
+            h->mlqe[d] = h->mlqe[e], h->mlqo[d] = h->mlqo[e], h->mlpe[d] = h->mlpe[e], h->mlpo[d] = h->mlpo[e];
             h->mne[d] = h->mne[e], h->mno[d] = h->mno[e], h->mlam[d] = h->mlam[e];
             h->mphi_h[d] = h->mphi_h[e], h->mord[d] = h->mord[e];
             continue;
@@ -1127,9 +1133,22 @@ int modal_prepare(ads_ctx *h) {
             for (int i = 0; i < hh; ++i) Po[(size_t)i + (size_t)b * hh] = Pf(i, O[b]);
             le[ne + b] = lam[O[b]];
         }
-        double **dsts[5] = {&h->mQe[d], &h->mQo[d], &h->mPe[d], &h->mPo[d], &h->mlam[d]};
-        const std::vector<double> *srcs[5] = {&Qe, &Qo, &Pe, &Po, &le};
-        for (int q = 0; q < 5; ++q) {
+        // padded copies (column-major, leading dimension a multiple of 4)
+        auto padded = [](const std::vector<double> &a, int rows, int cols, int &ld, int halve_col) {
+            ld = std::max(4, (rows + 3) / 4 * 4);
+            std::vector<double> b((size_t)ld * std::max(cols, 1), 0.0);
+            for (int c = 0; c < cols; ++c)
+                for (int r = 0; r < rows; ++r) b[(size_t)r + (size_t)c * ld] = a[(size_t)r + (size_t)c * rows] * (c == halve_col ? 0.5 : 1.0);
+            return b;
+        };
+        std::vector<double> Qe2 = padded(Qe, ne, H, h->mlqe[d], (n & 1) ? H - 1 : -1);
+        std::vector<double> Qo2 = padded(Qo, no, hh, h->mlqo[d], -1);
+        std::vector<double> Pe2 = padded(Pe, H, ne, h->mlpe[d], -1);
+        std::vector<double> Po2 = padded(Po, hh, no, h->mlpo[d], -1);
+        double **dsts[9] = {&h->mQe[d], &h->mQo[d], &h->mPe[d], &h->mPo[d], &h->mlam[d],
+                            &h->mQe2[d], &h->mQo2[d], &h->mPe2[d], &h->mPo2[d]};
+        const std::vector<double> *srcs[9] = {&Qe, &Qo, &Pe, &Po, &le, &Qe2, &Qo2, &Pe2, &Po2};
+        for (int q = 0; q < 9; ++q) {
             if ((rc = dalloc(h, (void **)dsts[q], sizeof(double) * srcs[q]->size()))) return rc;
             CUDA_TRY(h, cudaMemcpy(*dsts[q], srcs[q]->data(), sizeof(double) * srcs[q]->size(), cudaMemcpyHostToDevice));
         }
@@ -1160,16 +1179,23 @@ int modal_transform(ads_ctx *h, bool inverse, const double *in, double *a, doubl
         m.ne = h->mne[d];
         m.no = h->mno[d];
         m.Qe = h->mQe[d], m.Qo = h->mQo[d], m.Pe = h->mPe[d], m.Po = h->mPo[d];
+        m.Qe2 = h->mQe2[d], m.Qo2 = h->mQo2[d], m.Pe2 = h->mPe2[d], m.Po2 = h->mPo2[d];
+        m.lqe = h->mlqe[d], m.lqo = h->mlqo[d], m.lpe = h->mlpe[d], m.lpo = h->mlpo[d];
         m.inverse = inverse ? 1 : 0;
         if (d == 0) {         // x lines: contiguous rows of pitch sy
             m.ks = 1, m.ls = g.sy, m.nl = g.n1 * g.n2, m.bs = 0, m.nb = 1;
+            m.kdim = 0, m.td[0] = g.n0, m.td[1] = (long)g.n1 * g.n2, m.td[2] = 1, m.ts1 = g.sy, m.ts2 = g.sz * g.n2;
         } else if (d == 1) {  // y lines: adjacent in x, one batch per plane
             m.ks = g.sy, m.ls = 1, m.nl = g.n0, m.bs = g.sz, m.nb = g.n2;
+            m.kdim = 1, m.td[0] = g.n0, m.td[1] = g.n1, m.td[2] = g.n2, m.ts1 = g.sy, m.ts2 = g.sz;
         } else {              // z lines: every (x, y) position of a plane, row padding included (zero)
             m.ks = g.sz, m.ls = 1, m.nl = (int)g.sz, m.bs = 0, m.nb = 1;
+            m.kdim = 1, m.td[0] = g.sz, m.td[1] = g.n2, m.td[2] = 1, m.ts1 = g.sz, m.ts2 = g.sz * g.n2;
         }
         ProfScope ps(h, 4);
-        if (launch_modal_gemm(m, h->stream)) return fail(h, ADS_E_INVAL, "modal transform: grid too large");
+        const int lr = launch_modal_gemm(m, h->stream);
+        if (lr == -2) return fail(h, ADS_E_CUDA, "modal transform: TMA descriptor encoding failed");
+        if (lr) return fail(h, ADS_E_INVAL, "modal transform: grid too large");
         int rc;
         if ((rc = check_launch(h, "modal transform"))) return rc;
         src = dsts[d];

@@ -1810,6 +1810,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     return fn;
 }
 
+// general 3D fp64 map: dims (d0, d1, d2) elements, strides (s1, s2) in elements, box (b0, b1, b2);
+// out-of-bounds boxes are zero-filled (modal_tc.cu)
+int encode_map_3d(CUtensorMap *m, const double *base, long d0, long d1, long d2, long s1, long s2, unsigned b0,
+                  unsigned b1, unsigned b2) {
+    auto enc = tmap_encoder();
+    if (!enc) return -1;
+    const cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+    const cuuint64_t strides[2] = {(cuuint64_t)s1 * 8, (cuuint64_t)s2 * 8};
+    const cuuint32_t box[3] = {b0, b1, b2}, es[3] = {1, 1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -1;
+}
+
 // 3D fp64 field (n0, n1, n2) with strides (sy, sz) elements, box (b0, b1, b2); OOB -> 0
 static int encode_field_map(CUtensorMap *m, const double *base, const Geom &g, unsigned b0, unsigned b1,
                             unsigned b2) {

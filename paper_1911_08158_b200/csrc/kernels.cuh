@@ -135,7 +135,17 @@ struct ModalGemmArgs {
     int n = 0, ne = 0, no = 0, H = 0, hh = 0;
     const double *Qe = nullptr, *Qo = nullptr, *Pe = nullptr, *Po = nullptr;
     int inverse = 0;
+    // tensor-core path: the same maps column-major with even leading dimensions (TMA strides are
+    // 16-byte multiples) -- Q_e with its middle column (n odd) halved: the fold loads u(h) twice
+    const double *Qe2 = nullptr, *Qo2 = nullptr, *Pe2 = nullptr, *Po2 = nullptr;
+    int lqe = 0, lqo = 0, lpe = 0, lpo = 0;
+    // the addressing as a 3D tensor (for the TMA maps): element (k, l, b) of the axis view
+    long td[3] = {0, 0, 0}, ts1 = 0, ts2 = 0;
+    int kdim = 0;  // which tensor dimension is k (0: x lines, k contiguous; 1: y / z)
+    int tail_only = 0;  // run only the CUDA-core tail rows (the tensor-core path did the full tiles)
 };
+int encode_map_3d(CUtensorMap *m, const double *base, long d0, long d1, long d2, long s1, long s2, unsigned b0,
+                  unsigned b1, unsigned b2);
 int launch_modal_gemm(const ModalGemmArgs &g, cudaStream_t s);
 // dense caller layout (n0 n1 n2, x fastest) <-> pitched field (sy, sz): to_pitched = 1 unpacks
 void launch_repack(const double *src, double *dst, const Geom &g, int to_pitched, cudaStream_t s);

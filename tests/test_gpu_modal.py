@@ -45,6 +45,7 @@ def _state(shape, seed, bc=1):
 
 
 @pytest.mark.parametrize("nel,p,tau,nsteps", [((16, 16, 16), 2, 1e-2, 20), ((21, 13, 30), 3, 5e-3, 37),
+                                              ((131, 70, 150), 3, 2e-3, 9), ((200, 129, 67), 2, 1e-3, 5),
                                               ((9, 11, 7), 1, 2e-2, 64), ((12, 10, 8), 5, 4e-3, 5)])
 def test_free_run_vs_modal_oracle_and_stepping(ads, nel, p, tau, nsteps):
     g = ads.Solver(nel, p, tau)
