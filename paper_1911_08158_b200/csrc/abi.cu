@@ -469,8 +469,9 @@ int guard(ads_ctx *h) {
 
 // ---- step pieces ----
 int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g, double sign, double *Pout,
-            double *r, bool devsrc = false, const double *kw = nullptr) {
+            double *r, bool devsrc = false, const double *kw = nullptr, const double *Ph = nullptr) {
     KopArgs a;
+    a.Ph = Ph;
     a.U = U;
     a.V = V;
     a.Pout = Pout;
@@ -838,60 +839,78 @@ std::vector<ads_ctx *> slabs_of(ads_ctx *h) {
         if (r_ != ncclSuccess) return fail(h, ADS_E_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
     } while (0)
 
-// send first p owned planes of F down / last p up; receive the neighbours' into the halos
-int exch_halo(ads_ctx *G, double *ads_ctx::*F) {
-    for (ads_ctx *m : slabs_of(G)) {
-        const long sz = m->geo.sz, hp = (long)m->halo * sz, nl = m->n[2];
-        double *f = m->*F;
-        if (m->dist == 3) {
-            if (m->prev)
-                CUDA_TRY(m, cudaMemcpyAsync(f - hp, m->prev->*F + (m->prev->n[2] - m->halo) * sz, sizeof(double) * hp,
-                                            cudaMemcpyDeviceToDevice, m->stream));
-            if (m->next)
-                CUDA_TRY(m, cudaMemcpyAsync(f + nl * sz, m->next->*F, sizeof(double) * hp, cudaMemcpyDeviceToDevice,
-                                            m->stream));
-        } else if (m->dist == 1) {
-            NCCL_TRY(m, ncclGroupStart());
-            if (m->has_prev) {
-                NCCL_TRY(m, ncclSend(f, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
-                NCCL_TRY(m, ncclRecv(f - hp, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
-            }
-            if (m->has_next) {
-                NCCL_TRY(m, ncclSend(f + (nl - m->halo) * sz, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
-                NCCL_TRY(m, ncclRecv(f + nl * sz, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
-            }
-            NCCL_TRY(m, ncclGroupEnd());
+// Exchanges between neighbouring z-slabs as one schedule both back ends run: every entry moves
+// `count` doubles from region `sr` of slab `src` to region `dr` of slab `dst`.  An NCCL rank posts
+// the entries it takes part in (send or receive, one group on its stream); a virtual group copies
+// every entry on the device.  The tested virtual path therefore exercises exactly the pairing the
+// NCCL path uses.
+struct Xfer {
+    int src, dst, sr, dr;
+    long count;
+};
+template <class Resolve>
+int run_schedule(ads_ctx *G, const std::vector<Xfer> &xs, Resolve res) {
+    if (G->dist == 2) {
+        for (const Xfer &x : xs) {
+            ads_ctx *ms = G->members[x.src], *md = G->members[x.dst];
+            CUDA_TRY(md, cudaMemcpyAsync(res(md, x.dr), res(ms, x.sr), sizeof(double) * x.count, cudaMemcpyDeviceToDevice,
+                                         md->stream));
         }
+    } else if (G->dist == 1) {
+        NCCL_TRY(G, ncclGroupStart());
+        for (const Xfer &x : xs) {
+            if (x.src == G->rank) NCCL_TRY(G, ncclSend(res(G, x.sr), x.count, ncclDouble, x.dst, G->comm, G->stream));
+            if (x.dst == G->rank) NCCL_TRY(G, ncclRecv(res(G, x.dr), x.count, ncclDouble, x.src, G->comm, G->stream));
+        }
+        NCCL_TRY(G, ncclGroupEnd());
     }
     return ADS_OK;
 }
 
+// the world's slabs and their plane counts (every rank knows the whole plan)
+int slab_count(const ads_ctx *G) { return G->dist == 2 ? (int)G->members.size() : G->world; }
+
+// halo exchange of a field: slab j's last p owned planes -> slab j+1's lower halo, slab j+1's first
+// p owned planes -> slab j's upper halo
+enum { RG_LOW_OWNED, RG_HIGH_OWNED, RG_LOW_HALO, RG_HIGH_HALO };
+int exch_halo(ads_ctx *G, double *ads_ctx::*F) {
+    std::vector<Xfer> xs;
+    const long hp = (long)G->p * (G->dist == 2 ? G->members[0]->geo.sz : G->geo.sz);
+    for (int j = 0; j + 1 < slab_count(G); ++j) {
+        xs.push_back({j, j + 1, RG_HIGH_OWNED, RG_LOW_HALO, hp});
+        xs.push_back({j + 1, j, RG_LOW_OWNED, RG_HIGH_HALO, hp});
+    }
+    return run_schedule(G, xs, [F](ads_ctx *m, int r) -> double * {
+        const long sz = m->geo.sz, nl = m->n[2], p = m->p;
+        double *f = m->*F;
+        switch (r) {
+            case RG_LOW_OWNED: return f;
+            case RG_HIGH_OWNED: return f + (nl - p) * sz;
+            case RG_LOW_HALO: return f - p * sz;
+            default: return f + nl * sz;
+        }
+    });
+}
+
 // tips of the local z solution X = Wk: tip_prev <- previous slab's last p planes,
 // tip_next <- next slab's first p planes
+enum { RG_WK_LOW, RG_WK_HIGH, RG_TIP_PREV, RG_TIP_NEXT };
 int exch_tips(ads_ctx *G) {
-    for (ads_ctx *m : slabs_of(G)) {
-        const long sz = m->geo.sz, hp = (long)m->p * sz, nl = m->n[2];
-        if (m->dist == 3) {
-            if (m->prev)
-                CUDA_TRY(m, cudaMemcpyAsync(m->tip_prev, m->prev->Wk + (m->prev->n[2] - m->p) * sz, sizeof(double) * hp,
-                                            cudaMemcpyDeviceToDevice, m->stream));
-            if (m->next)
-                CUDA_TRY(m, cudaMemcpyAsync(m->tip_next, m->next->Wk, sizeof(double) * hp, cudaMemcpyDeviceToDevice,
-                                            m->stream));
-        } else if (m->dist == 1) {
-            NCCL_TRY(m, ncclGroupStart());
-            if (m->has_prev) {
-                NCCL_TRY(m, ncclSend(m->Wk, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
-                NCCL_TRY(m, ncclRecv(m->tip_prev, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
-            }
-            if (m->has_next) {
-                NCCL_TRY(m, ncclSend(m->Wk + (nl - m->p) * sz, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
-                NCCL_TRY(m, ncclRecv(m->tip_next, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
-            }
-            NCCL_TRY(m, ncclGroupEnd());
-        }
+    std::vector<Xfer> xs;
+    const long hp = (long)G->p * (G->dist == 2 ? G->members[0]->geo.sz : G->geo.sz);
+    for (int j = 0; j + 1 < slab_count(G); ++j) {
+        xs.push_back({j, j + 1, RG_WK_HIGH, RG_TIP_PREV, hp});
+        xs.push_back({j + 1, j, RG_WK_LOW, RG_TIP_NEXT, hp});
     }
-    return ADS_OK;
+    return run_schedule(G, xs, [](ads_ctx *m, int r) -> double * {
+        const long sz = m->geo.sz, nl = m->n[2], p = m->p;
+        switch (r) {
+            case RG_WK_LOW: return m->Wk;
+            case RG_WK_HIGH: return m->Wk + (nl - p) * sz;
+            case RG_TIP_PREV: return m->tip_prev;
+            default: return m->tip_next;
+        }
+    });
 }
 
 void zargs(ads_ctx *m, ZfixArgs &a) {
@@ -938,39 +957,51 @@ int run_zfix(ads_ctx *m, double *Aout, double kick) {
     return check_launch(m, "zfix");
 }
 
-// stage-1 values: b0buf -> next slab's b0_prev2, u0buf -> previous slab's u0_next2
+// stage-1 values: b0buf -> next slab's b0_prev2, u0buf -> previous slab's u0_next2 (slab j+1 needs
+// b_{j-1}^0, which exists for j >= 1; slab j-1 needs u_{j+1}^0, which exists for j <= G-2)
+enum { RG_B0, RG_U0, RG_B0_PREV2, RG_U0_NEXT2 };
 int exch_stage1(ads_ctx *G) {
-    for (ads_ctx *m : slabs_of(G)) {
-        const long hp = (long)m->p * m->geo.sz;
-        if (m->dist == 3) {
-            if (m->prev && m->prev->has_prev)
-                CUDA_TRY(m, cudaMemcpyAsync(m->b0_prev2, m->prev->b0buf, sizeof(double) * hp, cudaMemcpyDeviceToDevice,
-                                            m->stream));
-            if (m->next && m->next->has_next)
-                CUDA_TRY(m, cudaMemcpyAsync(m->u0_next2, m->next->u0buf, sizeof(double) * hp, cudaMemcpyDeviceToDevice,
-                                            m->stream));
-        } else if (m->dist == 1) {
-            NCCL_TRY(m, ncclGroupStart());
-            if (m->has_next && m->has_prev)  // slab j+1 needs b_{j-1}^0 (exists if j >= 1)
-                NCCL_TRY(m, ncclSend(m->b0buf, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
-            if (m->rank >= 2) NCCL_TRY(m, ncclRecv(m->b0_prev2, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
-            if (m->has_prev && m->has_next)  // slab j-1 needs u_{j+1}^0 (exists if j <= G-2)
-                NCCL_TRY(m, ncclSend(m->u0buf, hp, ncclDouble, m->rank - 1, m->comm, m->stream));
-            if (m->rank + 2 < m->world)
-                NCCL_TRY(m, ncclRecv(m->u0_next2, hp, ncclDouble, m->rank + 1, m->comm, m->stream));
-            NCCL_TRY(m, ncclGroupEnd());
-        }
+    std::vector<Xfer> xs;
+    const int W = slab_count(G);
+    const long hp = (long)G->p * (G->dist == 2 ? G->members[0]->geo.sz : G->geo.sz);
+    for (int j = 1; j + 1 < W; ++j) {
+        xs.push_back({j, j + 1, RG_B0, RG_B0_PREV2, hp});
+        xs.push_back({j, j - 1, RG_U0, RG_U0_NEXT2, hp});
     }
-    return ADS_OK;
+    return run_schedule(G, xs, [](ads_ctx *m, int r) -> double * {
+        switch (r) {
+            case RG_B0: return m->b0buf;
+            case RG_U0: return m->u0buf;
+            case RG_B0_PREV2: return m->b0_prev2;
+            default: return m->u0_next2;
+        }
+    });
 }
 
 // One drift + solve + kick over all slabs: A = D^-1 (F(t) - K (U + tau_d V)), V += kick A,
 // U <- U + tau_d V when tau_d != 0 (the step) -- with tau_d = 0 this is the half-kick init.
 int dist_solve(ads_ctx *G, double tau_d, double g, double kick, bool keepA) {
     int rc;
-    if ((rc = exch_halo(G, &ads_ctx::U)) || (rc = exch_halo(G, &ads_ctx::V))) return rc;
+    // only the drifted field crosses the interfaces: each slab forms P = U + tau V on its p first
+    // and last owned planes (into U2, where the operator kernel writes P anyway), the P planes are
+    // exchanged into U2's halos, and the operator kernel reads its halo planes from there -- half
+    // the bytes of exchanging U and V (the half-kick start, tau_d = 0, exchanges U alone)
+    if (tau_d != 0.0) {
+        for (ads_ctx *m : slabs_of(G)) {
+            const long hp = (long)m->p * m->geo.sz, nl = m->n[2];
+            launch_drift(m->U, m->V, tau_d, m->U2, hp, m->stream);
+            launch_drift(m->U + (nl - m->p) * m->geo.sz, m->V + (nl - m->p) * m->geo.sz, tau_d,
+                         m->U2 + (nl - m->p) * m->geo.sz, hp, m->stream);
+            if ((rc = check_launch(m, "drift edges"))) return rc;
+        }
+        if ((rc = exch_halo(G, &ads_ctx::U2))) return rc;
+    } else if ((rc = exch_halo(G, &ads_ctx::U))) {
+        return rc;
+    }
     for (ads_ctx *m : slabs_of(G)) {
-        if ((rc = run_kop(m, m->U, m->V, tau_d, g, -1.0, tau_d != 0.0 ? m->U2 : nullptr, m->R))) return rc;
+        if ((rc = run_kop(m, m->U, m->V, tau_d, g, -1.0, tau_d != 0.0 ? m->U2 : nullptr, m->R, false, nullptr,
+                          tau_d != 0.0 ? m->U2 : nullptr)))
+            return rc;
         if ((rc = run_sweep(m, 0, m->R, m->Wk, nullptr, 0.0)) || (rc = run_sweep(m, 1, m->Wk, m->R, nullptr, 0.0)) ||
             (rc = run_sweep_tab(m, 2, m->tabZ, m->R, m->Wk, nullptr, 0.0)))
             return rc;

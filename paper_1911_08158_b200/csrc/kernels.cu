@@ -892,7 +892,7 @@ __device__ __forceinline__ void k4_wait(unsigned mb, unsigned parity) {
 // staging / tile / global offsets of slot m, -1: none or not owned; pv[m]: the previous plane's P).
 // LIVE: the plane exists in memory; ZDIR: a zero-Dirichlet z face (outside the restricted space:
 // it counts as zero in the plane differences)
-template <int P, bool LIVE, bool ZDIR>
+template <int P, bool LIVE, bool ZDIR, bool PONLY = false>
 __device__ __forceinline__ void k4_stage_a(const KopArgs &a, double (&pv)[K4Geo<P>::SA], const int (&so_)[K4Geo<P>::SA],
                                            const int (&po_)[K4Geo<P>::SA], const long (&go_)[K4Geo<P>::SA], int sbase,
                                            int pbase, int dbase, double *pout) {
@@ -900,7 +900,9 @@ __device__ __forceinline__ void k4_stage_a(const KopArgs &a, double (&pv)[K4Geo<
 #pragma unroll
     for (int m = 0; m < G::SA; ++m) {
         if (G::NA % K4_THREADS != 0 && m == G::SA - 1 && po_[m] < 0) break;
-        const double p = LIVE ? fma(a.tau, k4_smem[sbase + G::STG + so_[m]], k4_smem[sbase + so_[m]]) : 0.0;
+        // PONLY: a slab halo plane staged from Ph (the neighbour's P itself)
+        const double p = !LIVE ? 0.0 : PONLY ? k4_smem[sbase + so_[m]]
+                                            : fma(a.tau, k4_smem[sbase + G::STG + so_[m]], k4_smem[sbase + so_[m]]);
         const double pz = ZDIR ? 0.0 : p;
         k4_smem[pbase + po_[m]] = p;
         k4_smem[dbase + po_[m]] = pz - pv[m];
@@ -950,8 +952,8 @@ __device__ __forceinline__ void k4_zscatter(const KopArgs &a, double (&A0)[2 * P
 }
 
 template <int P, bool XI, bool YI>
-__device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *tmu, const CUtensorMap *tmv, int sh,
-                                          int x0, int y0, int z0, int z1) {
+__device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *tmu, const CUtensorMap *tmv,
+                                          const CUtensorMap *tmp, int sh, int x0, int y0, int z0, int z1) {
     using G = K4Geo<P>;
     constexpr int W = G::W, NC = G::NC, HY = G::HY, PP = G::PP;
     // shared memory: k4_smem[sh + offset]; sh aligns the TMA staging to 128 bytes
@@ -984,7 +986,17 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
         if (ii >= npl) return;
         const int kk = kk0 + ii, slot = ii % K4_NPF;
         const unsigned mb = mb0 + 8u * slot;
-        if (kk >= a.zv0 && kk < a.zv1) {
+        if (a.Ph && kk >= a.zv0 && kk < a.zv1 && (kk < 0 || kk >= a.geo.n2)) {  // slab halo plane: P itself
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                         "r"((unsigned)(G::HXE * HY * sizeof(double)))
+                         : "memory");
+            const unsigned d = (unsigned)__cvta_generic_to_shared(k4_smem + sh + slot * 2 * G::STG);
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(d),
+                "l"(reinterpret_cast<unsigned long long>(tmp)), "r"(x0 - G::PA), "r"(y0 - P), "r"(kk - a.zv0), "r"(mb)
+                : "memory");
+        } else if (kk >= a.zv0 && kk < a.zv1) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
                          "r"((unsigned)(2 * G::HXE * HY * sizeof(double)))
                          : "memory");
@@ -1058,6 +1070,8 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
             const int db = sh + G::OFF_DT + b * G::PT;
             double *const po = (a.Pout && kk >= z0 && kk < z1) ? a.Pout + (long)kk * sz : nullptr;
             if (!(kk >= a.zv0 && kk < a.zv1)) k4_stage_a<P, false, false>(a, pv, so_, po_, go_, sb, pb, db, po);
+            else if (a.Ph && (kk < 0 || kk >= a.geo.n2))
+                k4_stage_a<P, true, false, true>(a, pv, so_, po_, go_, sb, pb, db, po);
             else if (kk + a.zoff == a.zd0 || kk + a.zoff == a.zd1)
                 k4_stage_a<P, true, true>(a, pv, so_, po_, go_, sb, pb, db, po);
             else k4_stage_a<P, true, false>(a, pv, so_, po_, go_, sb, pb, db, po);
@@ -1224,7 +1238,8 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
 
 template <int P>
 __global__ void __launch_bounds__(K4_THREADS, P <= 3 ? 2 : 1)
-    kop4_kernel(const KopArgs a, const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmv) {
+    kop4_kernel(const KopArgs a, const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmv,
+                const __grid_constant__ CUtensorMap tmp) {
     // TMA staging needs 128-byte alignment of the dynamic shared memory window
     const int sh = (int)(((128 - (__cvta_generic_to_shared(k4_smem) & 127)) & 127) / sizeof(double));
     const int x0 = kop_origin(a.ilo[0], a.ihi[0], K4_X) + (int)blockIdx.x * K4_X;
@@ -1232,10 +1247,10 @@ __global__ void __launch_bounds__(K4_THREADS, P <= 3 ? 2 : 1)
     const int z0 = blockIdx.z * a.zlen, z1 = min(a.geo.n2, z0 + a.zlen);
     const bool xi = x0 >= a.ilo[0] && x0 + K4_X - 1 <= a.ihi[0];
     const bool yi = y0 >= a.ilo[1] && y0 + K4_Y - 1 <= a.ihi[1];
-    if (xi && yi) kop4_tile<P, true, true>(a, &tmu, &tmv, sh, x0, y0, z0, z1);
-    else if (xi) kop4_tile<P, true, false>(a, &tmu, &tmv, sh, x0, y0, z0, z1);
-    else if (yi) kop4_tile<P, false, true>(a, &tmu, &tmv, sh, x0, y0, z0, z1);
-    else kop4_tile<P, false, false>(a, &tmu, &tmv, sh, x0, y0, z0, z1);
+    if (xi && yi) kop4_tile<P, true, true>(a, &tmu, &tmv, &tmp, sh, x0, y0, z0, z1);
+    else if (xi) kop4_tile<P, true, false>(a, &tmu, &tmv, &tmp, sh, x0, y0, z0, z1);
+    else if (yi) kop4_tile<P, false, true>(a, &tmu, &tmv, &tmp, sh, x0, y0, z0, z1);
+    else kop4_tile<P, false, false>(a, &tmu, &tmv, &tmp, sh, x0, y0, z0, z1);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1656,6 +1671,12 @@ __global__ void axpby_kernel(long N, double alpha, const double *__restrict__ x,
         y[q] = alpha * x[q] + beta * y[q];
 }
 
+__global__ void drift_kernel(const double *__restrict__ U, const double *__restrict__ V, double tau,
+                             double *__restrict__ P, long N) {
+    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x)
+        P[q] = fma(tau, V[q], U[q]);
+}
+
 __global__ void mask_boundary_kernel(double *u, Geom g, int zoff, int ngz) {
     long N = (long)g.n0 * g.n1 * g.n2;
     for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x) {
@@ -1778,11 +1799,13 @@ static int kop_launch(const KopArgs &a, cudaStream_t s) {
     gm.n2 = b.zv1 - b.zv0;
     const double *ub = a.U + (long)b.zv0 * a.geo.sz, *vb = (a.V ? a.V : a.U) + (long)b.zv0 * a.geo.sz;
     if (!a.V) b.tau = 0.0;
-    CUtensorMap tmu, tmv;
-    if (encode_field_map(&tmu, ub, gm, G::HXE, G::HY, 1) || encode_field_map(&tmv, vb, gm, G::HXE, G::HY, 1))
+    CUtensorMap tmu, tmv, tmp;
+    const double *pb = a.Ph ? a.Ph + (long)b.zv0 * a.geo.sz : ub;
+    if (encode_field_map(&tmu, ub, gm, G::HXE, G::HY, 1) || encode_field_map(&tmv, vb, gm, G::HXE, G::HY, 1) ||
+        encode_field_map(&tmp, pb, gm, G::HXE, G::HY, 1))
         return -2;
     dim3 grd(gx, gy, (a.geo.n2 + b.zlen - 1) / b.zlen);
-    kop4_kernel<P><<<grd, K4_THREADS, sm, s>>>(b, tmu, tmv);
+    kop4_kernel<P><<<grd, K4_THREADS, sm, s>>>(b, tmu, tmv, tmp);
     return 0;
 }
 
@@ -1951,6 +1974,10 @@ int launch_axis_apply(int p, int d, const double *band, const double *in, double
 int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s) {
     axpby_kernel<<<grid_for(N), 256, 0, s>>>(N, alpha, x, beta, y);
     return 0;
+}
+
+void launch_drift(const double *U, const double *V, double tau, double *P, long N, cudaStream_t s) {
+    drift_kernel<<<grid_for(N), 256, 0, s>>>(U, V, tau, P, N);
 }
 
 int launch_mask_boundary(double *u, const Geom &g, cudaStream_t s, int zoff, int ngz) {

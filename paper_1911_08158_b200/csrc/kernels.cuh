@@ -56,6 +56,9 @@ struct KopArgs {
     double wzc[2 * kMaxP] = {};
     // global planes whose P counts as zero in those differences (zero-Dirichlet z faces; -1: none)
     int zd0 = -1, zd1 = -1;
+    // z-slabs: the halo planes (outside [0, n2)) hold the neighbours' drifted field P itself in Ph
+    // (exchanged instead of U and V); the kernel reads them there (nullptr: U + tau V everywhere)
+    const double *Ph = nullptr;
     // z-slabs: local plane k is global row k + zoff of Mz, Kz (and of bz); input planes
     // [zv0, zv1) exist in memory (halo planes of a slab); outputs are planes [0, n2)
     int zoff = 0, zv0 = 0, zv1 = -1;
@@ -177,6 +180,8 @@ int launch_kron3(int p, const double *in, double *out, const KronTerms &k3, doub
                  cudaStream_t s);
 // y = alpha x + beta y over N elements
 int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s);
+// P = U + tau V over N contiguous elements (the drift of a slab's edge planes)
+void launch_drift(const double *U, const double *V, double tau, double *P, long N, cudaStream_t s);
 // zero the boundary faces of a field (Dirichlet masking)
 // (slabs: local plane k is global plane k + zoff of ngz; default the field is the whole grid)
 int launch_mask_boundary(double *u, const Geom &g, cudaStream_t s, int zoff = 0, int ngz = -1);
