@@ -1667,35 +1667,28 @@ int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const i
         if (cmp && (cmp[t] < 0 || cmp[t] >= h->ncomp))
             return fail(h, ADS_E_INVAL, "component %d on a handle with %d components", cmp[t], h->ncomp);
     for (ads_ctx *m : slabs_of(h)) {
-        CUDA_TRY(m, cudaMemsetAsync(m->U, 0, sizeof(double) * m->Nalloc * m->ncomp, m->stream));
+        // one pass writes every term of every component (zero on the Dirichlet faces); udot0 = 0
         CUDA_TRY(m, cudaMemsetAsync(m->V, 0, sizeof(double) * m->Nalloc * m->ncomp, m->stream));
-        if (nterms > 0) {
-            // factors: sx n0, sy n1, sz ngz (global z); a slab uses rows [zbeg, zbeg + nl)
-            const int n0 = m->n[0], n1 = m->n[1], n2 = m->ngz;
-            std::vector<double> packed((size_t)nterms * (n0 + n1 + n2));
-            double *d = nullptr;
-            if ((rc = dalloc(m, (void **)&d, sizeof(double) * packed.size()))) return rc;
-            for (int t = 0; t < nterms; ++t) {
-                std::memcpy(&packed[(size_t)t * (n0 + n1 + n2)], sx + (size_t)t * n0, sizeof(double) * n0);
-                std::memcpy(&packed[(size_t)t * (n0 + n1 + n2) + n0], sy + (size_t)t * n1, sizeof(double) * n1);
-                std::memcpy(&packed[(size_t)t * (n0 + n1 + n2) + n0 + n1], sz + (size_t)t * n2, sizeof(double) * n2);
-            }
-            CUDA_TRY(m, cudaMemcpy(d, packed.data(), sizeof(double) * packed.size(), cudaMemcpyHostToDevice));
-            for (int t = 0; t < nterms; ++t) {
-                const double *b = d + (size_t)t * (n0 + n1 + n2);
-                launch_add_separable(comp(m->U, m, cmp ? cmp[t] : 0), amp[t], b, b + n0, b + n0 + n1 + m->zbeg, m->geo,
-                                     m->stream);
-                if ((rc = check_launch(m, "separable"))) return rc;
-            }
-            CUDA_TRY(m, cudaStreamSynchronize(m->stream));
-            cudaFree(d);
-            m->allocs.pop_back();
+        const int n0 = m->n[0], n1 = m->n[1], n2 = m->ngz;
+        const size_t tl = 2 + (size_t)n0 + n1 + n2;
+        std::vector<double> packed((size_t)std::max(nterms, 1) * tl, 0.0);
+        for (int t = 0; t < nterms; ++t) {
+            double *f = &packed[(size_t)t * tl];
+            f[0] = amp[t];
+            f[1] = cmp ? cmp[t] : 0;
+            std::memcpy(f + 2, sx + (size_t)t * n0, sizeof(double) * n0);
+            std::memcpy(f + 2 + n0, sy + (size_t)t * n1, sizeof(double) * n1);
+            std::memcpy(f + 2 + n0 + n1, sz + (size_t)t * n2, sizeof(double) * n2);
         }
-        if (m->bc == ADS_BC_DIRICHLET0)
-            for (int c = 0; c < m->ncomp; ++c) {
-                launch_mask_boundary(comp(m->U, m, c), m->geo, m->stream, m->zbeg, zmask(m));
-                if ((rc = check_launch(m, "mask"))) return rc;
-            }
+        double *d = nullptr;
+        if ((rc = dalloc(m, (void **)&d, sizeof(double) * packed.size()))) return rc;
+        CUDA_TRY(m, cudaMemcpyAsync(d, packed.data(), sizeof(double) * packed.size(), cudaMemcpyHostToDevice, m->stream));
+        const bool dir = m->bc == ADS_BC_DIRICHLET0;
+        launch_set_separable(m->U, m->Nalloc, m->ncomp, nterms, d, n0, n1, n2, m->geo, m->zbeg, dir ? 1 : 0,
+                             dir ? 1 : 0, dir ? zmask(m) : 0, m->stream);
+        if ((rc = check_launch(m, "separable"))) return rc;
+        CUDA_TRY(m, cudaStreamSynchronize(m->stream));  // the packed factors live in a host vector
+        dfree(m, d);
     }
     return h->ncomp == 3 ? el_init(h) : init_state(h);
 }

@@ -1,10 +1,12 @@
 // kernels.cu -- sm_100a fp64 kernels of the ADS wave step (arXiv:1911.08158).
 //
-//   kop_kernel   : drift P = U + tau V, source, and the sum-factorised
+//   kop4_kernel  : drift P = U + tau V, source, and the sum-factorised
 //                  Kronecker operator K P (Eq. 14, 3D) in ONE
-//                  pass: a 32x8 (x,y) tile marches along z; per plane the x- and
-//                  y-passes run from shared memory and the z-pass from a
-//                  register ring of 2p+1 planes.  HBM: reads U, V; writes P, r.
+//                  pass, every stiffness factor on P itself (K first; Kz in
+//                  plane-difference form): a 32x16 (x,y) tile marches along z;
+//                  per plane the x- and y-passes run from shared memory and the
+//                  z-pass from a register ring of 2p+1 planes.  HBM: reads U, V;
+//                  writes P, r.
 //   sweep_kernel : batched banded LU solves A_d^-1 along x, y or z
 //                  (PAPER.md:533-618).  Each line is split into C chunks; every
 //                  chunk runs the p-term recurrences twice (zero incoming state
@@ -408,12 +410,12 @@ __global__ void __launch_bounds__(SW<LW, C>::THREADS, 512 / SW<LW, C>::THREADS)
         // n0 zero-filled by the TMA unit (out-of-bounds fill); mbarrier completion.  The next
         // tile's load is issued after the first in-solve barrier (everyone has read the buffer);
         // the kick's V tile is loaded at the tile start and consumed after the solve.
-        const long sl = a.dir == 1 ? g.sy : g.sz;
-        const long sb = a.dir == 1 ? g.sz : g.sy;
         const int nb = a.dir == 1 ? g.n2 : g.n1;
         const int nib = (g.n0 + SW_LW - 1) / SW_LW;
         const long ntiles = (long)nib * nb;
         const bool kick = a.mode == 1;
+        const long sl = a.dir == 1 ? g.sy : g.sz;
+        const long sb = a.dir == 1 ? g.sz : g.sy;
         const int nv = max(0, min(L, n - s));  // rows of my chunk inside the line
         // buffers (128-byte aligned) and two mbarriers after them
         double *ibase = buf + ((128 - (reinterpret_cast<uintptr_t>(buf) & 127)) & 127) / sizeof(double);
@@ -486,6 +488,9 @@ __global__ void __launch_bounds__(SW<LW, C>::THREADS, 512 / SW<LW, C>::THREADS)
 #pragma unroll
                 for (int j = 0; j < L; ++j) vb[j * SW_LW] = v[j];
             } else {
+                // a (the last step of a batch) is stored straight from registers: staging it by TMA
+                // needs the input tile, and serialising the next tile's load behind that store
+                // measured no faster (1.02 vs ~1.0 ms at c4)
                 wait(mb_v, ph);
                 double *po = a.out ? a.out + base : nullptr;
 #pragma unroll
@@ -515,310 +520,8 @@ __global__ void __launch_bounds__(SW<LW, C>::THREADS, 512 / SW<LW, C>::THREADS)
     }
 }
 
-// ------------------------------------------------------------------------------------------
-// fused drift + source + K-apply (v3)
-//
-//   P = U + tau V (written to Pout),  r = g (bx (x) by (x) bz) + sign K P,
-//   K = Kx My Mz + Mx Ky Mz + Mx My Kz   (Eq. 14, 3D)
-// by sum factorisation: y-pass Y1 = My P, Y2 = Ky P; x-pass S = Kx Y1 + Mx Y2,
-// T = Mx Y1; z-pass K P = Mz S + Kz T  (7 banded passes).
-//
-// CTA = 256 threads on a KT_X x KT_Y = 32 x 16 output tile, marching along z over
-// [z0, z1).  Per input plane kk (two barriers):
-//   - copy warps stream the raw U, V plane of the haloed tile HBM -> shared memory in
-//     16-byte cp.async pieces (the x halo is rounded up to an even width so every piece
-//     is aligned; out-of-domain pieces are zero-filled by the copy), KT_NPF-1 planes ahead;
-//   - y-pass warps: item (column, 4 rows) forms P = U + tau V on 4+2p rows, writes the
-//     owned P to HBM and Y1/Y2 of its 4 rows to shared memory;
-//   - x-pass, all warps: lane = x, warp = 2 rows: S, T from 2p+1 neighbouring (Y1, Y2);
-//   - z-pass: input plane kk adds Mz(k,kk) S + Kz(k,kk) T to the 2p+1 pending output
-//     planes k = kk-p..kk+p held in registers; output kk-p is complete and stored.
-// Interior tiles/planes (Toeplitz rows, symmetric after host_setup build_space) use the
-// constant-bank rows in pair-sum form (p+1 distinct coefficients per band); boundary
-// tiles read staged rows from shared memory, boundary planes from global memory.
-// HBM traffic: U, V read once (halos re-read from L2), P and r written once.
-// ------------------------------------------------------------------------------------------
-constexpr int KT_X = 32, KT_Y = 16, KT_THREADS = 256, KT_NPF = 4, KT_RY = 4;
-template <int P>
-struct KopGeo {
-    static constexpr int W = 2 * P + 1;
-    static constexpr int PA = (P + 1) & ~1;               // even x halo of the copied tile
-    static constexpr int HX = KT_X + 2 * PA, HY = KT_Y + 2 * P, HN = HX * HY;
-    static constexpr int NC = KT_X + 2 * P;               // columns the x-pass needs
-    static constexpr int NITEM = NC * (KT_Y / KT_RY);     // y-pass items
-    static constexpr int YW = (NITEM + 31) / 32;          // y-pass warps
-    static constexpr int NCT = KT_THREADS - 32 * YW;      // copy threads
-    static constexpr int NPAIR = HN / 2;                  // 16-byte pieces per field and plane
-    static constexpr int NSLOT = (NPAIR + NCT - 1) / NCT;
-    // shared memory (doubles): raw ring [NPF][U|V][HY][HX] | Y tiles [2][KT_Y][NC] double2 | rows
-    static constexpr int RING = KT_NPF * 2 * HN, YT = 2 * KT_Y * NC * 2, XB = KT_X * 2 * W, YB = KT_Y * 2 * W;
-    static constexpr int SMEM = RING + YT + XB + YB;
-    static_assert(NCT >= 32, "at least one copy warp");
-};
-
-// z-pass scatter of one input plane kk (ring slot U = (kk - kk0) mod W, see kop_tile)
-template <int P, int U>
-__device__ __forceinline__ void kop_zscatter(const KopArgs &a, double (&A0)[2 * P + 1], double (&A1)[2 * P + 1],
-                                             double s0, double t0, double s1, double t1, int kk, bool zint,
-                                             double &o0, double &o1) {
-    constexpr int W = 2 * P + 1;
-    if (zint) {
-#pragma unroll
-        for (int c = 0; c < W; ++c) {
-            const int sl = ((U - P + c) % W + W) % W, d = c < P ? P - c : c - P;
-            A0[sl] = fma(a.mc[2][P + d], s0, A0[sl]);
-            A0[sl] = fma(a.kc[2][P + d], t0, A0[sl]);
-            A1[sl] = fma(a.mc[2][P + d], s1, A1[sl]);
-            A1[sl] = fma(a.kc[2][P + d], t1, A1[sl]);
-        }
-    } else {
-        const int n2 = a.geo.n2;
-#pragma unroll
-        for (int c = 0; c < W; ++c) {
-            const int sl = ((U - P + c) % W + W) % W;
-            const int k = kk - P + c;
-            double mz_ = 0.0, kz_ = 0.0;
-            if (k >= 0 && k < n2) {  // output planes; band rows are global rows k + zoff
-                mz_ = __ldg(a.mz + (long)(k + a.zoff) * W + 2 * P - c);
-                kz_ = a.kw[2] * __ldg(a.kz + (long)(k + a.zoff) * W + 2 * P - c);
-            }
-            A0[sl] = fma(mz_, s0, A0[sl]);
-            A0[sl] = fma(kz_, t0, A0[sl]);
-            A1[sl] = fma(mz_, s1, A1[sl]);
-            A1[sl] = fma(kz_, t1, A1[sl]);
-        }
-    }
-    constexpr int so = ((U - P) % W + W) % W;  // slot of the completed output kk - P
-    o0 = A0[so];
-    o1 = A1[so];
-    A0[so] = 0.0;
-    A1[so] = 0.0;
-}
-
-__device__ __forceinline__ void cp_async16_zfill(unsigned sdst, const double *gsrc, unsigned nbytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst), "l"(gsrc), "r"(nbytes) : "memory");
-}
-
 // first tile origin: ilo - T when the Toeplitz interior exists (ilo <= ihi), else 0
 __host__ __device__ inline int kop_origin(int ilo, int ihi, int T) { return ilo <= ihi ? ilo - T : 0; }
-
-template <int P, bool XI, bool YI>
-__device__ __forceinline__ void kop_tile(const KopArgs &a, double *smem, int x0, int y0, int z0, int z1) {
-    using G = KopGeo<P>;
-    constexpr int W = G::W, HX = G::HX, HN = G::HN, NC = G::NC, PA = G::PA;
-    double *ring = smem;
-    double2 *Ys = reinterpret_cast<double2 *>(smem + G::RING);
-    double *xb = smem + G::RING + G::YT;  // [W][2][KT_X]: (Mx, Kx) rows of x0 + lane (lane fastest)
-    double *yb = xb + G::XB;              // [KT_Y][2][W]: (My, Ky) rows of y0 + row
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int n0 = a.geo.n0, n1 = a.geo.n1, n2 = a.geo.n2;
-    const long sy = a.geo.sy, sz = a.geo.sz;
-
-    if (!XI)  // stage boundary band rows (zero outside the domain)
-        for (int e = tid; e < KT_X * 2 * W; e += KT_THREADS) {
-            const int xr = e % KT_X, m = (e / KT_X) & 1, c = e / (2 * KT_X), X = x0 + xr;
-            xb[e] = (X >= 0 && X < n0) ? (m ? a.kw[0] : 1.0) * __ldg((m ? a.kx : a.mx) + (long)X * W + c) : 0.0;
-        }
-    if (!YI) {
-        for (int e = tid; e < KT_Y * 2 * W; e += KT_THREADS) {
-            const int yr = e / (2 * W), m = (e / W) & 1, c = e % W, Y = y0 + yr;
-            yb[e] = (Y >= 0 && Y < n1) ? (m ? a.kw[1] : 1.0) * __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
-        }
-    }
-
-    // ---- copy threads: 16-byte pieces e = ct + NCT m of the [HY][HX/2] plane (fixed per thread)
-    const bool copier = tid >= 32 * G::YW;
-    const int ct = tid - 32 * G::YW;
-    int goff[G::NSLOT];
-    unsigned inr = 0;
-#pragma unroll
-    for (int m = 0; m < G::NSLOT; ++m) {
-        const int e = ct + m * G::NCT, hy = e / (HX / 2), hx = 2 * (e - hy * (HX / 2));
-        const int X = x0 - PA + hx, Y = y0 - P + hy;
-        const bool in = copier && e < G::NPAIR && X >= 0 && X < n0 && Y >= 0 && Y < n1;
-        goff[m] = in ? (Y * (int)sy + X) : 0;
-        if (in) inr |= 1u << m;
-    }
-    const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;
-    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * (ct > 0 ? ct : 0);
-    auto issue = [&](int ii) {
-        // planes outside [zv0, zv1) are zero: nothing is copied (their y/x passes are skipped)
-        if (copier && ii < npl && kk0 + ii >= a.zv0 && kk0 + ii < a.zv1) {
-            const int kk = kk0 + ii;
-            const unsigned su = ring_s + 8u * (unsigned)((ii & (KT_NPF - 1)) * 2 * HN);
-            const bool kv = true;
-            const double *pu = a.U + (kv ? (long)kk * sz : 0), *pv = a.V + (kv ? (long)kk * sz : 0);
-#pragma unroll
-            for (int m = 0; m < G::NSLOT; ++m) {
-                if (ct + m * G::NCT >= G::NPAIR) break;
-                const unsigned nb = (kv && (inr >> m & 1)) ? 16u : 0u;
-                cp_async16_zfill(su + 16u * m * G::NCT, pu + goff[m], nb);
-                cp_async16_zfill(su + 16u * m * G::NCT + 8u * HN, pv + goff[m], nb);
-            }
-        }
-        cp_async_commit();
-    };
-
-    // ---- y-pass item: needed column nc (haloed column PA - P + nc), output rows 4 grp .. 4 grp + 3
-    const bool yitem = tid < G::NITEM;
-    const int nc = tid % NC, grp = tid / NC, hcol = PA - P + nc;
-    const int Xc = x0 - P + nc;
-    const bool pown = yitem && nc >= P && nc < P + KT_X && Xc >= 0 && Xc < n0;
-    // owned P of this item: rows y0 + 4 grp + r (r < prows) at column Xc, plane offset added per plane
-    // rows r in [prow0, prows) of the item are inside the grid
-    const int prow0 = max(0, -(y0 + KT_RY * grp)), prows = min(KT_RY, n1 - (y0 + KT_RY * grp));
-    double *const pbase = (a.Pout && pown && prows > prow0) ? a.Pout + (long)(y0 + KT_RY * grp) * sy + Xc : nullptr;
-    // ---- x-pass outputs: X = x0 + lane, rows 2w, 2w+1
-    const int X = x0 + lane;
-    const int Yo0 = y0 + 2 * w;
-    const bool xin = X >= 0 && X < n0;
-    const bool own0 = xin && Yo0 >= 0 && Yo0 < n1, own1 = xin && Yo0 + 1 >= 0 && Yo0 + 1 < n1;
-    const double sxy0 = (a.bx && own0) ? __ldg(a.bx + X) * __ldg(a.by + Yo0) : 0.0;
-    const double sxy1 = (a.bx && own1) ? __ldg(a.bx + X) * __ldg(a.by + Yo0 + 1) : 0.0;
-    const long oxy = (long)Yo0 * sy + X;
-    const bool has_src = a.bx != nullptr;
-    double gsrc = a.g;
-    if (has_src && a.dstep) {  // source time from the device step counter (CUDA graph replays)
-        const double x = 3.141592653589793238462643383 * a.f0 * ((double)(*a.dstep + 1) * a.tau_g - a.t0);
-        gsrc = a.amp * (a.wav ? (1.0 - 2.0 * x * x) * exp(-x * x) : 1.0);
-    }
-    double *rq = a.r + oxy + (long)z0 * sz;  // output plane z0 first; advanced per completed plane
-
-    // pending outputs: A0/A1[(k - kk0) mod W] accumulates plane k of rows 2w, 2w+1
-    double A0[W], A1[W];
-#pragma unroll
-    for (int c = 0; c < W; ++c) A0[c] = A1[c] = 0.0;
-
-#pragma unroll
-    for (int i = 0; i < KT_NPF - 1; ++i) issue(i);
-    __syncthreads();  // staged band rows visible
-
-    // one barrier per plane: iteration ii runs the y-pass of plane ii (Ys buffer ii & 1) and the
-    // x/z passes of plane ii - 1 (buffer (ii - 1) & 1), so the two overlap across warps
-    int zslot = W - 1;  // ring slot of plane ii - 1 = (ii - 1) mod W
-    for (int ii = 0; ii <= npl; ++ii) {
-        const int kk = kk0 + ii, kx = kk - 1;
-        if (ii < npl) cp_async_wait<KT_NPF - 2>();
-        __syncthreads();  // plane kk landed; Ys[(ii-1)&1] complete; ring slot (ii-1)%NPF free
-        if (ii < npl) issue(ii + KT_NPF - 1);
-        // ---- y-pass of plane kk into Ys buffer ii & 1 (zero planes outside [zv0, zv1) skipped)
-        if (yitem && ii < npl && kk >= a.zv0 && kk < a.zv1) {
-            double2 *Ysb = Ys + (ii & 1) * KT_Y * NC;
-            const double *bu = ring + (ii & (KT_NPF - 1)) * 2 * HN, *bv = bu + HN;
-            double pr[KT_RY + 2 * P];
-#pragma unroll
-            for (int r = 0; r < KT_RY + 2 * P; ++r) {
-                const int e = (KT_RY * grp + r) * HX + hcol;
-                pr[r] = fma(a.tau, bv[e], bu[e]);
-            }
-            if (pbase && kk >= z0 && kk < z1) {
-                double *pp = pbase + (long)kk * sz;
-#pragma unroll
-                for (int r = 0; r < KT_RY; ++r)
-                    if (r >= prow0 && r < prows) pp[r * sy] = pr[r + P];
-            }
-#pragma unroll
-            for (int r = 0; r < KT_RY; ++r) {
-                const int yr = KT_RY * grp + r;
-                double y1, y2;
-                if (YI) {
-                    const double ce = pr[r + P];
-                    y1 = a.mc[1][P] * ce;
-                    y2 = a.kc[1][P] * ce;
-#pragma unroll
-                    for (int d = 1; d <= P; ++d) {
-                        const double sp = pr[r + P - d] + pr[r + P + d];
-                        y1 = fma(a.mc[1][P + d], sp, y1);
-                        y2 = fma(a.kc[1][P + d], sp, y2);
-                    }
-                } else {
-                    y1 = 0.0;
-                    y2 = 0.0;
-#pragma unroll
-                    for (int c = 0; c < W; ++c) {
-                        y1 = fma(yb[(yr * 2 + 0) * W + c], pr[r + c], y1);
-                        y2 = fma(yb[(yr * 2 + 1) * W + c], pr[r + c], y2);
-                    }
-                }
-                Ysb[yr * NC + nc] = make_double2(y1, y2);
-            }
-        }
-        // ---- x-pass of plane kx = kk - 1 from Ys buffer (ii - 1) & 1
-        if (ii == 0) continue;
-        zslot = zslot == W - 1 ? 0 : zslot + 1;
-        const double2 *Yr = Ys + ((ii - 1) & 1) * KT_Y * NC;
-        double s0, t0, s1, t1;
-        if (kx < a.zv0 || kx >= a.zv1) {  // a zero plane: it only advances the z ring
-            s0 = t0 = s1 = t1 = 0.0;
-        } else if (XI) {
-            const double2 c0 = Yr[(2 * w) * NC + lane + P], c1 = Yr[(2 * w + 1) * NC + lane + P];
-            s0 = fma(a.kc[0][P], c0.x, a.mc[0][P] * c0.y);
-            t0 = a.mc[0][P] * c0.x;
-            s1 = fma(a.kc[0][P], c1.x, a.mc[0][P] * c1.y);
-            t1 = a.mc[0][P] * c1.x;
-#pragma unroll
-            for (int d = 1; d <= P; ++d) {
-                const double2 l0 = Yr[(2 * w) * NC + lane + P - d], r0 = Yr[(2 * w) * NC + lane + P + d];
-                const double2 l1 = Yr[(2 * w + 1) * NC + lane + P - d], r1 = Yr[(2 * w + 1) * NC + lane + P + d];
-                const double a0 = l0.x + r0.x, b0 = l0.y + r0.y, a1 = l1.x + r1.x, b1 = l1.y + r1.y;
-                s0 = fma(a.kc[0][P + d], a0, s0);
-                s0 = fma(a.mc[0][P + d], b0, s0);
-                t0 = fma(a.mc[0][P + d], a0, t0);
-                s1 = fma(a.kc[0][P + d], a1, s1);
-                s1 = fma(a.mc[0][P + d], b1, s1);
-                t1 = fma(a.mc[0][P + d], a1, t1);
-            }
-        } else {
-            s0 = t0 = s1 = t1 = 0.0;
-#pragma unroll
-            for (int c = 0; c < W; ++c) {
-                const double mx_ = xb[(c * 2 + 0) * KT_X + lane], kx_ = xb[(c * 2 + 1) * KT_X + lane];
-                const double2 q0 = Yr[(2 * w) * NC + lane + c], q1 = Yr[(2 * w + 1) * NC + lane + c];
-                s0 = fma(kx_, q0.x, s0);
-                s0 = fma(mx_, q0.y, s0);
-                t0 = fma(mx_, q0.x, t0);
-                s1 = fma(kx_, q1.x, s1);
-                s1 = fma(mx_, q1.y, s1);
-                t1 = fma(mx_, q1.x, t1);
-            }
-        }
-        // ---- z-pass (a switch makes every ring slot index compile-time)
-        const bool zint = kx + a.zoff - P >= a.ilo[2] && kx + a.zoff + P <= a.ihi[2];
-        double o0 = 0.0, o1 = 0.0;
-        switch (zslot) {
-#define ADS_ZCASE(U)                                                                   \
-    case U:                                                                            \
-        if constexpr (U < W) kop_zscatter<P, U>(a, A0, A1, s0, t0, s1, t1, kx, zint, o0, o1); \
-        break;
-            ADS_ZCASE(0) ADS_ZCASE(1) ADS_ZCASE(2) ADS_ZCASE(3) ADS_ZCASE(4) ADS_ZCASE(5)
-            ADS_ZCASE(6) ADS_ZCASE(7) ADS_ZCASE(8) ADS_ZCASE(9) ADS_ZCASE(10)
-#undef ADS_ZCASE
-        }
-        // output plane kx - P is complete: r = g bx by bz + sign K P
-        if (kx - P >= z0) {
-            const double gz = has_src ? gsrc * __ldg(a.bz + kx - P + a.zoff) : 0.0;
-            if (own0) rq[0] = fma(a.sign, o0, gz * sxy0);
-            if (own1) rq[sy] = fma(a.sign, o1, gz * sxy1);
-            rq += sz;
-        }
-    }
-}
-
-template <int P>
-__global__ void __launch_bounds__(KT_THREADS, 2) kop_kernel(const KopArgs a) {
-    extern __shared__ __align__(16) double smem[];
-    // tiles are aligned to the Toeplitz interior: tile 1 starts at ilo (interior tiles use the
-    // constant-bank pair-sum form; only the first and last tile per direction are generic)
-    const int x0 = kop_origin(a.ilo[0], a.ihi[0], KT_X) + (int)blockIdx.x * KT_X;
-    const int y0 = kop_origin(a.ilo[1], a.ihi[1], KT_Y) + (int)blockIdx.y * KT_Y;
-    const int z0 = blockIdx.z * a.zlen, z1 = min(a.geo.n2, z0 + a.zlen);
-    const bool xi = x0 >= a.ilo[0] && x0 + KT_X - 1 <= a.ihi[0];
-    const bool yi = y0 >= a.ilo[1] && y0 + KT_Y - 1 <= a.ihi[1];
-    if (xi && yi) kop_tile<P, true, true>(a, smem, x0, y0, z0, z1);
-    else if (xi) kop_tile<P, true, false>(a, smem, x0, y0, z0, z1);
-    else if (yi) kop_tile<P, false, true>(a, smem, x0, y0, z0, z1);
-    else kop_tile<P, false, false>(a, smem, x0, y0, z0, z1);
-}
 
 // ------------------------------------------------------------------------------------------
 // fused drift + source + K-apply (v4, "K first")
@@ -1079,7 +782,7 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
         // ---- B: plane c = kk0 + ib (Ky P, Kx P, owned P) and D = P_c - P_{c-1} (My D)
         const int ib = ii - 1;
         if (ib >= 0 && ib < npl) {
-            const int b = ib & 1, kc_ = kk0 + ib;
+            const int b = ib & 1;
             const double *pt = k4_smem + sh + G::OFF_PT + b * G::PT;
             const double *dt = k4_smem + sh + G::OFF_DT + b * G::PT;
             if (w < G::CW) {
@@ -1388,7 +1091,7 @@ int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {
 
 // Kronecker triples out = beta out + sum_t alpha_t (Fx_t (x) Fy_t (x) Fz_t) in, t < T <= 2, sharing
 // input and output (elasticity couplings: the two triples of an off-diagonal
-// block Upsilon_ik go in one pass; general bands, no Toeplitz assumption).  Same structure as kop_kernel:
+// block Upsilon_ik go in one pass; general bands, no Toeplitz assumption).  Same structure as the round-1 operator kernel:
 // 32 x 16 output tile marching z over a piece [z0, z1); per input plane (one barrier):
 //   - all threads stream the haloed plane HBM -> shared memory in 16-byte zero-filling cp.async
 //     pieces, KR_NPF - 1 planes ahead;
@@ -1470,7 +1173,6 @@ __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__re
     };
     const bool yitem = tid < G::NITEM;
     const int nc = tid % NC, grp = tid / NC, hcol = PA - P + nc;
-    const int Xc = x0 - P + nc;
     const int X = x0 + lane, Yo = y0 + 2 * w;
     const bool own0 = X < n0 && Yo < n1, own1 = X < n0 && Yo + 1 < n1;
     double r0[T][W], r1[T][W];  // X_t planes kk - 2p .. kk of rows 2w, 2w + 1 (r[.][W-1] newest)
@@ -1671,6 +1373,32 @@ __global__ void axpby_kernel(long N, double alpha, const double *__restrict__ x,
         y[q] = alpha * x[q] + beta * y[q];
 }
 
+// u_c = sum over the terms t of component c of amp_t sx_t[i] sy_t[j] sz_t[k + zoff], zero on the
+// Dirichlet faces (mx, my: x / y faces; ngz > 0: the global z faces 0 and ngz - 1): one write pass
+// for all terms and components.  f: per term [amp, comp, sx (n0), sy (n1), sz (nzf)]
+__global__ void set_separable_kernel(double *u, long cstride, int nterms, const double *__restrict__ f, int n0f, int n1f,
+                                     int nzf, Geom g, int zoff, int mx, int my, int ngz, int ncomp) {
+    const long N = (long)g.n0 * g.n1 * g.n2;
+    const long tl = 2 + n0f + n1f + nzf;
+    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(q % g.n0);
+        const long t = q / g.n0;
+        const int j = (int)(t % g.n1), k = (int)(t / g.n1);
+        const int kg = k + zoff;
+        const bool bnd = (mx && (i == 0 || i == g.n0 - 1)) || (my && (j == 0 || j == g.n1 - 1)) ||
+                         (ngz > 0 && (kg == 0 || kg == ngz - 1));
+        double acc[3] = {0.0, 0.0, 0.0};
+        if (!bnd)
+            for (int m = 0; m < nterms; ++m) {
+                const double *ft = f + m * tl;
+                const int c = (int)ft[1];
+                acc[c] = fma(ft[0] * __ldg(ft + 2 + i) * __ldg(ft + 2 + n0f + j), __ldg(ft + 2 + n0f + n1f + kg), acc[c]);
+            }
+        const long o = (long)k * g.sz + (long)j * g.sy + i;
+        for (int c = 0; c < ncomp; ++c) u[c * cstride + o] = acc[c];
+    }
+}
+
 __global__ void drift_kernel(const double *__restrict__ U, const double *__restrict__ V, double tau,
                              double *__restrict__ P, long N) {
     for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x)
@@ -1687,18 +1415,6 @@ __global__ void mask_boundary_kernel(double *u, Geom g, int zoff, int ngz) {
         const int kg = k + zoff;  // global plane
         if (i == 0 || j == 0 || i == g.n0 - 1 || j == g.n1 - 1 || (ngz > 0 && (kg == 0 || kg == ngz - 1)))
             u[(long)k * g.sz + (long)j * g.sy + i] = 0.0;
-    }
-}
-
-__global__ void add_separable_kernel(double *u, double amp, const double *sx, const double *sy, const double *sz,
-                                     Geom g) {
-    long N = (long)g.n0 * g.n1 * g.n2;
-    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x) {
-        int i = q % g.n0;
-        long t = q / g.n0;
-        int j = t % g.n1;
-        int k = t / g.n1;
-        u[(long)k * g.sz + (long)j * g.sy + i] += amp * sx[i] * sy[j] * sz[k];
     }
 }
 
@@ -1766,26 +1482,10 @@ static int kop_pieces(int n2, int P, long tiles, long resident, double halo) {
 
 template <int P>
 static int kop_launch(const KopArgs &a, cudaStream_t s) {
-    static const bool v3 = [] {  // A/B switch: the v3 (mass-first) kernel
-        const char *e = std::getenv("ADS_KOP_V3");
-        return e && std::atoi(e) != 0;
-    }();
     KopArgs b = a;
     if (b.zv1 < b.zv0) {  // no halo planes: exactly the output planes exist
         b.zv0 = 0;
         b.zv1 = a.geo.n2;
-    }
-    if (v3) {
-        using G = KopGeo<P>;
-        const size_t sm = sizeof(double) * G::SMEM;
-        const LaunchFacts lf = launch_facts((const void *)kop_kernel<P>, KT_THREADS, sm);
-        const int ox = kop_origin(a.ilo[0], a.ihi[0], KT_X), oy = kop_origin(a.ilo[1], a.ihi[1], KT_Y);
-        const int gx = (a.geo.n0 - ox + KT_X - 1) / KT_X, gy = (a.geo.n1 - oy + KT_Y - 1) / KT_Y;
-        const int nz = kop_pieces(a.geo.n2, P, (long)gx * gy, (long)lf.per_sm * lf.nsm, 2.0 * P);
-        b.zlen = a.zlen > 0 ? a.zlen : (a.geo.n2 + nz - 1) / nz;
-        dim3 grd(gx, gy, (a.geo.n2 + b.zlen - 1) / b.zlen);
-        kop_kernel<P><<<grd, KT_THREADS, sm, s>>>(b);
-        return 0;
     }
     using G = K4Geo<P>;
     const size_t sm = sizeof(double) * G::SMEM;
@@ -1976,18 +1676,18 @@ int launch_axpby(long N, double alpha, const double *x, double beta, double *y, 
     return 0;
 }
 
+void launch_set_separable(double *u, long cstride, int ncomp, int nterms, const double *f, int n0f, int n1f, int nzf,
+                          const Geom &g, int zoff, int mx, int my, int ngz, cudaStream_t s) {
+    set_separable_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(u, cstride, nterms, f, n0f, n1f, nzf, g, zoff,
+                                                                            mx, my, ngz, ncomp);
+}
+
 void launch_drift(const double *U, const double *V, double tau, double *P, long N, cudaStream_t s) {
     drift_kernel<<<grid_for(N), 256, 0, s>>>(U, V, tau, P, N);
 }
 
 int launch_mask_boundary(double *u, const Geom &g, cudaStream_t s, int zoff, int ngz) {
     mask_boundary_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(u, g, zoff, ngz < 0 ? g.n2 : ngz);
-    return 0;
-}
-
-int launch_add_separable(double *u, double amp, const double *sx, const double *sy, const double *sz, const Geom &g,
-                         cudaStream_t s) {
-    add_separable_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(u, amp, sx, sy, sz, g);
     return 0;
 }
 

@@ -180,14 +180,16 @@ int launch_kron3(int p, const double *in, double *out, const KronTerms &k3, doub
                  cudaStream_t s);
 // y = alpha x + beta y over N elements
 int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s);
+// u_c = sum_{t: comp_t = c} amp_t sx_t (x) sy_t (x) sz_t for every component c < ncomp (component stride
+// cstride), zero on the Dirichlet faces (mx, my; ngz > 0: global z faces), in one pass.  f holds per
+// term [amp, comp, sx (n0f), sy (n1f), sz (nzf, global z)]; local plane k is global plane k + zoff.
+void launch_set_separable(double *u, long cstride, int ncomp, int nterms, const double *f, int n0f, int n1f, int nzf,
+                          const Geom &g, int zoff, int mx, int my, int ngz, cudaStream_t s);
 // P = U + tau V over N contiguous elements (the drift of a slab's edge planes)
 void launch_drift(const double *U, const double *V, double tau, double *P, long N, cudaStream_t s);
 // zero the boundary faces of a field (Dirichlet masking)
 // (slabs: local plane k is global plane k + zoff of ngz; default the field is the whole grid)
 int launch_mask_boundary(double *u, const Geom &g, cudaStream_t s, int zoff = 0, int ngz = -1);
-// u += amp * sx (x) sy (x) sz
-int launch_add_separable(double *u, double amp, const double *sx, const double *sy, const double *sz, const Geom &g,
-                         cudaStream_t s);
 // deterministic dot product: partial sums into `partial` (>= 1024 doubles), result into *res (device)
 int launch_dot(long N, const double *x, const double *y, double *partial, double *res, cudaStream_t s);
 
