@@ -553,7 +553,7 @@ __host__ __device__ inline int kop_origin(int ilo, int ihi, int T) { return ilo 
 // in pair form; boundary tiles read staged rows, boundary planes read global rows.
 // HBM traffic: U, V read once (halos from L2), P and r written once: 32 B/DOF.
 // ------------------------------------------------------------------------------------------
-constexpr int K4_X = 32, K4_Y = 16, K4_THREADS = 256, K4_NPF = 3, K4_XP = 34;
+constexpr int K4_X = 32, K4_Y = 16, K4_THREADS = 256, K4_NPF = 2, K4_XP = 36, K4_YQP = 44;
 template <int P>
 struct K4Geo {
     static constexpr int W = 2 * P + 1;
@@ -574,15 +574,27 @@ struct K4Geo {
     static_assert(RW >= 1, "row-item warps");
     static constexpr int al16(int v) { return (v + 15) & ~15; }
     static constexpr int STG = al16(HXE * HY);          // one staged field plane (128-byte multiple)
-    static constexpr int PT = al16(HY * PP), YQ = al16(K4_Y * NC * 2);
-    static constexpr int X1 = al16(HY * K4_XP), XB = al16(K4_X * 2 * W), YB = al16(K4_Y * 2 * W);
+    // stage C runs on the FP64 tensor cores: KS k-steps of 4 cover the 8 + 2p band columns of an 8-wide
+    // output block; the (Ky P, My D) tile rows are padded to K4_YQP double2 and the Kx P tile to HX1
+    // rows (zero: the fragments of the last block read past the haloed tile)
+    static constexpr int KS = (8 + 2 * P + 3) / 4, HX1 = 8 + 4 * KS;
+    static_assert(24 + 4 * KS <= K4_YQP && HX1 >= HY, "stage-C fragment windows");
+    static constexpr int PT = al16(HY * PP), YQ = al16(K4_Y * K4_YQP * 2);
+    static constexpr int X1 = al16(HX1 * K4_XP), XB = al16(K4_X * 2 * W), YB = al16(K4_Y * 2 * W);
+    static constexpr int FR = al16(6 * KS * 32);  // band fragments: Mx per n block (4), My per m block (2)
     static constexpr int OFF_PT = K4_NPF * 2 * STG, OFF_DT = OFF_PT + 2 * PT, OFF_YQ = OFF_DT + 2 * PT;
     static constexpr int OFF_X1 = OFF_YQ + 2 * YQ, OFF_XB = OFF_X1 + 2 * X1, OFF_YB = OFF_XB + XB;
-    static constexpr int OFF_MB = OFF_YB + YB;
+    static constexpr int OFF_FR = OFF_YB + YB, OFF_MB = OFF_FR + FR;
     static constexpr int SMEM = OFF_MB + 16 + 16;       // mbarriers + 128-byte alignment slack
 };
 
 extern __shared__ __align__(128) double k4_smem[];
+
+__device__ __forceinline__ void k4_dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
 
 __device__ __forceinline__ void k4_wait(unsigned mb, unsigned parity) {
     asm volatile(
@@ -597,7 +609,7 @@ __device__ __forceinline__ void k4_wait(unsigned mb, unsigned parity) {
 // it counts as zero in the plane differences)
 template <int P, bool LIVE, bool ZDIR, bool PONLY = false>
 __device__ __forceinline__ void k4_stage_a(const KopArgs &a, double (&pv)[K4Geo<P>::SA], const int (&so_)[K4Geo<P>::SA],
-                                           const int (&po_)[K4Geo<P>::SA], const long (&go_)[K4Geo<P>::SA], int sbase,
+                                           const int (&po_)[K4Geo<P>::SA], const int (&go_)[K4Geo<P>::SA], int sbase,
                                            int pbase, int dbase, double *pout) {
     using G = K4Geo<P>;
 #pragma unroll
@@ -677,6 +689,32 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
             const int yr = e / (2 * W), m = (e / W) & 1, c = e % W, Y = y0 + yr;
             yb[e] = (Y >= 0 && Y < n1) ? (m ? a.kw[1] : 1.0) * __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
         }
+    // band fragments (constant over the planes), per lane l and k step s4 (k = 4 s4 + l%4):
+    // B[k][n] = Mx(x0 + 8 nj + n, band c = k - n), n = l/4, for the column blocks nj = 0..3, then
+    // A[m][k] = My(y0 + 8 mi + m, band c = k - m), m = l/4, for the row blocks mi = 0, 1
+    for (int e = tid; e < 6 * G::KS * 32; e += K4_THREADS) {
+        const int l = e & 31, s4 = (e >> 5) % G::KS, blk = (e >> 5) / G::KS;
+        const int cb = 4 * s4 + (l & 3) - (l >> 2);
+        double v = 0.0;
+        if (cb >= 0 && cb <= 2 * P) {
+            if (blk < 4) v = XI ? a.mc[0][cb] : (x0 + 8 * blk + (l >> 2) >= 0 && x0 + 8 * blk + (l >> 2) < n0
+                                                     ? __ldg(a.mx + (long)(x0 + 8 * blk + (l >> 2)) * W + cb) : 0.0);
+            else v = YI ? a.mc[1][cb] : (y0 + 8 * (blk - 4) + (l >> 2) >= 0 && y0 + 8 * (blk - 4) + (l >> 2) < n1
+                                             ? __ldg(a.my + (long)(y0 + 8 * (blk - 4) + (l >> 2)) * W + cb) : 0.0);
+        }
+        k4_smem[sh + G::OFF_FR + e] = v;
+    }
+    // zero the stage-C fragment padding (never written by stage B)
+    for (int e = tid; e < 2 * K4_Y * (K4_YQP - NC); e += K4_THREADS) {
+        const int b = e / (K4_Y * (K4_YQP - NC)), q = e % (K4_Y * (K4_YQP - NC));
+        reinterpret_cast<double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ)[(q / (K4_YQP - NC)) * K4_YQP + NC + q % (K4_YQP - NC)] =
+            make_double2(0.0, 0.0);
+    }
+    if constexpr (G::HX1 > HY)
+        for (int e = tid; e < 2 * (G::HX1 - HY) * K4_XP; e += K4_THREADS) {
+            const int b = e / ((G::HX1 - HY) * K4_XP), q = e % ((G::HX1 - HY) * K4_XP);
+            k4_smem[sh + G::OFF_X1 + b * G::X1 + HY * K4_XP + q] = 0.0;
+        }
     const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;  // input planes z0 - P .. z1 + P - 1
     if (tid == 0) {
         for (int i = 0; i < K4_NPF; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb0 + 8u * i) : "memory");
@@ -723,7 +761,7 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
 
     // stage-A slot offsets (staging, P/D tiles) and previous P; stage-C rings (pending output planes)
     int so_[G::SA], po_[G::SA];
-    long go_[G::SA];
+    int go_[G::SA];
 #pragma unroll
     for (int m = 0; m < G::SA; ++m) {
         const int e = tid + K4_THREADS * m, hy = e / NC, hx = e - hy * NC;
@@ -732,7 +770,7 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
         const int X = x0 - P + hx, Y = y0 - P + hy;  // owned: inside the output tile and the grid
         const bool own = e < G::NA && hx >= P && hx < P + K4_X && hy >= P && hy < P + K4_Y && X >= 0 && X < n0 &&
                          Y >= 0 && Y < n1;
-        go_[m] = own ? (long)Y * sy + X : -1;
+        go_[m] = own ? Y * (int)sy + X : -1;
     }
     double pv[G::SA], A0[W], A1[W];
 #pragma unroll
@@ -740,20 +778,25 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
 #pragma unroll
     for (int c = 0; c < W; ++c) A0[c] = A1[c] = 0.0;
 
-    // stage-C constants: output column X = x0 + lane, rows y0 + 2w, y0 + 2w + 1
-    // (tiles start at ilo - 32 / ilo - 16 for the interior alignment: X, Y can be negative)
-    const int X = x0 + lane, yr0 = 2 * w;
-    const bool xin = X >= 0 && X < n0;
-    const bool own0 = xin && y0 + yr0 >= 0 && y0 + yr0 < n1, own1 = xin && y0 + yr0 + 1 >= 0 && y0 + yr0 + 1 < n1;
+    // stage-C constants: warp w owns the 8 x 8 output block (rows 8 mi.., columns 8 nj..), lane l the
+    // outputs (row y0 + 8 mi + l/4, columns x0 + 8 nj + 2 (l%4) + {0, 1}); tiles start at ilo - 32 /
+    // ilo - 16 (interior alignment): rows and columns can be negative
+    const int mi = w >> 2, nj = w & 3;
+    const int Yo = y0 + 8 * mi + (lane >> 2), X = x0 + 8 * nj + 2 * (lane & 3);
+    const bool yin = Yo >= 0 && Yo < n1;
+    const bool own0 = yin && X >= 0 && X < n0, own1 = yin && X + 1 >= 0 && X + 1 < n0;
     const bool has_src = a.bx != nullptr;
-    const double sxy0 = (has_src && own0) ? __ldg(a.bx + X) * __ldg(a.by + y0 + yr0) : 0.0;
-    const double sxy1 = (has_src && own1) ? __ldg(a.bx + X) * __ldg(a.by + y0 + yr0 + 1) : 0.0;
+    const double sxy0 = (has_src && own0) ? __ldg(a.bx + X) * __ldg(a.by + Yo) : 0.0;
+    const double sxy1 = (has_src && own1) ? __ldg(a.bx + X + 1) * __ldg(a.by + Yo) : 0.0;
+    const double *const frx = k4_smem + sh + G::OFF_FR + nj * G::KS * 32 + lane;
+    const double *const fry = k4_smem + sh + G::OFF_FR + (4 + mi) * G::KS * 32 + lane;
     double gsrc = a.g;
     if (has_src && a.dstep) {  // source time from the device step counter (CUDA graph replays)
         const double x = 3.141592653589793238462643383 * a.f0 * ((double)(*a.dstep + 1) * a.tau_g - a.t0);
         gsrc = a.amp * (a.wav ? (1.0 - 2.0 * x * x) * exp(-x * x) : 1.0);
     }
-    double *rq = a.r + (long)(y0 + yr0) * sy + X + (long)z0 * sz;
+    double *rq = a.r + (long)Yo * sy + X + (long)z0 * sz;
+    const bool pair = own0 && own1 && (reinterpret_cast<unsigned long long>(rq) & 15) == 0;  // sz keeps it
     // stage-B column item (threads [0, NCOL)) and row item (warps [CW, 8)) constants
     const int nc = tid % NC, g4 = tid / NC;
     const int rq4 = (lane & 3) + 4 * (lane >> 4), rsub = (lane >> 2) & 3;
@@ -825,9 +868,9 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
                             }
                         }
                     }
-                    double2 *o = reinterpret_cast<double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ) + (4 * g4) * NC + nc;
+                    double2 *o = reinterpret_cast<double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ) + (4 * g4) * K4_YQP + nc;
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) o[r * NC] = make_double2(ky[r], mq[r]);
+                    for (int r = 0; r < 4; ++r) o[r * K4_YQP] = make_double2(ky[r], mq[r]);
                 }
             } else {
                 // row items: a warp covers 4 rows x 8 column quads (16-byte window loads)
@@ -865,61 +908,28 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
                 }
             }
         }
-        // ---- C: plane c = kk0 + ic: G = My (Kx P) + Mx (Ky P), dT_{c-1} = Mx (My D) into the z ring
+        // ---- C: plane c = kk0 + ic: G = My (Kx P) + Mx (Ky P), dT_{c-1} = Mx (My D) into the z ring.
+        // DMMA m8n8k4: warp w owns the 8 x 8 block (rows 8 mi.., columns 8 nj..); lane l its outputs
+        // (row 8 mi + l/4, columns 8 nj + 2 (l%4) + {0, 1}).  Mx acts as the B operand (band, in
+        // registers) on the (Ky P, My D) rows, My as the A operand on the Kx P columns.
         const int ic = ii - 2;
         if (ic >= 0) {
             const int b = ic & 1, kc_ = kk0 + ic, kout = kc_ - P;
-            const double2 *Y0 = reinterpret_cast<const double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ) + yr0 * NC + lane;
-            const double2 *Y1 = Y0 + NC;
-            const double *Xc2 = k4_smem + sh + G::OFF_X1 + b * G::X1 + yr0 * K4_XP + lane;
-            double g0, g1, t0, t1;
-            if (XI) {
-                const double2 c0 = Y0[P], c1 = Y1[P];
-                g0 = a.mc[0][P] * c0.x;
-                t0 = a.mc[0][P] * c0.y;
-                g1 = a.mc[0][P] * c1.x;
-                t1 = a.mc[0][P] * c1.y;
+            const double2 *Yq = reinterpret_cast<const double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ) +
+                                (8 * mi + (lane >> 2)) * K4_YQP + 8 * nj + (lane & 3);
+            const double *Xq = k4_smem + sh + G::OFF_X1 + b * G::X1 + (8 * mi + (lane & 3)) * K4_XP + 8 * nj + (lane >> 2);
+            double gacc[2] = {0.0, 0.0}, hacc[2] = {0.0, 0.0}, tacc[2] = {0.0, 0.0};
 #pragma unroll
-                for (int d = 1; d <= P; ++d) {
-                    const double2 l0 = Y0[P - d], r0 = Y0[P + d], l1 = Y1[P - d], r1 = Y1[P + d];
-                    g0 = fma(a.mc[0][P + d], l0.x + r0.x, g0);
-                    t0 = fma(a.mc[0][P + d], l0.y + r0.y, t0);
-                    g1 = fma(a.mc[0][P + d], l1.x + r1.x, g1);
-                    t1 = fma(a.mc[0][P + d], l1.y + r1.y, t1);
-                }
-            } else {
-                g0 = t0 = g1 = t1 = 0.0;
-#pragma unroll
-                for (int c = 0; c < W; ++c) {
-                    const double m = xb[(c * 2) * K4_X + lane];
-                    const double2 q0 = Y0[c], q1 = Y1[c];
-                    g0 = fma(m, q0.x, g0);
-                    t0 = fma(m, q0.y, t0);
-                    g1 = fma(m, q1.x, g1);
-                    t1 = fma(m, q1.y, t1);
-                }
+            for (int s4 = 0; s4 < G::KS; ++s4) {
+                const double2 av = Yq[4 * s4];
+                const double bv = Xq[4 * s4 * K4_XP], bmx = frx[32 * s4], amy = fry[32 * s4];
+                k4_dmma(gacc, av.x, bmx);
+                k4_dmma(tacc, av.y, bmx);
+                k4_dmma(hacc, amy, bv);
             }
-            double xw[2 * P + 2];  // Kx P rows yr0 .. yr0 + 2P + 1 at column lane
-#pragma unroll
-            for (int c = 0; c < 2 * P + 2; ++c) xw[c] = Xc2[c * K4_XP];
-            if (YI) {
-                g0 = fma(a.mc[1][P], xw[P], g0);
-                g1 = fma(a.mc[1][P], xw[P + 1], g1);
-#pragma unroll
-                for (int d = 1; d <= P; ++d) {
-                    g0 = fma(a.mc[1][P + d], xw[P - d] + xw[P + d], g0);
-                    g1 = fma(a.mc[1][P + d], xw[P + 1 - d] + xw[P + 1 + d], g1);
-                }
-            } else {
-                const double *r0 = yb + (yr0 * 2) * W, *r1 = yb + ((yr0 + 1) * 2) * W;
-#pragma unroll
-                for (int c = 0; c < W; ++c) {
-                    g0 = fma(r0[c], xw[c], g0);
-                    g1 = fma(r1[c], xw[c + 1], g1);
-                }
-            }
+            const double g0 = gacc[0] + hacc[0], g1 = gacc[1] + hacc[1], t0 = tacc[0], t1 = tacc[1];
             const bool zint = kc_ + a.zoff - P >= a.ilo[2] && kc_ + a.zoff + P <= a.ihi[2];
-            double o0 = 0.0, o1 = 0.0;  // t0, t1: dT_{c-1} = Mx My D of rows yr0, yr0 + 1
+            double o0 = 0.0, o1 = 0.0;  // t0, t1: dT_{c-1} = Mx My D of the lane's two outputs
             switch (ic % W) {
 #define ADS_K4C(U)                                                                      \
     case U:                                                                             \
@@ -931,8 +941,10 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
             }
             if (kout >= z0) {  // output plane kout = c - P: r = g src + sign K P
                 const double gz = has_src ? gsrc * __ldg(a.bz + kout + a.zoff) : 0.0;
-                if (own0) rq[0] = fma(a.sign, o0, gz * sxy0);
-                if (own1) rq[sy] = fma(a.sign, o1, gz * sxy1);
+                const double r0 = fma(a.sign, o0, gz * sxy0), r1 = fma(a.sign, o1, gz * sxy1);
+                if (pair) *reinterpret_cast<double2 *>(rq) = make_double2(r0, r1);
+                else if (own0) rq[0] = r0;
+                else if (own1) rq[1] = r1;
                 rq += sz;
             }
         }
