@@ -1680,15 +1680,21 @@ int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const i
             std::memcpy(f + 2 + n0, sy + (size_t)t * n1, sizeof(double) * n1);
             std::memcpy(f + 2 + n0 + n1, sz + (size_t)t * n2, sizeof(double) * n2);
         }
-        double *d = nullptr;
-        if ((rc = dalloc(m, (void **)&d, sizeof(double) * packed.size()))) return rc;
+        // the packed factors go to the work field Wk (free until the start procedure below writes
+        // it; stream order), or to a scratch allocation when they do not fit.  A pageable-source
+        // copy has consumed the host vector when cudaMemcpyAsync returns.
+        const bool fits = packed.size() <= (size_t)m->Nalloc;
+        double *d = fits ? m->Wk : nullptr;
+        if (!fits && (rc = dalloc(m, (void **)&d, sizeof(double) * packed.size()))) return rc;
         CUDA_TRY(m, cudaMemcpyAsync(d, packed.data(), sizeof(double) * packed.size(), cudaMemcpyHostToDevice, m->stream));
         const bool dir = m->bc == ADS_BC_DIRICHLET0;
         launch_set_separable(m->U, m->Nalloc, m->ncomp, nterms, d, n0, n1, n2, m->geo, m->zbeg, dir ? 1 : 0,
                              dir ? 1 : 0, dir ? zmask(m) : 0, m->stream);
         if ((rc = check_launch(m, "separable"))) return rc;
-        CUDA_TRY(m, cudaStreamSynchronize(m->stream));  // the packed factors live in a host vector
-        dfree(m, d);
+        if (!fits) {
+            CUDA_TRY(m, cudaStreamSynchronize(m->stream));
+            dfree(m, d);
+        }
     }
     return h->ncomp == 3 ? el_init(h) : init_state(h);
 }

@@ -1388,26 +1388,45 @@ __global__ void axpby_kernel(long N, double alpha, const double *__restrict__ x,
 // u_c = sum over the terms t of component c of amp_t sx_t[i] sy_t[j] sz_t[k + zoff], zero on the
 // Dirichlet faces (mx, my: x / y faces; ngz > 0: the global z faces 0 and ngz - 1): one write pass
 // for all terms and components.  f: per term [amp, comp, sx (n0), sy (n1), sz (nzf)]
-__global__ void set_separable_kernel(double *u, long cstride, int nterms, const double *__restrict__ f, int n0f, int n1f,
-                                     int nzf, Geom g, int zoff, int mx, int my, int ngz, int ncomp) {
-    const long N = (long)g.n0 * g.n1 * g.n2;
+// sum of separable terms amp_m fx_m(i) fy_m(j) fz_m(k) into component c_m (zero on the masked
+// faces): block per (j, k) line, the term weights amp fy fz of the line staged in shared memory in
+// chunks of 256 terms, threads along x
+constexpr int SEP_THREADS = 128, SEP_CHUNK = 256;
+__global__ void __launch_bounds__(SEP_THREADS) set_separable_kernel(double *u, long cstride, int nterms,
+                                                                    const double *__restrict__ f, int n0f, int n1f,
+                                                                    int nzf, Geom g, int zoff, int mx, int my, int ngz,
+                                                                    int ncomp) {
+    __shared__ double wt[SEP_CHUNK];
+    __shared__ int cm[SEP_CHUNK];
+    const int j = blockIdx.y, k = blockIdx.z, kg = k + zoff;
     const long tl = 2 + n0f + n1f + nzf;
-    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x) {
-        const int i = (int)(q % g.n0);
-        const long t = q / g.n0;
-        const int j = (int)(t % g.n1), k = (int)(t / g.n1);
-        const int kg = k + zoff;
-        const bool bnd = (mx && (i == 0 || i == g.n0 - 1)) || (my && (j == 0 || j == g.n1 - 1)) ||
-                         (ngz > 0 && (kg == 0 || kg == ngz - 1));
+    const bool line0 = (my && (j == 0 || j == g.n1 - 1)) || (ngz > 0 && (kg == 0 || kg == ngz - 1));
+    for (int i0 = blockIdx.x * SEP_THREADS; i0 < g.n0; i0 += gridDim.x * SEP_THREADS) {
+        const int i = i0 + threadIdx.x;
         double acc[3] = {0.0, 0.0, 0.0};
-        if (!bnd)
-            for (int m = 0; m < nterms; ++m) {
-                const double *ft = f + m * tl;
-                const int c = (int)ft[1];
-                acc[c] = fma(ft[0] * __ldg(ft + 2 + i) * __ldg(ft + 2 + n0f + j), __ldg(ft + 2 + n0f + n1f + kg), acc[c]);
+        for (int m0 = 0; m0 < nterms && !line0; m0 += SEP_CHUNK) {
+            const int nm = min(SEP_CHUNK, nterms - m0);
+            __syncthreads();
+            for (int t = threadIdx.x; t < nm; t += SEP_THREADS) {
+                const double *ft = f + (m0 + t) * tl;
+                wt[t] = ft[0] * ft[2 + n0f + j] * ft[2 + n0f + n1f + kg];
+                cm[t] = (int)ft[1];
             }
-        const long o = (long)k * g.sz + (long)j * g.sy + i;
-        for (int c = 0; c < ncomp; ++c) u[c * cstride + o] = acc[c];
+            __syncthreads();
+            if (i < g.n0)
+                for (int t = 0; t < nm; ++t) {
+                    const double fx = __ldg(f + (m0 + t) * tl + 2 + i);
+                    const int c = cm[t];
+                    if (c == 0) acc[0] = fma(wt[t], fx, acc[0]);
+                    else if (c == 1) acc[1] = fma(wt[t], fx, acc[1]);
+                    else acc[2] = fma(wt[t], fx, acc[2]);
+                }
+        }
+        if (i < g.n0) {
+            const bool z0 = mx && (i == 0 || i == g.n0 - 1);
+            const long o = (long)k * g.sz + (long)j * g.sy + i;
+            for (int c = 0; c < ncomp; ++c) u[c * cstride + o] = z0 ? 0.0 : acc[c];
+        }
     }
 }
 
@@ -1690,8 +1709,8 @@ int launch_axpby(long N, double alpha, const double *x, double beta, double *y, 
 
 void launch_set_separable(double *u, long cstride, int ncomp, int nterms, const double *f, int n0f, int n1f, int nzf,
                           const Geom &g, int zoff, int mx, int my, int ngz, cudaStream_t s) {
-    set_separable_kernel<<<grid_for((long)g.n0 * g.n1 * g.n2), 256, 0, s>>>(u, cstride, nterms, f, n0f, n1f, nzf, g, zoff,
-                                                                            mx, my, ngz, ncomp);
+    const dim3 grid((g.n0 + SEP_THREADS - 1) / SEP_THREADS, g.n1, g.n2);
+    set_separable_kernel<<<grid, SEP_THREADS, 0, s>>>(u, cstride, nterms, f, n0f, n1f, nzf, g, zoff, mx, my, ngz, ncomp);
 }
 
 void launch_drift(const double *U, const double *V, double tau, double *P, long N, cudaStream_t s) {

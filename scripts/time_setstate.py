@@ -21,5 +21,14 @@ for _ in range(3):
     s.set_state_separable([t.amp for t in terms], sx, sy, sz, [t.comp for t in terms])
     torch.cuda.synchronize()
     t2 = time.perf_counter()
+    # the start procedure alone: set_state from a device copy of the field (one D2D copy + start)
     print(f"{wl.name}: {len(terms)} terms: 1D projections {1e3 * (t1 - t0):.2f} ms, set_state_separable "
           f"(one pass + half-kick start) {1e3 * (t2 - t1):.2f} ms", flush=True)
+ud = torch.zeros(tuple(reversed(s.n)), dtype=torch.float64, device="cuda")
+for _ in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s.set_state(ud)
+    torch.cuda.synchronize()
+    print(f"{wl.name}: set_state(device field) (D2D copy + half-kick start) {1e3 * (time.perf_counter() - t0):.2f} ms",
+          flush=True)
