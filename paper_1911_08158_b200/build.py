@@ -41,13 +41,17 @@ def build(force: bool = False, verbose: bool = False, extra=(), out=None) -> str
         return LIB
     objs = []
     nvcc = _nvcc()
-    for src in SOURCES:
-        obj = os.path.join(CSRC, src + ".o")
+    procs = []
+    for src in SOURCES:  # the translation units compile in parallel
+        obj = os.path.join(CSRC, src + (("." + os.path.basename(out)) if out else "") + ".o")
         cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
+        procs.append((subprocess.Popen(cmd), cmd))
         objs.append(obj)
+    for pr, cmd in procs:
+        if pr.wait() != 0:
+            raise subprocess.CalledProcessError(pr.returncode, cmd)
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-lcudart", "-lnccl"]
     subprocess.check_call(cmd)
     for o in objs:

@@ -26,6 +26,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -541,36 +542,40 @@ __host__ __device__ inline int kop_origin(int ilo, int ihi, int T) { return ilo 
 //
 // CTA = 256 threads on a K4_X x K4_Y = 32 x 16 output tile, marching along z over [z0, z1).
 // Per input plane c (TMA box of U and V over the haloed tile, K4_NPF - 1 planes ahead):
-//   A. every position of the (32 + 2p) x (16 + 2p) haloed tile: P = U + tau V into the P tile and
-//      the plane difference D = P_c - P_{c-1} (previous P kept in a register) into the D tile;
-//   B. column items (column, 4 rows): Ky P and My D, and the owned P to HBM; row items (row,
-//      4 columns): Kx P;
-//   C. lane = x, 2 rows per thread: G_c = My (Kx P) + Mx (Ky P) and dT_{c-1} = Mx (My D) scattered
-//      (weights Mz, wz) into a register ring of 2p + 1 pending output planes; output plane c - p
-//      is complete: r = g src + sign ring.
-// The three stages run skewed (A of plane ii, B of ii - 1, C of ii - 2) on double-buffered tiles
-// with one barrier per plane.  Interior tiles/planes use the Toeplitz rows (kernel parameters)
-// in pair form; boundary tiles read staged rows, boundary planes read global rows.
+//   A. P = U + tau V over the staged box, a column pair per thread step (16-byte shared loads and
+//      stores), into a ring of three P tiles whose columns are the staging columns; zero on planes
+//      outside memory and on zero-Dirichlet z faces (their Mz / Mx / My columns are zero, and they
+//      count as zero in the plane differences); the owned P to HBM;
+//   B. column items (column, 4 rows): Ky P_c and My D with D = P_c - P_{c-1} formed from two P
+//      tiles of the ring; row items (row, 4 columns): Kx P_c;
+//   C. lane = x, 2 rows per thread: G_c = My (Kx P) + Mx (Ky P) and dT_{c-1} = Mx (My D) on the
+//      FP64 tensor cores (band fragments in registers), scattered with (Mz, wz) into a register ring
+//      of 2p + 1 pending output planes; output plane c - p is complete: r = g src + sign ring.
+// The three stages run skewed (A of plane ii, B of ii - 1, C of ii - 2) with one barrier per
+// plane.  Interior tiles/planes use the Toeplitz rows (kernel parameters) in pair form; boundary
+// tiles read staged rows, boundary planes read global rows.
 // HBM traffic: U, V read once (halos from L2), P and r written once: 32 B/DOF.
 // ------------------------------------------------------------------------------------------
-constexpr int K4_X = 32, K4_Y = 16, K4_THREADS = 256, K4_NPF = 2, K4_XP = 36, K4_YQP = 44;
+constexpr int K4_X = 32, K4_Y = 16, K4_THREADS = 256, K4_NPF = 3, K4_XP = 36, K4_YQP = 44;
 template <int P>
 struct K4Geo {
     static constexpr int W = 2 * P + 1;
     static constexpr int PA = (P + 1) & ~1;             // even x halo of the TMA box
+    static constexpr int SFT = PA - P;                  // staged column of haloed column 0 (0 or 1)
     static constexpr int HXE = K4_X + 2 * PA;           // staged columns
     static constexpr int HY = K4_Y + 2 * P;             // rows of the haloed tile
     static constexpr int NC = K4_X + 2 * P;             // columns of the haloed tile
-    // P tile pitch: even with pitch/2 odd, so the row items' 16-byte loads (a quarter-warp = 2 rows
-    // x 4 column quads) hit 8 distinct bank groups
-    static constexpr int PP = ((NC / 2) % 2 == 1) ? NC : NC + 2;
-    static constexpr int NA = NC * HY;                  // stage-A positions
+    // P tile pitch: the staging row plus 2, so pitch/2 is odd (HXE/2 = 16 + PA is even) and the row
+    // items' 16-byte loads (a quarter-warp = 2 rows x 4 column quads) hit 8 distinct bank groups
+    static constexpr int PP = HXE + 2;
+    static constexpr int NPR = HXE / 2;                 // column pairs per staged row
+    static constexpr int NA = NPR * HY;                 // stage-A pairs
     static constexpr int SA = (NA + K4_THREADS - 1) / K4_THREADS;
     static constexpr int NCOL = NC * (K4_Y / 4);        // column items (4 output rows each)
     static constexpr int CW = (NCOL + 31) / 32;         // warps running column items
     static constexpr int RW = K4_THREADS / 32 - CW;     // warps running row items
     static constexpr int RG = (HY + 3) / 4;             // row-item groups of 4 rows x 8 column quads
-    static constexpr int RWIN = 4 + 2 * P;              // row-item window (even)
+    static constexpr int RWIN = 4 + 2 * P + 2 * SFT;    // row-item window from the aligned staged column
     static_assert(RW >= 1, "row-item warps");
     static constexpr int al16(int v) { return (v + 15) & ~15; }
     static constexpr int STG = al16(HXE * HY);          // one staged field plane (128-byte multiple)
@@ -581,16 +586,18 @@ struct K4Geo {
     static_assert(24 + 4 * KS <= K4_YQP && HX1 >= HY, "stage-C fragment windows");
     static constexpr int PT = al16(HY * PP), YQ = al16(K4_Y * K4_YQP * 2);
     static constexpr int X1 = al16(HX1 * K4_XP), XB = al16(K4_X * 2 * W), YB = al16(K4_Y * 2 * W);
-    static constexpr int FR = al16(6 * KS * 32);  // band fragments: Mx per n block (4), My per m block (2)
-    static constexpr int OFF_PT = K4_NPF * 2 * STG, OFF_DT = OFF_PT + 2 * PT, OFF_YQ = OFF_DT + 2 * PT;
+    static constexpr int OFF_PT = K4_NPF * 2 * STG, OFF_YQ = OFF_PT + 3 * PT;
     static constexpr int OFF_X1 = OFF_YQ + 2 * YQ, OFF_XB = OFF_X1 + 2 * X1, OFF_YB = OFF_XB + XB;
-    static constexpr int OFF_FR = OFF_YB + YB, OFF_MB = OFF_FR + FR;
+    static constexpr int OFF_MB = OFF_YB + YB;
     static constexpr int SMEM = OFF_MB + 16 + 16;       // mbarriers + 128-byte alignment slack
 };
 
 extern __shared__ __align__(128) double k4_smem[];
 
 __device__ __forceinline__ void k4_dmma(double (&d)[2], double a, double b) {
+#ifdef ADS_ABL_NODMMA  // experiment builds only (scripts/ablate_kop.sh)
+    d[0] += a; d[1] += b; return;
+#endif
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                  : "+d"(d[0]), "+d"(d[1])
                  : "d"(a), "d"(b));
@@ -603,26 +610,37 @@ __device__ __forceinline__ void k4_wait(unsigned mb, unsigned parity) {
         " @!P1 bra K4W_%=;\n}\n" ::"r"(mb), "r"(parity) : "memory");
 }
 
-// stage A of input plane kk: P tile, D = P - P_prev tile, owned P to HBM (so_[m] / po_[m] / go_[m]:
-// staging / tile / global offsets of slot m, -1: none or not owned; pv[m]: the previous plane's P).
-// LIVE: the plane exists in memory; ZDIR: a zero-Dirichlet z face (outside the restricted space:
-// it counts as zero in the plane differences)
-template <int P, bool LIVE, bool ZDIR, bool PONLY = false>
-__device__ __forceinline__ void k4_stage_a(const KopArgs &a, double (&pv)[K4Geo<P>::SA], const int (&so_)[K4Geo<P>::SA],
-                                           const int (&po_)[K4Geo<P>::SA], const int (&go_)[K4Geo<P>::SA], int sbase,
-                                           int pbase, int dbase, double *pout) {
+// stage A of one input plane: column pairs m of this thread (so_: staging offset, -1 none; po_: P
+// tile offset; go_: global offset of the pair's first column; om_: bit 0/1 owned columns, bit 2 the
+// pair store is 16-byte aligned).  KIND 0: no plane in memory (P = 0); 1: slab halo plane (P staged
+// from Ph in the U half); 2: zero-Dirichlet z face (P = U + tau V to HBM, zero in the tile);
+// 3: P = U + tau V
+template <int P, int KIND>
+__device__ __forceinline__ void k4_stage_a(double tau, const int (&so_)[K4Geo<P>::SA], const int (&po_)[K4Geo<P>::SA],
+                                           const int (&go_)[K4Geo<P>::SA], const int (&om_)[K4Geo<P>::SA], int sbase,
+                                           int pbase, double *pout) {
     using G = K4Geo<P>;
 #pragma unroll
     for (int m = 0; m < G::SA; ++m) {
-        if (G::NA % K4_THREADS != 0 && m == G::SA - 1 && po_[m] < 0) break;
-        // PONLY: a slab halo plane staged from Ph (the neighbour's P itself)
-        const double p = !LIVE ? 0.0 : PONLY ? k4_smem[sbase + so_[m]]
-                                            : fma(a.tau, k4_smem[sbase + G::STG + so_[m]], k4_smem[sbase + so_[m]]);
-        const double pz = ZDIR ? 0.0 : p;
-        k4_smem[pbase + po_[m]] = p;
-        k4_smem[dbase + po_[m]] = pz - pv[m];
-        pv[m] = pz;
-        if (pout && go_[m] >= 0) pout[go_[m]] = p;
+        if (G::NA % K4_THREADS != 0 && m == G::SA - 1 && so_[m] < 0) break;
+        double2 p = make_double2(0.0, 0.0);
+        if (KIND != 0) {
+            const double2 u = *reinterpret_cast<const double2 *>(k4_smem + sbase + so_[m]);
+            if (KIND == 1) p = u;
+            else {
+                const double2 v = *reinterpret_cast<const double2 *>(k4_smem + sbase + G::STG + so_[m]);
+                p = make_double2(fma(tau, v.x, u.x), fma(tau, v.y, u.y));
+            }
+        }
+        *reinterpret_cast<double2 *>(k4_smem + pbase + po_[m]) = KIND == 2 ? make_double2(0.0, 0.0) : p;
+        if (KIND != 0 && pout) {
+            const int om = om_[m];
+            if (om == 7) *reinterpret_cast<double2 *>(pout + go_[m]) = p;
+            else {
+                if (om & 1) pout[go_[m]] = p.x;
+                if (om & 2) pout[go_[m] + 1] = p.y;
+            }
+        }
     }
 }
 
@@ -670,7 +688,7 @@ template <int P, bool XI, bool YI>
 __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *tmu, const CUtensorMap *tmv,
                                           const CUtensorMap *tmp, int sh, int x0, int y0, int z0, int z1) {
     using G = K4Geo<P>;
-    constexpr int W = G::W, NC = G::NC, HY = G::HY, PP = G::PP;
+    constexpr int W = G::W, NC = G::NC, HY = G::HY, PP = G::PP, SFT = G::SFT;
     // shared memory: k4_smem[sh + offset]; sh aligns the TMA staging to 128 bytes
     double *const xb = k4_smem + sh + G::OFF_XB;  // [W][2][K4_X]: (Mx, kw0 Kx) rows of x0 + xr
     double *const yb = k4_smem + sh + G::OFF_YB;  // [K4_Y][2][W]: (My, kw1 Ky) rows of y0 + yr
@@ -689,22 +707,7 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
             const int yr = e / (2 * W), m = (e / W) & 1, c = e % W, Y = y0 + yr;
             yb[e] = (Y >= 0 && Y < n1) ? (m ? a.kw[1] : 1.0) * __ldg((m ? a.ky : a.my) + (long)Y * W + c) : 0.0;
         }
-    // band fragments (constant over the planes), per lane l and k step s4 (k = 4 s4 + l%4):
-    // B[k][n] = Mx(x0 + 8 nj + n, band c = k - n), n = l/4, for the column blocks nj = 0..3, then
-    // A[m][k] = My(y0 + 8 mi + m, band c = k - m), m = l/4, for the row blocks mi = 0, 1
-    for (int e = tid; e < 6 * G::KS * 32; e += K4_THREADS) {
-        const int l = e & 31, s4 = (e >> 5) % G::KS, blk = (e >> 5) / G::KS;
-        const int cb = 4 * s4 + (l & 3) - (l >> 2);
-        double v = 0.0;
-        if (cb >= 0 && cb <= 2 * P) {
-            if (blk < 4) v = XI ? a.mc[0][cb] : (x0 + 8 * blk + (l >> 2) >= 0 && x0 + 8 * blk + (l >> 2) < n0
-                                                     ? __ldg(a.mx + (long)(x0 + 8 * blk + (l >> 2)) * W + cb) : 0.0);
-            else v = YI ? a.mc[1][cb] : (y0 + 8 * (blk - 4) + (l >> 2) >= 0 && y0 + 8 * (blk - 4) + (l >> 2) < n1
-                                             ? __ldg(a.my + (long)(y0 + 8 * (blk - 4) + (l >> 2)) * W + cb) : 0.0);
-        }
-        k4_smem[sh + G::OFF_FR + e] = v;
-    }
-    // zero the stage-C fragment padding (never written by stage B)
+    // zero the stage-C fragment padding (never written by stage B) and the P tile of plane -1
     for (int e = tid; e < 2 * K4_Y * (K4_YQP - NC); e += K4_THREADS) {
         const int b = e / (K4_Y * (K4_YQP - NC)), q = e % (K4_Y * (K4_YQP - NC));
         reinterpret_cast<double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ)[(q / (K4_YQP - NC)) * K4_YQP + NC + q % (K4_YQP - NC)] =
@@ -715,6 +718,7 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
             const int b = e / ((G::HX1 - HY) * K4_XP), q = e % ((G::HX1 - HY) * K4_XP);
             k4_smem[sh + G::OFF_X1 + b * G::X1 + HY * K4_XP + q] = 0.0;
         }
+    for (int e = tid; e < G::PT; e += K4_THREADS) k4_smem[sh + G::OFF_PT + 2 * G::PT + e] = 0.0;
     const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;  // input planes z0 - P .. z1 + P - 1
     if (tid == 0) {
         for (int i = 0; i < K4_NPF; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb0 + 8u * i) : "memory");
@@ -759,22 +763,21 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
     if (tid == 0)
         for (int i = 0; i < K4_NPF - 1; ++i) issue(i);
 
-    // stage-A slot offsets (staging, P/D tiles) and previous P; stage-C rings (pending output planes)
-    int so_[G::SA], po_[G::SA];
-    int go_[G::SA];
+    // stage-A pairs of this thread: staging / P tile / global offsets and ownership
+    int so_[G::SA], po_[G::SA], go_[G::SA], om_[G::SA];
 #pragma unroll
     for (int m = 0; m < G::SA; ++m) {
-        const int e = tid + K4_THREADS * m, hy = e / NC, hx = e - hy * NC;
-        so_[m] = e < G::NA ? hy * G::HXE + hx + (G::PA - P) : -1;
-        po_[m] = e < G::NA ? hy * PP + hx : -1;
-        const int X = x0 - P + hx, Y = y0 - P + hy;  // owned: inside the output tile and the grid
-        const bool own = e < G::NA && hx >= P && hx < P + K4_X && hy >= P && hy < P + K4_Y && X >= 0 && X < n0 &&
-                         Y >= 0 && Y < n1;
-        go_[m] = own ? Y * (int)sy + X : -1;
+        const int e = tid + K4_THREADS * m, hy = e / G::NPR, cp = e - hy * G::NPR;
+        const int X = x0 - G::PA + 2 * cp, Y = y0 - P + hy;  // global column of the pair's first element
+        so_[m] = e < G::NA ? hy * G::HXE + 2 * cp : -1;
+        po_[m] = e < G::NA ? hy * PP + 2 * cp : 0;
+        const bool yo = e < G::NA && hy >= P && hy < P + K4_Y && Y >= 0 && Y < n1;
+        const bool o0 = yo && X >= x0 && X < x0 + K4_X && X >= 0 && X < n0;
+        const bool o1 = yo && X + 1 >= x0 && X + 1 < x0 + K4_X && X + 1 >= 0 && X + 1 < n0;
+        go_[m] = Y * (int)sy + X;
+        om_[m] = (o0 ? 1 : 0) | (o1 ? 2 : 0) | ((X & 1) == 0 ? 4 : 0);
     }
-    double pv[G::SA], A0[W], A1[W];
-#pragma unroll
-    for (int m = 0; m < G::SA; ++m) pv[m] = 0.0;
+    double A0[W], A1[W];
 #pragma unroll
     for (int c = 0; c < W; ++c) A0[c] = A1[c] = 0.0;
 
@@ -788,8 +791,21 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
     const bool has_src = a.bx != nullptr;
     const double sxy0 = (has_src && own0) ? __ldg(a.bx + X) * __ldg(a.by + Yo) : 0.0;
     const double sxy1 = (has_src && own1) ? __ldg(a.bx + X + 1) * __ldg(a.by + Yo) : 0.0;
-    const double *const frx = k4_smem + sh + G::OFF_FR + nj * G::KS * 32 + lane;
-    const double *const fry = k4_smem + sh + G::OFF_FR + (4 + mi) * G::KS * 32 + lane;
+    // band fragments (constant over the planes), per k step s4 (k = 4 s4 + l%4):
+    // B[k][n] = Mx(x0 + 8 nj + n, band c = k - n), n = l/4;  A[m][k] = My(y0 + 8 mi + m, band c = k - m)
+    double frx[G::KS], fry[G::KS];
+#pragma unroll
+    for (int s4 = 0; s4 < G::KS; ++s4) {
+        const int cb = 4 * s4 + (lane & 3) - (lane >> 2);
+        const int xr = x0 + 8 * nj + (lane >> 2), yr = y0 + 8 * mi + (lane >> 2);
+        double vx = 0.0, vy = 0.0;
+        if (cb >= 0 && cb <= 2 * P) {
+            vx = XI ? a.mc[0][cb] : (xr >= 0 && xr < n0 ? __ldg(a.mx + (long)xr * W + cb) : 0.0);
+            vy = YI ? a.mc[1][cb] : (yr >= 0 && yr < n1 ? __ldg(a.my + (long)yr * W + cb) : 0.0);
+        }
+        frx[s4] = vx;
+        fry[s4] = vy;
+    }
     double gsrc = a.g;
     if (has_src && a.dstep) {  // source time from the device step counter (CUDA graph replays)
         const double x = 3.141592653589793238462643383 * a.f0 * ((double)(*a.dstep + 1) * a.tau_g - a.t0);
@@ -801,71 +817,108 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
     const int nc = tid % NC, g4 = tid / NC;
     const int rq4 = (lane & 3) + 4 * (lane >> 4), rsub = (lane >> 2) & 3;
 
-    for (int ii = 0; ii < npl + 2; ++ii) {
-        if (ii < npl && w == 0) k4_wait(mb0 + 8u * (ii % K4_NPF), (unsigned)((ii / K4_NPF) & 1));
-        __syncthreads();  // plane ii landed; A(ii-1), B(ii-2), C(ii-3) done: buffers and slot free
+    // one plane step; ST: a steady-state plane (every stage active, a plain interior input plane,
+    // Toeplitz z rows, an owned output plane), which skips the per-plane case analysis
+    auto plane = [&](const int ii, auto st_tag) {
+        constexpr bool ST = decltype(st_tag)::value;
+#ifndef ADS_ABL_NOSYNC
+        __syncthreads();  // C(ii-3), B(ii-2), A(ii-1) done: tiles, staging slot (ii-1) % K4_NPF free
+#endif
         if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             issue(ii + K4_NPF - 1);
         }
-        // ---- A: input plane kk = kk0 + ii
-        if (ii < npl) {
-            const int kk = kk0 + ii;
-            const int b = ii & 1;
-            const int sb = sh + (ii % K4_NPF) * 2 * G::STG, pb = sh + G::OFF_PT + b * G::PT;
-            const int db = sh + G::OFF_DT + b * G::PT;
-            double *const po = (a.Pout && kk >= z0 && kk < z1) ? a.Pout + (long)kk * sz : nullptr;
-            if (!(kk >= a.zv0 && kk < a.zv1)) k4_stage_a<P, false, false>(a, pv, so_, po_, go_, sb, pb, db, po);
-            else if (a.Ph && (kk < 0 || kk >= a.geo.n2))
-                k4_stage_a<P, true, false, true>(a, pv, so_, po_, go_, sb, pb, db, po);
-            else if (kk + a.zoff == a.zd0 || kk + a.zoff == a.zd1)
-                k4_stage_a<P, true, true>(a, pv, so_, po_, go_, sb, pb, db, po);
-            else k4_stage_a<P, true, false>(a, pv, so_, po_, go_, sb, pb, db, po);
+        // program order C, B, A: no stage reads what another writes in this interval, and C's
+        // shared loads, then B's, go first (the compiler cannot hoist a shared load above a
+        // shared store it cannot disambiguate); only A waits for the TMA of plane ii
+        // ---- C: plane c = kk0 + ic: G = My (Kx P) + Mx (Ky P), dT_{c-1} = Mx (My D) into the z ring.
+        // DMMA m8n8k4: warp w owns the 8 x 8 block (rows 8 mi.., columns 8 nj..); lane l its outputs
+        // (row 8 mi + l/4, columns 8 nj + 2 (l%4) + {0, 1}).  Mx acts as the B operand (band, in
+        // registers) on the (Ky P, My D) rows, My as the A operand on the Kx P columns.
+        const int ic = ii - 2;
+        if (ST || ic >= 0) {
+            const int b = ic & 1, kc_ = kk0 + ic, kout = kc_ - P;
+            const double2 *Yq = reinterpret_cast<const double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ) +
+                                (8 * mi + (lane >> 2)) * K4_YQP + 8 * nj + (lane & 3);
+            const double *Xq = k4_smem + sh + G::OFF_X1 + b * G::X1 + (8 * mi + (lane & 3)) * K4_XP + 8 * nj + (lane >> 2);
+            // two accumulators per product (even / odd k steps): dependent DMMA chains of KS / 2
+            double gacc[2][2] = {}, hacc[2][2] = {}, tacc[2][2] = {};
+#pragma unroll
+            for (int s4 = 0; s4 < G::KS; ++s4) {
+                const double2 av = Yq[4 * s4];
+                const double bv = Xq[4 * s4 * K4_XP];
+                k4_dmma(gacc[s4 & 1], av.x, frx[s4]);
+                k4_dmma(tacc[s4 & 1], av.y, frx[s4]);
+                k4_dmma(hacc[s4 & 1], fry[s4], bv);
+            }
+            const double g0 = (gacc[0][0] + gacc[1][0]) + (hacc[0][0] + hacc[1][0]);
+            const double g1 = (gacc[0][1] + gacc[1][1]) + (hacc[0][1] + hacc[1][1]);
+            const double t0 = tacc[0][0] + tacc[1][0], t1 = tacc[0][1] + tacc[1][1];
+            const bool zint = ST || (kc_ + a.zoff - P >= a.ilo[2] && kc_ + a.zoff + P <= a.ihi[2]);
+            double o0 = 0.0, o1 = 0.0;  // t0, t1: dT_{c-1} = Mx My D of the lane's two outputs
+#ifdef ADS_ABL_NOZ
+            o0 = g0 + t0; o1 = g1 + t1;
+            if (false)
+#endif
+            switch (ic % W) {
+#define ADS_K4C(U)                                                                      \
+    case U:                                                                             \
+        if constexpr (U < W) k4_zscatter<P, U>(a, A0, A1, g0, g1, t0, t1, kc_, zint, o0, o1); \
+        break;
+                ADS_K4C(0) ADS_K4C(1) ADS_K4C(2) ADS_K4C(3) ADS_K4C(4) ADS_K4C(5)
+                ADS_K4C(6) ADS_K4C(7) ADS_K4C(8) ADS_K4C(9) ADS_K4C(10)
+#undef ADS_K4C
+            }
+            if (ST || kout >= z0) {  // output plane kout = c - P: r = g src + sign K P
+                const double gz = has_src ? gsrc * __ldg(a.bz + kout + a.zoff) : 0.0;
+                const double r0 = fma(a.sign, o0, gz * sxy0), r1 = fma(a.sign, o1, gz * sxy1);
+                if (pair) *reinterpret_cast<double2 *>(rq) = make_double2(r0, r1);
+                else if (own0) rq[0] = r0;
+                else if (own1) rq[1] = r1;
+                rq += sz;
+            }
         }
-        // ---- B: plane c = kk0 + ib (Ky P, Kx P, owned P) and D = P_c - P_{c-1} (My D)
+        // ---- B: plane c = kk0 + ib (Ky P, Kx P) and D = P_c - P_{c-1} (My D)
         const int ib = ii - 1;
-        if (ib >= 0 && ib < npl) {
+        if (ST || (ib >= 0 && ib < npl)) {
             const int b = ib & 1;
-            const double *pt = k4_smem + sh + G::OFF_PT + b * G::PT;
-            const double *dt = k4_smem + sh + G::OFF_DT + b * G::PT;
+            const double *pt = k4_smem + sh + G::OFF_PT + (ib % 3) * G::PT;
             if (w < G::CW) {
                 if (tid < G::NCOL) {
-                    double pw[4 + 2 * P];
+                    const int off = (4 * g4) * PP + nc + SFT;
+                    double pw[4 + 2 * P], dw[4 + 2 * P];
 #pragma unroll
-                    for (int r = 0; r < 4 + 2 * P; ++r) pw[r] = pt[(4 * g4 + r) * PP + nc];
-                    double ky[4], mq[4] = {0.0, 0.0, 0.0, 0.0};
+                    for (int r = 0; r < 4 + 2 * P; ++r) {
+                        pw[r] = pt[off + r * PP];
+                        // plane c - 1 from its tile (keeping the item's previous window in registers
+                        // measured the same time at c4 and spills at p = 3)
+                        dw[r] = pw[r] - k4_smem[sh + G::OFF_PT + ((ib + 2) % 3) * G::PT + off + r * PP];
+                    }
+                    double ky[4], mq[4];
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
+#ifdef ADS_ABL_NOCOL
+                        ky[r] = pw[r] + pw[r + 2 * P]; mq[r] = dw[r] + dw[r + 2 * P]; continue;
+#endif
                         if (YI) {
-                            double s = a.kc[1][P] * pw[r + P];
+                            double s = a.kc[1][P] * pw[r + P], t = a.mc[1][P] * dw[r + P];
 #pragma unroll
-                            for (int d = 1; d <= P; ++d) s = fma(a.kc[1][P + d], pw[r + P - d] + pw[r + P + d], s);
-                            ky[r] = s;
-                        } else {
-                            const double *row = yb + ((4 * g4 + r) * 2 + 1) * W;
-                            double s = 0.0;
-#pragma unroll
-                            for (int c = 0; c < W; ++c) s = fma(row[c], pw[r + c], s);
-                            ky[r] = s;
-                        }
-                    }
-                    {
-#pragma unroll
-                        for (int r = 0; r < 4 + 2 * P; ++r) pw[r] = dt[(4 * g4 + r) * PP + nc];
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            if (YI) {
-                                double s = a.mc[1][P] * pw[r + P];
-#pragma unroll
-                                for (int d = 1; d <= P; ++d) s = fma(a.mc[1][P + d], pw[r + P - d] + pw[r + P + d], s);
-                                mq[r] = s;
-                            } else {
-                                const double *row = yb + ((4 * g4 + r) * 2) * W;
-                                double s = 0.0;
-#pragma unroll
-                                for (int c = 0; c < W; ++c) s = fma(row[c], pw[r + c], s);
-                                mq[r] = s;
+                            for (int d = 1; d <= P; ++d) {
+                                s = fma(a.kc[1][P + d], pw[r + P - d] + pw[r + P + d], s);
+                                t = fma(a.mc[1][P + d], dw[r + P - d] + dw[r + P + d], t);
                             }
+                            ky[r] = s;
+                            mq[r] = t;
+                        } else {
+                            const double *rk = yb + ((4 * g4 + r) * 2 + 1) * W, *rm = yb + ((4 * g4 + r) * 2) * W;
+                            double s = 0.0, t = 0.0;
+#pragma unroll
+                            for (int c = 0; c < W; ++c) {
+                                s = fma(rk[c], pw[r + c], s);
+                                t = fma(rm[c], dw[r + c], t);
+                            }
+                            ky[r] = s;
+                            mq[r] = t;
                         }
                     }
                     double2 *o = reinterpret_cast<double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ) + (4 * g4) * K4_YQP + nc;
@@ -873,10 +926,11 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
                     for (int r = 0; r < 4; ++r) o[r * K4_YQP] = make_double2(ky[r], mq[r]);
                 }
             } else {
-                // row items: a warp covers 4 rows x 8 column quads (16-byte window loads)
+                // row items: a warp covers 4 rows x 8 column quads (16-byte window loads from the
+                // aligned staged column 4 q; haloed column 4 q + j is window element j + SFT)
 #pragma unroll 1
-                for (int grp = w - G::CW; grp < G::RG; grp += G::RW) {
-                    const int hy = 4 * grp + rsub;
+                for (int t = 0; t < (G::RG + G::RW - 1) / G::RW; ++t) {
+                    const int hy = 4 * (w - G::CW + t * G::RW) + rsub;
                     if (hy < HY) {
                         const double2 *src = reinterpret_cast<const double2 *>(pt + hy * PP + 4 * rq4);
                         double pw[G::RWIN];
@@ -889,66 +943,61 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
                         double kx[4];
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
+#ifdef ADS_ABL_NOROW
+                            kx[j] = pw[j] + pw[j + 2 * P]; continue;
+#endif
                             if (XI) {
-                                double s = a.kc[0][P] * pw[j + P];
+                                double s = a.kc[0][P] * pw[j + P + SFT];
 #pragma unroll
-                                for (int d = 1; d <= P; ++d) s = fma(a.kc[0][P + d], pw[j + P - d] + pw[j + P + d], s);
+                                for (int d = 1; d <= P; ++d)
+                                    s = fma(a.kc[0][P + d], pw[j + P + SFT - d] + pw[j + P + SFT + d], s);
                                 kx[j] = s;
                             } else {
                                 double s = 0.0;
 #pragma unroll
-                                for (int c = 0; c < W; ++c) s = fma(xb[(c * 2 + 1) * K4_X + 4 * rq4 + j], pw[j + c], s);
+                                for (int c = 0; c < W; ++c) s = fma(xb[(c * 2 + 1) * K4_X + 4 * rq4 + j], pw[j + c + SFT], s);
                                 kx[j] = s;
                             }
                         }
+                        // odd quads store their second half first: each quarter-warp store then hits 8
+                        // distinct bank groups (row pitch 18 x 16 bytes)
                         double2 *o = reinterpret_cast<double2 *>(k4_smem + sh + G::OFF_X1 + b * G::X1 + hy * K4_XP + 4 * rq4);
-                        o[0] = make_double2(kx[0], kx[1]);
-                        o[1] = make_double2(kx[2], kx[3]);
+                        const int sw = lane & 1;
+                        o[sw] = sw ? make_double2(kx[2], kx[3]) : make_double2(kx[0], kx[1]);
+                        o[sw ^ 1] = sw ? make_double2(kx[0], kx[1]) : make_double2(kx[2], kx[3]);
                     }
                 }
             }
         }
-        // ---- C: plane c = kk0 + ic: G = My (Kx P) + Mx (Ky P), dT_{c-1} = Mx (My D) into the z ring.
-        // DMMA m8n8k4: warp w owns the 8 x 8 block (rows 8 mi.., columns 8 nj..); lane l its outputs
-        // (row 8 mi + l/4, columns 8 nj + 2 (l%4) + {0, 1}).  Mx acts as the B operand (band, in
-        // registers) on the (Ky P, My D) rows, My as the A operand on the Kx P columns.
-        const int ic = ii - 2;
-        if (ic >= 0) {
-            const int b = ic & 1, kc_ = kk0 + ic, kout = kc_ - P;
-            const double2 *Yq = reinterpret_cast<const double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ) +
-                                (8 * mi + (lane >> 2)) * K4_YQP + 8 * nj + (lane & 3);
-            const double *Xq = k4_smem + sh + G::OFF_X1 + b * G::X1 + (8 * mi + (lane & 3)) * K4_XP + 8 * nj + (lane >> 2);
-            double gacc[2] = {0.0, 0.0}, hacc[2] = {0.0, 0.0}, tacc[2] = {0.0, 0.0};
-#pragma unroll
-            for (int s4 = 0; s4 < G::KS; ++s4) {
-                const double2 av = Yq[4 * s4];
-                const double bv = Xq[4 * s4 * K4_XP], bmx = frx[32 * s4], amy = fry[32 * s4];
-                k4_dmma(gacc, av.x, bmx);
-                k4_dmma(tacc, av.y, bmx);
-                k4_dmma(hacc, amy, bv);
-            }
-            const double g0 = gacc[0] + hacc[0], g1 = gacc[1] + hacc[1], t0 = tacc[0], t1 = tacc[1];
-            const bool zint = kc_ + a.zoff - P >= a.ilo[2] && kc_ + a.zoff + P <= a.ihi[2];
-            double o0 = 0.0, o1 = 0.0;  // t0, t1: dT_{c-1} = Mx My D of the lane's two outputs
-            switch (ic % W) {
-#define ADS_K4C(U)                                                                      \
-    case U:                                                                             \
-        if constexpr (U < W) k4_zscatter<P, U>(a, A0, A1, g0, g1, t0, t1, kc_, zint, o0, o1); \
-        break;
-                ADS_K4C(0) ADS_K4C(1) ADS_K4C(2) ADS_K4C(3) ADS_K4C(4) ADS_K4C(5)
-                ADS_K4C(6) ADS_K4C(7) ADS_K4C(8) ADS_K4C(9) ADS_K4C(10)
-#undef ADS_K4C
-            }
-            if (kout >= z0) {  // output plane kout = c - P: r = g src + sign K P
-                const double gz = has_src ? gsrc * __ldg(a.bz + kout + a.zoff) : 0.0;
-                const double r0 = fma(a.sign, o0, gz * sxy0), r1 = fma(a.sign, o1, gz * sxy1);
-                if (pair) *reinterpret_cast<double2 *>(rq) = make_double2(r0, r1);
-                else if (own0) rq[0] = r0;
-                else if (own1) rq[1] = r1;
-                rq += sz;
-            }
+        // ---- A: input plane kk = kk0 + ii into P tile ii % 3
+        if (ST || ii < npl) {
+            k4_wait(mb0 + 8u * (ii % K4_NPF), (unsigned)((ii / K4_NPF) & 1));
+            const int kk = kk0 + ii;
+            const int sb = sh + (ii % K4_NPF) * 2 * G::STG, pb = sh + G::OFF_PT + (ii % 3) * G::PT;
+            double *const po = (a.Pout && kk >= z0 && kk < z1) ? a.Pout + (long)kk * sz : nullptr;
+            if (ST) k4_stage_a<P, 3>(a.tau, so_, po_, go_, om_, sb, pb, po);
+            else if (!(kk >= a.zv0 && kk < a.zv1)) k4_stage_a<P, 0>(a.tau, so_, po_, go_, om_, sb, pb, po);
+            else if (a.Ph && (kk < 0 || kk >= a.geo.n2)) k4_stage_a<P, 1>(a.tau, so_, po_, go_, om_, sb, pb, po);
+            else if (kk + a.zoff == a.zd0 || kk + a.zoff == a.zd1) k4_stage_a<P, 2>(a.tau, so_, po_, go_, om_, sb, pb, po);
+            else k4_stage_a<P, 3>(a.tau, so_, po_, go_, om_, sb, pb, po);
         }
+    };
+    // steady range [ss0, ss1): ii >= 2 + 2p (stages B, C active, output owned), input plane plain
+    // (in memory, not a slab halo, not a zero-Dirichlet face), zint for the stage-C plane ii - 2
+    int klo = a.zv0, khi = a.zv1;
+    if (a.Ph) {
+        klo = max(klo, 0);
+        khi = min(khi, a.geo.n2);
     }
+    if (a.zd0 >= 0) klo = max(klo, a.zd0 - a.zoff + 1);
+    if (a.zd1 >= 0) khi = min(khi, a.zd1 - a.zoff);
+    const int ss0 = max(max(2 + 2 * P, klo - kk0), a.ilo[2] - a.zoff + P - kk0 + 2);
+    const int ss1 = max(ss0, min(min(npl, khi - kk0), a.ihi[2] - a.zoff - P - kk0 + 3));
+    using SF = std::integral_constant<bool, false>;
+    using STT = std::integral_constant<bool, true>;
+    for (int ii = 0; ii < ss0; ++ii) plane(ii, SF{});
+    for (int ii = ss0; ii < ss1; ++ii) plane(ii, STT{});
+    for (int ii = ss1; ii < npl + 2; ++ii) plane(ii, SF{});
 }
 
 template <int P>

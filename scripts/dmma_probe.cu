@@ -50,6 +50,31 @@ __global__ void dfma_kernel(double *out, int iters, double a, double b) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+
+// mixed: every warp interleaves NACC DMMA chains with 16 DFMA chains (are the FP64 tensor and the
+// FP64 vector pipes separate?)
+__global__ void mixed_kernel(double *out, int iters, double a, double b) {
+    double d[8][2], f[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i][0] = d[i][1] = threadIdx.x * 1e-3 + i;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) f[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            dmma(d[i][0], d[i][1], a, b);
+            f[2 * i] = fma(a, f[2 * i], b);
+            f[2 * i + 1] = fma(a, f[2 * i + 1], b);
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += d[i][0] + d[i][1];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += f[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main() {
     double hA[32], hB[32], hD[64], ref[64];
     for (int i = 0; i < 32; ++i) { hA[i] = 1.0 + i * 0.37; hB[i] = 2.0 - i * 0.11; }
@@ -91,6 +116,11 @@ int main() {
         warps * iters * 8 * 512.0);
     run("dfma 16 chains", [&] { dfma_kernel<<<blocks, threads>>>(dO, iters, 1.0000001, 1e-9); },
         (double)blocks * threads * iters * 16 * 2.0);
+    // mixed: 8 DMMA (8*512 flops per warp) + 16 DFMA (16*32*2 flops per warp) per iteration
+    run("mixed 8 dmma+16 dfma", [&] { mixed_kernel<<<blocks, threads>>>(dO, iters, 1.0000001, 0.9999999); },
+        warps * iters * (8 * 512.0 + 16 * 64.0));
+    run("dmma 8 acc (alone)", [&] { tput_kernel<8><<<blocks, threads>>>(dO, iters, 1.0000001, 0.9999999); },
+        warps * iters * 8 * 512.0);
     cudaError_t e = cudaGetLastError();
     printf("status: %s\n", cudaGetErrorString(e));
     return 0;
