@@ -152,6 +152,21 @@ int ads_create_dist(ads_handle *h, int nx, int ny, int nz, int p, double tau, in
 int ads_create_virtual(ads_handle *h, int nx, int ny, int nz, int p, double tau, int bc, int nslabs);
 int ads_local_extent(ads_handle h, int *z_begin, int *z_count);
 
+/* z-direction solve of the slab decomposition (north_star: "an NCCL all-to-all transpose or a
+ * distributed SPIKE reduced system, whichever measures faster"; the z-line solves are the third
+ * sweep).  mode ADS_ZSOLVE_SPIKE (default): each slab solves its diagonal block
+ * of A_z and the exact SPIKE correction couples the slabs (above).  mode ADS_ZSOLVE_ALLTOALL:
+ * after the local x and y sweeps the right-hand side is transposed -- slab r receives y block
+ * [r n_y / G, (r+1) n_y / G) of every global plane (one grouped NCCL send/recv per peer; device
+ * copies in a virtual group) --, solved along complete z-lines with the single-GPU factors of
+ * A_z, transposed back and applied by the kick.  Both give the same result up to rounding.  The
+ * first switch to ADS_ZSOLVE_ALLTOALL allocates 3 slab-sized buffers per slab (4 on an NCCL rank).
+ * Collective on NCCL slabs (every rank must call it with the same mode).  Errors: ADS_E_INVAL
+ * (not a slab handle, bad mode, more than 64 slabs or fewer y rows than slabs). */
+#define ADS_ZSOLVE_SPIKE 0
+#define ADS_ZSOLVE_ALLTOALL 1
+int ads_set_zsolve(ads_handle h, int mode);
+
 /* Attach a CUDA stream (cudaStream_t passed as void*).  NULL (which is also what
  * torch.cuda.current_stream().cuda_stream is for PyTorch's default stream) selects the
  * library's own stream, a blocking stream that is ordered against the legacy default

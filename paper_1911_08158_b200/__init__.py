@@ -31,7 +31,7 @@ EXPORTS = [
     "ads_time", "ads_step_count", "ads_dims", "ads_apply_k", "ads_solve_d", "ads_sweep", "ads_launch_count",
     "ads_last_error", "ads_destroy", "ads_profile_enable", "ads_profile_read", "ads_step_bytes",
     "ads_get_unique_id", "ads_slab_plan", "ads_create_dist", "ads_create_virtual", "ads_local_extent",
-    "ads_modal_basis", "ads_modal_advance", "ads_set_scheme", "ads_set_tau",
+    "ads_modal_basis", "ads_modal_advance", "ads_set_scheme", "ads_set_tau", "ads_set_zsolve",
 ]
 
 
@@ -86,6 +86,7 @@ def lib():
             "ads_modal_advance": (_I, [_H, _L]),
             "ads_set_scheme": (_I, [_H, _I]),
             "ads_set_tau": (_I, [_H, _D]),
+            "ads_set_zsolve": (_I, [_H, _I]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -263,6 +264,10 @@ class Solver:
         """1 = reading R1 (default), 0 = the literal Eq. 16 (ads_set_scheme); set the state again."""
         self._check(lib().ads_set_scheme(self.h, scheme))
 
+    def set_zsolve(self, mode):
+        """Slab handles: 0 = distributed SPIKE (default), 1 = all-to-all transpose (ads_set_zsolve)."""
+        self._check(lib().ads_set_zsolve(self.h, mode))
+
     def modal_advance(self, nsteps):
         """Advance by nsteps R1 steps exactly in modal space (ads_modal_advance)."""
         self._check(lib().ads_modal_advance(self.h, nsteps))
@@ -326,12 +331,14 @@ def project_1d(solver, func, d):
     return solver.mass_solve_1d(d, solver.load_vector(d, func))
 
 
-def make_solver(wl, dist=None, virtual_slabs=0, u0=None):
+def make_solver(wl, dist=None, virtual_slabs=0, u0=None, zsolve=0):
     """Solver for a workloads.Workload with its initial state and source set (library-side projection,
     or the given coefficients u0).  dist=(rank, world, uid): this process's z-slab;
-    virtual_slabs=G: all G slabs on this device."""
+    virtual_slabs=G: all G slabs on this device; zsolve: slab z solve (0 SPIKE, 1 all-to-all)."""
     s = Solver(wl.nel, wl.p, wl.tau, wl.bc, elastic=wl.elastic, lam=wl.lam, mu=wl.mu, rho=wl.rho, dist=dist,
                virtual_slabs=virtual_slabs)
+    if zsolve:
+        s.set_zsolve(zsolve)
     if wl.source is not None:
         src = wl.source
         b = [s.load_vector(d, src.f[d]) for d in range(3)]

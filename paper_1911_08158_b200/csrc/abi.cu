@@ -79,6 +79,14 @@ struct ads_ctx {
     double qt[2 * kMaxP][2 * kMaxP] = {}, qb[2 * kMaxP][2 * kMaxP] = {};
     double wbp[kMaxP][kMaxP] = {}, vtm[kMaxP][kMaxP] = {}, wbm[kMaxP][kMaxP] = {}, vtn[kMaxP][kMaxP] = {};
     ncclComm_t comm = nullptr;
+    // all-to-all z solve (ads_set_zsolve, zsolve = 1): the slab's y block [py0[r], py0[r+1]) of every
+    // global plane (the "pencil", geometry pgeo) is gathered from all slabs, solved along z with the
+    // global A_z table tabG, and returned into arecv ([q][k][row][x] blocks) for the kick
+    int zsolve = 0;
+    std::vector<int> py0, z0s, nls;
+    Geom pgeo;
+    SolveTab tabG;
+    double *pen_in = nullptr, *pen_out = nullptr, *arecv = nullptr, *a2a_send = nullptr;
     std::vector<ads_ctx *> members;                  // dist = 2
     ads_ctx *prev = nullptr, *next = nullptr;        // dist = 3
     double *dpartial = nullptr, *dres = nullptr;
@@ -529,7 +537,7 @@ int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g
 }
 
 int run_sweep_tab(ads_ctx *h, int d, const SolveTab &tab, const double *in, double *out, double *V, double kick,
-                  long *inc = nullptr) {
+                  long *inc = nullptr, const Geom *geo = nullptr) {
     SweepArgs a;
     a.dstep_inc = inc;
     a.in = in;
@@ -537,7 +545,7 @@ int run_sweep_tab(ads_ctx *h, int d, const SolveTab &tab, const double *in, doub
     a.V = V;
     a.kick = kick;
     a.t = tab;
-    a.geo = h->geo;
+    a.geo = geo ? *geo : h->geo;
     a.dir = d;
     a.mode = V ? 1 : 0;
     ProfScope ps(h, 1 + d);
@@ -978,6 +986,85 @@ int exch_stage1(ads_ctx *G) {
     });
 }
 
+// All-to-all z solve (ads_set_zsolve(h, ADS_ZSOLVE_ALLTOALL)), after the local x and y sweeps left
+// each slab's right-hand side in R: (1) transpose -- slab s sends the rows of y block q of its
+// owned planes to slab q, which stacks them by global plane into its pencil (the full z extent of
+// y block q); (2) every pencil solves A_z along its complete z-lines (the single-GPU table); (3) the
+// planes of slab s in pencil q return to slab s (arecv block q); (4) kick V += kick a, A = a.
+// NCCL ranks pack their strided send blocks with a 2D device copy; a virtual group copies directly.
+int a2a_zsolve(ads_ctx *G, double kick, bool keepA) {
+    const int W = slab_count(G);
+    auto pny = [](const ads_ctx *m, int q) { return m->py0[q + 1] - m->py0[q]; };
+    if (G->dist == 2) {
+        for (ads_ctx *s_ : G->members)
+            for (int q = 0; q < W; ++q) {
+                ads_ctx *t = G->members[q];
+                const size_t w = sizeof(double) * pny(s_, q) * s_->geo.sy;
+                CUDA_TRY(G, cudaMemcpy2DAsync(t->pen_in + (long)s_->zbeg * t->pgeo.sz, sizeof(double) * t->pgeo.sz,
+                                              s_->R + (long)s_->py0[q] * s_->geo.sy, sizeof(double) * s_->geo.sz, w,
+                                              s_->n[2], cudaMemcpyDeviceToDevice, G->stream));
+            }
+    } else {
+        const int me = G->rank, nl = G->n[2];
+        const long sy = G->geo.sy;
+        for (int q = 0; q < W; ++q) {
+            const size_t w = sizeof(double) * pny(G, q) * sy;
+            double *dst = q == me ? G->pen_in + (long)G->zbeg * G->pgeo.sz : G->a2a_send + (long)nl * G->py0[q] * sy;
+            CUDA_TRY(G, cudaMemcpy2DAsync(dst, q == me ? sizeof(double) * G->pgeo.sz : w, G->R + (long)G->py0[q] * sy,
+                                          sizeof(double) * G->geo.sz, w, nl, cudaMemcpyDeviceToDevice, G->stream));
+        }
+        NCCL_TRY(G, ncclGroupStart());
+        for (int q = 0; q < W; ++q) {
+            if (q == me) continue;
+            NCCL_TRY(G, ncclSend(G->a2a_send + (long)nl * G->py0[q] * sy, (size_t)nl * pny(G, q) * sy, ncclDouble, q,
+                                 G->comm, G->stream));
+            NCCL_TRY(G, ncclRecv(G->pen_in + (long)G->z0s[q] * G->pgeo.sz, (size_t)G->nls[q] * G->pgeo.sz, ncclDouble,
+                                 q, G->comm, G->stream));
+        }
+        NCCL_TRY(G, ncclGroupEnd());
+    }
+    int rc;
+    for (ads_ctx *m : slabs_of(G))
+        if ((rc = run_sweep_tab(m, 2, m->tabG, m->pen_in, m->pen_out, nullptr, 0.0, nullptr, &m->pgeo))) return rc;
+    if (G->dist == 2) {
+        for (ads_ctx *s_ : G->members)
+            for (int q = 0; q < W; ++q) {
+                ads_ctx *t = G->members[q];
+                CUDA_TRY(G, cudaMemcpyAsync(s_->arecv + (long)s_->n[2] * s_->py0[q] * s_->geo.sy,
+                                            t->pen_out + (long)s_->zbeg * t->pgeo.sz,
+                                            sizeof(double) * s_->n[2] * t->pgeo.sz, cudaMemcpyDeviceToDevice, G->stream));
+            }
+    } else {
+        const int me = G->rank, nl = G->n[2];
+        const long sy = G->geo.sy;
+        CUDA_TRY(G, cudaMemcpyAsync(G->arecv + (long)nl * G->py0[me] * sy, G->pen_out + (long)G->zbeg * G->pgeo.sz,
+                                    sizeof(double) * nl * G->pgeo.sz, cudaMemcpyDeviceToDevice, G->stream));
+        NCCL_TRY(G, ncclGroupStart());
+        for (int q = 0; q < W; ++q) {
+            if (q == me) continue;
+            NCCL_TRY(G, ncclSend(G->pen_out + (long)G->z0s[q] * G->pgeo.sz, (size_t)G->nls[q] * G->pgeo.sz, ncclDouble,
+                                 q, G->comm, G->stream));
+            NCCL_TRY(G, ncclRecv(G->arecv + (long)nl * G->py0[q] * sy, (size_t)nl * pny(G, q) * sy, ncclDouble, q,
+                                 G->comm, G->stream));
+        }
+        NCCL_TRY(G, ncclGroupEnd());
+    }
+    for (ads_ctx *m : slabs_of(G)) {
+        KickA2AArgs k;
+        k.arecv = m->arecv;
+        k.V = m->V;
+        k.A = keepA ? m->A : nullptr;
+        k.kick = kick;
+        k.geo = m->geo;
+        k.nq = W;
+        for (int q = 0; q <= W; ++q) k.py0[q] = m->py0[q];
+        ProfScope ps(m, 3);
+        if (launch_kick_a2a(k, m->stream)) return fail(m, ADS_E_INVAL, "kick_a2a: too many slabs");
+        if ((rc = check_launch(m, "kick_a2a"))) return rc;
+    }
+    return ADS_OK;
+}
+
 // One drift + solve + kick over all slabs: A = D^-1 (F(t) - K (U + tau_d V)), V += kick A,
 // U <- U + tau_d V when tau_d != 0 (the step) -- with tau_d = 0 this is the half-kick init.
 int dist_solve(ads_ctx *G, double tau_d, double g, double kick, bool keepA) {
@@ -1003,8 +1090,14 @@ int dist_solve(ads_ctx *G, double tau_d, double g, double kick, bool keepA) {
                           tau_d != 0.0 ? m->U2 : nullptr)))
             return rc;
         if ((rc = run_sweep(m, 0, m->R, m->Wk, nullptr, 0.0)) || (rc = run_sweep(m, 1, m->Wk, m->R, nullptr, 0.0)) ||
-            (rc = run_sweep_tab(m, 2, m->tabZ, m->R, m->Wk, nullptr, 0.0)))
+            (!G->zsolve && (rc = run_sweep_tab(m, 2, m->tabZ, m->R, m->Wk, nullptr, 0.0))))
             return rc;
+    }
+    if (G->zsolve) {
+        if ((rc = a2a_zsolve(G, kick, keepA))) return rc;
+        if (tau_d != 0.0)
+            for (ads_ctx *m : slabs_of(G)) std::swap(m->U, m->U2);
+        return ADS_OK;
     }
     if ((rc = exch_tips(G))) return rc;
     if (G->world > 2) {  // interface refinement needs the neighbours' stage-1 values
@@ -1540,6 +1633,50 @@ int ads_modal_advance(ads_handle h, long nsteps) {
     if ((rc = run_sweep(h, 2, h->R, h->A, nullptr, 0.0))) return rc;
     launch_set_long(h->dstep, h->step, h->stream);  // source time of later graph replays
     return check_launch(h, "set_step");
+}
+
+// the pencil buffers and the global A_z table of one slab (first switch to the all-to-all solve)
+static int a2a_prepare(ads_ctx *m, int W) {
+    if (m->pen_in) return ADS_OK;
+    slab_plan(m->ngz, W, m->z0s, m->nls);
+    m->py0.assign(W + 1, 0);
+    for (int q = 0; q <= W; ++q) m->py0[q] = (int)((long)q * m->n[1] / W);
+    for (int q = 0; q < W; ++q)
+        if (m->py0[q + 1] <= m->py0[q]) return fail(m, ADS_E_INVAL, "all-to-all: %d slabs exceed n_y = %d", W, m->n[1]);
+    m->pgeo = m->geo;
+    m->pgeo.n1 = m->py0[m->rank + 1] - m->py0[m->rank];
+    m->pgeo.n2 = m->ngz;
+    m->pgeo.sz = m->geo.sy * m->pgeo.n1;
+    int rc;
+    const Band A = shifted(m->sp[2], m->tau * m->tau / 4.0, m->sp[2].bc);
+    if ((rc = make_solve_tab(m, A, "A_z (all-to-all pencils)", m->tabG))) return rc;
+    const size_t pb = sizeof(double) * m->pgeo.sz * m->pgeo.n2, fb = sizeof(double) * m->Nalloc;
+    if ((rc = dalloc(m, (void **)&m->pen_in, pb)) || (rc = dalloc(m, (void **)&m->pen_out, pb)) ||
+        (rc = dalloc(m, (void **)&m->arecv, fb)) || (m->dist == 1 && (rc = dalloc(m, (void **)&m->a2a_send, fb))))
+        return rc;
+    CUDA_TRY(m, cudaMemsetAsync(m->pen_in, 0, pb, m->stream));
+    CUDA_TRY(m, cudaMemsetAsync(m->pen_out, 0, pb, m->stream));
+    return ADS_OK;
+}
+
+int ads_set_zsolve(ads_handle h, int mode) {
+    DeviceScope ds_(h);
+    int rc = guard(h);
+    if (rc) return rc;
+    if (!h->dist || h->dist == 3 || (mode != ADS_ZSOLVE_SPIKE && mode != ADS_ZSOLVE_ALLTOALL))
+        return fail(h, ADS_E_INVAL, "set_zsolve: slab handles (ads_create_dist / ads_create_virtual), mode 0 or 1");
+    const int W = slab_count(h);
+    if (mode == ADS_ZSOLVE_ALLTOALL && W > kMaxA2A) return fail(h, ADS_E_INVAL, "all-to-all: at most %d slabs", kMaxA2A);
+    if (mode == ADS_ZSOLVE_ALLTOALL)
+        for (ads_ctx *m : slabs_of(h))
+            if ((rc = a2a_prepare(m, W))) {
+                if (m != h) h->err = m->err;
+                return m != h ? fail(h, rc, "%s", m->err.c_str()) : rc;
+            }
+    h->zsolve = mode;
+    for (ads_ctx *m : slabs_of(h)) m->zsolve = mode;
+    drop_graphs(h);
+    return ADS_OK;
 }
 
 int ads_local_extent(ads_handle h, int *z_begin, int *z_count) {

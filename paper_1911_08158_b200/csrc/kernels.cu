@@ -1762,6 +1762,27 @@ void launch_set_separable(double *u, long cstride, int ncomp, int nterms, const 
     set_separable_kernel<<<grid, SEP_THREADS, 0, s>>>(u, cstride, nterms, f, n0f, n1f, nzf, g, zoff, mx, my, ngz, ncomp);
 }
 
+// thread per (x, row, plane); the row's y block found by a scan of the (few) block starts
+__global__ void __launch_bounds__(256) kick_a2a_kernel(const KickA2AArgs a) {
+    const int i = blockIdx.x * 64 + (threadIdx.x & 63), j = blockIdx.y * 4 + (threadIdx.x >> 6), k = blockIdx.z;
+    const Geom &g = a.geo;
+    if (i >= g.n0 || j >= g.n1) return;
+    int q = 0;
+    while (q + 1 < a.nq && j >= a.py0[q + 1]) ++q;
+    const int r0 = a.py0[q], nr = a.py0[q + 1] - r0;
+    const double v = a.arecv[(long)g.n2 * r0 * g.sy + ((long)k * nr + (j - r0)) * g.sy + i];
+    const long o = (long)k * g.sz + (long)j * g.sy + i;
+    a.V[o] = fma(a.kick, v, a.V[o]);
+    if (a.A) a.A[o] = v;
+}
+
+int launch_kick_a2a(const KickA2AArgs &a, cudaStream_t s) {
+    if (a.nq < 1 || a.nq > kMaxA2A) return -1;
+    dim3 grd((a.geo.n0 + 63) / 64, (a.geo.n1 + 3) / 4, a.geo.n2);
+    kick_a2a_kernel<<<grd, 256, 0, s>>>(a);
+    return 0;
+}
+
 void launch_drift(const double *U, const double *V, double tau, double *P, long N, cudaStream_t s) {
     drift_kernel<<<grid_for(N), 256, 0, s>>>(U, V, tau, P, N);
 }

@@ -187,6 +187,19 @@ void launch_set_separable(double *u, long cstride, int ncomp, int nterms, const 
                           const Geom &g, int zoff, int mx, int my, int ngz, cudaStream_t s);
 // P = U + tau V over N contiguous elements (the drift of a slab's edge planes)
 void launch_drift(const double *U, const double *V, double tau, double *P, long N, cudaStream_t s);
+// all-to-all z solve (ads_set_zsolve): kick from the returned pencil blocks.  arecv holds, for each
+// y block q (rows [py0[q], py0[q+1])), the slab's solution a as [k][j - py0[q]][i] (row pitch g.sy)
+// at offset g.n2 py0[q] g.sy; V += kick a and A = a (A may be null) on the slab's owned planes.
+constexpr int kMaxA2A = 64;
+struct KickA2AArgs {
+    const double *arecv = nullptr;
+    double *V = nullptr, *A = nullptr;
+    double kick = 0.0;
+    Geom geo;
+    int nq = 1;
+    int py0[kMaxA2A + 1] = {};
+};
+int launch_kick_a2a(const KickA2AArgs &a, cudaStream_t s);
 // zero the boundary faces of a field (Dirichlet masking)
 // (slabs: local plane k is global plane k + zoff of ngz; default the field is the whole grid)
 int launch_mask_boundary(double *u, const Geom &g, cudaStream_t s, int zoff = 0, int ngz = -1);

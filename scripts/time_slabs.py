@@ -12,8 +12,8 @@ import paper_1911_08158_b200 as ads  # noqa: E402
 import workloads  # noqa: E402
 
 wl = workloads.get(sys.argv[1] if len(sys.argv) > 1 else "c4")
-for G in [0, 2, 4, 8]:
-    s = ads.make_solver(wl, virtual_slabs=G)
+for G, zs in [(0, 0), (2, 0), (4, 0), (8, 0), (2, 1), (4, 1), (8, 1)]:
+    s = ads.make_solver(wl, virtual_slabs=G, zsolve=zs)
     st = torch.cuda.Stream()
     s.set_stream(st)
     s.step(3)
@@ -25,7 +25,7 @@ for G in [0, 2, 4, 8]:
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
-    print(f"{wl.name} slabs={G or 1}{' (single-GPU path)' if not G else ''}: {ms:.3f} ms/step "
+    print(f"{wl.name} slabs={G or 1}{' (single-GPU path)' if not G else ''}{' all-to-all' if zs else ''}: {ms:.3f} ms/step "
           f"(all slabs on one GPU), {(s.launch_count() - n0) / 20:.0f} launches/step", flush=True)
     s.close()
     del s

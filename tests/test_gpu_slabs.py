@@ -31,12 +31,14 @@ def ads():
     return ads
 
 
-def _run(ads, wl, nslabs, checkpoints):
+def _run(ads, wl, nslabs, checkpoints, zsolve=0):
     # both sides start from the same coefficients (the oracle's projection); the source load
     # vectors are formed independently.  One step is held to 1e-12 against the extended-precision
     # oracle (T1), later checkpoints to 1e-9 against the fp64 oracle.
     u0 = oracle.project_separable(wl)
     g = ads.Solver(wl.nel, wl.p, wl.tau, wl.bc, virtual_slabs=nslabs)
+    if zsolve:
+        g.set_zsolve(zsolve)
     if wl.source is not None:
         src = wl.source
         g.set_source([g.load_vector(d, src.f[d]) for d in range(3)], src.wavelet, src.f0, src.t0, src.amp)
@@ -148,3 +150,72 @@ def test_virtual_group_set_stream(ads):
     r.step(8)
     for a, b in zip(g.get_state(), r.get_state()):
         assert np.array_equal(a, b)
+
+
+# ---- all-to-all z solve (ads_set_zsolve(h, ADS_ZSOLVE_ALLTOALL), north_star's alternative) ----
+
+@pytest.mark.parametrize("nslabs,nz", [(2, 150), (3, 225), (8, 513)])
+def test_alltoall_virtual_vs_oracle(ads, nslabs, nz):
+    """The transpose path (y blocks gathered into full-z pencils, single-GPU A_z factors, returned
+    for the kick) against the oracle: 1e-12 after one step (extended-precision truth), 1e-9 after
+    the run; y extents that split unevenly (19 / 3, 21 / 8)."""
+    wl = workloads.get("c4").scaled(12, 12)
+    wl.nel = (17, 16 if nslabs == 3 else 18, nz)
+    _run(ads, wl, nslabs, [1, 12], zsolve=1)
+
+
+def test_alltoall_forced_p2_and_natural(ads):
+    wl = workloads.get("c3").scaled(12, 40)
+    wl.nel = (12, 14, 230)
+    _run(ads, wl, 4, [1, 40], zsolve=1)
+    wl = workloads.get("c2").scaled(10, 20)
+    wl.nel = (10, 9, 160)
+    wl.bc = 0
+    _run(ads, wl, 2, [1, 20], zsolve=1)
+
+
+def test_alltoall_matches_spike_and_switches(ads):
+    """Both z solves give the same state to rounding; a run may switch between them."""
+    wl = workloads.get("c4").scaled(16, 10)
+    wl.nel = (21, 18, 300)
+    a = ads.make_solver(wl, virtual_slabs=4, zsolve=1)
+    b = ads.make_solver(wl, virtual_slabs=4)
+    a.step(6)
+    b.step(6)
+    for x, y in zip(a.get_state(), b.get_state()):
+        assert rel(x, y) < 1e-12
+    a.set_zsolve(0)
+    b.set_zsolve(1)
+    a.step(4)
+    b.step(4)
+    for x, y in zip(a.get_state(), b.get_state()):
+        assert rel(x, y) < 1e-12
+    assert np.allclose(a.energy(), b.energy(), rtol=1e-12)
+
+
+def test_alltoall_nccl_world1(ads):
+    """NCCL slab handle (one rank) on the all-to-all path: local transposes only."""
+    wl = workloads.get("c2").scaled(12, 8)
+    u0 = oracle.project_separable(wl)
+    ref = ads.Solver(wl.nel, wl.p, wl.tau, wl.bc)
+    ref.set_state(u0)
+    ref.step(8)
+    g = ads.Solver(wl.nel, wl.p, wl.tau, wl.bc, dist=(0, 1, ads.get_unique_id()))
+    g.set_zsolve(1)
+    g.set_state(u0)
+    g.step(8)
+    for x, y in zip(g.get_state(), ref.get_state()):
+        assert rel(x, y) < 1e-13
+    assert np.allclose(g.energy(), ref.energy(), rtol=1e-13)
+
+
+def test_alltoall_errors(ads):
+    s = ads.Solver((8, 8, 8), 2, 1e-3)
+    with pytest.raises(ads.AdsError):
+        s.set_zsolve(1)  # not a slab handle
+    g = ads.Solver((8, 8, 100), 2, 1e-3, virtual_slabs=2)
+    with pytest.raises(ads.AdsError):
+        g.set_zsolve(2)
+    g2 = ads.Solver((3, 2, 254), 2, 1e-3, virtual_slabs=8)  # 4 y rows < 8 slabs
+    with pytest.raises(ads.AdsError):
+        g2.set_zsolve(1)
