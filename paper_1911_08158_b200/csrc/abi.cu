@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 #include <string>
 #include <vector>
@@ -554,6 +555,13 @@ int run_sweep_tab(ads_ctx *h, int d, const SolveTab &tab, const double *in, doub
         launch_line1(in, out, V, 1.0 / a00, kick, inc, h->geo, h->stream);
         return check_launch(h, "line1");
     }
+    // the z blocks of thin slabs: one thread per line (ADS_LINE_SWEEP=0 disables)
+    static const bool line_ok = [] {
+        const char *e = std::getenv("ADS_LINE_SWEEP");
+        return !(e && e[0] == '0');
+    }();
+    if (line_ok && &tab == &h->tabZ && out && tab.n <= kLineSweepMax && launch_line_sweep(h->p, a, h->stream) == 0)
+        return check_launch(h, "line sweep");
     const int lr = launch_sweep(h->p, a, h->stream);
     if (lr == -2) return fail(h, ADS_E_CUDA, "sweep: TMA descriptor encoding failed");
     if (lr) return fail(h, ADS_E_INVAL, "sweep: unsupported p/chunk");

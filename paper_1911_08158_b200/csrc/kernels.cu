@@ -1354,9 +1354,14 @@ static void kron3_launch(const double *in, double *out, const KronTerms &k3, dou
         const int zl = (g.n2 + nz - 1) / nz;
         if (zl < 2 * P + 1 && nz > 1) break;
         const long ctas = tiles * ((g.n2 + zl - 1) / zl);
-        const double cost = ((double)ctas / resident + 0.5) * (zl + 2.0 * P);
+        const double cost = (ctas <= resident ? 1.0 : (double)ctas / resident + 0.5) * (zl + 2.0 * P);
         if (cost < best_cost * 0.999) { best_cost = cost; best = nz; }
     }
+    static const int nz_env = [] {  // experiment override of the split
+        const char *e = std::getenv("ADS_KRON_NZ");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (nz_env > 0) best = nz_env;
     const int zlen = (g.n2 + best - 1) / best;
     dim3 grd(gx, gy, (g.n2 + zlen - 1) / zlen);
     kron3_kernel<P, T><<<grd, KR_THREADS, sm, s>>>(in, out, k3, beta, g, zlen);
@@ -1539,7 +1544,8 @@ static int encode_field_map(CUtensorMap *m, const double *base, const Geom &g, u
 
 // z split: CTAs are scheduled dynamically, so the time is about (CTAs per resident slot + 1/2 for
 // the tail) x (planes per CTA incl. 2p halo planes); this fit the measured v3 kop times at 515^3
-// for 1..12 pieces within 3 % (1.69 ms unsplit, 1.49 ms at 4 pieces)
+// for 1..12 pieces within 3 % (1.69 ms unsplit, 1.49 ms at 4 pieces).  A split that fits one wave
+// has no tail (c5, 130^3: 6 pieces in one wave beat 10 in 1.5 waves, 1.22 -> 1.04 ms per step)
 static int kop_pieces(int n2, int P, long tiles, long resident, double halo) {
     int best = 1;
     double best_cost = 1e300;
@@ -1547,7 +1553,8 @@ static int kop_pieces(int n2, int P, long tiles, long resident, double halo) {
         const int zl = (n2 + nz - 1) / nz;
         if (zl < 2 * P + 1 && nz > 1) break;
         const long ctas = tiles * ((n2 + zl - 1) / zl);
-        const double cost = ((double)ctas / resident + 0.5) * (zl + halo);
+        // one wave: no tail; several: the fluid model's mean tail of half a piece
+        const double cost = (ctas <= resident ? 1.0 : (double)ctas / resident + 0.5) * (zl + halo);
         if (cost < best_cost * 0.999) {
             best_cost = cost;
             best = nz;
@@ -1715,6 +1722,65 @@ static int sweep_dispatch(const SweepArgs &a, cudaStream_t s) {
         case 33: return sweep_launch_L<P, 33>(a, s);
     }
     return -1;
+}
+
+// sequential banded LU along one line per thread (PAPER.md:533-618 as printed): forward
+// y_i = r_i - sum_k l_{i,k} y_{i-k} (far terms first: y_{i-1} enters last), y kept in `out`;
+// backward x_i = y_i dinv_i - sum_k us_{i,k} x_{i+k}, out = x, V += kick x.  Threads of a block
+// take adjacent x-lines (coalesced rows).  (Staging each block of lines in shared memory with one
+// bulk copy per row measured slower: a whole line per thread caps residency at ~7 warps/SM.)
+template <int P>
+__global__ void __launch_bounds__(128, 8) line_sweep_kernel(const SweepArgs a) {
+    const int x = blockIdx.x * 128 + threadIdx.x, w = blockIdx.y;
+    if (a.dstep_inc && x == 0 && w == 0) *a.dstep_inc += 1;
+    const Geom &g = a.geo;
+    if (x >= g.n0) return;
+    const long ls = a.dir == 2 ? g.sz : g.sy, ws = a.dir == 2 ? g.sy : g.sz;
+    const int n = a.t.n;
+    const double *in = a.in + w * ws + x;  // may alias out (in-place solves)
+    double *out = a.out + w * ws + x;       // holds y between the passes
+    double *__restrict__ vv = a.V ? a.V + w * ws + x : nullptr;
+    const double *__restrict__ L = a.t.l, *__restrict__ U = a.t.us, *__restrict__ D = a.t.dinv;
+    double h[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) h[k] = 0.0;  // h[k] = y_{i-1-k}
+#pragma unroll 4
+    for (int i = 0; i < n; ++i) {
+        double s = in[i * ls];
+#pragma unroll
+        for (int k = P - 1; k >= 0; --k) s = fma(-__ldg(L + i * P + k), h[k], s);
+#pragma unroll
+        for (int k = P - 1; k > 0; --k) h[k] = h[k - 1];
+        h[0] = s;
+        out[i * ls] = s;
+    }
+#pragma unroll
+    for (int k = 0; k < P; ++k) h[k] = 0.0;  // h[k] = x_{i+1+k}
+#pragma unroll 4
+    for (int i = n - 1; i >= 0; --i) {
+        double v = out[i * ls] * __ldg(D + i);
+#pragma unroll
+        for (int k = P - 1; k >= 0; --k) v = fma(-__ldg(U + i * P + k), h[k], v);
+#pragma unroll
+        for (int k = P - 1; k > 0; --k) h[k] = h[k - 1];
+        h[0] = v;
+        out[i * ls] = v;
+        if (vv) vv[i * ls] = fma(a.kick, v, vv[i * ls]);
+    }
+}
+
+int launch_line_sweep(int p, const SweepArgs &a, cudaStream_t s) {
+    if (a.dir == 0 || a.t.n > kLineSweepMax || !a.out) return -1;
+    dim3 grd((a.geo.n0 + 127) / 128, a.dir == 2 ? a.geo.n1 : a.geo.n2);
+    switch (p) {
+        case 1: line_sweep_kernel<1><<<grd, 128, 0, s>>>(a); break;
+        case 2: line_sweep_kernel<2><<<grd, 128, 0, s>>>(a); break;
+        case 3: line_sweep_kernel<3><<<grd, 128, 0, s>>>(a); break;
+        case 4: line_sweep_kernel<4><<<grd, 128, 0, s>>>(a); break;
+        case 5: line_sweep_kernel<5><<<grd, 128, 0, s>>>(a); break;
+        default: return -1;
+    }
+    return 0;
 }
 
 int launch_sweep(int p, const SweepArgs &a, cudaStream_t s) {

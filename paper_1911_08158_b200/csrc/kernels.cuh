@@ -157,6 +157,14 @@ void launch_repack(const double *src, double *dst, const Geom &g, int to_pitched
 void launch_line1(const double *in, double *out, double *V, double scale, double kick, long *inc, const Geom &g,
                   cudaStream_t s);
 int launch_sweep(int p, const SweepArgs &a, cudaStream_t s);
+// Short lines along y (dir 1) or z (dir 2): one thread per line running the sequential banded LU
+// recurrences of the factors in a.t (rows [0, t.n)), threads of a block on adjacent x-lines
+// (coalesced rows); y is kept in `out` between the forward and the backward pass.  Same modes
+// as launch_sweep (kick, dstep_inc).  Used for the z blocks of thin slabs (at most kLineSweepMax
+// planes), where the partitioned kernel's per-tile overheads dominate (c4 as 8 slabs of 65
+// planes: 6.49 -> 6.03 ms of summed work); slower than it from ~65-row lines of a whole grid up.
+constexpr int kLineSweepMax = 96;
+int launch_line_sweep(int p, const SweepArgs &a, cudaStream_t s);
 // dynamic shared memory (bytes) a sweep along dir needs for these tables (one output buffer)
 long sweep_smem_bytes(int p, const SolveTab &t, int dir);
 constexpr long kMaxSmemPerCta = 227L * 1024;
