@@ -123,6 +123,10 @@ struct ads_ctx {
     bool has_src = false;
     int wavelet = 0;
     double f0 = 0, t0 = 0, amp = 0;
+    // elasticity: two side streams and a pool of events for the independent launches of a step
+    // (fork/join; inside a graph capture they become parallel branches)
+    cudaStream_t side[2] = {nullptr, nullptr};
+    cudaEvent_t fev[8] = {};
     std::vector<void *> allocs;
     // profiling (ads_profile_enable): event pairs per kernel class
     bool prof = false;
@@ -709,24 +713,56 @@ int ups_offdiag(ads_ctx *h, int i, int k, const double *in, double *out, double 
     return check_launch(h, "kron3");
 }
 
+// Concurrency of the elastic step: lane 0 is the handle's stream, lanes 1, 2 its side streams.
+// after(h, to, from): lane `to` waits for everything enqueued so far on lane `from` (an event);
+// on(h, lane, f): run f with the handle's launches going to that lane.
+cudaStream_t lane_stream(ads_ctx *h, int lane) { return lane == 0 ? h->stream : h->side[lane - 1]; }
+int after(ads_ctx *h, int to, int from, int ev) {
+    CUDA_TRY(h, cudaEventRecord(h->fev[ev], lane_stream(h, from)));
+    CUDA_TRY(h, cudaStreamWaitEvent(lane_stream(h, to), h->fev[ev], 0));
+    return ADS_OK;
+}
+template <class F>
+int on(ads_ctx *h, int lane, F f) {
+    cudaStream_t keep = h->stream;
+    h->stream = lane_stream(h, lane);
+    const int rc = f();
+    h->stream = keep;
+    return rc;
+}
+
 // out_i (+)= coef (Ups in)_i for all i.  The diagonal blocks go through the fused operator
 // kernel: out_i = coef mu K (in_i + tau_d v_i) with the drift written to pout_i if non-null.
+// The three components run on three lanes (the off-diagonal blocks read every component's drift,
+// so the lanes join between the two phases).
 int ups_apply(ads_ctx *h, const double *in, const double *v, double tau_d, double *pout, double *out, double coef) {
     int rc;
+    if ((rc = after(h, 1, 0, 0)) || (rc = after(h, 2, 0, 1))) return rc;
     // diagonal blocks Ups_ii = mu K + (mu + lam) K_(i): the operator kernel with direction i's K
     // term weighted (2 mu + lam) / mu
     for (int i = 0; i < 3; ++i) {
         double kw[3] = {1.0, 1.0, 1.0};
         kw[i] = (2.0 * h->mu + h->lam) / h->mu;
-        if ((rc = run_kop(h, comp((double *)in, h, i), comp((double *)v, h, i), tau_d, 0.0, coef * h->mu,
-                          pout ? comp(pout, h, i) : nullptr, comp(out, h, i), false, kw)))
+        if ((rc = on(h, i, [&] {
+                 return run_kop(h, comp((double *)in, h, i), comp((double *)v, h, i), tau_d, 0.0, coef * h->mu,
+                                pout ? comp(pout, h, i) : nullptr, comp(out, h, i), false, kw);
+             })))
             return rc;
     }
+    // every lane waits for every drift: lane 0 joins lanes 1, 2, then lanes 1, 2 wait for lane 0
+    if ((rc = after(h, 0, 1, 2)) || (rc = after(h, 0, 2, 3)) || (rc = after(h, 1, 0, 4)) || (rc = after(h, 2, 0, 5)))
+        return rc;
     const double *P = pout ? pout : in;  // the drifted field the blocks act on
-    for (int i = 0; i < 3; ++i) {
-        for (int k = 0; k < 3; ++k)
-            if (k != i && (rc = ups_offdiag(h, i, k, comp((double *)P, h, k), comp(out, h, i), coef))) return rc;
-    }
+    for (int i = 0; i < 3; ++i)
+        if ((rc = on(h, i, [&] {
+                 for (int k = 0; k < 3; ++k) {
+                     int r = k != i ? ups_offdiag(h, i, k, comp((double *)P, h, k), comp(out, h, i), coef) : 0;
+                     if (r) return r;
+                 }
+                 return 0;
+             })))
+            return rc;
+    if ((rc = after(h, 0, 1, 6)) || (rc = after(h, 0, 2, 7))) return rc;
     return ADS_OK;
 }
 
@@ -745,20 +781,29 @@ int s_solve(ads_ctx *h, int i, double *x, const double *in = nullptr) {
 int el_dsolve(ads_ctx *h, double *X) {
     const double hh = -0.5 * h->tau * h->tau;
     int rc;
-    for (int i = 0; i < 3; ++i) {  // w_i = X_i - tau^2/2 sum_{j<i} Ups_ij w_j (the first term reads X_i)
-        double *wi = comp(h->W, h, i);
-        for (int j = 0; j < i; ++j)
-            if ((rc = ups_offdiag(h, i, j, comp(h->W, h, j), wi, hh, j == 0 ? comp(X, h, i) : nullptr))) return rc;
-        if ((rc = s_solve(h, i, wi, i == 0 ? comp(X, h, 0) : nullptr))) return rc;
-    }
-    for (int i = 2; i >= 0; --i) {
-        double *zi = comp(X, h, i);
-        if ((rc = tri(h, zi, comp(h->W, h, i), h->dd[0].mband, h->dd[1].mband, h->dd[2].mband, h->rho, 0.0)))
-            return rc;
-        for (int j = i + 1; j < 3; ++j)
-            if ((rc = ups_offdiag(h, i, j, comp(X, h, j), zi, hh))) return rc;
-        if ((rc = s_solve(h, i, zi))) return rc;
-    }
+    double *w0 = comp(h->W, h, 0), *w1 = comp(h->W, h, 1), *w2 = comp(h->W, h, 2);
+    double *z0 = comp(X, h, 0), *z1 = comp(X, h, 1), *z2 = comp(X, h, 2);
+    auto rhoM = [&](double *z, const double *w) {
+        return tri(h, z, w, h->dd[0].mband, h->dd[1].mband, h->dd[2].mband, h->rho, 0.0);
+    };
+    // predictor: w_i = S_i^-1 (X_i - tau^2/2 sum_{j<i} Ups_ij w_j) (the first coupling reads X_i);
+    // w_2's coupling to w_0 runs on lane 1 while lane 0 finishes w_1
+    if ((rc = s_solve(h, 0, w0, z0))) return rc;
+    if ((rc = after(h, 1, 0, 0))) return rc;
+    if ((rc = on(h, 1, [&] { return ups_offdiag(h, 2, 0, w0, w2, hh, z2); }))) return rc;
+    if ((rc = ups_offdiag(h, 1, 0, w0, w1, hh, z1)) || (rc = s_solve(h, 1, w1))) return rc;
+    if ((rc = after(h, 0, 1, 1))) return rc;
+    if ((rc = ups_offdiag(h, 2, 1, w1, w2, hh)) || (rc = s_solve(h, 2, w2))) return rc;
+    // corrector: z_i = S_i^-1 (rho M w_i - tau^2/2 sum_{j>i} Ups_ij z_j); z_1, z_0's mass products
+    // on lanes 1, 2 from the start, z_0's coupling to z_2 on lane 2 once z_2 is final
+    if ((rc = after(h, 1, 0, 2)) || (rc = after(h, 2, 0, 3))) return rc;
+    if ((rc = on(h, 1, [&] { return rhoM(z1, w1); })) || (rc = on(h, 2, [&] { return rhoM(z0, w0); }))) return rc;
+    if ((rc = rhoM(z2, w2)) || (rc = s_solve(h, 2, z2))) return rc;
+    if ((rc = after(h, 2, 0, 4)) || (rc = on(h, 2, [&] { return ups_offdiag(h, 0, 2, z2, z0, hh); }))) return rc;
+    if ((rc = after(h, 0, 1, 5))) return rc;
+    if ((rc = ups_offdiag(h, 1, 2, z2, z1, hh)) || (rc = s_solve(h, 1, z1))) return rc;
+    if ((rc = after(h, 0, 2, 6))) return rc;
+    if ((rc = ups_offdiag(h, 0, 1, z1, z0, hh)) || (rc = s_solve(h, 0, z0))) return rc;
     return ADS_OK;
 }
 
@@ -1422,6 +1467,13 @@ static int create_common(ads_handle *out, int nx, int ny, int nz, int p, double 
             cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamDefault);
             if (e != cudaSuccess) rc = fail(h, ADS_E_CUDA, "stream: %s", cudaGetErrorString(e));
             h->own_stream = true;
+            if (ncomp == 3 && rc == ADS_OK) {
+                for (cudaStream_t &st : h->side)
+                    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) rc = ADS_E_CUDA;
+                for (cudaEvent_t &ev : h->fev)
+                    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) rc = ADS_E_CUDA;
+                if (rc) rc = fail(h, ADS_E_CUDA, "elastic side streams");
+            }
         }
         if (rc == ADS_OK) {  // zero everything: row padding and domain-boundary halos stay 0 forever
             for (auto &f : fields) cudaMemsetAsync(*f.first, 0, f.second, h->stream);
@@ -2064,6 +2116,10 @@ int ads_destroy(ads_handle h) {
     for (void *p : h->allocs) cudaFree(p);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    for (cudaStream_t st : h->side)
+        if (st) cudaStreamDestroy(st);
+    for (cudaEvent_t ev : h->fev)
+        if (ev) cudaEventDestroy(ev);
     delete h;
     return ADS_OK;
 }
