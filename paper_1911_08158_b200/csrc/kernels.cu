@@ -841,19 +841,18 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
             const double2 *Yq = reinterpret_cast<const double2 *>(k4_smem + sh + G::OFF_YQ + b * G::YQ) +
                                 (8 * mi + (lane >> 2)) * K4_YQP + 8 * nj + (lane & 3);
             const double *Xq = k4_smem + sh + G::OFF_X1 + b * G::X1 + (8 * mi + (lane & 3)) * K4_XP + 8 * nj + (lane >> 2);
-            // two accumulators per product (even / odd k steps): dependent DMMA chains of KS / 2
-            double gacc[2][2] = {}, hacc[2][2] = {}, tacc[2][2] = {};
+            double gacc[2] = {0.0, 0.0}, hacc[2] = {0.0, 0.0}, tacc[2] = {0.0, 0.0};
 #pragma unroll
             for (int s4 = 0; s4 < G::KS; ++s4) {
                 const double2 av = Yq[4 * s4];
                 const double bv = Xq[4 * s4 * K4_XP];
-                k4_dmma(gacc[s4 & 1], av.x, frx[s4]);
-                k4_dmma(tacc[s4 & 1], av.y, frx[s4]);
-                k4_dmma(hacc[s4 & 1], fry[s4], bv);
+                k4_dmma(gacc, av.x, frx[s4]);
+                k4_dmma(tacc, av.y, frx[s4]);
+                k4_dmma(hacc, fry[s4], bv);
             }
-            const double g0 = (gacc[0][0] + gacc[1][0]) + (hacc[0][0] + hacc[1][0]);
-            const double g1 = (gacc[0][1] + gacc[1][1]) + (hacc[0][1] + hacc[1][1]);
-            const double t0 = tacc[0][0] + tacc[1][0], t1 = tacc[0][1] + tacc[1][1];
+            // (two accumulators per product, even / odd k steps, measured no faster and change the
+            // rounding of a by ~1e-11 at p = 5: single chains)
+            const double g0 = gacc[0] + hacc[0], g1 = gacc[1] + hacc[1], t0 = tacc[0], t1 = tacc[1];
             const bool zint = ST || (kc_ + a.zoff - P >= a.ilo[2] && kc_ + a.zoff + P <= a.ihi[2]);
             double o0 = 0.0, o1 = 0.0;  // t0, t1: dT_{c-1} = Mx My D of the lane's two outputs
 #ifdef ADS_ABL_NOZ

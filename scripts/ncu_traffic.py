@@ -27,7 +27,7 @@ def main(rep, out):
         rd = float(r[col["dram__bytes_read.sum"]]) * UNIT[units[col["dram__bytes_read.sum"]]]
         wr = float(r[col["dram__bytes_write.sum"]]) * UNIT[units[col["dram__bytes_write.sum"]]]
         t = float(r[col["gpu__time_duration.sum"]]) * TUNIT[units[col["gpu__time_duration.sum"]]]
-        if "kop_kernel" in name:
+        if "kop_kernel" in name or "kop4_kernel" in name:
             key = "kop"
         elif "sweep_kernel" in name:
             key = ["sweep_x", "sweep_y", "sweep_z_kick"][min(sweeps, 2)]
