@@ -742,6 +742,10 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
                 "l"(reinterpret_cast<unsigned long long>(tmp)), "r"(x0 - G::PA), "r"(y0 - P), "r"(kk - a.zv0), "r"(mb)
                 : "memory");
         } else if (kk >= a.zv0 && kk < a.zv1) {
+#ifdef ADS_ABL_NOTMA  // experiment builds only: no plane loads
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(mb) : "memory");
+            return;
+#endif
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
                          "r"((unsigned)(2 * G::HXE * HY * sizeof(double)))
                          : "memory");
@@ -970,7 +974,9 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
         }
         // ---- A: input plane kk = kk0 + ii into P tile ii % 3
         if (ST || ii < npl) {
+#ifndef ADS_ABL_NOWAIT  // experiment builds only: data races, timing of the rest
             k4_wait(mb0 + 8u * (ii % K4_NPF), (unsigned)((ii / K4_NPF) & 1));
+#endif
             const int kk = kk0 + ii;
             const int sb = sh + (ii % K4_NPF) * 2 * G::STG, pb = sh + G::OFF_PT + (ii % 3) * G::PT;
             double *const po = (a.Pout && kk >= z0 && kk < z1) ? a.Pout + (long)kk * sz : nullptr;

@@ -1,9 +1,10 @@
 #!/bin/bash
-# Round-2 evidence for the current build (TAG names it): ncu --set full of one c4 step (kop + 3
-# sweeps) and its DRAM traffic, bench (c4 and c5, both arms), ncu launch list of a short bench,
+# Round-2 evidence for the current build (TAG names it): ncu --set full of the c4 operator kernel
+# and its DRAM traffic, bench (c4 and c5, both arms), ncu launch list of a short bench,
 # smoke, the full GPU suite, per-config / slab / set-state / modal timings.  Outputs in gpurun_out/.
 T=${TAG:-r2_v1}
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"kop|sweep" -s 4 -c 4 -o gpurun_out/prof_$T -f python scripts/prof_step.py c4 2 > gpurun_out/ncu_full_$T.log 2>&1
+# (one kernel per capture: gpurun_out/ must stay under 64 MiB to come back)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"kop" -s 1 -c 1 -o gpurun_out/prof_$T -f python scripts/prof_step.py c4 2 > gpurun_out/ncu_full_$T.log 2>&1
 python scripts/ncu_traffic.py gpurun_out/prof_$T.ncu-rep gpurun_out/${T}_traffic.json > /dev/null 2>&1 && cp gpurun_out/${T}_traffic.json profiles/
 timeout 900 python bench.py > gpurun_out/bench_$T.json 2> gpurun_out/bench_$T.err
 timeout 600 python bench.py --config c5 --steps 50 --no-configs > gpurun_out/bench_c5_$T.json 2> gpurun_out/bench_c5_$T.err
@@ -17,4 +18,3 @@ timeout 300 python scripts/time_setstate.py c4 > gpurun_out/setstate_$T.log 2>&1
 timeout 300 python scripts/time_modal.py > gpurun_out/modal_$T.log 2>&1
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$T.txt 2>&1; echo rc=$? >> gpurun_out/pytest_gpu_$T.txt
 tail -3 gpurun_out/pytest_gpu_$T.txt; tail -2 gpurun_out/smoke_$T.log; cat gpurun_out/configs_$T.log gpurun_out/kernels_$T.log
-timeout 600 ncu --set full --clock-control none -k regex:"modal" -c 6 -o gpurun_out/prof_modal_$T -f python scripts/prof_modal.py > gpurun_out/ncu_modal_$T.log 2>&1
