@@ -42,8 +42,20 @@ def build(force: bool = False, verbose: bool = False, extra=(), out=None) -> str
     objs = []
     nvcc = _nvcc()
     procs = []
+    # objects of the product build are kept in build/ and reused while newer than their source and
+    # every header (force rebuilds them all); experiment variants are compiled fresh and removed
+    cache = os.path.join(HERE, "build")
+    os.makedirs(cache, exist_ok=True)
+    hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS if os.path.exists(os.path.join(CSRC, h)))
     for src in SOURCES:  # the translation units compile in parallel
-        obj = os.path.join(CSRC, src + (("." + os.path.basename(out)) if out else "") + ".o")
+        if out:
+            obj = os.path.join(CSRC, src + "." + os.path.basename(out) + ".o")
+        else:
+            obj = os.path.join(cache, src + ".o")
+            if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(
+                    hdr_t, os.path.getmtime(os.path.join(CSRC, src))):
+                objs.append(obj)
+                continue
         cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
@@ -54,8 +66,9 @@ def build(force: bool = False, verbose: bool = False, extra=(), out=None) -> str
             raise subprocess.CalledProcessError(pr.returncode, cmd)
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-lcudart", "-lnccl"]
     subprocess.check_call(cmd)
-    for o in objs:
-        os.remove(o)
+    if out:
+        for o in objs:
+            os.remove(o)
     return lib
 
 
