@@ -8,7 +8,7 @@ from paper_1911_08158_b200 import build as b  # noqa: E402
 
 
 def one(spec):
-    name, flags = spec.split("=")
+    name, flags = spec.split("=", 1)
     out = os.path.join(b.HERE, f"libads_ablate_{name}.so")
     b.build(extra=flags.split(","), out=out)
     return out
