@@ -1157,16 +1157,20 @@ int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {
 
 // Kronecker triples out = beta out + sum_t alpha_t (Fx_t (x) Fy_t (x) Fz_t) in, t < T <= 2, sharing
 // input and output (elasticity couplings: the two triples of an off-diagonal
-// block Upsilon_ik go in one pass; general bands, no Toeplitz assumption).  Same structure as the round-1 operator kernel:
-// 32 x 16 output tile marching z over a piece [z0, z1); per input plane (one barrier):
+// block Upsilon_ik go in one pass; general bands, no Toeplitz assumption).
+// 32 x 16 output tile marching z over a piece [z0, z1) of at most KR_ZMAX planes; per input plane
+// (one barrier):
 //   - all threads stream the haloed plane HBM -> shared memory in 16-byte zero-filling cp.async
 //     pieces, KR_NPF - 1 planes ahead;
 //   - y-pass items (column, 4 rows): Y = Fy in from a register window of 4 + 2p rows into a
 //     double-buffered Y tile;
-//   - x-pass of the previous plane (lane = x, 2 rows per thread): X = Fx Y;
-//   - z: a register ring of the last 2p + 1 X planes; output plane kk - 2p ... gathered with Fz.
+//   - x-pass of the previous plane (lane = x, 2 rows per thread, the lane's Fx rows in registers):
+//     X = Fx Y;
+//   - z: a register ring of the last 2p + 1 X planes, indexed statically (the march is dispatched
+//     on the plane index mod 2p + 1, so no ring shifts); output plane kk - 2p ... gathered with the
+//     piece's alpha_t Fz_t rows, staged once in shared memory.
 // HBM traffic: in read once (halos from L2), out written once (read once when beta != 0).
-constexpr int KR_X = 32, KR_Y = 16, KR_THREADS = 256, KR_NPF = 4, KR_RY = 4;
+constexpr int KR_X = 32, KR_Y = 16, KR_THREADS = 256, KR_NPF = 4, KR_RY = 4, KR_ZMAX = 160;
 template <int P, int T>
 struct KronGeo {
     static constexpr int W = 2 * P + 1;
@@ -1175,9 +1179,11 @@ struct KronGeo {
     static constexpr int NC = KR_X + 2 * P;  // columns the x-pass needs
     static constexpr int NITEM = NC * (KR_Y / KR_RY);
     static constexpr int NPAIR = HN / 2, NSLOT = (NPAIR + KR_THREADS - 1) / KR_THREADS;
-    // shared memory (doubles): ring [NPF][HY][HX] | Y tiles [2][KR_Y][NC][T] | Fx [T][W][KR_X] | Fy [T][KR_Y][W]
-    static constexpr int RING = KR_NPF * HN, YT = 2 * KR_Y * NC * T, XB = T * W * KR_X, YB = T * KR_Y * W;
-    static constexpr int SMEM = RING + YT + XB + YB;
+    // shared memory (doubles): ring [NPF][HY][HX] | Y tiles [2][KR_Y][NC][T] | Fy [T][KR_Y][W] |
+    // alpha Fz [KR_ZMAX][W][T]
+    static constexpr int RING = KR_NPF * HN, YT = 2 * KR_Y * NC * T, YB = T * KR_Y * W, ZB = KR_ZMAX * W * T;
+    static_assert(RING % 2 == 0 && YT % 2 == 0 && (T == 1 || YB % 2 == 0), "16-byte aligned Fy / Fz tables");
+    static constexpr int SMEM = RING + YT + YB + ZB;
     static_assert(NITEM <= KR_THREADS, "one y-pass item per thread");
 };
 
@@ -1190,33 +1196,38 @@ __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__re
     extern __shared__ __align__(16) double smem[];
     double *ring = smem;
     double *Ys = smem + G::RING;  // [2][KR_Y][NC][T]
-    double *cx = Ys + G::YT;      // [T][W][KR_X]: Fx_t rows of x0 + lane (lane fastest)
-    double *cy = cx + G::XB;      // [T][KR_Y][W]: Fy_t rows of y0 + row
+    double *cy = Ys + G::YT;      // [KR_Y][W][T]: Fy_t rows of y0 + row (both terms of a tap adjacent)
+    double *fzs = cy + G::YB;     // [z1 - z0][W][T]: alpha_t Fz_t rows of the piece's output planes
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int n0 = g.n0, n1 = g.n1, n2 = g.n2;
     const long sy = g.sy, sz = g.sz;
     const int x0 = blockIdx.x * KR_X, y0 = blockIdx.y * KR_Y;
     const int z0 = blockIdx.z * zlen, z1 = min(n2, z0 + zlen);
+    for (int e = tid; e < KR_Y * W; e += KR_THREADS) {
+        const int yr = e / W, c = e % W, Y = y0 + yr;
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-        for (int e = tid; e < W * KR_X; e += KR_THREADS) {
-            const int xr = e % KR_X, c = e / KR_X, X = x0 + xr;
-            cx[t * W * KR_X + e] = X < n0 ? __ldg(k3.fx[t] + (long)X * W + c) : 0.0;
-        }
-        for (int e = tid; e < KR_Y * W; e += KR_THREADS) {
-            const int yr = e / W, c = e % W, Y = y0 + yr;
-            cy[t * KR_Y * W + e] = Y < n1 ? __ldg(k3.fy[t] + (long)Y * W + c) : 0.0;
-        }
+        for (int t = 0; t < T; ++t) cy[e * T + t] = Y < n1 ? __ldg(k3.fy[t] + (long)Y * W + c) : 0.0;
     }
+    for (int e = tid; e < (z1 - z0) * W; e += KR_THREADS) {
+        const int c = e % W, k = z0 + e / W;
+#pragma unroll
+        for (int t = 0; t < T; ++t) fzs[e * T + t] = k3.alpha[t] * __ldg(k3.fz[t] + (long)k * W + c);
+    }
+    const int X = x0 + lane, Yo = y0 + 2 * w;
+    double fxr[T][W];  // Fx_t row of this lane's column
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+#pragma unroll
+        for (int c = 0; c < W; ++c) fxr[t][c] = X < n0 ? __ldg(k3.fx[t] + (long)X * W + c) : 0.0;
     // copies: 16-byte pieces e = tid + 256 m of the [HY][HX/2] plane
     int goff[G::NSLOT];
     unsigned inr = 0;
 #pragma unroll
     for (int m = 0; m < G::NSLOT; ++m) {
         const int e = tid + m * KR_THREADS, hy = e / (HX / 2), hx = 2 * (e - hy * (HX / 2));
-        const int X = x0 - PA + hx, Y = y0 - P + hy;
-        const bool ok = e < G::NPAIR && X >= 0 && X < n0 && Y >= 0 && Y < n1;
-        goff[m] = ok ? (Y * (int)sy + X) : 0;
+        const int Xg = x0 - PA + hx, Yg = y0 - P + hy;
+        const bool ok = e < G::NPAIR && Xg >= 0 && Xg < n0 && Yg >= 0 && Yg < n1;
+        goff[m] = ok ? (Yg * (int)sy + Xg) : 0;
         if (ok) inr |= 1u << m;
     }
     const int kk0 = z0 - P, npl = z1 - z0 + 2 * P;  // input planes z0 - p .. z1 + p - 1
@@ -1239,35 +1250,30 @@ __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__re
     };
     const bool yitem = tid < G::NITEM;
     const int nc = tid % NC, grp = tid / NC, hcol = PA - P + nc;
-    const int X = x0 + lane, Yo = y0 + 2 * w;
     const bool own0 = X < n0 && Yo < n1, own1 = X < n0 && Yo + 1 < n1;
-    double r0[T][W], r1[T][W];  // X_t planes kk - 2p .. kk of rows 2w, 2w + 1 (r[.][W-1] newest)
+    double r0[T][W], r1[T][W];  // X_t planes by slot: plane q in slot q mod W
 #pragma unroll
     for (int t = 0; t < T; ++t)
 #pragma unroll
         for (int c = 0; c < W; ++c) r0[t][c] = r1[t][c] = 0.0;
-    // the epilogue's operands of output plane k (alpha_t Fz_t rows, old out when beta != 0) are
-    // loaded one plane ahead: a synchronous read-modify-write would stall every plane on DRAM
-    double fzr[T][W], ob0 = 0.0, ob1 = 0.0;
+    // the old out / addend of output plane k (beta != 0) is loaded one plane ahead: a synchronous
+    // read-modify-write would stall every plane on DRAM latency
+    double ob0 = 0.0, ob1 = 0.0;
     const long oxy = (long)Yo * sy + X;
+    const double *ad = k3.addend ? k3.addend : out;
     auto prefetch = [&](int k) {
-        if (k >= z0 && k < z1) {
-#pragma unroll
-            for (int t = 0; t < T; ++t)
-#pragma unroll
-                for (int c = 0; c < W; ++c) fzr[t][c] = k3.alpha[t] * __ldg(k3.fz[t] + (long)k * W + c);
-            if (beta != 0.0) {
-                const double *ad = k3.addend ? k3.addend : out;
-                ob0 = own0 ? ad[(long)k * sz + oxy] : 0.0;
-                ob1 = own1 ? ad[(long)k * sz + oxy + sy] : 0.0;
-            }
+        if (beta != 0.0 && k >= z0 && k < z1) {
+            ob0 = own0 ? ad[(long)k * sz + oxy] : 0.0;
+            ob1 = own1 ? ad[(long)k * sz + oxy + sy] : 0.0;
         }
     };
     prefetch(z0);
 #pragma unroll
     for (int i = 0; i < KR_NPF - 1; ++i) issue(i);
     __syncthreads();  // band rows staged
-    for (int ii = 0; ii <= npl; ++ii) {
+    // one plane step; U = slot of the x-pass plane kx = kk0 + ii - 1 (kx mod W)
+    auto plane = [&](const int ii, auto u_tag) {
+        constexpr int U = decltype(u_tag)::value;
         if (ii < npl) cp_async_wait<KR_NPF - 2>();
         __syncthreads();  // plane ii landed; Y tile (ii - 1) & 1 complete; ring slot (ii - 1) free
         issue(ii + KR_NPF - 1);
@@ -1280,59 +1286,64 @@ __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__re
 #pragma unroll
             for (int r = 0; r < KR_RY; ++r) {
                 double acc[T];
+                const double *c = cy + (KR_RY * grp + r) * W * T;
 #pragma unroll
-                for (int t = 0; t < T; ++t) {
-                    const double *c = cy + t * KR_Y * W + (KR_RY * grp + r) * W;
-                    acc[t] = 0.0;
+                for (int t = 0; t < T; ++t) acc[t] = 0.0;
 #pragma unroll
-                    for (int q = 0; q < W; ++q) acc[t] = fma(c[q], pr[r + q], acc[t]);
+                for (int q = 0; q < W; ++q) {
+                    if constexpr (T == 2) {  // both terms' tap q in one 16-byte load
+                        const double2 cq = reinterpret_cast<const double2 *>(c)[q];
+                        acc[0] = fma(cq.x, pr[r + q], acc[0]);
+                        acc[1] = fma(cq.y, pr[r + q], acc[1]);
+                    } else {
+                        acc[0] = fma(c[q], pr[r + q], acc[0]);
+                    }
                 }
                 if constexpr (T == 2) reinterpret_cast<double2 *>(yb)[r * NC] = make_double2(acc[0], acc[1]);
                 else yb[r * NC] = acc[0];
             }
         }
-        if (ii == 0) continue;
+        if (ii == 0) return;
         // x-pass of input plane kx = kk0 + ii - 1, then the z gather for output kx - p
         const int kx = kk0 + ii - 1;
         const double *yr0 = Ys + (((ii - 1) & 1) * KR_Y * NC + (2 * w) * NC + lane) * T, *yr1 = yr0 + NC * T;
-        double x0v[T], x1v[T];
 #pragma unroll
-        for (int t = 0; t < T; ++t) x0v[t] = x1v[t] = 0.0;
+        for (int t = 0; t < T; ++t) r0[t][U] = r1[t][U] = 0.0;
 #pragma unroll
         for (int c = 0; c < W; ++c) {
             if constexpr (T == 2) {
                 const double2 q0 = reinterpret_cast<const double2 *>(yr0)[c];
                 const double2 q1 = reinterpret_cast<const double2 *>(yr1)[c];
-                const double f0 = cx[c * KR_X + lane], f1 = cx[W * KR_X + c * KR_X + lane];
-                x0v[0] = fma(f0, q0.x, x0v[0]);
-                x1v[0] = fma(f0, q1.x, x1v[0]);
-                x0v[T - 1] = fma(f1, q0.y, x0v[T - 1]);
-                x1v[T - 1] = fma(f1, q1.y, x1v[T - 1]);
+                r0[0][U] = fma(fxr[0][c], q0.x, r0[0][U]);
+                r1[0][U] = fma(fxr[0][c], q1.x, r1[0][U]);
+                r0[T - 1][U] = fma(fxr[T - 1][c], q0.y, r0[T - 1][U]);
+                r1[T - 1][U] = fma(fxr[T - 1][c], q1.y, r1[T - 1][U]);
             } else {
-                const double f = cx[c * KR_X + lane];
-                x0v[0] = fma(f, yr0[c], x0v[0]);
-                x1v[0] = fma(f, yr1[c], x1v[0]);
+                r0[0][U] = fma(fxr[0][c], yr0[c], r0[0][U]);
+                r1[0][U] = fma(fxr[0][c], yr1[c], r1[0][U]);
             }
         }
-#pragma unroll
-        for (int t = 0; t < T; ++t) {
-#pragma unroll
-            for (int c = 0; c < W - 1; ++c) {
-                r0[t][c] = r0[t][c + 1];
-                r1[t][c] = r1[t][c + 1];
-            }
-            r0[t][W - 1] = x0v[t];
-            r1[t][W - 1] = x1v[t];
-        }
-        const int k = kx - P;  // rings hold planes k - p .. k + p
+        const int k = kx - P;  // slots hold planes k - p .. k + p: plane k - p + c in slot (U + 1 + c) mod W
         if (k >= z0 && k < z1) {
+            const double *fz = fzs + (k - z0) * W * T;
+            double fzr[T][W];
+#pragma unroll
+            for (int c = 0; c < W; ++c) {
+                if constexpr (T == 2) {
+                    const double2 f = reinterpret_cast<const double2 *>(fz)[c];
+                    fzr[0][c] = f.x;
+                    fzr[1][c] = f.y;
+                } else {
+                    fzr[0][c] = fz[c];
+                }
+            }
             double a0 = 0.0, a1 = 0.0;
 #pragma unroll
             for (int t = 0; t < T; ++t)
 #pragma unroll
                 for (int c = 0; c < W; ++c) {
-                    a0 = fma(fzr[t][c], r0[t][c], a0);
-                    a1 = fma(fzr[t][c], r1[t][c], a1);
+                    a0 = fma(fzr[t][c], r0[t][(U + 1 + c) % W], a0);
+                    a1 = fma(fzr[t][c], r1[t][(U + 1 + c) % W], a1);
                 }
             double *o = out + (long)k * sz + oxy;
             const double w0 = beta == 0.0 ? a0 : fma(beta, ob0, a0);
@@ -1341,12 +1352,24 @@ __global__ void __launch_bounds__(KR_THREADS, 2) kron3_kernel(const double *__re
             if (own0) o[0] = w0;
             if (own1) o[sy] = w1;
         }
+    };
+    int u = ((kk0 - 1) % W + W) % W;  // slot of plane kk0 + ii - 1
+    for (int ii = 0; ii <= npl; ++ii, u = u + 1 == W ? 0 : u + 1) {
+        switch (u) {
+#define ADS_KRC(V)                                                                     \
+    case V:                                                                            \
+        if constexpr (V < W) plane(ii, std::integral_constant<int, V>{});              \
+        break;
+            ADS_KRC(0) ADS_KRC(1) ADS_KRC(2) ADS_KRC(3) ADS_KRC(4) ADS_KRC(5)
+            ADS_KRC(6) ADS_KRC(7) ADS_KRC(8) ADS_KRC(9) ADS_KRC(10)
+#undef ADS_KRC
+        }
     }
 }
 
 template <int P, int T>
-static void kron3_launch(const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
-                         cudaStream_t s) {
+static int kron3_launch(const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
+                        cudaStream_t s) {
     using G = KronGeo<P, T>;
     const size_t sm = sizeof(double) * G::SMEM;
     const LaunchFacts lf = launch_facts((const void *)kron3_kernel<P, T>, KR_THREADS, sm);
@@ -1357,6 +1380,7 @@ static void kron3_launch(const double *in, double *out, const KronTerms &k3, dou
     double best_cost = 1e300;
     for (int nz = 1; nz <= 64; ++nz) {
         const int zl = (g.n2 + nz - 1) / nz;
+        if (zl > KR_ZMAX) continue;  // the piece's Fz rows are staged in shared memory
         if (zl < 2 * P + 1 && nz > 1) break;
         const long ctas = tiles * ((g.n2 + zl - 1) / zl);
         const double cost = (ctas <= resident ? 1.0 : (double)ctas / resident + 0.5) * (zl + 2.0 * P);
@@ -1368,28 +1392,26 @@ static void kron3_launch(const double *in, double *out, const KronTerms &k3, dou
     }();
     if (nz_env > 0) best = nz_env;
     const int zlen = (g.n2 + best - 1) / best;
+    if (zlen > KR_ZMAX) return -1;
     dim3 grd(gx, gy, (g.n2 + zlen - 1) / zlen);
     kron3_kernel<P, T><<<grd, KR_THREADS, sm, s>>>(in, out, k3, beta, g, zlen);
+    return 0;
 }
 
 template <int P>
 static int kron3_dispatch(const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
                           cudaStream_t s) {
-    if (k3.nterms == 1) {
-        kron3_launch<P, 1>(in, out, k3, beta, g, s);
-        return 0;
-    }
+    if (k3.nterms == 1) return kron3_launch<P, 1>(in, out, k3, beta, g, s);
     if constexpr (P <= 3) {  // two terms in one pass (registers: two gather rings)
-        kron3_launch<P, 2>(in, out, k3, beta, g, s);
+        return kron3_launch<P, 2>(in, out, k3, beta, g, s);
     } else {  // two passes, the second accumulating
         KronTerms a = k3, b = k3;
         a.nterms = b.nterms = 1;
         b.addend = nullptr;  // the second pass accumulates onto the first
         b.fx[0] = k3.fx[1], b.fy[0] = k3.fy[1], b.fz[0] = k3.fz[1], b.alpha[0] = k3.alpha[1];
-        kron3_launch<P, 1>(in, out, a, beta, g, s);
-        kron3_launch<P, 1>(in, out, b, 1.0, g, s);
+        if (kron3_launch<P, 1>(in, out, a, beta, g, s)) return -1;
+        return kron3_launch<P, 1>(in, out, b, 1.0, g, s);
     }
-    return 0;
 }
 
 int launch_kron3(int p, const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
