@@ -49,6 +49,9 @@ FALLBACK_HBM_GBS = 6650.0
 KERNELS = ["kop", "sweep_x", "sweep_y", "sweep_z_kick"]
 C4_DOFS = 515 ** 3  # the committed traffic captures are of config c4 on one GPU
 ELASTIC_STEP_BYTES = 176.0  # elasticity bytes per vector DOF and step (estimate)
+# the elastic step as built, per DOF: diagonal blocks 32, coupling pairs 2 x 24,
+# six ADS solves 2 x 3 x 16, predictor/corrector couplings 2 x 24, rho M 16, kick 24
+ELASTIC_PLAN_BYTES = 264.0
 
 
 def peaks():
@@ -319,8 +322,11 @@ def run_ours(args, rank, world, local):
         roofline = {"bound": "hbm", "kernel": "elastic step (all launches)", "achieved": achieved, "peak": hbm,
                     "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
                     "algorithmic_bytes": step_bytes / 1e9, "step_bytes_per_dof": ELASTIC_STEP_BYTES,
+                    "plan_bytes_per_dof": ELASTIC_PLAN_BYTES,
+                    "plan_frac": ELASTIC_PLAN_BYTES * N / (ms / args.steps / 1e3) / 1e9 / hbm,
                     "note": "SURVEY.md §8(d) estimate: 170-180 B per vector DOF and step (6 ADS solves, "
-                            "Kronecker triples); c5 fields (17.6 MB per component) are L2-resident"}
+                            "Kronecker triples); the step as built moves 264 B per DOF (DESIGN.md §7); "
+                            "c5 fields (17.6 MB per component) are L2-resident"}
     else:
         shares = kms / kms.sum() if kms.sum() > 0 else kms
         dom = int(np.argmax(kms))

@@ -128,6 +128,14 @@ struct ads_ctx {
     cudaStream_t side[2] = {nullptr, nullptr};
     cudaEvent_t fev[8] = {};
     std::vector<void *> allocs;
+    // bands whose interior rows are one row bitwise (device pointer -> rows [lo, hi], the row):
+    // the Kronecker kernel takes a tile's y-pass coefficients from its parameters there
+    struct ToepRow {
+        const double *dev;
+        int lo, hi;
+        double row[2 * kMaxP + 1];
+    };
+    std::vector<ToepRow> toep;
     // profiling (ads_profile_enable): event pairs per kernel class
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -386,6 +394,22 @@ int build_slab_tables(ads_ctx *h, const Band &A) {
     return ADS_OK;
 }
 
+// rows of a band [n][2p+1] equal to its middle row bitwise: the largest range around the middle
+void note_toeplitz(ads_ctx *h, const double *dev, const std::vector<double> &b, int n) {
+    const int W = 2 * h->p + 1, mid = n / 2;
+    auto same = [&](int i) {
+        for (int c = 0; c < W; ++c)
+            if (b[(size_t)i * W + c] != b[(size_t)mid * W + c]) return false;
+        return true;
+    };
+    ads_ctx::ToepRow r{dev, mid, mid, {}};
+    while (r.lo > 0 && same(r.lo - 1)) --r.lo;
+    while (r.hi < n - 1 && same(r.hi + 1)) ++r.hi;
+    for (int c = 0; c < W; ++c) r.row[c] = b[(size_t)mid * W + c];
+    if (n < 3) r.lo = 1, r.hi = 0;
+    h->toep.push_back(r);
+}
+
 int build_direction(ads_ctx *h, int d) {
     Space1D &s = h->sp[d];
     const int p = h->p;
@@ -451,12 +475,17 @@ int build_direction(ads_ctx *h, int d) {
         if ((rc = upload(h, &D.bband, s.B.v)) || (rc = upload(h, &D.btband, BT.v)) ||
             (rc = upload(h, &D.slband, SLa.v)) || (rc = upload(h, &D.ssband, SSa.v)))
             return rc;
+        note_toeplitz(h, D.bband, s.B.v, n);
+        note_toeplitz(h, D.btband, BT.v, n);
+        note_toeplitz(h, D.slband, SLa.v, n);
+        note_toeplitz(h, D.ssband, SSa.v, n);
     }
     std::vector<double> mb(s.M.v), kb(s.K.v), wz;
     diff_weights(s, wz);
     if (D.t_hi > D.t_lo)
         for (int m = 0; m < 2 * p; ++m) D.wzrow[m] = wz[(size_t)D.t_lo * 2 * p + m];
     if ((rc = upload(h, &D.mband, mb)) || (rc = upload(h, &D.kband, kb)) || (rc = upload(h, &D.wzband, wz))) return rc;
+    note_toeplitz(h, D.mband, mb, n);
     return ADS_OK;
 }
 
@@ -686,11 +715,23 @@ int init_state(ads_ctx *h) {
 // ---------------------------------------------------------------------------------------
 double *comp(double *f, const ads_ctx *h, int c) { return f + (long)c * h->Nalloc; }
 
+// Kronecker y factors: the Toeplitz interior of each Fy_t (ads_ctx::toep) into the kernel arguments
+void set_yrows(const ads_ctx *h, KronTerms &k3) {
+    for (int t = 0; t < k3.nterms; ++t)
+        for (const auto &r : h->toep)
+            if (r.dev == k3.fy[t]) {
+                k3.fylo[t] = r.lo;
+                k3.fyhi[t] = r.hi;
+                for (int c = 0; c < 2 * h->p + 1; ++c) k3.fyrow[t][c] = r.row[c];
+            }
+}
+
 // out = alpha (Fx (x) Fy (x) Fz) in + beta out   (Fd: band [n_d][2p+1], acting along d)
 int tri(ads_ctx *h, double *out, const double *in, const double *fx, const double *fy, const double *fz,
         double alpha, double beta) {
     KronTerms k3;
     k3.fx[0] = fx, k3.fy[0] = fy, k3.fz[0] = fz, k3.alpha[0] = alpha;
+    set_yrows(h, k3);
     if (launch_kron3(h->p, in, out, k3, beta, h->geo, h->stream)) return fail(h, ADS_E_INVAL, "kron3: unsupported p");
     return check_launch(h, "kron3");
 }
@@ -709,6 +750,7 @@ int ups_offdiag(ads_ctx *h, int i, int k, const double *in, double *out, double 
     }
     k3.alpha[0] = coef * h->mu;
     k3.alpha[1] = coef * h->lam;
+    set_yrows(h, k3);
     if (launch_kron3(h->p, in, out, k3, 1.0, h->geo, h->stream)) return fail(h, ADS_E_INVAL, "kron3: unsupported p");
     return check_launch(h, "kron3");
 }

@@ -183,6 +183,10 @@ struct KronTerms {
     const double *fx[2] = {nullptr, nullptr}, *fy[2] = {nullptr, nullptr}, *fz[2] = {nullptr, nullptr};
     double alpha[2] = {0.0, 0.0};
     const double *addend = nullptr;  // beta multiplies this field instead of out (nullptr: out)
+    // rows [fylo[t], fyhi[t]] of Fy_t are the row fyrow[t] bitwise (uniform-mesh interior): tiles
+    // inside take the y-pass coefficients from the kernel parameters (lo > hi: none)
+    int fylo[2] = {1, 1}, fyhi[2] = {0, 0};
+    double fyrow[2][2 * kMaxP + 1] = {};
 };
 int launch_kron3(int p, const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
                  cudaStream_t s);

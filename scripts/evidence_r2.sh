@@ -16,5 +16,8 @@ timeout 300 python scripts/time_kernels.py c3 c4 > gpurun_out/kernels_$T.log 2>&
 timeout 300 python scripts/time_slabs.py c4 > gpurun_out/slabs_$T.log 2>&1
 timeout 300 python scripts/time_setstate.py c4 > gpurun_out/setstate_$T.log 2>&1
 timeout 300 python scripts/time_modal.py > gpurun_out/modal_$T.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:kron3_kernel -s 14 -c 1 -o gpurun_out/kron3_$T -f python scripts/prof_c5_scaled.py 256 > gpurun_out/ncu_kron3_$T.log 2>&1
+timeout 900 python scripts/time_elastic_scaled.py 128 256 512 > gpurun_out/el_scaled_$T.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/c5x512_launches_$T.csv python scripts/prof_c5_scaled.py 512 > /dev/null 2>&1
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$T.txt 2>&1; echo rc=$? >> gpurun_out/pytest_gpu_$T.txt
 tail -3 gpurun_out/pytest_gpu_$T.txt; tail -2 gpurun_out/smoke_$T.log; cat gpurun_out/configs_$T.log gpurun_out/kernels_$T.log

@@ -21,6 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6533.5
 BYTES = 176.0
+PLAN = 264.0  # the step as built
 
 
 def rel(a, b):
@@ -52,9 +53,11 @@ for nel in [int(v) for v in sys.argv[1:]] or [128, 256, 512]:
     nsteps = 3 + 3 * K
     dof = wl.ndof
     frac = BYTES * dof / (best * 1e-3) / 1e9 / PEAK
+    pfrac = PLAN * dof / (best * 1e-3) / 1e9 / PEAK
     drift = abs(e_end[2] - e_start[2]) / e_start[2]
     print(f"c5@{nel}: {dof} DOFs ({dof // 3} per component), setup {t_setup:.1f} s, {best:.3f} ms/step, "
           f"{dof / (best * 1e-3):.3e} DOF-steps/s, {frac:.3f} of HBM on {BYTES:.0f} B/DOF ({PEAK} GB/s), "
+          f"{pfrac:.3f} on the {PLAN:.0f} B/DOF the step moves, "
           f"{lps:.0f} launches/step; invariant over {nsteps} steps: {e_start[2]:.12e} -> {e_end[2]:.12e} "
           f"(rel {drift:.2e})", flush=True)
     del s
