@@ -20,4 +20,12 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:kron
 timeout 900 python scripts/time_elastic_scaled.py 128 256 512 > gpurun_out/el_scaled_$T.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/c5x512_launches_$T.csv python scripts/prof_c5_scaled.py 512 > /dev/null 2>&1
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$T.txt 2>&1; echo rc=$? >> gpurun_out/pytest_gpu_$T.txt
+# summaries on the box; the full reports stay there (gpurun_out/ must stay under 64 MiB)
+python scripts/ncu_summary.py gpurun_out/prof_$T.ncu-rep > gpurun_out/ncu_summary_kop_$T.md 2>&1
+python scripts/ncu_lines.py gpurun_out/prof_$T.ncu-rep kop4_kernelILi3 30 > gpurun_out/ncu_lines_kop_$T.txt 2>&1
+python scripts/ncu_summary.py gpurun_out/kron3_$T.ncu-rep > gpurun_out/ncu_summary_kron3_$T.md 2>&1
+python scripts/ncu_lines.py gpurun_out/kron3_$T.ncu-rep kron3_kernelILi2ELi2E 30 > gpurun_out/ncu_lines_kron3_$T.txt 2>&1
+python scripts/launch_agg.py gpurun_out/c5x512_launches_$T.csv 37 > gpurun_out/c5x512_table_$T.txt 2>&1
+rm -f gpurun_out/*.ncu-rep gpurun_out/c5x512_launches_$T.csv
+du -sh gpurun_out
 tail -3 gpurun_out/pytest_gpu_$T.txt; tail -2 gpurun_out/smoke_$T.log; cat gpurun_out/configs_$T.log gpurun_out/kernels_$T.log
