@@ -46,6 +46,10 @@ OP_CASES = [
     ((6, 13, 5), 3, 0, 1.3, 0.7, 1.2, 0.05),
     ((40, 5, 6), 1, 1, 0.0, 2.0, 0.5, 0.3),
     ((3, 3, 3), 2, 0, 2.0, 0.5, 1.0, 1.0),
+    # grids with Kronecker tiles inside the Toeplitz interior of every F_y (the coefficient-from-
+    # parameters path of kron3_kernel) next to boundary tiles, and z pieces with staged F_z rows
+    ((40, 40, 12), 2, 1, 1.0, 1.0, 1.0, 1e-3),
+    ((20, 52, 33), 3, 0, 0.8, 1.1, 1.3, 2e-2),
 ]
 
 
