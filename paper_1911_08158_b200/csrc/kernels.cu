@@ -1188,16 +1188,20 @@ struct KronGeo {
 };
 
 // T terms sharing the input and the output: out = beta out + sum_t alpha_t (Fx_t (x) Fy_t (x) Fz_t) in
-template <int P, int T, bool YT>
+// SH (pairs): a factor both terms share, detected on the host by band identity: 1 = F_y (one y
+// product Y, both x products from it), 2 = F_z (alpha_t folded into F_x: one ring X = sum_t alpha_t
+// F_x,t Y_t and one gather); 0 = none.  TY / TZ: y products / z rings per point.
+template <int P, int T, bool YT, int SH>
 __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double *__restrict__ out, const KronTerms &k3,
                                            double beta, const Geom &g, int zlen) {
     using G = KronGeo<P, T>;
     constexpr int W = G::W, HX = G::HX, HN = G::HN, NC = G::NC, PA = G::PA;
+    constexpr int TY = SH == 1 ? 1 : T, TZ = SH == 2 ? 1 : T;
     extern __shared__ __align__(16) double smem[];
     double *ring = smem;
-    double *Ys = smem + G::RING;  // [2][KR_Y][NC][T]
+    double *Ys = smem + G::RING;  // [2][KR_Y][NC][TY]
     double *cy = Ys + G::YT;      // [KR_Y][W][T]: Fy_t rows of y0 + row (both terms of a tap adjacent)
-    double *fzs = cy + G::YB;     // [z1 - z0][W][T]: alpha_t Fz_t rows of the piece's output planes
+    double *fzs = cy + G::YB;     // [z1 - z0][W][TZ]: alpha_t Fz_t rows of the piece's output planes (SH 2: Fz)
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int n0 = g.n0, n1 = g.n1, n2 = g.n2;
     const long sy = g.sy, sz = g.sz;
@@ -1211,14 +1215,15 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
     for (int e = tid; e < (z1 - z0) * W; e += KR_THREADS) {
         const int c = e % W, k = z0 + e / W;
 #pragma unroll
-        for (int t = 0; t < T; ++t) fzs[e * T + t] = k3.alpha[t] * __ldg(k3.fz[t] + (long)k * W + c);
+        for (int t = 0; t < TZ; ++t)
+            fzs[e * TZ + t] = (SH == 2 ? 1.0 : k3.alpha[t]) * __ldg(k3.fz[t] + (long)k * W + c);
     }
     const int X = x0 + lane, Yo = y0 + 2 * w;
     double fxr[T][W];  // Fx_t row of this lane's column
 #pragma unroll
     for (int t = 0; t < T; ++t)
 #pragma unroll
-        for (int c = 0; c < W; ++c) fxr[t][c] = X < n0 ? __ldg(k3.fx[t] + (long)X * W + c) : 0.0;
+        for (int c = 0; c < W; ++c) fxr[t][c] = X < n0 ? (SH == 2 ? k3.alpha[t] : 1.0) * __ldg(k3.fx[t] + (long)X * W + c) : 0.0;
     // copies: 16-byte pieces e = tid + 256 m of the [HY][HX/2] plane
     int goff[G::NSLOT];
     unsigned inr = 0;
@@ -1251,9 +1256,9 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
     const bool yitem = tid < G::NITEM;
     const int nc = tid % NC, grp = tid / NC, hcol = PA - P + nc;
     const bool own0 = X < n0 && Yo < n1, own1 = X < n0 && Yo + 1 < n1;
-    double r0[T][W], r1[T][W];  // X_t planes by slot: plane q in slot q mod W
+    double r0[TZ][W], r1[TZ][W];  // X_t planes by slot: plane q in slot q mod W
 #pragma unroll
-    for (int t = 0; t < T; ++t)
+    for (int t = 0; t < TZ; ++t)
 #pragma unroll
         for (int c = 0; c < W; ++c) r0[t][c] = r1[t][c] = 0.0;
     // the old out / addend of output plane k (beta != 0) is loaded one plane ahead: a synchronous
@@ -1282,39 +1287,52 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
             double pr[KR_RY + 2 * P];
 #pragma unroll
             for (int r = 0; r < KR_RY + 2 * P; ++r) pr[r] = b[r * HX];
-            double *yb = Ys + ((ii & 1) * KR_Y * NC + KR_RY * grp * NC + nc) * T;
+            double *yb = Ys + ((ii & 1) * KR_Y * NC + KR_RY * grp * NC + nc) * TY;
 #pragma unroll
             for (int r = 0; r < KR_RY; ++r) {
-                double acc[T];
+                double acc[TY];
                 [[maybe_unused]] const double *c = cy + (KR_RY * grp + r) * W * T;
 #pragma unroll
-                for (int t = 0; t < T; ++t) acc[t] = 0.0;
+                for (int t = 0; t < TY; ++t) acc[t] = 0.0;
 #pragma unroll
                 for (int q = 0; q < W; ++q) {
                     if constexpr (YT) {  // Toeplitz rows: the coefficients are kernel parameters
 #pragma unroll
-                        for (int t = 0; t < T; ++t) acc[t] = fma(k3.fyrow[t][q], pr[r + q], acc[t]);
-                    } else if constexpr (T == 2) {  // both terms' tap q in one 16-byte load
+                        for (int t = 0; t < TY; ++t) acc[t] = fma(k3.fyrow[t][q], pr[r + q], acc[t]);
+                    } else if constexpr (TY == 2) {  // both terms' tap q in one 16-byte load
                         const double2 cq = reinterpret_cast<const double2 *>(c)[q];
                         acc[0] = fma(cq.x, pr[r + q], acc[0]);
                         acc[1] = fma(cq.y, pr[r + q], acc[1]);
                     } else {
-                        acc[0] = fma(c[q], pr[r + q], acc[0]);
+                        acc[0] = fma(c[q * T], pr[r + q], acc[0]);
                     }
                 }
-                if constexpr (T == 2) reinterpret_cast<double2 *>(yb)[r * NC] = make_double2(acc[0], acc[1]);
+                if constexpr (TY == 2) reinterpret_cast<double2 *>(yb)[r * NC] = make_double2(acc[0], acc[1]);
                 else yb[r * NC] = acc[0];
             }
         }
         if (ii == 0) return;
         // x-pass of input plane kx = kk0 + ii - 1, then the z gather for output kx - p
         const int kx = kk0 + ii - 1;
-        const double *yr0 = Ys + (((ii - 1) & 1) * KR_Y * NC + (2 * w) * NC + lane) * T, *yr1 = yr0 + NC * T;
+        const double *yr0 = Ys + (((ii - 1) & 1) * KR_Y * NC + (2 * w) * NC + lane) * TY, *yr1 = yr0 + NC * TY;
 #pragma unroll
-        for (int t = 0; t < T; ++t) r0[t][U] = r1[t][U] = 0.0;
+        for (int t = 0; t < TZ; ++t) r0[t][U] = r1[t][U] = 0.0;
 #pragma unroll
         for (int c = 0; c < W; ++c) {
-            if constexpr (T == 2) {
+            if constexpr (SH == 1) {  // one Y, both x products
+                const double q0 = yr0[c], q1 = yr1[c];
+                r0[0][U] = fma(fxr[0][c], q0, r0[0][U]);
+                r1[0][U] = fma(fxr[0][c], q1, r1[0][U]);
+                r0[1][U] = fma(fxr[1][c], q0, r0[1][U]);
+                r1[1][U] = fma(fxr[1][c], q1, r1[1][U]);
+            } else if constexpr (SH == 2) {  // both terms into one ring (alpha_t in F_x,t)
+                const double2 q0 = reinterpret_cast<const double2 *>(yr0)[c];
+                const double2 q1 = reinterpret_cast<const double2 *>(yr1)[c];
+                r0[0][U] = fma(fxr[0][c], q0.x, r0[0][U]);
+                r1[0][U] = fma(fxr[0][c], q1.x, r1[0][U]);
+                r0[0][U] = fma(fxr[1][c], q0.y, r0[0][U]);
+                r1[0][U] = fma(fxr[1][c], q1.y, r1[0][U]);
+            } else if constexpr (T == 2) {
                 const double2 q0 = reinterpret_cast<const double2 *>(yr0)[c];
                 const double2 q1 = reinterpret_cast<const double2 *>(yr1)[c];
                 r0[0][U] = fma(fxr[0][c], q0.x, r0[0][U]);
@@ -1328,11 +1346,11 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
         }
         const int k = kx - P;  // slots hold planes k - p .. k + p: plane k - p + c in slot (U + 1 + c) mod W
         if (k >= z0 && k < z1) {
-            const double *fz = fzs + (k - z0) * W * T;
-            double fzr[T][W];
+            const double *fz = fzs + (k - z0) * W * TZ;
+            double fzr[TZ][W];
 #pragma unroll
             for (int c = 0; c < W; ++c) {
-                if constexpr (T == 2) {
+                if constexpr (TZ == 2) {
                     const double2 f = reinterpret_cast<const double2 *>(fz)[c];
                     fzr[0][c] = f.x;
                     fzr[1][c] = f.y;
@@ -1342,7 +1360,7 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
             }
             double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-            for (int t = 0; t < T; ++t)
+            for (int t = 0; t < TZ; ++t)
 #pragma unroll
                 for (int c = 0; c < W; ++c) {
                     a0 = fma(fzr[t][c], r0[t][(U + 1 + c) % W], a0);
@@ -1372,23 +1390,23 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
 
 // single triples fit 3 CTAs per SM without spills up to p = 3 (measured 8 % faster at c5@512);
 // pairs spill at 80 registers and keep 2
-template <int P, int T>
+template <int P, int T, int SH>
 __global__ void __launch_bounds__(KR_THREADS, (T == 1 && P <= 3) ? 3 : 2) kron3_kernel(const double *__restrict__ in, double *__restrict__ out,
                                                                const KronTerms k3, double beta, Geom g, int zlen) {
     const int y0 = blockIdx.y * KR_Y;
     bool yt = true;
 #pragma unroll
     for (int t = 0; t < T; ++t) yt = yt && y0 >= k3.fylo[t] && y0 + KR_Y - 1 <= k3.fyhi[t];
-    if (yt) kron3_tile<P, T, true>(in, out, k3, beta, g, zlen);
-    else kron3_tile<P, T, false>(in, out, k3, beta, g, zlen);
+    if (yt) kron3_tile<P, T, true, SH>(in, out, k3, beta, g, zlen);
+    else kron3_tile<P, T, false, SH>(in, out, k3, beta, g, zlen);
 }
 
-template <int P, int T>
+template <int P, int T, int SH = 0>
 static int kron3_launch(const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
                         cudaStream_t s) {
     using G = KronGeo<P, T>;
     const size_t sm = sizeof(double) * G::SMEM;
-    const LaunchFacts lf = launch_facts((const void *)kron3_kernel<P, T>, KR_THREADS, sm);
+    const LaunchFacts lf = launch_facts((const void *)kron3_kernel<P, T, SH>, KR_THREADS, sm);
     const int gx = (g.n0 + KR_X - 1) / KR_X, gy = (g.n1 + KR_Y - 1) / KR_Y;
     // z pieces by the fluid wave model of kop_launch (each piece reads 2p halo planes)
     const long resident = (long)lf.per_sm * lf.nsm, tiles = (long)gx * gy;
@@ -1410,7 +1428,7 @@ static int kron3_launch(const double *in, double *out, const KronTerms &k3, doub
     const int zlen = (g.n2 + best - 1) / best;
     if (zlen > KR_ZMAX) return -1;
     dim3 grd(gx, gy, (g.n2 + zlen - 1) / zlen);
-    kron3_kernel<P, T><<<grd, KR_THREADS, sm, s>>>(in, out, k3, beta, g, zlen);
+    kron3_kernel<P, T, SH><<<grd, KR_THREADS, sm, s>>>(in, out, k3, beta, g, zlen);
     return 0;
 }
 
@@ -1419,7 +1437,13 @@ static int kron3_dispatch(const double *in, double *out, const KronTerms &k3, do
                           cudaStream_t s) {
     if (k3.nterms == 1) return kron3_launch<P, 1>(in, out, k3, beta, g, s);
     if constexpr (P <= 3) {  // two terms in one pass (registers: two gather rings)
-        return kron3_launch<P, 2>(in, out, k3, beta, g, s);
+        static const bool share = [] {  // experiment switch (scripts/): ADS_KRON_SHARE=0 off
+            const char *e = std::getenv("ADS_KRON_SHARE");
+            return !(e && e[0] == '0');
+        }();
+        if (share && k3.fz[0] == k3.fz[1]) return kron3_launch<P, 2, 2>(in, out, k3, beta, g, s);
+        if (share && k3.fy[0] == k3.fy[1]) return kron3_launch<P, 2, 1>(in, out, k3, beta, g, s);
+        return kron3_launch<P, 2, 0>(in, out, k3, beta, g, s);
     } else {  // two passes, the second accumulating
         KronTerms a = k3, b = k3;
         a.nterms = b.nterms = 1;
