@@ -558,6 +558,7 @@ int run_kop(ads_ctx *h, const double *U, const double *V, double tau_d, double g
         }
     }
     a.wz = h->dd[2].wzband;
+    a.pdl = h->ncomp == 3;  // the elastic step launches with programmatic dependencies
     if (h->sp[2].bc == ADS_BC_DIRICHLET0) {
         a.zd0 = 0;
         a.zd1 = h->ngz - 1;
@@ -582,6 +583,7 @@ int run_sweep_tab(ads_ctx *h, int d, const SolveTab &tab, const double *in, doub
     a.geo = geo ? *geo : h->geo;
     a.dir = d;
     a.mode = V ? 1 : 0;
+    a.pdl = h->ncomp == 3;
     ProfScope ps(h, 1 + d);
     if (tab.n == 1) {  // the 2D axis: a 1 x 1 system per line (P-wave A_z = M_z + eta K_z = 1)
         const double a00 = h->sp[d].M.get(0, 0) + 0.25 * h->tau * h->tau * h->sp[d].K.get(0, 0);
@@ -854,7 +856,7 @@ int el_step(ads_ctx *h) {
     int rc;
     if ((rc = ups_apply(h, h->U, h->V, h->tau, h->U2, h->A, -1.0))) return rc;
     if ((rc = el_dsolve(h, h->A))) return rc;
-    launch_axpby(3 * h->Nalloc, h->tau, h->A, 1.0, h->V, h->stream);
+    launch_axpby(3 * h->Nalloc, h->tau, h->A, 1.0, h->V, h->stream, true);
     if ((rc = check_launch(h, "axpby"))) return rc;
     std::swap(h->U, h->U2);
     return ADS_OK;

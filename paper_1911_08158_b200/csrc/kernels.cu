@@ -32,6 +32,14 @@
 
 namespace ads {
 
+// Programmatic dependent launch (sm_90+): the step's kernels are launched with programmatic stream
+// serialisation (launch_pdl), let their successor launch as soon as they start, and wait for their
+// predecessor's completion (and memory flush) before touching any field the step reads or writes;
+// only constant tables are staged before the wait, so the successor's launch and prologue overlap
+// the predecessor's tail.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // Per-device launch facts of a kernel at a dynamic shared-memory size, cached and thread-safe:
 // the SM count, the resident CTAs per SM, and the >48 KB opt-in (raised to the largest size the
 // kernel has been launched with on that device).
@@ -296,6 +304,7 @@ __global__ void __launch_bounds__(SW<LW, C>::THREADS, 512 / SW<LW, C>::THREADS)
     constexpr int SW_LW = LW, SW_G = SW<LW, C>::G, SW_THREADS = SW<LW, C>::THREADS;
     extern __shared__ __align__(16) double smem[];
     constexpr int FW = Rec<P>::FW, BW = Rec<P>::BW;
+    pdl_launch_dependents();
     const SolveTab &t = a.t;
     const int nedge = sweep_edge_rows(t);
     double *shTf = smem, *shRb = shTf + C * P * P;
@@ -329,6 +338,7 @@ __global__ void __launch_bounds__(SW<LW, C>::THREADS, 512 / SW<LW, C>::THREADS)
     const bool walk_ub = uni && (w + 1) * SW_G - 1 + t.Kb < t.c_hi;
     const SweepSmem sm{shTf, shRb, ef, eb, shf, shb};
     const Geom &g = a.geo;
+    pdl_wait();  // fields (and the step counter) from here on
     auto solve = [&](double (&v)[L], auto after) {
         if (uni) solve_chunk<P, L, LW, true>(v, t, sm, c, q, walk_uf, walk_ub, recf, recb, after);
         else solve_chunk<P, L, LW, false>(v, t, sm, c, q, false, false, recf, recb, after);
@@ -764,6 +774,7 @@ __device__ __forceinline__ void kop4_tile(const KopArgs &a, const CUtensorMap *t
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(mb) : "memory");
         }
     };
+    pdl_wait();  // fields (U, V, dstep) from here on
     if (tid == 0)
         for (int i = 0; i < K4_NPF - 1; ++i) issue(i);
 
@@ -1009,6 +1020,7 @@ template <int P>
 __global__ void __launch_bounds__(K4_THREADS, P <= 3 ? 2 : 1)
     kop4_kernel(const KopArgs a, const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmv,
                 const __grid_constant__ CUtensorMap tmp) {
+    pdl_launch_dependents();
     // TMA staging needs 128-byte alignment of the dynamic shared memory window
     const int sh = (int)(((128 - (__cvta_generic_to_shared(k4_smem) & 127)) & 127) / sizeof(double));
     const int x0 = kop_origin(a.ilo[0], a.ihi[0], K4_X) + (int)blockIdx.x * K4_X;
@@ -1272,6 +1284,7 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
             ob1 = own1 ? ad[(long)k * sz + oxy + sy] : 0.0;
         }
     };
+    pdl_wait();  // fields from here on
     prefetch(z0);
 #pragma unroll
     for (int i = 0; i < KR_NPF - 1; ++i) issue(i);
@@ -1393,12 +1406,38 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
 template <int P, int T, int SH>
 __global__ void __launch_bounds__(KR_THREADS, (T == 1 && P <= 3) ? 3 : 2) kron3_kernel(const double *__restrict__ in, double *__restrict__ out,
                                                                const KronTerms k3, double beta, Geom g, int zlen) {
+    pdl_launch_dependents();
     const int y0 = blockIdx.y * KR_Y;
     bool yt = true;
 #pragma unroll
     for (int t = 0; t < T; ++t) yt = yt && y0 >= k3.fylo[t] && y0 + KR_Y - 1 <= k3.fyhi[t];
     if (yt) kron3_tile<P, T, true, SH>(in, out, k3, beta, g, zlen);
     else kron3_tile<P, T, false, SH>(in, out, k3, beta, g, zlen);
+}
+
+// launch with programmatic stream serialisation when `pdl` (the kernel calls pdl_wait before
+// touching the fields); ADS_PDL=0 launches plainly (experiment switch).  Used for the elastic step
+// (c5: 793 -> 771 us/step); the P-wave steps measured 1-5 % slower with it and launch plainly.
+static bool pdl_on() {
+    static const bool on = [] {
+        const char *e = std::getenv("ADS_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+template <class... KArgs, class... Args>
+static void launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl && pdl_on() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
 template <int P, int T, int SH = 0>
@@ -1428,7 +1467,7 @@ static int kron3_launch(const double *in, double *out, const KronTerms &k3, doub
     const int zlen = (g.n2 + best - 1) / best;
     if (zlen > KR_ZMAX) return -1;
     dim3 grd(gx, gy, (g.n2 + zlen - 1) / zlen);
-    kron3_kernel<P, T, SH><<<grd, KR_THREADS, sm, s>>>(in, out, k3, beta, g, zlen);
+    launch_pdl(true, kron3_kernel<P, T, SH>, grd, dim3(KR_THREADS), sm, s, in, out, k3, beta, g, zlen);
     return 0;
 }
 
@@ -1502,6 +1541,8 @@ __global__ void __launch_bounds__(128) axis_apply_kernel(const double *__restric
 }
 
 __global__ void axpby_kernel(long N, double alpha, const double *__restrict__ x, double beta, double *__restrict__ y) {
+    pdl_launch_dependents();
+    pdl_wait();
     for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < N; q += (long)gridDim.x * blockDim.x)
         y[q] = alpha * x[q] + beta * y[q];
 }
@@ -1659,7 +1700,7 @@ static int kop_launch(const KopArgs &a, cudaStream_t s) {
         encode_field_map(&tmp, pb, gm, G::HXE, G::HY, 1))
         return -2;
     dim3 grd(gx, gy, (a.geo.n2 + b.zlen - 1) / b.zlen);
-    kop4_kernel<P><<<grd, K4_THREADS, sm, s>>>(b, tmu, tmv, tmp);
+    launch_pdl(a.pdl, kop4_kernel<P>, grd, dim3(K4_THREADS), sm, s, b, tmu, tmv, tmp);
     return 0;
 }
 
@@ -1755,7 +1796,7 @@ static int sweep_launch(const SweepArgs &a, cudaStream_t s) {
             (!a.mode && encode_field_map(&b.tm_out, a.out, g, LW, y ? rb : 1, y ? 1 : rb)))
             return -2;  // TMA descriptor could not be encoded
     }
-    sweep_kernel<P, L, X, LW, C><<<grd, NT, sm, s>>>(b);
+    launch_pdl(a.pdl, sweep_kernel<P, L, X, LW, C>, grd, dim3(NT), sm, s, b);
     return 0;
 }
 
@@ -1884,8 +1925,8 @@ int launch_axis_apply(int p, int d, const double *band, const double *in, double
     return 0;
 }
 
-int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s) {
-    axpby_kernel<<<grid_for(N), 256, 0, s>>>(N, alpha, x, beta, y);
+int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s, bool pdl) {
+    launch_pdl(pdl, axpby_kernel, dim3(grid_for(N)), dim3(256), 0, s, N, alpha, x, beta, y);
     return 0;
 }
 

@@ -66,6 +66,7 @@ struct KopArgs {
     // (R = Ricker if wav, else 1) replaces the host value g
     const long *dstep = nullptr;
     int wav = 0;
+    bool pdl = false;  // programmatic dependent launch (the elastic step)
     double f0 = 0.0, t0 = 0.0, amp = 0.0, tau_g = 0.0;
 };
 
@@ -113,6 +114,7 @@ struct SweepArgs {
     int rb = 0, nbox = 0;
     // y/z sweeps: number of output (or V) tile buffers, 1 or 2 (set by the launcher when the
     // shared memory holds a second one: a TMA store is then waited for two tiles later)
+    bool pdl = false;  // programmatic dependent launch (the elastic step)
     int vbufs = 1;
     long *dstep_inc = nullptr;  // y/z: block 0 increments the device step counter (graph steps)
 };
@@ -191,7 +193,7 @@ struct KronTerms {
 int launch_kron3(int p, const double *in, double *out, const KronTerms &k3, double beta, const Geom &g,
                  cudaStream_t s);
 // y = alpha x + beta y over N elements
-int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s);
+int launch_axpby(long N, double alpha, const double *x, double beta, double *y, cudaStream_t s, bool pdl = false);
 // u_c = sum_{t: comp_t = c} amp_t sx_t (x) sy_t (x) sz_t for every component c < ncomp (component stride
 // cstride), zero on the Dirichlet faces (mx, my; ngz > 0: global z faces), in one pass.  f holds per
 // term [amp, comp, sx (n0f), sy (n1f), sz (nzf, global z)]; local plane k is global plane k + zoff.
