@@ -881,13 +881,10 @@ int el_energy(ads_ctx *h, double res[3]) {
     const long N3 = 3 * h->Nalloc;
     const long fb = sizeof(double) * h->Nalloc;
     int rc;
-    double acc[3] = {0, 0, 0};
-    auto dot = [&](long n, const double *x, const double *y, double &dst) -> int {
-        double v = 0.0;
-        launch_dot(n, x, y, h->dpartial, h->dres, h->stream);
-        CUDA_TRY(h, cudaMemcpyAsync(&v, h->dres, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-        dst += v;
+    // the 8 dot products land in dres[0..7] on the stream; one copy and one host wait at the end
+    // (summed on the host in the same order as before)
+    auto dot = [&](long n, const double *x, const double *y, int slot) -> int {
+        launch_dot(n, x, y, h->dpartial, h->dres + slot, h->stream);
         return ADS_OK;
     };
     // kinetic
@@ -896,15 +893,14 @@ int el_energy(ads_ctx *h, double res[3]) {
     for (int c = 0; c < 3; ++c) {
         if ((rc = tri(h, h->T3, comp(h->W, h, c), h->dd[0].mband, h->dd[1].mband, h->dd[2].mband, h->rho, 0.0)))
             return rc;
-        if ((rc = dot(h->Nalloc, comp(h->W, h, c), h->T3, acc[0]))) return rc;
+        if ((rc = dot(h->Nalloc, comp(h->W, h, c), h->T3, c))) return rc;
     }
     // potential
     if ((rc = ups_apply(h, h->U, h->U, 0.0, nullptr, h->W, 1.0))) return rc;
-    if ((rc = dot(N3, h->U, h->W, acc[1]))) return rc;
+    if ((rc = dot(N3, h->U, h->W, 3))) return rc;
     // invariant: U' Ups (U + tau V)
     if ((rc = ups_apply(h, h->U, h->V, h->tau, h->U2, h->W, 1.0))) return rc;
-    if ((rc = dot(N3, h->U, h->W, acc[2]))) return rc;
-    double inv = 0.0;
+    if ((rc = dot(N3, h->U, h->W, 4))) return rc;
     for (int i = 0; i < 3; ++i) {
         double *g = comp(h->W, h, i);
         const double *F[3];
@@ -916,8 +912,16 @@ int el_energy(ads_ctx *h, double res[3]) {
         for (int d = 0; d < 3; ++d)
             if ((rc = run_sweep_tab(h, d, h->dd[d].tabM, h->T3, h->T3, nullptr, 0.0))) return rc;
         launch_axpby(h->Nalloc, 1.0 / h->rho, h->T3, 0.0, h->T3, h->stream);
-        if ((rc = dot(h->Nalloc, g, h->T3, inv))) return rc;
+        if ((rc = dot(h->Nalloc, g, h->T3, 5 + i))) return rc;
     }
+    double d[8];
+    CUDA_TRY(h, cudaMemcpyAsync(d, h->dres, sizeof d, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    double acc[3] = {0, 0, 0}, inv = 0.0;
+    for (int c = 0; c < 3; ++c) acc[0] += d[c];
+    acc[1] += d[3];
+    acc[2] += d[4];
+    for (int i = 0; i < 3; ++i) inv += d[5 + i];
     res[0] = 0.5 * acc[0];
     res[1] = 0.5 * acc[1];
     res[2] = 0.5 * inv + 0.5 * acc[2];
