@@ -1182,7 +1182,10 @@ int launch_zfix(int p, const ZfixArgs &a, cudaStream_t s) {
 //     on the plane index mod 2p + 1, so no ring shifts); output plane kk - 2p ... gathered with the
 //     piece's alpha_t Fz_t rows, staged once in shared memory.
 // HBM traffic: in read once (halos from L2), out written once (read once when beta != 0).
-constexpr int KR_X = 32, KR_Y = 16, KR_THREADS = 256, KR_NPF = 4, KR_RY = 4, KR_ZMAX = 160;
+#ifndef ADS_KR_RY
+#define ADS_KR_RY 4
+#endif
+constexpr int KR_X = 32, KR_Y = 16, KR_THREADS = 256, KR_NPF = 4, KR_RY = ADS_KR_RY, KR_ZMAX = 160;
 template <int P, int T>
 struct KronGeo {
     static constexpr int W = 2 * P + 1;
@@ -1196,7 +1199,7 @@ struct KronGeo {
     static constexpr int RING = KR_NPF * HN, YT = 2 * KR_Y * NC * T, YB = T * KR_Y * W, ZB = KR_ZMAX * W * T;
     static_assert(RING % 2 == 0 && YT % 2 == 0 && (T == 1 || YB % 2 == 0), "16-byte aligned Fy / Fz tables");
     static constexpr int SMEM = RING + YT + YB + ZB;
-    static_assert(NITEM <= KR_THREADS, "one y-pass item per thread");
+    static_assert(NITEM <= 2 * KR_THREADS, "at most two y-pass items per thread");
 };
 
 // T terms sharing the input and the output: out = beta out + sum_t alpha_t (Fx_t (x) Fy_t (x) Fz_t) in
@@ -1265,8 +1268,7 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
         }
         cp_async_commit();
     };
-    const bool yitem = tid < G::NITEM;
-    const int nc = tid % NC, grp = tid / NC, hcol = PA - P + nc;
+    const int hcol0 = PA - P;
     const bool own0 = X < n0 && Yo < n1, own1 = X < n0 && Yo + 1 < n1;
     double r0[TZ][W], r1[TZ][W];  // X_t planes by slot: plane q in slot q mod W
 #pragma unroll
@@ -1295,7 +1297,9 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
         if (ii < npl) cp_async_wait<KR_NPF - 2>();
         __syncthreads();  // plane ii landed; Y tile (ii - 1) & 1 complete; ring slot (ii - 1) free
         issue(ii + KR_NPF - 1);
-        if (yitem && ii < npl) {  // y-pass of input plane kk0 + ii, every term from one window
+        // y-pass of input plane kk0 + ii, every term from one window: item = (column, KR_RY rows)
+        auto ypass = [&](const int item) {
+            const int nc = item % NC, grp = item / NC, hcol = hcol0 + nc;
             const double *b = ring + (ii & (KR_NPF - 1)) * HN + KR_RY * grp * HX + hcol;
             double pr[KR_RY + 2 * P];
 #pragma unroll
@@ -1323,6 +1327,11 @@ __device__ __forceinline__ void kron3_tile(const double *__restrict__ in, double
                 if constexpr (TY == 2) reinterpret_cast<double2 *>(yb)[r * NC] = make_double2(acc[0], acc[1]);
                 else yb[r * NC] = acc[0];
             }
+        };
+        if (ii < npl) {
+            if (tid < G::NITEM) ypass(tid);
+            if constexpr (G::NITEM > KR_THREADS)
+                if (tid + KR_THREADS < G::NITEM) ypass(tid + KR_THREADS);
         }
         if (ii == 0) return;
         // x-pass of input plane kx = kk0 + ii - 1, then the z gather for output kx - p
