@@ -14,6 +14,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges appear in nsys / ncu when a tool is attached
 
 #include "../../include/ads.h"
 #include "host_setup.h"
@@ -488,6 +489,12 @@ int build_direction(ads_ctx *h, int d) {
     note_toeplitz(h, D.mband, mb, n);
     return ADS_OK;
 }
+
+// NVTX range over an ABI call (a no-op without an attached tool)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // every ABI entry works on the handle's device (the one current at ads_create), and restores the
 // caller's current device on return
@@ -1687,6 +1694,7 @@ int ads_modal_basis(int nel, int p, int bc, double *lambda, double *phi) {
 }
 
 int ads_modal_advance(ads_handle h, long nsteps) {
+    NvtxRange nv_("ads_modal_advance");
     DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
@@ -1876,6 +1884,7 @@ int ads_set_source(ads_handle h, const double *bx, const double *by, const doubl
 }
 
 int ads_set_state(ads_handle h, const double *u, const double *udot, int mem) {
+    NvtxRange nv_("ads_set_state");
     DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
@@ -1903,6 +1912,7 @@ int ads_set_state(ads_handle h, const double *u, const double *udot, int mem) {
 
 int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const int *cmp, const double *sx,
                             const double *sy, const double *sz) {
+    NvtxRange nv_("ads_set_state_separable");
     DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
@@ -1945,6 +1955,7 @@ int ads_set_state_separable(ads_handle h, int nterms, const double *amp, const i
 }
 
 int ads_step(ads_handle h, int nsteps) {
+    NvtxRange nv_("ads_step");
     DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
@@ -1989,6 +2000,7 @@ int ads_step(ads_handle h, int nsteps) {
 }
 
 int ads_energy(ads_handle h, double out[3]) {
+    NvtxRange nv_("ads_energy");
     DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
@@ -2008,6 +2020,7 @@ int ads_energy(ads_handle h, double out[3]) {
 }
 
 int ads_get_state(ads_handle h, double *u, double *udot, double *a, int mem) {
+    NvtxRange nv_("ads_get_state");
     DeviceScope ds_(h);
     int rc = guard(h);
     if (rc) return rc;
