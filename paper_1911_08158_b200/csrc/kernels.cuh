@@ -148,6 +148,7 @@ struct ModalGemmArgs {
     long td[3] = {0, 0, 0}, ts1 = 0, ts2 = 0;
     int kdim = 0;  // which tensor dimension is k (0: x lines, k contiguous; 1: y / z)
     int tail_only = 0;  // run only the CUDA-core tail rows (the tensor-core path did the full tiles)
+    int fuse_tail = 0;  // the TMA kernels' last full-tile CTAs also compute the (<= 4) tail rows
 };
 int encode_map_3d(CUtensorMap *m, const double *base, long d0, long d1, long d2, long s1, long s2, unsigned b0,
                   unsigned b1, unsigned b2);

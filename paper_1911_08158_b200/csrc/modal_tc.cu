@@ -359,6 +359,11 @@ __global__ void __launch_bounds__(MT_THREADS) modal_fwd_tma(const ModalGemmArgs 
     const int M = q ? g.no : g.ne, K = q ? g.hh : g.H;
     const int mt = blockIdx.x, m0 = 64 * mt, l0 = blockIdx.y * 64;
     if (mt >= M / 64) return;
+    // the last full tile's CTA also computes the tail rows [64 (M / 64), M) (<= 4: the A box's 4
+    // extra rows hold them) on CUDA cores from the same staged operand tiles
+    const int TR = M - 64 * (M / 64);
+    const bool tail = g.fuse_tail && mt == M / 64 - 1 && TR > 0;
+    double tacc[2] = {0.0, 0.0};  // tail rows tr, tr + 2 of line tn
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int sh = (int)(((128 - (__cvta_generic_to_shared(mt_smem) & 127)) & 127) / sizeof(double));
     double *sm = mt_smem + sh;
@@ -419,6 +424,16 @@ __global__ void __launch_bounds__(MT_THREADS) modal_fwd_tma(const ModalGemmArgs 
 #pragma unroll
                 for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], bb[j]);
         }
+        if (tail) {
+            const int tn = tid & 63, tr = tid >> 6;
+#pragma unroll 4
+            for (int kk = 0; kk < 16; ++kk) {
+                const double t = KX ? fma(sg, Tm[tn * 20 + 15 - kk + mo], Ts[tn * 20 + kk])
+                                    : fma(sg, Tm[(15 - kk) * 68 + tn], Ts[kk * 68 + tn]);
+                if (tr < TR) tacc[0] = fma(As[kk * AP + 64 + tr], t, tacc[0]);
+                if (tr + 2 < TR) tacc[1] = fma(As[kk * AP + 64 + tr + 2], t, tacc[1]);
+            }
+        }
         __syncthreads();  // every warp is done with this slot
         if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -427,6 +442,13 @@ __global__ void __launch_bounds__(MT_THREADS) modal_fwd_tma(const ModalGemmArgs 
     }
     const int slot0 = q ? g.ne : 0;
     const long boff = (long)b * g.bs;
+    if (tail) {
+        const int tn = tid & 63, tr = tid >> 6, l = l0 + tn;
+        if (l < g.nl)
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                if (tr + 2 * u < TR) g.out[(long)(slot0 + 64 * (M / 64) + tr + 2 * u) * g.ks + boff + (long)l * g.ls] = tacc[u];
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int m = m0 + wm + 8 * i + (lane >> 2);
@@ -455,6 +477,11 @@ __global__ void __launch_bounds__(MT_THREADS) modal_inv_tma(const ModalGemmArgs 
     const int b = blockIdx.z, mt = blockIdx.x, i0 = 32 * mt, l0 = blockIdx.y * 64;
     const int H = g.H, hh = g.hh, n = g.n;
     if (mt >= H / 32) return;
+    // the last full tile's CTA also computes the tail rows [32 (H / 32), H) (<= 4: the A box's 4
+    // extra rows hold them; rows >= hh of P_o are zero padding)
+    const int TR = H - 32 * (H / 32);
+    const bool tail = g.fuse_tail && mt == H / 32 - 1 && TR > 0;
+    double tte[2] = {0.0, 0.0}, tto[2] = {0.0, 0.0};  // tail rows tr, tr + 2 of line tn
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int sh = (int)(((128 - (__cvta_generic_to_shared(mt_smem) & 127)) & 127) / sizeof(double));
     double *sm = mt_smem + sh;
@@ -512,6 +539,16 @@ __global__ void __launch_bounds__(MT_THREADS) modal_inv_tma(const ModalGemmArgs 
         const double *As = sm + slot * STAGE, *Ts = As + ASZ;
         if (kt < nke) body(acc[0], As, Ts, 0);
         else body(acc[1], As, Ts, KX ? (g.ne & 1) : 0);
+        if (tail) {
+            const int tn = tid & 63, tr = tid >> 6, ko = kt < nke ? 0 : (KX ? (g.ne & 1) : 0);
+            double(&ta)[2] = kt < nke ? tte : tto;
+#pragma unroll 4
+            for (int kk = 0; kk < 16; ++kk) {
+                const double c = KX ? Ts[tn * 20 + kk + ko] : Ts[kk * 68 + tn];
+                if (tr < TR) ta[0] = fma(As[kk * AP + 32 + tr], c, ta[0]);
+                if (tr + 2 < TR) ta[1] = fma(As[kk * AP + 32 + tr + 2], c, ta[1]);
+            }
+        }
         __syncthreads();
         if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -539,6 +576,23 @@ __global__ void __launch_bounds__(MT_THREADS) modal_inv_tma(const ModalGemmArgs 
                 }
             }
     }
+    if (tail) {
+        const int tn = tid & 63, tr = tid >> 6, l = l0 + tn;
+        if (l < g.nl) {
+            const long lo = (long)l * g.ls + boff;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int r = 32 * (H / 32) + tr + 2 * u;
+                if (tr + 2 * u >= TR) continue;
+                if (r < hh) {
+                    g.out[(long)r * g.ks + lo] = tte[u] + tto[u];
+                    g.out[(long)(n - 1 - r) * g.ks + lo] = tte[u] - tto[u];
+                } else {
+                    g.out[(long)r * g.ks + lo] = tte[u];
+                }
+            }
+        }
+    }
 }
 
 }  // namespace
@@ -551,6 +605,17 @@ int launch_modal_gemm(const ModalGemmArgs &g, cudaStream_t s) {
     // full tiles on the TMA-fed tensor-core kernels (when the maps are available), the rest on
     // the register-staged kernels (tail rows, or everything)
     const bool tma = g.Qe2 && g.td[0] > 0;
+    // the tail rows ride in the TMA kernels' last full-tile CTAs when there are at most 4 of them
+    // (ADS_MODAL_FUSE_TAIL=0: the separate CUDA-core tail kernel, experiment switch)
+    static const bool fuse_ok = [] {
+        const char *e = std::getenv("ADS_MODAL_FUSE_TAIL");
+        return !(e && e[0] == '0');
+    }();
+    auto fits = [](int M, int T) { return M >= T && M % T <= 4; };
+    const bool fuse = tma && fuse_ok &&
+                      (g.inverse ? fits(g.H, 32) : (fits(g.ne, 64) && (g.no == 0 || fits(g.no, 64))));
+    ModalGemmArgs gf = g;
+    gf.fuse_tail = fuse ? 1 : 0;
     if (tma) {
         CUtensorMap tA0, tA1, tT;
         const unsigned tb0 = kx ? 20 : 68, tb1 = kx ? 64 : 16;
@@ -566,7 +631,7 @@ int launch_modal_gemm(const ModalGemmArgs &g, cudaStream_t s) {
                 auto fn = kx ? modal_fwd_tma<true> : modal_fwd_tma<false>;
                 cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
                 dim3 grd(mt, ny, 2 * g.nb);
-                fn<<<grd, MT_THREADS, sm, s>>>(g, tA0, tA1, tT);
+                fn<<<grd, MT_THREADS, sm, s>>>(gf, tA0, tA1, tT);
             }
         } else if (g.H / 32 > 0) {
             if (encode_map_3d(&tA0, g.Pe2, g.lpe, std::max(g.ne, 1), 1, g.lpe, (long)g.lpe * std::max(g.ne, 1), 36, 16,
@@ -578,9 +643,10 @@ int launch_modal_gemm(const ModalGemmArgs &g, cudaStream_t s) {
             auto fn = kx ? modal_inv_tma<true> : modal_inv_tma<false>;
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             dim3 grd(g.H / 32, ny, g.nb);
-            fn<<<grd, MT_THREADS, sm, s>>>(g, tA0, tA1, tT);
+            fn<<<grd, MT_THREADS, sm, s>>>(gf, tA0, tA1, tT);
         }
     }
+    if (fuse) return 0;
     ModalGemmArgs t = g;
     t.tail_only = tma ? 1 : 0;
     if (!g.inverse) {
